@@ -1,0 +1,199 @@
+/*
+ * fluxattn_b200.h -- C-ABI of the B200-native Fluxion sparse-decode hot path.
+ *
+ * Plain pointers and sizes only: no CUDA or torch types cross this boundary.
+ * Device-memory arguments are marked [dev]; host-memory ones [host].  All
+ * kernels run on the context's stream; calls are asynchronous unless stated.
+ * Every function returns FX_OK (0) or a negative status; the thread-local
+ * message from fx_last_error() then starts with the reference's stable error
+ * code ("empty-context: ...", "invalid-granularity: ...", ...).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   fx_build_metadata(_levels)  <- build_metadata      src/block_index.cpp:10-39
+ *   fx_block_scores             <- block_score          src/block_index.cpp:41-53
+ *   fx_select_blocks/fx_topk    <- topk_blocks          src/block_index.cpp:55-83
+ *   fx_blocks_for_budget        <- blocks_for_budget    src/block_index.cpp:96-103
+ *   fx_plan_groups              <- plan_group/volume/budget_at src/selector.cpp:9-46
+ *   fx_predict                  <- predict/forward      src/predictor.cpp:161-185
+ *   fx_sparse_decode            <- execute_task         src/scheduler.cpp:78-96
+ *        (default_kv_attention attention.cpp:143-151, sparse_attention
+ *         block_index.cpp:85-94, merge_into attention.cpp:89-104, fused)
+ *   fx_gathered_attention       <- gathered_attention_unchecked attention.cpp:57-87
+ *   fx_merge_partials           <- combine_partials/merge_into attention.cpp:89-129
+ *   fx_decode_step              <- run(queue, profile, RunMode::Executed)
+ *                                  src/scheduler.cpp:283-287 over one decode step
+ *                                  of run_decode (src/pipeline.cpp:292-363)
+ */
+#ifndef FLUXATTN_B200_H
+#define FLUXATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FX_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FX_API __attribute__((visibility("default")))
+#else
+#define FX_API
+#endif
+
+/* status codes */
+#define FX_OK 0
+#define FX_ERR_INVALID (-1)  /* bad argument / shape ("bad-shape", "invalid-granularity", ...) */
+#define FX_ERR_CUDA (-2)     /* CUDA runtime failure */
+#define FX_ERR_NOMEM (-3)    /* device allocation failed */
+#define FX_ERR_STATE (-4)    /* "no-context", "stale-selection", ... */
+
+/* storage types of K/V/metadata */
+#define FX_F32 0
+#define FX_BF16 1
+
+/* plan modes of fx_decode_step */
+#define FX_PLAN_PROPS 0 /* head properties -> on-device plan_group (pipeline.cpp:329) */
+#define FX_PLAN_FIXED 1 /* one (blk, bgt) for every head (pipeline.cpp:304-311)      */
+#define FX_PLAN_FULL 2  /* blk 128, bgt 1 (pipeline.cpp:298-303)                     */
+#define FX_PLAN_GIVEN 3 /* caller-provided [dev] blk per group + budget per head     */
+
+typedef struct fx_ctx fx_ctx;
+
+/* Batched, device-resident KV: K and V are [batch][kv_heads][l_cap][head_dim]
+ * in `dtype`, each (b, g) row range in position order
+ * sink | cpu | local | new  (kv_cache.hpp:13-18), i.e. rows
+ * [0, l_sink) sink, [l_sink, l_sink+l_cpu) cpu, then l_local local rows,
+ * then decode-time rows appended at l_sink+l_cpu+l_local+step.
+ * Query head h of sequence b belongs to group h / group_size. */
+typedef struct fx_layout {
+    int32_t batch;
+    int32_t kv_heads;
+    int32_t group_size;
+    int32_t head_dim;
+    int32_t dtype;
+    int32_t reserved;
+    int64_t l_sink;
+    int64_t l_cpu;
+    int64_t l_local;
+    int64_t l_cap;
+} fx_layout;
+
+/* Per-step arguments of fx_decode_step.  [dev] unless noted. */
+typedef struct fx_step_args {
+    const void* k;               /* [B][Hkv][l_cap][D] */
+    const void* v;
+    const void* meta[4];         /* levels blk 16/32/64/128: [B][Hkv][nblk][2][D] (min row, max row) */
+    const float* absmax;         /* [B][Hkv][D] max_row |k_cpu[row][d]| (from fx_build_metadata_levels) */
+    int64_t l_new;               /* decode rows already appended */
+    const float* q;              /* [B][H][D] f32 */
+    int32_t plan_mode;           /* FX_PLAN_* */
+    int32_t fixed_block_size;    /* FX_PLAN_FIXED */
+    double fixed_budget;         /* FX_PLAN_FIXED */
+    const double* bgt0;          /* FX_PLAN_PROPS: [B][H] head properties (budget_oracle.hpp:17-21) */
+    const double* kslope;
+    const int32_t* streaming;
+    int32_t* plan_blk;           /* in (GIVEN) / out: [B][Hkv] chosen granularity, 0 = streaming group */
+    double* plan_budgets;        /* in (GIVEN) / out: [B][H] per-head budget */
+    double* plan_volume;         /* out, optional: [B][Hkv] V(blk*) (selector.cpp:12) */
+    double* plan_cand_volumes;   /* out, optional: [B][Hkv][4] */
+    int32_t* plan_kblocks;       /* out, optional: [B][H] blocks_for_budget */
+    uint32_t* sel_bits;          /* out, optional: [B][H][sel_words] bit i = block i selected */
+    int32_t sel_words;           /* words per head in sel_bits (>= ceil(nblk16/32)) */
+    float* o;                    /* out: [B][H][D] f32 attention output (defaults (+) sparse) */
+    float* lse;                  /* out, optional: [B][H] natural-log LSE of the merged output */
+} fx_step_args;
+
+/* ---- context, errors, memory ------------------------------------------ */
+FX_API const char* fx_last_error(void);
+FX_API int fx_abi_version(void);
+FX_API int fx_ctx_create(int device, fx_ctx** out);
+FX_API int fx_ctx_destroy(fx_ctx* ctx);
+/* Use an external cudaStream_t (passed as void*); NULL = the ctx's own stream. */
+FX_API int fx_ctx_set_stream(fx_ctx* ctx, void* stream);
+FX_API void* fx_ctx_stream(fx_ctx* ctx);
+FX_API int fx_ctx_synchronize(fx_ctx* ctx);
+/* Kernels launched through this context so far. */
+FX_API uint64_t fx_ctx_launches(fx_ctx* ctx);
+FX_API int fx_malloc(fx_ctx* ctx, size_t bytes, void** dptr);
+FX_API int fx_free(fx_ctx* ctx, void* dptr);
+FX_API int fx_memcpy_h2d(fx_ctx* ctx, void* dst, const void* src, size_t bytes);
+FX_API int fx_memcpy_d2h(fx_ctx* ctx, void* dst, const void* src, size_t bytes);
+FX_API int fx_memset(fx_ctx* ctx, void* dptr, int value, size_t bytes);
+
+/* ---- sizes -------------------------------------------------------------- */
+FX_API int64_t fx_block_count(int64_t rows, int32_t block_size);
+/* bytes of one metadata level for the whole batch */
+FX_API size_t fx_meta_level_bytes(const fx_layout* lay, int32_t block_size);
+/* device scratch fx_decode_step needs (allocated lazily inside the ctx) */
+FX_API size_t fx_step_scratch_bytes(const fx_layout* lay);
+
+/* ---- K1: metadata -------------------------------------------------------- */
+/* All four candidate levels of every (b, g) in one streaming pass over the cpu
+ * segment, plus absmax[b][g][d] = max_row |k[row][d]| used by the selection
+ * error bound.  meta*: [B][Hkv][nblk(blk)][2][D] in lay->dtype. */
+FX_API int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, void* meta16,
+                             void* meta32, void* meta64, void* meta128, float* absmax);
+/* One matrix at any granularity >= 1 (the per-head reference API). k: [dev]
+ * [rows][dim] in dtype; meta: [dev] [nblk][2][dim] in dtype. */
+FX_API int fx_build_metadata(fx_ctx* ctx, const void* k, int32_t dtype, int64_t rows, int32_t dim,
+                      int32_t block_size, void* meta);
+
+/* ---- K2: scoring and selection ------------------------------------------- */
+/* Exact f64 Quest scores of every block (block_score for b = 0..nblk-1). */
+FX_API int fx_block_scores(fx_ctx* ctx, const float* q, const void* meta, int32_t dtype, int64_t nblk,
+                    int32_t dim, double* scores);
+/* topk_blocks for one query: blocks_out [dev] [min(k,nblk)] in selection order
+ * (score desc, id asc); *k_eff [host] = min(k, nblk); *clamped [host] = k > nblk. */
+FX_API int fx_topk_blocks(fx_ctx* ctx, const float* q, const void* meta, int32_t dtype, int64_t nblk,
+                   int32_t dim, int64_t k, uint32_t* blocks_out, int64_t* k_eff, int32_t* clamped);
+
+/* ---- K5: selector and predictor ------------------------------------------ */
+/* plan_group for n groups of G heads (props [dev] [n][G]) plus blocks_for_budget
+ * of each head at the chosen granularity. Outputs [dev]. */
+FX_API int fx_plan_groups(fx_ctx* ctx, int32_t n_groups, int32_t group_size, int64_t l_cpu,
+                   const double* bgt0, const double* kslope, const int32_t* streaming,
+                   int32_t* blk, double* budgets, double* volume, double* cand_volumes,
+                   int32_t* kblocks);
+/* blocks_for_budget on device for n (budget, blk) pairs. */
+FX_API int fx_blocks_for_budget(fx_ctx* ctx, int32_t n, const double* budgets, const int32_t* blk,
+                         int64_t l_cpu, int32_t* kblocks);
+
+typedef struct fx_model fx_model;
+/* Upload a 41->256->384->3 predictor: weights row-major [out][in] f64 and the
+ * 41 (mu, sigma) normalization pairs, all [host]. */
+FX_API int fx_model_create(fx_ctx* ctx, const double* w1, const double* b1, const double* w2,
+                    const double* b2, const double* w3, const double* b3, const double* mu,
+                    const double* sigma, fx_model** out);
+FX_API int fx_model_destroy(fx_model* m);
+/* predict() for n raw feature vectors [dev] [n][41] f64 -> head properties
+ * bgt0 = clamp(z0,0,1), k = z1, streaming = sigmoid(z2) >= 0.5 (pipeline.cpp:287-288).
+ * z [dev, optional] [n][3] raw logits. */
+FX_API int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features, double* bgt0,
+               double* kslope, int32_t* streaming, double* z);
+
+/* ---- K3/K4: attention ----------------------------------------------------- */
+/* One whole decode step of the batch: plan -> score/select -> sparse GQA
+ * attention over defaults + selected blocks with the fused LSE merge. */
+FX_API int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* args);
+/* gathered_attention_unchecked for one query over rows idx[0..n) (ascending)
+ * of k/v [dev] [rows][dim]; o [dev] [dim] f32, lse [dev] f32 (-inf if n == 0). */
+FX_API int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void* v,
+                          int32_t dtype, int64_t rows, int32_t dim, const uint32_t* idx,
+                          int64_t n, float* o, float* lse);
+/* merge of n partials ([dev] o [n][dim], lse [n]; lse = -inf marks an empty
+ * partial) -> o [dev] [dim], lse [dev]. */
+FX_API int fx_merge_partials(fx_ctx* ctx, int32_t n, int32_t dim, const float* o_parts,
+                      const float* lse_parts, float* o, float* lse);
+/* Write decode row `row` (= l_sink+l_cpu+l_local+step) of every (b, g) from
+ * k_new/v_new [dev] [B][Hkv][D] f32 (append_new, kv_cache.hpp:68-73). */
+FX_API int fx_append_kv(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_t row,
+                 const float* k_new, const float* v_new);
+/* Convert f32 -> dtype on device (n elements). */
+FX_API int fx_convert(fx_ctx* ctx, const float* src, void* dst, int32_t dtype, size_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLUXATTN_B200_H */

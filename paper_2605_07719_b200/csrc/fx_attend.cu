@@ -1,0 +1,737 @@
+// fx_attend.cu -- K3 + K4: block-sparse GQA split-K decode attention with the
+// fused log-sum-exp merge.
+//
+// Reference semantics (per head h of a group, scheduler.cpp:78-96):
+//   acc = default_kv_attention(q, cache)          attention.cpp:143-151
+//   acc = merge_into(acc, sparse_attention(q, cache, topk(...)))
+// i.e. exact softmax attention of q over  sink + local + new  and the
+// selected cpu-segment blocks, merged by LSE (attention.cpp:89-104).
+//
+// Work decomposition.  k_worklist (fx_select.cu) lays every (b, g) out as a
+// list of 16-row "boxes" (defaults first, then the union of the group's
+// selected blocks) with a G-bit head mask per box; all lists concatenate
+// into one global box sequence.  A persistent grid splits that sequence into
+// equal contiguous ranges (split-K over the whole batch): a CTA walks its
+// range, keeps running (m, l, O) per head, and at the end of each (b, g) run
+// writes one partial (o, lse).  The last CTA to finish a (b, g) merges its
+// partials (at most a handful) into the final output -- the fused epilogue.
+//
+// k_attend_tma (bf16, D in {64, 128}, G <= 8):
+//   warp 4        producer: TMA 2-D tiled loads (SWIZZLE_128B) of K and V
+//                 boxes into a kStages-deep smem ring, mbarrier completion;
+//   warps 0..3    consumers: one box each per 4-box tile;
+//                 S^T[16 tok x 8 heads] = K . Q^T  (mma.sync m16n8k16 bf16,
+//                 q split hi+lo so q keeps ~16 mantissa bits),
+//                 online softmax in f32 (exp2 domain),
+//                 O^T[D x 8] += V^T . P^T (P^T transposed in-register with
+//                 movmatrix, V^T via ldmatrix.trans).
+//   G <= 8 heads fill the n8 side of the MMA, so one MMA serves all heads of
+//   the group and K/V are read from HBM exactly once per (b, g, token).
+//   tcgen05 needs M >= 64 rows of one operand; with one query token per head
+//   the widest dense side is G <= 8, so the legacy m16n8k16 shape is the
+//   right tool here (the kernel is HBM-bound: ~4 flop/byte).
+// k_attend_generic: any dtype (f32 path of config 1), any G <= 16, D <= 256,
+//   and index lists (the per-query reference API); CUDA-core f32 math.
+#include <cuda.h>
+
+#include "fx_common.cuh"
+
+namespace fx {
+namespace {
+
+constexpr int kCWarps = 4;      // consumer warps
+constexpr int kTileBoxes = 4;   // boxes per pipeline tile (one per consumer warp)
+constexpr int kStages = 5;
+constexpr int kGen = 128;       // threads of the generic kernel
+constexpr int kGenMaxG = 16;
+constexpr int kGenMaxD = 256;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
+
+struct TileHdr {
+    int32_t bg, flags, nb, pad;
+    Box box[kTileBoxes];
+};
+
+struct View {
+    int n_bg, Hkv, G, D;
+    int64_t l_cap;
+    const void* k;
+    const void* v;
+    const float* q;
+    const uint32_t* idx;
+    const Box* boxes;
+    int64_t box_stride;
+    const int32_t* bg_start;
+    float* part_o;
+    float* part_lse;
+    int32_t* bg_done;
+    float* o;
+    float* lse;
+};
+
+__device__ __forceinline__ int cta_of(int64_t x, int64_t NB, int grid) {
+    return (int)(((x + 1) * grid - 1) / NB);
+}
+__device__ __forceinline__ int find_bg(const int32_t* start, int n_bg, int64_t x) {
+    int lo = 0, hi = n_bg - 1;  // largest bg with start[bg] <= x
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(start + mid) <= x) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Final LSE merge of the partials of one (b, g) (attention.cpp:89-104 applied
+// across the CTAs that covered it).  Natural-log LSEs; -inf = empty partial.
+__device__ void merge_bg(const View& p, int bg, int slot0, int nparts, int t, int nt) {
+    const int b = bg / p.Hkv, g = bg % p.Hkv;
+    const int64_t H = (int64_t)p.Hkv * p.G;
+    for (int e = t; e < p.G * p.D; e += nt) {
+        const int h = e / p.D, d = e % p.D;
+        float M = -INFINITY;
+        for (int i = 0; i < nparts; ++i) M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(slot0 + i) * p.G + h));
+        const int64_t oh = (int64_t)b * H + (int64_t)g * p.G + h;
+        if (M == -INFINITY) {
+            p.o[oh * p.D + d] = 0.0f;
+            if (d == 0 && p.lse) p.lse[oh] = -INFINITY;
+            continue;
+        }
+        float num = 0.0f, den = 0.0f;
+        for (int i = 0; i < nparts; ++i) {
+            const float li = __ldcg(p.part_lse + (int64_t)(slot0 + i) * p.G + h);
+            if (li == -INFINITY) continue;
+            const float w = __expf(li - M);
+            num += w * __ldcg(p.part_o + ((int64_t)(slot0 + i) * p.G + h) * p.D + d);
+            den += w;
+        }
+        p.o[oh * p.D + d] = num / den;
+        if (d == 0 && p.lse) p.lse[oh] = M + __logf(den);
+    }
+}
+
+// After a CTA wrote its partial for `bg`: count it; the last contributor
+// merges.  Called by `nt` threads that share named barrier `bar`.
+__device__ void finish_bg(const View& p, int bg, int64_t NB, int grid, int t, int nt, int bar,
+                          int* s_flag) {
+    __threadfence();
+    named_bar_sync(bar, nt);
+    if (t == 0) {
+        const int64_t s = __ldg(p.bg_start + bg), e = __ldg(p.bg_start + bg + 1);
+        const int cf = cta_of(s, NB, grid), cl = cta_of(e - 1, NB, grid);
+        const int prev = atomicAdd(p.bg_done + bg, 1);
+        s_flag[0] = (prev == cl - cf) ? 1 : 0;
+        s_flag[1] = cf;
+        s_flag[2] = cl - cf + 1;
+    }
+    named_bar_sync(bar, nt);
+    if (s_flag[0]) {
+        __threadfence();
+        merge_bg(p, bg, s_flag[1] + bg, s_flag[2], t, nt);
+    }
+    named_bar_sync(bar, nt);
+}
+
+// ---------------------------------------------------------------------------
+// TMA + mma.sync kernel
+// ---------------------------------------------------------------------------
+template <int D>
+struct TmaCfg {
+    static constexpr int NCH = D * 2 / 128;            // 128-byte column chunks per row
+    static constexpr int BOX_BYTES = kBoxRows * 128;   // one TMA box = 2 KB
+    static constexpr int KV_BYTES = kTileBoxes * NCH * BOX_BYTES;
+    static constexpr int STAGE_BYTES = 2 * KV_BYTES;
+    static constexpr int NT = D / 16;                  // k-steps (QK) and m-tiles (PV)
+    static constexpr int WO_LD = D + 4;
+    static constexpr size_t TILES = (size_t)kStages * STAGE_BYTES;
+    static constexpr size_t HDR = TILES;
+    static constexpr size_t BAR = HDR + kStages * sizeof(TileHdr);
+    static constexpr size_t WO = BAR + 2 * kStages * sizeof(uint64_t);
+    static constexpr size_t WM = WO + (size_t)kCWarps * 8 * WO_LD * sizeof(float);
+    static constexpr size_t WL = WM + kCWarps * 8 * sizeof(float);
+    static constexpr size_t FLAG = WL + kCWarps * 8 * sizeof(float);
+    static constexpr size_t TOTAL = FLAG + 16 + 1024;  // + alignment slack
+};
+
+template <int D>
+__global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ CUtensorMap tmK,
+                                                       const __grid_constant__ CUtensorMap tmV,
+                                                       const View p) {
+    using C = TmaCfg<D>;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    TileHdr* hdr = reinterpret_cast<TileHdr*>(smem + C::HDR);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR);
+    uint64_t* empty = full + kStages;
+    float* wO = reinterpret_cast<float*>(smem + C::WO);
+    float* wm = reinterpret_cast<float*>(smem + C::WM);
+    float* wl = reinterpret_cast<float*>(smem + C::WL);
+    int* s_flag = reinterpret_cast<int*>(smem + C::FLAG);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, kCWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int grid = gridDim.x, cta = blockIdx.x;
+    const int64_t NB = __ldg(p.bg_start + p.n_bg);
+    const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
+
+    if (warp == kCWarps) {
+        // ------------------------------ producer ------------------------------
+        if (lane == 0) {
+            tma_prefetch_desc(&tmK);
+            tma_prefetch_desc(&tmV);
+        }
+        int st = 0;
+        uint32_t ph = 0;
+        int64_t x = r0;
+        int bg = r0 < r1 ? find_bg(p.bg_start, p.n_bg, r0) : 0;
+        while (x < r1) {
+            const int64_t s_bg = __ldg(p.bg_start + bg);
+            const int64_t bg_end = min(r1, (int64_t)__ldg(p.bg_start + bg + 1));
+            const Box* bl = p.boxes + (int64_t)bg * p.box_stride - s_bg;
+            bool first = true;
+            int64_t win = -1;  // 32-box prefetch window [win, win + 32)
+            Box wbox{0, 0, 0};
+            while (x < bg_end) {
+                if (win < 0 || x + kTileBoxes > win + 32) {
+                    win = x;
+                    const int64_t gx = x + lane;
+                    if (gx < bg_end) wbox = bl[gx];
+                }
+                const int nb = (int)min((int64_t)kTileBoxes, bg_end - x);
+                Box bx[kTileBoxes];
+#pragma unroll
+                for (int i = 0; i < kTileBoxes; ++i) {
+                    const int src = (int)(x - win) + i;
+                    bx[i].row = __shfl_sync(0xffffffffu, wbox.row, src & 31);
+                    const uint32_t nm = __shfl_sync(0xffffffffu, (uint32_t)wbox.n | ((uint32_t)wbox.mask << 16), src & 31);
+                    bx[i].n = (uint16_t)(nm & 0xffffu);
+                    bx[i].mask = (uint16_t)(nm >> 16);
+                }
+                if (lane == 0) {
+                    mbar_wait(empty + st, ph ^ 1u);
+                    TileHdr& H = hdr[st];
+                    H.bg = bg;
+                    H.nb = nb;
+                    H.flags = (first ? F_FIRST : 0) | (x + nb == bg_end ? F_LAST : 0);
+#pragma unroll
+                    for (int i = 0; i < kTileBoxes; ++i) H.box[i] = bx[i];
+                    mbar_arrive_expect_tx(full + st, (uint32_t)(nb * 2 * C::NCH * C::BOX_BYTES));
+                    unsigned char* kt = smem + (size_t)st * C::STAGE_BYTES;
+                    unsigned char* vt = kt + C::KV_BYTES;
+                    for (int i = 0; i < nb; ++i) {
+                        const int row = (int)((int64_t)bg * p.l_cap + bx[i].row);
+#pragma unroll
+                        for (int ch = 0; ch < C::NCH; ++ch) {
+                            const size_t off = (size_t)(i * C::NCH + ch) * C::BOX_BYTES;
+                            tma_load_2d(kt + off, &tmK, full + st, ch * 64, row);
+                            tma_load_2d(vt + off, &tmV, full + st, ch * 64, row);
+                        }
+                    }
+                }
+                __syncwarp();
+                first = false;
+                x += nb;
+                if (++st == kStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+            ++bg;
+        }
+        if (lane == 0) {
+            mbar_wait(empty + st, ph ^ 1u);
+            hdr[st].flags = F_END;
+            mbar_arrive(full + st);
+        }
+        return;
+    }
+
+    // ------------------------------- consumers -------------------------------
+    const float sl2 = rsqrtf((float)D) * kLog2e;
+    const int tok0 = lane >> 2, h0 = 2 * (lane & 3);
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float O[C::NT][4];
+    uint32_t qh[C::NT][2], ql[C::NT][2];
+#pragma unroll
+    for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
+    int st = 0;
+    uint32_t ph = 0;
+    while (true) {
+        mbar_wait(full + st, ph);
+        const int flags = hdr[st].flags;
+        if (flags & F_END) break;
+        const int bg = hdr[st].bg, nb = hdr[st].nb;
+        const Box bx = hdr[st].box[warp];
+        if (flags & F_FIRST) {
+            const int b = bg / p.Hkv, g = bg % p.Hkv, hq = lane >> 2;
+            const float* qp = p.q + ((int64_t)b * p.Hkv * p.G + (int64_t)g * p.G + hq) * D;
+#pragma unroll
+            for (int j = 0; j < C::NT; ++j) {
+                const int d0 = 16 * j + 2 * (lane & 3);
+                float2 x0 = make_float2(0.f, 0.f), x1 = make_float2(0.f, 0.f);
+                if (hq < p.G) {
+                    x0 = *reinterpret_cast<const float2*>(qp + d0);
+                    x1 = *reinterpret_cast<const float2*>(qp + d0 + 8);
+                }
+                const float a0 = __bfloat162float(__float2bfloat16_rn(x0.x));
+                const float a1 = __bfloat162float(__float2bfloat16_rn(x0.y));
+                const float a2 = __bfloat162float(__float2bfloat16_rn(x1.x));
+                const float a3 = __bfloat162float(__float2bfloat16_rn(x1.y));
+                qh[j][0] = pack_bf16(a0, a1);
+                qh[j][1] = pack_bf16(a2, a3);
+                ql[j][0] = pack_bf16(x0.x - a0, x0.y - a1);
+                ql[j][1] = pack_bf16(x1.x - a2, x1.y - a3);
+            }
+            m0 = m1 = -INFINITY;
+            l0 = l1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
+        }
+        if (warp < nb) {
+            const uint32_t kb = smem_u32(smem + (size_t)st * C::STAGE_BYTES) + warp * C::NCH * C::BOX_BYTES;
+            const uint32_t vb = kb + C::KV_BYTES;
+            float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+            float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};
+            {
+                const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+                for (int j = 0; j < C::NT; ++j) {
+                    const int u = ((j & 3) << 1) + (lane >> 4);
+                    const uint32_t addr = kb + (j >> 2) * C::BOX_BYTES + r * 128 + ((u ^ (r & 7)) << 4);
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4(addr, a0, a1, a2, a3);
+                    mma_bf16_16816((j & 1) ? sb : sa, a0, a1, a2, a3, qh[j][0], qh[j][1]);
+                    mma_bf16_16816((j & 1) ? sd : sc, a0, a1, a2, a3, ql[j][0], ql[j][1]);
+                }
+            }
+            const bool v0 = tok0 < bx.n, v1 = tok0 + 8 < bx.n;
+            const bool e0 = (bx.mask >> h0) & 1, e1 = (bx.mask >> (h0 + 1)) & 1;
+            const float s00 = (v0 && e0) ? ((sa[0] + sb[0]) + (sc[0] + sd[0])) * sl2 : -INFINITY;
+            const float s01 = (v0 && e1) ? ((sa[1] + sb[1]) + (sc[1] + sd[1])) * sl2 : -INFINITY;
+            const float s10 = (v1 && e0) ? ((sa[2] + sb[2]) + (sc[2] + sd[2])) * sl2 : -INFINITY;
+            const float s11 = (v1 && e1) ? ((sa[3] + sb[3]) + (sc[3] + sd[3])) * sl2 : -INFINITY;
+            float c0 = fmaxf(s00, s10), c1 = fmaxf(s01, s11);
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, o));
+                c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+            }
+            const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+            const float b0 = n0 == -INFINITY ? 0.f : n0, b1 = n1 == -INFINITY ? 0.f : n1;
+            const float al0 = n0 == -INFINITY ? 1.f : exp2f(m0 - n0);
+            const float al1 = n1 == -INFINITY ? 1.f : exp2f(m1 - n1);
+            const uint32_t x0 = pack_bf16(exp2f(s00 - b0), exp2f(s01 - b1));
+            const uint32_t x1 = pack_bf16(exp2f(s10 - b0), exp2f(s11 - b1));
+            l0 = l0 * al0 + (bf16lo_to_f(x0) + bf16lo_to_f(x1));
+            l1 = l1 * al1 + (bf16hi_to_f(x0) + bf16hi_to_f(x1));
+            m0 = n0;
+            m1 = n1;
+            const uint32_t pb0 = movmatrix_t(x0), pb1 = movmatrix_t(x1);
+            const int mi = lane >> 3;
+            const int r = (lane & 7) + (mi >> 1) * 8;
+#pragma unroll
+            for (int i = 0; i < C::NT; ++i) {
+                O[i][0] *= al0;
+                O[i][1] *= al1;
+                O[i][2] *= al0;
+                O[i][3] *= al1;
+                const int u = ((i & 3) << 1) + (mi & 1);
+                const uint32_t addr = vb + (i >> 2) * C::BOX_BYTES + r * 128 + ((u ^ (r & 7)) << 4);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(addr, a0, a1, a2, a3);
+                mma_bf16_16816(O[i], a0, a1, a2, a3, pb0, pb1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        if (flags & F_LAST) {
+            // ---- flush: combine the 4 warps' states into this CTA's partial ----
+            float t0 = l0, t1 = l1;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+                t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+            }
+            if (lane < 4) {
+                wm[warp * 8 + h0] = m0;
+                wm[warp * 8 + h0 + 1] = m1;
+                wl[warp * 8 + h0] = t0;
+                wl[warp * 8 + h0 + 1] = t1;
+            }
+            float* wo = wO + (size_t)warp * 8 * C::WO_LD;
+#pragma unroll
+            for (int i = 0; i < C::NT; ++i) {
+                const int d0 = 16 * i + tok0;
+                wo[h0 * C::WO_LD + d0] = O[i][0];
+                wo[(h0 + 1) * C::WO_LD + d0] = O[i][1];
+                wo[h0 * C::WO_LD + d0 + 8] = O[i][2];
+                wo[(h0 + 1) * C::WO_LD + d0 + 8] = O[i][3];
+            }
+            named_bar_sync(1, kCWarps * 32);
+            const int slot = blockIdx.x + bg;
+            for (int e = tid; e < p.G * D; e += kCWarps * 32) {
+                const int h = e / D, d = e % D;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) M = fmaxf(M, wm[w * 8 + h]);
+                float num = 0.f, den = 0.f;
+                if (M != -INFINITY) {
+#pragma unroll
+                    for (int w = 0; w < kCWarps; ++w) {
+                        const float mw = wm[w * 8 + h];
+                        const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
+                        num += f * wO[((size_t)w * 8 + h) * C::WO_LD + d];
+                        den += f * wl[w * 8 + h];
+                    }
+                }
+                p.part_o[((int64_t)slot * p.G + h) * D + d] = den > 0.f ? num / den : 0.f;
+                if (d == 0)
+                    p.part_lse[(int64_t)slot * p.G + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
+            }
+            finish_bg(p, bg, NB, grid, tid, kCWarps * 32, 1, s_flag);
+        }
+        if (++st == kStages) {
+            st = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// generic kernel (any dtype, CUDA cores)
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
+    using T = typename Elem<DT>::T;
+    extern __shared__ float gsm[];
+    const int t = threadIdx.x, G = p.G, D = p.D;
+    // dynamic smem: Ks[16][D+1] | Vs[16][D] | qs[G][D] | sc[16][G] | mst,lst,alp[G]
+    float* Ksm = gsm;
+    float* Vsm = Ksm + kBoxRows * (D + 1);
+    float* qsm = Vsm + kBoxRows * D;
+    float* scm = qsm + G * D;
+    float* mst = scm + kBoxRows * G;
+    float* lst = mst + G;
+    float* alp = lst + G;
+    __shared__ int s_flag[4];
+#define Ks(r, d) Ksm[(r) * (D + 1) + (d)]
+#define Vs(r, d) Vsm[(r) * D + (d)]
+#define qs(h, d) qsm[(h) * D + (d)]
+#define sc(r, h) scm[(r) * G + (h)]
+    const int grid = gridDim.x, cta = blockIdx.x;
+    const int64_t NB = __ldg(p.bg_start + p.n_bg);
+    const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
+    if (r0 >= r1) return;
+    const float scale = rsqrtf((float)D);
+    float acc[kGenMaxG][2];
+    int bg = find_bg(p.bg_start, p.n_bg, r0);
+    int64_t s_bg = __ldg(p.bg_start + bg), e_bg = __ldg(p.bg_start + bg + 1);
+    bool fresh = true;
+    for (int64_t x = r0; x < r1; ++x) {
+        if (fresh) {
+            const int b = bg / p.Hkv, g = bg % p.Hkv;
+            const float* qp = p.q + ((int64_t)b * p.Hkv * G + (int64_t)g * G) * D;
+            for (int e = t; e < G * D; e += kGen) qs(e / D, e % D) = qp[e];
+            if (t < G) {
+                mst[t] = -INFINITY;
+                lst[t] = 0.f;
+            }
+#pragma unroll
+            for (int h = 0; h < kGenMaxG; ++h) acc[h][0] = acc[h][1] = 0.f;
+            fresh = false;
+        }
+        const Box bx = p.boxes[(int64_t)bg * p.box_stride + (x - s_bg)];
+        const T* kb = static_cast<const T*>(p.k) + (int64_t)bg * p.l_cap * D;
+        const T* vb = static_cast<const T*>(p.v) + (int64_t)bg * p.l_cap * D;
+        for (int e = t; e < kBoxRows * D; e += kGen) {
+            const int r = e / D, d = e % D;
+            float kv = 0.f, vv = 0.f;
+            if (r < bx.n) {
+                const int64_t row = p.idx ? (int64_t)p.idx[bx.row + r] : (int64_t)bx.row + r;
+                kv = tofl(kb[row * D + d]);
+                vv = tofl(vb[row * D + d]);
+            }
+            Ks(r, d) = kv;
+            Vs(r, d) = vv;
+        }
+        __syncthreads();
+        for (int pr = t; pr < kBoxRows * G; pr += kGen) {
+            const int tok = pr / G, h = pr % G;
+            float s = -INFINITY;
+            if (tok < bx.n && ((bx.mask >> h) & 1)) {
+                float a = 0.f;
+                for (int d = 0; d < D; ++d) a = fmaf(qs(h, d), Ks(tok, d), a);
+                s = a * scale;
+            }
+            sc(tok, h) = s;
+        }
+        __syncthreads();
+        if (t < G) {
+            float mx = mst[t];
+            for (int tok = 0; tok < kBoxRows; ++tok) mx = fmaxf(mx, sc(tok, t));
+            const float a = mx == -INFINITY ? 1.f : expf(mst[t] - mx);
+            const float base = mx == -INFINITY ? 0.f : mx;
+            float sum = 0.f;
+            for (int tok = 0; tok < kBoxRows; ++tok) {
+                const float pv = expf(sc(tok, t) - base);
+                sc(tok, t) = pv;
+                sum += pv;
+            }
+            lst[t] = lst[t] * a + sum;
+            mst[t] = mx;
+            alp[t] = a;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int dd = 0; dd < 2; ++dd) {
+            const int d = t + dd * kGen;
+            if (d < D) {
+#pragma unroll
+                for (int h = 0; h < kGenMaxG; ++h) {
+                    if (h < G) {
+                        float a = acc[h][dd] * alp[h];
+                        for (int tok = 0; tok < kBoxRows; ++tok) a = fmaf(sc(tok, h), Vs(tok, d), a);
+                        acc[h][dd] = a;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (x + 1 == r1 || x + 1 == e_bg) {
+            const int slot = cta + bg;
+#pragma unroll
+            for (int dd = 0; dd < 2; ++dd) {
+                const int d = t + dd * kGen;
+                if (d < D) {
+#pragma unroll
+                    for (int h = 0; h < kGenMaxG; ++h)
+                        if (h < G)
+                            p.part_o[((int64_t)slot * G + h) * D + d] = lst[h] > 0.f ? acc[h][dd] / lst[h] : 0.f;
+                }
+            }
+            if (t < G)
+                p.part_lse[(int64_t)slot * G + t] = lst[t] > 0.f ? mst[t] + logf(lst[t]) : -INFINITY;
+            finish_bg(p, bg, NB, grid, t, kGen, 1, s_flag);
+            if (x + 1 < r1) {
+                ++bg;
+                s_bg = __ldg(p.bg_start + bg);
+                e_bg = __ldg(p.bg_start + bg + 1);
+                fresh = true;
+            }
+        }
+    }
+}
+
+#undef Ks
+#undef Vs
+#undef qs
+#undef sc
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+__global__ void k_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done) {
+    const int64_t nb = (n + kBoxRows - 1) / kBoxRows;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nb) {
+        Box b;
+        b.row = (int32_t)(j * kBoxRows);
+        b.n = (uint16_t)min((int64_t)kBoxRows, n - j * kBoxRows);
+        b.mask = 1;
+        boxes[j] = b;
+    }
+    if (j == 0) {
+        bg_start[0] = 0;
+        bg_start[1] = (int32_t)nb;
+        bg_done[0] = 0;
+    }
+}
+
+__global__ void k_merge_partials(int n, int dim, const float* __restrict__ op,
+                                 const float* __restrict__ lp, float* __restrict__ o,
+                                 float* __restrict__ lse) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    float M = -INFINITY;
+    for (int i = 0; i < n; ++i) M = fmaxf(M, lp[i]);
+    if (d < dim) {
+        if (M == -INFINITY) {
+            o[d] = 0.f;
+        } else {
+            float num = 0.f, den = 0.f;
+            for (int i = 0; i < n; ++i) {
+                if (lp[i] == -INFINITY) continue;
+                const float w = expf(lp[i] - M);
+                num += w * op[(int64_t)i * dim + d];
+                den += w;
+            }
+            o[d] = num / den;
+            if (d == 0 && lse) lse[0] = M + logf(den);
+        }
+    }
+    if (d == 0 && lse && M == -INFINITY) lse[0] = -INFINITY;
+}
+
+template <typename T>
+__global__ void k_append(int64_t n_bg, int D, int64_t l_cap, int64_t row, T* k, T* v,
+                         const float* kn, const float* vn) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_bg * D) return;
+    const int64_t bg = e / D, d = e % D;
+    k[(bg * l_cap + row) * D + d] = (T)kn[e];
+    v[(bg * l_cap + row) * D + d] = (T)vn[e];
+}
+
+template <typename T>
+__global__ void k_convert(const float* src, T* dst, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (T)src[i];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        FX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+        FX_REQUIRE(ptr != nullptr && q == cudaDriverEntryPointSuccess, FX_ERR_CUDA,
+                   "cuda-error: cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// [rows][D] bf16, box = 16 rows x 64 columns (128 B), 128-byte swizzle.
+CUtensorMap make_kv_map(const void* base, int D, int64_t rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kBoxRows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    FX_REQUIRE(r == CUDA_SUCCESS, FX_ERR_CUDA, "cuda-error: cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+View make_view(const AttendArgs& a) {
+    View v;
+    v.n_bg = a.L.batch * a.L.kv_heads;
+    v.Hkv = a.L.kv_heads;
+    v.G = a.L.group_size;
+    v.D = a.L.head_dim;
+    v.l_cap = a.L.l_cap;
+    v.k = a.k;
+    v.v = a.v;
+    v.q = a.q;
+    v.idx = a.idx;
+    v.boxes = a.boxes;
+    v.box_stride = a.box_stride;
+    v.bg_start = a.bg_start;
+    v.part_o = a.part_o;
+    v.part_lse = a.part_lse;
+    v.bg_done = a.bg_done;
+    v.o = a.o;
+    v.lse = a.lse;
+    return v;
+}
+
+template <int D>
+void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
+    const View v = make_view(a);
+    const int64_t rows = (int64_t)v.n_bg * a.L.l_cap;
+    const CUtensorMap mk = make_kv_map(a.k, D, rows), mv = make_kv_map(a.v, D, rows);
+    const size_t smem = TmaCfg<D>::TOTAL;
+    FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_attend_tma<D><<<grid, 160, smem, s>>>(mk, mv, v);
+}
+
+}  // namespace
+
+bool attend_uses_tma(const fx_layout& L, bool has_idx) {
+    return !has_idx && L.dtype == FX_BF16 && (L.head_dim == 64 || L.head_dim == 128) &&
+           L.group_size <= 8;
+}
+
+int attend_grid(const fx_layout& L, bool has_idx, int num_sms) {
+    return attend_uses_tma(L, has_idx) ? num_sms : num_sms * 4;
+}
+
+void launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
+    FX_REQUIRE(a.L.group_size >= 1 && a.L.group_size <= kGenMaxG, FX_ERR_INVALID,
+               "bad-shape: group_size must be in [1, 16]");
+    FX_REQUIRE(a.L.head_dim >= 1 && a.L.head_dim <= kGenMaxD, FX_ERR_INVALID,
+               "bad-shape: head_dim must be in [1, 256]");
+    if (allow_tma && attend_uses_tma(a.L, a.idx != nullptr)) {
+        if (a.L.head_dim == 128) launch_tma<128>(a, grid, s);
+        else launch_tma<64>(a, grid, s);
+    } else {
+        const View v = make_view(a);
+        const int D = a.L.head_dim, G = a.L.group_size;
+        const size_t smem = sizeof(float) * ((size_t)kBoxRows * (D + 1) + (size_t)kBoxRows * D +
+                                             (size_t)G * D + (size_t)kBoxRows * G + 3 * G);
+        if (a.L.dtype == FX_BF16) {
+            FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_attend_generic<FX_BF16><<<grid, kGen, smem, s>>>(v);
+        } else {
+            FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_attend_generic<FX_F32><<<grid, kGen, smem, s>>>(v);
+        }
+    }
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done,
+                        cudaStream_t s) {
+    const int64_t nb = std::max<int64_t>(1, cdiv(n, kBoxRows));
+    k_index_boxes<<<(unsigned)cdiv(nb, 256), 256, 0, s>>>(n, boxes, bg_start, bg_done);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_merge_partials(int n, int dim, const float* o_parts, const float* lse_parts, float* o,
+                           float* lse, cudaStream_t s) {
+    k_merge_partials<<<(unsigned)cdiv(dim, 128), 128, 0, s>>>(n, dim, o_parts, lse_parts, o, lse);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_append(const fx_layout& L, void* k, void* v, int64_t row, const float* kn,
+                   const float* vn, cudaStream_t s) {
+    const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
+    const unsigned grid = (unsigned)cdiv(n_bg * L.head_dim, 256);
+    if (L.dtype == FX_BF16)
+        k_append<__nv_bfloat16><<<grid, 256, 0, s>>>(n_bg, L.head_dim, L.l_cap, row,
+                                                     static_cast<__nv_bfloat16*>(k),
+                                                     static_cast<__nv_bfloat16*>(v), kn, vn);
+    else
+        k_append<float><<<grid, 256, 0, s>>>(n_bg, L.head_dim, L.l_cap, row, static_cast<float*>(k),
+                                             static_cast<float*>(v), kn, vn);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    if (dtype == FX_BF16) k_convert<__nv_bfloat16><<<grid, 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+    else k_convert<float><<<grid, 256, 0, s>>>(src, static_cast<float*>(dst), n);
+    FX_CUDA(cudaGetLastError());
+}
+
+}  // namespace fx

@@ -1,0 +1,597 @@
+// fx_capi.cu -- the C-ABI (include/fluxattn_b200.h): context, device scratch,
+// and the entry points that sequence the K1..K5 kernels.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "fx_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FX_OK;
+    } catch (const fx::Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("internal: ") + e.what();
+        return FX_ERR_STATE;
+    }
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        if (p) FX_CUDA(cudaFree(p));
+        p = nullptr;
+        bytes = 0;
+        n = (n + 255) & ~size_t(255);
+        if (cudaMalloc(&p, n) != cudaSuccess) {
+            cudaGetLastError();
+            fx::fail(FX_ERR_NOMEM, "out-of-memory: device scratch of " + std::to_string(n) + " bytes");
+        }
+        bytes = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// Bump allocator over one DevBuf (all regions 256-byte aligned).
+struct Carve {
+    size_t off = 0;
+    template <class T>
+    size_t take(size_t n) {
+        const size_t o = off;
+        off += (n * sizeof(T) + 255) & ~size_t(255);
+        return o;
+    }
+};
+
+void check_layout(const fx_layout* L) {
+    FX_REQUIRE(L != nullptr, FX_ERR_INVALID, "bad-shape: null layout");
+    FX_REQUIRE(L->batch > 0 && L->kv_heads > 0 && L->group_size > 0 && L->head_dim > 0,
+               FX_ERR_INVALID, "bad-shape: non-positive layout dimension");
+    FX_REQUIRE(L->dtype == FX_F32 || L->dtype == FX_BF16, FX_ERR_INVALID, "bad-shape: unknown dtype");
+    FX_REQUIRE(L->l_sink >= 0 && L->l_cpu >= 0 && L->l_local >= 0, FX_ERR_INVALID,
+               "bad-shape: negative segment length");
+    FX_REQUIRE(L->l_cap >= L->l_sink + L->l_cpu + L->l_local, FX_ERR_INVALID,
+               "bad-shape: l_cap smaller than sink + cpu + local");
+    FX_REQUIRE(L->l_cap * L->batch * L->kv_heads < (int64_t)INT32_MAX, FX_ERR_INVALID,
+               "bad-shape: more than 2^31 cache rows");
+}
+
+int elem_bytes(int dtype) { return dtype == FX_BF16 ? 2 : 4; }
+}  // namespace
+
+struct fx_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    DevBuf step;  // fx_decode_step scratch
+    DevBuf api;   // per-query API scratch
+};
+
+struct fx_model {
+    fx_ctx* ctx = nullptr;
+    DevBuf buf;
+    const double *w1t, *b1, *w2t, *b2, *w3t, *b3, *mu, *sigma;
+};
+
+namespace {
+struct DeviceGuard {
+    explicit DeviceGuard(fx_ctx* c) {
+        FX_REQUIRE(c != nullptr, FX_ERR_STATE, "no-context: null fx_ctx");
+        FX_CUDA(cudaSetDevice(c->device));
+    }
+};
+
+struct StepScratch {
+    int32_t* blk;
+    double* budgets;
+    int32_t* kblocks;
+    float* approx;
+    int64_t approx_stride;
+    uint32_t* sel_bits;
+    int sel_words;
+    uint64_t* cand_keys;
+    uint32_t* cand_ids;
+    fx::Box* boxes;
+    int64_t box_stride;
+    int32_t* bg_count;
+    int32_t* bg_start;
+    int32_t* bg_done;
+    float* part_o;
+    float* part_lse;
+};
+
+StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
+    const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
+    const int64_t heads = n_bg * L.group_size;
+    const int64_t nblk16 = std::max<int64_t>(1, fx::level_blocks(L.l_cpu, 16));
+    const int words = (int)fx::cdiv(nblk16, 32);
+    const int64_t tail_max = L.l_cap - L.l_sink - L.l_cpu;
+    const int64_t box_stride =
+        fx::cdiv(L.l_sink, fx::kBoxRows) + fx::cdiv(tail_max, fx::kBoxRows) + nblk16 + 2;
+    Carve c;
+    const size_t o_blk = c.take<int32_t>(n_bg);
+    const size_t o_bud = c.take<double>(heads);
+    const size_t o_kb = c.take<int32_t>(heads);
+    const size_t o_apx = c.take<float>(heads * nblk16);
+    const size_t o_bits = c.take<uint32_t>(heads * words);
+    const size_t o_ck = c.take<uint64_t>(heads * nblk16);
+    const size_t o_ci = c.take<uint32_t>(heads * nblk16);
+    const size_t o_box = c.take<fx::Box>(n_bg * box_stride);
+    const size_t o_cnt = c.take<int32_t>(n_bg);
+    const size_t o_st = c.take<int32_t>(n_bg + 1);
+    const size_t o_dn = c.take<int32_t>(n_bg + 1);
+    const size_t o_po = c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
+    const size_t o_pl = c.take<float>((grid + n_bg) * L.group_size);
+    if (alloc) ctx->step.ensure(c.off);
+    char* b = static_cast<char*>(ctx->step.p);
+    StepScratch s;
+    s.blk = reinterpret_cast<int32_t*>(b + o_blk);
+    s.budgets = reinterpret_cast<double*>(b + o_bud);
+    s.kblocks = reinterpret_cast<int32_t*>(b + o_kb);
+    s.approx = reinterpret_cast<float*>(b + o_apx);
+    s.approx_stride = nblk16;
+    s.sel_bits = reinterpret_cast<uint32_t*>(b + o_bits);
+    s.sel_words = words;
+    s.cand_keys = reinterpret_cast<uint64_t*>(b + o_ck);
+    s.cand_ids = reinterpret_cast<uint32_t*>(b + o_ci);
+    s.boxes = reinterpret_cast<fx::Box*>(b + o_box);
+    s.box_stride = box_stride;
+    s.bg_count = reinterpret_cast<int32_t*>(b + o_cnt);
+    s.bg_start = reinterpret_cast<int32_t*>(b + o_st);
+    s.bg_done = reinterpret_cast<int32_t*>(b + o_dn);
+    s.part_o = reinterpret_cast<float*>(b + o_po);
+    s.part_lse = reinterpret_cast<float*>(b + o_pl);
+    return s;
+}
+
+size_t step_bytes(const fx_layout& L, int grid) {
+    const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
+    const int64_t heads = n_bg * L.group_size;
+    const int64_t nblk16 = std::max<int64_t>(1, fx::level_blocks(L.l_cpu, 16));
+    const int words = (int)fx::cdiv(nblk16, 32);
+    const int64_t tail_max = L.l_cap - L.l_sink - L.l_cpu;
+    const int64_t box_stride =
+        fx::cdiv(L.l_sink, fx::kBoxRows) + fx::cdiv(tail_max, fx::kBoxRows) + nblk16 + 2;
+    Carve c;
+    c.take<int32_t>(n_bg);
+    c.take<double>(heads);
+    c.take<int32_t>(heads);
+    c.take<float>(heads * nblk16);
+    c.take<uint32_t>(heads * words);
+    c.take<uint64_t>(heads * nblk16);
+    c.take<uint32_t>(heads * nblk16);
+    c.take<fx::Box>(n_bg * box_stride);
+    c.take<int32_t>(n_bg);
+    c.take<int32_t>(n_bg + 1);
+    c.take<int32_t>(n_bg + 1);
+    c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
+    c.take<float>((grid + n_bg) * L.group_size);
+    return c.off;
+}
+
+int64_t next_pow2(int64_t x) {
+    int64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+}  // namespace
+
+extern "C" {
+
+const char* fx_last_error(void) { return g_last_error.c_str(); }
+int fx_abi_version(void) { return FX_ABI_VERSION; }
+
+int fx_ctx_create(int device, fx_ctx** out) {
+    return guarded([&] {
+        FX_REQUIRE(out != nullptr, FX_ERR_INVALID, "bad-shape: null out pointer");
+        int n = 0;
+        FX_CUDA(cudaGetDeviceCount(&n));
+        FX_REQUIRE(device >= 0 && device < n, FX_ERR_INVALID, "bad-shape: no such CUDA device");
+        FX_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        FX_CUDA(cudaGetDeviceProperties(&prop, device));
+        FX_REQUIRE(prop.major == 10, FX_ERR_CUDA,
+                   "cuda-error: this library is built for sm_100a (B200) only");
+        auto* c = new fx_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        FX_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        c->stream = c->own;
+        *out = c;
+    });
+}
+
+int fx_ctx_destroy(fx_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        ctx->step.release();
+        ctx->api.release();
+        if (ctx->own) cudaStreamDestroy(ctx->own);
+        delete ctx;
+    });
+}
+
+int fx_ctx_set_stream(fx_ctx* ctx, void* stream) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    });
+}
+
+void* fx_ctx_stream(fx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int fx_ctx_synchronize(fx_ctx* ctx) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uint64_t fx_ctx_launches(fx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fx_malloc(fx_ctx* ctx, size_t bytes, void** dptr) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        if (cudaMalloc(dptr, std::max<size_t>(bytes, 1)) != cudaSuccess) {
+            cudaGetLastError();
+            fx::fail(FX_ERR_NOMEM, "out-of-memory: fx_malloc");
+        }
+    });
+}
+
+int fx_free(fx_ctx* ctx, void* dptr) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        if (dptr) FX_CUDA(cudaFree(dptr));
+    });
+}
+
+int fx_memcpy_h2d(fx_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    });
+}
+
+int fx_memcpy_d2h(fx_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        FX_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int fx_memset(fx_ctx* ctx, void* dptr, int value, size_t bytes) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_CUDA(cudaMemsetAsync(dptr, value, bytes, ctx->stream));
+    });
+}
+
+int64_t fx_block_count(int64_t rows, int32_t block_size) {
+    return block_size > 0 ? fx::cdiv(rows, block_size) : 0;
+}
+
+size_t fx_meta_level_bytes(const fx_layout* lay, int32_t block_size) {
+    if (!lay || block_size <= 0) return 0;
+    return (size_t)lay->batch * lay->kv_heads * fx::cdiv(lay->l_cpu, block_size) * 2 *
+           lay->head_dim * elem_bytes(lay->dtype);
+}
+
+size_t fx_step_scratch_bytes(const fx_layout* lay) {
+    if (!lay) return 0;
+    return step_bytes(*lay, 148 * 4);
+}
+
+int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, void* m16,
+                             void* m32, void* m64, void* m128, float* absmax) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        fx::launch_meta_levels(*lay, k, m16, m32, m64, m128, absmax, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_build_metadata(fx_ctx* ctx, const void* k, int32_t dtype, int64_t rows, int32_t dim,
+                      int32_t block_size, void* meta) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(block_size > 0, FX_ERR_INVALID, "invalid-granularity: block size must be >= 1");
+        FX_REQUIRE(dim > 0 && rows >= 0, FX_ERR_INVALID, "bad-shape: metadata input");
+        fx::launch_meta_generic(k, dtype, rows, dim, block_size, meta, ctx->stream);
+        ctx->launches += rows > 0 ? 1 : 0;
+    });
+}
+
+int fx_block_scores(fx_ctx* ctx, const float* q, const void* meta, int32_t dtype, int64_t nblk,
+                    int32_t dim, double* scores) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        fx::launch_exact_scores(q, meta, dtype, nblk, dim, scores, ctx->stream);
+        ctx->launches += nblk > 0 ? 1 : 0;
+    });
+}
+
+int fx_topk_blocks(fx_ctx* ctx, const float* q, const void* meta, int32_t dtype, int64_t nblk,
+                   int32_t dim, int64_t k, uint32_t* blocks_out, int64_t* k_eff,
+                   int32_t* clamped) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(k >= 0 && nblk >= 0, FX_ERR_INVALID, "bad-shape: negative k or block count");
+        const int64_t ke = std::min(k, nblk);
+        if (k_eff) *k_eff = ke;
+        if (clamped) *clamped = k > nblk ? 1 : 0;
+        if (ke == 0) return;
+        const int64_t cap = next_pow2(nblk);
+        Carve c;
+        const size_t ok = c.take<uint64_t>(cap), oi = c.take<uint32_t>(cap);
+        ctx->api.ensure(c.off);
+        char* b = static_cast<char*>(ctx->api.p);
+        fx::launch_topk_exact(q, meta, dtype, nblk, dim, ke, blocks_out,
+                              reinterpret_cast<uint64_t*>(b + ok), reinterpret_cast<uint32_t*>(b + oi),
+                              cap, ctx->stream);
+        int lg = 0;
+        for (int64_t x = cap; x > 1; x >>= 1) ++lg;
+        ctx->launches += 1 + (uint64_t)lg * (lg + 1) / 2;
+    });
+}
+
+int fx_plan_groups(fx_ctx* ctx, int32_t n_groups, int32_t group_size, int64_t l_cpu,
+                   const double* bgt0, const double* kslope, const int32_t* streaming,
+                   int32_t* blk, double* budgets, double* volume, double* cand_volumes,
+                   int32_t* kblocks) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(n_groups >= 0, FX_ERR_INVALID, "bad-shape: negative group count");
+        FX_REQUIRE(group_size >= 1, FX_ERR_INVALID, "empty-group: plan_group needs at least one head");
+        if (n_groups == 0) return;
+        fx_layout L{};
+        L.batch = n_groups;
+        L.kv_heads = 1;
+        L.group_size = group_size;
+        L.head_dim = 1;
+        L.l_cpu = l_cpu;
+        fx::launch_prepare(L, FX_PLAN_PROPS, 0, 0.0, bgt0, kslope, streaming, blk, budgets, volume,
+                           cand_volumes, kblocks, nullptr, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_blocks_for_budget(fx_ctx* ctx, int32_t n, const double* budgets, const int32_t* blk,
+                         int64_t l_cpu, int32_t* kblocks) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        fx::launch_blocks_for_budget(n, budgets, blk, l_cpu, kblocks, ctx->stream);
+        ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+int fx_model_create(fx_ctx* ctx, const double* w1, const double* b1, const double* w2,
+                    const double* b2, const double* w3, const double* b3, const double* mu,
+                    const double* sigma, fx_model** out) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        constexpr int F = 41, H1 = 256, H2 = 384, O = 3;
+        // marshal to the device layout: transposed weights [in][out]
+        std::vector<double> h;
+        auto put_t = [&](const double* w, int outs, int ins) {
+            for (int i = 0; i < ins; ++i)
+                for (int o = 0; o < outs; ++o) h.push_back(w[(size_t)o * ins + i]);
+        };
+        auto put = [&](const double* x, int n) { h.insert(h.end(), x, x + n); };
+        put_t(w1, H1, F);
+        put(b1, H1);
+        put_t(w2, H2, H1);
+        put(b2, H2);
+        put_t(w3, O, H2);
+        put(b3, O);
+        put(mu, F);
+        put(sigma, F);
+        auto* m = new fx_model();
+        m->ctx = ctx;
+        m->buf.ensure(h.size() * sizeof(double));
+        FX_CUDA(cudaMemcpy(m->buf.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+        const double* d = static_cast<const double*>(m->buf.p);
+        m->w1t = d;
+        d += F * H1;
+        m->b1 = d;
+        d += H1;
+        m->w2t = d;
+        d += H1 * H2;
+        m->b2 = d;
+        d += H2;
+        m->w3t = d;
+        d += H2 * O;
+        m->b3 = d;
+        d += O;
+        m->mu = d;
+        d += F;
+        m->sigma = d;
+        *out = m;
+    });
+}
+
+int fx_model_destroy(fx_model* m) {
+    return guarded([&] {
+        if (!m) return;
+        cudaSetDevice(m->ctx->device);
+        m->buf.release();
+        delete m;
+    });
+}
+
+int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features, double* bgt0,
+               double* kslope, int32_t* streaming, double* z) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(m != nullptr, FX_ERR_STATE, "no-model: predictor source requires a model");
+        fx::launch_predict(n, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma,
+                           features, bgt0, kslope, streaming, z, ctx->stream);
+        ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(a != nullptr && a->k && a->v && a->q && a->o, FX_ERR_STATE,
+                   "no-context: decode step has no executable payload");
+        const fx_layout& L = *lay;
+        FX_REQUIRE(a->l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + a->l_new <= L.l_cap,
+                   FX_ERR_INVALID, "bad-shape: decoded rows exceed l_cap");
+        FX_REQUIRE(a->plan_mode >= FX_PLAN_PROPS && a->plan_mode <= FX_PLAN_GIVEN, FX_ERR_INVALID,
+                   "bad-shape: unknown plan mode");
+        const bool sparse = L.l_cpu > 0;
+        if (sparse) {
+            for (int i = 0; i < 4; ++i)
+                FX_REQUIRE(a->meta[i] != nullptr, FX_ERR_STATE, "no-context: missing block metadata");
+            FX_REQUIRE(a->absmax != nullptr, FX_ERR_STATE, "no-context: missing absmax");
+        }
+        if (a->plan_mode == FX_PLAN_PROPS)
+            FX_REQUIRE(a->bgt0 && a->kslope && a->streaming, FX_ERR_STATE,
+                       "no-context: plan mode PROPS needs head properties");
+        if (a->plan_mode == FX_PLAN_GIVEN)
+            FX_REQUIRE(a->plan_blk && a->plan_budgets, FX_ERR_STATE,
+                       "no-context: plan mode GIVEN needs blk and budgets");
+        const int grid = fx::attend_grid(L, false, ctx->num_sms);
+        StepScratch s = carve_step(ctx, L, grid, true);
+        if (a->sel_bits) {
+            FX_REQUIRE(a->sel_words >= s.sel_words, FX_ERR_INVALID, "bad-shape: sel_words too small");
+            s.sel_bits = a->sel_bits;
+            s.sel_words = a->sel_words;
+        }
+        int32_t* blk = a->plan_blk ? a->plan_blk : s.blk;
+        double* budgets = a->plan_budgets ? a->plan_budgets : s.budgets;
+        int32_t* kblocks = a->plan_kblocks ? a->plan_kblocks : s.kblocks;
+        cudaStream_t st = ctx->stream;
+        fx::launch_prepare(L, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
+                           a->kslope, a->streaming, blk, budgets, a->plan_volume,
+                           a->plan_cand_volumes, kblocks, s.bg_done, st);
+        int n = 1;
+        if (sparse) {
+            fx::launch_approx_scores(L, a->meta, a->q, blk, kblocks, s.approx, s.approx_stride, st);
+            fx::launch_select(L, a->meta, a->absmax, a->q, blk, kblocks, s.approx, s.approx_stride,
+                              s.sel_bits, s.sel_words, s.cand_keys, s.cand_ids, st);
+            n += 2;
+        } else {
+            FX_CUDA(cudaMemsetAsync(blk, 0, sizeof(int32_t) * L.batch * L.kv_heads, st));
+        }
+        fx::launch_worklist(L, a->l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
+                            s.bg_count, s.bg_start, s.bg_done, st);
+        fx::AttendArgs aa{};
+        aa.L = L;
+        aa.k = a->k;
+        aa.v = a->v;
+        aa.q = a->q;
+        aa.idx = nullptr;
+        aa.boxes = s.boxes;
+        aa.box_stride = s.box_stride;
+        aa.bg_start = s.bg_start;
+        aa.part_o = s.part_o;
+        aa.part_lse = s.part_lse;
+        aa.bg_done = s.bg_done;
+        aa.o = a->o;
+        aa.lse = a->lse;
+        fx::launch_attend(aa, grid, true, st);
+        n += 2;
+        ctx->launches += n;
+    });
+}
+
+int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void* v,
+                          int32_t dtype, int64_t rows, int32_t dim, const uint32_t* idx,
+                          int64_t n, float* o, float* lse) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(dim > 0 && n >= 0, FX_ERR_INVALID, "bad-shape: gathered attention input");
+        if (n == 0) {  // merge identity: o = 0, lse = -inf
+            fx::launch_merge_partials(0, dim, nullptr, nullptr, o, lse, ctx->stream);
+            ctx->launches += 1;
+            return;
+        }
+        fx_layout L{};
+        L.batch = 1;
+        L.kv_heads = 1;
+        L.group_size = 1;
+        L.head_dim = dim;
+        L.dtype = dtype;
+        L.l_cap = rows;
+        const int64_t nb = fx::cdiv(n, fx::kBoxRows);
+        const int grid = (int)std::min<int64_t>(nb, (int64_t)ctx->num_sms * 4);
+        Carve c;
+        const size_t ob = c.take<fx::Box>(nb), os = c.take<int32_t>(2), od = c.take<int32_t>(2);
+        const size_t oo = c.take<float>((size_t)(grid + 1) * dim), ol = c.take<float>(grid + 1);
+        ctx->api.ensure(c.off);
+        char* b = static_cast<char*>(ctx->api.p);
+        fx::AttendArgs aa{};
+        aa.L = L;
+        aa.k = k;
+        aa.v = v;
+        aa.q = q;
+        aa.idx = idx;
+        aa.boxes = reinterpret_cast<fx::Box*>(b + ob);
+        aa.box_stride = nb;
+        aa.bg_start = reinterpret_cast<int32_t*>(b + os);
+        aa.bg_done = reinterpret_cast<int32_t*>(b + od);
+        aa.part_o = reinterpret_cast<float*>(b + oo);
+        aa.part_lse = reinterpret_cast<float*>(b + ol);
+        aa.o = o;
+        aa.lse = lse;
+        fx::launch_index_boxes(n, const_cast<fx::Box*>(aa.boxes), const_cast<int32_t*>(aa.bg_start),
+                               aa.bg_done, ctx->stream);
+        fx::launch_attend(aa, grid, false, ctx->stream);
+        ctx->launches += 2;
+    });
+}
+
+int fx_merge_partials(fx_ctx* ctx, int32_t n, int32_t dim, const float* o_parts,
+                      const float* lse_parts, float* o, float* lse) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(n >= 0 && dim > 0, FX_ERR_INVALID, "bad-shape: merge input");
+        fx::launch_merge_partials(n, dim, o_parts, lse_parts, o, lse, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_append_kv(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_t row,
+                 const float* k_new, const float* v_new) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(row >= 0 && row < lay->l_cap, FX_ERR_INVALID, "bad-shape: append row out of range");
+        fx::launch_append(*lay, k, v, row, k_new, v_new, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_convert(fx_ctx* ctx, const float* src, void* dst, int32_t dtype, size_t n) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        fx::launch_convert(src, dst, dtype, n, ctx->stream);
+        ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// fx_internal.h -- host-side internals shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "fluxattn_b200.h"
+
+namespace fx {
+
+// Rows per TMA box / per attention "box" (one 16-token slab of one (b, g)).
+constexpr int kBoxRows = 16;
+// Candidate granularities, selector.hpp:12.
+constexpr int kLevels[4] = {16, 32, 64, 128};
+
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+#define FX_CUDA(call)                                                                       \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            ::fx::fail(FX_ERR_CUDA, std::string("cuda-error: ") + cudaGetErrorString(e_) + \
+                                        " (" #call ")");                                    \
+    } while (0)
+
+#define FX_REQUIRE(cond, status, msg)            \
+    do {                                         \
+        if (!(cond)) ::fx::fail((status), (msg)); \
+    } while (0)
+
+// Box descriptor: rows [row, row + n) of one (b, g) (or, for index boxes,
+// entries [row, row + n) of an index list); `mask` bit h = query head h of
+// the group attends these rows.
+struct Box {
+    int32_t row;
+    uint16_t n;
+    uint16_t mask;
+};
+static_assert(sizeof(Box) == 8, "Box is 8 bytes");
+
+// Device-side bookkeeping of one decode step (lives in ctx scratch).
+struct StepCounters {
+    int32_t total_boxes;  // filled after the worklist kernel (prefix of per-(b,g) counts)
+    int32_t pad[31];
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t level_blocks(int64_t l_cpu, int blk) { return cdiv(l_cpu, blk); }
+
+// ---- kernel launchers (one per .cu) --------------------------------------
+// fx_metadata.cu
+void launch_meta_levels(const fx_layout& L, const void* k, void* m16, void* m32, void* m64,
+                        void* m128, float* absmax, cudaStream_t s);
+void launch_meta_generic(const void* k, int dtype, int64_t rows, int dim, int blk, void* meta,
+                         cudaStream_t s);
+
+// fx_plan.cu
+void launch_prepare(const fx_layout& L, int plan_mode, int fixed_blk, double fixed_budget,
+                    const double* bgt0, const double* kslope, const int32_t* streaming,
+                    int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
+                    int32_t* bg_done, cudaStream_t s);
+void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, int64_t l_cpu,
+                              int32_t* kblocks, cudaStream_t s);
+void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
+                    const double* b2, const double* w3t, const double* b3, const double* mu,
+                    const double* sigma, const double* feats, double* bgt0, double* kslope,
+                    int32_t* streaming, double* z, cudaStream_t s);
+
+// fx_select.cu
+void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
+                          const int32_t* blk, const int32_t* kblocks, float* approx,
+                          int64_t approx_stride, cudaStream_t s);
+void launch_select(const fx_layout& L, const void* const meta[4], const float* absmax,
+                   const float* q, const int32_t* blk, const int32_t* kblocks,
+                   const float* approx, int64_t approx_stride, uint32_t* sel_bits, int sel_words,
+                   uint64_t* cand_keys, uint32_t* cand_ids, cudaStream_t s);
+void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
+                     const uint32_t* sel_bits, int sel_words, Box* boxes, int64_t box_stride,
+                     int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s);
+void launch_exact_scores(const float* q, const void* meta, int dtype, int64_t nblk, int dim,
+                         double* scores, cudaStream_t s);
+// exact scores of all blocks, sorted (score desc, id asc); first k ids out.
+// tmp arrays hold `cap` (power of two >= nblk) entries.
+void launch_topk_exact(const float* q, const void* meta, int dtype, int64_t nblk, int dim,
+                       int64_t k, uint32_t* blocks_out, uint64_t* tmp_keys, uint32_t* tmp_ids,
+                       int64_t cap, cudaStream_t s);
+void launch_meta_absmax(const void* meta, int dtype, int64_t nblk, int dim, float* absmax,
+                        cudaStream_t s);
+
+// fx_attend.cu
+struct AttendArgs {
+    fx_layout L;
+    const void* k;
+    const void* v;
+    const float* q;           // [B][H][D]
+    const uint32_t* idx;      // index boxes (API path) or nullptr
+    const Box* boxes;         // [n_bg][box_stride]
+    int64_t box_stride;
+    const int32_t* bg_start;  // [n_bg + 1] exclusive prefix of box counts
+    float* part_o;            // [(grid + n_bg)][G][D]
+    float* part_lse;          // [(grid + n_bg)][G]
+    int32_t* bg_done;         // [n_bg], zeroed before the launch
+    float* o;                 // [B][H][D]
+    float* lse;               // [B][H] or nullptr
+};
+bool attend_uses_tma(const fx_layout& L, bool has_idx);
+int attend_grid(const fx_layout& L, bool has_idx, int num_sms);
+void launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s);
+void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done,
+                        cudaStream_t s);
+void launch_merge_partials(int n, int dim, const float* o_parts, const float* lse_parts, float* o,
+                           float* lse, cudaStream_t s);
+void launch_append(const fx_layout& L, void* k, void* v, int64_t row, const float* kn,
+                   const float* vn, cudaStream_t s);
+void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream_t s);
+
+}  // namespace fx

@@ -1,0 +1,219 @@
+// fx_plan.cu -- K5: the granularity-budget selector and the head-property
+// predictor, on device.
+//
+//   budget_at / volume / plan_group   selector.cpp:9-46  (Eq. 1, Eq. 3)
+//   blocks_for_budget                  block_index.cpp:96-103
+//   forward / predict                  predictor.cpp:161-185
+//
+// All f64 arithmetic uses explicit round-to-nearest intrinsics (__dmul_rn,
+// __dadd_rn, ...) in the reference's operation order: the reference host
+// build has no FMA (no -march), and contraction would move results by an
+// ulp, which can flip k = ceil(.) at a boundary.
+#include "fx_common.cuh"
+
+namespace fx {
+namespace {
+
+__device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }
+
+// log2 of the candidate granularities is exact.
+__device__ __forceinline__ double log2_blk(int blk) {
+    return blk == 16 ? 4.0 : blk == 32 ? 5.0 : blk == 64 ? 6.0 : blk == 128 ? 7.0 : log2((double)blk);
+}
+
+// selector.cpp:15-19
+__device__ __forceinline__ double budget_at(double bgt0, double k, int streaming, int blk) {
+    if (streaming) return 0.0;
+    const double kk = (k < 0.0) ? 0.0 : k;  // std::max(k, 0.0)
+    return clamp01(__dadd_rn(bgt0, __dmul_rn(kk, log2_blk(blk))));
+}
+
+// selector.cpp:9-13 given the already-clamped sequential budget sum
+__device__ __forceinline__ double volume_of(int blk, int64_t l_cpu, double clamped_sum) {
+    const double L = (double)l_cpu;
+    return __dadd_rn(__ddiv_rn(__dmul_rn(2.0, L), (double)blk), __dmul_rn(__dmul_rn(2.0, L), clamped_sum));
+}
+
+// block_index.cpp:96-103
+__device__ __forceinline__ int32_t blocks_for_budget(double budget, int64_t l_cpu, int blk) {
+    if (!(budget > 0.0) || l_cpu == 0 || blk <= 0) return 0;
+    const int64_t nblk = (l_cpu + blk - 1) / blk;
+    const double raw = __ddiv_rn(__dmul_rn(budget, (double)l_cpu), (double)blk);
+    const double c = ceil(__dsub_rn(raw, 1e-12));
+    int64_t k = c <= 0.0 ? 0 : (int64_t)c;
+    if (k < 1) k = 1;
+    return (int32_t)(k < nblk ? k : nblk);
+}
+
+// Sequential (head-order) sum of clamped budgets across the warp's G lanes.
+__device__ __forceinline__ double seq_sum(double v, int G) {
+    double s = 0.0;
+    for (int h = 0; h < G; ++h) s = __dadd_rn(s, clamp01(__shfl_sync(0xffffffffu, v, h)));
+    return s;
+}
+
+// One warp per (b, g): plan the group, derive per-head k, reset the step's
+// per-group completion counter.
+__global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_blk,
+                          double fixed_budget, const double* __restrict__ bgt0,
+                          const double* __restrict__ kslope, const int32_t* __restrict__ streaming,
+                          int32_t* __restrict__ blk_out, double* __restrict__ budgets,
+                          double* __restrict__ volume, double* __restrict__ cand,
+                          int32_t* __restrict__ kblocks, int32_t* __restrict__ bg_done) {
+    const int bg = blockIdx.x;
+    const int h = threadIdx.x;
+    const bool act = h < G;
+    const int64_t head = (int64_t)bg * G + h;
+    if (h == 0 && bg_done) {
+        bg_done[bg] = 0;
+        if (bg == 0) bg_done[n_bg] = 0;  // worklist completion counter
+    }
+    int blk = 0;
+    double bud = 0.0, vol = 0.0, cv[4] = {0, 0, 0, 0};
+    if (mode == FX_PLAN_PROPS) {
+        const double b0 = act ? bgt0[head] : 0.0;
+        const double ks = act ? kslope[head] : 0.0;
+        const int st = act ? (streaming[head] != 0) : 1;
+        const bool all_streaming = __all_sync(0xffffffffu, st != 0);
+        if (!all_streaming) {  // plan_group, selector.cpp:21-46
+            double best = 0.0;
+            for (int c = 0; c < 4; ++c) {
+                const int cb = 16 << c;
+                const double b = budget_at(b0, ks, st, cb);
+                const double v = volume_of(cb, l_cpu, seq_sum(b, G));
+                cv[c] = v;
+                if (blk == 0 || v <= best) {  // ties go to the larger blk
+                    best = v;
+                    blk = cb;
+                    bud = b;
+                }
+            }
+            vol = best;
+        }
+    } else if (mode == FX_PLAN_FIXED || mode == FX_PLAN_FULL) {
+        const bool full = mode == FX_PLAN_FULL;
+        blk = full ? 128 : fixed_blk;
+        bud = full ? 1.0 : fixed_budget;
+        const double s = seq_sum(bud, G);
+        if (full) {  // pipeline.cpp:298-303
+            vol = __dmul_rn(2.0, (double)l_cpu);
+            for (int c = 0; c < 4; ++c) cv[c] = vol;
+        } else {  // pipeline.cpp:304-311
+            vol = volume_of(blk, l_cpu, s);
+            for (int c = 0; c < 4; ++c) cv[c] = volume_of(16 << c, l_cpu, s);
+        }
+    } else {  // FX_PLAN_GIVEN
+        blk = blk_out[bg];
+        bud = act ? budgets[head] : 0.0;
+        if (blk > 0) vol = volume_of(blk, l_cpu, seq_sum(bud, G));
+    }
+    if (h == 0) {
+        if (mode != FX_PLAN_GIVEN) blk_out[bg] = blk;
+        if (volume) volume[bg] = vol;
+        if (cand)
+            for (int c = 0; c < 4; ++c) cand[bg * 4 + c] = cv[c];
+    }
+    if (act) {
+        if (mode != FX_PLAN_GIVEN) budgets[head] = bud;
+        if (kblocks) kblocks[head] = blk > 0 ? blocks_for_budget(bud, l_cpu, blk) : 0;
+    }
+}
+
+__global__ void k_blocks_for_budget(int n, const double* __restrict__ budgets,
+                                    const int32_t* __restrict__ blk, int64_t l_cpu,
+                                    int32_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = blocks_for_budget(budgets[i], l_cpu, blk[i]);
+}
+
+// predictor.cpp:40-53 linear_forward (bias-first, sequential, unfused) with
+// weights stored transposed [in][out] so that thread o reads coalesced.
+__device__ __forceinline__ double linear_row(const double* __restrict__ wt, double bias,
+                                             const double* a, int in, int out, int o) {
+    double s = bias;
+    for (int i = 0; i < in; ++i) s = __dadd_rn(s, __dmul_rn(a[i], wt[(int64_t)i * out + o]));
+    return s;
+}
+
+constexpr int kF = 41, kH1 = 256, kH2 = 384;
+
+// One CTA (384 threads) per feature row: normalize -> 41->256->384->3.
+__global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
+                                                 const double* __restrict__ b1,
+                                                 const double* __restrict__ w2t,
+                                                 const double* __restrict__ b2,
+                                                 const double* __restrict__ w3t,
+                                                 const double* __restrict__ b3,
+                                                 const double* __restrict__ mu,
+                                                 const double* __restrict__ sigma,
+                                                 const double* __restrict__ feats,
+                                                 double* __restrict__ bgt0, double* __restrict__ kslope,
+                                                 int32_t* __restrict__ streaming,
+                                                 double* __restrict__ zout) {
+    __shared__ double x[kF], a1[kH1], a2[kH2];
+    const int r = blockIdx.x, t = threadIdx.x;
+    if (t < kF) {  // features.cpp:226-233
+        const double sg = sigma[t];
+        x[t] = sg > 0.0 ? __ddiv_rn(__dsub_rn(feats[(int64_t)r * kF + t], mu[t]), sg) : 0.0;
+    }
+    __syncthreads();
+    if (t < kH1) {
+        const double s = linear_row(w1t, b1[t], x, kF, kH1, t);
+        a1[t] = s > 0.0 ? s : 0.0;
+    }
+    __syncthreads();
+    {
+        const double s = linear_row(w2t, b2[t], a1, kH1, kH2, t);
+        a2[t] = s > 0.0 ? s : 0.0;
+    }
+    __syncthreads();
+    if (t < 3) {
+        const double z = linear_row(w3t, b3[t], a2, kH2, 3, t);
+        if (zout) zout[(int64_t)r * 3 + t] = z;
+        if (t == 0) bgt0[r] = clamp01(z);
+        if (t == 1) kslope[r] = z;
+        if (t == 2) {
+            const double sp = 1.0 / (1.0 + exp(-z));  // sigmoid, predictor.cpp:20
+            streaming[r] = sp >= 0.5 ? 1 : 0;          // pipeline.cpp:288
+        }
+    }
+}
+
+}  // namespace
+
+void launch_prepare(const fx_layout& L, int plan_mode, int fixed_blk, double fixed_budget,
+                    const double* bgt0, const double* kslope, const int32_t* streaming,
+                    int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
+                    int32_t* bg_done, cudaStream_t s) {
+    const int n_bg = L.batch * L.kv_heads;
+    FX_REQUIRE(L.group_size >= 1 && L.group_size <= 32, FX_ERR_INVALID,
+               "bad-shape: group_size must be in [1, 32]");
+    if (plan_mode == FX_PLAN_FIXED) {
+        bool ok = false;
+        for (int c = 0; c < 4; ++c) ok |= kLevels[c] == fixed_blk;
+        FX_REQUIRE(ok, FX_ERR_INVALID, "invalid-granularity: blk must be one of 16/32/64/128");
+    }
+    k_prepare<<<n_bg, 32, 0, s>>>(n_bg, L.group_size, L.l_cpu, plan_mode, fixed_blk, fixed_budget,
+                                  bgt0, kslope, streaming, blk, budgets, volume, cand, kblocks,
+                                  bg_done);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, int64_t l_cpu,
+                              int32_t* kblocks, cudaStream_t s) {
+    if (n <= 0) return;
+    k_blocks_for_budget<<<(n + 255) / 256, 256, 0, s>>>(n, budgets, blk, l_cpu, kblocks);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
+                    const double* b2, const double* w3t, const double* b3, const double* mu,
+                    const double* sigma, const double* feats, double* bgt0, double* kslope,
+                    int32_t* streaming, double* z, cudaStream_t s) {
+    if (n <= 0) return;
+    k_predict<<<n, kH2, 0, s>>>(w1t, b1, w2t, b2, w3t, b3, mu, sigma, feats, bgt0, kslope,
+                                streaming, z);
+    FX_CUDA(cudaGetLastError());
+}
+
+}  // namespace fx
