@@ -110,7 +110,8 @@ FX_API const char* fx_last_error(void);
 FX_API int fx_abi_version(void);
 FX_API int fx_ctx_create(int device, fx_ctx** out);
 FX_API int fx_ctx_destroy(fx_ctx* ctx);
-/* Use an external cudaStream_t (passed as void*); NULL = the ctx's own stream. */
+/* Run on an external cudaStream_t (passed as void*); NULL = the legacy default
+ * stream.  Until this is called the ctx uses its own non-blocking stream. */
 FX_API int fx_ctx_set_stream(fx_ctx* ctx, void* stream);
 FX_API void* fx_ctx_stream(fx_ctx* ctx);
 FX_API int fx_ctx_synchronize(fx_ctx* ctx);

@@ -86,13 +86,20 @@ __device__ __forceinline__ int find_bg(const int32_t* start, int n_bg, int64_t x
 
 // Final LSE merge of the partials of one (b, g) (attention.cpp:89-104 applied
 // across the CTAs that covered it).  Natural-log LSEs; -inf = empty partial.
-__device__ void merge_bg(const View& p, int bg, int slot0, int nparts, int t, int nt) {
+__device__ __forceinline__ bool cta_nonempty(int c, int64_t NB, int grid) {
+    return NB * c / grid < NB * (c + 1) / grid;
+}
+
+// Partials of `bg` live in slots c + bg for the non-empty CTAs c in [cf, cl].
+__device__ void merge_bg(const View& p, int bg, int cf, int cl, int64_t NB, int grid, int t,
+                         int nt) {
     const int b = bg / p.Hkv, g = bg % p.Hkv;
     const int64_t H = (int64_t)p.Hkv * p.G;
     for (int e = t; e < p.G * p.D; e += nt) {
         const int h = e / p.D, d = e % p.D;
         float M = -INFINITY;
-        for (int i = 0; i < nparts; ++i) M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(slot0 + i) * p.G + h));
+        for (int c = cf; c <= cl; ++c)
+            if (cta_nonempty(c, NB, grid)) M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(c + bg) * p.G + h));
         const int64_t oh = (int64_t)b * H + (int64_t)g * p.G + h;
         if (M == -INFINITY) {
             p.o[oh * p.D + d] = 0.0f;
@@ -100,11 +107,12 @@ __device__ void merge_bg(const View& p, int bg, int slot0, int nparts, int t, in
             continue;
         }
         float num = 0.0f, den = 0.0f;
-        for (int i = 0; i < nparts; ++i) {
-            const float li = __ldcg(p.part_lse + (int64_t)(slot0 + i) * p.G + h);
+        for (int c = cf; c <= cl; ++c) {
+            if (!cta_nonempty(c, NB, grid)) continue;
+            const float li = __ldcg(p.part_lse + (int64_t)(c + bg) * p.G + h);
             if (li == -INFINITY) continue;
             const float w = __expf(li - M);
-            num += w * __ldcg(p.part_o + ((int64_t)(slot0 + i) * p.G + h) * p.D + d);
+            num += w * __ldcg(p.part_o + ((int64_t)(c + bg) * p.G + h) * p.D + d);
             den += w;
         }
         p.o[oh * p.D + d] = num / den;
@@ -121,15 +129,17 @@ __device__ void finish_bg(const View& p, int bg, int64_t NB, int grid, int t, in
     if (t == 0) {
         const int64_t s = __ldg(p.bg_start + bg), e = __ldg(p.bg_start + bg + 1);
         const int cf = cta_of(s, NB, grid), cl = cta_of(e - 1, NB, grid);
+        int n = 0;  // contributing (non-empty) CTAs
+        for (int c = cf; c <= cl; ++c) n += cta_nonempty(c, NB, grid);
         const int prev = atomicAdd(p.bg_done + bg, 1);
-        s_flag[0] = (prev == cl - cf) ? 1 : 0;
+        s_flag[0] = (prev == n - 1) ? 1 : 0;
         s_flag[1] = cf;
-        s_flag[2] = cl - cf + 1;
+        s_flag[2] = cl;
     }
     named_bar_sync(bar, nt);
     if (s_flag[0]) {
         __threadfence();
-        merge_bg(p, bg, s_flag[1] + bg, s_flag[2], t, nt);
+        merge_bg(p, bg, s_flag[1], s_flag[2], NB, grid, t, nt);
     }
     named_bar_sync(bar, nt);
 }

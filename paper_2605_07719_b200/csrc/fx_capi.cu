@@ -233,7 +233,8 @@ int fx_ctx_destroy(fx_ctx* ctx) {
 int fx_ctx_set_stream(fx_ctx* ctx, void* stream) {
     return guarded([&] {
         DeviceGuard g(ctx);
-        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+        // NULL is the legacy default stream (torch's default stream handle is 0)
+        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     });
 }
 
