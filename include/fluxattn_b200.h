@@ -11,11 +11,12 @@
  * Reference interfaces replaced (paths relative to /root/reference/proj):
  *   fx_build_metadata(_levels)  <- build_metadata      src/block_index.cpp:10-39
  *   fx_block_scores             <- block_score          src/block_index.cpp:41-53
- *   fx_select_blocks/fx_topk    <- topk_blocks          src/block_index.cpp:55-83
+ *   fx_topk_blocks              <- topk_blocks          src/block_index.cpp:55-83
+ *        (batched: fx_decode_step, sel_bits output)
  *   fx_blocks_for_budget        <- blocks_for_budget    src/block_index.cpp:96-103
  *   fx_plan_groups              <- plan_group/volume/budget_at src/selector.cpp:9-46
  *   fx_predict                  <- predict/forward      src/predictor.cpp:161-185
- *   fx_sparse_decode            <- execute_task         src/scheduler.cpp:78-96
+ *   fx_decode_step              <- execute_task         src/scheduler.cpp:78-96
  *        (default_kv_attention attention.cpp:143-151, sparse_attention
  *         block_index.cpp:85-94, merge_into attention.cpp:89-104, fused)
  *   fx_gathered_attention       <- gathered_attention_unchecked attention.cpp:57-87
@@ -117,6 +118,20 @@ FX_API void* fx_ctx_stream(fx_ctx* ctx);
 FX_API int fx_ctx_synchronize(fx_ctx* ctx);
 /* Kernels launched through this context so far. */
 FX_API uint64_t fx_ctx_launches(fx_ctx* ctx);
+
+/* Optional CUDA-event timing of each kernel launch on the ctx stream. */
+#define FX_KERNEL_PLAN 0     /* K5 prepare/plan          */
+#define FX_KERNEL_SCORE 1    /* K2a approximate scores   */
+#define FX_KERNEL_SELECT 2   /* K2b exact top-k select   */
+#define FX_KERNEL_WORKLIST 3 /* union -> boxes           */
+#define FX_KERNEL_ATTEND 4   /* K3+K4 attention + merge  */
+#define FX_KERNEL_METADATA 5 /* K1 metadata levels       */
+#define FX_KERNEL_APPEND 6   /* decode-row append        */
+#define FX_KERNEL_COUNT 7
+FX_API int fx_ctx_set_timing(fx_ctx* ctx, int enable);
+/* Accumulated milliseconds and launch count of one kernel id (synchronizes). */
+FX_API int fx_ctx_kernel_time(fx_ctx* ctx, int32_t kernel, double* total_ms, int64_t* launches);
+FX_API int fx_ctx_reset_timing(fx_ctx* ctx);
 FX_API int fx_malloc(fx_ctx* ctx, size_t bytes, void** dptr);
 FX_API int fx_free(fx_ctx* ctx, void* dptr);
 FX_API int fx_memcpy_h2d(fx_ctx* ctx, void* dst, const void* src, size_t bytes);

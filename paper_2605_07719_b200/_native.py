@@ -19,6 +19,7 @@ FX_PLAN_PROPS = 0
 FX_PLAN_FIXED = 1
 FX_PLAN_FULL = 2
 FX_PLAN_GIVEN = 3
+KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append")
 
 _p = C.c_void_p
 _i32 = C.c_int32
@@ -60,6 +61,9 @@ _SIGS = {
     "fx_ctx_stream": (_p, [_p]),
     "fx_ctx_synchronize": (C.c_int, [_p]),
     "fx_ctx_launches": (C.c_uint64, [_p]),
+    "fx_ctx_set_timing": (C.c_int, [_p, C.c_int]),
+    "fx_ctx_kernel_time": (C.c_int, [_p, _i32, C.POINTER(C.c_double), C.POINTER(_i64)]),
+    "fx_ctx_reset_timing": (C.c_int, [_p]),
     "fx_malloc": (C.c_int, [_p, _sz, C.POINTER(_p)]),
     "fx_free": (C.c_int, [_p, _p]),
     "fx_memcpy_h2d": (C.c_int, [_p, _p, _p, _sz]),

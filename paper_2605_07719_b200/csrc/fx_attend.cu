@@ -151,7 +151,8 @@ template <int D>
 struct TmaCfg {
     static constexpr int NCH = D * 2 / 128;            // 128-byte column chunks per row
     static constexpr int BOX_BYTES = kBoxRows * 128;   // one TMA box = 2 KB
-    static constexpr int KV_BYTES = kTileBoxes * NCH * BOX_BYTES;
+    static constexpr int CHUNK_BYTES = kTileBoxes * BOX_BYTES;  // one column chunk of a tile
+    static constexpr int KV_BYTES = NCH * CHUNK_BYTES;
     static constexpr int STAGE_BYTES = 2 * KV_BYTES;
     static constexpr int NT = D / 16;                  // k-steps (QK) and m-tiles (PV)
     static constexpr int WO_LD = D + 4;
@@ -168,6 +169,8 @@ struct TmaCfg {
 template <int D>
 __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ CUtensorMap tmK,
                                                        const __grid_constant__ CUtensorMap tmV,
+                                                       const __grid_constant__ CUtensorMap tmK64,
+                                                       const __grid_constant__ CUtensorMap tmV64,
                                                        const View p) {
     using C = TmaCfg<D>;
     extern __shared__ unsigned char smem_raw[];
@@ -198,6 +201,8 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
         if (lane == 0) {
             tma_prefetch_desc(&tmK);
             tma_prefetch_desc(&tmV);
+            tma_prefetch_desc(&tmK64);
+            tma_prefetch_desc(&tmV64);
         }
         int st = 0;
         uint32_t ph = 0;
@@ -237,13 +242,25 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                     mbar_arrive_expect_tx(full + st, (uint32_t)(nb * 2 * C::NCH * C::BOX_BYTES));
                     unsigned char* kt = smem + (size_t)st * C::STAGE_BYTES;
                     unsigned char* vt = kt + C::KV_BYTES;
-                    for (int i = 0; i < nb; ++i) {
-                        const int row = (int)((int64_t)bg * p.l_cap + bx[i].row);
+                    // 3-D maps {64 cols, rows, column chunk}: one TMA moves a whole
+                    // box of rows across every 128-byte chunk.  A tile of 4
+                    // contiguous full boxes is ONE 64-row TMA per tensor and lands
+                    // chunk-major [chunk][64 rows][128 B]; otherwise one 16-row TMA
+                    // per box, box-major [box][chunk][16 rows][128 B].
+                    bool contig = nb == kTileBoxes;
 #pragma unroll
-                        for (int ch = 0; ch < C::NCH; ++ch) {
-                            const size_t off = (size_t)(i * C::NCH + ch) * C::BOX_BYTES;
-                            tma_load_2d(kt + off, &tmK, full + st, ch * 64, row);
-                            tma_load_2d(vt + off, &tmV, full + st, ch * 64, row);
+                    for (int i = 0; i < kTileBoxes; ++i)
+                        contig = contig && bx[i].n == kBoxRows && bx[i].row == bx[0].row + i * kBoxRows;
+                    H.pad = contig ? 1 : 0;
+                    if (contig) {
+                        const int row = (int)((int64_t)bg * p.l_cap + bx[0].row);
+                        tma_load_3d(kt, &tmK64, full + st, 0, row, 0);
+                        tma_load_3d(vt, &tmV64, full + st, 0, row, 0);
+                    } else {
+                        for (int i = 0; i < nb; ++i) {
+                            const int row = (int)((int64_t)bg * p.l_cap + bx[i].row);
+                            tma_load_3d(kt + i * C::NCH * C::BOX_BYTES, &tmK, full + st, 0, row, 0);
+                            tma_load_3d(vt + i * C::NCH * C::BOX_BYTES, &tmV, full + st, 0, row, 0);
                         }
                     }
                 }
@@ -281,6 +298,7 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
         if (flags & F_END) break;
         const int bg = hdr[st].bg, nb = hdr[st].nb;
         const Box bx = hdr[st].box[warp];
+        const bool cmaj = hdr[st].pad != 0;  // chunk-major (contiguous) tile
         if (flags & F_FIRST) {
             const int b = bg / p.Hkv, g = bg % p.Hkv, hq = lane >> 2;
             const float* qp = p.q + ((int64_t)b * p.Hkv * p.G + (int64_t)g * p.G + hq) * D;
@@ -307,7 +325,9 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
             for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
         }
         if (warp < nb) {
-            const uint32_t kb = smem_u32(smem + (size_t)st * C::STAGE_BYTES) + warp * C::NCH * C::BOX_BYTES;
+            const uint32_t cstride = cmaj ? C::CHUNK_BYTES : C::BOX_BYTES;
+            const uint32_t kb = smem_u32(smem + (size_t)st * C::STAGE_BYTES) +
+                                warp * (cmaj ? C::BOX_BYTES : C::NCH * C::BOX_BYTES);
             const uint32_t vb = kb + C::KV_BYTES;
             float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
             float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};
@@ -316,7 +336,7 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
 #pragma unroll
                 for (int j = 0; j < C::NT; ++j) {
                     const int u = ((j & 3) << 1) + (lane >> 4);
-                    const uint32_t addr = kb + (j >> 2) * C::BOX_BYTES + r * 128 + ((u ^ (r & 7)) << 4);
+                    const uint32_t addr = kb + (j >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
                     uint32_t a0, a1, a2, a3;
                     ldsm_x4(addr, a0, a1, a2, a3);
                     mma_bf16_16816((j & 1) ? sb : sa, a0, a1, a2, a3, qh[j][0], qh[j][1]);
@@ -355,7 +375,7 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                 O[i][2] *= al0;
                 O[i][3] *= al1;
                 const int u = ((i & 3) << 1) + (mi & 1);
-                const uint32_t addr = vb + (i >> 2) * C::BOX_BYTES + r * 128 + ((u ^ (r & 7)) << 4);
+                const uint32_t addr = vb + (i >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4_t(addr, a0, a1, a2, a3);
                 mma_bf16_16816(O[i], a0, a1, a2, a3, pb0, pb1);
@@ -627,14 +647,15 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// [rows][D] bf16, box = 16 rows x 64 columns (128 B), 128-byte swizzle.
-CUtensorMap make_kv_map(const void* base, int D, int64_t rows) {
+// [rows][D] bf16 viewed as 3-D {64 columns, rows, D/64 chunks} (strides: row
+// D*2 bytes, chunk 128 bytes); box = {64, box_rows, D/64}; 128-byte swizzle.
+CUtensorMap make_kv_map(const void* base, int D, int64_t rows, int box_rows) {
     CUtensorMap m;
-    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-    const cuuint32_t box[2] = {64, (cuuint32_t)kBoxRows};
-    const cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+    const cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(D / 64)};
+    const cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
+    const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)(D / 64)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
                                    dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -668,10 +689,12 @@ template <int D>
 void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
     const View v = make_view(a);
     const int64_t rows = (int64_t)v.n_bg * a.L.l_cap;
-    const CUtensorMap mk = make_kv_map(a.k, D, rows), mv = make_kv_map(a.v, D, rows);
+    const CUtensorMap mk = make_kv_map(a.k, D, rows, kBoxRows), mv = make_kv_map(a.v, D, rows, kBoxRows);
+    const CUtensorMap mk64 = make_kv_map(a.k, D, rows, kBoxRows * kTileBoxes);
+    const CUtensorMap mv64 = make_kv_map(a.v, D, rows, kBoxRows * kTileBoxes);
     const size_t smem = TmaCfg<D>::TOTAL;
     FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_attend_tma<D><<<grid, 160, smem, s>>>(mk, mv, v);
+    k_attend_tma<D><<<grid, 160, smem, s>>>(mk, mv, mk64, mv64, v);
 }
 
 }  // namespace

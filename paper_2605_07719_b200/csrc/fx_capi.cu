@@ -82,6 +82,16 @@ struct fx_ctx {
     uint64_t launches = 0;
     DevBuf step;  // fx_decode_step scratch
     DevBuf api;   // per-query API scratch
+    // optional per-kernel CUDA-event timing (fx_ctx_set_timing)
+    bool timing = false;
+    std::vector<cudaEvent_t> pool;
+    struct Pending {
+        int id;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    double total_ms[FX_KERNEL_COUNT] = {};
+    int64_t count[FX_KERNEL_COUNT] = {};
 };
 
 struct fx_model {
@@ -91,6 +101,49 @@ struct fx_model {
 };
 
 namespace {
+cudaEvent_t pool_event(fx_ctx* c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    FX_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+// Brackets one kernel launch with CUDA events on the ctx stream when timing.
+struct Timed {
+    fx_ctx* c;
+    int id;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timed(fx_ctx* ctx, int kid) : c(ctx), id(kid) {
+        if (!c->timing) return;
+        a = pool_event(c);
+        b = pool_event(c);
+        FX_CUDA(cudaEventRecord(a, c->stream));
+    }
+    ~Timed() {
+        if (!c->timing || !a) return;
+        cudaEventRecord(b, c->stream);
+        c->pending.push_back({id, a, b});
+    }
+};
+
+void collect_timing(fx_ctx* c) {
+    if (c->pending.empty()) return;
+    FX_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        FX_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        c->total_ms[p.id] += ms;
+        c->count[p.id] += 1;
+        c->pool.push_back(p.a);
+        c->pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
 struct DeviceGuard {
     explicit DeviceGuard(fx_ctx* c) {
         FX_REQUIRE(c != nullptr, FX_ERR_STATE, "no-context: null fx_ctx");
@@ -223,6 +276,8 @@ int fx_ctx_destroy(fx_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        collect_timing(ctx);
+        for (auto e : ctx->pool) cudaEventDestroy(e);
         ctx->step.release();
         ctx->api.release();
         if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -248,6 +303,35 @@ int fx_ctx_synchronize(fx_ctx* ctx) {
 }
 
 uint64_t fx_ctx_launches(fx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fx_ctx_set_timing(fx_ctx* ctx, int enable) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        collect_timing(ctx);
+        ctx->timing = enable != 0;
+    });
+}
+
+int fx_ctx_kernel_time(fx_ctx* ctx, int32_t kernel, double* total_ms, int64_t* launches) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(kernel >= 0 && kernel < FX_KERNEL_COUNT, FX_ERR_INVALID, "bad-shape: kernel id");
+        collect_timing(ctx);
+        if (total_ms) *total_ms = ctx->total_ms[kernel];
+        if (launches) *launches = ctx->count[kernel];
+    });
+}
+
+int fx_ctx_reset_timing(fx_ctx* ctx) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        collect_timing(ctx);
+        for (int i = 0; i < FX_KERNEL_COUNT; ++i) {
+            ctx->total_ms[i] = 0.0;
+            ctx->count[i] = 0;
+        }
+    });
+}
 
 int fx_malloc(fx_ctx* ctx, size_t bytes, void** dptr) {
     return guarded([&] {
@@ -308,6 +392,7 @@ int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, v
     return guarded([&] {
         DeviceGuard g(ctx);
         check_layout(lay);
+        Timed tm(ctx, FX_KERNEL_METADATA);
         fx::launch_meta_levels(*lay, k, m16, m32, m64, m128, absmax, ctx->stream);
         ctx->launches += 1;
     });
@@ -486,20 +571,33 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         double* budgets = a->plan_budgets ? a->plan_budgets : s.budgets;
         int32_t* kblocks = a->plan_kblocks ? a->plan_kblocks : s.kblocks;
         cudaStream_t st = ctx->stream;
-        fx::launch_prepare(L, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
-                           a->kslope, a->streaming, blk, budgets, a->plan_volume,
-                           a->plan_cand_volumes, kblocks, s.bg_done, st);
+        {
+            Timed tm(ctx, FX_KERNEL_PLAN);
+            fx::launch_prepare(L, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
+                               a->kslope, a->streaming, blk, budgets, a->plan_volume,
+                               a->plan_cand_volumes, kblocks, s.bg_done, st);
+        }
         int n = 1;
         if (sparse) {
-            fx::launch_approx_scores(L, a->meta, a->q, blk, kblocks, s.approx, s.approx_stride, st);
-            fx::launch_select(L, a->meta, a->absmax, a->q, blk, kblocks, s.approx, s.approx_stride,
-                              s.sel_bits, s.sel_words, s.cand_keys, s.cand_ids, st);
+            {
+                Timed tm(ctx, FX_KERNEL_SCORE);
+                fx::launch_approx_scores(L, a->meta, a->q, blk, kblocks, s.approx, s.approx_stride, st);
+            }
+            {
+                Timed tm(ctx, FX_KERNEL_SELECT);
+                fx::launch_select(L, a->meta, a->absmax, a->q, blk, kblocks, s.approx,
+                                  s.approx_stride, s.sel_bits, s.sel_words, s.cand_keys,
+                                  s.cand_ids, st);
+            }
             n += 2;
         } else {
             FX_CUDA(cudaMemsetAsync(blk, 0, sizeof(int32_t) * L.batch * L.kv_heads, st));
         }
-        fx::launch_worklist(L, a->l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
-                            s.bg_count, s.bg_start, s.bg_done, st);
+        {
+            Timed tm(ctx, FX_KERNEL_WORKLIST);
+            fx::launch_worklist(L, a->l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
+                                s.bg_count, s.bg_start, s.bg_done, st);
+        }
         fx::AttendArgs aa{};
         aa.L = L;
         aa.k = a->k;
@@ -514,7 +612,10 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         aa.bg_done = s.bg_done;
         aa.o = a->o;
         aa.lse = a->lse;
-        fx::launch_attend(aa, grid, true, st);
+        {
+            Timed tm(ctx, FX_KERNEL_ATTEND);
+            fx::launch_attend(aa, grid, true, st);
+        }
         n += 2;
         ctx->launches += n;
     });
@@ -582,6 +683,7 @@ int fx_append_kv(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_t ro
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(row >= 0 && row < lay->l_cap, FX_ERR_INVALID, "bad-shape: append row out of range");
+        Timed tm(ctx, FX_KERNEL_APPEND);
         fx::launch_append(*lay, k, v, row, k_new, v_new, ctx->stream);
         ctx->launches += 1;
     });
