@@ -165,6 +165,13 @@ FX_API int fx_block_scores(fx_ctx* ctx, const float* q, const void* meta, int32_
 FX_API int fx_topk_blocks(fx_ctx* ctx, const float* q, const void* meta, int32_t dtype, int64_t nblk,
                    int32_t dim, int64_t k, uint32_t* blocks_out, int64_t* k_eff, int32_t* clamped);
 
+/* The selection prefilter's approximate f32 scores of every block of every
+ * head at the group granularity blk [dev] [B][Hkv] -> out [dev] [B][H][nblk16]
+ * (row stride nblk16), and the bound scale c of |approx - exact| <= c *
+ * sum_d |q_d| absmax_d that fx_decode_step uses ([host] *eps_scale). */
+FX_API int fx_approx_scores(fx_ctx* ctx, const fx_layout* lay, const void* const meta[4],
+                            const float* q, const int32_t* blk, float* out, double* eps_scale);
+
 /* ---- K5: selector and predictor ------------------------------------------ */
 /* plan_group for n groups of G heads (props [dev] [n][G]) plus blocks_for_budget
  * of each head at the chosen granularity. Outputs [dev]. */

@@ -77,7 +77,9 @@ _SIGS = {
     "fx_block_scores": (C.c_int, [_p, _p, _p, _i32, _i64, _i32, _p]),
     "fx_topk_blocks": (C.c_int, [_p, _p, _p, _i32, _i64, _i32, _i64, _p, C.POINTER(_i64),
                                  C.POINTER(_i32)]),
-    "fx_plan_groups": (C.c_int, [_p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "fx_approx_scores": (C.c_int, [_p, C.POINTER(Layout), _p * 4, _p, _p, _p,
+                                   C.POINTER(C.c_double)]),
+    "fx_plan_groups":(C.c_int, [_p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
     "fx_blocks_for_budget": (C.c_int, [_p, _i32, _p, _p, _i64, _p]),
     "fx_model_create": (C.c_int, [_p] + [_p] * 8 + [C.POINTER(_p)]),
     "fx_model_destroy": (C.c_int, [_p]),

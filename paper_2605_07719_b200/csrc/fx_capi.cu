@@ -182,7 +182,7 @@ StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
     const size_t o_blk = c.take<int32_t>(n_bg);
     const size_t o_bud = c.take<double>(heads);
     const size_t o_kb = c.take<int32_t>(heads);
-    const size_t o_apx = c.take<float>(heads * nblk16);
+    const size_t o_apx = c.take<float>(heads * ((nblk16 + 3) & ~int64_t(3)));
     const size_t o_bits = c.take<uint32_t>(heads * words);
     const size_t o_ck = c.take<uint64_t>(heads * nblk16);
     const size_t o_ci = c.take<uint32_t>(heads * nblk16);
@@ -199,7 +199,7 @@ StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
     s.budgets = reinterpret_cast<double*>(b + o_bud);
     s.kblocks = reinterpret_cast<int32_t*>(b + o_kb);
     s.approx = reinterpret_cast<float*>(b + o_apx);
-    s.approx_stride = nblk16;
+    s.approx_stride = (nblk16 + 3) & ~int64_t(3);
     s.sel_bits = reinterpret_cast<uint32_t*>(b + o_bits);
     s.sel_words = words;
     s.cand_keys = reinterpret_cast<uint64_t*>(b + o_ck);
@@ -226,7 +226,7 @@ size_t step_bytes(const fx_layout& L, int grid) {
     c.take<int32_t>(n_bg);
     c.take<double>(heads);
     c.take<int32_t>(heads);
-    c.take<float>(heads * nblk16);
+    c.take<float>(heads * ((nblk16 + 3) & ~int64_t(3)));
     c.take<uint32_t>(heads * words);
     c.take<uint64_t>(heads * nblk16);
     c.take<uint32_t>(heads * nblk16);
@@ -439,6 +439,28 @@ int fx_topk_blocks(fx_ctx* ctx, const float* q, const void* meta, int32_t dtype,
         int lg = 0;
         for (int64_t x = cap; x > 1; x >>= 1) ++lg;
         ctx->launches += 1 + (uint64_t)lg * (lg + 1) / 2;
+    });
+}
+
+int fx_approx_scores(fx_ctx* ctx, const fx_layout* lay, const void* const meta[4],
+                     const float* q, const int32_t* blk, float* out, double* eps_scale) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const int64_t heads = (int64_t)lay->batch * lay->kv_heads * lay->group_size;
+        Carve c;
+        const size_t ok = c.take<int32_t>(heads);
+        ctx->api.ensure(c.off);
+        int32_t* kb = reinterpret_cast<int32_t*>(static_cast<char*>(ctx->api.p) + ok);
+        // k = 1 for every head: forces scoring wherever a group has >= 2 blocks
+        std::vector<int32_t> ones(heads, 1);
+        FX_CUDA(cudaMemcpyAsync(kb, ones.data(), sizeof(int32_t) * heads, cudaMemcpyHostToDevice,
+                                ctx->stream));
+        fx::launch_approx_scores(*lay, meta, q, blk, kb, out,
+                                 std::max<int64_t>(1, fx::level_blocks(lay->l_cpu, 16)), ctx->stream);
+        FX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (eps_scale) *eps_scale = fx::approx_eps_scale(*lay);
+        ctx->launches += 1;
     });
 }
 

@@ -73,7 +73,8 @@ void launch_predict(int n, const double* w1t, const double* b1, const double* w2
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
                     int32_t* streaming, double* z, cudaStream_t s);
 
-// fx_select.cu
+// fx_score.cu / fx_topk.cu / fx_select.cu
+double approx_eps_scale(const fx_layout& L);
 void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
                           const int32_t* blk, const int32_t* kblocks, float* approx,
                           int64_t approx_stride, cudaStream_t s);

@@ -1,0 +1,317 @@
+// fx_topk.cu -- K2b: bit-exact budgeted top-k block selection per head,
+// topk_blocks (block_index.cpp:55-83): the k highest reference scores, ties to
+// the lower block id, k clamped to the block count.
+//
+// One CTA per head over the approximate scores of fx_score.cu, which satisfy
+// |a - s| <= eps for the reference score s:
+//   1. a linear value-range histogram of a (2048 bins) locates the bin b* that
+//      holds the k-th largest approximate score A_k, so A_k lies in
+//      [e_lo, e_hi] = bin b*'s value range widened by one bin on each side
+//      (the widening absorbs the f32 rounding of the bin map);
+//   2. a > e_hi + 2 eps  =>  s > A_k + eps >= (true k-th score): in the
+//      reference top-k whatever the tie rule;  a < e_lo - 2 eps  =>  out;
+//      everything else is the "band" (typically tens of blocks);
+//   3. band blocks are re-scored with the reference recipe -- products in f64
+//      (exact) by a warp, the sum in dimension order by one lane, unfused --
+//      and ranked by (score desc, id asc); the rest of the k come from there.
+// Output: the selection as a bitmask over the group's blocks.
+#include <algorithm>
+
+#include "fx_common.cuh"
+
+namespace fx {
+namespace {
+
+constexpr int kT = 256;           // threads per selection CTA
+constexpr int kNW = kT / 32;
+constexpr int kBins = 2048;
+constexpr int kMaxWords = 4096;   // nblk <= 131072 at the chosen granularity
+constexpr int kSmemKeys = 16384;  // approximate scores staged in smem up to this many
+constexpr int kSmallCand = 512;   // band ranked in smem by counting up to this size
+
+struct MetaPtrs {
+    const void* p[4];
+};
+__device__ __forceinline__ const void* level_ptr(const void* const* meta, int blk) {
+    return meta[blk == 16 ? 0 : blk == 32 ? 1 : blk == 64 ? 2 : 3];
+}
+
+__device__ __forceinline__ float cta_reduce_max(float v, float* red) {
+    v = warp_max(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float r = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kNW; ++i) r = fmaxf(r, red[i]);
+    return r;
+}
+
+// Reference score of one block by one warp: f64 products in parallel (exact),
+// dimension-order sum by lane 0 (block_index.cpp:41-53).  Valid in lane 0.
+template <typename T>
+__device__ double warp_exact_score(const float* __restrict__ q, const T* __restrict__ mn,
+                                   const T* __restrict__ mx, int D, double* prod) {
+    const int lane = threadIdx.x & 31;
+    for (int d = lane; d < D; d += 32) {
+        const double qd = (double)q[d];
+        const double lo = __dmul_rn(qd, (double)tofl(mn[d]));
+        const double hi = __dmul_rn(qd, (double)tofl(mx[d]));
+        prod[d] = (lo < hi) ? hi : lo;  // std::max(lo, hi)
+    }
+    __syncwarp();
+    double s = 0.0;
+    if (lane == 0)
+        for (int d = 0; d < D; ++d) s = __dadd_rn(s, prod[d]);
+    __syncwarp();
+    return s;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kT) k_select(
+    MetaPtrs meta, const float* __restrict__ absmax, const float* __restrict__ q,
+    const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int Hkv, int G,
+    int D, int64_t l_cpu, const float* __restrict__ approx, int64_t astride, double eps_scale,
+    uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
+    uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap) {
+    using T = typename Elem<DT>::T;
+    // dynamic smem: keys[keys_cap] f32 | hist[kBins] | prod[kNW][D] f64 | ck[kSmallCand] | ci[kSmallCand]
+    extern __shared__ __align__(16) unsigned char dsm[];
+    float* s_keys = reinterpret_cast<float*>(dsm);
+    int32_t* hist = reinterpret_cast<int32_t*>(dsm + (size_t)keys_cap * 4);
+    double* prod_all = reinterpret_cast<double*>(hist + kBins);
+    uint64_t* ck = reinterpret_cast<uint64_t*>(prod_all + kNW * D);
+    uint32_t* ci = reinterpret_cast<uint32_t*>(ck + kSmallCand);
+    __shared__ float red[kNW];
+    __shared__ int s_bin[2];
+    __shared__ unsigned long long s_ndef, s_ncand;
+    __shared__ double s_eps;
+
+    const int64_t head = blockIdx.x;
+    const int64_t H = (int64_t)Hkv * G;
+    const int b = (int)(head / H), h = (int)(head % H), g = h / G;
+    const int bg = b * Hkv + g;
+    const int blk = blk_arr[bg];
+    const int64_t k = kblocks[head];
+    uint32_t* bits = sel_bits + head * sel_words;
+    const int64_t nblk = blk > 0 ? cdiv_dev(l_cpu, blk) : 0;
+    const int W = (int)cdiv_dev(nblk, 32);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    if (nblk == 0 || k <= 0) {
+        for (int j = t; j < W; j += kT) bits[j] = 0u;
+        return;
+    }
+    if (k >= nblk) {  // clamped: every block (block_index.cpp:61-64)
+        for (int j = t; j < W; j += kT) {
+            const int64_t rem = nblk - (int64_t)j * 32;
+            bits[j] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+        }
+        return;
+    }
+    const T* mbase = static_cast<const T*>(level_ptr(meta.p, blk)) + (int64_t)bg * nblk * 2 * D;
+    const float* qh = q + head * D;
+    const float* sc = approx + head * astride;
+    const bool staged = nblk <= keys_cap;
+
+    // ---- 0. stage (128-bit loads, several in flight), min/max, error bound ----
+    float mx = -INFINITY, mn = INFINITY;
+    bool fin_all = true;
+    auto see = [&](float a) {
+        if (isfinite(a)) {
+            mx = fmaxf(mx, a);
+            mn = fminf(mn, a);
+        } else {
+            fin_all = false;
+        }
+    };
+    {
+        const int64_t n4 = nblk >> 2;
+        const float4* sc4 = reinterpret_cast<const float4*>(sc);
+#pragma unroll 4
+        for (int64_t i = t; i < n4; i += kT) {
+            const float4 v = __ldg(sc4 + i);
+            if (staged) reinterpret_cast<float4*>(s_keys)[i] = v;
+            see(v.x);
+            see(v.y);
+            see(v.z);
+            see(v.w);
+        }
+        for (int64_t i = n4 * 4 + t; i < nblk; i += kT) {
+            const float a = sc[i];
+            if (staged) s_keys[i] = a;
+            see(a);
+        }
+    }
+    for (int i = t; i < kBins; i += kT) hist[i] = 0;
+    if (warp == 0) {
+        double a = 0.0;
+        for (int d = lane; d < D; d += 32)
+            a += fabs((double)qh[d]) * (double)absmax[(int64_t)bg * D + d];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) {
+            s_eps = a * eps_scale * 1.01 + 1e-30;
+            s_ndef = 0;
+            s_ncand = 0;
+        }
+    }
+    const float gmx = cta_reduce_max(mx, red);
+    const float gmn = -cta_reduce_max(-mn, red);
+    const bool sane = __syncthreads_and(fin_all) && isfinite(s_eps);
+    const float* src = staged ? s_keys : sc;
+    const double eps = s_eps;
+
+    // ---- 1. bracket A_k ----
+    double e_lo = -INFINITY, e_hi = INFINITY;  // non-finite prefilter: band = everything
+    if (sane && !(gmx > gmn)) {
+        e_lo = e_hi = (double)gmx;  // all equal: A_k is that value
+    } else if (sane) {
+        const float scale = (float)kBins / (gmx - gmn);
+        for (int64_t i = t; i < nblk; i += kT) {
+            const float f = (src[i] - gmn) * scale;
+            atomicAdd(&hist[f >= (float)(kBins - 1) ? kBins - 1 : (f <= 0.f ? 0 : (int)f)], 1);
+        }
+        __syncthreads();
+        if (warp == 0) {  // bin holding the k-th largest, scanning from the top
+            constexpr int PER = kBins / 32;
+            int tot = 0;
+            for (int i = 0; i < PER; ++i) tot += hist[lane * PER + i];
+            int incl = tot;  // count over lanes >= lane
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_down_sync(0xffffffffu, incl, o);
+                if (lane + o < 32) incl += v;
+            }
+            const int excl = incl - tot;
+            if (excl < k && k <= incl) {
+                int above = excl;
+                for (int i = PER - 1; i >= 0; --i) {
+                    above += hist[lane * PER + i];
+                    if (above >= k) {
+                        s_bin[0] = lane * PER + i;
+                        break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const double w = ((double)gmx - (double)gmn) / kBins;
+        e_lo = (double)gmn + (s_bin[0] - 1) * w;
+        e_hi = (double)gmn + (s_bin[0] + 2) * w;
+    }
+    const double hi = e_hi + 2.0 * eps, lo = e_lo - 2.0 * eps;
+
+    // ---- 2. classify: definite-in bits, band appended (warp-aggregated) ----
+    uint32_t* cids = cand_ids + head * cand_stride;
+    uint64_t* ckeys = cand_keys + head * cand_stride;
+    for (int j = warp; j < W; j += kNW) {
+        const int64_t i = (int64_t)j * 32 + lane;
+        const bool in = i < nblk;
+        const double a = in ? (double)src[i] : 0.0;
+        const bool def = in && a > hi;
+        const bool cand = in && !def && a >= lo;
+        const uint32_t bd = __ballot_sync(0xffffffffu, def);
+        const uint32_t bc = __ballot_sync(0xffffffffu, cand);
+        unsigned long long base = 0;
+        if (lane == 0) {
+            bits[j] = bd;
+            if (bd) atomicAdd(&s_ndef, (unsigned long long)__popc(bd));
+            if (bc) base = atomicAdd(&s_ncand, (unsigned long long)__popc(bc));
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (cand) {
+            const int64_t pos = (int64_t)base + __popc(bc & ((1u << lane) - 1u));
+            cids[pos] = (uint32_t)i;
+            if (pos < kSmallCand) ci[pos] = (uint32_t)i;
+        }
+    }
+    __syncthreads();
+    const int64_t n_def = (int64_t)s_ndef, n_cand = (int64_t)s_ncand;
+    const int64_t need = k - n_def;
+    const bool small = n_cand <= kSmallCand;
+
+    // ---- 3. exact scores of the band, rank, set bits ----
+    for (int64_t c = warp; c < n_cand; c += kNW) {
+        const uint32_t id = small ? ci[c] : cids[c];
+        const double s = warp_exact_score(qh, mbase + (int64_t)id * 2 * D,
+                                          mbase + (int64_t)id * 2 * D + D, D, prod_all + warp * D);
+        if (lane == 0) {
+            if (small) ck[c] = f64_key(s);
+            else ckeys[c] = f64_key(s);
+        }
+    }
+    __syncthreads();
+    if (small) {
+        for (int64_t c = t; c < n_cand; c += kT) {
+            const uint64_t kc = ck[c];
+            const uint32_t idc = ci[c];
+            int64_t rank = 0;
+            for (int64_t j = 0; j < n_cand; ++j) {
+                const uint64_t kj = ck[j];
+                rank += (kj > kc) || (kj == kc && ci[j] < idc);
+            }
+            if (rank < need) atomicOr(&bits[idc >> 5], 1u << (idc & 31));
+        }
+    } else if (t == 0) {
+        // Large band (degenerate data): bisect the threshold key, then take the
+        // tied keys lowest id first.
+        uint64_t lo_k = 0, hi_k = ~0ull;  // invariant: count(>= lo_k) >= need
+        while (lo_k < hi_k) {
+            const uint64_t mid = lo_k + ((hi_k - lo_k) >> 1) + 1;
+            int64_t ge = 0;
+            for (int64_t c = 0; c < n_cand; ++c) ge += ckeys[c] >= mid;
+            if (ge >= need) lo_k = mid;
+            else hi_k = mid - 1;
+        }
+        int64_t take = need;
+        for (int64_t c = 0; c < n_cand; ++c)
+            if (ckeys[c] > lo_k) {
+                atomicOr(&bits[cids[c] >> 5], 1u << (cids[c] & 31));
+                --take;
+            }
+        uint32_t last = 0;  // ids taken so far are < ... strictly increasing sweep
+        bool first = true;
+        while (take-- > 0) {
+            uint32_t best = 0xffffffffu;
+            for (int64_t c = 0; c < n_cand; ++c)
+                if (ckeys[c] == lo_k && (first || cids[c] > last) && cids[c] < best) best = cids[c];
+            atomicOr(&bits[best >> 5], 1u << (best & 31));
+            last = best;
+            first = false;
+        }
+    }
+}
+
+}  // namespace
+
+double approx_eps_scale(const fx_layout& L);
+
+void launch_select(const fx_layout& L, const void* const meta[4], const float* absmax,
+                   const float* q, const int32_t* blk, const int32_t* kblocks,
+                   const float* approx, int64_t approx_stride, uint32_t* sel_bits, int sel_words,
+                   uint64_t* cand_keys, uint32_t* cand_ids, cudaStream_t s) {
+    MetaPtrs mp{{meta[0], meta[1], meta[2], meta[3]}};
+    FX_REQUIRE(level_blocks(L.l_cpu, 16) <= (int64_t)kMaxWords * 32, FX_ERR_INVALID,
+               "bad-shape: cpu segment too long for one selection CTA");
+    FX_REQUIRE(L.head_dim <= 256, FX_ERR_INVALID, "bad-shape: head_dim must be <= 256");
+    const int64_t heads = (int64_t)L.batch * L.kv_heads * L.group_size;
+    const int64_t nmax = level_blocks(L.l_cpu, 16);
+    const int keys_cap = (int)((std::min<int64_t>(nmax, kSmemKeys) + 3) & ~int64_t(3));
+    const size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)kNW * L.head_dim * 8 +
+                        (size_t)kSmallCand * 12;
+    const double eps = approx_eps_scale(L);
+    if (L.dtype == FX_BF16) {
+        FX_CUDA(cudaFuncSetAttribute(k_select<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_select<FX_BF16><<<(unsigned)heads, kT, smem, s>>>(
+            mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
+            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap);
+    } else {
+        FX_CUDA(cudaFuncSetAttribute(k_select<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_select<FX_F32><<<(unsigned)heads, kT, smem, s>>>(
+            mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
+            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap);
+    }
+    FX_CUDA(cudaGetLastError());
+}
+
+}  // namespace fx

@@ -381,6 +381,38 @@ def test_execute_task_api(engine, coracle):
     assert rel_err(np.stack(out), wo) < 1e-3
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_approx_score_error_bound(engine, coracle, dtype):
+    """Realized prefilter error vs the bound the exact selection relies on."""
+    import ctypes as C
+    from paper_2605_07719_b200 import _native as N
+    B, Hkv, G, D, l_cpu = 2, 2, 4, 128, 6000
+    dec, host, q = make_decoder(engine, B, Hkv, G, D, 64, l_cpu, 256, dtype, seed=21,
+                                structured=True)
+    worst = 0.0
+    for blk in (16, 32, 64, 128):
+        nblk16 = (l_cpu + 15) // 16
+        out = torch.zeros((B, Hkv * G, nblk16), dtype=torch.float32, device="cuda")
+        blk_t = torch.full((B, Hkv), blk, dtype=torch.int32, device="cuda")
+        qd = torch.as_tensor(q).cuda()
+        eps = C.c_double(0)
+        meta = (C.c_void_p * 4)(*[m.data_ptr() for m in dec.meta])
+        N.check(N.LIB.fx_approx_scores(engine.ctx, C.byref(dec.lay), meta, qd.data_ptr(),
+                                       blk_t.data_ptr(), out.data_ptr(), C.byref(eps)))
+        out = out.cpu().numpy()
+        am = dec.absmax.cpu().numpy()
+        for (b, g), (k, _) in host.items():
+            mins, maxs = coracle.build_metadata(k[64:64 + l_cpu], blk)
+            for hg in range(G):
+                h = g * G + hg
+                exact = coracle.block_scores(q[b, h], mins, maxs)
+                bound = float(np.abs(q[b, h]).astype(np.float64) @ am[b, g].astype(np.float64))
+                err = np.abs(out[b, h, :len(exact)].astype(np.float64) - exact).max()
+                worst = max(worst, err / bound)
+    # the selection assumes err <= eps_scale * bound; demand an 8x safety margin
+    assert worst * 8 <= eps.value, (worst, eps.value)
+
+
 def test_launch_count_per_step(engine):
     dec, _, q = make_decoder(engine, 1, 2, 4, 128, 64, 500, 256, "bf16", seed=0)
     qd = torch.as_tensor(q).cuda()
