@@ -10,39 +10,18 @@
 // build has no FMA (no -march), and contraction would move results by an
 // ulp, which can flip k = ceil(.) at a boundary.
 #include "fx_common.cuh"
+#include "fx_selector_math.h"
 
 namespace fx {
 namespace {
 
-__device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }
-
-// log2 of the candidate granularities is exact.
-__device__ __forceinline__ double log2_blk(int blk) {
-    return blk == 16 ? 4.0 : blk == 32 ? 5.0 : blk == 64 ? 6.0 : blk == 128 ? 7.0 : log2((double)blk);
-}
-
-// selector.cpp:15-19
-__device__ __forceinline__ double budget_at(double bgt0, double k, int streaming, int blk) {
-    if (streaming) return 0.0;
-    const double kk = (k < 0.0) ? 0.0 : k;  // std::max(k, 0.0)
-    return clamp01(__dadd_rn(bgt0, __dmul_rn(kk, log2_blk(blk))));
-}
-
-// selector.cpp:9-13 given the already-clamped sequential budget sum
+using sel::budget_at;
+using sel::clamp01;
 __device__ __forceinline__ double volume_of(int blk, int64_t l_cpu, double clamped_sum) {
-    const double L = (double)l_cpu;
-    return __dadd_rn(__ddiv_rn(__dmul_rn(2.0, L), (double)blk), __dmul_rn(__dmul_rn(2.0, L), clamped_sum));
+    return sel::volume_from_sum(blk, l_cpu, clamped_sum);
 }
-
-// block_index.cpp:96-103
 __device__ __forceinline__ int32_t blocks_for_budget(double budget, int64_t l_cpu, int blk) {
-    if (!(budget > 0.0) || l_cpu == 0 || blk <= 0) return 0;
-    const int64_t nblk = (l_cpu + blk - 1) / blk;
-    const double raw = __ddiv_rn(__dmul_rn(budget, (double)l_cpu), (double)blk);
-    const double c = ceil(__dsub_rn(raw, 1e-12));
-    int64_t k = c <= 0.0 ? 0 : (int64_t)c;
-    if (k < 1) k = 1;
-    return (int32_t)(k < nblk ? k : nblk);
+    return (int32_t)sel::blocks_for_budget(budget, l_cpu, blk);
 }
 
 // Sequential (head-order) sum of clamped budgets across the warp's G lanes.
