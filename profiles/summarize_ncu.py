@@ -1,0 +1,79 @@
+"""Summarize ncu artifacts into profiles/: per-kernel table from a `--set full`
+report and per-launch shares from a `gpu__time_duration` launch list.
+
+    python profiles/summarize_ncu.py gpurun_out/step_r1.ncu-rep gpurun_out/launches_r1.csv > profiles/r1_summary.md
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+METRICS = [
+    ("gpu__time_duration.sum", "time"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "LSU ld sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "LSU ld requests"),
+    ("launch__registers_per_thread", "regs"),
+    ("launch__grid_size", "grid"),
+]
+
+
+def full_report(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    print(f"## ncu --set full: {path}\n")
+    print("| kernel | " + " | ".join(n for _, n in METRICS) + " | top stalls |")
+    print("|---" * (len(METRICS) + 2) + "|")
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+        cells = []
+        for m, _ in METRICS:
+            if m in hdr:
+                i = hdr.index(m)
+                cells.append(f"{r[i]} {units[i]}".strip())
+            else:
+                cells.append("-")
+        st = [(h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
+               float(r[i] or 0)) for i, h in enumerate(hdr)
+              if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")]
+        st = ", ".join(f"{n} {v:.2f}" for n, v in sorted(st, key=lambda x: -x[1])[:3])
+        print(f"| {name} | " + " | ".join(cells) + f" | {st} |")
+    print()
+
+
+def launch_list(path):
+    lines = [ln for ln in open(path) if ln.startswith('"')]  # drop ncu's ==PROF== chatter
+    rows = list(csv.DictReader(lines))
+    t = defaultdict(list)
+    by = defaultdict(dict)
+    for r in rows:
+        key = (r["ID"], r["Kernel Name"].split("(")[0].replace("void ", ""))
+        by[key][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    for (i, name), m in by.items():
+        t[name].append(m)
+    tot = sum(m.get("gpu__time_duration.sum", 0) for v in t.values() for m in v)
+    print(f"## launch list (cold-cache, serialised): {path}\n")
+    print("| kernel | launches | mean time | share of step | DRAM read/launch |")
+    print("|---|---|---|---|---|")
+    for name, v in sorted(t.items(), key=lambda kv: -sum(m.get("gpu__time_duration.sum", 0) for m in kv[1])):
+        s = sum(m.get("gpu__time_duration.sum", 0) for m in v)
+        rd = sum(m.get("dram__bytes_read.sum", 0) for m in v) / len(v)
+        print(f"| {name} | {len(v)} | {s / len(v):.1f} | {100 * s / tot:.1f}% | {rd:.3g} |")
+    print()
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        if p.endswith(".ncu-rep"):
+            full_report(p)
+        else:
+            launch_list(p)
