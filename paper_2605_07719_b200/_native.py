@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libfluxattn_b200.so")
+LIB_PATH = os.environ.get("FLUXATTN_B200_LIB", os.path.join(HERE, "_lib", "libfluxattn_b200.so"))
 
 FX_OK = 0
 FX_F32 = 0

@@ -40,8 +40,9 @@ namespace fx {
 namespace {
 
 constexpr int kCWarps = 4;      // consumer warps
-constexpr int kTileBoxes = 4;   // boxes per pipeline tile (one per consumer warp)
-constexpr int kStages = 5;
+constexpr int kBPW = 2;         // boxes per consumer warp per tile (32 tokens: 2 MMA m-tiles)
+constexpr int kTileBoxes = kCWarps * kBPW;  // boxes per pipeline tile
+constexpr int kStages = 3;      // 64 KB stages (K + V of 8 boxes)
 constexpr int kGen = 128;       // threads of the generic kernel
 constexpr int kGenMaxG = 16;
 constexpr int kGenMaxD = 256;
@@ -213,13 +214,18 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
             const int64_t bg_end = min(r1, (int64_t)__ldg(p.bg_start + bg + 1));
             const Box* bl = p.boxes + (int64_t)bg * p.box_stride - s_bg;
             bool first = true;
-            int64_t win = -1;  // 32-box prefetch window [win, win + 32)
-            Box wbox{0, 0, 0};
+            // box descriptors in two 32-box register windows, the next one
+            // loaded 8 tiles ahead so its latency never stalls the TMA issue
+            int64_t win = x;
+            Box wbox{0, 0, 0}, wnext{0, 0, 0};
+            if (x + lane < bg_end) wbox = bl[x + lane];
+            if (x + 32 + lane < bg_end) wnext = bl[x + 32 + lane];
             while (x < bg_end) {
-                if (win < 0 || x + kTileBoxes > win + 32) {
-                    win = x;
-                    const int64_t gx = x + lane;
-                    if (gx < bg_end) wbox = bl[gx];
+                if (x >= win + 32) {  // tiles never straddle windows (both 4-aligned from s_bg)
+                    win += 32;
+                    wbox = wnext;
+                    const int64_t gx = win + 32 + lane;
+                    if (gx < bg_end) wnext = bl[gx];
                 }
                 const int nb = (int)min((int64_t)kTileBoxes, bg_end - x);
                 Box bx[kTileBoxes];
@@ -297,7 +303,9 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
         const int flags = hdr[st].flags;
         if (flags & F_END) break;
         const int bg = hdr[st].bg, nb = hdr[st].nb;
-        const Box bx = hdr[st].box[warp];
+        const int i0 = warp * kBPW;          // this warp's boxes: i0, i0 + 1
+        const Box bxa = hdr[st].box[i0];
+        const Box bxb = hdr[st].box[i0 + 1];
         const bool cmaj = hdr[st].pad != 0;  // chunk-major (contiguous) tile
         if (flags & F_FIRST) {
             const int b = bg / p.Hkv, g = bg % p.Hkv, hq = lane >> 2;
@@ -324,32 +332,55 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
 #pragma unroll
             for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
         }
-        if (warp < nb) {
+#ifdef FX_ATTEND_NO_MATH  // profiling variant: data delivery only
+        if (false) {
+#else
+        if (i0 < nb) {
+#endif
+            // two boxes (32 tokens) per warp: independent MMA chains interleave
+            const bool two = i0 + 1 < nb;  // warp-uniform
             const uint32_t cstride = cmaj ? C::CHUNK_BYTES : C::BOX_BYTES;
-            const uint32_t kb = smem_u32(smem + (size_t)st * C::STAGE_BYTES) +
-                                warp * (cmaj ? C::BOX_BYTES : C::NCH * C::BOX_BYTES);
-            const uint32_t vb = kb + C::KV_BYTES;
-            float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-            float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint32_t bstride = cmaj ? C::BOX_BYTES : C::NCH * C::BOX_BYTES;
+            const uint32_t ka = smem_u32(smem + (size_t)st * C::STAGE_BYTES) + i0 * bstride;
+            const uint32_t kb2 = ka + bstride;
+            float sha[4] = {0.f, 0.f, 0.f, 0.f}, sla[4] = {0.f, 0.f, 0.f, 0.f};
+            float shb[4] = {0.f, 0.f, 0.f, 0.f}, slb[4] = {0.f, 0.f, 0.f, 0.f};
             {
                 const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
                 for (int j = 0; j < C::NT; ++j) {
                     const int u = ((j & 3) << 1) + (lane >> 4);
-                    const uint32_t addr = kb + (j >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
+                    const uint32_t off = (j >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
                     uint32_t a0, a1, a2, a3;
-                    ldsm_x4(addr, a0, a1, a2, a3);
-                    mma_bf16_16816((j & 1) ? sb : sa, a0, a1, a2, a3, qh[j][0], qh[j][1]);
-                    mma_bf16_16816((j & 1) ? sd : sc, a0, a1, a2, a3, ql[j][0], ql[j][1]);
+                    ldsm_x4(ka + off, a0, a1, a2, a3);
+                    mma_bf16_16816(sha, a0, a1, a2, a3, qh[j][0], qh[j][1]);
+                    mma_bf16_16816(sla, a0, a1, a2, a3, ql[j][0], ql[j][1]);
+                    if (two) {
+                        ldsm_x4(kb2 + off, a0, a1, a2, a3);
+                        mma_bf16_16816(shb, a0, a1, a2, a3, qh[j][0], qh[j][1]);
+                        mma_bf16_16816(slb, a0, a1, a2, a3, ql[j][0], ql[j][1]);
+                    }
                 }
             }
-            const bool v0 = tok0 < bx.n, v1 = tok0 + 8 < bx.n;
-            const bool e0 = (bx.mask >> h0) & 1, e1 = (bx.mask >> (h0 + 1)) & 1;
-            const float s00 = (v0 && e0) ? ((sa[0] + sb[0]) + (sc[0] + sd[0])) * sl2 : -INFINITY;
-            const float s01 = (v0 && e1) ? ((sa[1] + sb[1]) + (sc[1] + sd[1])) * sl2 : -INFINITY;
-            const float s10 = (v1 && e0) ? ((sa[2] + sb[2]) + (sc[2] + sd[2])) * sl2 : -INFINITY;
-            const float s11 = (v1 && e1) ? ((sa[3] + sb[3]) + (sc[3] + sd[3])) * sl2 : -INFINITY;
-            float c0 = fmaxf(s00, s10), c1 = fmaxf(s01, s11);
+            // scores (log2 domain), masked by token validity and head selection
+            float s[2][4];
+            {
+                const Box bxs[2] = {bxa, bxb};
+                const float* hiv[2] = {sha, shb};
+                const float* lov[2] = {sla, slb};
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const bool live = q == 0 || two;
+                    const bool v0 = live && tok0 < bxs[q].n, v1 = live && tok0 + 8 < bxs[q].n;
+                    const bool e0 = (bxs[q].mask >> h0) & 1, e1 = (bxs[q].mask >> (h0 + 1)) & 1;
+                    s[q][0] = (v0 && e0) ? (hiv[q][0] + lov[q][0]) * sl2 : -INFINITY;
+                    s[q][1] = (v0 && e1) ? (hiv[q][1] + lov[q][1]) * sl2 : -INFINITY;
+                    s[q][2] = (v1 && e0) ? (hiv[q][2] + lov[q][2]) * sl2 : -INFINITY;
+                    s[q][3] = (v1 && e1) ? (hiv[q][3] + lov[q][3]) * sl2 : -INFINITY;
+                }
+            }
+            float c0 = fmaxf(fmaxf(s[0][0], s[0][2]), fmaxf(s[1][0], s[1][2]));
+            float c1 = fmaxf(fmaxf(s[0][1], s[0][3]), fmaxf(s[1][1], s[1][3]));
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, o));
@@ -359,13 +390,21 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
             const float b0 = n0 == -INFINITY ? 0.f : n0, b1 = n1 == -INFINITY ? 0.f : n1;
             const float al0 = n0 == -INFINITY ? 1.f : exp2f(m0 - n0);
             const float al1 = n1 == -INFINITY ? 1.f : exp2f(m1 - n1);
-            const uint32_t x0 = pack_bf16(exp2f(s00 - b0), exp2f(s01 - b1));
-            const uint32_t x1 = pack_bf16(exp2f(s10 - b0), exp2f(s11 - b1));
-            l0 = l0 * al0 + (bf16lo_to_f(x0) + bf16lo_to_f(x1));
-            l1 = l1 * al1 + (bf16hi_to_f(x0) + bf16hi_to_f(x1));
+            uint32_t x[2][2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                x[q][0] = pack_bf16(exp2f(s[q][0] - b0), exp2f(s[q][1] - b1));
+                x[q][1] = pack_bf16(exp2f(s[q][2] - b0), exp2f(s[q][3] - b1));
+            }
+            l0 = l0 * al0 + ((bf16lo_to_f(x[0][0]) + bf16lo_to_f(x[0][1])) +
+                             (bf16lo_to_f(x[1][0]) + bf16lo_to_f(x[1][1])));
+            l1 = l1 * al1 + ((bf16hi_to_f(x[0][0]) + bf16hi_to_f(x[0][1])) +
+                             (bf16hi_to_f(x[1][0]) + bf16hi_to_f(x[1][1])));
             m0 = n0;
             m1 = n1;
-            const uint32_t pb0 = movmatrix_t(x0), pb1 = movmatrix_t(x1);
+            const uint32_t pa0 = movmatrix_t(x[0][0]), pa1 = movmatrix_t(x[0][1]);
+            const uint32_t pb0 = movmatrix_t(x[1][0]), pb1 = movmatrix_t(x[1][1]);
+            const uint32_t va = ka + C::KV_BYTES, vb2 = kb2 + C::KV_BYTES;
             const int mi = lane >> 3;
             const int r = (lane & 7) + (mi >> 1) * 8;
 #pragma unroll
@@ -375,10 +414,14 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                 O[i][2] *= al0;
                 O[i][3] *= al1;
                 const int u = ((i & 3) << 1) + (mi & 1);
-                const uint32_t addr = vb + (i >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
+                const uint32_t off = (i >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
                 uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(addr, a0, a1, a2, a3);
-                mma_bf16_16816(O[i], a0, a1, a2, a3, pb0, pb1);
+                ldsm_x4_t(va + off, a0, a1, a2, a3);
+                mma_bf16_16816(O[i], a0, a1, a2, a3, pa0, pa1);
+                if (two) {
+                    ldsm_x4_t(vb2 + off, a0, a1, a2, a3);
+                    mma_bf16_16816(O[i], a0, a1, a2, a3, pb0, pb1);
+                }
             }
         }
         __syncwarp();
