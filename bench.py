@@ -245,7 +245,7 @@ def run_ours(a):
     eng = Engine(local)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    shape = (B, HKV, a.context + total_steps, D)
+    shape = (B, HKV, SparseDecoder.cap_rows(a.context, total_steps), D)
     k = torch.empty(shape, dtype=torch.bfloat16, device=dev)
     v = torch.empty(shape, dtype=torch.bfloat16, device=dev)
     for b in range(B):  # synthetic N(0,1) KV, generated on device

@@ -13,13 +13,18 @@
 // into one global box sequence.  A persistent grid splits that sequence into
 // equal contiguous ranges (split-K over the whole batch): a CTA walks its
 // range, keeps running (m, l, O) per head, and at the end of each (b, g) run
-// writes one partial (o, lse).  The last CTA to finish a (b, g) merges its
-// partials (at most a handful) into the final output -- the fused epilogue.
+// writes the final output when the run lay wholly inside its range, else one
+// partial (o, lse).  Only the two runs cut by a range end can be partial; at
+// the end of its range a CTA counts itself in for those, and the last
+// contributor merges the partials -- the fused epilogue, with no global
+// fence or atomic issued mid-stream.
 //
 // k_attend_tma (bf16, D in {64, 128}, G <= 8):
-//   warp 4        producer: TMA 2-D tiled loads (SWIZZLE_128B) of K and V
-//                 boxes into a kStages-deep smem ring, mbarrier completion;
-//   warps 0..3    consumers: one box each per 4-box tile;
+//   warp 4        producer: one 3-D TMA per 16-row box and tensor
+//                 (SWIZZLE_128B) into a kStages-deep ring of 8-box tiles,
+//                 mbarrier completion;
+//   warps 0..3    consumers: two boxes each per 8-box tile (q of the next
+//                 run prefetched into registers);
 //                 S^T[16 tok x 8 heads] = K . Q^T  (mma.sync m16n8k16 bf16,
 //                 q split hi+lo so q keeps ~16 mantissa bits),
 //                 online softmax in f32 (exp2 domain),
@@ -43,15 +48,21 @@ constexpr int kCWarps = 4;      // consumer warps
 constexpr int kBPW = 2;         // boxes per consumer warp per tile (32 tokens: 2 MMA m-tiles)
 constexpr int kTileBoxes = kCWarps * kBPW;  // boxes per pipeline tile
 constexpr int kStages = 3;      // 64 KB stages (K + V of 8 boxes)
+// TMA kernel warps: kCWarps consumers + one producer
+constexpr int kProducer = kCWarps, kTmaThreads = (kCWarps + 1) * 32;
 constexpr int kGen = 128;       // threads of the generic kernel
 constexpr int kGenMaxG = 16;
 constexpr int kGenMaxD = 256;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
+// tile flags: first / last tile of a run; the run lies wholly in this CTA
+// (its partial is the final output); end of the CTA's range
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_SOLE = 8;
 
 struct TileHdr {
     int32_t bg, flags, nb, pad;
+    int32_t s, e;  // the run's real box range [s, e) in the global sequence
+    int32_t unused[2];
     Box box[kTileBoxes];
 };
 
@@ -65,15 +76,26 @@ struct View {
     const Box* boxes;
     int64_t box_stride;
     const int32_t* bg_start;
+    int pad;  // virtual boxes ending each run in the split (never loaded)
     float* part_o;
     float* part_lse;
-    int32_t* bg_done;
+    int32_t* bg_done;  // [n_bg] contributor counters, zeroed before the launch
     float* o;
     float* lse;
 };
 
 __device__ __forceinline__ int cta_of(int64_t x, int64_t NB, int grid) {
     return (int)(((x + 1) * grid - 1) / NB);
+}
+// Warp-cooperative find_bg: every lane counts the run starts <= x over a
+// strided slice (independent loads, all in flight at once), then a warp sum.
+// One L2 round trip instead of log2(n_bg) dependent ones.
+__device__ __forceinline__ int find_bg_warp(const int32_t* start, int n_bg, int64_t x, int lane) {
+    int cnt = 0;
+    for (int j = 1 + lane; j < n_bg; j += 32) cnt += __ldg(start + j) <= x ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    return cnt;  // start[] is non-decreasing and start[0] = 0 <= x
 }
 __device__ __forceinline__ int find_bg(const int32_t* start, int n_bg, int64_t x) {
     int lo = 0, hi = n_bg - 1;  // largest bg with start[bg] <= x
@@ -91,69 +113,210 @@ __device__ __forceinline__ bool cta_nonempty(int c, int64_t NB, int grid) {
     return NB * c / grid < NB * (c + 1) / grid;
 }
 
-// Partials of `bg` live in slots c + bg for the non-empty CTAs c in [cf, cl].
-__device__ void merge_bg(const View& p, int bg, int cf, int cl, int64_t NB, int grid, int t,
-                         int nt) {
+constexpr int kMaxContrib = 160;  // contributor list held in smem (>= TMA grid)
+
+// Shared scratch of the run merge (MG = largest group size).
+template <int MG>
+struct MergeSmem {
+    int nruns;
+    int runs[2];                // this CTA's runs cut by its range ends (first, last)
+    int rs[2], re[2];           // their real box ranges [s, e)
+    int flag[2];
+    int n;
+    int list[kMaxContrib];      // contributing CTAs (their partial slots are c + bg)
+    float w[kMaxContrib * MG];  // per (contributor, head): LSE, then softmax weight
+    float den[MG];
+    float lse[MG];
+};
+
+// Merge the partials of run `bg` (attention.cpp:89-104 applied across the
+// CTAs that covered it) into the final output.  `nt` threads, barrier `bar`.
+template <int MG>
+__device__ void merge_run(const View& p, int bg, int64_t NB, int grid, int t, int nt, int bar,
+                          MergeSmem<MG>* ms) {
+    const int G = p.G, D = p.D;
+    const int64_t s = __ldg(p.bg_start + bg), e = __ldg(p.bg_start + bg + 1) - p.pad;
+    const int cf = cta_of(s, NB, grid), cl = cta_of(e - 1, NB, grid);
     const int b = bg / p.Hkv, g = bg % p.Hkv;
-    const int64_t H = (int64_t)p.Hkv * p.G;
-    for (int e = t; e < p.G * p.D; e += nt) {
-        const int h = e / p.D, d = e % p.D;
-        float M = -INFINITY;
+    const int64_t head0 = (int64_t)b * p.Hkv * G + (int64_t)g * G;
+    if (t == 0) {
+        int n = 0;
         for (int c = cf; c <= cl; ++c)
-            if (cta_nonempty(c, NB, grid)) M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(c + bg) * p.G + h));
-        const int64_t oh = (int64_t)b * H + (int64_t)g * p.G + h;
-        if (M == -INFINITY) {
-            p.o[oh * p.D + d] = 0.0f;
-            if (d == 0 && p.lse) p.lse[oh] = -INFINITY;
-            continue;
+            if (cta_nonempty(c, NB, grid)) {
+                if (n < kMaxContrib) ms->list[n] = c;
+                ++n;
+            }
+        ms->n = n;
+    }
+    named_bar_sync(bar, nt);
+    const int n = ms->n;
+    if (n <= kMaxContrib) {
+        for (int i = t; i < n * G; i += nt)
+            ms->w[i] = __ldcg(p.part_lse + (int64_t)(ms->list[i / G] + bg) * G + i % G);
+        named_bar_sync(bar, nt);
+        for (int h = t; h < G; h += nt) {
+            float M = -INFINITY;
+            for (int i = 0; i < n; ++i) M = fmaxf(M, ms->w[i * G + h]);
+            float den = 0.f;
+            for (int i = 0; i < n; ++i) {
+                const float li = ms->w[i * G + h];
+                const float wi = (M == -INFINITY || li == -INFINITY) ? 0.f : __expf(li - M);
+                ms->w[i * G + h] = wi;
+                den += wi;
+            }
+            ms->den[h] = den;
+            ms->lse[h] = den > 0.f ? M + __logf(den) : -INFINITY;
         }
-        float num = 0.0f, den = 0.0f;
-        for (int c = cf; c <= cl; ++c) {
-            if (!cta_nonempty(c, NB, grid)) continue;
-            const float li = __ldcg(p.part_lse + (int64_t)(c + bg) * p.G + h);
-            if (li == -INFINITY) continue;
-            const float w = __expf(li - M);
-            num += w * __ldcg(p.part_o + ((int64_t)(c + bg) * p.G + h) * p.D + d);
-            den += w;
+        named_bar_sync(bar, nt);
+        for (int i = t; i < G * D; i += nt) {
+            const int h = i / D, d = i % D;
+            float num = 0.f;
+            for (int j = 0; j < n; ++j) {
+                const float wj = ms->w[j * G + h];
+                if (wj != 0.f) num += wj * __ldcg(p.part_o + ((int64_t)(ms->list[j] + bg) * G + h) * D + d);
+            }
+            const float den = ms->den[h];
+            p.o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
+            if (d == 0 && p.lse) p.lse[head0 + h] = ms->lse[h];
         }
-        p.o[oh * p.D + d] = num / den;
-        if (d == 0 && p.lse) p.lse[oh] = M + __logf(den);
+    } else {  // very long run (generic path only): weights recomputed per element
+        for (int i = t; i < G * D; i += nt) {
+            const int h = i / D, d = i % D;
+            float M = -INFINITY;
+            for (int c = cf; c <= cl; ++c)
+                if (cta_nonempty(c, NB, grid)) M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(c + bg) * G + h));
+            float num = 0.f, den = 0.f;
+            for (int c = cf; c <= cl && M != -INFINITY; ++c) {
+                if (!cta_nonempty(c, NB, grid)) continue;
+                const float li = __ldcg(p.part_lse + (int64_t)(c + bg) * G + h);
+                if (li == -INFINITY) continue;
+                const float wi = __expf(li - M);
+                num += wi * __ldcg(p.part_o + ((int64_t)(c + bg) * G + h) * D + d);
+                den += wi;
+            }
+            p.o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
+            if (d == 0 && p.lse) p.lse[head0 + h] = den > 0.f ? M + __logf(den) : -INFINITY;
+        }
+    }
+    named_bar_sync(bar, nt);
+}
+
+// End of a CTA's range.  Runs wholly inside the CTA were written final at
+// their flush; only the (at most two) runs cut by the range ends left
+// partials.  Count this CTA in for each; the last contributor merges.  Done
+// once, after the CTA's streaming: a global fence or atomic issued while the
+// SM saturates HBM with its own TMA reads waits microseconds behind that
+// traffic, so none is issued mid-stream.
+// Fast merge for the TMA kernel (G * D / 8 <= nt, at most kFastN
+// contributors): every thread owns 8 consecutive columns of one head and
+// issues all its loads (LSE + two float4 per contributor) before using any,
+// so the merge costs one L2 round trip.
+constexpr int kFastN = 4;
+__device__ bool merge_run_fast(const View& p, int bg, const int* list, int n, int t) {
+    const int G = p.G, D = p.D, per = D / 8;
+    if (n > kFastN || G * per > kCWarps * 32 || (D & 7) || (reinterpret_cast<uintptr_t>(p.o) & 15) ||
+        (reinterpret_cast<uintptr_t>(p.part_o) & 15))
+        return false;
+    if (t < G * per) {
+        const int h = t / per, d0 = (t % per) * 8;
+        float l[kFastN];
+        float4 a[kFastN], b[kFastN];
+#pragma unroll
+        for (int j = 0; j < kFastN; ++j)
+            if (j < n) {
+                const int64_t slot = (int64_t)(list[j] + bg) * G + h;
+                l[j] = __ldcg(p.part_lse + slot);
+                a[j] = __ldcg(reinterpret_cast<const float4*>(p.part_o + slot * D + d0));
+                b[j] = __ldcg(reinterpret_cast<const float4*>(p.part_o + slot * D + d0 + 4));
+            }
+        float M = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kFastN; ++j)
+            if (j < n) M = fmaxf(M, l[j]);
+        float den = 0.f, o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < kFastN; ++j)
+            if (j < n && l[j] != -INFINITY) {
+                const float w = __expf(l[j] - M);
+                den += w;
+                o[0] += w * a[j].x; o[1] += w * a[j].y; o[2] += w * a[j].z; o[3] += w * a[j].w;
+                o[4] += w * b[j].x; o[5] += w * b[j].y; o[6] += w * b[j].z; o[7] += w * b[j].w;
+            }
+        const int b_ = bg / p.Hkv, g = bg % p.Hkv;
+        const int64_t oh = (int64_t)b_ * p.Hkv * G + (int64_t)g * G + h;
+        const float inv = den > 0.f ? 1.f / den : 0.f;
+        float4* dst = reinterpret_cast<float4*>(p.o + oh * D + d0);
+        dst[0] = make_float4(o[0] * inv, o[1] * inv, o[2] * inv, o[3] * inv);
+        dst[1] = make_float4(o[4] * inv, o[5] * inv, o[6] * inv, o[7] * inv);
+        if (d0 == 0 && p.lse) p.lse[oh] = den > 0.f ? M + __logf(den) : -INFINITY;
+    }
+    return true;
+}
+
+// End of a CTA's range.  Runs wholly inside the CTA were written final at
+// their flush; only the (at most two) runs cut by the range ends left
+// partials.  Count this CTA in for each; the last contributor merges.  Done
+// once, after the CTA's streaming: a global fence or atomic issued while the
+// SM saturates HBM with its own TMA reads waits microseconds behind that
+// traffic, so none is issued mid-stream.  Cost: fence + counter atomic +
+// one round trip per merged run (fast path).
+template <int MG>
+__device__ void finish_cta(const View& p, int64_t NB, int grid, int t, int nt, int bar,
+                           MergeSmem<MG>* ms, bool fast) {
+    const int nruns = ms->nruns;  // written before the caller's last barrier
+    if (nruns == 0) return;
+    __threadfence();
+    named_bar_sync(bar, nt);
+    if (t < nruns) {  // both counter round trips in flight together
+        const int bg = ms->runs[t];
+        const int cf = cta_of(ms->rs[t], NB, grid), cl = cta_of(ms->re[t] - 1, NB, grid);
+        int n = 0;
+        for (int c = cf; c <= cl; ++c) n += cta_nonempty(c, NB, grid);
+        ms->flag[t] = atomicAdd(p.bg_done + bg, 1) == n - 1;
+    }
+    named_bar_sync(bar, nt);
+    for (int k = 0; k < nruns; ++k) {
+        if (!ms->flag[k]) continue;
+        __threadfence();
+        const int bg = ms->runs[k];
+        if (fast) {
+            const int cf = cta_of(ms->rs[k], NB, grid), cl = cta_of(ms->re[k] - 1, NB, grid);
+            int list[kFastN], n = 0;
+            for (int c = cf; c <= cl && n <= kFastN; ++c)
+                if (cta_nonempty(c, NB, grid)) {
+                    if (n < kFastN) list[n] = c;
+                    ++n;
+                }
+            if (merge_run_fast(p, bg, list, n, t)) continue;
+        }
+        merge_run(p, bg, NB, grid, t, nt, bar, ms);
     }
 }
 
-// After a CTA wrote its partial for `bg`: count it; the last contributor
-// merges.  Called by `nt` threads that share named barrier `bar`.
-__device__ void finish_bg(const View& p, int bg, int64_t NB, int grid, int t, int nt, int bar,
-                          int* s_flag) {
-    __threadfence();
-    named_bar_sync(bar, nt);
-    if (t == 0) {
-        const int64_t s = __ldg(p.bg_start + bg), e = __ldg(p.bg_start + bg + 1);
-        const int cf = cta_of(s, NB, grid), cl = cta_of(e - 1, NB, grid);
-        int n = 0;  // contributing (non-empty) CTAs
-        for (int c = cf; c <= cl; ++c) n += cta_nonempty(c, NB, grid);
-        const int prev = atomicAdd(p.bg_done + bg, 1);
-        s_flag[0] = (prev == n - 1) ? 1 : 0;
-        s_flag[1] = cf;
-        s_flag[2] = cl;
-    }
-    named_bar_sync(bar, nt);
-    if (s_flag[0]) {
-        __threadfence();
-        merge_bg(p, bg, s_flag[1], s_flag[2], NB, grid, t, nt);
-    }
-    named_bar_sync(bar, nt);
+#ifdef FX_TRACE  // profiling build only: per-CTA start/end time, runs, tiles
+__device__ long long g_trace[12 * 2048];
+__device__ __forceinline__ long long globaltimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // TMA + mma.sync kernel
 // ---------------------------------------------------------------------------
+// Tensor maps of K (0) and V (1) viewed 3-D {64 cols, rows, D/64 chunks}
+// (strides: row D*2 B, chunk 128 B); box = 16 rows x all chunks, 128-B swizzle.
+struct KvMaps {
+    CUtensorMap box[2];
+};
+
 template <int D>
 struct TmaCfg {
     static constexpr int NCH = D * 2 / 128;            // 128-byte column chunks per row
     static constexpr int BOX_BYTES = kBoxRows * 128;   // one TMA box = 2 KB
-    static constexpr int CHUNK_BYTES = kTileBoxes * BOX_BYTES;  // one column chunk of a tile
-    static constexpr int KV_BYTES = NCH * CHUNK_BYTES;
+    static constexpr int UNIT_BYTES = NCH * BOX_BYTES;  // one box across all column chunks
+    static constexpr int KV_BYTES = kTileBoxes * UNIT_BYTES;
     static constexpr int STAGE_BYTES = 2 * KV_BYTES;
     static constexpr int NT = D / 16;                  // k-steps (QK) and m-tiles (PV)
     static constexpr int WO_LD = D + 4;
@@ -163,15 +326,12 @@ struct TmaCfg {
     static constexpr size_t WO = BAR + 2 * kStages * sizeof(uint64_t);
     static constexpr size_t WM = WO + (size_t)kCWarps * 8 * WO_LD * sizeof(float);
     static constexpr size_t WL = WM + kCWarps * 8 * sizeof(float);
-    static constexpr size_t FLAG = WL + kCWarps * 8 * sizeof(float);
-    static constexpr size_t TOTAL = FLAG + 16 + 1024;  // + alignment slack
+    static constexpr size_t MRG = WL + kCWarps * 8 * sizeof(float);
+    static constexpr size_t TOTAL = MRG + sizeof(MergeSmem<8>) + 1024;  // + alignment slack
 };
 
 template <int D>
-__global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ CUtensorMap tmK,
-                                                       const __grid_constant__ CUtensorMap tmV,
-                                                       const __grid_constant__ CUtensorMap tmK64,
-                                                       const __grid_constant__ CUtensorMap tmV64,
+__global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_constant__ KvMaps maps,
                                                        const View p) {
     using C = TmaCfg<D>;
     extern __shared__ unsigned char smem_raw[];
@@ -182,7 +342,7 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
     float* wO = reinterpret_cast<float*>(smem + C::WO);
     float* wm = reinterpret_cast<float*>(smem + C::WM);
     float* wl = reinterpret_cast<float*>(smem + C::WL);
-    int* s_flag = reinterpret_cast<int*>(smem + C::FLAG);
+    MergeSmem<8>* ms = reinterpret_cast<MergeSmem<8>*>(smem + C::MRG);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -190,6 +350,7 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
             mbar_init(full + i, 1);
             mbar_init(empty + i, kCWarps);
         }
+        ms->nruns = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -197,22 +358,30 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
     const int64_t NB = __ldg(p.bg_start + p.n_bg);
     const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
 
-    if (warp == kCWarps) {
+    if (warp == kProducer) {
         // ------------------------------ producer ------------------------------
         if (lane == 0) {
-            tma_prefetch_desc(&tmK);
-            tma_prefetch_desc(&tmV);
-            tma_prefetch_desc(&tmK64);
-            tma_prefetch_desc(&tmV64);
+            tma_prefetch_desc(&maps.box[0]);
+            tma_prefetch_desc(&maps.box[1]);
         }
         int st = 0;
+#ifdef FX_TRACE
+        long long p_wait = 0;
+#endif
         uint32_t ph = 0;
         int64_t x = r0;
-        int bg = r0 < r1 ? find_bg(p.bg_start, p.n_bg, r0) : 0;
+        int bg = r0 < r1 ? find_bg_warp(p.bg_start, p.n_bg, r0, lane) : 0;
         while (x < r1) {
             const int64_t s_bg = __ldg(p.bg_start + bg);
-            const int64_t bg_end = min(r1, (int64_t)__ldg(p.bg_start + bg + 1));
+            const int64_t next_bg = __ldg(p.bg_start + bg + 1);
+            const int64_t bg_end = min(r1, next_bg - p.pad);  // real boxes only
+            if (x >= bg_end) {  // only virtual boxes of this run in our range
+                x = next_bg;
+                ++bg;
+                continue;
+            }
             const Box* bl = p.boxes + (int64_t)bg * p.box_stride - s_bg;
+            const int sole = (s_bg >= r0 && next_bg - p.pad <= r1) ? F_SOLE : 0;
             bool first = true;
             // box descriptors in two 32-box register windows, the next one
             // loaded 8 tiles ahead so its latency never stalls the TMA issue
@@ -238,36 +407,39 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                     bx[i].mask = (uint16_t)(nm >> 16);
                 }
                 if (lane == 0) {
+#ifdef FX_TRACE
+                    const long long pw0 = globaltimer();
                     mbar_wait(empty + st, ph ^ 1u);
+                    p_wait += globaltimer() - pw0;
+#else
+                    mbar_wait(empty + st, ph ^ 1u);
+#endif
                     TileHdr& H = hdr[st];
                     H.bg = bg;
                     H.nb = nb;
-                    H.flags = (first ? F_FIRST : 0) | (x + nb == bg_end ? F_LAST : 0);
+                    H.s = (int32_t)s_bg;
+                    H.e = (int32_t)(next_bg - p.pad);
+                    H.flags = (first ? F_FIRST : 0) | (x + nb == bg_end ? F_LAST | sole : 0);
 #pragma unroll
                     for (int i = 0; i < kTileBoxes; ++i) H.box[i] = bx[i];
-                    mbar_arrive_expect_tx(full + st, (uint32_t)(nb * 2 * C::NCH * C::BOX_BYTES));
                     unsigned char* kt = smem + (size_t)st * C::STAGE_BYTES;
                     unsigned char* vt = kt + C::KV_BYTES;
-                    // 3-D maps {64 cols, rows, column chunk}: one TMA moves a whole
-                    // box of rows across every 128-byte chunk.  A tile of 4
-                    // contiguous full boxes is ONE 64-row TMA per tensor and lands
-                    // chunk-major [chunk][64 rows][128 B]; otherwise one 16-row TMA
-                    // per box, box-major [box][chunk][16 rows][128 B].
-                    bool contig = nb == kTileBoxes;
-#pragma unroll
-                    for (int i = 0; i < kTileBoxes; ++i)
-                        contig = contig && bx[i].n == kBoxRows && bx[i].row == bx[0].row + i * kBoxRows;
-                    H.pad = contig ? 1 : 0;
-                    if (contig) {
-                        const int row = (int)((int64_t)bg * p.l_cap + bx[0].row);
-                        tma_load_3d(kt, &tmK64, full + st, 0, row, 0);
-                        tma_load_3d(vt, &tmV64, full + st, 0, row, 0);
-                    } else {
-                        for (int i = 0; i < nb; ++i) {
-                            const int row = (int)((int64_t)bg * p.l_cap + bx[i].row);
-                            tma_load_3d(kt + i * C::NCH * C::BOX_BYTES, &tmK, full + st, 0, row, 0);
-                            tma_load_3d(vt + i * C::NCH * C::BOX_BYTES, &tmV, full + st, 0, row, 0);
-                        }
+                    // Maximal runs of row-contiguous boxes move as power-of-two
+                    // pieces (8/4/2/1 boxes), ONE TMA per piece and tensor: a
+                    // piece of n boxes starting at tile slot s lands chunk-major
+                    // [chunk][16 n rows][128 B] in slots s..s+n-1 (each slot is
+                    // one box across all chunks), so a scattered box is one op
+                    // and a contiguous 8-box tile is one op.  The header records
+                    // each box's piece start / length for the consumers.
+                    // one 3-D TMA per box and tensor (measured faster than merging
+                    // contiguous runs: scratch/tma_bench.cu); box-major smem
+                    // [box][chunk][16 rows][128 B], 128-byte swizzle.
+                    mbar_arrive_expect_tx(full + st, (uint32_t)(nb * 2 * C::NCH * C::BOX_BYTES));
+                    const int64_t base = (int64_t)bg * p.l_cap;
+                    for (int i = 0; i < nb; ++i) {
+                        const int row0 = (int)(base + bx[i].row);
+                        tma_load_3d(kt + i * C::UNIT_BYTES, &maps.box[0], full + st, 0, row0, 0);
+                        tma_load_3d(vt + i * C::UNIT_BYTES, &maps.box[1], full + st, 0, row0, 0);
                     }
                 }
                 __syncwarp();
@@ -278,10 +450,14 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                     ph ^= 1u;
                 }
             }
+            x = max(x, next_bg);  // skip the run's virtual boxes
             ++bg;
         }
         if (lane == 0) {
             mbar_wait(empty + st, ph ^ 1u);
+#ifdef FX_TRACE
+            g_trace[blockIdx.x * 12 + 7] = p_wait;
+#endif
             hdr[st].flags = F_END;
             mbar_arrive(full + st);
         }
@@ -296,28 +472,67 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
     uint32_t qh[C::NT][2], ql[C::NT][2];
 #pragma unroll
     for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
+    float2 qn[C::NT][2];  // raw fp32 q of run qn_bg (prefetched)
+    int qn_bg = -1;
+    auto load_q = [&](int qb) {
+        const int b = qb / p.Hkv, g = qb % p.Hkv, hq = lane >> 2;
+        const float* qp = p.q + ((int64_t)b * p.Hkv * p.G + (int64_t)g * p.G + hq) * D;
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) {
+            const int d0 = 16 * j + 2 * (lane & 3);
+            qn[j][0] = qn[j][1] = make_float2(0.f, 0.f);
+            if (hq < p.G) {
+                qn[j][0] = __ldg(reinterpret_cast<const float2*>(qp + d0));
+                qn[j][1] = __ldg(reinterpret_cast<const float2*>(qp + d0 + 8));
+            }
+        }
+        qn_bg = qb;
+    };
     int st = 0;
     uint32_t ph = 0;
+#ifdef FX_TRACE
+    if (tid == 0) g_trace[blockIdx.x * 12 + 0] = globaltimer();
+    int runs = 0, tiles = 0;
+    long long t_wait = 0, t_first = 0, t_flush = 0, tw0 = 0;
+#endif
     while (true) {
+#ifdef FX_TRACE
+        tw0 = globaltimer();
+#endif
         mbar_wait(full + st, ph);
+#ifdef FX_TRACE
+        t_wait += globaltimer() - tw0;
+#endif
         const int flags = hdr[st].flags;
-        if (flags & F_END) break;
+        if (flags & F_END) {
+#ifdef FX_TRACE
+            if (tid == 0) {
+                g_trace[blockIdx.x * 12 + 1] = globaltimer();
+                g_trace[blockIdx.x * 12 + 2] = runs;
+                g_trace[blockIdx.x * 12 + 3] = tiles;
+                g_trace[blockIdx.x * 12 + 4] = t_wait;
+                g_trace[blockIdx.x * 12 + 5] = t_first;
+                g_trace[blockIdx.x * 12 + 6] = t_flush;
+            }
+#endif
+            break;
+        }
+#ifdef FX_TRACE
+        ++tiles;
+        runs += (hdr[st].flags & F_FIRST) ? 1 : 0;
+#endif
         const int bg = hdr[st].bg, nb = hdr[st].nb;
         const int i0 = warp * kBPW;          // this warp's boxes: i0, i0 + 1
         const Box bxa = hdr[st].box[i0];
         const Box bxb = hdr[st].box[i0 + 1];
-        const bool cmaj = hdr[st].pad != 0;  // chunk-major (contiguous) tile
+#ifdef FX_TRACE
+        tw0 = globaltimer();
+#endif
         if (flags & F_FIRST) {
-            const int b = bg / p.Hkv, g = bg % p.Hkv, hq = lane >> 2;
-            const float* qp = p.q + ((int64_t)b * p.Hkv * p.G + (int64_t)g * p.G + hq) * D;
+            if (bg != qn_bg) load_q(bg);  // prefetch missed (a skipped run)
 #pragma unroll
             for (int j = 0; j < C::NT; ++j) {
-                const int d0 = 16 * j + 2 * (lane & 3);
-                float2 x0 = make_float2(0.f, 0.f), x1 = make_float2(0.f, 0.f);
-                if (hq < p.G) {
-                    x0 = *reinterpret_cast<const float2*>(qp + d0);
-                    x1 = *reinterpret_cast<const float2*>(qp + d0 + 8);
-                }
+                const float2 x0 = qn[j][0], x1 = qn[j][1];
                 const float a0 = __bfloat162float(__float2bfloat16_rn(x0.x));
                 const float a1 = __bfloat162float(__float2bfloat16_rn(x0.y));
                 const float a2 = __bfloat162float(__float2bfloat16_rn(x1.x));
@@ -327,11 +542,17 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                 ql[j][0] = pack_bf16(x0.x - a0, x0.y - a1);
                 ql[j][1] = pack_bf16(x1.x - a2, x1.y - a3);
             }
+            // the next run of this CTA is almost always bg + 1: its q loads
+            // stay in flight for the whole run
+            if (bg + 1 < p.n_bg) load_q(bg + 1);
             m0 = m1 = -INFINITY;
             l0 = l1 = 0.f;
 #pragma unroll
             for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
         }
+#ifdef FX_TRACE
+        if (flags & F_FIRST) { __syncwarp(); t_first += globaltimer() - tw0; }
+#endif
 #ifdef FX_ATTEND_NO_MATH  // profiling variant: data delivery only
         if (false) {
 #else
@@ -339,10 +560,9 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
 #endif
             // two boxes (32 tokens) per warp: independent MMA chains interleave
             const bool two = i0 + 1 < nb;  // warp-uniform
-            const uint32_t cstride = cmaj ? C::CHUNK_BYTES : C::BOX_BYTES;
-            const uint32_t bstride = cmaj ? C::BOX_BYTES : C::NCH * C::BOX_BYTES;
-            const uint32_t ka = smem_u32(smem + (size_t)st * C::STAGE_BYTES) + i0 * bstride;
-            const uint32_t kb2 = ka + bstride;
+            constexpr uint32_t csa = C::BOX_BYTES, csb = C::BOX_BYTES;  // chunk stride in a box
+            const uint32_t ka = smem_u32(smem + (size_t)st * C::STAGE_BYTES) + i0 * C::UNIT_BYTES;
+            const uint32_t kb2 = ka + C::UNIT_BYTES;
             float sha[4] = {0.f, 0.f, 0.f, 0.f}, sla[4] = {0.f, 0.f, 0.f, 0.f};
             float shb[4] = {0.f, 0.f, 0.f, 0.f}, slb[4] = {0.f, 0.f, 0.f, 0.f};
             {
@@ -350,13 +570,13 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
 #pragma unroll
                 for (int j = 0; j < C::NT; ++j) {
                     const int u = ((j & 3) << 1) + (lane >> 4);
-                    const uint32_t off = (j >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
+                    const uint32_t off = r * 128 + ((u ^ (r & 7)) << 4);
                     uint32_t a0, a1, a2, a3;
-                    ldsm_x4(ka + off, a0, a1, a2, a3);
+                    ldsm_x4(ka + (j >> 2) * csa + off, a0, a1, a2, a3);
                     mma_bf16_16816(sha, a0, a1, a2, a3, qh[j][0], qh[j][1]);
                     mma_bf16_16816(sla, a0, a1, a2, a3, ql[j][0], ql[j][1]);
                     if (two) {
-                        ldsm_x4(kb2 + off, a0, a1, a2, a3);
+                        ldsm_x4(kb2 + (j >> 2) * csb + off, a0, a1, a2, a3);
                         mma_bf16_16816(shb, a0, a1, a2, a3, qh[j][0], qh[j][1]);
                         mma_bf16_16816(slb, a0, a1, a2, a3, ql[j][0], ql[j][1]);
                     }
@@ -414,20 +634,23 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                 O[i][2] *= al0;
                 O[i][3] *= al1;
                 const int u = ((i & 3) << 1) + (mi & 1);
-                const uint32_t off = (i >> 2) * cstride + r * 128 + ((u ^ (r & 7)) << 4);
+                const uint32_t off = r * 128 + ((u ^ (r & 7)) << 4);
                 uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(va + off, a0, a1, a2, a3);
+                ldsm_x4_t(va + (i >> 2) * csa + off, a0, a1, a2, a3);
                 mma_bf16_16816(O[i], a0, a1, a2, a3, pa0, pa1);
                 if (two) {
-                    ldsm_x4_t(vb2 + off, a0, a1, a2, a3);
+                    ldsm_x4_t(vb2 + (i >> 2) * csb + off, a0, a1, a2, a3);
                     mma_bf16_16816(O[i], a0, a1, a2, a3, pb0, pb1);
                 }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + st);
+#ifdef FX_TRACE
+        tw0 = globaltimer();
+#endif
         if (flags & F_LAST) {
-            // ---- flush: combine the 4 warps' states into this CTA's partial ----
+            // ---- flush: hand this warp's run state to the epilogue warp ----
             float t0 = l0, t1 = l1;
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
@@ -440,17 +663,30 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                 wl[warp * 8 + h0] = t0;
                 wl[warp * 8 + h0 + 1] = t1;
             }
-            float* wo = wO + (size_t)warp * 8 * C::WO_LD;
+            {
+                float* wo = wO + (size_t)warp * 8 * C::WO_LD;
 #pragma unroll
-            for (int i = 0; i < C::NT; ++i) {
-                const int d0 = 16 * i + tok0;
-                wo[h0 * C::WO_LD + d0] = O[i][0];
-                wo[(h0 + 1) * C::WO_LD + d0] = O[i][1];
-                wo[h0 * C::WO_LD + d0 + 8] = O[i][2];
-                wo[(h0 + 1) * C::WO_LD + d0 + 8] = O[i][3];
+                for (int i = 0; i < C::NT; ++i) {
+                    const int d0 = 16 * i + tok0;
+                    wo[h0 * C::WO_LD + d0] = O[i][0];
+                    wo[(h0 + 1) * C::WO_LD + d0] = O[i][1];
+                    wo[h0 * C::WO_LD + d0 + 8] = O[i][2];
+                    wo[(h0 + 1) * C::WO_LD + d0 + 8] = O[i][3];
+                }
             }
             named_bar_sync(1, kCWarps * 32);
-            const int slot = blockIdx.x + bg;
+            // a run wholly inside this CTA is final; else a partial for finish_cta
+            const bool sole = flags & F_SOLE;
+            if (!sole && tid == 0) {
+                ms->runs[ms->nruns] = bg;
+                ms->rs[ms->nruns] = hdr[st].s;
+                ms->re[ms->nruns] = hdr[st].e;
+                ++ms->nruns;
+            }
+            const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * p.G + (int64_t)(bg % p.Hkv) * p.G
+                                       : (int64_t)(blockIdx.x + bg) * p.G;
+            float* dst_o = sole ? p.o : p.part_o;
+            float* dst_l = sole ? p.lse : p.part_lse;
             for (int e = tid; e < p.G * D; e += kCWarps * 32) {
                 const int h = e / D, d = e % D;
                 float M = -INFINITY;
@@ -466,17 +702,27 @@ __global__ void __launch_bounds__(160, 1) k_attend_tma(const __grid_constant__ C
                         den += f * wl[w * 8 + h];
                     }
                 }
-                p.part_o[((int64_t)slot * p.G + h) * D + d] = den > 0.f ? num / den : 0.f;
-                if (d == 0)
-                    p.part_lse[(int64_t)slot * p.G + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
+                dst_o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
+                if (d == 0 && dst_l) dst_l[head0 + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
             }
-            finish_bg(p, bg, NB, grid, tid, kCWarps * 32, 1, s_flag);
+            named_bar_sync(1, kCWarps * 32);  // wO / wm / wl reused by the next run
+#ifdef FX_TRACE
+            t_flush += globaltimer() - tw0;
+#endif
         }
         if (++st == kStages) {
             st = 0;
             ph ^= 1u;
         }
     }
+    finish_cta(p, NB, grid, tid, kCWarps * 32, 1, ms, true);
+#ifdef FX_TRACE
+    if (tid == 0) {
+        g_trace[blockIdx.x * 12 + 8] = globaltimer();
+        g_trace[blockIdx.x * 12 + 9] = ms->nruns;
+        g_trace[blockIdx.x * 12 + 10] = ms->nruns > 0 ? ms->flag[0] + (ms->nruns > 1 ? ms->flag[1] : 0) : 0;
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -495,21 +741,30 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
     float* mst = scm + kBoxRows * G;
     float* lst = mst + G;
     float* alp = lst + G;
-    __shared__ int s_flag[4];
 #define Ks(r, d) Ksm[(r) * (D + 1) + (d)]
 #define Vs(r, d) Vsm[(r) * D + (d)]
 #define qs(h, d) qsm[(h) * D + (d)]
 #define sc(r, h) scm[(r) * G + (h)]
+    __shared__ MergeSmem<kGenMaxG> ms;
     const int grid = gridDim.x, cta = blockIdx.x;
     const int64_t NB = __ldg(p.bg_start + p.n_bg);
     const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
     if (r0 >= r1) return;
+    if (t == 0) ms.nruns = 0;
     const float scale = rsqrtf((float)D);
     float acc[kGenMaxG][2];
     int bg = find_bg(p.bg_start, p.n_bg, r0);
     int64_t s_bg = __ldg(p.bg_start + bg), e_bg = __ldg(p.bg_start + bg + 1);
     bool fresh = true;
     for (int64_t x = r0; x < r1; ++x) {
+        while (x >= e_bg - p.pad) {  // range starts in (or reaches) virtual boxes
+            x = e_bg;
+            if (x >= r1) goto done;
+            ++bg;
+            s_bg = __ldg(p.bg_start + bg);
+            e_bg = __ldg(p.bg_start + bg + 1);
+            fresh = true;
+        }
         if (fresh) {
             const int b = bg / p.Hkv, g = bg % p.Hkv;
             const float* qp = p.q + ((int64_t)b * p.Hkv * G + (int64_t)g * G) * D;
@@ -579,22 +834,32 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
             }
         }
         __syncthreads();
-        if (x + 1 == r1 || x + 1 == e_bg) {
-            const int slot = cta + bg;
+        if (x + 1 == r1 || x + 1 == e_bg - p.pad) {
+            // a run wholly inside this CTA is final; else a partial for finish_cta
+            const bool sole = s_bg >= r0 && e_bg - p.pad <= r1;
+            if (!sole && t == 0) {
+                ms.runs[ms.nruns] = bg;
+                ms.rs[ms.nruns] = (int)s_bg;
+                ms.re[ms.nruns] = (int)(e_bg - p.pad);
+                ++ms.nruns;
+            }
+            const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * G + (int64_t)(bg % p.Hkv) * G
+                                       : (int64_t)(cta + bg) * G;
+            float* dst_o = sole ? p.o : p.part_o;
+            float* dst_l = sole ? p.lse : p.part_lse;
 #pragma unroll
             for (int dd = 0; dd < 2; ++dd) {
                 const int d = t + dd * kGen;
                 if (d < D) {
 #pragma unroll
                     for (int h = 0; h < kGenMaxG; ++h)
-                        if (h < G)
-                            p.part_o[((int64_t)slot * G + h) * D + d] = lst[h] > 0.f ? acc[h][dd] / lst[h] : 0.f;
+                        if (h < G) dst_o[(head0 + h) * D + d] = lst[h] > 0.f ? acc[h][dd] / lst[h] : 0.f;
                 }
             }
-            if (t < G)
-                p.part_lse[(int64_t)slot * G + t] = lst[t] > 0.f ? mst[t] + logf(lst[t]) : -INFINITY;
-            finish_bg(p, bg, NB, grid, t, kGen, 1, s_flag);
+            if (t < G && dst_l) dst_l[head0 + t] = lst[t] > 0.f ? mst[t] + logf(lst[t]) : -INFINITY;
+            __syncthreads();
             if (x + 1 < r1) {
+                x = e_bg - 1;  // skip the run's virtual boxes
                 ++bg;
                 s_bg = __ldg(p.bg_start + bg);
                 e_bg = __ldg(p.bg_start + bg + 1);
@@ -602,6 +867,9 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
             }
         }
     }
+done:
+    __syncthreads();
+    finish_cta(p, NB, grid, t, kGen, 1, &ms, false);
 }
 
 #undef Ks
@@ -720,6 +988,7 @@ View make_view(const AttendArgs& a) {
     v.boxes = a.boxes;
     v.box_stride = a.box_stride;
     v.bg_start = a.bg_start;
+    v.pad = a.pad;
     v.part_o = a.part_o;
     v.part_lse = a.part_lse;
     v.bg_done = a.bg_done;
@@ -732,12 +1001,12 @@ template <int D>
 void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
     const View v = make_view(a);
     const int64_t rows = (int64_t)v.n_bg * a.L.l_cap;
-    const CUtensorMap mk = make_kv_map(a.k, D, rows, kBoxRows), mv = make_kv_map(a.v, D, rows, kBoxRows);
-    const CUtensorMap mk64 = make_kv_map(a.k, D, rows, kBoxRows * kTileBoxes);
-    const CUtensorMap mv64 = make_kv_map(a.v, D, rows, kBoxRows * kTileBoxes);
+    KvMaps maps;
+    maps.box[0] = make_kv_map(a.k, D, rows, kBoxRows);
+    maps.box[1] = make_kv_map(a.v, D, rows, kBoxRows);
     const size_t smem = TmaCfg<D>::TOTAL;
     FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_attend_tma<D><<<grid, 160, smem, s>>>(mk, mv, mk64, mv64, v);
+    k_attend_tma<D><<<grid, kTmaThreads, smem, s>>>(maps, v);
 }
 
 }  // namespace
@@ -751,7 +1020,7 @@ int attend_grid(const fx_layout& L, bool has_idx, int num_sms) {
     return attend_uses_tma(L, has_idx) ? num_sms : num_sms * 4;
 }
 
-void launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
+int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
     FX_REQUIRE(a.L.group_size >= 1 && a.L.group_size <= kGenMaxG, FX_ERR_INVALID,
                "bad-shape: group_size must be in [1, 16]");
     FX_REQUIRE(a.L.head_dim >= 1 && a.L.head_dim <= kGenMaxD, FX_ERR_INVALID,
@@ -773,6 +1042,7 @@ void launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s
         }
     }
     FX_CUDA(cudaGetLastError());
+    return 1;
 }
 
 void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done,
@@ -811,3 +1081,9 @@ void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream
 }
 
 }  // namespace fx
+
+#ifdef FX_TRACE
+extern "C" FX_API int fx_debug_trace(long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, fx::g_trace, sizeof(long long) * n) == cudaSuccess ? 0 : -2;
+}
+#endif

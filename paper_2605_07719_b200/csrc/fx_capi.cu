@@ -629,6 +629,7 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         aa.boxes = s.boxes;
         aa.box_stride = s.box_stride;
         aa.bg_start = s.bg_start;
+        aa.pad = fx::kRunPad;  // the worklist prefix includes kRunPad per run
         aa.part_o = s.part_o;
         aa.part_lse = s.part_lse;
         aa.bg_done = s.bg_done;
@@ -636,9 +637,9 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         aa.lse = a->lse;
         {
             Timed tm(ctx, FX_KERNEL_ATTEND);
-            fx::launch_attend(aa, grid, true, st);
+            n += fx::launch_attend(aa, grid, true, st);
         }
-        n += 2;
+        n += 1;  // worklist
         ctx->launches += n;
     });
 }
@@ -677,15 +678,14 @@ int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void
         aa.boxes = reinterpret_cast<fx::Box*>(b + ob);
         aa.box_stride = nb;
         aa.bg_start = reinterpret_cast<int32_t*>(b + os);
-        aa.bg_done = reinterpret_cast<int32_t*>(b + od);
         aa.part_o = reinterpret_cast<float*>(b + oo);
         aa.part_lse = reinterpret_cast<float*>(b + ol);
+        aa.bg_done = reinterpret_cast<int32_t*>(b + od);
         aa.o = o;
         aa.lse = lse;
         fx::launch_index_boxes(n, const_cast<fx::Box*>(aa.boxes), const_cast<int32_t*>(aa.bg_start),
                                aa.bg_done, ctx->stream);
-        fx::launch_attend(aa, grid, false, ctx->stream);
-        ctx->launches += 2;
+        ctx->launches += 1 + fx::launch_attend(aa, grid, false, ctx->stream);
     });
 }
 

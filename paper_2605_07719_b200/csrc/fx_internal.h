@@ -13,6 +13,11 @@ namespace fx {
 
 // Rows per TMA box / per attention "box" (one 16-token slab of one (b, g)).
 constexpr int kBoxRows = 16;
+// Virtual boxes appended to every (b, g) run when the attention grid splits the
+// global box sequence: a run's fixed cost (q load, partial flush, merge) is
+// ~this many boxes of streaming, so CTAs covering many short runs get fewer
+// boxes.  Virtual boxes are never loaded.
+constexpr int kRunPad = 16;
 // Candidate granularities, selector.hpp:12.
 constexpr int kLevels[4] = {16, 32, 64, 128};
 
@@ -104,7 +109,8 @@ struct AttendArgs {
     const uint32_t* idx;      // index boxes (API path) or nullptr
     const Box* boxes;         // [n_bg][box_stride]
     int64_t box_stride;
-    const int32_t* bg_start;  // [n_bg + 1] exclusive prefix of box counts
+    const int32_t* bg_start;  // [n_bg + 1] exclusive prefix of (box count + pad)
+    int pad;                  // virtual boxes at the end of each run (kRunPad or 0)
     float* part_o;            // [(grid + n_bg)][G][D]
     float* part_lse;          // [(grid + n_bg)][G]
     int32_t* bg_done;         // [n_bg], zeroed before the launch
@@ -113,7 +119,8 @@ struct AttendArgs {
 };
 bool attend_uses_tma(const fx_layout& L, bool has_idx);
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms);
-void launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s);
+// returns the number of kernels launched
+int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s);
 void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done,
                         cudaStream_t s);
 void launch_merge_partials(int n, int dim, const float* o_parts, const float* lse_parts, float* o,

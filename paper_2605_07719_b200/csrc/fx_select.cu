@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_worklist(int Hkv, int G, int64_t l_sink
     // last CTA: exclusive prefix of box counts over (b, g)
     for (int i0 = 0, run = 0; i0 < n_bg; i0 += blockDim.x) {
         const int i = i0 + t;
-        int v = i < n_bg ? __ldcg(bg_count + i) : 0;
+        int v = i < n_bg ? __ldcg(bg_count + i) + kRunPad : 0;  // + virtual run cost
         // block inclusive scan of v
         int x = v;
         for (int o = 1; o < 32; o <<= 1) {

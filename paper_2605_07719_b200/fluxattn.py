@@ -412,7 +412,7 @@ class SparseDecoder:
         self.tdtype = tdt
         self.lay = N.Layout(batch, kv_heads, group_size, head_dim,
                             N.FX_BF16 if dtype == "bf16" else N.FX_F32, 0, l_sink, l_cpu,
-                            l_local, l_sink + l_cpu + l_local + max_new)
+                            l_local, SparseDecoder.cap_rows(l_sink + l_cpu + l_local, max_new))
         shape = (batch, kv_heads, self.lay.l_cap, head_dim)
         dev = engine.device
         self.k = k if k is not None else torch.zeros(shape, dtype=tdt, device=dev)
@@ -437,6 +437,12 @@ class SparseDecoder:
         self.o = torch.empty((batch, H, head_dim), dtype=torch.float32, device=dev)
         self.lse = torch.empty((batch, H), dtype=torch.float32, device=dev)
         self.args = N.StepArgs()
+
+    @staticmethod
+    def cap_rows(context: int, max_new: int) -> int:
+        """Rows per (b, g): context + decode room, rounded up to a multiple of 16
+        so every (b, g) starts on a 16-row TMA unit."""
+        return (context + max_new + 15) // 16 * 16
 
     # -- data --------------------------------------------------------------
     def load_group(self, b: int, g: int, k: np.ndarray, v: np.ndarray) -> None:

@@ -418,4 +418,4 @@ def test_launch_count_per_step(engine):
     qd = torch.as_tensor(q).cuda()
     n0 = engine.launches()
     dec.step(qd, fixed=(16, 0.05))
-    assert engine.launches() - n0 == 5
+    assert engine.launches() - n0 == 5  # plan, score, select, worklist, attend (+ fused merge)
