@@ -24,6 +24,11 @@
  *   fx_decode_step              <- run(queue, profile, RunMode::Executed)
  *                                  src/scheduler.cpp:283-287 over one decode step
  *                                  of run_decode (src/pipeline.cpp:292-363)
+ *   fx_cp_candidates/threshold/select/combine
+ *                               <- topk_blocks + merge_into (block_index.cpp:55-83,
+ *                                  attention.cpp:89-104) split over context-parallel
+ *                                  shards (the 1M-token C5 case; the reference has no
+ *                                  multi-device code)
  */
 #ifndef FLUXATTN_B200_H
 #define FLUXATTN_B200_H
@@ -35,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FX_ABI_VERSION 1
+#define FX_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define FX_API __attribute__((visibility("default")))
@@ -104,6 +109,12 @@ typedef struct fx_step_args {
     int32_t sel_words;           /* words per head in sel_bits (>= ceil(nblk16/32)) */
     float* o;                    /* out: [B][H][D] f32 attention output (defaults (+) sparse) */
     float* lse;                  /* out, optional: [B][H] natural-log LSE of the merged output */
+    /* context-parallel shard (C5); all zero on a single device */
+    int64_t l_cpu_total;         /* cpu rows of the WHOLE sequence: plan_group and blocks_for_budget
+                                    use it (0 = lay->l_cpu) */
+    int64_t cpu_offset;          /* global row of this shard's first cpu row (multiple of 128) */
+    const uint32_t* sel_in;      /* given selection [B][H][sel_words] over this shard's blocks at
+                                    plan_blk: skips score/select (requires FX_PLAN_GIVEN) */
 } fx_step_args;
 
 /* ---- context, errors, memory ------------------------------------------ */
@@ -215,6 +226,47 @@ FX_API int fx_append_kv(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int
                  const float* k_new, const float* v_new);
 /* Convert f32 -> dtype on device (n elements). */
 FX_API int fx_convert(fx_ctx* ctx, const float* src, void* dst, int32_t dtype, size_t n);
+
+/* ---- context-parallel decode (C5) ------------------------------------------
+ * The cpu segment is split into contiguous 128-row-aligned shards, one per
+ * rank (sink rows on rank 0, local + decoded rows on the last rank), so block
+ * b of every granularity lives whole on one shard and keeps its global id.
+ * The global top-k of each head (topk_blocks, block_index.cpp:55-83) is
+ * reproduced bit-exactly from the shards' local top-k lists:
+ *   1. fx_cp_candidates: every shard selects its min(k, nblk_local) best
+ *      blocks and emits them with exact reference scores;
+ *   2. exchange kth (all-gather) -> fx_cp_threshold: T = max over shards of
+ *      the local k-th key, a lower bound of the global k-th score;
+ *   3. exchange the entries with key >= T (all-gather) -> fx_cp_select: the
+ *      global (score desc, id asc) rank of each own entry, bits for rank < k;
+ *   4. fx_decode_step (FX_PLAN_GIVEN + sel_in) -> the shard's (o, lse);
+ *   5. exchange (o, lse) (all-gather) -> fx_cp_combine (merge_into).
+ * Keys are order-preserving u64 images of the f64 scores (0 = empty slot). */
+/* Plan with args->l_cpu_total (plan_* outputs as in fx_decode_step), select this
+ * shard's best min(k, nblk_local) blocks per head and emit them sorted (score
+ * desc, id asc): keys/ids [dev] [B*H][cap] (global block ids, zero-filled past
+ * count), count [dev] [B*H], kth [dev] [B*H] = key of the k-th entry when the
+ * shard holds >= k blocks, else 0. */
+FX_API int fx_cp_candidates(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* args,
+                            int64_t cap, uint64_t* keys, uint32_t* ids, int32_t* count,
+                            uint64_t* kth);
+/* thresh [dev] [n] = max over the R shards of kth_all [dev] [R][n];
+ * keep [dev] [n] = entries of this shard's sorted keys [n][cap] with key >= thresh. */
+FX_API int fx_cp_threshold(fx_ctx* ctx, int32_t ranks, int64_t n, int64_t cap,
+                           const uint64_t* keys, const uint64_t* kth_all, uint64_t* thresh,
+                           int32_t* keep);
+/* From the gathered candidates gkeys/gids [dev] [R][n = B*H][m] (each shard's
+ * first m sorted entries; slots with key < thresh or key 0 are ignored), set
+ * bit (id - cpu_offset/blk) of sel_out [dev] [B*H][sel_words] for every entry
+ * of shard `self` whose global rank by (key desc, id asc) is < kblocks[h]. */
+FX_API int fx_cp_select(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t self, int64_t m,
+                        const uint64_t* gkeys, const uint32_t* gids, const uint64_t* thresh,
+                        const int32_t* kblocks, const int32_t* blk, int64_t cpu_offset,
+                        uint32_t* sel_out, int32_t sel_words);
+/* merge_into over the R shard partials: o_parts [dev] [R][n][dim], lse_parts
+ * [dev] [R][n] (natural log, -inf = empty) -> o [dev] [n][dim], lse [dev] [n]. */
+FX_API int fx_cp_combine(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim, const float* o_parts,
+                         const float* lse_parts, float* o, float* lse);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@ FX_PLAN_PROPS = 0
 FX_PLAN_FIXED = 1
 FX_PLAN_FULL = 2
 FX_PLAN_GIVEN = 3
+ABI_VERSION = 2
 KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append")
 
 _p = C.c_void_p
@@ -41,7 +42,9 @@ class StepArgs(C.Structure):
                 ("fixed_budget", C.c_double), ("bgt0", _p), ("kslope", _p), ("streaming", _p),
                 ("plan_blk", _p), ("plan_budgets", _p), ("plan_volume", _p),
                 ("plan_cand_volumes", _p), ("plan_kblocks", _p), ("sel_bits", _p),
-                ("sel_words", _i32), ("o", _p), ("lse", _p)]
+                ("sel_words", _i32), ("o", _p), ("lse", _p),
+                # context-parallel shard (C5); zero on a single device
+                ("l_cpu_total", _i64), ("cpu_offset", _i64), ("sel_in", _p)]
 
 
 class NativeError(RuntimeError):
@@ -89,6 +92,11 @@ _SIGS = {
     "fx_merge_partials": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p]),
     "fx_append_kv": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p]),
     "fx_convert": (C.c_int, [_p, _p, _p, _i32, _sz]),
+    "fx_cp_candidates": (C.c_int, [_p, C.POINTER(Layout), C.POINTER(StepArgs), _i64, _p, _p, _p, _p]),
+    "fx_cp_threshold": (C.c_int, [_p, _i32, _i64, _i64, _p, _p, _p, _p]),
+    "fx_cp_select": (C.c_int, [_p, C.POINTER(Layout), _i32, _i32, _i64, _p, _p, _p, _p, _p, _i64,
+                               _p, _i32]),
+    "fx_cp_combine": (C.c_int, [_p, _i32, _i64, _i32, _p, _p, _p, _p]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -104,7 +112,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.fx_abi_version() != 1:
+    if lib.fx_abi_version() != ABI_VERSION:
         raise ImportError("fluxattn_b200 ABI version mismatch")
     return lib
 

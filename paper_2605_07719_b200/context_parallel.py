@@ -1,0 +1,229 @@
+"""Context-parallel sparse decode over cpu-segment shards (config C5: 1M-token
+context, batch 4, 8 x B200).
+
+The reference is single-device: ``execute_task``
+(scheduler.cpp:78-96) runs topk_blocks (block_index.cpp:55-83) over the whole
+cpu segment and merge_into (attention.cpp:89-104) over the partials.  Here the
+cpu segment of every (b, g) is split into contiguous 128-row-aligned shards,
+one per rank, with the sink rows on rank 0 and local + decoded rows on the last
+rank.  A block of any candidate granularity (16..128) then lives whole on one
+shard and keeps its global id, and one decode step is
+
+    1. fx_cp_candidates  plan (whole-sequence L_cpu), local top-min(k, nblk)
+                          with exact reference scores, sorted
+    2. all-gather kth  -> fx_cp_threshold   T = max_r (local k-th key)
+    3. all-gather the entries with key >= T -> fx_cp_select   global ranks
+    4. fx_decode_step  (given plan + given selection) -> shard (o, lse)
+    5. all-gather (o, lse) -> fx_cp_combine (LSE merge)
+
+which reproduces the single-device selection bit-exactly (argument in
+csrc/fx_cp.cu) and its output within the f32 merge tolerance.  All three
+exchanges are small (B*H*8 B, ~B*H*k*12 B, B*H*(D+1)*4 B); they go through
+``torch.distributed`` (NCCL over NVLink on the box).  ``LoopbackComm`` runs all
+shards of a step in one process (tests, and the single-GPU measurement), with
+the identical phase code.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import LIB, check
+from .fluxattn import Engine, SparseDecoder
+
+ALIGN = 128  # shard boundaries: multiple of every candidate granularity
+
+
+def shard_bounds(l_cpu: int, ranks: int) -> List[Tuple[int, int]]:
+    """(offset, rows) of each rank's cpu chunk: equal 128-aligned chunks, the
+    last one holding the remainder (possibly empty chunks at the end)."""
+    chunk = -(-l_cpu // ranks)
+    chunk = -(-chunk // ALIGN) * ALIGN
+    out = []
+    for r in range(ranks):
+        a = min(l_cpu, r * chunk)
+        out.append((a, min(l_cpu, a + chunk) - a))
+    return out
+
+
+def shard_kv(k_full: torch.Tensor, l_sink: int, l_cpu: int, l_local: int, rank: int, ranks: int,
+             max_new: int = 64) -> torch.Tensor:
+    """Rank `rank`'s rows of a single-device cache [B][Hkv][rows][D] (sink | cpu |
+    local ...), laid out as that shard's SparseDecoder cache."""
+    off, n = shard_bounds(l_cpu, ranks)[rank]
+    last = rank == ranks - 1
+    parts = []
+    if rank == 0:
+        parts.append(k_full[:, :, :l_sink])
+    parts.append(k_full[:, :, l_sink + off:l_sink + off + n])
+    if last:
+        parts.append(k_full[:, :, l_sink + l_cpu:l_sink + l_cpu + l_local])
+    rows = sum(p.shape[2] for p in parts)
+    cap = SparseDecoder.cap_rows(rows, max_new if last else 0)
+    out = torch.zeros(k_full.shape[:2] + (cap, k_full.shape[3]), dtype=k_full.dtype,
+                      device=k_full.device)
+    out[:, :, :rows] = torch.cat(parts, dim=2)
+    return out
+
+
+class TorchComm:
+    """Exchanges of one rank over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.ranks = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, local: Sequence[torch.Tensor]) -> torch.Tensor:
+        (t,) = local
+        t = t.contiguous()
+        out = torch.empty((self.ranks,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return out
+
+    def max_int(self, local: Sequence[int], device) -> int:
+        (v,) = local
+        t = torch.tensor([int(v)], dtype=torch.int64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+
+class LoopbackComm:
+    """All ranks' shards in this process: the exchanges are stacks."""
+
+    def __init__(self, ranks: int):
+        self.ranks = ranks
+
+    def all_gather(self, local: Sequence[torch.Tensor]) -> torch.Tensor:
+        assert len(local) == self.ranks
+        return torch.stack([t.contiguous() for t in local])
+
+    def max_int(self, local: Sequence[int], device) -> int:
+        return max(int(v) for v in local)
+
+
+class CPShard:
+    """One rank's share of a context-parallel batch: a SparseDecoder over its
+    cpu chunk (+ sink rows on rank 0, + local and decoded rows on the last)."""
+
+    def __init__(self, engine: Engine, rank: int, ranks: int, batch: int, kv_heads: int,
+                 group_size: int, head_dim: int, l_sink: int, l_cpu_total: int, l_local: int,
+                 max_new: int = 64, dtype: str = "bf16", k: torch.Tensor = None,
+                 v: torch.Tensor = None):
+        self.rank, self.ranks = rank, ranks
+        off, n = shard_bounds(l_cpu_total, ranks)[rank]
+        if n == 0:
+            raise RuntimeError("empty-context: more shards than 128-row cpu chunks")
+        last = rank == ranks - 1
+        self.dec = SparseDecoder(engine, batch, kv_heads, group_size, head_dim,
+                                 l_sink if rank == 0 else 0, n, l_local if last else 0,
+                                 max_new if last else 0, dtype, k, v)
+        self.dec.l_cpu_total = l_cpu_total
+        self.dec.cpu_offset = off
+        self.eng = engine
+        self.offset, self.rows = off, n
+        nh = batch * kv_heads * group_size
+        self.n_heads = nh
+        self.cap = (n + 15) // 16
+        dev = engine.device
+        self.keys = torch.zeros((nh, self.cap), dtype=torch.int64, device=dev)  # u64 keys
+        self.ids = torch.zeros((nh, self.cap), dtype=torch.int32, device=dev)
+        self.count = torch.zeros(nh, dtype=torch.int32, device=dev)
+        self.kth = torch.zeros(nh, dtype=torch.int64, device=dev)
+        self.thresh = torch.zeros(nh, dtype=torch.int64, device=dev)
+        self.keep = torch.zeros(nh, dtype=torch.int32, device=dev)
+        self.sel = torch.zeros((batch, kv_heads * group_size, self.dec.sel_words), dtype=torch.int32,
+                               device=dev)
+        self.o = torch.empty((batch, kv_heads * group_size, head_dim), dtype=torch.float32, device=dev)
+        self.lse = torch.empty((batch, kv_heads * group_size), dtype=torch.float32, device=dev)
+
+    @property
+    def is_last(self) -> bool:
+        return self.rank == self.ranks - 1
+
+    # -- phases ------------------------------------------------------------------
+    def candidates(self, q: torch.Tensor, **plan) -> torch.Tensor:
+        d = self.dec
+        a = d._args(q, plan.get("props"), plan.get("fixed"), plan.get("full", False),
+                    plan.get("blk"), plan.get("budgets"))
+        check(LIB.fx_cp_candidates(self.eng.ctx, C.byref(d.lay), C.byref(a), self.cap,
+                                   self.keys.data_ptr(), self.ids.data_ptr(),
+                                   self.count.data_ptr(), self.kth.data_ptr()))
+        return self.kth
+
+    def threshold(self, kth_all: torch.Tensor) -> int:
+        check(LIB.fx_cp_threshold(self.eng.ctx, self.ranks, self.n_heads, self.cap,
+                                  self.keys.data_ptr(), kth_all.data_ptr(),
+                                  self.thresh.data_ptr(), self.keep.data_ptr()))
+        return int(self.keep.max().item()) if self.n_heads else 0
+
+    def head_candidates(self, m: int) -> Tuple[torch.Tensor, torch.Tensor]:
+        """This shard's first m sorted entries per head (the exchanged slice)."""
+        if m <= self.cap:
+            return self.keys[:, :m], self.ids[:, :m]
+        pad = m - self.cap
+        return (torch.nn.functional.pad(self.keys, (0, pad)),
+                torch.nn.functional.pad(self.ids, (0, pad), value=-1))
+
+    def select(self, gkeys: torch.Tensor, gids: torch.Tensor, m: int) -> None:
+        d = self.dec
+        check(LIB.fx_cp_select(self.eng.ctx, C.byref(d.lay), self.ranks, self.rank, m,
+                               gkeys.data_ptr(), gids.data_ptr(), self.thresh.data_ptr(),
+                               d.plan_kblocks.data_ptr(), d.plan_blk.data_ptr(), self.offset,
+                               self.sel.data_ptr(), d.sel_words))
+
+    def attend(self, q: torch.Tensor):
+        return self.dec.step(q, blk="keep", out=self.o, lse=self.lse, sel_in=self.sel)
+
+    def combine(self, o_all: torch.Tensor, lse_all: torch.Tensor, o: torch.Tensor,
+                lse: torch.Tensor) -> None:
+        D = o.shape[-1]
+        check(LIB.fx_cp_combine(self.eng.ctx, self.ranks, self.n_heads, D, o_all.data_ptr(),
+                                lse_all.data_ptr(), o.data_ptr(), lse.data_ptr()))
+
+    def global_selection(self, b: int, h: int) -> torch.Tensor:
+        """Global ids of the blocks this shard selected for head h of b."""
+        g = h // self.dec.lay.group_size
+        blk = int(self.dec.plan_blk[b, g].item())
+        if blk == 0:
+            return np.zeros(0, np.int64)
+        words = self.sel[b, h].cpu().numpy().view(np.uint32)
+        nblk = (self.rows + blk - 1) // blk
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:nblk]
+        return np.nonzero(bits)[0] + self.offset // blk
+
+
+def cp_decode_step(shards: Sequence, comm, q: torch.Tensor, out: Sequence[Tuple[torch.Tensor, torch.Tensor]] = None,
+                   **plan):
+    """One context-parallel decode step over this process's shards (one per
+    rank under torch.distributed, all of them under LoopbackComm).  Returns the
+    merged (o [B][H][D], lse [B][H]) of each local shard (identical on every
+    rank)."""
+    for s in shards:
+        s.candidates(q, **plan)
+    kth_all = comm.all_gather([s.kth for s in shards])
+    m = comm.max_int([s.threshold(kth_all) for s in shards], q.device)
+    m = max(m, 1)
+    cand = [s.head_candidates(m) for s in shards]
+    gkeys = comm.all_gather([c[0] for c in cand])
+    gids = comm.all_gather([c[1] for c in cand])
+    for s in shards:
+        s.select(gkeys, gids, m)
+    parts = [s.attend(q) for s in shards]
+    o_all = comm.all_gather([p[0] for p in parts])
+    lse_all = comm.all_gather([p[1] for p in parts])
+    res = []
+    for i, s in enumerate(shards):
+        if out is not None:
+            o, lse = out[i]
+        else:
+            o, lse = torch.empty_like(s.o), torch.empty_like(s.lse)
+        s.combine(o_all, lse_all, o, lse)
+        res.append((o, lse))
+    return res

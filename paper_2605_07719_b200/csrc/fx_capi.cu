@@ -246,6 +246,82 @@ int64_t next_pow2(int64_t x) {
 }
 }  // namespace
 
+namespace {
+
+// Validation + plan + score/select shared by fx_decode_step and
+// fx_cp_candidates.  Returns the kernels launched; fills `s.sel_bits` (or
+// points it at the caller's / given selection).
+struct Planned {
+    int32_t* blk;
+    double* budgets;
+    int32_t* kblocks;
+    int launches;
+};
+Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, StepScratch& s,
+                        bool need_meta_for_select) {
+    FX_REQUIRE(a->l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + a->l_new <= L.l_cap,
+               FX_ERR_INVALID, "bad-shape: decoded rows exceed l_cap");
+    FX_REQUIRE(a->plan_mode >= FX_PLAN_PROPS && a->plan_mode <= FX_PLAN_GIVEN, FX_ERR_INVALID,
+               "bad-shape: unknown plan mode");
+    const bool sparse = L.l_cpu > 0;
+    const bool given_sel = a->sel_in != nullptr;
+    const int64_t l_plan = a->l_cpu_total > 0 ? a->l_cpu_total : L.l_cpu;
+    FX_REQUIRE(l_plan >= L.l_cpu && a->cpu_offset >= 0 && a->cpu_offset % 128 == 0 &&
+                   a->cpu_offset + L.l_cpu <= l_plan,
+               FX_ERR_INVALID, "bad-shape: shard [cpu_offset, +l_cpu) outside l_cpu_total or unaligned");
+    if (sparse && (!given_sel || need_meta_for_select)) {
+        for (int i = 0; i < 4; ++i)
+            FX_REQUIRE(a->meta[i] != nullptr, FX_ERR_STATE, "no-context: missing block metadata");
+        FX_REQUIRE(a->absmax != nullptr, FX_ERR_STATE, "no-context: missing absmax");
+    }
+    if (a->plan_mode == FX_PLAN_PROPS)
+        FX_REQUIRE(a->bgt0 && a->kslope && a->streaming, FX_ERR_STATE,
+                   "no-context: plan mode PROPS needs head properties");
+    if (a->plan_mode == FX_PLAN_GIVEN)
+        FX_REQUIRE(a->plan_blk && a->plan_budgets, FX_ERR_STATE,
+                   "no-context: plan mode GIVEN needs blk and budgets");
+    if (given_sel) {
+        FX_REQUIRE(a->plan_mode == FX_PLAN_GIVEN, FX_ERR_INVALID,
+                   "bad-shape: a given selection needs plan mode GIVEN");
+        FX_REQUIRE(a->sel_words >= s.sel_words, FX_ERR_INVALID, "bad-shape: sel_words too small");
+        s.sel_bits = const_cast<uint32_t*>(a->sel_in);
+        s.sel_words = a->sel_words;
+    } else if (a->sel_bits) {
+        FX_REQUIRE(a->sel_words >= s.sel_words, FX_ERR_INVALID, "bad-shape: sel_words too small");
+        s.sel_bits = a->sel_bits;
+        s.sel_words = a->sel_words;
+    }
+    Planned p;
+    p.blk = a->plan_blk ? a->plan_blk : s.blk;
+    p.budgets = a->plan_budgets ? a->plan_budgets : s.budgets;
+    p.kblocks = a->plan_kblocks ? a->plan_kblocks : s.kblocks;
+    cudaStream_t st = ctx->stream;
+    {
+        Timed tm(ctx, FX_KERNEL_PLAN);
+        fx::launch_prepare(L, l_plan, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
+                           a->kslope, a->streaming, p.blk, p.budgets, a->plan_volume,
+                           a->plan_cand_volumes, p.kblocks, s.bg_done, st);
+    }
+    p.launches = 1;
+    if (sparse && !given_sel) {
+        {
+            Timed tm(ctx, FX_KERNEL_SCORE);
+            fx::launch_approx_scores(L, a->meta, a->q, p.blk, p.kblocks, s.approx, s.approx_stride, st);
+        }
+        {
+            Timed tm(ctx, FX_KERNEL_SELECT);
+            fx::launch_select(L, a->meta, a->absmax, a->q, p.blk, p.kblocks, s.approx,
+                              s.approx_stride, s.sel_bits, s.sel_words, s.cand_keys, s.cand_ids, st);
+        }
+        p.launches += 2;
+    } else if (!sparse) {
+        FX_CUDA(cudaMemsetAsync(p.blk, 0, sizeof(int32_t) * L.batch * L.kv_heads, st));
+    }
+    return p;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* fx_last_error(void) { return g_last_error.c_str(); }
@@ -479,7 +555,7 @@ int fx_plan_groups(fx_ctx* ctx, int32_t n_groups, int32_t group_size, int64_t l_
         L.group_size = group_size;
         L.head_dim = 1;
         L.l_cpu = l_cpu;
-        fx::launch_prepare(L, FX_PLAN_PROPS, 0, 0.0, bgt0, kslope, streaming, blk, budgets, volume,
+        fx::launch_prepare(L, l_cpu, FX_PLAN_PROPS, 0, 0.0, bgt0, kslope, streaming, blk, budgets, volume,
                            cand_volumes, kblocks, nullptr, ctx->stream);
         ctx->launches += 1;
     });
@@ -566,55 +642,12 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         FX_REQUIRE(a != nullptr && a->k && a->v && a->q && a->o, FX_ERR_STATE,
                    "no-context: decode step has no executable payload");
         const fx_layout& L = *lay;
-        FX_REQUIRE(a->l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + a->l_new <= L.l_cap,
-                   FX_ERR_INVALID, "bad-shape: decoded rows exceed l_cap");
-        FX_REQUIRE(a->plan_mode >= FX_PLAN_PROPS && a->plan_mode <= FX_PLAN_GIVEN, FX_ERR_INVALID,
-                   "bad-shape: unknown plan mode");
-        const bool sparse = L.l_cpu > 0;
-        if (sparse) {
-            for (int i = 0; i < 4; ++i)
-                FX_REQUIRE(a->meta[i] != nullptr, FX_ERR_STATE, "no-context: missing block metadata");
-            FX_REQUIRE(a->absmax != nullptr, FX_ERR_STATE, "no-context: missing absmax");
-        }
-        if (a->plan_mode == FX_PLAN_PROPS)
-            FX_REQUIRE(a->bgt0 && a->kslope && a->streaming, FX_ERR_STATE,
-                       "no-context: plan mode PROPS needs head properties");
-        if (a->plan_mode == FX_PLAN_GIVEN)
-            FX_REQUIRE(a->plan_blk && a->plan_budgets, FX_ERR_STATE,
-                       "no-context: plan mode GIVEN needs blk and budgets");
         const int grid = fx::attend_grid(L, false, ctx->num_sms);
         StepScratch s = carve_step(ctx, L, grid, true);
-        if (a->sel_bits) {
-            FX_REQUIRE(a->sel_words >= s.sel_words, FX_ERR_INVALID, "bad-shape: sel_words too small");
-            s.sel_bits = a->sel_bits;
-            s.sel_words = a->sel_words;
-        }
-        int32_t* blk = a->plan_blk ? a->plan_blk : s.blk;
-        double* budgets = a->plan_budgets ? a->plan_budgets : s.budgets;
-        int32_t* kblocks = a->plan_kblocks ? a->plan_kblocks : s.kblocks;
+        const Planned pl = plan_and_select(ctx, L, a, s, false);
+        int32_t* blk = pl.blk;
+        int n = pl.launches;
         cudaStream_t st = ctx->stream;
-        {
-            Timed tm(ctx, FX_KERNEL_PLAN);
-            fx::launch_prepare(L, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
-                               a->kslope, a->streaming, blk, budgets, a->plan_volume,
-                               a->plan_cand_volumes, kblocks, s.bg_done, st);
-        }
-        int n = 1;
-        if (sparse) {
-            {
-                Timed tm(ctx, FX_KERNEL_SCORE);
-                fx::launch_approx_scores(L, a->meta, a->q, blk, kblocks, s.approx, s.approx_stride, st);
-            }
-            {
-                Timed tm(ctx, FX_KERNEL_SELECT);
-                fx::launch_select(L, a->meta, a->absmax, a->q, blk, kblocks, s.approx,
-                                  s.approx_stride, s.sel_bits, s.sel_words, s.cand_keys,
-                                  s.cand_ids, st);
-            }
-            n += 2;
-        } else {
-            FX_CUDA(cudaMemsetAsync(blk, 0, sizeof(int32_t) * L.batch * L.kv_heads, st));
-        }
         {
             Timed tm(ctx, FX_KERNEL_WORKLIST);
             fx::launch_worklist(L, a->l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
@@ -715,6 +748,68 @@ int fx_convert(fx_ctx* ctx, const float* src, void* dst, int32_t dtype, size_t n
     return guarded([&] {
         DeviceGuard g(ctx);
         fx::launch_convert(src, dst, dtype, n, ctx->stream);
+        ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+// ---- context-parallel decode (C5) ----------------------------------------
+
+int fx_cp_candidates(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, int64_t cap,
+                     uint64_t* keys, uint32_t* ids, int32_t* count, uint64_t* kth) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const fx_layout& L = *lay;
+        FX_REQUIRE(a != nullptr && a->q && keys && ids && count && kth, FX_ERR_STATE,
+                   "no-context: candidate selection has no payload");
+        FX_REQUIRE(L.l_cpu > 0, FX_ERR_INVALID, "empty-context: shard has no cpu rows");
+        FX_REQUIRE(a->sel_in == nullptr, FX_ERR_INVALID, "bad-shape: candidates select, sel_in must be null");
+        FX_REQUIRE(cap >= fx::level_blocks(L.l_cpu, 16), FX_ERR_INVALID,
+                   "bad-shape: cap must hold every block of the shard at granularity 16");
+        const int grid = fx::attend_grid(L, false, ctx->num_sms);
+        StepScratch s = carve_step(ctx, L, grid, true);
+        const Planned pl = plan_and_select(ctx, L, a, s, true);
+        fx::launch_cp_candidates(L, a->meta, a->q, pl.blk, pl.kblocks, s.sel_bits, s.sel_words,
+                                 a->cpu_offset, cap, keys, ids, count, kth, ctx->stream);
+        ctx->launches += pl.launches + 1;
+    });
+}
+
+int fx_cp_threshold(fx_ctx* ctx, int32_t ranks, int64_t n, int64_t cap, const uint64_t* keys,
+                    const uint64_t* kth_all, uint64_t* thresh, int32_t* keep) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(ranks >= 1 && n >= 0 && cap >= 1, FX_ERR_INVALID, "bad-shape: threshold input");
+        fx::launch_cp_threshold(ranks, n, cap, keys, kth_all, thresh, keep, ctx->stream);
+        ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+int fx_cp_select(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t self, int64_t m,
+                 const uint64_t* gkeys, const uint32_t* gids, const uint64_t* thresh,
+                 const int32_t* kblocks, const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out,
+                 int32_t sel_words) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(ranks >= 1 && self >= 0 && self < ranks && m >= 0, FX_ERR_INVALID,
+                   "bad-shape: rank / candidate count");
+        FX_REQUIRE(cpu_offset >= 0 && cpu_offset % 128 == 0, FX_ERR_INVALID,
+                   "bad-shape: cpu_offset must be a multiple of 128");
+        FX_REQUIRE(sel_words >= fx::cdiv(std::max<int64_t>(1, fx::level_blocks(lay->l_cpu, 16)), 32),
+                   FX_ERR_INVALID, "bad-shape: sel_words too small");
+        fx::launch_cp_select(*lay, ranks, self, m, gkeys, gids, thresh, kblocks, blk, cpu_offset,
+                             sel_out, sel_words, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_cp_combine(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim, const float* o_parts,
+                  const float* lse_parts, float* o, float* lse) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(ranks >= 1 && n >= 0 && dim > 0, FX_ERR_INVALID, "bad-shape: combine input");
+        fx::launch_cp_combine(ranks, n, dim, o_parts, lse_parts, o, lse, ctx->stream);
         ctx->launches += n > 0 ? 1 : 0;
     });
 }

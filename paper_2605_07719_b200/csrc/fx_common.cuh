@@ -56,6 +56,24 @@ __device__ __forceinline__ uint64_t f64_key(double f) {
 // ---------------------------------------------------------------------------
 // warp helpers
 // ---------------------------------------------------------------------------
+// Exact reference score (block_index.cpp:41-53): f64, dimension order, unfused.
+template <typename T>
+__device__ double exact_score(const float* __restrict__ q, const T* __restrict__ mn,
+                              const T* __restrict__ mx, int D) {
+    double s = 0.0;
+    for (int d = 0; d < D; ++d) {
+        const double qd = (double)q[d];
+        const double lo = __dmul_rn(qd, (double)tofl(mn[d]));
+        const double hi = __dmul_rn(qd, (double)tofl(mx[d]));
+        s = __dadd_rn(s, (lo < hi) ? hi : lo);
+    }
+    return s;
+}
+
+// (key desc, id asc) "less" = comes first
+__device__ __forceinline__ bool first_of(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+    return ka != kb ? ka > kb : ia < ib;
+}
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -1,0 +1,270 @@
+// fx_cp.cu -- context-parallel decode (config C5): the global budgeted top-k
+// of topk_blocks (block_index.cpp:55-83) and the LSE merge of merge_into
+// (attention.cpp:89-104), split over cpu-segment shards.
+//
+// Why the two exchanges reproduce the single-device selection bit-exactly:
+// a block in the global top-k of a head is beaten by fewer than k blocks
+// overall, hence by fewer than k blocks of its own shard, so it is in that
+// shard's local top-k (candidates).  If shard r holds >= k blocks, its k-th
+// local score t_r is <= the global k-th score, so T = max_r t_r is a lower
+// bound: only entries with score >= T can be selected, and the shard that
+// attains T contributes k of them.  The global rank of an entry under the
+// reference's strict total order (score desc, id asc) is the sum over shards
+// of the entries that precede it -- one binary search per shard list, since
+// every list is sorted by that same order.
+#include <algorithm>
+
+#include "fx_common.cuh"
+
+namespace fx {
+namespace {
+
+constexpr int kT = 256;
+
+struct MetaLevels {
+    const void* p[4];  // blk 16 / 32 / 64 / 128
+};
+
+// Local candidates of one head: the ids of the shard's selected blocks, exact
+// reference scores as keys, bitonic-sorted in smem by (key desc, id asc).
+template <int DT>
+__global__ void __launch_bounds__(kT) k_cp_candidates(
+    const MetaLevels meta_levels, const float* __restrict__ q,
+    const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks,
+    const uint32_t* __restrict__ sel_bits, int sel_words, int Hkv, int G, int D, int64_t l_cpu,
+    int64_t cpu_offset, int64_t cap, int sort_n, uint64_t* __restrict__ keys_out,
+    uint32_t* __restrict__ ids_out, int32_t* __restrict__ count_out, uint64_t* __restrict__ kth_out) {
+    using T = typename Elem<DT>::T;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(dsm);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + sort_n);
+    __shared__ int s_wpos[kT + 1];
+    const int64_t head = blockIdx.x;
+    const int64_t H = (int64_t)Hkv * G;
+    const int b = (int)(head / H), h = (int)(head % H);
+    const int bg = b * Hkv + h / G;
+    const int t = threadIdx.x;
+    const int blk = blk_arr[bg];
+    const int64_t k = kblocks[head];
+    const int64_t nblk = blk > 0 ? cdiv_dev(l_cpu, blk) : 0;
+    const int W = (int)cdiv_dev(nblk, 32);
+    const uint32_t* bits = sel_bits + head * sel_words;
+    // 1. compact the selected ids (thread-contiguous word ranges, block scan)
+    const int per = (W + kT - 1) / kT;
+    const int w0 = min(W, t * per), w1 = min(W, w0 + per);
+    int c = 0;
+    for (int w = w0; w < w1; ++w) c += __popc(bits[w]);
+    s_wpos[t + 1] = c;
+    __syncthreads();
+    if (t == 0) {
+        s_wpos[0] = 0;
+        for (int i = 1; i <= kT; ++i) s_wpos[i] += s_wpos[i - 1];
+    }
+    __syncthreads();
+    const int n = s_wpos[kT];  // = min(k, nblk) by the selection
+    int pos = s_wpos[t];
+    for (int w = w0; w < w1; ++w) {
+        uint32_t u = bits[w];
+        while (u) {
+            const int l = __ffs(u) - 1;
+            u &= u - 1;
+            si[pos++] = (uint32_t)(w * 32 + l);
+        }
+    }
+    __syncthreads();
+    // 2. exact scores (block_index.cpp:41-53) -> keys; pad to sort_n
+    const T* mbase = blk > 0 ? static_cast<const T*>(meta_levels.p[blk == 16 ? 0 : blk == 32 ? 1 : blk == 64 ? 2 : 3]) +
+                                   (int64_t)bg * nblk * 2 * D
+                             : nullptr;
+    const float* qh = q + head * D;
+    const int64_t off_blk = blk > 0 ? cpu_offset / blk : 0;
+    for (int i = t; i < sort_n; i += kT) {
+        if (i < n) {
+            const uint32_t id = si[i];
+            sk[i] = f64_key(exact_score(qh, mbase + (int64_t)id * 2 * D, mbase + (int64_t)id * 2 * D + D, D));
+            si[i] = (uint32_t)(id + off_blk);  // global block id
+        } else {
+            sk[i] = 0;
+            si[i] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    // 3. bitonic sort, (key desc, id asc) first
+    for (int kk = 2; kk <= sort_n; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = t; i < sort_n; i += kT) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const bool up = (i & kk) == 0;
+                    const uint64_t a = sk[i], e = sk[p];
+                    const uint32_t ia = si[i], ie = si[p];
+                    if (up ? first_of(e, ie, a, ia) : first_of(a, ia, e, ie)) {
+                        sk[i] = e;
+                        sk[p] = a;
+                        si[i] = ie;
+                        si[p] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // 4. emit
+    for (int64_t i = t; i < cap; i += kT) {
+        keys_out[head * cap + i] = i < n ? sk[i] : 0ull;
+        ids_out[head * cap + i] = i < n ? si[i] : 0xffffffffu;
+    }
+    if (t == 0) {
+        count_out[head] = n;
+        kth_out[head] = (k > 0 && n >= k) ? sk[k - 1] : 0ull;
+    }
+}
+
+__global__ void k_cp_threshold(int R, int64_t n, int64_t cap, const uint64_t* __restrict__ keys,
+                               const uint64_t* __restrict__ kth_all, uint64_t* __restrict__ thresh,
+                               int32_t* __restrict__ keep) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t T = 0;
+    for (int r = 0; r < R; ++r) {
+        const uint64_t v = kth_all[(int64_t)r * n + i];
+        T = v > T ? v : T;
+    }
+    // sorted descending, zero-filled: entries with key >= max(T, 1)
+    const uint64_t lim = T > 0 ? T : 1ull;
+    const uint64_t* kh = keys + i * cap;
+    int64_t lo = 0, hi = cap;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (kh[mid] >= lim) lo = mid + 1;
+        else hi = mid;
+    }
+    thresh[i] = T;
+    keep[i] = (int32_t)lo;
+}
+
+// Global rank of each own entry; bits for rank < k.
+__global__ void __launch_bounds__(kT) k_cp_select(
+    int R, int self, int64_t n, int64_t m, const uint64_t* __restrict__ gkeys,
+    const uint32_t* __restrict__ gids, const uint64_t* __restrict__ thresh,
+    const int32_t* __restrict__ kblocks, const int32_t* __restrict__ blk_arr, int G,
+    int64_t cpu_offset, uint32_t* __restrict__ sel_out, int sel_words) {
+    const int64_t head = blockIdx.x;
+    const int t = threadIdx.x;
+    uint32_t* bits = sel_out + head * sel_words;
+    for (int w = t; w < sel_words; w += kT) bits[w] = 0u;
+    __syncthreads();
+    const int blk = blk_arr[head / G];
+    const int64_t k = kblocks[head];
+    if (blk <= 0 || k <= 0) return;
+    const uint64_t lim = thresh[head] > 0 ? thresh[head] : (uint64_t)1;
+    const int64_t off_blk = cpu_offset / blk;
+    const uint64_t* own_k = gkeys + ((int64_t)self * n + head) * m;
+    const uint32_t* own_i = gids + ((int64_t)self * n + head) * m;
+    for (int64_t j = t; j < m; j += kT) {
+        const uint64_t ke = own_k[j];
+        if (ke < lim) continue;  // below the bound (or an empty slot)
+        const uint32_t ie = own_i[j];
+        int64_t rank = j;         // own entries before j precede it
+        for (int r = 0; r < R && rank < k; ++r) {
+            if (r == self) continue;
+            const uint64_t* kr = gkeys + ((int64_t)r * n + head) * m;
+            const uint32_t* ir = gids + ((int64_t)r * n + head) * m;
+            int64_t lo = 0, hi = m;  // entries of list r that come first
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (kr[mid] >= lim && first_of(kr[mid], ir[mid], ke, ie)) lo = mid + 1;
+                else hi = mid;
+            }
+            rank += lo;
+        }
+        if (rank < k) {
+            const int64_t local = (int64_t)ie - off_blk;
+            atomicOr(&bits[local >> 5], 1u << (local & 31));
+        }
+    }
+}
+
+__global__ void k_cp_combine(int R, int64_t n, int D, const float* __restrict__ op,
+                             const float* __restrict__ lp, float* __restrict__ o,
+                             float* __restrict__ lse) {
+    const int64_t i = blockIdx.x;
+    float M = -INFINITY;
+    for (int r = 0; r < R; ++r) M = fmaxf(M, lp[(int64_t)r * n + i]);
+    float den = 0.f;
+    for (int r = 0; r < R; ++r) {
+        const float l = lp[(int64_t)r * n + i];
+        den += (l == -INFINITY) ? 0.f : expf(l - M);
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        float num = 0.f;
+        for (int r = 0; r < R; ++r) {
+            const float l = lp[(int64_t)r * n + i];
+            if (l != -INFINITY) num += expf(l - M) * op[((int64_t)r * n + i) * D + d];
+        }
+        o[i * D + d] = den > 0.f ? num / den : 0.f;
+    }
+    if (threadIdx.x == 0 && lse) lse[i] = den > 0.f ? M + logf(den) : -INFINITY;
+}
+
+}  // namespace
+
+int cp_sort_n(int64_t nblk16) {
+    int64_t s = 1;
+    while (s < nblk16) s <<= 1;
+    return (int)std::max<int64_t>(s, 32);
+}
+
+void launch_cp_candidates(const fx_layout& L, const void* const meta[4], const float* q,
+                          const int32_t* blk, const int32_t* kblocks, const uint32_t* sel_bits,
+                          int sel_words, int64_t cpu_offset, int64_t cap, uint64_t* keys,
+                          uint32_t* ids, int32_t* count, uint64_t* kth, cudaStream_t s) {
+    const int64_t heads = (int64_t)L.batch * L.kv_heads * L.group_size;
+    const int sort_n = cp_sort_n(std::max<int64_t>(1, level_blocks(L.l_cpu, 16)));
+    const size_t smem = (size_t)sort_n * 12;
+    FX_REQUIRE(smem <= 200 * 1024, FX_ERR_INVALID,
+               "bad-shape: context-parallel shard too long (more than 16384 blocks of 16)");
+    const MetaLevels ml{{meta[0], meta[1], meta[2], meta[3]}};
+    if (L.dtype == FX_BF16) {
+        auto kern = k_cp_candidates<FX_BF16>;
+        FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)heads, kT, smem, s>>>(
+            ml, q, blk, kblocks, sel_bits,
+            sel_words, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, cpu_offset, cap, sort_n,
+            keys, ids, count, kth);
+    } else {
+        auto kern = k_cp_candidates<FX_F32>;
+        FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)heads, kT, smem, s>>>(
+            ml, q, blk, kblocks, sel_bits, sel_words,
+            L.kv_heads, L.group_size, L.head_dim, L.l_cpu, cpu_offset, cap, sort_n, keys, ids,
+            count, kth);
+    }
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_cp_threshold(int R, int64_t n, int64_t cap, const uint64_t* keys,
+                         const uint64_t* kth_all, uint64_t* thresh, int32_t* keep, cudaStream_t s) {
+    if (n <= 0) return;
+    k_cp_threshold<<<(unsigned)cdiv(n, 128), 128, 0, s>>>(R, n, cap, keys, kth_all, thresh, keep);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_cp_select(const fx_layout& L, int R, int self, int64_t m, const uint64_t* gkeys,
+                      const uint32_t* gids, const uint64_t* thresh, const int32_t* kblocks,
+                      const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out, int sel_words,
+                      cudaStream_t s) {
+    const int64_t n = (int64_t)L.batch * L.kv_heads * L.group_size;
+    if (n <= 0) return;
+    k_cp_select<<<(unsigned)n, kT, 0, s>>>(R, self, n, m, gkeys, gids, thresh, kblocks, blk,
+                                           L.group_size, cpu_offset, sel_out, sel_words);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_cp_combine(int R, int64_t n, int dim, const float* o_parts, const float* lse_parts,
+                       float* o, float* lse, cudaStream_t s) {
+    if (n <= 0) return;
+    k_cp_combine<<<(unsigned)n, 128, 0, s>>>(R, n, dim, o_parts, lse_parts, o, lse);
+    FX_CUDA(cudaGetLastError());
+}
+
+}  // namespace fx

@@ -67,7 +67,7 @@ void launch_meta_generic(const void* k, int dtype, int64_t rows, int dim, int bl
                          cudaStream_t s);
 
 // fx_plan.cu
-void launch_prepare(const fx_layout& L, int plan_mode, int fixed_blk, double fixed_budget,
+void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed_blk, double fixed_budget,
                     const double* bgt0, const double* kslope, const int32_t* streaming,
                     int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
                     int32_t* bg_done, cudaStream_t s);
@@ -128,5 +128,19 @@ void launch_merge_partials(int n, int dim, const float* o_parts, const float* ls
 void launch_append(const fx_layout& L, void* k, void* v, int64_t row, const float* kn,
                    const float* vn, cudaStream_t s);
 void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream_t s);
+
+// fx_cp.cu (context-parallel shards, config C5)
+void launch_cp_candidates(const fx_layout& L, const void* const meta[4], const float* q,
+                          const int32_t* blk, const int32_t* kblocks, const uint32_t* sel_bits,
+                          int sel_words, int64_t cpu_offset, int64_t cap, uint64_t* keys,
+                          uint32_t* ids, int32_t* count, uint64_t* kth, cudaStream_t s);
+void launch_cp_threshold(int R, int64_t n, int64_t cap, const uint64_t* keys,
+                         const uint64_t* kth_all, uint64_t* thresh, int32_t* keep, cudaStream_t s);
+void launch_cp_select(const fx_layout& L, int R, int self, int64_t m, const uint64_t* gkeys,
+                      const uint32_t* gids, const uint64_t* thresh, const int32_t* kblocks,
+                      const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out, int sel_words,
+                      cudaStream_t s);
+void launch_cp_combine(int R, int64_t n, int dim, const float* o_parts, const float* lse_parts,
+                       float* o, float* lse, cudaStream_t s);
 
 }  // namespace fx

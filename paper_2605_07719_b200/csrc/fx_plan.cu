@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
 
 }  // namespace
 
-void launch_prepare(const fx_layout& L, int plan_mode, int fixed_blk, double fixed_budget,
+void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed_blk, double fixed_budget,
                     const double* bgt0, const double* kslope, const int32_t* streaming,
                     int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
                     int32_t* bg_done, cudaStream_t s) {
@@ -172,7 +172,7 @@ void launch_prepare(const fx_layout& L, int plan_mode, int fixed_blk, double fix
         for (int c = 0; c < 4; ++c) ok |= kLevels[c] == fixed_blk;
         FX_REQUIRE(ok, FX_ERR_INVALID, "invalid-granularity: blk must be one of 16/32/64/128");
     }
-    k_prepare<<<n_bg, 32, 0, s>>>(n_bg, L.group_size, L.l_cpu, plan_mode, fixed_blk, fixed_budget,
+    k_prepare<<<n_bg, 32, 0, s>>>(n_bg, L.group_size, l_plan, plan_mode, fixed_blk, fixed_budget,
                                   bgt0, kslope, streaming, blk, budgets, volume, cand, kblocks,
                                   bg_done);
     FX_CUDA(cudaGetLastError());

@@ -10,20 +10,6 @@ namespace {
 
 constexpr int kMaxWords = 4096;      // nblk <= 131072 per (b, g) at the chosen blk
 
-// Exact reference score (block_index.cpp:41-53): f64, dimension order, unfused.
-template <typename T>
-__device__ double exact_score(const float* __restrict__ q, const T* __restrict__ mn,
-                              const T* __restrict__ mx, int D) {
-    double s = 0.0;
-    for (int d = 0; d < D; ++d) {
-        const double qd = (double)q[d];
-        const double lo = __dmul_rn(qd, (double)tofl(mn[d]));
-        const double hi = __dmul_rn(qd, (double)tofl(mx[d]));
-        s = __dadd_rn(s, (lo < hi) ? hi : lo);
-    }
-    return s;
-}
-
 // Exclusive block scan of cnt[0..n) in place; returns the total.
 __device__ int64_t block_exclusive_scan(int32_t* cnt, int n, int64_t* wsum) {
     const int t = threadIdx.x, nt = blockDim.x;
@@ -214,10 +200,6 @@ __global__ void k_meta_absmax(const typename Elem<DT>::T* __restrict__ meta, int
     absmax[d] = a;
 }
 
-// (key desc, id asc) "less" = comes first
-__device__ __forceinline__ bool first_of(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
-    return ka != kb ? ka > kb : ia < ib;
-}
 __global__ void k_bitonic(uint64_t* keys, uint32_t* ids, int64_t n, int64_t j, int64_t kk) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t p = i ^ j;

@@ -29,6 +29,19 @@ constexpr int kMaxWords = 4096;   // nblk <= 131072 at the chosen granularity
 constexpr int kSmemKeys = 16384;  // approximate scores staged in smem up to this many
 constexpr int kSmallCand = 512;   // band ranked in smem by counting up to this size
 
+#ifdef FX_TRACE  // profiling build only: per-head phase times and band sizes
+__device__ long long g_sel_trace[8 * 8192];
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SEL_MARK(i) \
+    if (threadIdx.x == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + (i)] = gtimer();
+#else
+#define SEL_MARK(i)
+#endif
+
 struct MetaPtrs {
     const void* p[4];
 };
@@ -110,6 +123,7 @@ __global__ void __launch_bounds__(kT) k_select(
         }
         return;
     }
+    SEL_MARK(0);
     const T* mbase = static_cast<const T*>(level_ptr(meta.p, blk)) + (int64_t)bg * nblk * 2 * D;
     const float* qh = q + head * D;
     const float* sc = approx + head * astride;
@@ -161,6 +175,7 @@ __global__ void __launch_bounds__(kT) k_select(
     const bool sane = __syncthreads_and(fin_all) && isfinite(s_eps);
     const float* src = staged ? s_keys : sc;
     const double eps = s_eps;
+    SEL_MARK(1);
 
     // ---- 1. bracket A_k ----
     double e_lo = -INFINITY, e_hi = INFINITY;  // non-finite prefilter: band = everything
@@ -200,6 +215,7 @@ __global__ void __launch_bounds__(kT) k_select(
         e_hi = (double)gmn + (s_bin[0] + 2) * w;
     }
     const double hi = e_hi + 2.0 * eps, lo = e_lo - 2.0 * eps;
+    SEL_MARK(2);
 
     // ---- 2. classify: definite-in bits, band appended (warp-aggregated) ----
     uint32_t* cids = cand_ids + head * cand_stride;
@@ -229,6 +245,11 @@ __global__ void __launch_bounds__(kT) k_select(
     const int64_t n_def = (int64_t)s_ndef, n_cand = (int64_t)s_ncand;
     const int64_t need = k - n_def;
     const bool small = n_cand <= kSmallCand;
+    SEL_MARK(3);
+#ifdef FX_TRACE
+    if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + 6] = n_cand | (n_def << 32);
+    if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + 7] = k | ((int64_t)nblk << 32);
+#endif
 
     // ---- 3. exact scores of the band, rank, set bits ----
     for (int64_t c = warp; c < n_cand; c += kNW) {
@@ -241,6 +262,7 @@ __global__ void __launch_bounds__(kT) k_select(
         }
     }
     __syncthreads();
+    SEL_MARK(4);
     if (small) {
         for (int64_t c = t; c < n_cand; c += kT) {
             const uint64_t kc = ck[c];
@@ -280,6 +302,8 @@ __global__ void __launch_bounds__(kT) k_select(
             first = false;
         }
     }
+    __syncthreads();
+    SEL_MARK(5);
 }
 
 }  // namespace
@@ -313,5 +337,11 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
     }
     FX_CUDA(cudaGetLastError());
 }
+
+#ifdef FX_TRACE
+extern "C" FX_API int fx_debug_sel_trace(long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * n) == cudaSuccess ? 0 : -2;
+}
+#endif
 
 }  // namespace fx

@@ -437,6 +437,10 @@ class SparseDecoder:
         self.o = torch.empty((batch, H, head_dim), dtype=torch.float32, device=dev)
         self.lse = torch.empty((batch, H), dtype=torch.float32, device=dev)
         self.args = N.StepArgs()
+        # context-parallel shard (context_parallel.py): whole-sequence cpu
+        # length for the plan and this shard's first global cpu row
+        self.l_cpu_total = 0
+        self.cpu_offset = 0
 
     @staticmethod
     def cap_rows(context: int, max_new: int) -> int:
@@ -467,7 +471,7 @@ class SparseDecoder:
 
     # -- one decode step ------------------------------------------------------
     def step(self, q, props=None, fixed=None, full=False, blk=None, budgets=None,
-             out: torch.Tensor = None, lse: torch.Tensor = None):
+             out: torch.Tensor = None, lse: torch.Tensor = None, sel_in: torch.Tensor = None):
         """Plan -> select -> attend+merge for every head of the batch.
 
         q: [B][H][D] f32 (device tensor or host array).  Budget source, one of:
@@ -475,11 +479,19 @@ class SparseDecoder:
           fixed = (blk, bgt)                                      (pipeline.cpp:304-311)
           full  = True                                            (pipeline.cpp:298-303)
           blk = [B][Hkv], budgets = [B][H]                        (given plan)
+          blk = "keep"                        (given plan = the last step's plan)
+        sel_in: a given selection [B][H][sel_words] (skips score/select;
+        needs a given plan) -- the context-parallel attend phase.
         Returns (o [B][H][D] f32, lse [B][H]) as device tensors when q is a
         device tensor, else numpy arrays.
         """
         host = not isinstance(q, torch.Tensor)
         qd = torch.as_tensor(np.ascontiguousarray(q, np.float32)).to(self.eng.device) if host else q
+        a = self._args(qd, props, fixed, full, blk, budgets)
+        a.sel_in = None if sel_in is None else sel_in.data_ptr()
+        return self._finish(a, host, out, lse)
+
+    def _args(self, qd, props, fixed, full, blk, budgets) -> N.StepArgs:
         a = self.args
         a.k, a.v = self.k.data_ptr(), self.v.data_ptr()
         for i, m in enumerate(self.meta):
@@ -487,6 +499,9 @@ class SparseDecoder:
         a.absmax = self.absmax.data_ptr()
         a.l_new = self.l_new
         a.q = qd.data_ptr()
+        a.l_cpu_total = self.l_cpu_total
+        a.cpu_offset = self.cpu_offset
+        a.sel_in = None
         a.bgt0 = a.kslope = a.streaming = None
         if props is not None:
             a.plan_mode = N.FX_PLAN_PROPS
@@ -497,6 +512,8 @@ class SparseDecoder:
             a.fixed_block_size, a.fixed_budget = int(fixed[0]), float(fixed[1])
         elif full:
             a.plan_mode = N.FX_PLAN_FULL
+        elif isinstance(blk, str) and blk == "keep":
+            a.plan_mode = N.FX_PLAN_GIVEN
         else:
             a.plan_mode = N.FX_PLAN_GIVEN
             self.plan_blk.copy_(torch.as_tensor(np.asarray(blk, np.int32)))
@@ -516,6 +533,9 @@ class SparseDecoder:
         a.plan_kblocks = self.plan_kblocks.data_ptr()
         a.sel_bits = self.sel_bits.data_ptr()
         a.sel_words = self.sel_words
+        return a
+
+    def _finish(self, a, host, out, lse):
         o = self.o if out is None else out
         ls = self.lse if lse is None else lse
         a.o = o.data_ptr()

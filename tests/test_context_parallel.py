@@ -1,0 +1,131 @@
+"""Context-parallel decode (config C5): R cpu-segment shards with
+the candidate / threshold exchanges must reproduce the single-device
+selection bit-exactly and its output within the f32 merge tolerance.  All
+shards run on one GPU through LoopbackComm (the same phase code as the
+torch.distributed path; tests/test_context_parallel_gloo.py covers that
+path's exchanges on CPU)."""
+import numpy as np
+import pytest
+import torch
+
+
+
+def head_props(B, H, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(0.01, 0.08, (B, H)), rng.uniform(0.0, 0.01, (B, H)),
+            (rng.random((B, H)) < 0.4).astype(np.int32))
+
+
+def _full_and_shards(engine, R, B, Hkv, G, D, l_sink, l_cpu, l_local, dtype, seed, n_new=0):
+    from paper_2605_07719_b200.context_parallel import CPShard, shard_kv
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    torch.manual_seed(seed)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    dev = engine.device
+    max_new = max(4, n_new)
+    cap = SparseDecoder.cap_rows(l_sink + l_cpu + l_local, max_new)
+    k = torch.randn((B, Hkv, cap, D), device=dev).to(tdt)
+    v = torch.randn((B, Hkv, cap, D), device=dev).to(tdt)
+    # planted needles so the selections matter
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    for b in range(B):
+        for h in range(Hkv):
+            for _ in range(4):
+                s = l_sink + int(torch.randint(0, l_cpu - 16, (1,), generator=g))
+                k[b, h, s:s + 16] += (2.0 * torch.randn(D, generator=g)).to(dev, tdt)
+    full = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new, dtype, k=k, v=v)
+    full.build_metadata()
+    shards = []
+    for r in range(R):
+        kr = shard_kv(k, l_sink, l_cpu, l_local, r, R, max_new)
+        vr = shard_kv(v, l_sink, l_cpu, l_local, r, R, max_new)
+        sh = CPShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new, dtype, k=kr, v=vr)
+        sh.dec.build_metadata()
+        shards.append(sh)
+    if n_new:
+        for _ in range(n_new):
+            kn = torch.randn((B, Hkv, D), device=dev)
+            vn = torch.randn((B, Hkv, D), device=dev)
+            full.append(kn, vn)
+            shards[-1].dec.append(kn, vn)
+    q = torch.randn((B, Hkv * G, D), device=dev)
+    q = q / q.norm(dim=-1, keepdim=True) * D ** 0.5
+    return full, shards, q
+
+
+BF16_TOL = 4e-3  # well inside the north-star 2e-2 bf16 bound
+PLANS = [("fixed16", dict(fixed=(16, 0.05))), ("fixed128", dict(fixed=(128, 0.3))),
+         ("full", dict(full=True)), ("props", "props")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("name,plan", PLANS)
+def test_cp_matches_single_device(engine, R, name, plan):
+    from paper_2605_07719_b200.context_parallel import LoopbackComm, cp_decode_step
+    B, Hkv, G, D = 2, 2, 4, 128
+    l_sink, l_cpu, l_local = 64, 5000 + 37, 256
+    full, shards, q = _full_and_shards(engine, R, B, Hkv, G, D, l_sink, l_cpu, l_local, "bf16",
+                                       seed=R * 7 + len(name))
+    if plan == "props":
+        bgt0, ks, st = head_props(B, Hkv * G, seed=R)
+        plan = dict(props=tuple(torch.as_tensor(x, device=engine.device) for x in (bgt0, ks, st)))
+    o_ref, lse_ref = full.step(q, **plan)
+    (o, lse), *_ = cp_decode_step(shards, LoopbackComm(R), q, **plan)
+    torch.cuda.synchronize()
+    # plans agree (whole-sequence L_cpu on every shard)
+    for sh in shards:
+        assert torch.equal(sh.dec.plan_blk, full.plan_blk)
+        assert torch.equal(sh.dec.plan_kblocks, full.plan_kblocks)
+    # selections: the union of the shards' global ids == the single-device top-k
+    for b in range(B):
+        for h in range(Hkv * G):
+            want = full.selected_blocks(b, h)
+            got = np.sort(np.concatenate([sh.global_selection(b, h) for sh in shards]))
+            assert np.array_equal(got, want), (b, h, len(got), len(want))
+    # the bf16 attention kernel rounds P to bf16 relative to the running max,
+    # which depends on where a run is split: ~2^-9 relative per weight
+    torch.testing.assert_close(o, o_ref, rtol=BF16_TOL, atol=BF16_TOL)
+    torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_cp_decoded_rows_on_last_shard(engine):
+    from paper_2605_07719_b200.context_parallel import LoopbackComm, cp_decode_step
+    B, Hkv, G, D, R = 1, 2, 4, 128, 3
+    full, shards, q = _full_and_shards(engine, R, B, Hkv, G, D, 64, 3000, 256, "bf16", seed=5, n_new=3)
+    o_ref, lse_ref = full.step(q, fixed=(32, 0.1))
+    (o, lse), *_ = cp_decode_step(shards, LoopbackComm(R), q, fixed=(32, 0.1))
+    torch.testing.assert_close(o, o_ref, rtol=BF16_TOL, atol=BF16_TOL)
+    torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_cp_ties_bitexact(engine):
+    """Duplicated blocks across shards: equal scores resolve to the lower id,
+    exactly as topk_blocks does on one device."""
+    from paper_2605_07719_b200.context_parallel import LoopbackComm, cp_decode_step
+    from paper_2605_07719_b200.context_parallel import CPShard, shard_kv
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    B, Hkv, G, D, R = 1, 1, 4, 64, 4
+    l_sink, l_cpu, l_local = 64, 4096, 256
+    dev = engine.device
+    cap = SparseDecoder.cap_rows(l_sink + l_cpu + l_local, 4)
+    base = torch.randn((1, 1, 128, D), device=dev).to(torch.bfloat16)
+    k = base.repeat(1, 1, cap // 128 + 1, 1)[:, :, :cap].contiguous()
+    v = torch.randn((B, Hkv, cap, D), device=dev).to(torch.bfloat16)
+    full = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16", k=k, v=v)
+    full.build_metadata()
+    shards = []
+    for r in range(R):
+        sh = CPShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16",
+                     k=shard_kv(k, l_sink, l_cpu, l_local, r, R, 4), v=shard_kv(v, l_sink, l_cpu, l_local, r, R, 4))
+        sh.dec.build_metadata()
+        shards.append(sh)
+    q = torch.randn((B, Hkv * G, D), device=dev)
+    full.step(q, fixed=(64, 0.2))
+    cp_decode_step(shards, LoopbackComm(R), q, fixed=(64, 0.2))
+    for h in range(G):
+        want = full.selected_blocks(0, h)
+        got = np.sort(np.concatenate([sh.global_selection(0, h) for sh in shards]))
+        assert np.array_equal(got, want)
