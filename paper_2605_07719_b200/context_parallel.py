@@ -82,10 +82,10 @@ class TorchComm:
 
     def all_gather(self, local: Sequence[torch.Tensor]) -> torch.Tensor:
         (t,) = local
-        t = t.contiguous()
-        out = torch.empty((self.ranks,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        t = t.contiguous().reshape(1, -1)
+        out = torch.empty((self.ranks, t.shape[1]), dtype=t.dtype, device=t.device)
         self.dist.all_gather_into_tensor(out, t, group=self.group)
-        return out
+        return out.view((self.ranks,) + tuple(local[0].shape))
 
     def max_int(self, local: Sequence[int], device) -> int:
         (v,) = local
