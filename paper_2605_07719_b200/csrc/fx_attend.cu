@@ -333,6 +333,8 @@ struct TmaCfg {
 template <int D>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_constant__ KvMaps maps,
                                                        const View p) {
+    pdl_wait();
+    pdl_trigger();
     using C = TmaCfg<D>;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -730,6 +732,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
 // ---------------------------------------------------------------------------
 template <int DT>
 __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
+    pdl_wait();
+    pdl_trigger();
     using T = typename Elem<DT>::T;
     extern __shared__ float gsm[];
     const int t = threadIdx.x, G = p.G, D = p.D;
@@ -1006,7 +1010,7 @@ void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
     maps.box[1] = make_kv_map(a.v, D, rows, kBoxRows);
     const size_t smem = TmaCfg<D>::TOTAL;
     FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_attend_tma<D><<<grid, kTmaThreads, smem, s>>>(maps, v);
+    launch_pdl(k_attend_tma<D>, grid, kTmaThreads, smem, s, maps, v);
 }
 
 }  // namespace
@@ -1035,10 +1039,10 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
                                              (size_t)G * D + (size_t)kBoxRows * G + 3 * G);
         if (a.L.dtype == FX_BF16) {
             FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_attend_generic<FX_BF16><<<grid, kGen, smem, s>>>(v);
+            launch_pdl(k_attend_generic<FX_BF16>, grid, kGen, smem, s, v);
         } else {
             FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_attend_generic<FX_F32><<<grid, kGen, smem, s>>>(v);
+            launch_pdl(k_attend_generic<FX_F32>, grid, kGen, smem, s, v);
         }
     }
     FX_CUDA(cudaGetLastError());

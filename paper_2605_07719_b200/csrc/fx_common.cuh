@@ -127,6 +127,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
     return ok != 0;
 }
+// Programmatic dependent launch: the step's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs can
+// be resident while its predecessor drains; pdl_wait() (first thing, before
+// any read of the predecessor's output) blocks until the predecessor grid
+// completed and flushed, pdl_trigger() lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // Non-blocking probe (never suspends the warp in the barrier unit).
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
     uint32_t ok;

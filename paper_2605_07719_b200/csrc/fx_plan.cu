@@ -39,6 +39,8 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
                           int32_t* __restrict__ blk_out, double* __restrict__ budgets,
                           double* __restrict__ volume, double* __restrict__ cand,
                           int32_t* __restrict__ kblocks, int32_t* __restrict__ bg_done) {
+    pdl_wait();
+    pdl_trigger();
     const int bg = blockIdx.x;
     const int h = threadIdx.x;
     const bool act = h < G;
@@ -172,7 +174,7 @@ void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed
         for (int c = 0; c < 4; ++c) ok |= kLevels[c] == fixed_blk;
         FX_REQUIRE(ok, FX_ERR_INVALID, "invalid-granularity: blk must be one of 16/32/64/128");
     }
-    k_prepare<<<n_bg, 32, 0, s>>>(n_bg, L.group_size, l_plan, plan_mode, fixed_blk, fixed_budget,
+    launch_pdl(k_prepare, n_bg, 32, 0, s, n_bg, L.group_size, l_plan, plan_mode, fixed_blk, fixed_budget,
                                   bgt0, kslope, streaming, blk, budgets, volume, cand, kblocks,
                                   bg_done);
     FX_CUDA(cudaGetLastError());

@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(128) k_approx_scores_mma(MetaPtrs meta,
                                                            int Hkv, int G, int64_t l_cpu,
                                                            float* __restrict__ approx,
                                                            int64_t stride) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int KW = 2 * D;   // min row | max row
     constexpr int NP = KW / 32;  // k-step pairs
     TileCtx c;
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const 
                                                            int Hkv, int64_t l_cpu,
                                                            float* __restrict__ approx,
                                                            int64_t stride) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int LPR = D / 4;  // lanes per block row pair (4 dims per lane)
     static_assert(LPR <= 32 && 32 % LPR == 0, "head_dim");
     constexpr int RPW = 32 / LPR;
@@ -237,7 +241,7 @@ void launch_f32(const fx_layout& L, MetaPtrs mp, const float* q, const int32_t* 
                 cudaStream_t s) {
 #define FX_G(GG)                                                                                \
     case GG:                                                                                    \
-        k_approx_scores_f32<D, GG><<<grid, 256, 0, s>>>(mp, q, blk, kblocks, L.kv_heads,       \
+        launch_pdl(k_approx_scores_f32<D, GG>, grid, 256, 0, s, mp, q, blk, kblocks, L.kv_heads,       \
                                                         L.l_cpu, approx, stride);               \
         break;
     switch (L.group_size) {
@@ -262,10 +266,10 @@ void launch_approx_scores(const fx_layout& L, const void* const meta[4], const f
     const dim3 grid((unsigned)cdiv(level_blocks(L.l_cpu, 16), kTileBlocks),
                     (unsigned)(L.batch * L.kv_heads));
     if (L.dtype == FX_BF16 && D == 128)
-        k_approx_scores_mma<128><<<grid, 128, 0, s>>>(mp, q, blk, kblocks, L.kv_heads, L.group_size,
+        launch_pdl(k_approx_scores_mma<128>, grid, 128, 0, s, mp, q, blk, kblocks, L.kv_heads, L.group_size,
                                                       L.l_cpu, approx, approx_stride);
     else if (L.dtype == FX_BF16 && D == 64)
-        k_approx_scores_mma<64><<<grid, 128, 0, s>>>(mp, q, blk, kblocks, L.kv_heads, L.group_size,
+        launch_pdl(k_approx_scores_mma<64>, grid, 128, 0, s, mp, q, blk, kblocks, L.kv_heads, L.group_size,
                                                      L.l_cpu, approx, approx_stride);
     else if (L.dtype == FX_F32 && D == 128) launch_f32<128>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s);
     else if (L.dtype == FX_F32 && D == 64) launch_f32<64>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s);

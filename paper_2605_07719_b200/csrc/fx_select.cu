@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(256) k_worklist(int Hkv, int G, int64_t l_sink
                                                   int32_t* __restrict__ bg_count,
                                                   int32_t* __restrict__ bg_start,
                                                   int32_t* __restrict__ done, int stage_words) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t wcnt[kMaxWords];
     __shared__ int64_t wsum[257];
     __shared__ int s_last;
@@ -228,7 +230,7 @@ void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
     const int stage_words = (int)std::min<int64_t>(want, 24576);
     const size_t smem = (size_t)stage_words * 4;
     FX_CUDA(cudaFuncSetAttribute(k_worklist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_worklist<<<n_bg, 256, smem, s>>>(L.kv_heads, L.group_size, L.l_sink, L.l_cpu,
+    launch_pdl(k_worklist, n_bg, 256, smem, s, L.kv_heads, L.group_size, L.l_sink, L.l_cpu,
                                        L.l_local + l_new, blk, sel_bits, sel_words, boxes, box_stride,
                                        bg_count, bg_start, done, stage_words);
     FX_CUDA(cudaGetLastError());

@@ -49,36 +49,58 @@ __device__ __forceinline__ const void* level_ptr(const void* const* meta, int bl
     return meta[blk == 16 ? 0 : blk == 32 ? 1 : blk == 64 ? 2 : 3];
 }
 
-__device__ __forceinline__ float cta_reduce_max(float v, float* red) {
-    v = warp_max(v);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    float r = -INFINITY;
+// Reference score of one block by one thread (block_index.cpp:41-53): f64
+// products (exact), summed in dimension order, unfused.  q is f64 in smem;
+// the metadata row (smem or global, generic 16-byte loads) in vectors.
+__device__ __forceinline__ double score_step(double s, double qd, float lo, float hi) {
+    const double a = __dmul_rn(qd, (double)lo), c = __dmul_rn(qd, (double)hi);
+    return __dadd_rn(s, (a < c) ? c : a);
+}
+__device__ double exact_score_vec(const double* __restrict__ qs, const __nv_bfloat16* __restrict__ mn,
+                                  const __nv_bfloat16* __restrict__ mx, int D) {
+    double s = 0.0;
+    if ((D & 7) == 0) {
+        for (int d = 0; d < D; d += 8) {
+            const uint4 a = *reinterpret_cast<const uint4*>(mn + d);
+            const uint4 c = *reinterpret_cast<const uint4*>(mx + d);
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int i = 0; i < kNW; ++i) r = fmaxf(r, red[i]);
-    return r;
+            for (int u = 0; u < 4; ++u) {
+                s = score_step(s, qs[d + 2 * u], bf16lo_to_f(av[u]), bf16lo_to_f(cv[u]));
+                s = score_step(s, qs[d + 2 * u + 1], bf16hi_to_f(av[u]), bf16hi_to_f(cv[u]));
+            }
+        }
+        return s;
+    }
+    for (int d = 0; d < D; ++d) s = score_step(s, qs[d], __bfloat162float(mn[d]), __bfloat162float(mx[d]));
+    return s;
+}
+__device__ double exact_score_vec(const double* __restrict__ qs, const float* __restrict__ mn,
+                                  const float* __restrict__ mx, int D) {
+    double s = 0.0;
+    if ((D & 3) == 0) {
+        for (int d = 0; d < D; d += 4) {
+            const float4 a = *reinterpret_cast<const float4*>(mn + d);
+            const float4 c = *reinterpret_cast<const float4*>(mx + d);
+            s = score_step(s, qs[d], a.x, c.x);
+            s = score_step(s, qs[d + 1], a.y, c.y);
+            s = score_step(s, qs[d + 2], a.z, c.z);
+            s = score_step(s, qs[d + 3], a.w, c.w);
+        }
+        return s;
+    }
+    for (int d = 0; d < D; ++d) s = score_step(s, qs[d], mn[d], mx[d]);
+    return s;
 }
 
-// Reference score of one block by one warp: f64 products in parallel (exact),
-// dimension-order sum by lane 0 (block_index.cpp:41-53).  Valid in lane 0.
-template <typename T>
-__device__ double warp_exact_score(const float* __restrict__ q, const T* __restrict__ mn,
-                                   const T* __restrict__ mx, int D, double* prod) {
-    const int lane = threadIdx.x & 31;
-    for (int d = lane; d < D; d += 32) {
-        const double qd = (double)q[d];
-        const double lo = __dmul_rn(qd, (double)tofl(mn[d]));
-        const double hi = __dmul_rn(qd, (double)tofl(mx[d]));
-        prod[d] = (lo < hi) ? hi : lo;  // std::max(lo, hi)
-    }
-    __syncwarp();
-    double s = 0.0;
-    if (lane == 0)
-        for (int d = 0; d < D; ++d) s = __dadd_rn(s, prod[d]);
-    __syncwarp();
-    return s;
+// Same sum over a row in shared (or global) memory, 16-byte reads.
+__device__ __forceinline__ double exact_score_smem(const double* qs, const __nv_bfloat16* mn,
+                                                   const __nv_bfloat16* mx, int D) {
+    return exact_score_vec(qs, mn, mx, D);
+}
+__device__ __forceinline__ double exact_score_smem(const double* qs, const float* mn,
+                                                   const float* mx, int D) {
+    return exact_score_vec(qs, mn, mx, D);
 }
 
 template <int DT>
@@ -88,17 +110,19 @@ __global__ void __launch_bounds__(kT) k_select(
     int D, int64_t l_cpu, const float* __restrict__ approx, int64_t astride, double eps_scale,
     uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap) {
+    pdl_wait();
+    pdl_trigger();
     using T = typename Elem<DT>::T;
-    // dynamic smem: keys[keys_cap] f32 | hist[kBins] | prod[kNW][D] f64 | ck[kSmallCand] | ci[kSmallCand]
+    // dynamic smem: keys[keys_cap] f32 | hist[kBins] | q[D] f64 | ck[kSmallCand] | ci[kSmallCand]
     extern __shared__ __align__(16) unsigned char dsm[];
     float* s_keys = reinterpret_cast<float*>(dsm);
     int32_t* hist = reinterpret_cast<int32_t*>(dsm + (size_t)keys_cap * 4);
-    double* prod_all = reinterpret_cast<double*>(hist + kBins);
-    uint64_t* ck = reinterpret_cast<uint64_t*>(prod_all + kNW * D);
+    double* s_q = reinterpret_cast<double*>(hist + kBins);
+    uint64_t* ck = reinterpret_cast<uint64_t*>(s_q + D);
     uint32_t* ci = reinterpret_cast<uint32_t*>(ck + kSmallCand);
-    __shared__ float red[kNW];
-    __shared__ int s_bin[2];
-    __shared__ unsigned long long s_ndef, s_ncand;
+    __shared__ float red[2][kNW];
+    __shared__ int s_wsum[2][kNW];
+    __shared__ int s_bin;
     __shared__ double s_eps;
 
     const int64_t head = blockIdx.x;
@@ -159,20 +183,29 @@ __global__ void __launch_bounds__(kT) k_select(
         }
     }
     for (int i = t; i < kBins; i += kT) hist[i] = 0;
+    for (int d = t; d < D; d += kT) s_q[d] = (double)qh[d];
     if (warp == 0) {
         double a = 0.0;
         for (int d = lane; d < D; d += 32)
             a += fabs((double)qh[d]) * (double)absmax[(int64_t)bg * D + d];
         for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) {
-            s_eps = a * eps_scale * 1.01 + 1e-30;
-            s_ndef = 0;
-            s_ncand = 0;
-        }
+        if (lane == 0) s_eps = a * eps_scale * 1.01 + 1e-30;
     }
-    const float gmx = cta_reduce_max(mx, red);
-    const float gmn = -cta_reduce_max(-mn, red);
-    const bool sane = __syncthreads_and(fin_all) && isfinite(s_eps);
+    // one barrier round for max, min and finiteness
+    mx = warp_max(mx);
+    mn = -warp_max(-mn);
+    if (lane == 0) {
+        red[0][warp] = mx;
+        red[1][warp] = mn;
+    }
+    const bool sane_local = __syncthreads_and(fin_all);
+    float gmx = -INFINITY, gmn = INFINITY;
+#pragma unroll
+    for (int i = 0; i < kNW; ++i) {
+        gmx = fmaxf(gmx, red[0][i]);
+        gmn = fminf(gmn, red[1][i]);
+    }
+    const bool sane = sane_local && isfinite(s_eps);
     const float* src = staged ? s_keys : sc;
     const double eps = s_eps;
     SEL_MARK(1);
@@ -188,77 +221,121 @@ __global__ void __launch_bounds__(kT) k_select(
             atomicAdd(&hist[f >= (float)(kBins - 1) ? kBins - 1 : (f <= 0.f ? 0 : (int)f)], 1);
         }
         __syncthreads();
-        if (warp == 0) {  // bin holding the k-th largest, scanning from the top
-            constexpr int PER = kBins / 32;
-            int tot = 0;
-            for (int i = 0; i < PER; ++i) tot += hist[lane * PER + i];
-            int incl = tot;  // count over lanes >= lane
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_down_sync(0xffffffffu, incl, o);
-                if (lane + o < 32) incl += v;
-            }
-            const int excl = incl - tot;
-            if (excl < k && k <= incl) {
-                int above = excl;
-                for (int i = PER - 1; i >= 0; --i) {
-                    above += hist[lane * PER + i];
-                    if (above >= k) {
-                        s_bin[0] = lane * PER + i;
-                        break;
-                    }
+        // bin holding the k-th largest: each thread owns kBins/kT bins; suffix
+        // sums over threads (from the top) locate the owner, which scans them
+        constexpr int PB = kBins / kT;
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < PB; ++i) c += hist[t * PB + i];
+        int x = c;  // suffix sum within the warp (lanes >= lane)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_down_sync(0xffffffffu, x, o);
+            if (lane + o < 32) x += y;
+        }
+        if (lane == 0) s_wsum[0][warp] = x;
+        __syncthreads();
+        int S = x;
+        for (int w = warp + 1; w < kNW; ++w) S += s_wsum[0][w];
+        if (S >= k && S - c < k) {
+            int above = S - c;
+            for (int i = PB - 1; i >= 0; --i) {
+                above += hist[t * PB + i];
+                if (above >= k) {
+                    s_bin = t * PB + i;
+                    break;
                 }
             }
         }
         __syncthreads();
         const double w = ((double)gmx - (double)gmn) / kBins;
-        e_lo = (double)gmn + (s_bin[0] - 1) * w;
-        e_hi = (double)gmn + (s_bin[0] + 2) * w;
+        e_lo = (double)gmn + (s_bin - 1) * w;
+        e_hi = (double)gmn + (s_bin + 2) * w;
     }
     const double hi = e_hi + 2.0 * eps, lo = e_lo - 2.0 * eps;
     SEL_MARK(2);
 
-    // ---- 2. classify: definite-in bits, band appended (warp-aggregated) ----
+    // ---- 2. classify: definite-in bits, band ids (two conflict-free warp passes) ----
     uint32_t* cids = cand_ids + head * cand_stride;
     uint64_t* ckeys = cand_keys + head * cand_stride;
+    int wdef = 0, wcand = 0;  // this warp's totals (all lanes)
     for (int j = warp; j < W; j += kNW) {
         const int64_t i = (int64_t)j * 32 + lane;
         const bool in = i < nblk;
         const double a = in ? (double)src[i] : 0.0;
-        const bool def = in && a > hi;
-        const bool cand = in && !def && a >= lo;
-        const uint32_t bd = __ballot_sync(0xffffffffu, def);
-        const uint32_t bc = __ballot_sync(0xffffffffu, cand);
-        unsigned long long base = 0;
-        if (lane == 0) {
-            bits[j] = bd;
-            if (bd) atomicAdd(&s_ndef, (unsigned long long)__popc(bd));
-            if (bc) base = atomicAdd(&s_ncand, (unsigned long long)__popc(bc));
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (cand) {
-            const int64_t pos = (int64_t)base + __popc(bc & ((1u << lane) - 1u));
-            cids[pos] = (uint32_t)i;
-            if (pos < kSmallCand) ci[pos] = (uint32_t)i;
-        }
+        const uint32_t bd = __ballot_sync(0xffffffffu, in && a > hi);
+        const uint32_t bc = __ballot_sync(0xffffffffu, in && !(a > hi) && a >= lo);
+        if (lane == 0) bits[j] = bd;
+        wdef += __popc(bd);
+        wcand += __popc(bc);
+    }
+    if (lane == 0) {
+        s_wsum[0][warp] = wdef;
+        s_wsum[1][warp] = wcand;
     }
     __syncthreads();
-    const int64_t n_def = (int64_t)s_ndef, n_cand = (int64_t)s_ncand;
-    const int64_t need = k - n_def;
+    int64_t n_def = 0, n_cand = 0, base = 0;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) {
+        n_def += s_wsum[0][w];
+        if (w < warp) base += s_wsum[1][w];
+        n_cand += s_wsum[1][w];
+    }
     const bool small = n_cand <= kSmallCand;
+    for (int j = warp; j < W; j += kNW) {
+        const int64_t i = (int64_t)j * 32 + lane;
+        const bool in = i < nblk;
+        const double a = in ? (double)src[i] : 0.0;
+        const bool cand = in && !(a > hi) && a >= lo;
+        const uint32_t bc = __ballot_sync(0xffffffffu, cand);
+        if (cand) {
+            const int64_t pos = base + __popc(bc & ((1u << lane) - 1u));
+            if (small) ci[pos] = (uint32_t)i;
+            else cids[pos] = (uint32_t)i;
+        }
+        base += __popc(bc);
+    }
+    const int64_t need = k - n_def;
+    __syncthreads();
     SEL_MARK(3);
 #ifdef FX_TRACE
     if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + 6] = n_cand | (n_def << 32);
     if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + 7] = k | ((int64_t)nblk << 32);
 #endif
 
-    // ---- 3. exact scores of the band, rank, set bits ----
-    for (int64_t c = warp; c < n_cand; c += kNW) {
-        const uint32_t id = small ? ci[c] : cids[c];
-        const double s = warp_exact_score(qh, mbase + (int64_t)id * 2 * D,
-                                          mbase + (int64_t)id * 2 * D + D, D, prod_all + warp * D);
-        if (lane == 0) {
-            if (small) ck[c] = f64_key(s);
-            else ckeys[c] = f64_key(s);
+    // ---- 3. exact reference scores of the band ----
+    // The candidates' metadata rows are staged in smem (over the no longer
+    // needed keys + histogram) by coalesced 16-byte loads -- one round trip
+    // for a whole round -- then one thread per candidate sums its row.
+    {
+        const int row_b = 2 * D * (int)sizeof(T);
+        const int pitch = row_b + 16;  // 16-byte skew: conflict-free row-parallel reads
+        const int per_round = ((int)((size_t)keys_cap * 4 + kBins * 4)) / pitch;
+        const bool vec = (row_b & 15) == 0 && per_round >= 1;
+        unsigned char* stage = dsm;
+        for (int64_t c0 = 0; c0 < n_cand; c0 += (vec ? per_round : n_cand)) {
+            const int64_t step_ = vec ? (int64_t)per_round : n_cand;
+            const int nc = (int)(n_cand - c0 < step_ ? n_cand - c0 : step_);
+            if (vec) {
+                const int v16 = row_b / 16;
+                for (int e = t; e < nc * v16; e += kT) {
+                    const int cc = e / v16, u = e % v16;
+                    const uint32_t id = small ? ci[c0 + cc] : cids[c0 + cc];
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(mbase + (int64_t)id * 2 * D) + u);
+                    *reinterpret_cast<uint4*>(stage + (size_t)cc * pitch + u * 16) = x;
+                }
+                __syncthreads();
+            }
+            for (int cc = t; cc < nc; cc += kT) {
+                const int64_t c = c0 + cc;
+                const uint32_t id = small ? ci[c] : cids[c];
+                const T* mrow = vec ? reinterpret_cast<const T*>(stage + (size_t)cc * pitch)
+                                    : mbase + (int64_t)id * 2 * D;
+                const double sc_ = exact_score_smem(s_q, mrow, mrow + D, D);
+                if (small) ck[c] = f64_key(sc_);
+                else ckeys[c] = f64_key(sc_);
+            }
+            __syncthreads();
         }
     }
     __syncthreads();
@@ -321,17 +398,17 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
     const int64_t heads = (int64_t)L.batch * L.kv_heads * L.group_size;
     const int64_t nmax = level_blocks(L.l_cpu, 16);
     const int keys_cap = (int)((std::min<int64_t>(nmax, kSmemKeys) + 3) & ~int64_t(3));
-    const size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)kNW * L.head_dim * 8 +
+    const size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)L.head_dim * 8 +
                         (size_t)kSmallCand * 12;
     const double eps = approx_eps_scale(L);
     if (L.dtype == FX_BF16) {
         FX_CUDA(cudaFuncSetAttribute(k_select<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_select<FX_BF16><<<(unsigned)heads, kT, smem, s>>>(
+        launch_pdl(k_select<FX_BF16>, (unsigned)heads, kT, smem, s, 
             mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
             approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap);
     } else {
         FX_CUDA(cudaFuncSetAttribute(k_select<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_select<FX_F32><<<(unsigned)heads, kT, smem, s>>>(
+        launch_pdl(k_select<FX_F32>, (unsigned)heads, kT, smem, s, 
             mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
             approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap);
     }
