@@ -944,40 +944,6 @@ __global__ void k_convert(const float* src, T* dst, size_t n) {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        FX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
-        FX_REQUIRE(ptr != nullptr && q == cudaDriverEntryPointSuccess, FX_ERR_CUDA,
-                   "cuda-error: cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<EncodeTiledFn>(ptr);
-    }
-    return fn;
-}
-
-// [rows][D] bf16 viewed as 3-D {64 columns, rows, D/64 chunks} (strides: row
-// D*2 bytes, chunk 128 bytes); box = {64, box_rows, D/64}; 128-byte swizzle.
-CUtensorMap make_kv_map(const void* base, int D, int64_t rows, int box_rows) {
-    CUtensorMap m;
-    const cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(D / 64)};
-    const cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
-    const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)(D / 64)};
-    const cuuint32_t es[3] = {1, 1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
-                                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    FX_REQUIRE(r == CUDA_SUCCESS, FX_ERR_CUDA, "cuda-error: cuTensorMapEncodeTiled failed");
-    return m;
-}
-
 View make_view(const AttendArgs& a) {
     View v;
     v.n_bg = a.L.batch * a.L.kv_heads;
@@ -1006,14 +972,49 @@ void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
     const View v = make_view(a);
     const int64_t rows = (int64_t)v.n_bg * a.L.l_cap;
     KvMaps maps;
-    maps.box[0] = make_kv_map(a.k, D, rows, kBoxRows);
-    maps.box[1] = make_kv_map(a.v, D, rows, kBoxRows);
+    maps.box[0] = make_row_map(a.k, D, rows, kBoxRows);
+    maps.box[1] = make_row_map(a.v, D, rows, kBoxRows);
     const size_t smem = TmaCfg<D>::TOTAL;
     FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(k_attend_tma<D>, grid, kTmaThreads, smem, s, maps, v);
 }
 
 }  // namespace
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        FX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+        FX_REQUIRE(ptr != nullptr && q == cudaDriverEntryPointSuccess, FX_ERR_CUDA,
+                   "cuda-error: cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// [rows][D] bf16 viewed as 3-D {64 columns, rows, D/64 chunks} (strides: row
+// D*2 bytes, chunk 128 bytes); box = {64, box_rows, D/64}; 128-byte swizzle.
+// (K/V rows here; metadata rows [min | max] = D' = 2 * head_dim in fx_score.cu.)
+CUtensorMap make_row_map(const void* base, int D, int64_t rows, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(D / 64)};
+    const cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
+    const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)(D / 64)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
+                                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    FX_REQUIRE(r == CUDA_SUCCESS, FX_ERR_CUDA, "cuda-error: cuTensorMapEncodeTiled failed");
+    return m;
+}
 
 bool attend_uses_tma(const fx_layout& L, bool has_idx) {
     return !has_idx && L.dtype == FX_BF16 && (L.head_dim == 64 || L.head_dim == 128) &&

@@ -306,7 +306,8 @@ Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, 
     if (sparse && !given_sel) {
         {
             Timed tm(ctx, FX_KERNEL_SCORE);
-            fx::launch_approx_scores(L, a->meta, a->q, p.blk, p.kblocks, s.approx, s.approx_stride, st);
+            fx::launch_approx_scores(L, a->meta, a->q, p.blk, p.kblocks, s.approx, s.approx_stride,
+                                     ctx->num_sms, st);
         }
         {
             Timed tm(ctx, FX_KERNEL_SELECT);
@@ -533,7 +534,8 @@ int fx_approx_scores(fx_ctx* ctx, const fx_layout* lay, const void* const meta[4
         FX_CUDA(cudaMemcpyAsync(kb, ones.data(), sizeof(int32_t) * heads, cudaMemcpyHostToDevice,
                                 ctx->stream));
         fx::launch_approx_scores(*lay, meta, q, blk, kb, out,
-                                 std::max<int64_t>(1, fx::level_blocks(lay->l_cpu, 16)), ctx->stream);
+                                 std::max<int64_t>(1, fx::level_blocks(lay->l_cpu, 16)), ctx->num_sms,
+                                 ctx->stream);
         FX_CUDA(cudaStreamSynchronize(ctx->stream));
         if (eps_scale) *eps_scale = fx::approx_eps_scale(*lay);
         ctx->launches += 1;

@@ -1,6 +1,7 @@
 // fx_internal.h -- host-side internals shared by the .cu translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -100,7 +101,7 @@ void launch_predict(int n, const double* w1t, const double* b1, const double* w2
 double approx_eps_scale(const fx_layout& L);
 void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
                           const int32_t* blk, const int32_t* kblocks, float* approx,
-                          int64_t approx_stride, cudaStream_t s);
+                          int64_t approx_stride, int num_sms, cudaStream_t s);
 void launch_select(const fx_layout& L, const void* const meta[4], const float* absmax,
                    const float* q, const int32_t* blk, const int32_t* kblocks,
                    const float* approx, int64_t approx_stride, uint32_t* sel_bits, int sel_words,
@@ -119,6 +120,9 @@ void launch_meta_absmax(const void* meta, int dtype, int64_t nblk, int dim, floa
                         cudaStream_t s);
 
 // fx_attend.cu
+// 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},
+// box {64, box_rows, D/64}, 128-byte swizzle (D multiple of 64).
+CUtensorMap make_row_map(const void* base, int D, int64_t rows, int box_rows);
 struct AttendArgs {
     fx_layout L;
     const void* k;

@@ -21,6 +21,8 @@
 // leaves <= 2^-16 relative; tensor-core f32 accumulation adds a few ulp per
 // MMA over 32 MMAs -- tests/test_gpu_parity.py::test_approx_score_error_bound
 // measures the realized ratio, ~1e-6, against this 6e-5 budget).
+#include <algorithm>
+
 #include "fx_common.cuh"
 
 namespace fx {
@@ -61,77 +63,220 @@ __device__ __forceinline__ bool tile_ctx(const int32_t* blk_arr, const int32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// tensor-core path (bf16 metadata)
+// tensor-core path (bf16 metadata): TMA-fed, warp-specialized, persistent
 // ---------------------------------------------------------------------------
+// Work item: 64 consecutive blocks (metadata rows) of one (b, g) = one 3-D
+// TMA box {64 columns, 64 rows, 2D/64 chunks} with 128-byte swizzle (32 KB
+// at D = 128), the same row-box layout the attention kernel streams K with.
+// One CTA per SM: a producer warp walks the CTA's contiguous range of the
+// flattened item sequence (only groups that need ranking) issuing one TMA per
+// item into a kSStages ring; 4 consumer warps take 16 rows each:
+// S^T[16 blocks x 8 heads] = Meta[16 x 2D] . [q- ; q+] (ldmatrix + mma.sync
+// m16n8k16, f32 accumulate, q split into bf16 hi + lo).
+constexpr int kSRows = 64;
+constexpr int kSStages = 5;
+constexpr int kSCWarps = 4;
+constexpr int kSThreads = (kSCWarps + 1) * 32;
+constexpr int kMaxScoreGroups = 4096;
+
+struct MetaMaps {
+    CUtensorMap lvl[4];  // blk 16 / 32 / 64 / 128
+};
+
+struct ItemHdr {
+    int32_t bg, j0, n, end;
+};
+
 template <int D>
-__global__ void __launch_bounds__(128) k_approx_scores_mma(MetaPtrs meta,
-                                                           const float* __restrict__ q,
-                                                           const int32_t* __restrict__ blk_arr,
-                                                           const int32_t* __restrict__ kblocks,
-                                                           int Hkv, int G, int64_t l_cpu,
-                                                           float* __restrict__ approx,
-                                                           int64_t stride) {
+struct ScoreCfg {
+    static constexpr int RB = 2 * D * 2;       // bytes of one [min | max] row
+    static constexpr int NCH = RB / 128;       // 128-byte chunks per row
+    static constexpr int STAGE = kSRows * RB;  // one box
+    static constexpr int NT = 2 * D / 16;      // k-steps
+    static constexpr size_t HDR = (size_t)kSStages * STAGE;
+    static constexpr size_t BAR = HDR + kSStages * sizeof(ItemHdr);
+    static constexpr size_t PREF = BAR + 2 * kSStages * sizeof(uint64_t);
+    static constexpr size_t TOTAL = PREF + (kMaxScoreGroups + 1) * sizeof(int) + 1024;
+};
+
+__device__ __forceinline__ int level_of(int blk) { return blk == 16 ? 0 : blk == 32 ? 1 : blk == 64 ? 2 : 3; }
+
+__device__ __forceinline__ int group_items(const int32_t* blk_arr, const int32_t* kblocks, int bg,
+                                           int G, int64_t l_cpu) {
+    const int blk = blk_arr[bg];
+    if (blk <= 0) return 0;
+    const int64_t nblk = cdiv_dev(l_cpu, blk);
+    bool any = false;
+    for (int h = 0; h < G; ++h) {
+        const int32_t kk = kblocks[(int64_t)bg * G + h];
+        any |= (kk > 0 && kk < nblk);  // k = 0 or k >= nblk needs no ranking
+    }
+    return any ? (int)cdiv_dev(nblk, kSRows) : 0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
+    const __grid_constant__ MetaMaps maps, const float* __restrict__ q,
+    const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int n_bg, int G,
+    int64_t l_cpu, float* __restrict__ approx, int64_t stride) {
     pdl_wait();
     pdl_trigger();
-    constexpr int KW = 2 * D;   // min row | max row
-    constexpr int NP = KW / 32;  // k-step pairs
-    TileCtx c;
-    if (!tile_ctx(blk_arr, kblocks, Hkv, G, l_cpu, c)) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int hq = lane >> 2, t = lane & 3;
-    const __nv_bfloat16* base =
-        static_cast<const __nv_bfloat16*>(level_ptr(meta.p, c.blk)) + (int64_t)c.bg * c.nblk * KW;
-
-    // B fragments of [q- ; q+] for head hq, permuted like the A loads
-    uint32_t bh[NP][4], bl[NP][4];
-    {
-        const float* qh = q + (c.head0 + (hq < G ? hq : 0)) * D;
+    using C = ScoreCfg<D>;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    ItemHdr* hdr = reinterpret_cast<ItemHdr*>(smem + C::HDR);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR);
+    uint64_t* empty = full + kSStages;
+    int* s_pref = reinterpret_cast<int*>(smem + C::PREF);
+    __shared__ int s_wsum[kSThreads / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int NW = kSThreads / 32;
+    // exclusive prefix of items over the groups
+    int carry = 0;
+    for (int c0 = 0; c0 < n_bg; c0 += kSThreads) {
+        const int i = c0 + tid;
+        const int v = i < n_bg ? group_items(blk_arr, kblocks, i, G, l_cpu) : 0;
+        int x = v;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            float hi[8], lo[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int col = 32 * p + 8 * t + e;
-                const int d = col % D;
-                float x = hq < G ? __ldg(qh + d) : 0.f;
-                x = col < D ? fminf(x, 0.f) : fmaxf(x, 0.f);
-                hi[e] = __bfloat162float(__float2bfloat16_rn(x));
-                lo[e] = x - hi[e];
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                bh[p][i] = pack_bf16(hi[2 * i], hi[2 * i + 1]);
-                bl[p][i] = pack_bf16(lo[2 * i], lo[2 * i + 1]);
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
+        if (lane == 31) s_wsum[warp] = x;
+        __syncthreads();
+        int off = carry, tot = 0;
+        for (int w = 0; w < NW; ++w) {
+            if (w < warp) off += s_wsum[w];
+            tot += s_wsum[w];
+        }
+        if (i < n_bg) s_pref[i] = off + x - v;
+        __syncthreads();
+        carry += tot;
     }
-    for (int mt = warp; mt < kTileBlocks / 16; mt += 4) {
-        const int64_t j0 = c.t0 + mt * 16;
-        if (j0 >= c.nblk) break;
-        const int64_t r0 = min(j0 + hq, c.nblk - 1), r1 = min(j0 + hq + 8, c.nblk - 1);
-        uint4 va[NP], vb[NP];
+    if (tid == 0) {
+        s_pref[n_bg] = carry;
+        for (int i = 0; i < kSStages; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, kSCWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t total = carry;
+    const int64_t i0 = total * blockIdx.x / gridDim.x, i1 = total * (blockIdx.x + 1) / gridDim.x;
+
+    if (warp == kSCWarps) {
+        // ------------------------------ producer ------------------------------
+        if (lane == 0) {
+            for (int l = 0; l < 4; ++l) tma_prefetch_desc(&maps.lvl[l]);
+            int st = 0;
+            uint32_t ph = 0;
+            int bg = 0, cur = -1, lvl = 0;
+            int64_t nblk = 0;
+            if (i0 < i1) {
+                int lo = 0, hi = n_bg - 1;  // last group with s_pref[bg] <= i0
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_pref[mid] <= i0) lo = mid;
+                    else hi = mid - 1;
+                }
+                bg = lo;
+            }
+            for (int64_t it = i0; it < i1; ++it) {
+                while (s_pref[bg + 1] <= it) ++bg;
+                if (bg != cur) {
+                    cur = bg;
+                    const int blk = blk_arr[bg];
+                    lvl = level_of(blk);
+                    nblk = cdiv_dev(l_cpu, blk);
+                }
+                const int64_t j0 = (it - s_pref[bg]) * kSRows;
+                mbar_wait(empty + st, ph ^ 1u);
+                ItemHdr& H = hdr[st];
+                H.bg = bg;
+                H.j0 = (int32_t)j0;
+                H.n = (int32_t)(nblk - j0 < kSRows ? nblk - j0 : kSRows);
+                H.end = 0;
+                mbar_arrive_expect_tx(full + st, (uint32_t)C::STAGE);
+                tma_load_3d(smem + (size_t)st * C::STAGE, &maps.lvl[lvl], full + st, 0,
+                            (int)((int64_t)bg * nblk + j0), 0);
+                if (++st == kSStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+            mbar_wait(empty + st, ph ^ 1u);
+            hdr[st].end = 1;
+            mbar_arrive(full + st);
+        }
+        return;
+    }
+
+    // ------------------------------- consumers -------------------------------
+    constexpr int NT = C::NT;
+    const int hq = lane >> 2, tq = lane & 3;
+    uint32_t bh[NT][2], bl[NT][2];
+    int cur = -1;
+    int64_t head0 = 0;
+    int st = 0;
+    uint32_t ph = 0;
+    const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
+    while (true) {
+        mbar_wait(full + st, ph);
+        const ItemHdr H = hdr[st];
+        if (H.end) break;
+        if (H.bg != cur) {  // B fragments of [q- ; q+] for head hq of the group
+            cur = H.bg;
+            head0 = (int64_t)cur * G;
+            const float* qh = q + (head0 + (hq < G ? hq : 0)) * D;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            va[p] = __ldg(reinterpret_cast<const uint4*>(base + r0 * KW + 32 * p + 8 * t));
-            vb[p] = __ldg(reinterpret_cast<const uint4*>(base + r1 * KW + 32 * p + 8 * t));
-        }
-        float ch[4] = {0.f, 0.f, 0.f, 0.f}, cl[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int j = 0; j < NT; ++j) {
+                float x[4];
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            mma_bf16_16816(ch, va[p].x, vb[p].x, va[p].y, vb[p].y, bh[p][0], bh[p][1]);
-            mma_bf16_16816(cl, va[p].x, vb[p].x, va[p].y, vb[p].y, bl[p][0], bl[p][1]);
-            mma_bf16_16816(ch, va[p].z, vb[p].z, va[p].w, vb[p].w, bh[p][2], bh[p][3]);
-            mma_bf16_16816(cl, va[p].z, vb[p].z, va[p].w, vb[p].w, bl[p][2], bl[p][3]);
+                for (int e = 0; e < 4; ++e) {
+                    const int col = 16 * j + 2 * tq + (e & 1) + (e >> 1) * 8;
+                    float v = hq < G ? __ldg(qh + (col % D)) : 0.f;
+                    x[e] = col < D ? fminf(v, 0.f) : fmaxf(v, 0.f);
+                }
+                const float h0 = __bfloat162float(__float2bfloat16_rn(x[0]));
+                const float h1 = __bfloat162float(__float2bfloat16_rn(x[1]));
+                const float h2 = __bfloat162float(__float2bfloat16_rn(x[2]));
+                const float h3 = __bfloat162float(__float2bfloat16_rn(x[3]));
+                bh[j][0] = pack_bf16(h0, h1);
+                bh[j][1] = pack_bf16(h2, h3);
+                bl[j][0] = pack_bf16(x[0] - h0, x[1] - h1);
+                bl[j][1] = pack_bf16(x[2] - h2, x[3] - h3);
+            }
         }
-        const int h0 = 2 * t;
-        const int64_t ja = j0 + hq, jb = j0 + hq + 8;
-        if (h0 < G) {
-            if (ja < c.nblk) approx[(c.head0 + h0) * stride + ja] = ch[0] + cl[0];
-            if (jb < c.nblk) approx[(c.head0 + h0) * stride + jb] = ch[2] + cl[2];
+        if (warp * 16 < H.n) {
+            const uint32_t ka = smem_u32(smem + (size_t)st * C::STAGE) + warp * 16 * 128;
+            float ch[4] = {0.f, 0.f, 0.f, 0.f}, cl[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int u = ((j & 3) << 1) + (lane >> 4);
+                const uint32_t off = r * 128 + ((u ^ (r & 7)) << 4);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(ka + (j >> 2) * (kSRows * 128) + off, a0, a1, a2, a3);
+                mma_bf16_16816(ch, a0, a1, a2, a3, bh[j][0], bh[j][1]);
+                mma_bf16_16816(cl, a0, a1, a2, a3, bl[j][0], bl[j][1]);
+            }
+            const int h0 = 2 * tq;
+            const int ra = warp * 16 + hq, rb = ra + 8;
+            const int64_t ja = H.j0 + ra, jb = H.j0 + rb;
+            if (h0 < G) {
+                if (ra < H.n) approx[(head0 + h0) * stride + ja] = ch[0] + cl[0];
+                if (rb < H.n) approx[(head0 + h0) * stride + jb] = ch[2] + cl[2];
+            }
+            if (h0 + 1 < G) {
+                if (ra < H.n) approx[(head0 + h0 + 1) * stride + ja] = ch[1] + cl[1];
+                if (rb < H.n) approx[(head0 + h0 + 1) * stride + jb] = ch[3] + cl[3];
+            }
         }
-        if (h0 + 1 < G) {
-            if (ja < c.nblk) approx[(c.head0 + h0 + 1) * stride + ja] = ch[1] + cl[1];
-            if (jb < c.nblk) approx[(c.head0 + h0 + 1) * stride + jb] = ch[3] + cl[3];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        if (++st == kSStages) {
+            st = 0;
+            ph ^= 1u;
         }
     }
 }
@@ -251,6 +396,23 @@ void launch_f32(const fx_layout& L, MetaPtrs mp, const float* q, const int32_t* 
 #undef FX_G
 }
 
+template <int D>
+void launch_score_tma(const fx_layout& L, const void* const meta[4], const float* q,
+                      const int32_t* blk, const int32_t* kblocks, float* approx, int64_t stride,
+                      int num_sms, cudaStream_t s) {
+    const int n_bg = L.batch * L.kv_heads;
+    FX_REQUIRE(n_bg <= kMaxScoreGroups, FX_ERR_INVALID, "bad-shape: more than 4096 (b, g) groups");
+    MetaMaps maps;
+    for (int l = 0; l < 4; ++l) {
+        const int64_t rows = (int64_t)n_bg * level_blocks(L.l_cpu, kLevels[l]);
+        maps.lvl[l] = make_row_map(meta[l], 2 * D, std::max<int64_t>(rows, kSRows), kSRows);
+    }
+    const size_t smem = ScoreCfg<D>::TOTAL;
+    FX_CUDA(cudaFuncSetAttribute(k_score_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_pdl(k_score_tma<D>, (unsigned)std::max(1, num_sms), kSThreads, smem, s, maps, q, blk,
+               kblocks, n_bg, L.group_size, L.l_cpu, approx, stride);
+}
+
 }  // namespace
 
 double approx_eps_scale(const fx_layout& L) {
@@ -259,18 +421,17 @@ double approx_eps_scale(const fx_layout& L) {
 
 void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
                           const int32_t* blk, const int32_t* kblocks, float* approx,
-                          int64_t approx_stride, cudaStream_t s) {
+                          int64_t approx_stride, int num_sms, cudaStream_t s) {
     MetaPtrs mp{{meta[0], meta[1], meta[2], meta[3]}};
     const int D = L.head_dim;
     FX_REQUIRE(L.group_size <= 8, FX_ERR_INVALID, "bad-shape: group_size must be <= 8");
     const dim3 grid((unsigned)cdiv(level_blocks(L.l_cpu, 16), kTileBlocks),
                     (unsigned)(L.batch * L.kv_heads));
+    const int n_bg = L.batch * L.kv_heads;
     if (L.dtype == FX_BF16 && D == 128)
-        launch_pdl(k_approx_scores_mma<128>, grid, 128, 0, s, mp, q, blk, kblocks, L.kv_heads, L.group_size,
-                                                      L.l_cpu, approx, approx_stride);
+        launch_score_tma<128>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s);
     else if (L.dtype == FX_BF16 && D == 64)
-        launch_pdl(k_approx_scores_mma<64>, grid, 128, 0, s, mp, q, blk, kblocks, L.kv_heads, L.group_size,
-                                                     L.l_cpu, approx, approx_stride);
+        launch_score_tma<64>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s);
     else if (L.dtype == FX_F32 && D == 128) launch_f32<128>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s);
     else if (L.dtype == FX_F32 && D == 64) launch_f32<64>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s);
     else fail(FX_ERR_INVALID, "bad-shape: batched scoring supports head_dim 64 or 128");
