@@ -96,21 +96,26 @@ struct ScoreCfg {
     static constexpr size_t HDR = (size_t)kSStages * STAGE;
     static constexpr size_t BAR = HDR + kSStages * sizeof(ItemHdr);
     static constexpr size_t PREF = BAR + 2 * kSStages * sizeof(uint64_t);
-    static constexpr size_t TOTAL = PREF + (kMaxScoreGroups + 1) * sizeof(int) + 1024;
+    static constexpr size_t BLK = PREF + (kMaxScoreGroups + 1) * sizeof(int);
+    static constexpr size_t TOTAL = BLK + kMaxScoreGroups * sizeof(int) + 1024;
 };
 
 __device__ __forceinline__ int level_of(int blk) { return blk == 16 ? 0 : blk == 32 ? 1 : blk == 64 ? 2 : 3; }
 
+// items of group bg (0: streaming, or no head needs ranking); blk and the
+// G per-head k load together (one round trip)
 __device__ __forceinline__ int group_items(const int32_t* blk_arr, const int32_t* kblocks, int bg,
-                                           int G, int64_t l_cpu) {
-    const int blk = blk_arr[bg];
+                                           int G, int64_t l_cpu, int* blk_out) {
+    int32_t kk[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) kk[h] = h < G ? __ldg(kblocks + (int64_t)bg * G + h) : 0;
+    const int blk = __ldg(blk_arr + bg);
+    *blk_out = blk;
     if (blk <= 0) return 0;
     const int64_t nblk = cdiv_dev(l_cpu, blk);
     bool any = false;
-    for (int h = 0; h < G; ++h) {
-        const int32_t kk = kblocks[(int64_t)bg * G + h];
-        any |= (kk > 0 && kk < nblk);  // k = 0 or k >= nblk needs no ranking
-    }
+#pragma unroll
+    for (int h = 0; h < 8; ++h) any |= (kk[h] > 0 && kk[h] < nblk);  // k = 0 or >= nblk: no ranking
     return any ? (int)cdiv_dev(nblk, kSRows) : 0;
 }
 
@@ -128,6 +133,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR);
     uint64_t* empty = full + kSStages;
     int* s_pref = reinterpret_cast<int*>(smem + C::PREF);
+    int* s_blk = reinterpret_cast<int*>(smem + C::BLK);
     __shared__ int s_wsum[kSThreads / 32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int NW = kSThreads / 32;
@@ -135,7 +141,9 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     int carry = 0;
     for (int c0 = 0; c0 < n_bg; c0 += kSThreads) {
         const int i = c0 + tid;
-        const int v = i < n_bg ? group_items(blk_arr, kblocks, i, G, l_cpu) : 0;
+        int bv = 0;
+        const int v = i < n_bg ? group_items(blk_arr, kblocks, i, G, l_cpu, &bv) : 0;
+        if (i < n_bg) s_blk[i] = bv;
         int x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
                 while (s_pref[bg + 1] <= it) ++bg;
                 if (bg != cur) {
                     cur = bg;
-                    const int blk = blk_arr[bg];
+                    const int blk = s_blk[bg];
                     lvl = level_of(blk);
                     nblk = cdiv_dev(l_cpu, blk);
                 }
@@ -221,12 +229,28 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     int st = 0;
     uint32_t ph = 0;
     const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
+    int first_bg = -1;  // the CTA's first group: its q fragments load while the first box is in flight
+    if (i0 < i1) {
+        int lo = 0, hi = n_bg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= i0) lo = mid;
+            else hi = mid - 1;
+        }
+        while (s_pref[lo + 1] <= i0) ++lo;
+        first_bg = lo;
+    }
     while (true) {
-        mbar_wait(full + st, ph);
-        const ItemHdr H = hdr[st];
-        if (H.end) break;
-        if (H.bg != cur) {  // B fragments of [q- ; q+] for head hq of the group
-            cur = H.bg;
+        int want = first_bg;
+        ItemHdr H;
+        if (want < 0) {
+            mbar_wait(full + st, ph);
+            H = hdr[st];
+            if (H.end) break;
+            want = H.bg;
+        }
+        if (want != cur) {  // B fragments of [q- ; q+] for head hq of the group
+            cur = want;
             head0 = (int64_t)cur * G;
             const float* qh = q + (head0 + (hq < G ? hq : 0)) * D;
 #pragma unroll
@@ -247,6 +271,13 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
                 bl[j][0] = pack_bf16(x[0] - h0, x[1] - h1);
                 bl[j][1] = pack_bf16(x[2] - h2, x[3] - h3);
             }
+        }
+        if (first_bg >= 0) {  // prefetched; now wait for the first box
+            first_bg = -1;
+            mbar_wait(full + st, ph);
+            H = hdr[st];
+            if (H.end) break;
+            if (H.bg != cur) continue;  // (cannot happen: same range arithmetic)
         }
         if (warp * 16 < H.n) {
             const uint32_t ka = smem_u32(smem + (size_t)st * C::STAGE) + warp * 16 * 128;
