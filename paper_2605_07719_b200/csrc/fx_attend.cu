@@ -75,7 +75,8 @@ struct View {
     const uint32_t* idx;
     const Box* boxes;
     int64_t box_stride;
-    const int32_t* bg_start;
+    const int32_t* bg_start;  // global run starts (used when n_bg > kMaxPrefix)
+    const int32_t* bg_count;  // per-(b, g) box counts (run starts rebuilt in smem)
     int pad;  // virtual boxes ending each run in the split (never loaded)
     float* part_o;
     float* part_lse;
@@ -92,7 +93,7 @@ __device__ __forceinline__ int cta_of(int64_t x, int64_t NB, int grid) {
 // One L2 round trip instead of log2(n_bg) dependent ones.
 __device__ __forceinline__ int find_bg_warp(const int32_t* start, int n_bg, int64_t x, int lane) {
     int cnt = 0;
-    for (int j = 1 + lane; j < n_bg; j += 32) cnt += __ldg(start + j) <= x ? 1 : 0;
+    for (int j = 1 + lane; j < n_bg; j += 32) cnt += start[j] <= x ? 1 : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     return cnt;  // start[] is non-decreasing and start[0] = 0 <= x
@@ -101,7 +102,7 @@ __device__ __forceinline__ int find_bg(const int32_t* start, int n_bg, int64_t x
     int lo = 0, hi = n_bg - 1;  // largest bg with start[bg] <= x
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(start + mid) <= x) lo = mid;
+        if (start[mid] <= x) lo = mid;
         else hi = mid - 1;
     }
     return lo;
@@ -114,6 +115,41 @@ __device__ __forceinline__ bool cta_nonempty(int c, int64_t NB, int grid) {
 }
 
 constexpr int kMaxContrib = 160;  // contributor list held in smem (>= TMA grid)
+constexpr int kMaxPrefix = kMaxRunPrefix;  // (b, g) runs whose starts are rebuilt in smem
+
+// Run starts of the global box sequence: exclusive prefix of (box count +
+// pad) over the (b, g) runs, rebuilt by every CTA in smem from the
+// worklist's counts (one coalesced round trip), so the worklist publishes no
+// grid-wide prefix and the producer's run walk never touches global memory.
+// Larger batches fall back to the worklist's global bg_start.
+__device__ const int32_t* run_starts(const View& p, int32_t* s_start, int* wtmp, int t, int nt) {
+    if (p.n_bg > kMaxPrefix) return p.bg_start;
+    const int lane = t & 31, warp = t >> 5, nw = nt >> 5;
+    int carry = 0;
+    for (int c0 = 0; c0 < p.n_bg; c0 += nt) {
+        const int i = c0 + t;
+        const int v = i < p.n_bg ? __ldcg(p.bg_count + i) + p.pad : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wtmp[warp] = x;
+        __syncthreads();
+        int off = carry, tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) off += wtmp[w];
+            tot += wtmp[w];
+        }
+        if (i < p.n_bg) s_start[i] = off + x - v;
+        __syncthreads();
+        carry += tot;
+    }
+    if (t == 0) s_start[p.n_bg] = carry;
+    __syncthreads();
+    return s_start;
+}
 
 // Shared scratch of the run merge (MG = largest group size).
 template <int MG>
@@ -132,10 +168,9 @@ struct MergeSmem {
 // Merge the partials of run `bg` (attention.cpp:89-104 applied across the
 // CTAs that covered it) into the final output.  `nt` threads, barrier `bar`.
 template <int MG>
-__device__ void merge_run(const View& p, int bg, int64_t NB, int grid, int t, int nt, int bar,
-                          MergeSmem<MG>* ms) {
+__device__ void merge_run(const View& p, int bg, int64_t s, int64_t e, int64_t NB, int grid, int t,
+                          int nt, int bar, MergeSmem<MG>* ms) {
     const int G = p.G, D = p.D;
-    const int64_t s = __ldg(p.bg_start + bg), e = __ldg(p.bg_start + bg + 1) - p.pad;
     const int cf = cta_of(s, NB, grid), cl = cta_of(e - 1, NB, grid);
     const int b = bg / p.Hkv, g = bg % p.Hkv;
     const int64_t head0 = (int64_t)b * p.Hkv * G + (int64_t)g * G;
@@ -289,7 +324,7 @@ __device__ void finish_cta(const View& p, int64_t NB, int grid, int t, int nt, i
                 }
             if (merge_run_fast(p, bg, list, n, t)) continue;
         }
-        merge_run(p, bg, NB, grid, t, nt, bar, ms);
+        merge_run(p, bg, ms->rs[k], ms->re[k], NB, grid, t, nt, bar, ms);
     }
 }
 
@@ -327,7 +362,8 @@ struct TmaCfg {
     static constexpr size_t WM = WO + (size_t)kCWarps * 8 * WO_LD * sizeof(float);
     static constexpr size_t WL = WM + kCWarps * 8 * sizeof(float);
     static constexpr size_t MRG = WL + kCWarps * 8 * sizeof(float);
-    static constexpr size_t TOTAL = MRG + sizeof(MergeSmem<8>) + 1024;  // + alignment slack
+    static constexpr size_t STARTS = MRG + sizeof(MergeSmem<8>);
+    static constexpr size_t TOTAL = STARTS + (kMaxPrefix + 1) * sizeof(int32_t) + 1024;  // + align slack
 };
 
 template <int D>
@@ -345,6 +381,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
     float* wm = reinterpret_cast<float*>(smem + C::WM);
     float* wl = reinterpret_cast<float*>(smem + C::WL);
     MergeSmem<8>* ms = reinterpret_cast<MergeSmem<8>*>(smem + C::MRG);
+    int32_t* s_start = reinterpret_cast<int32_t*>(smem + C::STARTS);
+    __shared__ int s_wtmp[kTmaThreads / 32];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -355,9 +393,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
         ms->nruns = 0;
         fence_mbar_init();
     }
-    __syncthreads();
+    const int32_t* starts = run_starts(p, s_start, s_wtmp, tid, kTmaThreads);  // (syncs the CTA)
     const int grid = gridDim.x, cta = blockIdx.x;
-    const int64_t NB = __ldg(p.bg_start + p.n_bg);
+    const int64_t NB = starts[p.n_bg];
     const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
 
     if (warp == kProducer) {
@@ -372,10 +410,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
 #endif
         uint32_t ph = 0;
         int64_t x = r0;
-        int bg = r0 < r1 ? find_bg_warp(p.bg_start, p.n_bg, r0, lane) : 0;
+        int bg = r0 < r1 ? find_bg_warp(starts, p.n_bg, r0, lane) : 0;
         while (x < r1) {
-            const int64_t s_bg = __ldg(p.bg_start + bg);
-            const int64_t next_bg = __ldg(p.bg_start + bg + 1);
+            const int64_t s_bg = starts[bg];
+            const int64_t next_bg = starts[bg + 1];
             const int64_t bg_end = min(r1, next_bg - p.pad);  // real boxes only
             if (x >= bg_end) {  // only virtual boxes of this run in our range
                 x = next_bg;
@@ -750,23 +788,26 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
 #define qs(h, d) qsm[(h) * D + (d)]
 #define sc(r, h) scm[(r) * G + (h)]
     __shared__ MergeSmem<kGenMaxG> ms;
+    __shared__ int32_t s_start[kMaxPrefix + 1];
+    __shared__ int s_wtmp[kGen / 32];
+    const int32_t* starts = run_starts(p, s_start, s_wtmp, t, kGen);
     const int grid = gridDim.x, cta = blockIdx.x;
-    const int64_t NB = __ldg(p.bg_start + p.n_bg);
+    const int64_t NB = starts[p.n_bg];
     const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
     if (r0 >= r1) return;
     if (t == 0) ms.nruns = 0;
     const float scale = rsqrtf((float)D);
     float acc[kGenMaxG][2];
-    int bg = find_bg(p.bg_start, p.n_bg, r0);
-    int64_t s_bg = __ldg(p.bg_start + bg), e_bg = __ldg(p.bg_start + bg + 1);
+    int bg = find_bg(starts, p.n_bg, r0);
+    int64_t s_bg = starts[bg], e_bg = starts[bg + 1];
     bool fresh = true;
     for (int64_t x = r0; x < r1; ++x) {
         while (x >= e_bg - p.pad) {  // range starts in (or reaches) virtual boxes
             x = e_bg;
             if (x >= r1) goto done;
             ++bg;
-            s_bg = __ldg(p.bg_start + bg);
-            e_bg = __ldg(p.bg_start + bg + 1);
+            s_bg = starts[bg];
+            e_bg = starts[bg + 1];
             fresh = true;
         }
         if (fresh) {
@@ -865,8 +906,8 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
             if (x + 1 < r1) {
                 x = e_bg - 1;  // skip the run's virtual boxes
                 ++bg;
-                s_bg = __ldg(p.bg_start + bg);
-                e_bg = __ldg(p.bg_start + bg + 1);
+                s_bg = starts[bg];
+                e_bg = starts[bg + 1];
                 fresh = true;
             }
         }
@@ -884,7 +925,8 @@ done:
 // ---------------------------------------------------------------------------
 // small kernels
 // ---------------------------------------------------------------------------
-__global__ void k_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done) {
+__global__ void k_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_count,
+                              int32_t* bg_done) {
     const int64_t nb = (n + kBoxRows - 1) / kBoxRows;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < nb) {
@@ -897,6 +939,7 @@ __global__ void k_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t*
     if (j == 0) {
         bg_start[0] = 0;
         bg_start[1] = (int32_t)nb;
+        bg_count[0] = (int32_t)nb;
         bg_done[0] = 0;
     }
 }
@@ -958,6 +1001,7 @@ View make_view(const AttendArgs& a) {
     v.boxes = a.boxes;
     v.box_stride = a.box_stride;
     v.bg_start = a.bg_start;
+    v.bg_count = a.bg_count;
     v.pad = a.pad;
     v.part_o = a.part_o;
     v.part_lse = a.part_lse;
@@ -1050,10 +1094,10 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
     return 1;
 }
 
-void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done,
-                        cudaStream_t s) {
+void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_count,
+                        int32_t* bg_done, cudaStream_t s) {
     const int64_t nb = std::max<int64_t>(1, cdiv(n, kBoxRows));
-    k_index_boxes<<<(unsigned)cdiv(nb, 256), 256, 0, s>>>(n, boxes, bg_start, bg_done);
+    k_index_boxes<<<(unsigned)cdiv(nb, 256), 256, 0, s>>>(n, boxes, bg_start, bg_count, bg_done);
     FX_CUDA(cudaGetLastError());
 }
 

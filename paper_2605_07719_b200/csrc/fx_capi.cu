@@ -664,6 +664,7 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         aa.boxes = s.boxes;
         aa.box_stride = s.box_stride;
         aa.bg_start = s.bg_start;
+        aa.bg_count = s.bg_count;
         aa.pad = fx::kRunPad;  // the worklist prefix includes kRunPad per run
         aa.part_o = s.part_o;
         aa.part_lse = s.part_lse;
@@ -700,7 +701,8 @@ int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void
         const int64_t nb = fx::cdiv(n, fx::kBoxRows);
         const int grid = (int)std::min<int64_t>(nb, (int64_t)ctx->num_sms * 4);
         Carve c;
-        const size_t ob = c.take<fx::Box>(nb), os = c.take<int32_t>(2), od = c.take<int32_t>(2);
+        const size_t ob = c.take<fx::Box>(nb), os = c.take<int32_t>(2), od = c.take<int32_t>(2),
+                     oc = c.take<int32_t>(2);
         const size_t oo = c.take<float>((size_t)(grid + 1) * dim), ol = c.take<float>(grid + 1);
         ctx->api.ensure(c.off);
         char* b = static_cast<char*>(ctx->api.p);
@@ -713,13 +715,14 @@ int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void
         aa.boxes = reinterpret_cast<fx::Box*>(b + ob);
         aa.box_stride = nb;
         aa.bg_start = reinterpret_cast<int32_t*>(b + os);
+        aa.bg_count = reinterpret_cast<int32_t*>(b + oc);
         aa.part_o = reinterpret_cast<float*>(b + oo);
         aa.part_lse = reinterpret_cast<float*>(b + ol);
         aa.bg_done = reinterpret_cast<int32_t*>(b + od);
         aa.o = o;
         aa.lse = lse;
         fx::launch_index_boxes(n, const_cast<fx::Box*>(aa.boxes), const_cast<int32_t*>(aa.bg_start),
-                               aa.bg_done, ctx->stream);
+                               const_cast<int32_t*>(aa.bg_count), aa.bg_done, ctx->stream);
         ctx->launches += 1 + fx::launch_attend(aa, grid, false, ctx->stream);
     });
 }

@@ -19,6 +19,9 @@ constexpr int kBoxRows = 16;
 // ~this many boxes of streaming, so CTAs covering many short runs get fewer
 // boxes.  Virtual boxes are never loaded.
 constexpr int kRunPad = 16;
+// Batches up to this many (b, g) runs get their run starts rebuilt in smem
+// by the attention kernels from the worklist's per-run counts.
+constexpr int kMaxRunPrefix = 1024;
 // Candidate granularities, selector.hpp:12.
 constexpr int kLevels[4] = {16, 32, 64, 128};
 
@@ -131,7 +134,8 @@ struct AttendArgs {
     const uint32_t* idx;      // index boxes (API path) or nullptr
     const Box* boxes;         // [n_bg][box_stride]
     int64_t box_stride;
-    const int32_t* bg_start;  // [n_bg + 1] exclusive prefix of (box count + pad)
+    const int32_t* bg_start;  // [n_bg + 1] exclusive prefix of (box count + pad), for n_bg > 1024
+    const int32_t* bg_count;  // [n_bg] box counts (run starts rebuilt in smem for n_bg <= 1024)
     int pad;                  // virtual boxes at the end of each run (kRunPad or 0)
     float* part_o;            // [(grid + n_bg)][G][D]
     float* part_lse;          // [(grid + n_bg)][G]
@@ -143,8 +147,8 @@ bool attend_uses_tma(const fx_layout& L, bool has_idx);
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms);
 // returns the number of kernels launched
 int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s);
-void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_done,
-                        cudaStream_t s);
+void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_count,
+                        int32_t* bg_done, cudaStream_t s);
 void launch_merge_partials(int n, int dim, const float* o_parts, const float* lse_parts, float* o,
                            float* lse, cudaStream_t s);
 void launch_append(const fx_layout& L, void* k, void* v, int64_t row, const float* kn,

@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(256) k_worklist(int Hkv, int G, int64_t l_sink
         }
     }
     if (t == 0) bg_count[bg] = (int32_t)total;
+    if (n_bg <= kMaxRunPrefix) return;  // the attention kernels rebuild the run starts from the counts
     __threadfence();
     __syncthreads();
     if (t == 0) s_last = atomicAdd(&done[n_bg], 1) == n_bg - 1;

@@ -233,8 +233,9 @@ def test_spec_known_answers(engine):
 # ---------------------------------------------------------------------------
 # the batched decode step (K5 -> K2 -> K3/K4)
 # ---------------------------------------------------------------------------
-def _check_step(dec, host, q, coracle, blk_of, budgets_of, dtype, n_new=0):
-    """Selection bit-exact per head + output within tolerance per head."""
+def _check_step(dec, host, q, coracle, blk_of, budgets_of, dtype, n_new=0, groups=None):
+    """Selection bit-exact per head + output within tolerance per head (all
+    groups, or the listed (b, g))."""
     lay = dec.lay
     G, D = lay.group_size, lay.head_dim
     l_sink, l_cpu, l_local = lay.l_sink, lay.l_cpu, lay.l_local
@@ -242,6 +243,8 @@ def _check_step(dec, host, q, coracle, blk_of, budgets_of, dtype, n_new=0):
     lse = dec.lse.cpu().numpy()
     near_ties = 0
     for (b, g), (k, v) in host.items():
+        if groups is not None and (b, g) not in groups:
+            continue
         blk = blk_of(b, g)
         buds = budgets_of(b, g)
         kc = k[l_sink:l_sink + l_cpu]
@@ -283,6 +286,17 @@ def test_decode_step_shapes(engine, coracle, G, D):
     torch.cuda.synchronize()
     _check_step(dec, host, q, coracle, lambda b, g: 32, lambda b, g: [0.06] * G, "bf16",
                 n_new=5)
+
+
+def test_decode_step_many_groups_global_prefix(engine, coracle):
+    """> 1024 (b, g) runs: the worklist publishes the global run prefix and the
+    attention kernel reads it instead of rebuilding it in shared memory."""
+    B, Hkv, G, D = 130, 8, 4, 128
+    dec, host, q = make_decoder(engine, B, Hkv, G, D, 16, 300, 32, "bf16", seed=5)
+    dec.step(torch.as_tensor(q).cuda(), fixed=(16, 0.1))
+    torch.cuda.synchronize()
+    _check_step(dec, host, q, coracle, lambda b, g: 16, lambda b, g: [0.1] * G, "bf16",
+                groups=[(0, 0), (64, 3), (129, 7)])
 
 
 def test_decode_step_props_plan(engine, coracle):
