@@ -71,6 +71,21 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the
+    committed `ncu --set full` extract (profiles/ncu_traffic.json, written by
+    profiles/summarize_ncu.py from the same bench command); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        for name, rec in t["kernels"].items():
+            if kernel in name:
+                return rec["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -342,7 +357,7 @@ def run_ours(a):
         result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3+K4)",
                               "achieved": achieved, "peak": peak, "unit": "GB/s",
                               "frac": achieved / peak, "peak_kind": peak_kind,
-                              "traffic": None,
+                              "traffic": ncu_traffic("k_attend"),
                               "algorithmic_bytes_per_launch": attend_b / a.steps}
         score_ms = kt.get("score", float("nan"))
         step_bytes = (meta_b + attend_b) / a.steps

@@ -25,6 +25,27 @@ METRICS = [
 ]
 
 
+def traffic_json(path, out):
+    """Per-kernel DRAM bytes per launch (read + write) from a --set full report."""
+    import json
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    acc = defaultdict(list)
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(m)
+            b += float(r[i].replace(",", "")) * scale[units[i]]
+        acc[name].append(b)
+    json.dump({"source": path, "metric": "dram__bytes_read.sum + dram__bytes_write.sum",
+               "kernels": {k: {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v)}
+                           for k, v in acc.items()}}, open(out, "w"), indent=1)
+
+
 def full_report(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -50,6 +71,9 @@ def full_report(path):
     print()
 
 
+STEP_KERNELS = ("k_prepare", "k_score", "k_select", "k_worklist", "k_attend", "k_append", "k_approx")
+
+
 def launch_list(path):
     lines = [ln for ln in open(path) if ln.startswith('"')]  # drop ncu's ==PROF== chatter
     rows = list(csv.DictReader(lines))
@@ -59,10 +83,11 @@ def launch_list(path):
         key = (r["ID"], r["Kernel Name"].split("(")[0].replace("void ", ""))
         by[key][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
     for (i, name), m in by.items():
-        t[name].append(m)
+        if any(k in name for k in STEP_KERNELS):  # setup (KV generation, metadata) is not the step
+            t[name].append(m)
     tot = sum(m.get("gpu__time_duration.sum", 0) for v in t.values() for m in v)
     print(f"## launch list (cold-cache, serialised): {path}\n")
-    print("| kernel | launches | mean time | share of step | DRAM read/launch |")
+    print("| kernel | launches | mean time (ns) | share of step | DRAM read/launch |")
     print("|---|---|---|---|---|")
     for name, v in sorted(t.items(), key=lambda kv: -sum(m.get("gpu__time_duration.sum", 0) for m in kv[1])):
         s = sum(m.get("gpu__time_duration.sum", 0) for m in v)
@@ -72,7 +97,11 @@ def launch_list(path):
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
+    args = sys.argv[1:]
+    if args and args[0] == "--traffic":
+        traffic_json(args[1], args[2])
+        sys.exit(0)
+    for p in args:
         if p.endswith(".ncu-rep"):
             full_report(p)
         else:
