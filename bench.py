@@ -9,7 +9,7 @@ synthetic N(0,1) K/V generated on device.  Budgets: per-head properties
 SURVEY §8d perf run) -> on-device plan_group picks each group's granularity
 (16/32/64/128) and per-head budgets every step.
 
-One timed step = K5 plan -> K2 score/select -> worklist -> K3/K4 sparse GQA
+One timed step = K5 plan -> K2 score/select (+ fused worklist) -> K3/K4 sparse GQA
 attention + fused LSE merge for all 512 heads of the batch, plus the append of
 the step's new K/V row of every group.  Per-step working set is > 1 GB, far
 above the 126 MB L2, so no flush is needed between steps.

@@ -236,6 +236,23 @@ __device__ void merge_run(const View& p, int bg, int64_t s, int64_t e, int64_t N
     named_bar_sync(bar, nt);
 }
 
+// Runs with no real boxes (a context-parallel shard whose group selected
+// nothing there and holds no default rows; a streaming group without defaults)
+// reach no tile.  Their output is the merge identity -- o = 0, lse = -inf
+// (merge_into with an empty partial, attention.cpp:89-104) -- written by the
+// CTA whose range holds the run's first (virtual) box.
+__device__ void write_empty_runs(const View& p, const int32_t* starts, int64_t r0, int64_t r1,
+                                 int t, int nt) {
+    if (r0 >= r1) return;
+    for (int bg = find_bg(starts, p.n_bg, r0); bg < p.n_bg && starts[bg] < r1; ++bg) {
+        if (starts[bg] < r0 || starts[bg + 1] - starts[bg] > p.pad) continue;
+        const int64_t head0 = (int64_t)(bg / p.Hkv) * p.Hkv * p.G + (int64_t)(bg % p.Hkv) * p.G;
+        for (int i = t; i < p.G * p.D; i += nt) p.o[head0 * p.D + i] = 0.f;
+        if (p.lse)
+            for (int h = t; h < p.G; h += nt) p.lse[head0 + h] = -INFINITY;
+    }
+}
+
 // End of a CTA's range.  Runs wholly inside the CTA were written final at
 // their flush; only the (at most two) runs cut by the range ends left
 // partials.  Count this CTA in for each; the last contributor merges.  Done
@@ -561,7 +578,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
         ++tiles;
         runs += (hdr[st].flags & F_FIRST) ? 1 : 0;
 #endif
+        // everything the flush needs from the header is read before this warp
+        // releases the stage: once all warps arrive on empty[st] the producer
+        // refills hdr[st] with a later tile
         const int bg = hdr[st].bg, nb = hdr[st].nb;
+        const int run_s = hdr[st].s, run_e = hdr[st].e;
         const int i0 = warp * kBPW;          // this warp's boxes: i0, i0 + 1
         const Box bxa = hdr[st].box[i0];
         const Box bxb = hdr[st].box[i0 + 1];
@@ -719,8 +740,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
             const bool sole = flags & F_SOLE;
             if (!sole && tid == 0) {
                 ms->runs[ms->nruns] = bg;
-                ms->rs[ms->nruns] = hdr[st].s;
-                ms->re[ms->nruns] = hdr[st].e;
+                ms->rs[ms->nruns] = run_s;
+                ms->re[ms->nruns] = run_e;
                 ++ms->nruns;
             }
             const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * p.G + (int64_t)(bg % p.Hkv) * p.G
@@ -755,6 +776,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
             ph ^= 1u;
         }
     }
+    write_empty_runs(p, starts, r0, r1, tid, kCWarps * 32);
     finish_cta(p, NB, grid, tid, kCWarps * 32, 1, ms, true);
 #ifdef FX_TRACE
     if (tid == 0) {
@@ -914,6 +936,7 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
     }
 done:
     __syncthreads();
+    write_empty_runs(p, starts, r0, r1, t, kGen);
     finish_cta(p, NB, grid, t, kGen, 1, &ms, false);
 }
 

@@ -1,11 +1,13 @@
 // fx_capi.cu -- the C-ABI (include/fluxattn_b200.h): context, device scratch,
 // and the entry points that sequence the K1..K5 kernels.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
 
 #include "fx_internal.h"
+#include "fx_worklist.cuh"
 
 namespace {
 thread_local std::string g_last_error;
@@ -165,7 +167,7 @@ struct StepScratch {
     int64_t box_stride;
     int32_t* bg_count;
     int32_t* bg_start;
-    int32_t* bg_done;
+    int32_t* bg_done;  // [2 n_bg + 1]: attend counters | publish counter | select counters
     float* part_o;
     float* part_lse;
 };
@@ -189,7 +191,7 @@ StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
     const size_t o_box = c.take<fx::Box>(n_bg * box_stride);
     const size_t o_cnt = c.take<int32_t>(n_bg);
     const size_t o_st = c.take<int32_t>(n_bg + 1);
-    const size_t o_dn = c.take<int32_t>(n_bg + 1);
+    const size_t o_dn = c.take<int32_t>(2 * n_bg + 1);
     const size_t o_po = c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
     const size_t o_pl = c.take<float>((grid + n_bg) * L.group_size);
     if (alloc) ctx->step.ensure(c.off);
@@ -233,7 +235,7 @@ size_t step_bytes(const fx_layout& L, int grid) {
     c.take<fx::Box>(n_bg * box_stride);
     c.take<int32_t>(n_bg);
     c.take<int32_t>(n_bg + 1);
-    c.take<int32_t>(n_bg + 1);
+    c.take<int32_t>(2 * n_bg + 1);
     c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
     c.take<float>((grid + n_bg) * L.group_size);
     return c.off;
@@ -256,9 +258,11 @@ struct Planned {
     double* budgets;
     int32_t* kblocks;
     int launches;
+    bool fused;  // the worklist ran inside k_select
 };
+// wl != nullptr: fuse the worklist into the selection kernel (Planned.fused).
 Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, StepScratch& s,
-                        bool need_meta_for_select) {
+                        bool need_meta_for_select, const fx::WorklistArgs* wl = nullptr) {
     FX_REQUIRE(a->l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + a->l_new <= L.l_cap,
                FX_ERR_INVALID, "bad-shape: decoded rows exceed l_cap");
     FX_REQUIRE(a->plan_mode >= FX_PLAN_PROPS && a->plan_mode <= FX_PLAN_GIVEN, FX_ERR_INVALID,
@@ -303,6 +307,7 @@ Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, 
                            a->plan_cand_volumes, p.kblocks, s.bg_done, st);
     }
     p.launches = 1;
+    p.fused = false;
     if (sparse && !given_sel) {
         {
             Timed tm(ctx, FX_KERNEL_SCORE);
@@ -311,8 +316,17 @@ Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, 
         }
         {
             Timed tm(ctx, FX_KERNEL_SELECT);
+            fx::WorklistArgs w{};
+            if (wl) {
+                w = *wl;
+                w.blk = p.blk;
+                w.sel_bits = s.sel_bits;
+                w.sel_words = s.sel_words;
+            }
             fx::launch_select(L, a->meta, a->absmax, a->q, p.blk, p.kblocks, s.approx,
-                              s.approx_stride, s.sel_bits, s.sel_words, s.cand_keys, s.cand_ids, st);
+                              s.approx_stride, s.sel_bits, s.sel_words, s.cand_keys, s.cand_ids, st,
+                              wl ? &w : nullptr, s.bg_done + (int64_t)L.batch * L.kv_heads + 1);
+            p.fused = wl != nullptr;
         }
         p.launches += 2;
     } else if (!sparse) {
@@ -646,14 +660,20 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         const fx_layout& L = *lay;
         const int grid = fx::attend_grid(L, false, ctx->num_sms);
         StepScratch s = carve_step(ctx, L, grid, true);
-        const Planned pl = plan_and_select(ctx, L, a, s, false);
+        const int n_bg = L.batch * L.kv_heads;
+        const fx::WorklistArgs wl{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + a->l_new,
+                                  nullptr, nullptr, 0, s.boxes, s.box_stride, s.bg_count,
+                                  s.bg_start, s.bg_done + n_bg};
+        static const bool no_fuse = std::getenv("FX_DEBUG_NO_FUSED_WORKLIST") != nullptr;
+        const Planned pl = plan_and_select(ctx, L, a, s, false, no_fuse ? nullptr : &wl);
         int32_t* blk = pl.blk;
         int n = pl.launches;
         cudaStream_t st = ctx->stream;
-        {
+        if (!pl.fused) {
             Timed tm(ctx, FX_KERNEL_WORKLIST);
             fx::launch_worklist(L, a->l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
                                 s.bg_count, s.bg_start, s.bg_done, st);
+            n += 1;
         }
         fx::AttendArgs aa{};
         aa.L = L;
@@ -675,7 +695,6 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
             Timed tm(ctx, FX_KERNEL_ATTEND);
             n += fx::launch_attend(aa, grid, true, st);
         }
-        n += 1;  // worklist
         ctx->launches += n;
     });
 }

@@ -105,10 +105,14 @@ double approx_eps_scale(const fx_layout& L);
 void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
                           const int32_t* blk, const int32_t* kblocks, float* approx,
                           int64_t approx_stride, int num_sms, cudaStream_t s);
+struct WorklistArgs;
+// wl != nullptr: the selection kernel also builds the attention boxes (fused
+// worklist); sel_done = [n_bg] per-group head counters, zeroed by k_prepare.
 void launch_select(const fx_layout& L, const void* const meta[4], const float* absmax,
                    const float* q, const int32_t* blk, const int32_t* kblocks,
                    const float* approx, int64_t approx_stride, uint32_t* sel_bits, int sel_words,
-                   uint64_t* cand_keys, uint32_t* cand_ids, cudaStream_t s);
+                   uint64_t* cand_keys, uint32_t* cand_ids, cudaStream_t s,
+                   const WorklistArgs* wl = nullptr, int32_t* sel_done = nullptr);
 void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
                      const uint32_t* sel_bits, int sel_words, Box* boxes, int64_t box_stride,
                      int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s);

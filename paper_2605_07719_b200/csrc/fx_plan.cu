@@ -46,8 +46,9 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
     const bool act = h < G;
     const int64_t head = (int64_t)bg * G + h;
     if (h == 0 && bg_done) {
-        bg_done[bg] = 0;
-        if (bg == 0) bg_done[n_bg] = 0;  // worklist completion counter
+        bg_done[bg] = 0;                 // attention contributors of (b, g)
+        bg_done[n_bg + 1 + bg] = 0;      // selected heads of (b, g) (fused worklist)
+        if (bg == 0) bg_done[n_bg] = 0;  // worklist publish counter
     }
     int blk = 0;
     double bud = 0.0, vol = 0.0, cv[4] = {0, 0, 0, 0};

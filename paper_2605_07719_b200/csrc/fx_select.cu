@@ -3,168 +3,26 @@
 // ordered top-k).  Scoring lives in fx_score.cu, selection in fx_topk.cu.
 #include <algorithm>
 
-#include "fx_common.cuh"
+#include "fx_worklist.cuh"
 
 namespace fx {
 namespace {
 
 constexpr int kMaxWords = 4096;      // nblk <= 131072 per (b, g) at the chosen blk
 
-// Exclusive block scan of cnt[0..n) in place; returns the total.
-__device__ int64_t block_exclusive_scan(int32_t* cnt, int n, int64_t* wsum) {
-    const int t = threadIdx.x, nt = blockDim.x;
-    const int per = (n + nt - 1) / nt;
-    const int a = min(n, t * per), e = min(n, a + per);
-    int64_t s = 0;
-    for (int i = a; i < e; ++i) s += cnt[i];
-    wsum[t] = s;
-    __syncthreads();
-    if (t < 32) {  // warp scan of the nt partial sums
-        int64_t run = 0;
-        for (int base = 0; base < nt; base += 32) {
-            const int i = base + t;
-            const int64_t v = i < nt ? wsum[i] : 0;
-            int64_t x = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (t >= o) x += y;
-            }
-            if (i < nt) wsum[i] = run + x - v;
-            run += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (t == 0) wsum[nt] = run;
-    }
-    __syncthreads();
-    int64_t run = wsum[t];
-    for (int i = a; i < e; ++i) {
-        const int32_t v = cnt[i];
-        cnt[i] = (int32_t)run;
-        run += v;
-    }
-    __syncthreads();
-    return wsum[nt];
-}
-
 // ---------------------------------------------------------------------------
-// worklist: union of the group's selections -> 16-row boxes with head masks
+// worklist: union of the group's selections -> 16-row boxes with head masks.
+// Standalone only when no k_select ran this step (given selection / empty cpu
+// segment); otherwise the selection kernel's fused tail builds the boxes.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_worklist(int Hkv, int G, int64_t l_sink, int64_t l_cpu,
-                                                  int64_t l_tail, const int32_t* __restrict__ blk_arr,
-                                                  const uint32_t* __restrict__ sel_bits,
-                                                  int sel_words, Box* __restrict__ boxes,
-                                                  int64_t box_stride,
-                                                  int32_t* __restrict__ bg_count,
-                                                  int32_t* __restrict__ bg_start,
-                                                  int32_t* __restrict__ done, int stage_words) {
+__global__ void __launch_bounds__(256) k_worklist(WorklistArgs w, int stage_words) {
     pdl_wait();
     pdl_trigger();
     __shared__ int32_t wcnt[kMaxWords];
     __shared__ int64_t wsum[257];
-    __shared__ int s_last;
-    __shared__ int wtot[8];
-    const int bg = blockIdx.x, n_bg = gridDim.x;
-    const int b = bg / Hkv, g = bg % Hkv;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int blk = blk_arr[bg];
-    const uint16_t all = (uint16_t)((1u << G) - 1u);
-    Box* out = boxes + (int64_t)bg * box_stride;
-    // defaults: sink, then local + decoded rows (attention.cpp:143-151)
-    const int nb_s = (int)cdiv_dev(l_sink, kBoxRows);
-    const int nb_t = (int)cdiv_dev(l_tail, kBoxRows);
-    for (int i = t; i < nb_s + nb_t; i += blockDim.x) {
-        Box bx;
-        if (i < nb_s) {
-            bx.row = i * kBoxRows;
-            bx.n = (uint16_t)min((int64_t)kBoxRows, l_sink - (int64_t)i * kBoxRows);
-        } else {
-            const int r = i - nb_s;
-            bx.row = (int32_t)(l_sink + l_cpu + (int64_t)r * kBoxRows);
-            bx.n = (uint16_t)min((int64_t)kBoxRows, l_tail - (int64_t)r * kBoxRows);
-        }
-        bx.mask = all;
-        out[i] = bx;
-    }
-    const int nd = nb_s + nb_t;
-    int64_t total = nd;
-    if (blk > 0) {
-        const int64_t nblk = cdiv_dev(l_cpu, blk);
-        const int W = (int)cdiv_dev(nblk, 32);
-        const int bpb = blk / kBoxRows;
-        const int64_t last = nblk - 1;
-        const int nb_last = (int)cdiv_dev(l_cpu - last * blk, kBoxRows);
-        const uint32_t* hg = sel_bits + ((int64_t)b * Hkv * G + (int64_t)g * G) * sel_words;
-        // stage the group's G selection masks in smem (all loads in flight at once)
-        extern __shared__ uint32_t s_bits[];
-        const bool staged = (int64_t)G * W <= stage_words;
-        if (staged) {
-#pragma unroll 4
-            for (int i = t; i < G * W; i += blockDim.x) s_bits[i] = hg[(int64_t)(i / W) * sel_words + i % W];
-            __syncthreads();
-        }
-        const uint32_t* hb = staged ? s_bits : hg;
-        const int64_t hstride = staged ? W : sel_words;
-        for (int j = t; j < W; j += blockDim.x) {
-            uint32_t u = 0;
-            for (int h = 0; h < G; ++h) u |= hb[(int64_t)h * hstride + j];
-            int c = __popc(u) * bpb;
-            if ((last >> 5) == j && ((u >> (last & 31)) & 1u)) c -= bpb - nb_last;
-            wcnt[j] = c;
-        }
-        __syncthreads();
-        total += block_exclusive_scan(wcnt, W, wsum);
-        for (int j = warp; j < W; j += blockDim.x / 32) {
-            uint32_t u = 0, m = 0;  // union word; head mask of this lane's block
-            for (int h = 0; h < G; ++h) {
-                const uint32_t w = hb[(int64_t)h * hstride + j];
-                u |= w;
-                m |= ((w >> lane) & 1u) << h;
-            }
-            if ((u >> lane) & 1u) {
-                const int i = j * 32 + lane;
-                const int r0 = i * blk;  // < 2^31 (checked by the launcher)
-                const int len = min(blk, (int)(l_cpu - r0));
-                const int nb = (len + kBoxRows - 1) >> 4;
-                const int64_t o = nd + wcnt[j] + (int64_t)__popc(u & ((1u << lane) - 1u)) * bpb;
-                const int row0 = (int)l_sink + r0;
-                for (int x = 0; x < nb; ++x) {
-                    Box bx;
-                    bx.row = row0 + x * kBoxRows;
-                    bx.n = (uint16_t)min(kBoxRows, len - x * kBoxRows);
-                    bx.mask = (uint16_t)m;
-                    out[o + x] = bx;
-                }
-            }
-        }
-    }
-    if (t == 0) bg_count[bg] = (int32_t)total;
-    if (n_bg <= kMaxRunPrefix) return;  // the attention kernels rebuild the run starts from the counts
-    __threadfence();
-    __syncthreads();
-    if (t == 0) s_last = atomicAdd(&done[n_bg], 1) == n_bg - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // last CTA: exclusive prefix of box counts over (b, g)
-    for (int i0 = 0, run = 0; i0 < n_bg; i0 += blockDim.x) {
-        const int i = i0 + t;
-        int v = i < n_bg ? __ldcg(bg_count + i) + kRunPad : 0;  // + virtual run cost
-        // block inclusive scan of v
-        int x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) wtot[warp] = x;
-        __syncthreads();
-        int wo = 0;
-        for (int w = 0; w < warp; ++w) wo += wtot[w];
-        int ctot = 0;
-        for (int w = 0; w < 8; ++w) ctot += wtot[w];
-        if (i < n_bg) bg_start[i] = run + wo + x - v;
-        run += ctot;
-        __syncthreads();
-        if (i0 + (int)blockDim.x >= n_bg && t == 0) bg_start[n_bg] = run;
-    }
+    extern __shared__ uint32_t s_bits[];
+    worklist_group(w, blockIdx.x, wcnt, wsum, s_bits, stage_words);
+    worklist_publish(w, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -231,9 +89,9 @@ void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
     const int stage_words = (int)std::min<int64_t>(want, 24576);
     const size_t smem = (size_t)stage_words * 4;
     FX_CUDA(cudaFuncSetAttribute(k_worklist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_pdl(k_worklist, n_bg, 256, smem, s, L.kv_heads, L.group_size, L.l_sink, L.l_cpu,
-                                       L.l_local + l_new, blk, sel_bits, sel_words, boxes, box_stride,
-                                       bg_count, bg_start, done, stage_words);
+    const WorklistArgs w{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + l_new, blk, sel_bits,
+                         sel_words, boxes, box_stride, bg_count, bg_start, done + n_bg};
+    launch_pdl(k_worklist, n_bg, 256, smem, s, w, stage_words);
     FX_CUDA(cudaGetLastError());
 }
 

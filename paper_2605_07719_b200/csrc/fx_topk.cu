@@ -17,7 +17,7 @@
 // Output: the selection as a bitmask over the group's blocks.
 #include <algorithm>
 
-#include "fx_common.cuh"
+#include "fx_worklist.cuh"
 
 namespace fx {
 namespace {
@@ -104,14 +104,12 @@ __device__ __forceinline__ double exact_score_smem(const double* qs, const float
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kT) k_select(
+__device__ __forceinline__ void select_head(
     MetaPtrs meta, const float* __restrict__ absmax, const float* __restrict__ q,
     const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int Hkv, int G,
     int D, int64_t l_cpu, const float* __restrict__ approx, int64_t astride, double eps_scale,
     uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap) {
-    pdl_wait();
-    pdl_trigger();
     using T = typename Elem<DT>::T;
     // dynamic smem: keys[keys_cap] f32 | hist[kBins] | q[D] f64 | ck[kSmallCand] | ci[kSmallCand]
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -383,6 +381,38 @@ __global__ void __launch_bounds__(kT) k_select(
     SEL_MARK(5);
 }
 
+// One CTA per head.  With `wl.boxes` set, the CTA that completes the last head
+// of a group (sel_done[bg] reaches G) goes on to build that group's attention
+// boxes (fx_worklist.cuh) -- the union of the G selections is final then.
+template <int DT>
+__global__ void __launch_bounds__(kT) k_select(
+    MetaPtrs meta, const float* __restrict__ absmax, const float* __restrict__ q,
+    const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int Hkv, int G,
+    int D, int64_t l_cpu, const float* __restrict__ approx, int64_t astride, double eps_scale,
+    uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
+    uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap, WorklistArgs wl,
+    int32_t* __restrict__ sel_done, int stage_words) {
+    pdl_wait();
+    pdl_trigger();
+    select_head<DT>(meta, absmax, q, blk_arr, kblocks, Hkv, G, D, l_cpu, approx, astride,
+                    eps_scale, sel_bits, sel_words, cand_keys, cand_ids, cand_stride, keys_cap);
+    if (wl.boxes == nullptr) return;
+    __shared__ int s_last;
+    __shared__ int64_t s_wsum[kT + 1];
+    const int bg = (int)(blockIdx.x / G);
+    __threadfence();  // this head's bits visible before the group counter moves
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(sel_done + bg, 1) == G - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // dynamic smem (keys | histogram | ...) is free now: word counts, then staged masks
+    extern __shared__ __align__(16) unsigned char dsm[];
+    int32_t* wcnt = reinterpret_cast<int32_t*>(dsm);
+    worklist_group(wl, bg, wcnt, s_wsum, reinterpret_cast<uint32_t*>(dsm) + kMaxWords, stage_words);
+    worklist_publish(wl, (int)(gridDim.x / G));
+}
+
 }  // namespace
 
 double approx_eps_scale(const fx_layout& L);
@@ -390,7 +420,8 @@ double approx_eps_scale(const fx_layout& L);
 void launch_select(const fx_layout& L, const void* const meta[4], const float* absmax,
                    const float* q, const int32_t* blk, const int32_t* kblocks,
                    const float* approx, int64_t approx_stride, uint32_t* sel_bits, int sel_words,
-                   uint64_t* cand_keys, uint32_t* cand_ids, cudaStream_t s) {
+                   uint64_t* cand_keys, uint32_t* cand_ids, cudaStream_t s, const WorklistArgs* wl,
+                   int32_t* sel_done) {
     MetaPtrs mp{{meta[0], meta[1], meta[2], meta[3]}};
     FX_REQUIRE(level_blocks(L.l_cpu, 16) <= (int64_t)kMaxWords * 32, FX_ERR_INVALID,
                "bad-shape: cpu segment too long for one selection CTA");
@@ -398,19 +429,31 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
     const int64_t heads = (int64_t)L.batch * L.kv_heads * L.group_size;
     const int64_t nmax = level_blocks(L.l_cpu, 16);
     const int keys_cap = (int)((std::min<int64_t>(nmax, kSmemKeys) + 3) & ~int64_t(3));
-    const size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)L.head_dim * 8 +
-                        (size_t)kSmallCand * 12;
+    size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)L.head_dim * 8 +
+                  (size_t)kSmallCand * 12;
+    WorklistArgs w{};
+    int stage_words = 0;
+    if (wl) {
+        FX_REQUIRE(L.group_size <= 16, FX_ERR_INVALID, "bad-shape: group_size must be <= 16");
+        w = *wl;
+        // fused worklist: kMaxWords counts + the G staged masks (up to 96 KB) in the same smem
+        const int64_t want = (int64_t)L.group_size * cdiv(std::max<int64_t>(1, nmax), 32);
+        stage_words = (int)std::min<int64_t>(want, 24576);
+        smem = std::max(smem, (size_t)(kMaxWords + stage_words) * 4);
+    }
     const double eps = approx_eps_scale(L);
     if (L.dtype == FX_BF16) {
         FX_CUDA(cudaFuncSetAttribute(k_select<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        launch_pdl(k_select<FX_BF16>, (unsigned)heads, kT, smem, s, 
+        launch_pdl(k_select<FX_BF16>, (unsigned)heads, kT, smem, s,
             mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
-            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap);
+            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
+            w, sel_done, stage_words);
     } else {
         FX_CUDA(cudaFuncSetAttribute(k_select<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        launch_pdl(k_select<FX_F32>, (unsigned)heads, kT, smem, s, 
+        launch_pdl(k_select<FX_F32>, (unsigned)heads, kT, smem, s,
             mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
-            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap);
+            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
+            w, sel_done, stage_words);
     }
     FX_CUDA(cudaGetLastError());
 }

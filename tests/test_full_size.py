@@ -1,0 +1,233 @@
+"""Parity at BASELINE.json's full sizes.
+
+C2 (configs[1]): Llama layer, 128K context, batch 16, bf16, per-head budgets
+and per-group granularity from the on-device selector.  C3 (configs[2]):
+Qwen layer (28 q / 4 kv heads, G = 7), 256K context, batch 8.  C5
+(configs[4]): 1M context, batch 4, context-parallel over 8 shards (all on one
+GPU through LoopbackComm; tests/test_context_parallel_gloo.py covers the
+torch.distributed exchanges).
+
+KV is generated on the device; the oracle sees the exact bf16 bits of the
+sampled (b, g) groups (D2H, upcast to f32 -- SURVEY §8c bf16 recipe).
+Checked on every head of the batch (size-independent): the plan equals the
+oracle's plan_group bit-for-bit, each head selects exactly
+blocks_for_budget(...) blocks, outputs are finite.  Checked against the
+oracle on sampled groups: the selected block set bit-exact (mismatches only
+where the reference score gap is < 1e-6, reported), outputs within 2e-2
+(bf16), LSE within 1e-2.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+
+
+def _draw_props(B, H, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(0.01, 0.05, (B, H)), rng.uniform(0.0, 0.01, (B, H)),
+            (rng.random((B, H)) < 0.5).astype(np.int32))
+
+
+def _fill_kv(t, seed):
+    """N(0,1) bf16 K or V, generated per sequence to bound the f32 temporary."""
+    g = torch.Generator(device=t.device).manual_seed(seed)
+    for b in range(t.shape[0]):
+        t[b].copy_(torch.randn(t[b].shape, generator=g, device=t.device))
+
+
+def _queries(B, H, D, seed, dev):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    q = torch.randn((B, H, D), generator=g, device=dev)
+    q = q / q.norm(dim=-1, keepdim=True) * D ** 0.5
+    return q.bfloat16().float()
+
+
+def _decoder(engine, B, Hkv, G, D, l_cpu, seed, max_new=8):
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    l_sink, l_local = 64, 256
+    dec = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new=max_new, dtype="bf16")
+    _fill_kv(dec.k, seed)
+    _fill_kv(dec.v, seed + 1)
+    # planted needles (a few per group) so the selection is not a coin toss
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    for b in range(B):
+        for g in range(Hkv):
+            for _ in range(3):
+                s = l_sink + int(torch.randint(0, l_cpu - 16, (1,), generator=gen))
+                u = torch.randn(D, generator=gen)
+                dec.k[b, g, s:s + 16] += (3.0 * u / u.norm() * D ** 0.5 / 4).to(dec.k.device,
+                                                                               torch.bfloat16)
+    dec.build_metadata()
+    return dec
+
+
+def _group_host(dec, b, g):
+    lay = dec.lay
+    n = lay.l_sink + lay.l_cpu + lay.l_local + dec.l_new
+    return dec.k[b, g, :n].float().cpu().numpy(), dec.v[b, g, :n].float().cpu().numpy()
+
+
+def _check_plans(dec, coracle, props):
+    """Every group's plan bit-exact against plan_group (selector.cpp:19-46)."""
+    lay = dec.lay
+    G = lay.group_size
+    blk = dec.plan_blk.cpu().numpy()
+    bud = dec.plan_budgets.cpu().numpy()
+    kbl = dec.plan_kblocks.cpu().numpy()
+    bgt0, ks, st = props
+    for b in range(lay.batch):
+        for g in range(lay.kv_heads):
+            sl = slice(g * G, (g + 1) * G)
+            p = coracle.plan_group(bgt0[b, sl], ks[b, sl], st[b, sl], lay.l_cpu)
+            if p["streaming_group"]:
+                assert blk[b, g] == 0, (b, g)
+                continue
+            assert blk[b, g] == p["block_size"], (b, g)
+            assert np.array_equal(bud[b, sl], p["budgets"]), (b, g)
+            for hg in range(G):
+                assert kbl[b, g * G + hg] == coracle.blocks_for_budget(p["budgets"][hg], lay.l_cpu,
+                                                                      p["block_size"])
+
+
+def _check_counts(dec):
+    """popcount(selection bitmask) == plan_kblocks for every head."""
+    w = dec.sel_bits.view(torch.uint8).cpu().numpy()
+    cnt = np.unpackbits(w, axis=-1).sum(-1)
+    kb = dec.plan_kblocks.cpu().numpy()
+    blk = np.repeat(dec.plan_blk.cpu().numpy(), dec.lay.group_size, axis=1)
+    assert np.array_equal(np.where(blk > 0, cnt, 0), np.where(blk > 0, kb, 0))
+
+
+def _check_groups(dec, coracle, q, groups):
+    lay = dec.lay
+    G, l_sink, l_cpu, l_local = lay.group_size, lay.l_sink, lay.l_cpu, lay.l_local
+    o, lse = dec.o.cpu().numpy(), dec.lse.cpu().numpy()
+    qn = q.cpu().numpy()
+    near = 0
+    for b, g in groups:
+        k, v = _group_host(dec, b, g)
+        blk = int(dec.plan_blk[b, g].item())
+        buds = dec.plan_budgets[b, g * G:(g + 1) * G].cpu().numpy()
+        mins = maxs = None
+        if blk > 0:
+            mins, maxs = coracle.build_metadata(k[l_sink:l_sink + l_cpu], blk)
+            for hg in range(G):
+                h = g * G + hg
+                kb = coracle.blocks_for_budget(buds[hg], l_cpu, blk)
+                want, _ = coracle.topk_blocks(qn[b, h], mins, maxs, kb)
+                got = dec.selected_blocks(b, h)
+                if set(got.tolist()) != set(want.tolist()):
+                    gap = coracle.boundary_gap(qn[b, h], mins, maxs, kb)
+                    assert gap < 1e-6, f"selection mismatch (b={b}, h={h}, gap={gap})"
+                    near += 1
+        wo, wl, _ = coracle.execute_group(k, v, (l_sink, l_cpu, l_local, dec.l_new),
+                                          qn[b, g * G:(g + 1) * G], blk, buds, mins, maxs)
+        err = np.abs(o[b, g * G:(g + 1) * G] - wo).max() / max(1.0, np.abs(wo).max())
+        assert err < BF16_TOL, (b, g, err)
+        assert np.abs(lse[b, g * G:(g + 1) * G] - wl).max() < 1e-2, (b, g)
+    return near
+
+
+def _retrieval_groups(dec, n):
+    blk = dec.plan_blk.cpu().numpy()
+    idx = [(b, g) for b in range(blk.shape[0]) for g in range(blk.shape[1]) if blk[b, g] > 0]
+    pick = np.linspace(0, len(idx) - 1, n).round().astype(int)
+    return [idx[i] for i in sorted(set(pick.tolist()))]
+
+
+def test_c2_full_size_two_steps(engine, coracle):
+    """C2: 16 x 8 groups x 128K, props plan, two decode steps with an append."""
+    B, Hkv, G, D, l_cpu = 16, 8, 4, 128, 131072 - 320
+    dec = _decoder(engine, B, Hkv, G, D, l_cpu, seed=11)
+    props = _draw_props(B, Hkv * G, seed=1)
+    dprops = tuple(torch.as_tensor(x, device=engine.device) for x in props)
+    dev = engine.device
+    for step in range(2):
+        if step:
+            gen = torch.Generator(device=dev).manual_seed(100 + step)
+            dec.append(torch.randn((B, Hkv, D), generator=gen, device=dev).bfloat16().float(),
+                       torch.randn((B, Hkv, D), generator=gen, device=dev).bfloat16().float())
+        q = _queries(B, Hkv * G, D, seed=step, dev=dev)
+        dec.o.fill_(float("nan"))  # every head must be written this step
+        o, lse = dec.step(q, props=dprops)
+        torch.cuda.synchronize()
+        assert torch.isfinite(o).all() and torch.isfinite(lse).all()
+        _check_plans(dec, coracle, props)
+        _check_counts(dec)
+        near = _check_groups(dec, coracle, q, _retrieval_groups(dec, 3))
+        print(f"C2 step {step}: near-tie selection mismatches reported: {near}")
+
+
+def test_c2_full_budget_is_dense_attention(engine):
+    """FULL plan (pipeline.cpp:298-303) at 128K equals dense attention (torch f64)."""
+    B, Hkv, G, D, l_cpu = 16, 8, 4, 128, 131072 - 320
+    dec = _decoder(engine, B, Hkv, G, D, l_cpu, seed=21)
+    q = _queries(B, Hkv * G, D, seed=5, dev=engine.device)
+    o, lse = dec.step(q, full=True)
+    torch.cuda.synchronize()
+    for b, g in [(0, 0), (15, 7)]:
+        n = dec.lay.l_sink + l_cpu + dec.lay.l_local
+        k = dec.k[b, g, :n].double()
+        v = dec.v[b, g, :n].double()
+        qs = q[b, g * G:(g + 1) * G].double()
+        s = qs @ k.T / D ** 0.5
+        want_lse = torch.logsumexp(s, -1)
+        want = torch.softmax(s, -1) @ v
+        err = (o[b, g * G:(g + 1) * G].double() - want).abs().max() / max(1.0, want.abs().max())
+        assert err < BF16_TOL
+        assert (lse[b, g * G:(g + 1) * G].double() - want_lse).abs().max() < 1e-2
+
+
+def test_c3_full_size_qwen(engine, coracle):
+    """C3 shape: Qwen layer (28 q / 4 kv heads, G = 7), 256K, batch 8."""
+    B, Hkv, G, D, l_cpu = 8, 4, 7, 128, 262144 - 320
+    dec = _decoder(engine, B, Hkv, G, D, l_cpu, seed=31)
+    props = _draw_props(B, Hkv * G, seed=3)
+    q = _queries(B, Hkv * G, D, seed=7, dev=engine.device)
+    dec.o.fill_(float("nan"))
+    dec.step(q, props=tuple(torch.as_tensor(x, device=engine.device) for x in props))
+    torch.cuda.synchronize()
+    assert torch.isfinite(dec.o).all() and torch.isfinite(dec.lse).all()
+    _check_plans(dec, coracle, props)
+    _check_counts(dec)
+    _check_groups(dec, coracle, q, _retrieval_groups(dec, 3))
+
+
+def test_c5_full_size_context_parallel(engine, coracle):
+    """C5: 1M context, batch 4, 8 context-parallel shards -> the single-device
+    selection bit-exactly, outputs within the bf16 bound; one group checked
+    against the oracle at 1M."""
+    from paper_2605_07719_b200.context_parallel import CPShard, LoopbackComm, cp_decode_step, shard_kv
+    B, Hkv, G, D, R = 4, 8, 4, 128, 8
+    l_sink, l_cpu, l_local = 64, 1048576 - 320, 256
+    full = _decoder(engine, B, Hkv, G, D, l_cpu, seed=41, max_new=4)
+    shards = []
+    for r in range(R):
+        kr = shard_kv(full.k, l_sink, l_cpu, l_local, r, R, 4)
+        vr = shard_kv(full.v, l_sink, l_cpu, l_local, r, R, 4)
+        sh = CPShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16", k=kr, v=vr)
+        sh.dec.build_metadata()
+        shards.append(sh)
+    props = _draw_props(B, Hkv * G, seed=5)
+    dprops = tuple(torch.as_tensor(x, device=engine.device) for x in props)
+    q = _queries(B, Hkv * G, D, seed=9, dev=engine.device)
+    o_ref, lse_ref = full.step(q, props=dprops)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
+    for sh in shards:
+        sh.o.fill_(float("nan"))
+    (o, lse), *_ = cp_decode_step(shards, LoopbackComm(R), q, props=dprops)
+    torch.cuda.synchronize()
+    assert torch.isfinite(o_ref).all() and torch.isfinite(o).all() and not torch.isnan(lse).any()
+    for b in range(B):
+        for h in range(Hkv * G):
+            want = full.selected_blocks(b, h)
+            got = np.sort(np.concatenate([sh.global_selection(b, h) for sh in shards]))
+            assert np.array_equal(got, want), (b, h)
+    torch.testing.assert_close(o, o_ref, rtol=4e-3, atol=4e-3)
+    torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
+    _check_plans(full, coracle, props)
+    _check_groups(full, coracle, q, _retrieval_groups(full, 1))
