@@ -411,3 +411,247 @@ FXO_API void fxo_make_model(uint64_t seed, double* w1, double* b1, double* w2, d
         for (size_t o = 0; o < outs[l]; ++o) bs[l][o] = 0.0;
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Output-aware budget oracle -- budget_oracle.cpp:13-105, 149-172     */
+/* ------------------------------------------------------------------ */
+
+/* l2_norm / l2_distance over f64 (matrix.hpp:86-99): sequential sums. */
+static double fxo_l2_norm(const double* x, size_t n) {
+    double s = 0.0;
+    for (size_t i = 0; i < n; ++i) s += x[i] * x[i];
+    return sqrt(s);
+}
+static double fxo_l2_distance(const double* a, const double* b, size_t n) {
+    double s = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const double d = a[i] - b[i];
+        s += d * d;
+    }
+    return sqrt(s);
+}
+
+/* max_output_norm (budget_oracle.cpp:37-41): max_h ||o_h||. outs [n][dim]. */
+FXO_API double fxo_max_output_norm(const double* outs, size_t n, size_t dim) {
+    double m = 0.0;
+    for (size_t h = 0; h < n; ++h) {
+        const double x = fxo_l2_norm(outs + h * dim, dim);
+        if (m < x) m = x;
+    }
+    return m;
+}
+
+/* Segments of one group cache in the position layout sink | cpu | local | new. */
+typedef struct {
+    const float* k;
+    const float* v;
+    size_t dim, l_sink, l_cpu, l_local, l_new;
+} fxo_cache;
+
+/* default_kv_attention (attention.cpp:143-151): sink, local, new merged in
+ * that order.  Returns tokens (0 = empty). */
+static size_t fxo_default_partial(const fxo_cache* c, const float* q, double* o, double* lse,
+                                  double* part) {
+    const size_t off[3] = {0, c->l_sink + c->l_cpu, c->l_sink + c->l_cpu + c->l_local};
+    const size_t len[3] = {c->l_sink, c->l_local, c->l_new};
+    size_t tok = 0;
+    *lse = -INFINITY;
+    for (size_t j = 0; j < c->dim; ++j) o[j] = 0.0;
+    for (int s = 0; s < 3; ++s) {
+        if (len[s] == 0) continue;
+        double l;
+        const size_t t = fxo_gathered_attention(q, c->k + off[s] * c->dim, c->v + off[s] * c->dim,
+                                                c->dim, NULL, len[s], part, &l);
+        fxo_merge_into(o, lse, &tok, part, l, t, c->dim);
+    }
+    return tok;
+}
+
+/* cache_attention (attention.cpp:131-141): sink, cpu, local, new merged in
+ * position order.  o_full [dim].  Returns -1 on an empty cache. */
+FXO_API int fxo_cache_attention(const float* k, const float* v, size_t dim, size_t l_sink,
+                                size_t l_cpu, size_t l_local, size_t l_new, const float* q,
+                                double* o_full) {
+    const size_t off[4] = {0, l_sink, l_sink + l_cpu, l_sink + l_cpu + l_local};
+    const size_t len[4] = {l_sink, l_cpu, l_local, l_new};
+    double* part = (double*)malloc(dim * sizeof(double));
+    double lse = -INFINITY;
+    size_t tok = 0;
+    for (size_t j = 0; j < dim; ++j) o_full[j] = 0.0;
+    for (int s = 0; s < 4; ++s) {
+        if (len[s] == 0) continue;
+        double l;
+        const size_t t = fxo_gathered_attention(q, k + off[s] * dim, v + off[s] * dim, dim, NULL,
+                                                len[s], part, &l);
+        fxo_merge_into(o_full, &lse, &tok, part, l, t, dim);
+    }
+    free(part);
+    return tok == 0 ? -1 : 0;
+}
+
+/* reconstruction_deviation (budget_oracle.cpp:13-20). */
+static double fxo_deviation(const double* o, size_t tokens, const double* o_full, size_t dim,
+                            double normalizer) {
+    if (tokens == 0) return fxo_l2_norm(o_full, dim) / normalizer;
+    return fxo_l2_distance(o, o_full, dim) / normalizer;
+}
+
+/* label_streaming (budget_oracle.cpp:107-116): 1 = streaming.  Returns -1
+ * (degenerate-normalizer) when normalizer == 0 and the cpu segment is
+ * non-empty. */
+FXO_API int fxo_label_streaming(const float* k, const float* v, size_t dim, size_t l_sink,
+                                size_t l_cpu, size_t l_local, size_t l_new, const float* q,
+                                const double* o_full, double normalizer, double tau) {
+    if (l_cpu == 0) return 1;
+    if (normalizer == 0.0) return -1;
+    const fxo_cache c = {k, v, dim, l_sink, l_cpu, l_local, l_new};
+    double* o = (double*)malloc(dim * sizeof(double));
+    double* part = (double*)malloc(dim * sizeof(double));
+    double lse;
+    const size_t t = fxo_default_partial(&c, q, o, &lse, part);
+    const int r = fxo_deviation(o, t, o_full, dim, normalizer) <= tau;
+    free(o);
+    free(part);
+    return r;
+}
+
+
+/* min_budget (budget_oracle.cpp:54-105).  Scans block prefixes in score
+ * order; the first whose reconstruction deviation is <= tau wins.
+ * Outputs budget (realized token fraction), blocks, saturated.  Returns -1
+ * when normalizer == 0 (degenerate-normalizer), -2 on a bad granularity. */
+FXO_API int fxo_min_budget(const float* k, const float* v, size_t dim, size_t l_sink, size_t l_cpu,
+                           size_t l_local, size_t l_new, const float* q, int blk,
+                           const double* o_full, double normalizer, double tau, double* budget,
+                           size_t* blocks, int* saturated) {
+    if (normalizer == 0.0) return -1;
+    if (blk <= 0) return -2;
+    const fxo_cache c = {k, v, dim, l_sink, l_cpu, l_local, l_new};
+    double* def_o = (double*)malloc(dim * sizeof(double));
+    double* part = (double*)malloc(dim * sizeof(double));
+    double* acc = (double*)malloc(dim * sizeof(double));
+    double* merged = (double*)malloc(dim * sizeof(double));
+    double def_lse;
+    const size_t def_t = fxo_default_partial(&c, q, def_o, &def_lse, part);
+    *budget = 0.0;
+    *blocks = 0;
+    *saturated = 0;
+    if (fxo_deviation(def_o, def_t, o_full, dim, normalizer) <= tau || l_cpu == 0) goto out;
+    {
+        const float* kc = k + l_sink * dim;
+        const float* vc = v + l_sink * dim;
+        const size_t nblk = fxo_block_count(l_cpu, blk);
+        float* mins = (float*)malloc(nblk * dim * sizeof(float));
+        float* maxs = (float*)malloc(nblk * dim * sizeof(float));
+        fxo_build_metadata(kc, l_cpu, dim, blk, mins, maxs);
+        fxo_scored* sc = (fxo_scored*)malloc(nblk * sizeof(fxo_scored));
+        for (size_t b = 0; b < nblk; ++b) {
+            sc[b].score = fxo_block_score(q, mins + b * dim, maxs + b * dim, dim);
+            sc[b].id = (uint32_t)b;
+        }
+        qsort(sc, nblk, sizeof(fxo_scored), fxo_cmp_scored); /* score_order: strict total order */
+        double acc_lse = -INFINITY;
+        size_t acc_t = 0, tokens = 0, i;
+        for (i = 0; i < nblk; ++i) {
+            const size_t b = sc[i].id;
+            const size_t r0 = b * (size_t)blk;
+            const size_t r1 = r0 + (size_t)blk < l_cpu ? r0 + (size_t)blk : l_cpu;
+            double l;
+            const size_t t = fxo_gathered_attention(q, kc + r0 * dim, vc + r0 * dim, dim, NULL,
+                                                    r1 - r0, part, &l);
+            fxo_merge_into(acc, &acc_lse, &acc_t, part, l, t, dim);
+            tokens += r1 - r0;
+            /* merged = defaults (+) cpu_acc */
+            memcpy(merged, def_o, dim * sizeof(double));
+            double m_lse = def_lse;
+            size_t m_t = def_t;
+            fxo_merge_into(merged, &m_lse, &m_t, acc, acc_lse, acc_t, dim);
+            if (fxo_deviation(merged, m_t, o_full, dim, normalizer) <= tau) {
+                *budget = (double)tokens / (double)l_cpu;
+                *blocks = i + 1;
+                break;
+            }
+        }
+        if (i == nblk) {
+            *budget = 1.0;
+            *blocks = nblk;
+            *saturated = 1;
+        }
+        free(mins);
+        free(maxs);
+        free(sc);
+    }
+out:
+    free(def_o);
+    free(part);
+    free(acc);
+    free(merged);
+    return 0;
+}
+
+/* fit_curve (budget_oracle.cpp:149-172): least-squares slope of budget on
+ * log2(blk); intercept reported only.  Returns -1 (underdetermined) with
+ * fewer than 2 distinct block sizes. */
+FXO_API int fxo_fit_curve(const int* blks, const double* budgets, int n, double* k_out,
+                          double* free_intercept, double* max_abs_residual) {
+    int distinct = 0;
+    for (int i = 0; i < n; ++i) {
+        int seen = 0;
+        for (int j = 0; j < i; ++j)
+            if (blks[j] == blks[i]) seen = 1;
+        distinct += !seen;
+    }
+    if (distinct < 2) return -1;
+    double sx = 0.0, sy = 0.0;
+    for (int i = 0; i < n; ++i) {
+        sx += log2((double)blks[i]);
+        sy += budgets[i];
+    }
+    const double nn = (double)n, mx = sx / nn, my = sy / nn;
+    double sxx = 0.0, sxy = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double dx = log2((double)blks[i]) - mx;
+        sxx += dx * dx;
+        sxy += dx * (budgets[i] - my);
+    }
+    const double k = sxy / sxx;
+    *k_out = k;
+    *free_intercept = my - k * mx;
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double pred = *free_intercept + k * log2((double)blks[i]);
+        const double e = fabs(pred - budgets[i]);
+        if (r < e) r = e;
+    }
+    *max_abs_residual = r;
+    return 0;
+}
+
+/* The oracle-source HeadProperties of one head (pipeline.cpp:256-276):
+ * label_streaming, else min_budget at blk 1/16/32/64/128 and fit_curve over
+ * the last four with the blk-1 budget as bgt0.  budgets_out [5] (zeros for a
+ * streaming head).  Returns the fxo_min_budget / fxo_fit_curve error, or 0. */
+FXO_API int fxo_oracle_props(const float* k, const float* v, size_t dim, size_t l_sink,
+                             size_t l_cpu, size_t l_local, size_t l_new, const float* q,
+                             const double* o_full, double normalizer, double tau, double* bgt0,
+                             double* kslope, int* streaming, double* budgets_out) {
+    static const int label_blocks[5] = {1, 16, 32, 64, 128}; /* budget_oracle.hpp:26 */
+    for (int i = 0; i < 5; ++i) budgets_out[i] = 0.0;
+    *bgt0 = *kslope = 0.0;
+    const int st = fxo_label_streaming(k, v, dim, l_sink, l_cpu, l_local, l_new, q, o_full,
+                                       normalizer, tau);
+    if (st < 0) return st;
+    *streaming = st;
+    if (st) return 0;
+    for (int i = 0; i < 5; ++i) {
+        size_t nb;
+        int sat;
+        const int rc = fxo_min_budget(k, v, dim, l_sink, l_cpu, l_local, l_new, q, label_blocks[i],
+                                      o_full, normalizer, tau, &budgets_out[i], &nb, &sat);
+        if (rc) return rc;
+    }
+    double icpt, res;
+    const int rc = fxo_fit_curve(label_blocks + 1, budgets_out + 1, 4, kslope, &icpt, &res);
+    *bgt0 = budgets_out[0];
+    return rc;
+}

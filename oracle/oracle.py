@@ -85,6 +85,24 @@ class COracle:
         L.fxo_predict.argtypes = [_f64p] * 9 + [_f64p, _f64p]
         L.fxo_rng_normals.argtypes = [C.c_uint64, _f32p, _sz]
         L.fxo_make_model.argtypes = [C.c_uint64] + [_f64p] * 6
+        seg = [_f32p, _f32p, _sz, _sz, _sz, _sz, _sz, _f32p]
+        L.fxo_max_output_norm.argtypes = [_f64p, _sz, _sz]
+        L.fxo_max_output_norm.restype = C.c_double
+        L.fxo_cache_attention.argtypes = seg + [_f64p]
+        L.fxo_cache_attention.restype = C.c_int
+        L.fxo_label_streaming.argtypes = seg + [_f64p, C.c_double, C.c_double]
+        L.fxo_label_streaming.restype = C.c_int
+        L.fxo_min_budget.argtypes = seg + [C.c_int, _f64p, C.c_double, C.c_double,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_size_t),
+                                           C.POINTER(C.c_int)]
+        L.fxo_min_budget.restype = C.c_int
+        L.fxo_fit_curve.argtypes = [_i32p, _f64p, C.c_int, C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.fxo_fit_curve.restype = C.c_int
+        L.fxo_oracle_props.argtypes = seg + [_f64p, C.c_double, C.c_double,
+                                             C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int), _f64p]
+        L.fxo_oracle_props.restype = C.c_int
         self.lib = L
 
     # -- block index ------------------------------------------------------
@@ -214,6 +232,58 @@ class COracle:
         return out
 
 
+    # -- output-aware budget oracle (budget_oracle.cpp) ------------------------
+    @staticmethod
+    def _seg(k, v, seg, q):
+        k, v = _f32(k), _f32(v)
+        return [k, v, k.shape[1], *seg, _f32(q)]
+
+    def max_output_norm(self, outs):
+        outs = _f64(outs)
+        return self.lib.fxo_max_output_norm(outs, outs.shape[0], outs.shape[1])
+
+    def cache_attention(self, k, v, seg, q):
+        o = np.zeros(np.shape(k)[1], np.float64)
+        if self.lib.fxo_cache_attention(*self._seg(k, v, seg, q), o):
+            raise RuntimeError("empty-context: cache has no tokens")
+        return o
+
+    def label_streaming(self, k, v, seg, q, o_full, normalizer, tau=0.10):
+        r = self.lib.fxo_label_streaming(*self._seg(k, v, seg, q), _f64(o_full), normalizer, tau)
+        if r < 0:
+            raise RuntimeError("degenerate-normalizer: all head outputs are zero")
+        return bool(r)
+
+    def min_budget(self, k, v, seg, q, blk, o_full, normalizer, tau=0.10):
+        """-> (budget, blocks, saturated)"""
+        bud, nb, sat = C.c_double(0), C.c_size_t(0), C.c_int(0)
+        r = self.lib.fxo_min_budget(*self._seg(k, v, seg, q), blk, _f64(o_full), normalizer, tau,
+                                    C.byref(bud), C.byref(nb), C.byref(sat))
+        if r == -1:
+            raise RuntimeError("degenerate-normalizer: all head outputs are zero")
+        if r:
+            raise RuntimeError("invalid-granularity: blk must be >= 1")
+        return bud.value, nb.value, bool(sat.value)
+
+    def fit_curve(self, blks, budgets):
+        """-> (k, free_intercept, max_abs_residual)"""
+        k, a, r = C.c_double(0), C.c_double(0), C.c_double(0)
+        if self.lib.fxo_fit_curve(np.ascontiguousarray(blks, np.int32), _f64(budgets), len(blks),
+                                  C.byref(k), C.byref(a), C.byref(r)):
+            raise RuntimeError("underdetermined: need at least 2 distinct block sizes")
+        return k.value, a.value, r.value
+
+    def oracle_props(self, k, v, seg, q, o_full, normalizer, tau=0.10):
+        """pipeline.cpp:256-276 for one head -> (bgt0, k, streaming, budgets[5])"""
+        b0, ks, st = C.c_double(0), C.c_double(0), C.c_int(0)
+        buds = np.zeros(5, np.float64)
+        r = self.lib.fxo_oracle_props(*self._seg(k, v, seg, q), _f64(o_full), normalizer, tau,
+                                      C.byref(b0), C.byref(ks), C.byref(st), buds)
+        if r:
+            raise RuntimeError(f"budget oracle error {r}")
+        return b0.value, ks.value, bool(st.value), buds
+
+
 class RefOracle:
     """The compiled reference (oracle/_ref/libfluxref.so)."""
 
@@ -271,6 +341,16 @@ class RefOracle:
         L.ref_model_set_norms.argtypes = [C.c_void_p, _f64p, _f64p]
         L.ref_save_model.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_predict.argtypes = [C.c_void_p, _f64p, _f64p, _f64p]
+        seg = [_f32p, _f32p, _sz, _sz, _sz, _sz, _sz, _f32p]
+        L.ref_cache_attention.argtypes = seg + [_f64p]
+        L.ref_min_budget.argtypes = seg + [C.c_int, _f64p, C.c_double, C.c_double,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_int)]
+        L.ref_label_streaming.argtypes = seg + [_f64p, C.c_double, C.c_double, C.POINTER(C.c_int)]
+        L.ref_fit_curve.argtypes = [_i32p, _f64p, C.c_int, C.c_double, C.c_int,
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]
+        L.ref_max_output_norm.argtypes = [_f64p, _sz, _sz, C.POINTER(C.c_double)]
         self.lib = L
 
     def _check(self, rc):
@@ -381,6 +461,41 @@ class RefOracle:
         self._check(self.lib.ref_default_kv_attention(k, v, k.shape[1], *seg, _f32(q), o,
                                                       C.byref(lse), C.byref(tok)))
         return o, lse.value, tok.value
+
+    # -- output-aware budget oracle (budget_oracle.cpp) -------------------
+    def cache_attention(self, k, v, seg, q):
+        k, v = _f32(k), _f32(v)
+        o = np.zeros(k.shape[1])
+        self._check(self.lib.ref_cache_attention(k, v, k.shape[1], *seg, _f32(q), o))
+        return o
+
+    def min_budget(self, k, v, seg, q, blk, o_full, normalizer, tau=0.10):
+        k, v = _f32(k), _f32(v)
+        bud, nb, sat = C.c_double(0), C.c_uint64(0), C.c_int(0)
+        self._check(self.lib.ref_min_budget(k, v, k.shape[1], *seg, _f32(q), blk, _f64(o_full),
+                                            normalizer, tau, C.byref(bud), C.byref(nb),
+                                            C.byref(sat)))
+        return bud.value, nb.value, bool(sat.value)
+
+    def label_streaming(self, k, v, seg, q, o_full, normalizer, tau=0.10):
+        k, v = _f32(k), _f32(v)
+        st = C.c_int(0)
+        self._check(self.lib.ref_label_streaming(k, v, k.shape[1], *seg, _f32(q), _f64(o_full),
+                                                 normalizer, tau, C.byref(st)))
+        return bool(st.value)
+
+    def fit_curve(self, blks, budgets, bgt0=0.0, streaming=False):
+        k, a, r = C.c_double(0), C.c_double(0), C.c_double(0)
+        self._check(self.lib.ref_fit_curve(np.ascontiguousarray(blks, np.int32), _f64(budgets),
+                                           len(blks), bgt0, int(streaming), C.byref(k),
+                                           C.byref(a), C.byref(r)))
+        return k.value, a.value, r.value
+
+    def max_output_norm(self, outs):
+        outs = _f64(outs)
+        out = C.c_double(0)
+        self._check(self.lib.ref_max_output_norm(outs, outs.shape[0], outs.shape[1], C.byref(out)))
+        return out.value
 
     # -- executed scheduler (CPU baseline) -------------------------------
     def batch(self):

@@ -416,4 +416,67 @@ int ref_predict(void* h, const double* raw, double* out, double* z) {
     });
 }
 
+// ---------------------------------------------------------------------------
+// output-aware budget oracle (budget_oracle.cpp) for one head of one group
+// ---------------------------------------------------------------------------
+int ref_cache_attention(const float* k, const float* v, std::size_t dim, std::size_t l_sink,
+                        std::size_t l_cpu, std::size_t l_local, std::size_t l_new, const float* q,
+                        double* o_full) {
+    return guarded([&] {
+        const SegmentedKvCache cache = to_cache(k, v, dim, l_sink, l_cpu, l_local, l_new);
+        const auto o = cache_attention(std::span<const float>(q, dim), cache);
+        std::copy(o.begin(), o.end(), o_full);
+    });
+}
+
+int ref_min_budget(const float* k, const float* v, std::size_t dim, std::size_t l_sink,
+                   std::size_t l_cpu, std::size_t l_local, std::size_t l_new, const float* q,
+                   int blk, const double* o_full, double normalizer, double tau, double* budget,
+                   std::uint64_t* blocks, int* saturated) {
+    return guarded([&] {
+        const SegmentedKvCache cache = to_cache(k, v, dim, l_sink, l_cpu, l_local, l_new);
+        ErrorBudgetConfig cfg;
+        cfg.tau = tau;
+        const MinBudgetResult r = min_budget(std::span<const float>(q, dim), cache, blk,
+                                             std::span<const double>(o_full, dim), normalizer, cfg);
+        *budget = r.budget;
+        *blocks = r.blocks;
+        *saturated = r.saturated ? 1 : 0;
+    });
+}
+
+int ref_label_streaming(const float* k, const float* v, std::size_t dim, std::size_t l_sink,
+                        std::size_t l_cpu, std::size_t l_local, std::size_t l_new, const float* q,
+                        const double* o_full, double normalizer, double tau, int* streaming) {
+    return guarded([&] {
+        const SegmentedKvCache cache = to_cache(k, v, dim, l_sink, l_cpu, l_local, l_new);
+        ErrorBudgetConfig cfg;
+        cfg.tau = tau;
+        *streaming = label_streaming(std::span<const float>(q, dim), cache,
+                                     std::span<const double>(o_full, dim), normalizer, cfg)
+                         ? 1
+                         : 0;
+    });
+}
+
+int ref_fit_curve(const int* blks, const double* budgets, int n, double bgt0, int streaming,
+                  double* k, double* free_intercept, double* max_abs_residual) {
+    return guarded([&] {
+        std::vector<std::pair<int, double>> pts;
+        for (int i = 0; i < n; ++i) pts.emplace_back(blks[i], budgets[i]);
+        const FitResult r = fit_curve(pts, bgt0, streaming != 0);
+        *k = r.props.k;
+        *free_intercept = r.free_intercept;
+        *max_abs_residual = r.max_abs_residual;
+    });
+}
+
+int ref_max_output_norm(const double* outs, std::size_t n, std::size_t dim, double* out) {
+    return guarded([&] {
+        std::vector<std::vector<double>> v(n);
+        for (std::size_t h = 0; h < n; ++h) v[h].assign(outs + h * dim, outs + (h + 1) * dim);
+        *out = max_output_norm(v);
+    });
+}
+
 } // extern "C"

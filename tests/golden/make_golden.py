@@ -79,6 +79,40 @@ def main():
     out["pred_z"] = np.array([m.predict(f)[1] for f in feats])
     np.savez_compressed(os.path.join(OUT, "reference_small.npz"), **out)
     print("wrote", os.path.join(OUT, "reference_small.npz"))
+    budget_golden(ref, out, l_sink, l_cpu, l_local)
+
+
+def budget_golden(ref, small, l_sink, l_cpu, l_local):
+    """Output-aware budget oracle (budget_oracle.cpp:37-172) on the same
+    workload: o_full per head (cache_attention), the step normalizer, the
+    streaming label and min_budget at every label granularity for three tau,
+    and fit_curve -- all from the compiled reference."""
+    seg = (l_sink, l_cpu, l_local, 1)
+    q = small["q"]
+    H, D = q.shape
+    o_full = np.array([ref.cache_attention(small[f"k{h // 4}"], small[f"v{h // 4}"], seg, q[h])
+                       for h in range(H)])
+    norm = ref.max_output_norm(o_full)
+    out = {"o_full": o_full, "normalizer": np.array(norm)}
+    taus = (0.05, 0.10, 0.20)
+    out["taus"] = np.array(taus)
+    stream = np.zeros((len(taus), H), np.int32)
+    mb = np.zeros((len(taus), H, 5))
+    nb = np.zeros((len(taus), H, 5), np.int64)
+    sat = np.zeros((len(taus), H, 5), np.int32)
+    for ti, tau in enumerate(taus):
+        for h in range(H):
+            k, v = small[f"k{h // 4}"], small[f"v{h // 4}"]
+            stream[ti, h] = ref.label_streaming(k, v, seg, q[h], o_full[h], norm, tau)
+            for i, blk in enumerate((1, 16, 32, 64, 128)):
+                mb[ti, h, i], nb[ti, h, i], sat[ti, h, i] = ref.min_budget(k, v, seg, q[h], blk,
+                                                                           o_full[h], norm, tau)
+    out["streaming"], out["min_budget"], out["min_blocks"], out["saturated"] = stream, mb, nb, sat
+    fits = [ref.fit_curve([16, 32, 64, 128], mb[1, h, 1:]) for h in range(H)
+            if len(set(mb[1, h, 1:].tolist())) >= 1]
+    out["fit"] = np.array(fits)
+    np.savez_compressed(os.path.join(OUT, "reference_budget.npz"), **out)
+    print("wrote", os.path.join(OUT, "reference_budget.npz"))
 
 
 if __name__ == "__main__":

@@ -128,3 +128,61 @@ def test_live_against_compiled_reference(coracle, refo):
         assert np.array_equal(mine, theirs["blocks"]) and cl == theirs["clamped"]
         for bgt in (0.0, 0.01, 0.3, 1.0, 1.5):
             assert coracle.blocks_for_budget(bgt, L, max(blk, 1)) == refo.blocks_for_budget(bgt, L, max(blk, 1))
+
+
+# ---------------------------------------------------------------------------
+# output-aware budget oracle (budget_oracle.cpp) -- the label path of C3
+# ---------------------------------------------------------------------------
+GOLD_BUDGET = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                           "reference_budget.npz")
+
+
+def test_golden_budget_oracle(coracle, gold):
+    gb = np.load(GOLD_BUDGET)
+    seg = (64, 704, 256, 1)
+    q = gold["q"]
+    H = q.shape[0]
+    o_full = np.array([coracle.cache_attention(gold[f"k{h // 4}"], gold[f"v{h // 4}"], seg, q[h])
+                       for h in range(H)])
+    assert np.array_equal(o_full, gb["o_full"])
+    norm = coracle.max_output_norm(o_full)
+    assert norm == float(gb["normalizer"])
+    for ti, tau in enumerate(gb["taus"]):
+        for h in range(H):
+            k, v = gold[f"k{h // 4}"], gold[f"v{h // 4}"]
+            assert coracle.label_streaming(k, v, seg, q[h], o_full[h], norm, tau) == \
+                bool(gb["streaming"][ti, h])
+            for i, blk in enumerate((1, 16, 32, 64, 128)):
+                bud, nb, sat = coracle.min_budget(k, v, seg, q[h], blk, o_full[h], norm, tau)
+                assert bud == gb["min_budget"][ti, h, i] and nb == gb["min_blocks"][ti, h, i]
+                assert sat == bool(gb["saturated"][ti, h, i])
+    for h in range(H):
+        assert np.array_equal(coracle.fit_curve([16, 32, 64, 128], gb["min_budget"][1, h, 1:]),
+                              gb["fit"][h])
+    with pytest.raises(RuntimeError, match="^underdetermined"):
+        coracle.fit_curve([16, 16], [0.1, 0.2])
+
+
+def test_budget_oracle_live_against_compiled_reference(coracle, refo):
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        D = int(rng.choice([16, 64]))
+        seg = (int(rng.integers(0, 20)), int(rng.integers(50, 900)), int(rng.integers(0, 40)),
+               int(rng.integers(0, 3)))
+        L = sum(seg)
+        k = rng.standard_normal((L, D)).astype(np.float32)
+        v = rng.standard_normal((L, D)).astype(np.float32)
+        q = rng.standard_normal(D).astype(np.float32)
+        if trial % 2:  # a needle the query finds
+            s = seg[0] + int(rng.integers(0, seg[1] - 8))
+            k[s:s + 8] += 0.5 * q
+        o = coracle.cache_attention(k, v, seg, q)
+        assert np.array_equal(o, refo.cache_attention(k, v, seg, q))
+        norm = max(float(np.linalg.norm(o)), 1e-3)
+        for tau in (0.02, 0.1, 0.4):
+            if seg[0] + seg[2] + seg[3] > 0:
+                assert coracle.label_streaming(k, v, seg, q, o, norm, tau) == \
+                    refo.label_streaming(k, v, seg, q, o, norm, tau)
+            for blk in (1, 16, 64):
+                assert coracle.min_budget(k, v, seg, q, blk, o, norm, tau) == \
+                    refo.min_budget(k, v, seg, q, blk, o, norm, tau)
