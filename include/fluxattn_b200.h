@@ -227,6 +227,25 @@ FX_API int fx_append_kv(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int
 /* Convert f32 -> dtype on device (n elements). */
 FX_API int fx_convert(fx_ctx* ctx, const float* src, void* dst, int32_t dtype, size_t n);
 
+/* ---- output-aware budget oracle (labels) ---------------------------------- */
+/* The oracle head properties of every query head of the batch
+ * (pipeline.cpp:256-276, replaces per head: cache_attention attention.cpp:131-141,
+ * max_output_norm budget_oracle.cpp:37-41, label_streaming :107-116,
+ * min_budget :54-105 at blk 1/16/32/64/128, fit_curve :149-172).
+ * k, v: the layout's cache [dev] with l_new decoded rows; meta: the four levels
+ * of fx_build_metadata_levels (blk 16..128; may be NULL when l_cpu == 0);
+ * q [dev] [B][H][D] f32; criterion 0 = step normalizer max_h ||o_full_h|| of
+ * each sequence b (Output+Budget), 1 = ||o_full_h|| (OutputOnly).
+ * Outputs [dev]: o_full [B][H][D] f64, normalizer [B], budgets [B][H][5]
+ * (min_budget .budget per blk), blocks [B][H][5] (optional), bgt0, kslope
+ * [B][H], streaming [B][H] int32.  Synchronizes the ctx stream (the
+ * degenerate-normalizer check).  Errors: degenerate-normalizer, bad-shape,
+ * empty-context, no-context. */
+FX_API int fx_label_heads(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
+                          int64_t l_new, const void* const meta[4], const float* q, double tau,
+                          int32_t criterion, double* o_full, double* normalizer, double* budgets,
+                          int64_t* blocks, double* bgt0, double* kslope, int32_t* streaming);
+
 /* ---- context-parallel decode (C5) ------------------------------------------
  * The cpu segment is split into contiguous 128-row-aligned shards, one per
  * rank (sink rows on rank 0, local + decoded rows on the last rank), so block

@@ -97,6 +97,8 @@ _SIGS = {
     "fx_cp_select": (C.c_int, [_p, C.POINTER(Layout), _i32, _i32, _i64, _p, _p, _p, _p, _p, _i64,
                                _p, _i32]),
     "fx_cp_combine": (C.c_int, [_p, _i32, _i64, _i32, _p, _p, _p, _p]),
+    "fx_label_heads": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, C.POINTER(_p * 4), _p,
+                                 C.c_double, _i32, _p, _p, _p, _p, _p, _p, _p]),
 }
 
 EXPORTED = tuple(_SIGS)

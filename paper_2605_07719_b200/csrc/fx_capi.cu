@@ -84,6 +84,7 @@ struct fx_ctx {
     uint64_t launches = 0;
     DevBuf step;  // fx_decode_step scratch
     DevBuf api;   // per-query API scratch
+    DevBuf label; // fx_label_heads scratch
     // optional per-kernel CUDA-event timing (fx_ctx_set_timing)
     bool timing = false;
     std::vector<cudaEvent_t> pool;
@@ -773,6 +774,42 @@ int fx_convert(fx_ctx* ctx, const float* src, void* dst, int32_t dtype, size_t n
         DeviceGuard g(ctx);
         fx::launch_convert(src, dst, dtype, n, ctx->stream);
         ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+// ---- output-aware budget oracle (budget_oracle.cpp) ------------------------
+
+int fx_label_heads(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v, int64_t l_new,
+                   const void* const meta[4], const float* q, double tau, int32_t criterion,
+                   double* o_full, double* normalizer, double* budgets, int64_t* blocks,
+                   double* bgt0, double* kslope, int32_t* streaming) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const fx_layout& L = *lay;
+        FX_REQUIRE(k && v && q && o_full && normalizer && budgets && bgt0 && kslope && streaming,
+                   FX_ERR_STATE, "no-context: label call has no payload");
+        FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_new <= L.l_cap, FX_ERR_INVALID,
+                   "bad-shape: decoded rows exceed l_cap");
+        FX_REQUIRE(L.l_sink + L.l_cpu + L.l_local + l_new > 0, FX_ERR_INVALID,
+                   "empty-context: cache has no tokens");
+        FX_REQUIRE(criterion == 0 || criterion == 1, FX_ERR_INVALID, "bad-shape: unknown criterion");
+        if (L.l_cpu > 0)
+            for (int i = 0; i < 4; ++i)
+                FX_REQUIRE(meta && meta[i], FX_ERR_STATE, "no-context: missing block metadata");
+        const void* mp[4] = {nullptr, nullptr, nullptr, nullptr};
+        if (meta)
+            for (int i = 0; i < 4; ++i) mp[i] = meta[i];
+        ctx->label.ensure(fx::label_scratch_bytes(L, l_new) + 256);
+        int32_t* err = reinterpret_cast<int32_t*>(static_cast<char*>(ctx->label.p) +
+                                                  fx::label_scratch_bytes(L, l_new));
+        fx::launch_label(L, k, v, l_new, q, mp, tau, criterion, ctx->label.p, o_full, normalizer,
+                         budgets, blocks, bgt0, kslope, streaming, err, ctx->stream);
+        ctx->launches += L.l_cpu > 0 ? 7 : 5;
+        int32_t h_err = 0;
+        FX_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        FX_CUDA(cudaStreamSynchronize(ctx->stream));
+        FX_REQUIRE(h_err == 0, FX_ERR_INVALID, "degenerate-normalizer: all head outputs are zero");
     });
 }
 

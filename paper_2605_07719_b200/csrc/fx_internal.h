@@ -126,6 +126,13 @@ void launch_topk_exact(const float* q, const void* meta, int dtype, int64_t nblk
 void launch_meta_absmax(const void* meta, int dtype, int64_t nblk, int dim, float* absmax,
                         cudaStream_t s);
 
+// fx_label.cu: output-aware head labels (budget_oracle.cpp); device outputs
+size_t label_scratch_bytes(const fx_layout& L, int64_t l_new);
+void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_new, const float* q,
+                  const void* const meta[4], double tau, int criterion, void* scratch,
+                  double* o_full, double* normalizer, double* budgets, int64_t* blocks,
+                  double* bgt0, double* kslope, int32_t* streaming, int32_t* err, cudaStream_t s);
+
 // fx_attend.cu
 // 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},
 // box {64, box_rows, D/64}, 128-byte swizzle (D multiple of 64).

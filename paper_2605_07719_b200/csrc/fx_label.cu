@@ -1,0 +1,580 @@
+// fx_label.cu -- the output-aware budget oracle on the device: the labels
+// that make config C3's "output-aware budgets" (pipeline.cpp:256-276, oracle
+// property source) and the prefill budget features (pipeline.cpp:37-46).
+//
+// Per query head h of sequence b, over its group's cache sink | cpu | local | new:
+//   o_full      = cache_attention (attention.cpp:131-141)
+//   normalizer  = max_h ||o_full_h|| over the heads of b (budget_oracle.cpp:37-41;
+//                 criterion OutputOnly: ||o_full_h||, pipeline.cpp:264-266)
+//   streaming   = label_streaming (budget_oracle.cpp:107-116)
+//   budget[blk] = min_budget at blk in {1, 16, 32, 64, 128} (budget_oracle.cpp:54-105)
+//   k           = fit_curve over blk 16..128, bgt0 = budget[1] (budget_oracle.cpp:149-172)
+//
+// min_budget scans block prefixes in reference score order (score desc, id
+// asc; score = the exact f64 Quest bound, block_index.cpp:41-53 -- at blk 1 the
+// plain q.k dot) and stops at the first prefix whose reconstruction deviation
+// ||defaults (+) prefix - o_full|| / normalizer is <= tau.  Here:
+//   K_scores  exact f64 q.k of every row (sequential over d, unfused: these are
+//             also the blk-1 sort keys), and the per-head max of q.k/sqrt(D);
+//   K_sums    weights e = exp(q.k/sqrt(D) - max) in place of the dots, and
+//             Z, sum e*v over all rows and over the default rows (f64 atomics);
+//   K_norm    o_full, normalizer, defaults-only deviation, streaming;
+//   K_keys    exact Quest bounds of the blocks at 16..128 from the metadata levels;
+//   K_sort    per (head, level): stable LSD radix sort of ~f64_key(score)
+//             (8 x 8-bit passes, ids start ascending, so ties stay id-ascending);
+//   K_scan    per (head, level): R(m) = A + P(m) - Z(m) o_full accumulated in f64
+//             32 sorted blocks at a time, deviation(m) = ||R(m)|| / (Z(m) norm);
+//             the first m with deviation <= tau;
+//   K_fit     fit_curve and the head properties.
+// Parity: deviations are f64 with a different association than the
+// reference's pairwise LSE merges, so a prefix whose deviation lies within
+// ~1e-12 of tau can land one block off; tests report those separately.
+#include <algorithm>
+
+#include "fx_common.cuh"
+
+namespace fx {
+namespace {
+
+constexpr int kNL = 5;  // label granularities
+__constant__ int c_label_blk[kNL] = {1, 16, 32, 64, 128};
+constexpr int kMaxG = 16;
+constexpr int kSortT = 512, kSortW = kSortT / 32, kIpt = 8, kTile = kSortT * kIpt;
+
+struct LabelView {
+    int B, Hkv, G, D, criterion;
+    int64_t l_cap, l_sink, l_cpu, l_local, l_new, Lr;  // Lr = rows per group
+    const void* k;
+    const void* v;
+    const float* q;  // [nh][D]
+    const void* meta[4];
+    double tau;
+    double* S;            // [nh][Lr] q.k, then weights e
+    uint64_t* hmax;       // [nh] f64_key(max q.k / sqrt(D))
+    double* Of;           // [nh][D] sum e v, all rows
+    double* Od;           // [nh][D] sum e v, default rows
+    double* Zf;           // [nh]
+    double* Zd;           // [nh]
+    double* o_full;       // [nh][D]
+    double* normalizer;   // [B]
+    double* nrm_head;     // [nh] normalizer used for head h
+    int32_t* streaming;   // [nh]
+    uint64_t* keys[2];    // [nh][n_tot]
+    uint32_t* ids[2];
+    int64_t seg_off[kNL + 1];
+    double* budgets;      // [nh][5]
+    int64_t* blocks;      // [nh][5]
+    double* bgt0;         // [nh]
+    double* kslope;       // [nh]
+    int32_t* err;         // [1] degenerate-normalizer flag
+};
+
+__device__ __forceinline__ double key_f64(uint64_t k) {
+    return __longlong_as_double((long long)((k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float* f);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* f) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = bf16lo_to_f(w[i]);
+        f[2 * i + 1] = bf16hi_to_f(w[i]);
+    }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float* f) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+// K_scores: one thread per row, all G heads of the group (dimension-outer so
+// the row is read once; each head's sum stays in dimension order).
+template <typename T>
+__global__ void __launch_bounds__(256) k_lab_scores(const LabelView p) {
+    __shared__ double qs[kMaxG * 256];
+    const int bg = blockIdx.y, G = p.G, D = p.D;
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) qs[i] = (double)p.q[(int64_t)bg * G * D + i];
+    __syncthreads();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = t < p.Lr;
+    double s[kMaxG];
+#pragma unroll
+    for (int h = 0; h < kMaxG; ++h) s[h] = 0.0;
+    if (live) {
+        const T* row = static_cast<const T*>(p.k) + ((int64_t)bg * p.l_cap + t) * D;
+        for (int d0 = 0; d0 < D; d0 += 8) {
+            float f[8];
+            load8<T>(row + d0, f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double kd = (double)f[u];
+#pragma unroll
+                for (int h = 0; h < kMaxG; ++h)
+                    if (h < G) s[h] = __dadd_rn(s[h], __dmul_rn(qs[h * D + d0 + u], kd));
+            }
+        }
+    }
+    const double isd = 1.0 / sqrt((double)D);
+    const bool cpu = live && t >= p.l_sink && t < p.l_sink + p.l_cpu;
+    const int64_t n_tot = p.seg_off[kNL];
+    for (int h = 0; h < G; ++h) {
+        const int64_t head = (int64_t)bg * G + h;
+        if (live) p.S[head * p.Lr + t] = s[h];
+        if (cpu) {
+            p.keys[0][head * n_tot + (t - p.l_sink)] = ~f64_key(s[h]);
+            p.ids[0][head * n_tot + (t - p.l_sink)] = (uint32_t)(t - p.l_sink);
+        }
+        uint64_t m = live ? f64_key(__dmul_rn(s[h], isd)) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t y = __shfl_xor_sync(0xffffffffu, m, o);
+            m = y > m ? y : m;
+        }
+        if ((threadIdx.x & 31) == 0 && m) atomicMax((unsigned long long*)(p.hmax + head), (unsigned long long)m);
+    }
+}
+
+// K_sums: weights in place and the f64 sums over all rows / default rows.
+template <typename T>
+__global__ void __launch_bounds__(128) k_lab_sums(const LabelView p) {
+    __shared__ double e_s[128][kMaxG];
+    __shared__ unsigned char dflt[128];
+    const int bg = blockIdx.y, G = p.G, D = p.D;
+    const int64_t t0 = (int64_t)blockIdx.x * 128;
+    const double isd = 1.0 / sqrt((double)D);
+    {
+        const int64_t t = t0 + threadIdx.x;
+        const bool live = t < p.Lr;
+        dflt[threadIdx.x] = live && (t < p.l_sink || t >= p.l_sink + p.l_cpu);
+        for (int h = 0; h < G; ++h) {
+            const int64_t head = (int64_t)bg * G + h;
+            double e = 0.0;
+            if (live) {
+                const double m = key_f64(p.hmax[head]);
+                e = exp(__dmul_rn(p.S[head * p.Lr + t], isd) - m);
+                p.S[head * p.Lr + t] = e;
+            }
+            e_s[threadIdx.x][h] = e;
+        }
+    }
+    __syncthreads();
+    const int d = threadIdx.x;
+    const int nrow = (int)(p.Lr - t0 < 128 ? p.Lr - t0 : 128);
+    double af[kMaxG], ad[kMaxG];
+#pragma unroll
+    for (int h = 0; h < kMaxG; ++h) af[h] = ad[h] = 0.0;
+    if (d < D) {
+        const T* vb = static_cast<const T*>(p.v) + ((int64_t)bg * p.l_cap + t0) * D + d;
+        for (int i = 0; i < nrow; ++i) {
+            const double vd = (double)tofl(vb[(int64_t)i * D]);
+            const bool df = dflt[i];
+#pragma unroll
+            for (int h = 0; h < kMaxG; ++h)
+                if (h < G) {
+                    const double w = e_s[i][h] * vd;
+                    af[h] += w;
+                    if (df) ad[h] += w;
+                }
+        }
+        for (int h = 0; h < G; ++h) {
+            const int64_t head = (int64_t)bg * G + h;
+            atomicAdd(p.Of + head * D + d, af[h]);
+            atomicAdd(p.Od + head * D + d, ad[h]);
+        }
+    }
+    if (threadIdx.x < G) {
+        const int h = threadIdx.x;
+        double zf = 0.0, zd = 0.0;
+        for (int i = 0; i < nrow; ++i) {
+            zf += e_s[i][h];
+            if (dflt[i]) zd += e_s[i][h];
+        }
+        const int64_t head = (int64_t)bg * G + h;
+        atomicAdd(p.Zf + head, zf);
+        atomicAdd(p.Zd + head, zd);
+    }
+}
+
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < nw; ++i) s += red[i];
+    return s;
+}
+
+// K_norm: one CTA per sequence b.
+__global__ void __launch_bounds__(128) k_lab_norm(const LabelView p) {
+    __shared__ double red[8];
+    __shared__ double hn[1024];
+    const int b = blockIdx.x, H = p.Hkv * p.G, D = p.D, d = threadIdx.x;
+    double nrm = 0.0;
+    for (int h = 0; h < H; ++h) {
+        const int64_t head = (int64_t)b * H + h;
+        const double zf = p.Zf[head];
+        double of = 0.0;
+        if (d < D) {
+            of = zf > 0.0 ? p.Of[head * D + d] / zf : 0.0;
+            p.o_full[head * D + d] = of;
+        }
+        const double n2 = sqrt(block_sum(d < D ? of * of : 0.0, red));
+        if (h < 1024) hn[h] = n2;
+        nrm = fmax(nrm, n2);
+    }
+    if (d == 0) p.normalizer[b] = nrm;
+    for (int h = 0; h < H; ++h) {
+        const int64_t head = (int64_t)b * H + h;
+        const double nh = p.criterion == 1 ? hn[min(h, 1023)] : nrm;
+        const double zd = p.Zd[head];
+        double x = 0.0;
+        if (d < D) {
+            const double of = p.o_full[head * D + d];
+            x = zd > 0.0 ? p.Od[head * D + d] / zd - of : of;  // empty defaults: ||o_full||
+        }
+        const double dev = sqrt(block_sum(x * x, red)) / nh;
+        if (d == 0) {
+            p.nrm_head[head] = nh;
+            if (p.l_cpu == 0) {
+                p.streaming[head] = 1;
+            } else if (nh == 0.0) {
+                p.streaming[head] = 1;
+                atomicOr(p.err, 1);  // degenerate-normalizer
+            } else {
+                p.streaming[head] = dev <= p.tau;
+            }
+        }
+    }
+}
+
+// K_keys: exact Quest bounds of the blocks at 16..128 (levels 1..4).
+template <typename T>
+__global__ void __launch_bounds__(256) k_lab_keys(const LabelView p) {
+    const int64_t head = blockIdx.y;
+    const int lvl = blockIdx.z + 1;
+    if (p.streaming[head]) return;
+    const int blk = c_label_blk[lvl];
+    const int64_t nblk = cdiv_dev(p.l_cpu, blk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nblk) return;
+    const int D = p.D;
+    const int64_t bg = head / p.G;
+    const T* m = static_cast<const T*>(p.meta[lvl - 1]) + ((bg * nblk + i) * 2) * D;
+    const int64_t n_tot = p.seg_off[kNL];
+    const int64_t o = head * n_tot + p.seg_off[lvl] + i;
+    p.keys[0][o] = ~f64_key(exact_score(p.q + head * D, m, m + D, D));
+    p.ids[0][o] = (uint32_t)i;
+}
+
+// K_sort: one CTA per (head, level) segment, stable LSD radix sort of the
+// 64-bit keys (ascending = reference order), ids carried; 8 passes ping-pong
+// between the two buffers, ending in buffer 0.
+__global__ void __launch_bounds__(kSortT) k_lab_sort(const LabelView p) {
+    __shared__ uint32_t wcnt[kSortW][256];
+    __shared__ uint32_t base[256];
+    const int64_t head = blockIdx.x;
+    const int lvl = blockIdx.y;
+    if (p.streaming[head]) return;
+    const int64_t n_tot = p.seg_off[kNL];
+    const int64_t off = head * n_tot + p.seg_off[lvl];
+    const int64_t n = p.seg_off[lvl + 1] - p.seg_off[lvl];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int sh = pass * 8;
+        const uint64_t* ks = p.keys[pass & 1] + off;
+        const uint32_t* is = p.ids[pass & 1] + off;
+        uint64_t* kd = p.keys[(pass & 1) ^ 1] + off;
+        uint32_t* id = p.ids[(pass & 1) ^ 1] + off;
+        // histogram -> exclusive digit bases
+        for (int i = t; i < 256; i += kSortT) base[i] = 0;
+        __syncthreads();
+        for (int64_t i = t; i < n; i += kSortT) atomicAdd(&base[(ks[i] >> sh) & 255u], 1u);
+        __syncthreads();
+        if (w == 0) {
+            uint32_t run = 0;
+            for (int c = 0; c < 256; c += 32) {
+                const uint32_t v = base[c + lane];
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                base[c + lane] = run + x - v;
+                run += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        __syncthreads();
+        for (int64_t t0 = 0; t0 < n; t0 += kTile) {
+            // warp w owns items [t0 + w*256, t0 + (w+1)*256), 32 at a time in order
+            for (int i = lane; i < 256; i += 32) wcnt[w][i] = 0;
+            __syncwarp();
+            uint64_t kk[kIpt];
+            uint32_t ii[kIpt], rk[kIpt];
+            int dg[kIpt];
+#pragma unroll
+            for (int j = 0; j < kIpt; ++j) {
+                const int64_t x = t0 + (int64_t)w * (32 * kIpt) + j * 32 + lane;
+                const bool live = x < n;
+                kk[j] = live ? ks[x] : 0ull;
+                ii[j] = live ? is[x] : 0u;
+                dg[j] = live ? (int)((kk[j] >> sh) & 255u) : 256;
+            }
+#pragma unroll
+            for (int j = 0; j < kIpt; ++j) {
+                const uint32_t peers = __match_any_sync(0xffffffffu, dg[j]);
+                const int leader = __ffs(peers) - 1;
+                uint32_t old = 0;
+                if (lane == leader && dg[j] < 256) {
+                    old = wcnt[w][dg[j]];
+                    wcnt[w][dg[j]] = old + __popc(peers);
+                }
+                old = __shfl_sync(0xffffffffu, old, leader);
+                rk[j] = old + __popc(peers & lt);
+                __syncwarp();
+            }
+            __syncthreads();
+            if (t < 256) {  // per digit: bases of the warps in order
+                uint32_t run = base[t];
+                for (int q = 0; q < kSortW; ++q) {
+                    const uint32_t c = wcnt[q][t];
+                    wcnt[q][t] = run;
+                    run += c;
+                }
+                base[t] = run;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kIpt; ++j)
+                if (dg[j] < 256) {
+                    const uint32_t pos = wcnt[w][dg[j]] + rk[j];
+                    kd[pos] = kk[j];
+                    id[pos] = ii[j];
+                }
+            __syncthreads();
+        }
+    }
+}
+
+// K_scan: one CTA (128 threads, thread = dimension) per (head, level).
+// R(m) = A + sum_{j<m} u_j - Z(m) o_full with u_j = sum_{rows of block j} e v,
+// so defaults (+) first m blocks - o_full = R(m) / Z(m).
+constexpr int kChunk = 32;
+template <typename T>
+__global__ void __launch_bounds__(128) k_lab_scan(const LabelView p) {
+    __shared__ double sq[kChunk][129];
+    __shared__ double zz[kChunk];
+    __shared__ int64_t tk[kChunk];
+    __shared__ uint32_t cid[kChunk];
+    __shared__ int s_first;
+    const int64_t head = blockIdx.x;
+    const int lvl = blockIdx.y;
+    const int t = threadIdx.x, D = p.D, lane = t & 31, w = t >> 5;
+    double* bud = p.budgets + head * kNL + lvl;
+    int64_t* nbo = p.blocks ? p.blocks + head * kNL + lvl : nullptr;
+    if (p.streaming[head]) {  // defaults alone are within tau: zero blocks
+        if (t == 0) {
+            *bud = 0.0;
+            if (nbo) *nbo = 0;
+        }
+        return;
+    }
+    const int blk = c_label_blk[lvl];
+    const int64_t n = cdiv_dev(p.l_cpu, blk);
+    const int64_t n_tot = p.seg_off[kNL];
+    const uint32_t* order = p.ids[0] + head * n_tot + p.seg_off[lvl];
+    const double* E = p.S + head * p.Lr;
+    const int64_t bg = head / p.G;
+    const T* V = static_cast<const T*>(p.v) + bg * p.l_cap * D + (t < D ? t : 0);
+    const double nrm = p.nrm_head[head];
+    const double of = t < D ? p.o_full[head * D + t] : 0.0;
+    double R = t < D ? p.Od[head * D + t] - p.Zd[head] * of : 0.0;
+    double Z = p.Zd[head];
+    int64_t tokens = 0;
+    for (int64_t c0 = 0; c0 < n; c0 += kChunk) {
+        const int nb = (int)(n - c0 < kChunk ? n - c0 : kChunk);
+        if (t < nb) cid[t] = order[c0 + t];
+        if (t == 0) s_first = kChunk;
+        __syncthreads();
+        for (int j = 0; j < nb; ++j) {
+            const int64_t b0 = (int64_t)cid[j] * blk;
+            const int64_t r0 = p.l_sink + b0;
+            const int64_t r1 = p.l_sink + min(p.l_cpu, b0 + blk);
+            double zj = 0.0, uj = 0.0;
+#pragma unroll 4
+            for (int64_t r = r0; r < r1; ++r) {
+                const double e = E[r];
+                zj += e;
+                uj += e * (double)tofl(V[r * D]);
+            }
+            R += uj - zj * of;
+            Z += zj;
+            tokens += r1 - r0;
+            sq[j][t] = t < D ? R * R : 0.0;
+            if (t == 0) {
+                zz[j] = Z;
+                tk[j] = tokens;
+            }
+        }
+        __syncthreads();
+        for (int j = w; j < nb; j += 4) {  // 4 warps: deviation of each prefix
+            double x = 0.0;
+            for (int d = lane; d < D; d += 32) x += sq[j][d];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (lane == 0 && sqrt(x) / (zz[j] * nrm) <= p.tau) atomicMin(&s_first, j);
+        }
+        __syncthreads();
+        const int f = s_first;
+        if (f < nb) {
+            if (t == 0) {
+                *bud = (double)tk[f] / (double)p.l_cpu;
+                if (nbo) *nbo = c0 + f + 1;
+            }
+            return;
+        }
+        __syncthreads();
+    }
+    if (t == 0) {  // saturated: even the full selection violates tau
+        *bud = 1.0;
+        if (nbo) *nbo = n;
+    }
+}
+
+// K_fit: fit_curve over blk 16..128 (budget_oracle.cpp:149-172) with the
+// reference's operation order and no contraction; bgt0 = the blk-1 budget.
+__global__ void k_lab_fit(const LabelView p, int64_t nh) {
+    const int64_t head = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (head >= nh) return;
+    if (p.streaming[head]) {
+        p.bgt0[head] = 0.0;
+        p.kslope[head] = 0.0;
+        return;
+    }
+    const double* b = p.budgets + head * kNL;
+    double sx = 0.0, sy = 0.0;
+    for (int i = 1; i < kNL; ++i) {
+        sx = __dadd_rn(sx, (double)(__ffs(c_label_blk[i]) - 1));  // log2 of a power of two, exact
+        sy = __dadd_rn(sy, b[i]);
+    }
+    const double mx = __ddiv_rn(sx, 4.0), my = __ddiv_rn(sy, 4.0);
+    double sxx = 0.0, sxy = 0.0;
+    for (int i = 1; i < kNL; ++i) {
+        const double dx = __dsub_rn((double)(__ffs(c_label_blk[i]) - 1), mx);
+        sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
+        sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(b[i], my)));
+    }
+    p.kslope[head] = __ddiv_rn(sxy, sxx);
+    p.bgt0[head] = b[0];
+}
+
+}  // namespace
+
+size_t label_scratch_bytes(const fx_layout& L, int64_t l_new) {
+    const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
+    const int64_t Lr = L.l_sink + L.l_cpu + L.l_local + l_new;
+    int64_t n_tot = L.l_cpu;
+    for (int i = 1; i < kNL; ++i) n_tot += cdiv(L.l_cpu, kLevels[i - 1]);
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    return al((size_t)nh * Lr * 8) + 2 * al((size_t)nh * n_tot * 8) + 2 * al((size_t)nh * n_tot * 4) +
+           4 * al((size_t)nh * 8) + 2 * al((size_t)nh * L.head_dim * 8);
+}
+
+void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_new, const float* q,
+                  const void* const meta[4], double tau, int criterion, void* scratch,
+                  double* o_full, double* normalizer, double* budgets, int64_t* blocks,
+                  double* bgt0, double* kslope, int32_t* streaming, int32_t* err, cudaStream_t s) {
+    FX_REQUIRE(L.group_size <= kMaxG && L.head_dim <= 128 && L.head_dim % 8 == 0 &&
+                   L.group_size * L.head_dim <= kMaxG * 256,
+               FX_ERR_INVALID, "bad-shape: labels need group_size <= 16 and head_dim <= 128 (multiple of 8)");
+    FX_REQUIRE(L.kv_heads * L.group_size <= 1024, FX_ERR_INVALID, "bad-shape: more than 1024 heads");
+    const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
+    const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
+    const int D = L.head_dim;
+    LabelView p{};
+    p.B = L.batch;
+    p.Hkv = L.kv_heads;
+    p.G = L.group_size;
+    p.D = D;
+    p.criterion = criterion;
+    p.l_cap = L.l_cap;
+    p.l_sink = L.l_sink;
+    p.l_cpu = L.l_cpu;
+    p.l_local = L.l_local;
+    p.l_new = l_new;
+    p.Lr = L.l_sink + L.l_cpu + L.l_local + l_new;
+    p.k = k;
+    p.v = v;
+    p.q = q;
+    for (int i = 0; i < 4; ++i) p.meta[i] = meta[i];
+    p.tau = tau;
+    p.seg_off[0] = 0;
+    p.seg_off[1] = L.l_cpu;
+    for (int i = 1; i < kNL; ++i) p.seg_off[i + 1] = p.seg_off[i] + cdiv(L.l_cpu, kLevels[i - 1]);
+    const int64_t n_tot = p.seg_off[kNL];
+    char* c = static_cast<char*>(scratch);
+    auto take = [&](size_t bytes) {
+        char* r = c;
+        c += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    p.S = reinterpret_cast<double*>(take((size_t)nh * p.Lr * 8));
+    p.keys[0] = reinterpret_cast<uint64_t*>(take((size_t)nh * n_tot * 8));
+    p.keys[1] = reinterpret_cast<uint64_t*>(take((size_t)nh * n_tot * 8));
+    p.ids[0] = reinterpret_cast<uint32_t*>(take((size_t)nh * n_tot * 4));
+    p.ids[1] = reinterpret_cast<uint32_t*>(take((size_t)nh * n_tot * 4));
+    char* zero0 = c;
+    p.hmax = reinterpret_cast<uint64_t*>(take((size_t)nh * 8));
+    p.Of = reinterpret_cast<double*>(take((size_t)nh * D * 8));
+    p.Od = reinterpret_cast<double*>(take((size_t)nh * D * 8));
+    p.Zf = reinterpret_cast<double*>(take((size_t)nh * 8));
+    p.Zd = reinterpret_cast<double*>(take((size_t)nh * 8));
+    char* zero1 = c;
+    p.nrm_head = reinterpret_cast<double*>(take((size_t)nh * 8));
+    p.o_full = o_full;
+    p.normalizer = normalizer;
+    p.streaming = streaming;
+    p.budgets = budgets;
+    p.blocks = blocks;
+    p.bgt0 = bgt0;
+    p.kslope = kslope;
+    p.err = err;
+    FX_CUDA(cudaMemsetAsync(zero0, 0, (size_t)(zero1 - zero0), s));
+    FX_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
+    const bool bf = L.dtype == FX_BF16;
+    const dim3 g1((unsigned)cdiv(p.Lr, 256), (unsigned)n_bg);
+    if (bf) k_lab_scores<__nv_bfloat16><<<g1, 256, 0, s>>>(p);
+    else k_lab_scores<float><<<g1, 256, 0, s>>>(p);
+    FX_CUDA(cudaGetLastError());
+    const dim3 g2((unsigned)cdiv(p.Lr, 128), (unsigned)n_bg);
+    if (bf) k_lab_sums<__nv_bfloat16><<<g2, 128, 0, s>>>(p);
+    else k_lab_sums<float><<<g2, 128, 0, s>>>(p);
+    FX_CUDA(cudaGetLastError());
+    k_lab_norm<<<(unsigned)L.batch, 128, 0, s>>>(p);
+    FX_CUDA(cudaGetLastError());
+    if (L.l_cpu > 0) {
+        const dim3 g4((unsigned)cdiv(cdiv(L.l_cpu, 16), 256), (unsigned)nh, 4);
+        if (bf) k_lab_keys<__nv_bfloat16><<<g4, 256, 0, s>>>(p);
+        else k_lab_keys<float><<<g4, 256, 0, s>>>(p);
+        FX_CUDA(cudaGetLastError());
+        k_lab_sort<<<dim3((unsigned)nh, kNL), kSortT, 0, s>>>(p);
+        FX_CUDA(cudaGetLastError());
+    }
+    if (bf) k_lab_scan<__nv_bfloat16><<<dim3((unsigned)nh, kNL), 128, 0, s>>>(p);
+    else k_lab_scan<float><<<dim3((unsigned)nh, kNL), 128, 0, s>>>(p);
+    FX_CUDA(cudaGetLastError());
+    k_lab_fit<<<(unsigned)cdiv(nh, 128), 128, 0, s>>>(p, nh);
+    FX_CUDA(cudaGetLastError());
+}
+
+}  // namespace fx

@@ -545,6 +545,32 @@ class SparseDecoder:
             return o.cpu().numpy().copy(), ls.cpu().numpy().copy()
         return o, ls
 
+    # -- output-aware labels (budget_oracle.cpp) --------------------------------
+    def label_heads(self, q: torch.Tensor, tau: float = 0.10, output_only: bool = False) -> dict:
+        """Oracle head properties of every query head (pipeline.cpp:256-276):
+        o_full, the per-sequence normalizer, label_streaming, min_budget at blk
+        1/16/32/64/128 and fit_curve -> dict of device tensors (bgt0, kslope,
+        streaming [B][H]; budgets, blocks [B][H][5]; o_full [B][H][D] f64;
+        normalizer [B]).  The metadata levels must have been built."""
+        lay = self.lay
+        B, H, D = lay.batch, self.heads, lay.head_dim
+        dev = self.eng.device
+        qd = q.to(dev, torch.float32).contiguous()
+        out = dict(o_full=torch.empty((B, H, D), dtype=torch.float64, device=dev),
+                   normalizer=torch.empty(B, dtype=torch.float64, device=dev),
+                   budgets=torch.empty((B, H, 5), dtype=torch.float64, device=dev),
+                   blocks=torch.empty((B, H, 5), dtype=torch.int64, device=dev),
+                   bgt0=torch.empty((B, H), dtype=torch.float64, device=dev),
+                   kslope=torch.empty((B, H), dtype=torch.float64, device=dev),
+                   streaming=torch.empty((B, H), dtype=torch.int32, device=dev))
+        meta = (C.c_void_p * 4)(*[m.data_ptr() for m in self.meta])
+        check(LIB.fx_label_heads(self.eng.ctx, C.byref(lay), _ptr(self.k), _ptr(self.v),
+                                 self.l_new, meta, _ptr(qd), float(tau), 1 if output_only else 0,
+                                 *[_ptr(out[n]) for n in ("o_full", "normalizer", "budgets",
+                                                          "blocks", "bgt0", "kslope",
+                                                          "streaming")]))
+        return out
+
     def selected_blocks(self, b: int, h: int) -> np.ndarray:
         """Ids of the blocks head h of sequence b selected in the last step."""
         g = h // self.lay.group_size
