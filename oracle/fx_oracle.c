@@ -655,3 +655,205 @@ FXO_API int fxo_oracle_props(const float* k, const float* v, size_t dim, size_t 
     *bgt0 = budgets_out[0];
     return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* Features -- features.cpp:26-224                                    */
+/* ------------------------------------------------------------------ */
+
+#define FXO_EMPTY_LSE (-1e6) /* kEmptyLse, features.hpp:16 */
+#define FXO_STATS_N 32        /* scalar fields of the flat PrefillStats record */
+
+/* compute_moments (features.cpp:26-46): mean, population var, skew, excess kurt. */
+FXO_API void fxo_moments(const double* x, size_t n, double* out4) {
+    double mean = 0.0, m2 = 0.0, m3 = 0.0, m4 = 0.0;
+    out4[0] = out4[1] = out4[2] = out4[3] = 0.0;
+    if (n == 0) return;
+    for (size_t i = 0; i < n; ++i) mean += x[i];
+    mean /= (double)n;
+    for (size_t i = 0; i < n; ++i) {
+        const double d = x[i] - mean;
+        m2 += d * d;
+        m3 += d * d * d;
+        m4 += d * d * d * d;
+    }
+    m2 /= (double)n;
+    m3 /= (double)n;
+    m4 /= (double)n;
+    out4[0] = mean;
+    out4[1] = m2;
+    if (m2 > 0.0) {
+        out4[2] = m3 / pow(m2, 1.5);
+        out4[3] = m4 / (m2 * m2) - 3.0;
+    }
+}
+
+static double fxo_l2_norm_f(const float* x, size_t n) { /* matrix.hpp:80-84 */
+    double s = 0.0;
+    for (size_t i = 0; i < n; ++i) s += (double)x[i] * (double)x[i];
+    return sqrt(s);
+}
+
+/* segment_summary (features.cpp:66-77): lse and output norm of one segment. */
+static void fxo_segment_summary(const float* q, const float* k, const float* v, size_t rows,
+                                size_t dim, double* lse, double* out_norm) {
+    *lse = FXO_EMPTY_LSE;
+    *out_norm = 0.0;
+    if (rows == 0) return;
+    double* o = (double*)malloc(dim * sizeof(double));
+    fxo_gathered_attention(q, k, v, dim, NULL, rows, o, lse);
+    *out_norm = fxo_l2_norm(o, dim);
+    free(o);
+}
+
+/* gpu_output_norm (features.cpp:81-84): ||default_kv_attention||, 0 if empty. */
+FXO_API double fxo_gpu_output_norm(const float* k, const float* v, size_t dim, size_t l_sink,
+                                   size_t l_cpu, size_t l_local, size_t l_new, const float* q) {
+    const fxo_cache c = {k, v, dim, l_sink, l_cpu, l_local, l_new};
+    double* o = (double*)malloc(dim * sizeof(double));
+    double* part = (double*)malloc(dim * sizeof(double));
+    double lse;
+    const size_t t = fxo_default_partial(&c, q, o, &lse, part);
+    const double r = t == 0 ? 0.0 : fxo_l2_norm(o, dim);
+    free(o);
+    free(part);
+    return r;
+}
+
+/* prefill_stats (features.cpp:86-157) as a flat record of FXO_STATS_N + 3 dim
+ * doubles: [0] layer [1] head [2] l_cpu [3] l_sink [4] l_local [5] cpu_empty
+ * [6] sink_key_norm_mean [7] sink_value_norm_mean [8..11] k_cpu_norms
+ * [12..15] v_cpu_norms [16..19] z_anchor [20..22] lse sink/cpu/local anchor
+ * [23..25] out norm sink/cpu/local anchor [26..29] budget_features
+ * [30] cross_head_max_anchor [31] ||anchor||, then mean_k_cpu[dim],
+ * mean_v_cpu[dim], anchor_query[dim]. */
+FXO_API void fxo_prefill_stats(const float* k, const float* v, size_t dim, size_t l_sink,
+                               size_t l_cpu, size_t l_local, const float* anchor,
+                               const double* budget_features, double cross_head_max_anchor,
+                               int layer, int head, double* rec) {
+    for (size_t i = 0; i < FXO_STATS_N + 3 * dim; ++i) rec[i] = 0.0;
+    double* mk = rec + FXO_STATS_N;
+    double* mv = mk + dim;
+    double* an = mv + dim;
+    rec[0] = layer;
+    rec[1] = head;
+    rec[2] = (double)l_cpu;
+    rec[3] = (double)l_sink;
+    rec[4] = (double)l_local;
+    rec[5] = l_cpu == 0;
+    for (size_t j = 0; j < dim; ++j) an[j] = (double)anchor[j];
+    for (int i = 0; i < 4; ++i) rec[26 + i] = budget_features[i];
+    rec[30] = cross_head_max_anchor;
+    rec[31] = fxo_l2_norm_f(anchor, dim);
+    const size_t nmax = l_cpu > l_sink ? l_cpu : l_sink;
+    double* tmp = (double*)malloc((nmax ? nmax : 1) * sizeof(double));
+    if (l_sink > 0) {
+        double s = 0.0;
+        for (size_t i = 0; i < l_sink; ++i) tmp[i] = fxo_l2_norm_f(k + i * dim, dim);
+        for (size_t i = 0; i < l_sink; ++i) s += tmp[i];
+        rec[6] = s / (double)l_sink;
+        s = 0.0;
+        for (size_t i = 0; i < l_sink; ++i) tmp[i] = fxo_l2_norm_f(v + i * dim, dim);
+        for (size_t i = 0; i < l_sink; ++i) s += tmp[i];
+        rec[7] = s / (double)l_sink;
+    }
+    const float* kc = k + l_sink * dim;
+    const float* vc = v + l_sink * dim;
+    if (l_cpu > 0) {
+        for (size_t i = 0; i < l_cpu; ++i)
+            for (size_t j = 0; j < dim; ++j) {
+                mk[j] += (double)kc[i * dim + j];
+                mv[j] += (double)vc[i * dim + j];
+            }
+        for (size_t j = 0; j < dim; ++j) {
+            mk[j] /= (double)l_cpu;
+            mv[j] /= (double)l_cpu;
+        }
+        for (size_t i = 0; i < l_cpu; ++i) tmp[i] = fxo_l2_norm_f(kc + i * dim, dim);
+        fxo_moments(tmp, l_cpu, rec + 8);
+        for (size_t i = 0; i < l_cpu; ++i) tmp[i] = fxo_l2_norm_f(vc + i * dim, dim);
+        fxo_moments(tmp, l_cpu, rec + 12);
+        const double qn = rec[31];
+        for (size_t i = 0; i < l_cpu; ++i) tmp[i] = 0.0;
+        if (qn > 0.0) {
+            const double denom = qn * sqrt((double)dim);
+            for (size_t i = 0; i < l_cpu; ++i) tmp[i] = fxo_dot(anchor, kc + i * dim, dim) / denom;
+        }
+        fxo_moments(tmp, l_cpu, rec + 16);
+        fxo_segment_summary(anchor, kc, vc, l_cpu, dim, &rec[21], &rec[24]);
+    } else {
+        rec[21] = FXO_EMPTY_LSE;
+    }
+    fxo_segment_summary(anchor, k, v, l_sink, dim, &rec[20], &rec[23]);
+    const size_t lo = l_sink + l_cpu;
+    fxo_segment_summary(anchor, k + lo * dim, v + lo * dim, l_local, dim, &rec[22], &rec[25]);
+    free(tmp);
+}
+
+/* approx_lse_cpu (features.cpp:159-170). */
+static double fxo_approx_lse_cpu(const float* q, const double* rec, size_t dim) {
+    const size_t l_cpu = (size_t)rec[2];
+    if (l_cpu == 0) return FXO_EMPTY_LSE;
+    const double qn = fxo_l2_norm_f(q, dim);
+    if (qn == 0.0) return log((double)l_cpu);
+    const double* mk = rec + FXO_STATS_N;
+    double qk = 0.0;
+    for (size_t j = 0; j < dim; ++j) qk += (double)q[j] * mk[j];
+    const double mu_q = qk / (qn * sqrt((double)dim));
+    return log((double)l_cpu) + qn * mu_q + 0.5 * qn * qn * rec[17];
+}
+
+/* decode_features (features.cpp:172-224) -> out[41]. */
+FXO_API void fxo_decode_features(const float* k, const float* v, size_t dim, size_t l_sink,
+                                 size_t l_cpu, size_t l_local, size_t l_new, const float* q,
+                                 const double* rec, double cross_head_max_now, double* f) {
+    const double* mk = rec + FXO_STATS_N;
+    const double* mv = mk + dim;
+    const double* an = mv + dim;
+    for (int i = 0; i < 41; ++i) f[i] = 0.0;
+    f[0] = rec[0];
+    f[1] = rec[1];
+    f[2] = rec[2];
+    f[3] = rec[3] + rec[4] + (double)l_new;
+    f[4] = rec[6];
+    f[5] = rec[7];
+    f[6] = fxo_l2_norm(mk, dim);
+    f[7] = fxo_l2_norm(mv, dim);
+    for (int i = 0; i < 4; ++i) {
+        f[8 + i] = rec[8 + i];
+        f[12 + i] = rec[12 + i];
+        f[17 + i] = rec[16 + i];
+    }
+    const double qn = fxo_l2_norm_f(q, dim);
+    if (qn > 0.0 && rec[5] == 0.0) {
+        double qk = 0.0;
+        for (size_t j = 0; j < dim; ++j) qk += (double)q[j] * mk[j];
+        f[16] = qk / (qn * sqrt((double)dim));
+    }
+    double lse_s, on_s, lse_l, on_l;
+    fxo_segment_summary(q, k, v, l_sink, dim, &lse_s, &on_s);
+    const size_t lo = l_sink + l_cpu;
+    fxo_segment_summary(q, k + lo * dim, v + lo * dim, l_local, dim, &lse_l, &on_l);
+    f[21] = lse_s;
+    f[22] = fxo_approx_lse_cpu(q, rec, dim);
+    f[23] = lse_l;
+    f[24] = rec[20];
+    f[25] = rec[21];
+    f[26] = rec[22];
+    f[27] = on_s;
+    f[28] = on_l;
+    f[29] = rec[23];
+    f[30] = rec[24];
+    f[31] = rec[25];
+    /* ||anchor|| over the float anchor (l2_norm of span<const float>) */
+    const double anorm = rec[31];
+    f[32] = qn;
+    f[33] = anorm;
+    if (qn > 0.0 && anorm > 0.0) {
+        double d = 0.0;
+        for (size_t j = 0; j < dim; ++j) d += (double)q[j] * an[j];
+        f[34] = d / (qn * anorm);
+    }
+    for (int i = 0; i < 4; ++i) f[35 + i] = rec[26 + i];
+    f[39] = cross_head_max_now;
+    f[40] = rec[30];
+}

@@ -103,6 +103,12 @@ class COracle:
                                              C.POINTER(C.c_double), C.POINTER(C.c_double),
                                              C.POINTER(C.c_int), _f64p]
         L.fxo_oracle_props.restype = C.c_int
+        L.fxo_moments.argtypes = [_f64p, _sz, _f64p]
+        L.fxo_gpu_output_norm.argtypes = seg
+        L.fxo_gpu_output_norm.restype = C.c_double
+        L.fxo_prefill_stats.argtypes = [_f32p, _f32p, _sz, _sz, _sz, _sz, _f32p, _f64p, C.c_double,
+                                        C.c_int, C.c_int, _f64p]
+        L.fxo_decode_features.argtypes = seg + [_f64p, C.c_double, _f64p]
         self.lib = L
 
     # -- block index ------------------------------------------------------
@@ -284,6 +290,33 @@ class COracle:
         return b0.value, ks.value, bool(st.value), buds
 
 
+    # -- features (features.cpp) -----------------------------------------------
+    STATS_N = 32
+
+    def moments(self, x):
+        out = np.zeros(4)
+        x = _f64(x)
+        self.lib.fxo_moments(x, len(x), out)
+        return out
+
+    def gpu_output_norm(self, k, v, seg, q):
+        return self.lib.fxo_gpu_output_norm(*self._seg(k, v, seg, q))
+
+    def prefill_stats(self, k, v, seg3, anchor, budget4, cross_anchor, layer, head):
+        """prefill_stats (features.cpp:86-157) -> flat record [32 + 3 D]."""
+        k, v = _f32(k), _f32(v)
+        D = k.shape[1]
+        rec = np.zeros(self.STATS_N + 3 * D)
+        self.lib.fxo_prefill_stats(k, v, D, *seg3, _f32(anchor), _f64(budget4), cross_anchor,
+                                   layer, head, rec)
+        return rec
+
+    def decode_features(self, k, v, seg, q, rec, cross_now):
+        out = np.zeros(41)
+        self.lib.fxo_decode_features(*self._seg(k, v, seg, q), _f64(rec), cross_now, out)
+        return out
+
+
 class RefOracle:
     """The compiled reference (oracle/_ref/libfluxref.so)."""
 
@@ -351,6 +384,10 @@ class RefOracle:
                                     C.POINTER(C.c_double), C.POINTER(C.c_double),
                                     C.POINTER(C.c_double)]
         L.ref_max_output_norm.argtypes = [_f64p, _sz, _sz, C.POINTER(C.c_double)]
+        L.ref_features.argtypes = [_f32p, _f32p, _sz, _sz, _sz, _sz, _sz, _f32p, _f64p, C.c_double,
+                                   C.c_int, C.c_int, _f32p, C.c_double, _f64p, _f64p]
+        L.ref_gpu_output_norm.argtypes = seg
+        L.ref_gpu_output_norm.restype = C.c_double
         self.lib = L
 
     def _check(self, rc):
@@ -496,6 +533,20 @@ class RefOracle:
         out = C.c_double(0)
         self._check(self.lib.ref_max_output_norm(outs, outs.shape[0], outs.shape[1], C.byref(out)))
         return out.value
+
+    def features(self, k, v, seg, anchor, budget4, cross_anchor, layer, head, q, cross_now):
+        """prefill_stats (no decoded rows) + decode_features -> (record, features[41])."""
+        k, v = _f32(k), _f32(v)
+        D = k.shape[1]
+        rec = np.zeros(32 + 3 * D)
+        f = np.zeros(41)
+        self._check(self.lib.ref_features(k, v, D, *seg, _f32(anchor), _f64(budget4), cross_anchor,
+                                          layer, head, _f32(q), cross_now, rec, f))
+        return rec, f
+
+    def gpu_output_norm(self, k, v, seg, q):
+        k, v = _f32(k), _f32(v)
+        return self.lib.ref_gpu_output_norm(k, v, k.shape[1], *seg, _f32(q))
 
     # -- executed scheduler (CPU baseline) -------------------------------
     def batch(self):

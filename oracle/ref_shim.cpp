@@ -479,4 +479,61 @@ int ref_max_output_norm(const double* outs, std::size_t n, std::size_t dim, doub
     });
 }
 
+// ---------------------------------------------------------------------------
+// features (features.cpp): prefill_stats on the cache without decoded rows,
+// then decode_features on the cache with l_new decoded rows.  rec: the flat
+// record of fx_oracle.c (FXO_STATS_N = 32 scalars, then mean_k, mean_v,
+// anchor); feats: 41 values.
+// ---------------------------------------------------------------------------
+int ref_features(const float* k, const float* v, std::size_t dim, std::size_t l_sink,
+                 std::size_t l_cpu, std::size_t l_local, std::size_t l_new, const float* anchor,
+                 const double* budget4, double cross_anchor, int layer, int head, const float* q,
+                 double cross_now, double* rec, double* feats) {
+    return guarded([&] {
+        const SegmentedKvCache pre = to_cache(k, v, dim, l_sink, l_cpu, l_local, 0);
+        const std::array<double, 4> bf{budget4[0], budget4[1], budget4[2], budget4[3]};
+        const PrefillStats st = prefill_stats(layer, head, pre, std::span<const float>(anchor, dim),
+                                              bf, cross_anchor);
+        std::fill(rec, rec + 32 + 3 * dim, 0.0);
+        rec[0] = st.layer;
+        rec[1] = st.head;
+        rec[2] = double(st.l_cpu);
+        rec[3] = double(st.l_sink);
+        rec[4] = double(st.l_local);
+        rec[5] = st.cpu_empty ? 1.0 : 0.0;
+        rec[6] = st.sink_key_norm_mean;
+        rec[7] = st.sink_value_norm_mean;
+        const Moments* ms[3] = {&st.k_cpu_norms, &st.v_cpu_norms, &st.z_anchor};
+        for (int i = 0; i < 3; ++i) {
+            rec[8 + 4 * i] = ms[i]->mean;
+            rec[9 + 4 * i] = ms[i]->var;
+            rec[10 + 4 * i] = ms[i]->skew;
+            rec[11 + 4 * i] = ms[i]->kurt;
+        }
+        rec[20] = st.lse_sink_anchor;
+        rec[21] = st.lse_cpu_anchor;
+        rec[22] = st.lse_local_anchor;
+        rec[23] = st.out_sink_anchor_norm;
+        rec[24] = st.out_cpu_anchor_norm;
+        rec[25] = st.out_local_anchor_norm;
+        for (int i = 0; i < 4; ++i) rec[26 + i] = st.budget_features[i];
+        rec[30] = st.cross_head_max_anchor;
+        rec[31] = l2_norm(std::span<const float>(st.anchor_query));
+        for (std::size_t j = 0; j < dim; ++j) {
+            rec[32 + j] = st.mean_k_cpu[j];
+            rec[32 + dim + j] = st.mean_v_cpu[j];
+            rec[32 + 2 * dim + j] = st.anchor_query[j];
+        }
+        const SegmentedKvCache cache = to_cache(k, v, dim, l_sink, l_cpu, l_local, l_new);
+        const FeatureVector f = decode_features(std::span<const float>(q, dim), cache, st, cross_now);
+        std::copy(f.begin(), f.end(), feats);
+    });
+}
+
+double ref_gpu_output_norm(const float* k, const float* v, std::size_t dim, std::size_t l_sink,
+                           std::size_t l_cpu, std::size_t l_local, std::size_t l_new, const float* q) {
+    const SegmentedKvCache cache = to_cache(k, v, dim, l_sink, l_cpu, l_local, l_new);
+    return gpu_output_norm(std::span<const float>(q, dim), cache);
+}
+
 } // extern "C"

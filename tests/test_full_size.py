@@ -231,3 +231,46 @@ def test_c5_full_size_context_parallel(engine, coracle):
     torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
     _check_plans(full, coracle, props)
     _check_groups(full, coracle, q, _retrieval_groups(full, 1))
+
+
+def test_c3_output_aware_budgets_full_size(engine, coracle):
+    """C3 as BASELINE.json states it: Qwen layer, 256K, batch 8, output-aware
+    budgets -- the oracle head properties (pipeline.cpp:256-276) labelled on
+    the device for all 224 heads, checked against the C oracle on sampled
+    heads (min_budget at blk 1..128 over the 261,824-row cpu segment), then
+    fed to the on-device selector and the decode step."""
+    B, Hkv, G, D, l_cpu = 8, 4, 7, 128, 262144 - 320
+    dec = _decoder(engine, B, Hkv, G, D, l_cpu, seed=33)
+    q = _queries(B, Hkv * G, D, seed=13, dev=engine.device)
+    lab = dec.label_heads(q, tau=0.10)
+    torch.cuda.synchronize()
+    seg = (dec.lay.l_sink, l_cpu, dec.lay.l_local, 0)
+    qn = q.cpu().numpy()
+    nrm = lab["normalizer"].cpu().numpy()
+    bud = lab["budgets"].cpu().numpy()
+    st = lab["streaming"].cpu().numpy()
+    near = 0
+    for b, h in [(0, 0), (3, 11), (7, 27)]:
+        k, v = _group_host(dec, b, h // G)
+        o_full = coracle.cache_attention(k, v, seg, qn[b, h])
+        assert np.allclose(lab["o_full"][b, h].cpu().numpy(), o_full, rtol=1e-9, atol=1e-12)
+        assert bool(st[b, h]) == coracle.label_streaming(k, v, seg, qn[b, h], o_full, nrm[b], 0.10)
+        if st[b, h]:
+            continue
+        for i, blk in enumerate((1, 16, 32, 64, 128)):
+            w_b, w_n, _ = coracle.min_budget(k, v, seg, qn[b, h], blk, o_full, nrm[b], 0.10)
+            got = int(lab["blocks"][b, h, i])
+            if got != w_n:
+                assert abs(got - w_n) <= 1
+                near += 1
+            else:
+                assert bud[b, h, i] == w_b
+    assert near <= 1
+    props = (lab["bgt0"], lab["kslope"], lab["streaming"])
+    dec.o.fill_(float("nan"))
+    dec.step(q, props=props)
+    torch.cuda.synchronize()
+    assert torch.isfinite(dec.o).all()
+    _check_plans(dec, coracle, tuple(t.cpu().numpy() for t in props))
+    _check_counts(dec)
+    _check_groups(dec, coracle, q, _retrieval_groups(dec, 2))
