@@ -246,6 +246,28 @@ FX_API int fx_label_heads(fx_ctx* ctx, const fx_layout* lay, const void* k, cons
                           int32_t criterion, double* o_full, double* normalizer, double* budgets,
                           int64_t* blocks, double* bgt0, double* kslope, int32_t* streaming);
 
+/* ---- predictor features (features.cpp) ------------------------------------ */
+#define FX_STATS_SCALARS 32 /* flat PrefillStats record: 32 scalars + 3 * head_dim */
+/* prefill_stats (features.cpp:86-157) for every head, on the prefill cache
+ * (no decoded rows): rec [dev] [B][H][32 + 3 D] f64 -- [0] layer [1] head
+ * [2] l_cpu [3] l_sink [4] l_local [5] cpu_empty [6..7] sink key/value norm
+ * means [8..11] / [12..15] cpu key / value row-norm moments [16..19] z_anchor
+ * moments [20..22] anchor lse sink/cpu/local [23..25] anchor output norms
+ * [26..29] budget features (min_budget at blk 16..128 for the anchor, the
+ * step normalizer; pipeline.cpp:37-46) [30] cross_head_max_anchor
+ * [31] ||anchor||, then mean_k_cpu[D], mean_v_cpu[D], anchor[D].
+ * anchor [dev] [B][H][D] f32.  Synchronizes the ctx stream. */
+FX_API int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
+                            const void* const meta[4], const float* anchor, double tau,
+                            int32_t layer, double* rec);
+/* decode_features (features.cpp:172-224) for every head: features [dev]
+ * [B][H][41] f64 from the step's q [dev] [B][H][D], the cache with l_new
+ * decoded rows and the prefill records; feature 39 (cross_head_max_q) is the
+ * max over the heads of each sequence of gpu_output_norm (features.cpp:81-84).
+ * Feed to fx_predict. */
+FX_API int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
+                              int64_t l_new, const float* q, const double* rec, double* features);
+
 /* ---- context-parallel decode (C5) ------------------------------------------
  * The cpu segment is split into contiguous 128-row-aligned shards, one per
  * rank (sink rows on rank 0, local + decoded rows on the last rank), so block

@@ -97,6 +97,9 @@ _SIGS = {
     "fx_cp_select": (C.c_int, [_p, C.POINTER(Layout), _i32, _i32, _i64, _p, _p, _p, _p, _p, _i64,
                                _p, _i32]),
     "fx_cp_combine": (C.c_int, [_p, _i32, _i64, _i32, _p, _p, _p, _p]),
+    "fx_prefill_stats": (C.c_int, [_p, C.POINTER(Layout), _p, _p, C.POINTER(_p * 4), _p,
+                                   C.c_double, _i32, _p]),
+    "fx_decode_features": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p]),
     "fx_label_heads": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, C.POINTER(_p * 4), _p,
                                  C.c_double, _i32, _p, _p, _p, _p, _p, _p, _p]),
 }

@@ -813,6 +813,73 @@ int fx_label_heads(fx_ctx* ctx, const fx_layout* lay, const void* k, const void*
     });
 }
 
+// ---- predictor features (features.cpp) -------------------------------------
+
+int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
+                     const void* const meta[4], const float* anchor, double tau, int32_t layer,
+                     double* rec) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const fx_layout& L = *lay;
+        FX_REQUIRE(k && v && anchor && rec, FX_ERR_STATE, "no-context: prefill has no payload");
+        FX_REQUIRE(L.l_sink + L.l_cpu + L.l_local > 0, FX_ERR_INVALID,
+                   "empty-context: cache has no tokens");
+        if (L.l_cpu > 0)
+            for (int i = 0; i < 4; ++i)
+                FX_REQUIRE(meta && meta[i], FX_ERR_STATE, "no-context: missing block metadata");
+        const void* mp[4] = {nullptr, nullptr, nullptr, nullptr};
+        if (meta)
+            for (int i = 0; i < 4; ++i) mp[i] = meta[i];
+        const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
+        const size_t lab = fx::label_scratch_bytes(L, 0);
+        // label outputs the prefill only consumes internally, then the group accumulators
+        const size_t outs = (size_t)nh * L.head_dim * 8 + (size_t)L.batch * 8 + (size_t)nh * 5 * 8 * 2 +
+                            (size_t)nh * 8 * 3 + 4096;
+        ctx->label.ensure(lab + outs + fx::prefill_group_scratch_bytes(L) + 256);
+        char* b = static_cast<char*>(ctx->label.p) + lab;
+        auto take = [&](size_t bytes) {
+            char* r = b;
+            b += (bytes + 255) & ~size_t(255);
+            return r;
+        };
+        double* o_full = reinterpret_cast<double*>(take((size_t)nh * L.head_dim * 8));
+        double* nrm = reinterpret_cast<double*>(take((size_t)L.batch * 8));
+        double* bud = reinterpret_cast<double*>(take((size_t)nh * 5 * 8));
+        int64_t* blocks = reinterpret_cast<int64_t*>(take((size_t)nh * 5 * 8));
+        double* b0 = reinterpret_cast<double*>(take((size_t)nh * 8));
+        double* ks = reinterpret_cast<double*>(take((size_t)nh * 8));
+        int32_t* st = reinterpret_cast<int32_t*>(take((size_t)nh * 4));
+        int32_t* err = reinterpret_cast<int32_t*>(take(4));
+        void* grp = take(fx::prefill_group_scratch_bytes(L));
+        fx::launch_label(L, k, v, 0, anchor, mp, tau, 0, ctx->label.p, o_full, nrm, bud, blocks, b0, ks,
+                         st, err, ctx->stream, rec, layer);
+        fx::launch_prefill_group(L, k, v, rec, grp, ctx->stream);
+        ctx->launches += (L.l_cpu > 0 ? 8 : 6) + 3;
+        int32_t h_err = 0;
+        FX_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        FX_CUDA(cudaStreamSynchronize(ctx->stream));
+        FX_REQUIRE(h_err == 0, FX_ERR_INVALID, "degenerate-normalizer: all head outputs are zero");
+    });
+}
+
+int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
+                       int64_t l_new, const float* q, const double* rec, double* features) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const fx_layout& L = *lay;
+        FX_REQUIRE(k && v && q && rec && features, FX_ERR_STATE, "no-context: features have no payload");
+        FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_new <= L.l_cap, FX_ERR_INVALID,
+                   "bad-shape: decoded rows exceed l_cap");
+        const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
+        ctx->api.ensure((size_t)nh * 8 + 256);
+        fx::launch_decode_features(L, k, v, l_new, q, rec, features, static_cast<double*>(ctx->api.p),
+                                   ctx->stream);
+        ctx->launches += 2;
+    });
+}
+
 // ---- context-parallel decode (C5) ----------------------------------------
 
 int fx_cp_candidates(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, int64_t cap,

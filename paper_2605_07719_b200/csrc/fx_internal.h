@@ -126,12 +126,32 @@ void launch_topk_exact(const float* q, const void* meta, int dtype, int64_t nblk
 void launch_meta_absmax(const void* meta, int dtype, int64_t nblk, int dim, float* absmax,
                         cudaStream_t s);
 
-// fx_label.cu: output-aware head labels (budget_oracle.cpp); device outputs
+// Flat PrefillStats record (features.hpp:85-110), kStatsN + 3 D doubles per
+// head: [0] layer [1] head [2] l_cpu [3] l_sink [4] l_local [5] cpu_empty
+// [6] sink_key_norm_mean [7] sink_value_norm_mean [8..11] k_cpu_norms
+// [12..15] v_cpu_norms [16..19] z_anchor [20..22] lse sink/cpu/local anchor
+// [23..25] out norm sink/cpu/local anchor [26..29] budget_features
+// [30] cross_head_max_anchor [31] ||anchor||, then mean_k_cpu[D],
+// mean_v_cpu[D], anchor_query[D] (the oracle's fxo_prefill_stats layout).
+constexpr int kStatsN = 32;
+constexpr double kEmptyLseDev = -1e6;  // kEmptyLse, features.hpp:16
+
+// fx_label.cu: output-aware head labels (budget_oracle.cpp); device outputs.
+// prefill_rec != nullptr: q is the anchor and the anchor-side record fields
+// are written too (features.cpp:86-157).
 size_t label_scratch_bytes(const fx_layout& L, int64_t l_new);
 void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_new, const float* q,
                   const void* const meta[4], double tau, int criterion, void* scratch,
                   double* o_full, double* normalizer, double* budgets, int64_t* blocks,
-                  double* bgt0, double* kslope, int32_t* streaming, int32_t* err, cudaStream_t s);
+                  double* bgt0, double* kslope, int32_t* streaming, int32_t* err, cudaStream_t s,
+                  double* prefill_rec = nullptr, int layer = 0);
+// fx_features.cu: KV-only prefill fields (group statistics) and decode features
+void launch_prefill_group(const fx_layout& L, const void* k, const void* v, double* rec,
+                          void* scratch, cudaStream_t s);
+size_t prefill_group_scratch_bytes(const fx_layout& L);
+void launch_decode_features(const fx_layout& L, const void* k, const void* v, int64_t l_new,
+                            const float* q, const double* rec, double* feats, double* gpu_norm,
+                            cudaStream_t s);
 
 // fx_attend.cu
 // 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},

@@ -51,10 +51,14 @@ struct LabelView {
     double tau;
     double* S;            // [nh][Lr] q.k, then weights e
     uint64_t* hmax;       // [nh] f64_key(max q.k / sqrt(D))
-    double* Of;           // [nh][D] sum e v, all rows
+    double* Oseg;         // [nh][4][D] sum e v per segment (sink, cpu, local, new)
+    double* Zseg;         // [nh][4]    sum e per segment
+    double* Of;           // [nh][D] sum e v, all rows      (from the segments)
     double* Od;           // [nh][D] sum e v, default rows
     double* Zf;           // [nh]
     double* Zd;           // [nh]
+    double* zsum;         // [nh] sum over cpu rows of q.k (prefill z moments; null = off)
+    double* zc;           // [nh][3] sum (z - mean)^2,3,4 over cpu rows
     double* o_full;       // [nh][D]
     double* normalizer;   // [B]
     double* nrm_head;     // [nh] normalizer used for head h
@@ -130,6 +134,12 @@ __global__ void __launch_bounds__(256) k_lab_scores(const LabelView p) {
             p.keys[0][head * n_tot + (t - p.l_sink)] = ~f64_key(s[h]);
             p.ids[0][head * n_tot + (t - p.l_sink)] = (uint32_t)(t - p.l_sink);
         }
+        if (p.zsum) {
+            double z = cpu ? s[h] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+            if ((threadIdx.x & 31) == 0 && z != 0.0) atomicAdd(p.zsum + head, z);
+        }
         uint64_t m = live ? f64_key(__dmul_rn(s[h], isd)) : 0ull;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -140,24 +150,58 @@ __global__ void __launch_bounds__(256) k_lab_scores(const LabelView p) {
     }
 }
 
-// K_sums: weights in place and the f64 sums over all rows / default rows.
+// K_sums: weights in place and the f64 sums per segment (sink, cpu, local,
+// new); with p.zsum set, also the central powers of the prefill z values
+// (features.cpp:132-139) from the raw dots before they are replaced.
+__device__ __forceinline__ int seg_of(const LabelView& p, int64_t t) {
+    return t < p.l_sink ? 0 : t < p.l_sink + p.l_cpu ? 1 : t < p.l_sink + p.l_cpu + p.l_local ? 2 : 3;
+}
 template <typename T>
 __global__ void __launch_bounds__(128) k_lab_sums(const LabelView p) {
     __shared__ double e_s[128][kMaxG];
-    __shared__ unsigned char dflt[128];
+    __shared__ double zst[kMaxG][2];  // z mean, 1 / denominator
     const int bg = blockIdx.y, G = p.G, D = p.D;
     const int64_t t0 = (int64_t)blockIdx.x * 128;
     const double isd = 1.0 / sqrt((double)D);
+    const int nrow = (int)(p.Lr - t0 < 128 ? p.Lr - t0 : 128);
+    if (p.zsum && threadIdx.x < G) {  // ||q|| (matrix.hpp:80-84), z = q.k / (||q|| sqrt D)
+        const int h = threadIdx.x;
+        const float* qh = p.q + ((int64_t)bg * G + h) * D;
+        double n2 = 0.0;
+        for (int d = 0; d < D; ++d) n2 += (double)qh[d] * (double)qh[d];
+        const double qn = sqrt(n2);
+        const double den = qn * sqrt((double)D);
+        const double inv = qn > 0.0 ? 1.0 / den : 0.0;
+        zst[h][0] = p.l_cpu > 0 ? p.zsum[(int64_t)bg * G + h] * inv / (double)p.l_cpu : 0.0;
+        zst[h][1] = inv;
+    }
+    __syncthreads();
     {
         const int64_t t = t0 + threadIdx.x;
         const bool live = t < p.Lr;
-        dflt[threadIdx.x] = live && (t < p.l_sink || t >= p.l_sink + p.l_cpu);
+        const bool cpu = live && t >= p.l_sink && t < p.l_sink + p.l_cpu;
         for (int h = 0; h < G; ++h) {
             const int64_t head = (int64_t)bg * G + h;
+            const double raw = live ? p.S[head * p.Lr + t] : 0.0;
+            if (p.zsum) {  // central powers of z over the cpu rows (warp-uniform branch)
+                const double dz = cpu ? raw * zst[h][1] - zst[h][0] : 0.0;
+                double c2 = dz * dz, c3 = c2 * dz, c4 = c2 * c2;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+                    c3 += __shfl_xor_sync(0xffffffffu, c3, o);
+                    c4 += __shfl_xor_sync(0xffffffffu, c4, o);
+                }
+                if ((threadIdx.x & 31) == 0 && c2 != 0.0) {
+                    atomicAdd(p.zc + head * 3, c2);
+                    atomicAdd(p.zc + head * 3 + 1, c3);
+                    atomicAdd(p.zc + head * 3 + 2, c4);
+                }
+            }
             double e = 0.0;
             if (live) {
                 const double m = key_f64(p.hmax[head]);
-                e = exp(__dmul_rn(p.S[head * p.Lr + t], isd) - m);
+                e = exp(__dmul_rn(raw, isd) - m);
                 p.S[head * p.Lr + t] = e;
             }
             e_s[threadIdx.x][h] = e;
@@ -165,39 +209,34 @@ __global__ void __launch_bounds__(128) k_lab_sums(const LabelView p) {
     }
     __syncthreads();
     const int d = threadIdx.x;
-    const int nrow = (int)(p.Lr - t0 < 128 ? p.Lr - t0 : 128);
-    double af[kMaxG], ad[kMaxG];
+    // rows [t0, t0 + nrow) split at segment boundaries: one flush per segment
+    int i = 0;
+    while (i < nrow) {
+        const int sg = seg_of(p, t0 + i);
+        int j = i + 1;
+        while (j < nrow && seg_of(p, t0 + j) == sg) ++j;
+        if (d < D) {
+            double a[kMaxG];
 #pragma unroll
-    for (int h = 0; h < kMaxG; ++h) af[h] = ad[h] = 0.0;
-    if (d < D) {
-        const T* vb = static_cast<const T*>(p.v) + ((int64_t)bg * p.l_cap + t0) * D + d;
-        for (int i = 0; i < nrow; ++i) {
-            const double vd = (double)tofl(vb[(int64_t)i * D]);
-            const bool df = dflt[i];
+            for (int h = 0; h < kMaxG; ++h) a[h] = 0.0;
+            const T* vb = static_cast<const T*>(p.v) + ((int64_t)bg * p.l_cap + t0) * D + d;
+            for (int r = i; r < j; ++r) {
+                const double vd = (double)tofl(vb[(int64_t)r * D]);
+#pragma unroll
+                for (int h = 0; h < kMaxG; ++h)
+                    if (h < G) a[h] += e_s[r][h] * vd;
+            }
 #pragma unroll
             for (int h = 0; h < kMaxG; ++h)
-                if (h < G) {
-                    const double w = e_s[i][h] * vd;
-                    af[h] += w;
-                    if (df) ad[h] += w;
-                }
+                if (h < G) atomicAdd(p.Oseg + (((int64_t)bg * G + h) * 4 + sg) * D + d, a[h]);
         }
-        for (int h = 0; h < G; ++h) {
-            const int64_t head = (int64_t)bg * G + h;
-            atomicAdd(p.Of + head * D + d, af[h]);
-            atomicAdd(p.Od + head * D + d, ad[h]);
+        if (threadIdx.x < G) {
+            const int h = threadIdx.x;
+            double z = 0.0;
+            for (int r = i; r < j; ++r) z += e_s[r][h];
+            atomicAdd(p.Zseg + ((int64_t)bg * G + h) * 4 + sg, z);
         }
-    }
-    if (threadIdx.x < G) {
-        const int h = threadIdx.x;
-        double zf = 0.0, zd = 0.0;
-        for (int i = 0; i < nrow; ++i) {
-            zf += e_s[i][h];
-            if (dflt[i]) zd += e_s[i][h];
-        }
-        const int64_t head = (int64_t)bg * G + h;
-        atomicAdd(p.Zf + head, zf);
-        atomicAdd(p.Zd + head, zd);
+        i = j;
     }
 }
 
@@ -221,10 +260,21 @@ __global__ void __launch_bounds__(128) k_lab_norm(const LabelView p) {
     double nrm = 0.0;
     for (int h = 0; h < H; ++h) {
         const int64_t head = (int64_t)b * H + h;
-        const double zf = p.Zf[head];
+        const double* zs = p.Zseg + head * 4;
+        const double zd = zs[0] + zs[2] + zs[3];
+        const double zf = zd + zs[1];
+        if (d == 0) {
+            p.Zf[head] = zf;
+            p.Zd[head] = zd;
+        }
         double of = 0.0;
         if (d < D) {
-            of = zf > 0.0 ? p.Of[head * D + d] / zf : 0.0;
+            const double* os = p.Oseg + head * 4 * D + d;
+            const double od = os[0] + os[2 * D] + os[3 * D];
+            const double oa = od + os[D];
+            p.Od[head * D + d] = od;
+            p.Of[head * D + d] = oa;
+            of = zf > 0.0 ? oa / zf : 0.0;
             p.o_full[head * D + d] = of;
         }
         const double n2 = sqrt(block_sum(d < D ? of * of : 0.0, red));
@@ -235,11 +285,13 @@ __global__ void __launch_bounds__(128) k_lab_norm(const LabelView p) {
     for (int h = 0; h < H; ++h) {
         const int64_t head = (int64_t)b * H + h;
         const double nh = p.criterion == 1 ? hn[min(h, 1023)] : nrm;
-        const double zd = p.Zd[head];
+        const double* zs = p.Zseg + head * 4;
+        const double zd = zs[0] + zs[2] + zs[3];
         double x = 0.0;
         if (d < D) {
             const double of = p.o_full[head * D + d];
-            x = zd > 0.0 ? p.Od[head * D + d] / zd - of : of;  // empty defaults: ||o_full||
+            const double* os = p.Oseg + head * 4 * D + d;
+            x = zd > 0.0 ? (os[0] + os[2 * D] + os[3 * D]) / zd - of : of;  // empty defaults: ||o_full||
         }
         const double dev = sqrt(block_sum(x * x, red)) / nh;
         if (d == 0) {
@@ -478,6 +530,73 @@ __global__ void k_lab_fit(const LabelView p, int64_t nh) {
     p.bgt0[head] = b[0];
 }
 
+// Anchor-side fields of the prefill record (features.cpp:86-157; layout in
+// fx_internal.h kStats*): one CTA per sequence b; the KV-only (group) fields
+// come from fx_features.cu.
+__global__ void __launch_bounds__(128) k_pf_anchor(const LabelView p, double* rec, int layer) {
+    __shared__ double red[8];
+    const int b = blockIdx.x, H = p.Hkv * p.G, D = p.D, d = threadIdx.x;
+    const int RS = kStatsN + 3 * D;
+    double cross = 0.0;
+    for (int h = 0; h < H; ++h) {  // cross_head_max_anchor = max_h gpu_output_norm(anchor_h)
+        const int64_t head = (int64_t)b * H + h;
+        const double* zs = p.Zseg + head * 4;
+        const double zd = zs[0] + zs[2] + zs[3];
+        double x = 0.0;
+        if (d < D && zd > 0.0) x = p.Od[head * D + d] / zd;
+        const double n = sqrt(block_sum(x * x, red));
+        cross = fmax(cross, zd > 0.0 ? n : 0.0);
+    }
+    for (int h = 0; h < H; ++h) {
+        const int64_t head = (int64_t)b * H + h;
+        double* r = rec + head * RS;
+        const double m = key_f64(p.hmax[head]);
+        const double* zs = p.Zseg + head * 4;
+        double on[3];
+        const int segs[3] = {0, 1, 2};  // sink, cpu, local (prefill cache: no decoded rows)
+        for (int i = 0; i < 3; ++i) {
+            const double z = zs[segs[i]];
+            const double x = (d < D && z > 0.0) ? p.Oseg[(head * 4 + segs[i]) * D + d] / z : 0.0;
+            on[i] = sqrt(block_sum(x * x, red));
+        }
+        const float* an = p.q + head * D;
+        const double a2 = block_sum(d < D ? (double)an[d] * (double)an[d] : 0.0, red);
+        if (d < D) r[kStatsN + 2 * D + d] = (double)an[d];
+        if (d == 0) {
+            const int64_t lens[3] = {p.l_sink, p.l_cpu, p.l_local};
+            r[0] = layer;
+            r[1] = h;
+            r[2] = (double)p.l_cpu;
+            r[3] = (double)p.l_sink;
+            r[4] = (double)p.l_local;
+            r[5] = p.l_cpu == 0 ? 1.0 : 0.0;
+            for (int i = 0; i < 3; ++i) {
+                const bool live = lens[i] > 0 && zs[segs[i]] > 0.0;
+                r[20 + i] = live ? m + log(zs[segs[i]]) : kEmptyLseDev;
+                r[23 + i] = live ? on[i] : 0.0;
+            }
+            // z moments (mean, population var, skew, excess kurt; zero-variance -> 0, 0)
+            double zm[4] = {0.0, 0.0, 0.0, 0.0};
+            if (p.l_cpu > 0) {
+                const double qn = sqrt(a2);
+                const double inv = qn > 0.0 ? 1.0 / (qn * sqrt((double)D)) : 0.0;
+                const double n = (double)p.l_cpu;
+                zm[0] = p.zsum[head] * inv / n;
+                const double m2 = p.zc[head * 3] / n, m3 = p.zc[head * 3 + 1] / n, m4 = p.zc[head * 3 + 2] / n;
+                zm[1] = m2;
+                if (m2 > 0.0) {
+                    zm[2] = m3 / pow(m2, 1.5);
+                    zm[3] = m4 / (m2 * m2) - 3.0;
+                }
+            }
+            for (int i = 0; i < 4; ++i) r[16 + i] = zm[i];
+            for (int i = 0; i < 4; ++i) r[26 + i] = p.budgets[head * kNL + 1 + i];
+            r[30] = cross;
+            r[31] = sqrt(a2);
+        }
+    }
+}
+
 }  // namespace
 
 size_t label_scratch_bytes(const fx_layout& L, int64_t l_new) {
@@ -487,13 +606,15 @@ size_t label_scratch_bytes(const fx_layout& L, int64_t l_new) {
     for (int i = 1; i < kNL; ++i) n_tot += cdiv(L.l_cpu, kLevels[i - 1]);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     return al((size_t)nh * Lr * 8) + 2 * al((size_t)nh * n_tot * 8) + 2 * al((size_t)nh * n_tot * 4) +
-           4 * al((size_t)nh * 8) + 2 * al((size_t)nh * L.head_dim * 8);
+           5 * al((size_t)nh * 8) + 2 * al((size_t)nh * L.head_dim * 8) +
+           al((size_t)nh * 4 * L.head_dim * 8) + al((size_t)nh * 4 * 8) + al((size_t)nh * 3 * 8);
 }
 
 void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_new, const float* q,
                   const void* const meta[4], double tau, int criterion, void* scratch,
                   double* o_full, double* normalizer, double* budgets, int64_t* blocks,
-                  double* bgt0, double* kslope, int32_t* streaming, int32_t* err, cudaStream_t s) {
+                  double* bgt0, double* kslope, int32_t* streaming, int32_t* err, cudaStream_t s,
+                  double* prefill_rec, int layer) {
     FX_REQUIRE(L.group_size <= kMaxG && L.head_dim <= 128 && L.head_dim % 8 == 0 &&
                    L.group_size * L.head_dim <= kMaxG * 256,
                FX_ERR_INVALID, "bad-shape: labels need group_size <= 16 and head_dim <= 128 (multiple of 8)");
@@ -539,7 +660,12 @@ void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_ne
     p.Od = reinterpret_cast<double*>(take((size_t)nh * D * 8));
     p.Zf = reinterpret_cast<double*>(take((size_t)nh * 8));
     p.Zd = reinterpret_cast<double*>(take((size_t)nh * 8));
+    p.Oseg = reinterpret_cast<double*>(take((size_t)nh * 4 * D * 8));
+    p.Zseg = reinterpret_cast<double*>(take((size_t)nh * 4 * 8));
+    p.zsum = reinterpret_cast<double*>(take((size_t)nh * 8));
+    p.zc = reinterpret_cast<double*>(take((size_t)nh * 3 * 8));
     char* zero1 = c;
+    if (!prefill_rec) p.zsum = p.zc = nullptr;
     p.nrm_head = reinterpret_cast<double*>(take((size_t)nh * 8));
     p.o_full = o_full;
     p.normalizer = normalizer;
@@ -575,6 +701,10 @@ void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_ne
     FX_CUDA(cudaGetLastError());
     k_lab_fit<<<(unsigned)cdiv(nh, 128), 128, 0, s>>>(p, nh);
     FX_CUDA(cudaGetLastError());
+    if (prefill_rec) {
+        k_pf_anchor<<<(unsigned)L.batch, 128, 0, s>>>(p, prefill_rec, layer);
+        FX_CUDA(cudaGetLastError());
+    }
 }
 
 }  // namespace fx

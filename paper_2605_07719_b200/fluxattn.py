@@ -571,6 +571,34 @@ class SparseDecoder:
                                                           "streaming")]))
         return out
 
+    # -- predictor features (features.cpp) ---------------------------------------
+    STATS_SCALARS = 32
+
+    def prefill_stats(self, anchor: torch.Tensor, tau: float = 0.10, layer: int = 0) -> torch.Tensor:
+        """prefill_stats (features.cpp:86-157) of every head on the prefill cache
+        (no decoded rows): flat records [B][H][32 + 3 D] f64 on the device (layout
+        in include/fluxattn_b200.h).  Budget features: min_budget of the anchor at
+        blk 16..128 (pipeline.cpp:37-46)."""
+        lay = self.lay
+        rec = torch.zeros((lay.batch, self.heads, self.STATS_SCALARS + 3 * lay.head_dim),
+                          dtype=torch.float64, device=self.eng.device)
+        meta = (C.c_void_p * 4)(*[m.data_ptr() for m in self.meta])
+        a = anchor.to(self.eng.device, torch.float32).contiguous()
+        check(LIB.fx_prefill_stats(self.eng.ctx, C.byref(lay), _ptr(self.k), _ptr(self.v), meta,
+                                   _ptr(a), float(tau), int(layer), _ptr(rec)))
+        return rec
+
+    def decode_features(self, q: torch.Tensor, rec: torch.Tensor,
+                        out: torch.Tensor = None) -> torch.Tensor:
+        """decode_features (features.cpp:172-224) of every head -> [B][H][41] f64."""
+        lay = self.lay
+        f = out if out is not None else torch.empty((lay.batch, self.heads, 41), dtype=torch.float64,
+                                                    device=self.eng.device)
+        qd = q.to(self.eng.device, torch.float32).contiguous()
+        check(LIB.fx_decode_features(self.eng.ctx, C.byref(lay), _ptr(self.k), _ptr(self.v),
+                                     self.l_new, _ptr(qd), _ptr(rec), _ptr(f)))
+        return f
+
     def selected_blocks(self, b: int, h: int) -> np.ndarray:
         """Ids of the blocks head h of sequence b selected in the last step."""
         g = h // self.lay.group_size
@@ -581,3 +609,40 @@ class SparseDecoder:
         w = self.sel_bits[b, h].cpu().numpy().view(np.uint32)
         bits = np.unpackbits(w.view(np.uint8), bitorder="little")[:nblk]
         return np.nonzero(bits)[0]
+
+
+class Predictor:
+    """A 41->256->384->3 head-property predictor resident on the device
+    (predictor.cpp:161-185); params as the oracle's make_model dict."""
+
+    NAMES = ("w1", "b1", "w2", "b2", "w3", "b3", "mu", "sigma")
+
+    def __init__(self, engine: Engine, params: dict):
+        self.eng = engine
+        self._host = [np.ascontiguousarray(params[n], np.float64) for n in self.NAMES]
+        h = C.c_void_p()
+        check(LIB.fx_model_create(engine.ctx, *[a.ctypes.data for a in self._host], C.byref(h)))
+        self.h = h
+
+    def __call__(self, feats: torch.Tensor):
+        """features [..][41] f64 device -> (bgt0, kslope, streaming) shaped like feats[..., 0]."""
+        shape = feats.shape[:-1]
+        n = int(np.prod(shape)) if len(shape) else 1
+        dev = self.eng.device
+        b0 = torch.empty(shape, dtype=torch.float64, device=dev)
+        ks = torch.empty(shape, dtype=torch.float64, device=dev)
+        st = torch.empty(shape, dtype=torch.int32, device=dev)
+        check(LIB.fx_predict(self.eng.ctx, self.h, n, _ptr(feats.contiguous()), _ptr(b0), _ptr(ks),
+                             _ptr(st), None))
+        return b0, ks, st
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.fx_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
