@@ -174,105 +174,137 @@ __global__ void __launch_bounds__(128) k_pfg_write(fx_layout L, GroupAcc acc, do
 // ---------------------------------------------------------------------------
 // decode features
 // ---------------------------------------------------------------------------
-// One segment's attention summary for the query in qs: lse and output norm
-// (segment_summary, features.cpp:66-77); scores of its rows in s (by row).
-template <typename T>
-__device__ void seg_summary(const T* K, const T* V, int64_t r0, int n, int D, const double* qs,
-                            double* s, double* red, double isd, double* lse, double* onorm) {
-    const int t = threadIdx.x;
-    for (int i = t; i < n; i += blockDim.x) {
-        const T* kr = K + (r0 + i) * D;
-        double a = 0.0;
-        for (int d = 0; d < D; ++d) a += qs[d] * (double)tofl(kr[d]);
-        s[i] = a * isd;
-    }
-    __syncthreads();
-    double mx = -INFINITY;
-    for (int i = t; i < n; i += blockDim.x) mx = fmax(mx, s[i]);
-    const double m = block_max128(mx, red);
-    double z = 0.0;
-    for (int i = t; i < n; i += blockDim.x) z += exp(s[i] - m);
-    const double Z = block_sum128(z, red);
-    double o = 0.0;
-    if (t < D)
-        for (int i = 0; i < n; ++i) o += exp(s[i] - m) * (double)tofl(V[(r0 + i) * D + t]);
-    o = t < D ? o / Z : 0.0;
-    *onorm = sqrt(block_sum128(o * o, red));
-    *lse = m + log(Z);
-}
+// One CTA (256 threads) per (b, g), all G heads at once.  Each default
+// segment (sink, local, decoded) streams through shared memory 64 rows at a
+// time (K and V chunk as f32); scores for every (row, head) pair in f64,
+// online softmax per (head, segment), sum e v per (head, dimension).  The
+// segment partials give the sink / local summaries (segment_summary,
+// features.cpp:66-77) and, LSE-merged, default_kv_attention's output norm
+// (gpu_output_norm, features.cpp:81-84).  Sums associate differently from the
+// reference's sequential loops (~1e-16 relative).
+constexpr int kFT = 256, kFC = 64, kFMaxG = 8;
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_feat(fx_layout L, const void* kp, const void* vp,
+__global__ void __launch_bounds__(kFT) k_feat(fx_layout L, const void* kp, const void* vp,
                                               int64_t l_new, const float* q, const double* rec,
                                               double* feats, double* gpu_norm) {
-    extern __shared__ double sm[];
-    double* qs = sm;           // [D]
-    double* s = qs + L.head_dim;  // [rows of the largest default segment]
-    __shared__ double red[4];
-    const int64_t bg = blockIdx.x;
+    extern __shared__ __align__(16) unsigned char fsm[];
     const int D = L.head_dim, G = L.group_size, t = threadIdx.x;
+    float* Ks = reinterpret_cast<float*>(fsm);            // [kFC][D + 1]
+    float* Vs = Ks + kFC * (D + 1);                        // [kFC][D]
+    double* qs = reinterpret_cast<double*>(Vs + kFC * D);  // [G][D]
+    double* sc = qs + G * D;                               // [kFC][G] scores, then weights
+    double* part_o = sc + kFC * G;                         // [3][G][D] segment outputs (sum e v)
+    __shared__ double seg_m[3][kFMaxG], seg_z[3][kFMaxG], cm[kFMaxG];
+    __shared__ double red[kFT / 32];
+    const int64_t bg = blockIdx.x;
     const int RS = kStatsN + 3 * D;
     const double isd = 1.0 / sqrt((double)D);
     const T* K = static_cast<const T*>(kp) + bg * L.l_cap * D;
     const T* V = static_cast<const T*>(vp) + bg * L.l_cap * D;
-    const int64_t o_loc = L.l_sink + L.l_cpu, o_new = o_loc + L.l_local;
+    for (int i = t; i < G * D; i += kFT) qs[i] = (double)q[bg * G * D + i];
+    const int64_t seg_r0[3] = {0, L.l_sink + L.l_cpu, L.l_sink + L.l_cpu + L.l_local};
+    const int64_t seg_n[3] = {L.l_sink, L.l_local, l_new};
+    for (int sg = 0; sg < 3; ++sg) {
+        if (t < G) {
+            seg_m[sg][t] = -INFINITY;
+            seg_z[sg][t] = 0.0;
+        }
+        for (int i = t; i < G * D; i += kFT) part_o[sg * G * D + i] = 0.0;
+        __syncthreads();
+        for (int64_t c0 = 0; c0 < seg_n[sg]; c0 += kFC) {
+            const int nr = (int)min((int64_t)kFC, seg_n[sg] - c0);
+            for (int i = t; i < nr * D; i += kFT) {  // stage the chunk (coalesced)
+                const int r = i / D, d = i % D;
+                const int64_t row = seg_r0[sg] + c0 + r;
+                Ks[r * (D + 1) + d] = tofl(K[row * D + d]);
+                Vs[r * D + d] = tofl(V[row * D + d]);
+            }
+            __syncthreads();
+            for (int pr = t; pr < nr * G; pr += kFT) {  // one (row, head) score per thread
+                const int r = pr / G, h = pr % G;
+                const double* qh = qs + h * D;
+                const float* kr = Ks + r * (D + 1);
+                double a = 0.0;
+#pragma unroll 8
+                for (int d = 0; d < D; ++d) a += qh[d] * (double)kr[d];
+                sc[r * G + h] = a * isd;
+            }
+            __syncthreads();
+            if (t < G) {  // running max and rescale of this segment's partial
+                double mx = seg_m[sg][t];
+                for (int r = 0; r < nr; ++r) mx = fmax(mx, sc[r * G + t]);
+                cm[t] = mx;
+            }
+            __syncthreads();
+            for (int pr = t; pr < nr * G; pr += kFT) {
+                const int h = pr % G;
+                sc[pr] = exp(sc[pr] - cm[h]);
+            }
+            for (int i = t; i < G * D; i += kFT) {
+                const int h = i / D;
+                const double old = seg_m[sg][h];
+                if (old != cm[h] && old != -INFINITY) part_o[sg * G * D + i] *= exp(old - cm[h]);
+            }
+            __syncthreads();
+            if (t < G) {
+                const double old = seg_m[sg][t];
+                double z = (old == -INFINITY) ? 0.0 : seg_z[sg][t] * exp(old - cm[t]);
+                for (int r = 0; r < nr; ++r) z += sc[r * G + t];
+                seg_z[sg][t] = z;
+                seg_m[sg][t] = cm[t];
+            }
+            for (int i = t; i < G * D; i += kFT) {
+                const int h = i / D, d = i % D;
+                double a = 0.0;
+                for (int r = 0; r < nr; ++r) a += sc[r * G + h] * (double)Vs[r * D + d];
+                part_o[sg * G * D + i] += a;
+            }
+            __syncthreads();
+        }
+    }
+    // per head: segment summaries, merged default norm, record-derived features
     for (int h = 0; h < G; ++h) {
         const int64_t head = bg * G + h;
         const double* r = rec + head * RS;
         const double* mk = r + kStatsN;
         const double* mv = mk + D;
         const double* an = mv + D;
-        const float* qh = q + head * D;
-        if (t < D) qs[t] = (double)qh[t];
-        __syncthreads();
-        // sink / local summaries (segment_summary; empty -> kEmptyLse, 0)
-        double lse_s = kEmptyLseDev, on_s = 0.0, lse_l = kEmptyLseDev, on_l = 0.0;
-        if (L.l_sink > 0) seg_summary(K, V, 0, (int)L.l_sink, D, qs, s, red, isd, &lse_s, &on_s);
-        if (L.l_local > 0) seg_summary(K, V, o_loc, (int)L.l_local, D, qs, s, red, isd, &lse_l, &on_l);
-        // gpu_output_norm: default_kv_attention over sink, local, new merged
-        // (a common max over the three segments; merge_into is exact algebra)
-        const int n_def = (int)(L.l_sink + L.l_local + l_new);
-        double gnorm = 0.0;
-        if (n_def > 0) {
-            for (int i = t; i < n_def; i += blockDim.x) {
-                const int64_t row = i < L.l_sink ? i : o_loc + (i - L.l_sink);
-                const T* kr = K + row * D;
-                double a = 0.0;
-                for (int d = 0; d < D; ++d) a += qs[d] * (double)tofl(kr[d]);
-                s[i] = a * isd;
-            }
-            __syncthreads();
-            double mx = -INFINITY;
-            for (int i = t; i < n_def; i += blockDim.x) mx = fmax(mx, s[i]);
-            const double m = block_max128(mx, red);
-            double z = 0.0;
-            for (int i = t; i < n_def; i += blockDim.x) z += exp(s[i] - m);
-            const double Z = block_sum128(z, red);
-            double o = 0.0;
-            if (t < D)
-                for (int i = 0; i < n_def; ++i) {
-                    const int64_t row = i < L.l_sink ? i : o_loc + (i - L.l_sink);
-                    o += exp(s[i] - m) * (double)tofl(V[row * D + t]);
-                }
-            o = t < D ? o / Z : 0.0;
-            gnorm = sqrt(block_sum128(o * o, red));
+        const double* qh = qs + h * D;
+        double on[2], mz = -INFINITY;
+        for (int sg = 0; sg < 3; ++sg) mz = seg_n[sg] > 0 ? fmax(mz, seg_m[sg][h]) : mz;
+        double zt = 0.0, wsg[3];
+        for (int sg = 0; sg < 3; ++sg) {
+            wsg[sg] = seg_n[sg] > 0 ? exp(seg_m[sg][h] - mz) : 0.0;
+            zt += wsg[sg] * seg_z[sg][h];
         }
-        (void)o_new;
-        // query-side dot products (sequential order, matrix.hpp:74-84)
+        double x0 = 0.0, x1 = 0.0, xg = 0.0, qn2 = 0.0, qk = 0.0, qa = 0.0, nmk = 0.0, nmv = 0.0;
+        for (int d = t; d < D; d += kFT) {
+            const double o0 = seg_n[0] > 0 ? part_o[h * D + d] / seg_z[0][h] : 0.0;
+            const double o1 = seg_n[1] > 0 ? part_o[G * D + h * D + d] / seg_z[1][h] : 0.0;
+            double og = 0.0;
+            for (int sg = 0; sg < 3; ++sg) og += wsg[sg] * part_o[sg * G * D + h * D + d];
+            og = zt > 0.0 ? og / zt : 0.0;
+            x0 += o0 * o0;
+            x1 += o1 * o1;
+            xg += og * og;
+            qn2 += qh[d] * qh[d];
+            qk += qh[d] * mk[d];
+            qa += qh[d] * an[d];
+            nmk += mk[d] * mk[d];
+            nmv += mv[d] * mv[d];
+        }
+        on[0] = sqrt(block_sum128(x0, red));
+        on[1] = sqrt(block_sum128(x1, red));
+        const double gn = sqrt(block_sum128(xg, red));
+        qn2 = block_sum128(qn2, red);
+        qk = block_sum128(qk, red);
+        qa = block_sum128(qa, red);
+        nmk = block_sum128(nmk, red);
+        nmv = block_sum128(nmv, red);
         if (t == 0) {
             double* f = feats + head * kFeat;
-            double qn2 = 0.0, qk = 0.0, qa = 0.0;
-            for (int d = 0; d < D; ++d) {
-                qn2 += qs[d] * qs[d];
-                qk += qs[d] * mk[d];
-                qa += qs[d] * an[d];
-            }
             const double qn = sqrt(qn2);
-            double nmk = 0.0, nmv = 0.0;
-            for (int d = 0; d < D; ++d) {
-                nmk += mk[d] * mk[d];
-                nmv += mv[d] * mv[d];
-            }
             const bool cpu_empty = r[5] != 0.0;
             f[0] = r[0];
             f[1] = r[1];
@@ -288,7 +320,7 @@ __global__ void __launch_bounds__(128) k_feat(fx_layout L, const void* kp, const
                 f[17 + i] = r[16 + i];
             }
             f[16] = (qn > 0.0 && !cpu_empty) ? qk / (qn * sqrt((double)D)) : 0.0;
-            f[21] = lse_s;
+            f[21] = seg_n[0] > 0 ? seg_m[0][h] + log(seg_z[0][h]) : kEmptyLseDev;
             // approx_lse_cpu (features.cpp:159-170)
             const double l_cpu = r[2];
             if (l_cpu == 0.0) f[22] = kEmptyLseDev;
@@ -297,12 +329,12 @@ __global__ void __launch_bounds__(128) k_feat(fx_layout L, const void* kp, const
                 const double mu_q = qk / (qn * sqrt((double)D));
                 f[22] = log(l_cpu) + qn * mu_q + 0.5 * qn * qn * r[17];
             }
-            f[23] = lse_l;
+            f[23] = seg_n[1] > 0 ? seg_m[1][h] + log(seg_z[1][h]) : kEmptyLseDev;
             f[24] = r[20];
             f[25] = r[21];
             f[26] = r[22];
-            f[27] = on_s;
-            f[28] = on_l;
+            f[27] = seg_n[0] > 0 ? on[0] : 0.0;
+            f[28] = seg_n[1] > 0 ? on[1] : 0.0;
             f[29] = r[23];
             f[30] = r[24];
             f[31] = r[25];
@@ -311,9 +343,8 @@ __global__ void __launch_bounds__(128) k_feat(fx_layout L, const void* kp, const
             f[34] = (qn > 0.0 && r[31] > 0.0) ? qa / (qn * r[31]) : 0.0;
             for (int i = 0; i < 4; ++i) f[35 + i] = r[26 + i];
             f[40] = r[30];
-            gpu_norm[head] = gnorm;
+            gpu_norm[head] = zt > 0.0 ? gn : 0.0;
         }
-        __syncthreads();
     }
 }
 
@@ -358,18 +389,19 @@ void launch_prefill_group(const fx_layout& L, const void* k, const void* v, doub
 void launch_decode_features(const fx_layout& L, const void* k, const void* v, int64_t l_new,
                             const float* q, const double* rec, double* feats, double* gpu_norm,
                             cudaStream_t s) {
-    FX_REQUIRE(L.head_dim <= 128, FX_ERR_INVALID, "bad-shape: features need head_dim <= 128");
-    const int64_t n_def = L.l_sink + L.l_local + l_new;
-    FX_REQUIRE(n_def <= 16384, FX_ERR_INVALID, "bad-shape: more than 16384 default rows");
+    FX_REQUIRE(L.head_dim <= 256 && L.group_size <= kFMaxG, FX_ERR_INVALID,
+               "bad-shape: features need head_dim <= 256 and group_size <= 8");
     const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
-    const size_t smem = (size_t)(L.head_dim + std::max<int64_t>(n_def, 1)) * sizeof(double);
+    const int D = L.head_dim, G = L.group_size;
+    const size_t smem = (size_t)kFC * (D + 1) * 4 + (size_t)kFC * D * 4 + (size_t)G * D * 8 +
+                        (size_t)kFC * G * 8 + (size_t)3 * G * D * 8 + 16;
     const bool bf = L.dtype == FX_BF16;
     if (bf) {
         FX_CUDA(cudaFuncSetAttribute(k_feat<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_feat<__nv_bfloat16><<<(unsigned)n_bg, 128, smem, s>>>(L, k, v, l_new, q, rec, feats, gpu_norm);
+        k_feat<__nv_bfloat16><<<(unsigned)n_bg, kFT, smem, s>>>(L, k, v, l_new, q, rec, feats, gpu_norm);
     } else {
         FX_CUDA(cudaFuncSetAttribute(k_feat<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_feat<float><<<(unsigned)n_bg, 128, smem, s>>>(L, k, v, l_new, q, rec, feats, gpu_norm);
+        k_feat<float><<<(unsigned)n_bg, kFT, smem, s>>>(L, k, v, l_new, q, rec, feats, gpu_norm);
     }
     FX_CUDA(cudaGetLastError());
     k_feat_cross<<<(unsigned)L.batch, 128, 0, s>>>(L.kv_heads * L.group_size, gpu_norm, feats);

@@ -624,8 +624,9 @@ class Predictor:
         check(LIB.fx_model_create(engine.ctx, *[a.ctypes.data for a in self._host], C.byref(h)))
         self.h = h
 
-    def __call__(self, feats: torch.Tensor):
-        """features [..][41] f64 device -> (bgt0, kslope, streaming) shaped like feats[..., 0]."""
+    def __call__(self, feats: torch.Tensor, z: torch.Tensor = None):
+        """features [..][41] f64 device -> (bgt0, kslope, streaming) shaped like
+        feats[..., 0]; z (optional, [..][3] f64) receives the raw logits."""
         shape = feats.shape[:-1]
         n = int(np.prod(shape)) if len(shape) else 1
         dev = self.eng.device
@@ -633,7 +634,7 @@ class Predictor:
         ks = torch.empty(shape, dtype=torch.float64, device=dev)
         st = torch.empty(shape, dtype=torch.int32, device=dev)
         check(LIB.fx_predict(self.eng.ctx, self.h, n, _ptr(feats.contiguous()), _ptr(b0), _ptr(ks),
-                             _ptr(st), None))
+                             _ptr(st), _ptr(z)))
         return b0, ks, st
 
     def close(self):
