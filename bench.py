@@ -51,7 +51,17 @@ def args_parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling run: timed loop only")
-    return ap.parse_args()
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2: one layer, batch 16 (the metric's config); c4: 32 layers x batch 8 "
+                         "per GPU (configs[3], one 8-GPU shard), the layers' independent tasks "
+                         "batched into one step like run_decode's single queue (pipeline.cpp:354)")
+    a = ap.parse_args()
+    if a.workload == "c4":
+        a.layers, a.seqs = 32, 8
+        a.batch = a.layers * a.seqs  # (layer, sequence) pairs: independent (b, g) tasks
+    else:
+        a.layers, a.seqs = 1, a.batch
+    return a
 
 
 def head_props(batch, seed=1):
@@ -71,12 +81,14 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel):
+def ncu_traffic(kernel, workload="c2"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the
-    committed `ncu --set full` extract (profiles/ncu_traffic.json, written by
-    profiles/summarize_ncu.py from the same bench command); None if absent."""
+    committed `ncu --set full` extract of the same bench command and workload
+    (profiles/ncu_traffic.json for c2, profiles/ncu_traffic_<workload>.json
+    otherwise; written by profiles/summarize_ncu.py); None if absent."""
+    name = "ncu_traffic.json" if workload == "c2" else f"ncu_traffic_{workload}.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             t = json.load(f)
         for name, rec in t["kernels"].items():
             if kernel in name:
@@ -356,8 +368,8 @@ def run_ours(a):
         achieved = attend_b / a.steps / (attend_ms * 1e-3) / 1e9
         result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3+K4)",
                               "achieved": achieved, "peak": peak, "unit": "GB/s",
-                              "frac": achieved / peak, "peak_kind": peak_kind,
-                              "traffic": ncu_traffic("k_attend"),
+                              "frac": achieved / peak, "peak_kind": peak_kind, "timing": "per-kernel CUDA events in a separate pass with PDL off (events bracket each kernel alone)",
+                              "traffic": ncu_traffic("k_attend", a.workload),
                               "algorithmic_bytes_per_launch": attend_b / a.steps}
         score_ms = kt.get("score", float("nan"))
         step_bytes = (meta_b + attend_b) / a.steps
@@ -437,6 +449,7 @@ def run_ours(a):
         # the device.  Random-init 41->256->384->3 weights (the reference ships
         # no trained model); the output-layer bias is set to the drawn-props
         # operating point (bgt0 ~ 0.03, k ~ 0.005, streaming ~ half).
+    if not a.quick and a.workload == "c2":
         from paper_2605_07719_b200.fluxattn import Predictor
         rs = np.random.default_rng(5)
         params = {"w1": rs.standard_normal((256, 41)) * (2.0 / 41) ** 0.5, "b1": np.zeros(256),
@@ -478,18 +491,38 @@ def run_ours(a):
         t1.record()
         torch.cuda.synchronize()
         pms = t0.elapsed_time(t1)
-        stream_frac = float(pred(feats)[2].float().mean().item())
+        # phase split of one more step (events serialize the phases)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        i = step_i[0]
+        ev[0].record()
+        dec.decode_features(qs[i], rec, out=feats)
+        ev[1].record()
+        pp = pred(feats)
+        ev[2].record()
+        dec.step(qs[i], props=pp)
+        ev[3].record()
+        dec.append(kv_new[i, 0], kv_new[i, 1])
+        step_i[0] += 1
+        torch.cuda.synchronize()
+        stream_frac = float(pp[2].float().mean().item())
+        retr_groups = int((dec.plan_blk > 0).sum().item())
         result["predictor_path"] = {
             "value": world * a.steps / (pms / 1e3), "unit": UNIT, "ms_per_step": pms / a.steps,
+            "features_ms": ev[0].elapsed_time(ev[1]), "predict_ms": ev[1].elapsed_time(ev[2]),
+            "decode_step_ms": ev[2].elapsed_time(ev[3]), "retrieval_groups": retr_groups,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
             "per_step": "fx_decode_features + fx_predict + fx_decode_step + fx_append_kv",
             "model": "random-init 41-256-384-3, output bias at the drawn-props operating point"}
         pred.close()
 
     result["config"] = {
-        "workload": "C2: Llama-3-8B layer (32q/8kv heads, d128), 128K ctx, batch 16/GPU, "
-                    "per-head budgets + per-group granularity (16/32/64/128) from plan_group",
-        "context": a.context, "global_batch": B * world, "seq_len": a.context,
+        "workload": ("C2: Llama-3-8B layer (32q/8kv heads, d128), 128K ctx, batch 16/GPU, "
+                     "per-head budgets + per-group granularity (16/32/64/128) from plan_group")
+        if a.workload == "c2" else
+        ("C4: Llama-3-8B 32-layer decode step, 128K ctx, batch 8/GPU (64 over 8 GPUs), the 32 "
+         "layers' (b, g) tasks in one batched step; per-head budgets from plan_group"),
+        "layers": a.layers,
+        "context": a.context, "global_batch": a.seqs * world, "seq_len": a.context,
         "parallelism": f"batch-sharded x{world} (no collective)", "kv_dtype": "bf16",
         "l2": "per-step working set > 1 GB (inputs larger than the 126 MB L2); no flush",
         "meta_build_ms": meta_build_ms,

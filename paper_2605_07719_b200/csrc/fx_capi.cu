@@ -1,6 +1,7 @@
 // fx_capi.cu -- the C-ABI (include/fluxattn_b200.h): context, device scratch,
 // and the entry points that sequence the K1..K5 kernels.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -116,6 +117,9 @@ cudaEvent_t pool_event(fx_ctx* c) {
 }
 
 // Brackets one kernel launch with CUDA events on the ctx stream when timing.
+// contexts with event timing on: PDL is off process-wide while any is (fx_internal.h)
+std::atomic<int> g_timing_ctxs{0};
+
 struct Timed {
     fx_ctx* c;
     int id;
@@ -338,6 +342,10 @@ Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, 
 
 }  // namespace
 
+namespace fx {
+bool pdl_enabled() { return g_timing_ctxs.load(std::memory_order_relaxed) == 0; }
+}  // namespace fx
+
 extern "C" {
 
 const char* fx_last_error(void) { return g_last_error.c_str(); }
@@ -400,7 +408,9 @@ int fx_ctx_set_timing(fx_ctx* ctx, int enable) {
     return guarded([&] {
         DeviceGuard g(ctx);
         collect_timing(ctx);
-        ctx->timing = enable != 0;
+        const bool on = enable != 0;
+        if (on != ctx->timing) g_timing_ctxs += on ? 1 : -1;
+        ctx->timing = on;
     });
 }
 

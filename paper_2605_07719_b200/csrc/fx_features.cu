@@ -184,6 +184,22 @@ __global__ void __launch_bounds__(128) k_pfg_write(fx_layout L, GroupAcc acc, do
 // reference's sequential loops (~1e-16 relative).
 constexpr int kFT = 256, kFC = 64, kFMaxG = 8;
 
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* f) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = bf16lo_to_f(w[i]);
+        f[2 * i + 1] = bf16hi_to_f(w[i]);
+    }
+}
+__device__ __forceinline__ void ld8(const float* p, float* f) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kFT) k_feat(fx_layout L, const void* kp, const void* vp,
                                               int64_t l_new, const float* q, const double* rec,
@@ -214,11 +230,18 @@ __global__ void __launch_bounds__(kFT) k_feat(fx_layout L, const void* kp, const
         __syncthreads();
         for (int64_t c0 = 0; c0 < seg_n[sg]; c0 += kFC) {
             const int nr = (int)min((int64_t)kFC, seg_n[sg] - c0);
-            for (int i = t; i < nr * D; i += kFT) {  // stage the chunk (coalesced)
-                const int r = i / D, d = i % D;
-                const int64_t row = seg_r0[sg] + c0 + r;
-                Ks[r * (D + 1) + d] = tofl(K[row * D + d]);
-                Vs[r * D + d] = tofl(V[row * D + d]);
+            const int v8 = D / 8;  // stage the chunk: 16-byte (bf16) / 32-byte (f32) vectors
+            for (int i = t; i < nr * v8; i += kFT) {
+                const int r = i / v8, d0 = (i % v8) * 8;
+                const int64_t o = (seg_r0[sg] + c0 + r) * D + d0;
+                float kf[8], vf[8];
+                ld8(K + o, kf);
+                ld8(V + o, vf);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    Ks[r * (D + 1) + d0 + u] = kf[u];
+                    Vs[r * D + d0 + u] = vf[u];
+                }
             }
             __syncthreads();
             for (int pr = t; pr < nr * G; pr += kFT) {  // one (row, head) score per thread
@@ -389,8 +412,8 @@ void launch_prefill_group(const fx_layout& L, const void* k, const void* v, doub
 void launch_decode_features(const fx_layout& L, const void* k, const void* v, int64_t l_new,
                             const float* q, const double* rec, double* feats, double* gpu_norm,
                             cudaStream_t s) {
-    FX_REQUIRE(L.head_dim <= 256 && L.group_size <= kFMaxG, FX_ERR_INVALID,
-               "bad-shape: features need head_dim <= 256 and group_size <= 8");
+    FX_REQUIRE(L.head_dim <= 256 && L.head_dim % 8 == 0 && L.group_size <= kFMaxG, FX_ERR_INVALID,
+               "bad-shape: features need head_dim <= 256 (multiple of 8) and group_size <= 8");
     const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
     const int D = L.head_dim, G = L.group_size;
     const size_t smem = (size_t)kFC * (D + 1) * 4 + (size_t)kFC * D * 4 + (size_t)G * D * 8 +

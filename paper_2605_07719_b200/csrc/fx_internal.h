@@ -64,6 +64,10 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Launch as a programmatic dependent of the previous kernel on the stream
 // (see pdl_wait / pdl_trigger in fx_common.cuh).
+// PDL is switched off while per-kernel event timing is on (fx_ctx_set_timing),
+// so an event pair brackets one kernel alone instead of its programmatic wait
+// on the previous one.
+bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                 Args... args) {
@@ -76,7 +80,7 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     FX_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 inline int64_t level_blocks(int64_t l_cpu, int blk) { return cdiv(l_cpu, blk); }

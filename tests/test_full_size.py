@@ -274,3 +274,34 @@ def test_c3_output_aware_budgets_full_size(engine, coracle):
     _check_plans(dec, coracle, tuple(t.cpu().numpy() for t in props))
     _check_counts(dec)
     _check_groups(dec, coracle, q, _retrieval_groups(dec, 2))
+
+
+def test_c1_full_size_f32(engine, coracle):
+    """C1 (configs[0]): Llama layer, 32K, batch 1, fixed (blk 64, budget 0.05),
+    f32 KV -- every group against the oracle at 1e-3 (f32 bound)."""
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    B, Hkv, G, D = 1, 8, 4, 128
+    l_sink, l_cpu, l_local = 64, 32768 - 320, 256
+    dec = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new=4, dtype="f32")
+    _fill_kv(dec.k, 51)
+    _fill_kv(dec.v, 52)
+    dec.build_metadata()
+    q = _queries(B, Hkv * G, D, seed=17, dev=engine.device)
+    dec.o.fill_(float("nan"))
+    o, lse = dec.step(q, fixed=(64, 0.05))
+    torch.cuda.synchronize()
+    assert torch.isfinite(o).all()
+    on, ln, qn = o.cpu().numpy(), lse.cpu().numpy(), q.cpu().numpy()
+    for g in range(Hkv):
+        k, v = _group_host(dec, 0, g)
+        mins, maxs = coracle.build_metadata(k[l_sink:l_sink + l_cpu], 64)
+        kb = coracle.blocks_for_budget(0.05, l_cpu, 64)
+        assert kb == 26  # SURVEY §8: k = 26 at 32K / blk 64 / 0.05
+        for hg in range(G):
+            h = g * G + hg
+            want, _ = coracle.topk_blocks(qn[0, h], mins, maxs, kb)
+            assert set(dec.selected_blocks(0, h).tolist()) == set(want.tolist())
+        wo, wl, _ = coracle.execute_group(k, v, (l_sink, l_cpu, l_local, 0), qn[0, g * G:(g + 1) * G],
+                                          64, np.full(G, 0.05), mins, maxs)
+        assert np.abs(on[0, g * G:(g + 1) * G] - wo).max() / max(1.0, np.abs(wo).max()) < 1e-3
+        assert np.abs(ln[0, g * G:(g + 1) * G] - wl).max() < 1e-3
