@@ -994,6 +994,8 @@ __global__ void k_merge_partials(int n, int dim, const float* __restrict__ op,
 template <typename T>
 __global__ void k_append(int64_t n_bg, int D, int64_t l_cap, int64_t row, T* k, T* v,
                          const float* kn, const float* vn) {
+    pdl_wait();  // launched early behind the attention kernel (PDL); writes after it completes
+    pdl_trigger();
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n_bg * D) return;
     const int64_t bg = e / D, d = e % D;
@@ -1135,12 +1137,11 @@ void launch_append(const fx_layout& L, void* k, void* v, int64_t row, const floa
     const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
     const unsigned grid = (unsigned)cdiv(n_bg * L.head_dim, 256);
     if (L.dtype == FX_BF16)
-        k_append<__nv_bfloat16><<<grid, 256, 0, s>>>(n_bg, L.head_dim, L.l_cap, row,
-                                                     static_cast<__nv_bfloat16*>(k),
-                                                     static_cast<__nv_bfloat16*>(v), kn, vn);
+        launch_pdl(k_append<__nv_bfloat16>, grid, 256, 0, s, n_bg, L.head_dim, L.l_cap, row,
+                   static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v), kn, vn);
     else
-        k_append<float><<<grid, 256, 0, s>>>(n_bg, L.head_dim, L.l_cap, row, static_cast<float*>(k),
-                                             static_cast<float*>(v), kn, vn);
+        launch_pdl(k_append<float>, grid, 256, 0, s, n_bg, L.head_dim, L.l_cap, row,
+                   static_cast<float*>(k), static_cast<float*>(v), kn, vn);
     FX_CUDA(cudaGetLastError());
 }
 

@@ -17,7 +17,7 @@
 // Output: the selection as a bitmask over the group's blocks.
 #include <algorithm>
 
-#include "fx_worklist.cuh"
+#include "fx_common.cuh"
 
 namespace fx {
 namespace {
@@ -30,17 +30,23 @@ constexpr int kSmemKeys = 16384;  // approximate scores staged in smem up to thi
 constexpr int kSmallCand = 512;   // band ranked in smem by counting up to this size
 
 #ifdef FX_TRACE  // profiling build only: per-head phase times and band sizes
-__device__ long long g_sel_trace[8 * 8192];
+__device__ long long g_sel_trace[16 * 8192];
 __device__ __forceinline__ long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 #define SEL_MARK(i) \
-    if (threadIdx.x == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + (i)] = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 16 + (i)] = gtimer();
 #else
 #define SEL_MARK(i)
 #endif
+}  // namespace
+}  // namespace fx
+#define WL_MARK(i) SEL_MARK(i)
+#include "fx_worklist.cuh"
+namespace fx {
+namespace {
 
 struct MetaPtrs {
     const void* p[4];
@@ -297,8 +303,8 @@ __device__ __forceinline__ void select_head(
     __syncthreads();
     SEL_MARK(3);
 #ifdef FX_TRACE
-    if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + 6] = n_cand | (n_def << 32);
-    if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 8 + 7] = k | ((int64_t)nblk << 32);
+    if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 16 + 6] = n_cand | (n_def << 32);
+    if (t == 0 && blockIdx.x < 8192) g_sel_trace[blockIdx.x * 16 + 7] = k | ((int64_t)nblk << 32);
 #endif
 
     // ---- 3. exact reference scores of the band ----
@@ -394,8 +400,10 @@ __global__ void __launch_bounds__(kT) k_select(
     int32_t* __restrict__ sel_done, int stage_words) {
     pdl_wait();
     pdl_trigger();
+    SEL_MARK(10);
     select_head<DT>(meta, absmax, q, blk_arr, kblocks, Hkv, G, D, l_cpu, approx, astride,
                     eps_scale, sel_bits, sel_words, cand_keys, cand_ids, cand_stride, keys_cap);
+    SEL_MARK(11);
     if (wl.boxes == nullptr) return;
     __shared__ int s_last;
     __shared__ int64_t s_wsum[kT + 1];
@@ -409,8 +417,10 @@ __global__ void __launch_bounds__(kT) k_select(
     // dynamic smem (keys | histogram | ...) is free now: word counts, then staged masks
     extern __shared__ __align__(16) unsigned char dsm[];
     int32_t* wcnt = reinterpret_cast<int32_t*>(dsm);
+    SEL_MARK(8);
     worklist_group(wl, bg, wcnt, s_wsum, reinterpret_cast<uint32_t*>(dsm) + kMaxWords, stage_words);
     worklist_publish(wl, (int)(gridDim.x / G));
+    SEL_MARK(9);
 }
 
 }  // namespace
@@ -461,6 +471,11 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
 #ifdef FX_TRACE
 extern "C" FX_API int fx_debug_sel_trace(long long* out, int n) {
     return cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * n) == cudaSuccess ? 0 : -2;
+}
+extern "C" FX_API int fx_debug_sel_trace_clear(void) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_sel_trace) != cudaSuccess) return -2;
+    return cudaMemset(p, 0, sizeof(g_sel_trace)) == cudaSuccess ? 0 : -2;
 }
 #endif
 

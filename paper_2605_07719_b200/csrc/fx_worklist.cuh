@@ -13,6 +13,10 @@
 
 #include "fx_common.cuh"
 
+#ifndef WL_MARK
+#define WL_MARK(i)
+#endif
+
 namespace fx {
 
 struct WorklistArgs {
@@ -90,54 +94,61 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
     const int nd = nb_s + nb_t;
     int64_t total = nd;
     if (blk > 0) {
+        // thread per selection word: the G head words load together (one L2
+        // round trip), the union's box count goes to wcnt; after the scan the
+        // same thread emits its word's boxes (its set bits in order).
         const int64_t nblk = cdiv_dev(w.l_cpu, blk);
         const int W = (int)cdiv_dev(nblk, 32);
         const int bpb = blk / kBoxRows;
         const int64_t last = nblk - 1;
         const int nb_last = (int)cdiv_dev(w.l_cpu - last * blk, kBoxRows);
         const uint32_t* hg = w.sel_bits + ((int64_t)b * w.Hkv * G + (int64_t)g * G) * w.sel_words;
-        const bool staged = (int64_t)G * W <= stage_words;
-        if (staged) {
-#pragma unroll 4
-            for (int i = t; i < G * W; i += nt) s_bits[i] = __ldcg(hg + (int64_t)(i / W) * w.sel_words + i % W);
-            __syncthreads();
-        }
-        auto word = [&](int h, int j) -> uint32_t {
-            return staged ? s_bits[h * W + j] : __ldcg(hg + (int64_t)h * w.sel_words + j);
-        };
+        (void)s_bits;
+        (void)stage_words;
+        (void)lane;
+        (void)warp;
         for (int j = t; j < W; j += nt) {
             uint32_t u = 0;
-            for (int h = 0; h < G; ++h) u |= word(h, j);
+            for (int h = 0; h < G; ++h) u |= __ldcg(hg + (int64_t)h * w.sel_words + j);
             int c = __popc(u) * bpb;
             if ((last >> 5) == j && ((u >> (last & 31)) & 1u)) c -= bpb - nb_last;
             wcnt[j] = c;
         }
+        WL_MARK(12);
         __syncthreads();
         total += block_exclusive_scan(wcnt, W, wsum);
-        for (int j = warp; j < W; j += nt / 32) {
-            uint32_t u = 0, m = 0;  // union word; head mask of this lane's block
-            for (int h = 0; h < G; ++h) {
-                const uint32_t x = word(h, j);
-                u |= x;
-                m |= ((x >> lane) & 1u) << h;
+        WL_MARK(13);
+        for (int j = t; j < W; j += nt) {
+            uint32_t x[16];
+            uint32_t u = 0;
+#pragma unroll
+            for (int h = 0; h < 16; ++h) {
+                x[h] = h < G ? __ldcg(hg + (int64_t)h * w.sel_words + j) : 0u;
+                u |= x[h];
             }
-            if ((u >> lane) & 1u) {
-                const int i = j * 32 + lane;
-                const int r0 = i * blk;  // < 2^31 (checked by the launcher)
+            int64_t o = nd + wcnt[j];
+            while (u) {
+                const int l = __ffs(u) - 1;
+                u &= u - 1;
+                uint32_t m = 0;  // heads that selected this block
+#pragma unroll
+                for (int h = 0; h < 16; ++h) m |= ((x[h] >> l) & 1u) << h;
+                const int r0 = (j * 32 + l) * blk;  // < 2^31 (checked by the launcher)
                 const int len = min(blk, (int)(w.l_cpu - r0));
                 const int nb = (len + kBoxRows - 1) >> 4;
-                const int64_t o = nd + wcnt[j] + (int64_t)__popc(u & ((1u << lane) - 1u)) * bpb;
                 const int row0 = (int)w.l_sink + r0;
-                for (int x = 0; x < nb; ++x) {
+                for (int y = 0; y < nb; ++y) {
                     Box bx;
-                    bx.row = row0 + x * kBoxRows;
-                    bx.n = (uint16_t)min(kBoxRows, len - x * kBoxRows);
+                    bx.row = row0 + y * kBoxRows;
+                    bx.n = (uint16_t)min(kBoxRows, len - y * kBoxRows);
                     bx.mask = (uint16_t)m;
-                    out[o + x] = bx;
+                    out[o + y] = bx;
                 }
+                o += nb;
             }
         }
     }
+    WL_MARK(14);
     if (t == 0) w.bg_count[bg] = (int32_t)total;
 }
 
