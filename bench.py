@@ -466,7 +466,11 @@ def run_ours(a):
         # first step's features, as train() does on its training rows
         f0 = dec.decode_features(qs[0], rec, out=feats).reshape(-1, 41)
         params["mu"] = f0.mean(0).cpu().numpy()
-        params["sigma"] = (f0.std(0) + 1e-3 * f0.mean(0).abs()).cpu().numpy()
+        sd = f0.std(0)
+        # features constant across heads (layer, lengths, ...) get sigma 0: normalize()
+        # passes them through as 0 (features.cpp:226-233)
+        params["sigma"] = torch.where(sd > 1e-9 * (1 + f0.mean(0).abs()), sd,
+                                      torch.zeros_like(sd)).cpu().numpy()
         pred = Predictor(eng, params)
         z0 = torch.empty((B * H, 3), dtype=torch.float64, device=dev)
         pred(f0, z=z0)  # centre the streaming logit: about half the heads stream

@@ -882,11 +882,9 @@ int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const v
         FX_REQUIRE(k && v && q && rec && features, FX_ERR_STATE, "no-context: features have no payload");
         FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_new <= L.l_cap, FX_ERR_INVALID,
                    "bad-shape: decoded rows exceed l_cap");
-        const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
-        ctx->api.ensure((size_t)nh * 8 + 256);
-        fx::launch_decode_features(L, k, v, l_new, q, rec, features, static_cast<double*>(ctx->api.p),
-                                   ctx->stream);
-        ctx->launches += 2;
+        ctx->api.ensure(fx::decode_features_scratch_bytes(L, l_new));
+        fx::launch_decode_features(L, k, v, l_new, q, rec, features, ctx->api.p, ctx->stream);
+        ctx->launches += 3;
     });
 }
 

@@ -200,92 +200,128 @@ __device__ __forceinline__ void ld8(const float* p, float* f) {
     f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
+// Chunk partials: one CTA per (64-row chunk of a default segment, group):
+// m[h] = max score, z[h] = sum exp(s - m), o[h][d] = sum exp(s - m) v[d].
+struct FeatChunks {
+    int n_sink, n_local, n_new, n;  // chunks per segment, total per group
+    double* m;                      // [n_bg][n][G]
+    double* z;                      // [n_bg][n][G]
+    double* o;                      // [n_bg][n][G][D]
+};
+__device__ __forceinline__ void chunk_seg(const FeatChunks& c, int ci, int* sg, int* k) {
+    if (ci < c.n_sink) { *sg = 0; *k = ci; }
+    else if (ci < c.n_sink + c.n_local) { *sg = 1; *k = ci - c.n_sink; }
+    else { *sg = 2; *k = ci - c.n_sink - c.n_local; }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kFT) k_feat(fx_layout L, const void* kp, const void* vp,
-                                              int64_t l_new, const float* q, const double* rec,
-                                              double* feats, double* gpu_norm) {
+__global__ void __launch_bounds__(kFT) k_feat_chunk(fx_layout L, const void* kp, const void* vp,
+                                                    int64_t l_new, const float* q, FeatChunks fc) {
     extern __shared__ __align__(16) unsigned char fsm[];
     const int D = L.head_dim, G = L.group_size, t = threadIdx.x;
     float* Ks = reinterpret_cast<float*>(fsm);            // [kFC][D + 1]
     float* Vs = Ks + kFC * (D + 1);                        // [kFC][D]
     double* qs = reinterpret_cast<double*>(Vs + kFC * D);  // [G][D]
     double* sc = qs + G * D;                               // [kFC][G] scores, then weights
-    double* part_o = sc + kFC * G;                         // [3][G][D] segment outputs (sum e v)
-    __shared__ double seg_m[3][kFMaxG], seg_z[3][kFMaxG], cm[kFMaxG];
-    __shared__ double red[kFT / 32];
-    const int64_t bg = blockIdx.x;
-    const int RS = kStatsN + 3 * D;
+    __shared__ double cm[kFMaxG];
+    const int ci = blockIdx.x;
+    const int64_t bg = blockIdx.y;
+    int sg, k;
+    chunk_seg(fc, ci, &sg, &k);
+    const int64_t seg_r0[3] = {0, L.l_sink + L.l_cpu, L.l_sink + L.l_cpu + L.l_local};
+    const int64_t seg_n[3] = {L.l_sink, L.l_local, l_new};
+    const int64_t c0 = (int64_t)k * kFC;
+    const int nr = (int)min((int64_t)kFC, seg_n[sg] - c0);
     const double isd = 1.0 / sqrt((double)D);
     const T* K = static_cast<const T*>(kp) + bg * L.l_cap * D;
     const T* V = static_cast<const T*>(vp) + bg * L.l_cap * D;
     for (int i = t; i < G * D; i += kFT) qs[i] = (double)q[bg * G * D + i];
-    const int64_t seg_r0[3] = {0, L.l_sink + L.l_cpu, L.l_sink + L.l_cpu + L.l_local};
-    const int64_t seg_n[3] = {L.l_sink, L.l_local, l_new};
-    for (int sg = 0; sg < 3; ++sg) {
-        if (t < G) {
-            seg_m[sg][t] = -INFINITY;
-            seg_z[sg][t] = 0.0;
-        }
-        for (int i = t; i < G * D; i += kFT) part_o[sg * G * D + i] = 0.0;
-        __syncthreads();
-        for (int64_t c0 = 0; c0 < seg_n[sg]; c0 += kFC) {
-            const int nr = (int)min((int64_t)kFC, seg_n[sg] - c0);
-            const int v8 = D / 8;  // stage the chunk: 16-byte (bf16) / 32-byte (f32) vectors
-            for (int i = t; i < nr * v8; i += kFT) {
-                const int r = i / v8, d0 = (i % v8) * 8;
-                const int64_t o = (seg_r0[sg] + c0 + r) * D + d0;
-                float kf[8], vf[8];
-                ld8(K + o, kf);
-                ld8(V + o, vf);
+    const int v8 = D / 8;  // stage the chunk: 16-byte (bf16) / 32-byte (f32) vectors
+    for (int i = t; i < nr * v8; i += kFT) {
+        const int r = i / v8, d0 = (i % v8) * 8;
+        const int64_t o = (seg_r0[sg] + c0 + r) * D + d0;
+        float kf[8], vf[8];
+        ld8(K + o, kf);
+        ld8(V + o, vf);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    Ks[r * (D + 1) + d0 + u] = kf[u];
-                    Vs[r * D + d0 + u] = vf[u];
-                }
-            }
-            __syncthreads();
-            for (int pr = t; pr < nr * G; pr += kFT) {  // one (row, head) score per thread
-                const int r = pr / G, h = pr % G;
-                const double* qh = qs + h * D;
-                const float* kr = Ks + r * (D + 1);
-                double a = 0.0;
-#pragma unroll 8
-                for (int d = 0; d < D; ++d) a += qh[d] * (double)kr[d];
-                sc[r * G + h] = a * isd;
-            }
-            __syncthreads();
-            if (t < G) {  // running max and rescale of this segment's partial
-                double mx = seg_m[sg][t];
-                for (int r = 0; r < nr; ++r) mx = fmax(mx, sc[r * G + t]);
-                cm[t] = mx;
-            }
-            __syncthreads();
-            for (int pr = t; pr < nr * G; pr += kFT) {
-                const int h = pr % G;
-                sc[pr] = exp(sc[pr] - cm[h]);
-            }
-            for (int i = t; i < G * D; i += kFT) {
-                const int h = i / D;
-                const double old = seg_m[sg][h];
-                if (old != cm[h] && old != -INFINITY) part_o[sg * G * D + i] *= exp(old - cm[h]);
-            }
-            __syncthreads();
-            if (t < G) {
-                const double old = seg_m[sg][t];
-                double z = (old == -INFINITY) ? 0.0 : seg_z[sg][t] * exp(old - cm[t]);
-                for (int r = 0; r < nr; ++r) z += sc[r * G + t];
-                seg_z[sg][t] = z;
-                seg_m[sg][t] = cm[t];
-            }
-            for (int i = t; i < G * D; i += kFT) {
-                const int h = i / D, d = i % D;
-                double a = 0.0;
-                for (int r = 0; r < nr; ++r) a += sc[r * G + h] * (double)Vs[r * D + d];
-                part_o[sg * G * D + i] += a;
-            }
-            __syncthreads();
+        for (int u = 0; u < 8; ++u) {
+            Ks[r * (D + 1) + d0 + u] = kf[u];
+            Vs[r * D + d0 + u] = vf[u];
         }
     }
+    __syncthreads();
+    for (int pr = t; pr < nr * G; pr += kFT) {  // one (row, head) score per thread
+        const int r = pr / G, h = pr % G;
+        const double* qh = qs + h * D;
+        const float* kr = Ks + r * (D + 1);
+        double a = 0.0;
+#pragma unroll 8
+        for (int d = 0; d < D; ++d) a += qh[d] * (double)kr[d];
+        sc[r * G + h] = a * isd;
+    }
+    __syncthreads();
+    if (t < G) {
+        double mx = -INFINITY;
+        for (int r = 0; r < nr; ++r) mx = fmax(mx, sc[r * G + t]);
+        cm[t] = mx;
+    }
+    __syncthreads();
+    for (int pr = t; pr < nr * G; pr += kFT) sc[pr] = exp(sc[pr] - cm[pr % G]);
+    __syncthreads();
+    const int64_t slot = (bg * fc.n + ci) * G;
+    if (t < G) {
+        double z = 0.0;
+        for (int r = 0; r < nr; ++r) z += sc[r * G + t];
+        fc.m[slot + t] = cm[t];
+        fc.z[slot + t] = z;
+    }
+    for (int i = t; i < G * D; i += kFT) {
+        const int h = i / D, d = i % D;
+        double a = 0.0;
+        for (int r = 0; r < nr; ++r) a += sc[r * G + h] * (double)Vs[r * D + d];
+        fc.o[(slot + h) * D + d] = a;
+    }
+}
+
+// Per group: merge the chunk partials of each segment, then the features.
+__global__ void __launch_bounds__(kFT) k_feat(fx_layout L, int64_t l_new, const float* q,
+                                              const double* rec, FeatChunks fc, double* feats,
+                                              double* gpu_norm) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int D = L.head_dim, G = L.group_size, t = threadIdx.x;
+    double* qs = reinterpret_cast<double*>(fsm);  // [G][D]
+    double* part_o = qs + G * D;                  // [3][G][D] segment outputs (sum e v)
+    __shared__ double seg_m[3][kFMaxG], seg_z[3][kFMaxG];
+    __shared__ double red[kFT / 32];
+    const int64_t bg = blockIdx.x;
+    const int RS = kStatsN + 3 * D;
+    for (int i = t; i < G * D; i += kFT) qs[i] = (double)q[bg * G * D + i];
+    const int64_t seg_n[3] = {L.l_sink, L.l_local, l_new};
+    const int first[3] = {0, fc.n_sink, fc.n_sink + fc.n_local};
+    const int cnt[3] = {fc.n_sink, fc.n_local, fc.n_new};
+    if (t < 3 * G) {  // segment max and denominator over its chunks
+        const int sg = t / G, h = t % G;
+        double m = -INFINITY;
+        for (int c = 0; c < cnt[sg]; ++c) m = fmax(m, fc.m[(bg * fc.n + first[sg] + c) * G + h]);
+        double z = 0.0;
+        for (int c = 0; c < cnt[sg]; ++c) {
+            const int64_t sl = (bg * fc.n + first[sg] + c) * G + h;
+            z += fc.z[sl] * exp(fc.m[sl] - m);
+        }
+        seg_m[sg][h] = m;
+        seg_z[sg][h] = z;
+    }
+    __syncthreads();
+    for (int i = t; i < 3 * G * D; i += kFT) {
+        const int sg = i / (G * D), h = (i / D) % G, d = i % D;
+        double a = 0.0;
+        for (int c = 0; c < cnt[sg]; ++c) {
+            const int64_t sl = (bg * fc.n + first[sg] + c) * G + h;
+            a += fc.o[sl * D + d] * exp(fc.m[sl] - seg_m[sg][h]);
+        }
+        part_o[i] = a;
+    }
+    __syncthreads();
     // per head: segment summaries, merged default norm, record-derived features
     for (int h = 0; h < G; ++h) {
         const int64_t head = bg * G + h;
@@ -409,23 +445,46 @@ void launch_prefill_group(const fx_layout& L, const void* k, const void* v, doub
     FX_CUDA(cudaGetLastError());
 }
 
+size_t decode_features_scratch_bytes(const fx_layout& L, int64_t l_new) {
+    const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
+    const int64_t n = cdiv(L.l_sink, kFC) + cdiv(L.l_local, kFC) + cdiv(l_new, kFC);
+    return (size_t)(n_bg * n * L.group_size * (L.head_dim + 2) + n_bg * L.group_size + 64) * 8;
+}
+
 void launch_decode_features(const fx_layout& L, const void* k, const void* v, int64_t l_new,
-                            const float* q, const double* rec, double* feats, double* gpu_norm,
+                            const float* q, const double* rec, double* feats, void* scratch,
                             cudaStream_t s) {
     FX_REQUIRE(L.head_dim <= 256 && L.head_dim % 8 == 0 && L.group_size <= kFMaxG, FX_ERR_INVALID,
                "bad-shape: features need head_dim <= 256 (multiple of 8) and group_size <= 8");
     const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
     const int D = L.head_dim, G = L.group_size;
-    const size_t smem = (size_t)kFC * (D + 1) * 4 + (size_t)kFC * D * 4 + (size_t)G * D * 8 +
-                        (size_t)kFC * G * 8 + (size_t)3 * G * D * 8 + 16;
+    FeatChunks fc;
+    fc.n_sink = (int)cdiv(L.l_sink, kFC);
+    fc.n_local = (int)cdiv(L.l_local, kFC);
+    fc.n_new = (int)cdiv(l_new, kFC);
+    fc.n = fc.n_sink + fc.n_local + fc.n_new;
+    double* w = static_cast<double*>(scratch);
+    double* gpu_norm = w;
+    fc.m = gpu_norm + n_bg * G;
+    fc.z = fc.m + n_bg * fc.n * G;
+    fc.o = fc.z + n_bg * fc.n * G;
     const bool bf = L.dtype == FX_BF16;
-    if (bf) {
-        FX_CUDA(cudaFuncSetAttribute(k_feat<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_feat<__nv_bfloat16><<<(unsigned)n_bg, kFT, smem, s>>>(L, k, v, l_new, q, rec, feats, gpu_norm);
-    } else {
-        FX_CUDA(cudaFuncSetAttribute(k_feat<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_feat<float><<<(unsigned)n_bg, kFT, smem, s>>>(L, k, v, l_new, q, rec, feats, gpu_norm);
+    if (fc.n > 0) {
+        const size_t smem = (size_t)kFC * (D + 1) * 4 + (size_t)kFC * D * 4 + (size_t)G * D * 8 +
+                            (size_t)kFC * G * 8 + 16;
+        const dim3 grid((unsigned)fc.n, (unsigned)n_bg);
+        if (bf) {
+            FX_CUDA(cudaFuncSetAttribute(k_feat_chunk<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_feat_chunk<__nv_bfloat16><<<grid, kFT, smem, s>>>(L, k, v, l_new, q, fc);
+        } else {
+            FX_CUDA(cudaFuncSetAttribute(k_feat_chunk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_feat_chunk<float><<<grid, kFT, smem, s>>>(L, k, v, l_new, q, fc);
+        }
+        FX_CUDA(cudaGetLastError());
     }
+    const size_t smem2 = (size_t)G * D * 8 + (size_t)3 * G * D * 8 + 16;
+    FX_CUDA(cudaFuncSetAttribute(k_feat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    k_feat<<<(unsigned)n_bg, kFT, smem2, s>>>(L, l_new, q, rec, fc, feats, gpu_norm);
     FX_CUDA(cudaGetLastError());
     k_feat_cross<<<(unsigned)L.batch, 128, 0, s>>>(L.kv_heads * L.group_size, gpu_norm, feats);
     FX_CUDA(cudaGetLastError());

@@ -153,8 +153,9 @@ void launch_label(const fx_layout& L, const void* k, const void* v, int64_t l_ne
 void launch_prefill_group(const fx_layout& L, const void* k, const void* v, double* rec,
                           void* scratch, cudaStream_t s);
 size_t prefill_group_scratch_bytes(const fx_layout& L);
+size_t decode_features_scratch_bytes(const fx_layout& L, int64_t l_new);
 void launch_decode_features(const fx_layout& L, const void* k, const void* v, int64_t l_new,
-                            const float* q, const double* rec, double* feats, double* gpu_norm,
+                            const float* q, const double* rec, double* feats, void* scratch,
                             cudaStream_t s);
 
 // fx_attend.cu
