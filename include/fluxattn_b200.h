@@ -268,6 +268,34 @@ FX_API int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, co
 FX_API int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
                               int64_t l_new, const float* q, const double* rec, double* features);
 
+/* ---- synthetic workload generator (workload.cpp) ------------------------- */
+/* WorkloadSpec (workload.hpp:16-54), same fields and defaults semantics. */
+typedef struct fx_workload_spec {
+    uint64_t seed;
+    int32_t layers, heads, group_size, head_dim, context_len, sink_tokens, local_tokens,
+        decode_steps;
+    double streaming_frac, retrieval_frac, sink_frac, diffuse_frac;
+    int32_t needles, needle_tokens;
+    double needle_strength, payload_gain, local_boost, query_jitter, streaming_jitter,
+        decoy_strength, decoy_payload_strength;
+    int32_t decoy_tokens, decoy_payload_tokens;
+    double query_drift;
+} fx_workload_spec;
+/* generate(spec) (workload.cpp:154-308) into the device cache: batch entry b
+ * is layer layers[b] of the workload seeded seeds[b] [host arrays, B each]
+ * (the reference has no batch: b = an independent Workload).  K/V bulk on the
+ * device (counter-based SplitMix64), the O(d)-per-head structure on the host.
+ * Outputs [dev, optional]: anchor_q [B][H][D], step_q [steps][B][H][D],
+ * step_new_k / step_new_v [steps][B][Hkv][D] (decode trace, workload.cpp:280-305);
+ * archetypes [host, optional] [B][H] (0 streaming, 1 retrieval, 2 sink decoy,
+ * 3 diffuse).  The layout must match the spec (heads / group_size groups,
+ * head_dim, sink / cpu / local lengths).  Synchronizes the ctx stream.
+ * Errors: infeasible-spec, bad-shape. */
+FX_API int fx_generate(fx_ctx* ctx, const fx_workload_spec* spec, const fx_layout* lay,
+                       const uint64_t* seeds, const int32_t* layers, void* k, void* v,
+                       float* anchor_q, int32_t steps, float* step_q, float* step_new_k,
+                       float* step_new_v, int32_t* archetypes);
+
 /* ---- context-parallel decode (C5) ------------------------------------------
  * The cpu segment is split into contiguous 128-row-aligned shards, one per
  * rank (sink rows on rank 0, local + decoded rows on the last rank), so block

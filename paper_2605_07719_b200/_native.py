@@ -47,6 +47,35 @@ class StepArgs(C.Structure):
                 ("l_cpu_total", _i64), ("cpu_offset", _i64), ("sel_in", _p)]
 
 
+class WorkloadSpec(C.Structure):
+    """fx_workload_spec (workload.hpp:16-54)."""
+
+    _fields_ = [("seed", C.c_uint64), ("layers", _i32), ("heads", _i32), ("group_size", _i32),
+                ("head_dim", _i32), ("context_len", _i32), ("sink_tokens", _i32),
+                ("local_tokens", _i32), ("decode_steps", _i32), ("streaming_frac", C.c_double),
+                ("retrieval_frac", C.c_double), ("sink_frac", C.c_double),
+                ("diffuse_frac", C.c_double), ("needles", _i32), ("needle_tokens", _i32),
+                ("needle_strength", C.c_double), ("payload_gain", C.c_double),
+                ("local_boost", C.c_double), ("query_jitter", C.c_double),
+                ("streaming_jitter", C.c_double), ("decoy_strength", C.c_double),
+                ("decoy_payload_strength", C.c_double), ("decoy_tokens", _i32),
+                ("decoy_payload_tokens", _i32), ("query_drift", C.c_double)]
+
+    DEFAULTS = dict(seed=1, layers=4, heads=8, group_size=4, head_dim=64, context_len=4096,
+                    sink_tokens=64, local_tokens=256, decode_steps=8, streaming_frac=0.5,
+                    retrieval_frac=0.5, sink_frac=0.0, diffuse_frac=0.0, needles=1,
+                    needle_tokens=16, needle_strength=10.0, payload_gain=3.0, local_boost=7.0,
+                    query_jitter=0.2, streaming_jitter=0.45, decoy_strength=6.0,
+                    decoy_payload_strength=4.0, decoy_tokens=160, decoy_payload_tokens=64,
+                    query_drift=0.98)
+
+    @classmethod
+    def make(cls, **kw):
+        d = dict(cls.DEFAULTS)
+        d.update(kw)
+        return cls(**d)
+
+
 class NativeError(RuntimeError):
     """A non-zero fx_* status; the message carries the reference error code."""
 
@@ -100,6 +129,8 @@ _SIGS = {
     "fx_prefill_stats": (C.c_int, [_p, C.POINTER(Layout), _p, _p, C.POINTER(_p * 4), _p,
                                    C.c_double, _i32, _p]),
     "fx_decode_features": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p]),
+    "fx_generate": (C.c_int, [_p, C.POINTER(WorkloadSpec), C.POINTER(Layout), _p, _p, _p, _p, _p,
+                              _i32, _p, _p, _p, _p]),
     "fx_label_heads": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, C.POINTER(_p * 4), _p,
                                  C.c_double, _i32, _p, _p, _p, _p, _p, _p, _p]),
 }

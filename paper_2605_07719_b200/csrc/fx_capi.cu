@@ -2,6 +2,7 @@
 // and the entry points that sequence the K1..K5 kernels.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -885,6 +886,48 @@ int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const v
         ctx->api.ensure(fx::decode_features_scratch_bytes(L, l_new));
         fx::launch_decode_features(L, k, v, l_new, q, rec, features, ctx->api.p, ctx->stream);
         ctx->launches += 3;
+    });
+}
+
+// ---- synthetic workload generator (workload.cpp) ---------------------------
+
+void* api_scratch(size_t bytes, void* c) {
+    fx_ctx* ctx = static_cast<fx_ctx*>(c);
+    ctx->api.ensure(bytes);
+    return ctx->api.p;
+}
+
+int fx_generate(fx_ctx* ctx, const fx_workload_spec* sp, const fx_layout* lay, const uint64_t* seeds,
+                const int32_t* layers, void* k, void* v, float* anchor_q, int32_t steps,
+                float* step_q, float* step_new_k, float* step_new_v, int32_t* archetypes) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(sp && seeds && layers && k && v, FX_ERR_STATE, "no-context: generate has no payload");
+        const fx_layout& L = *lay;
+        // validate_spec (workload.cpp:124-146)
+        FX_REQUIRE(sp->context_len > sp->sink_tokens + sp->local_tokens, FX_ERR_INVALID,
+                   "infeasible-spec: context shorter than sink+local defaults");
+        FX_REQUIRE(sp->heads > 0 && sp->group_size > 0 && sp->heads % sp->group_size == 0, FX_ERR_INVALID,
+                   "infeasible-spec: heads must be a multiple of group_size");
+        const double fsum = sp->streaming_frac + sp->retrieval_frac + sp->sink_frac + sp->diffuse_frac;
+        FX_REQUIRE(std::abs(fsum - 1.0) <= 1e-9, FX_ERR_INVALID,
+                   "infeasible-spec: archetype fractions must sum to 1");
+        FX_REQUIRE(sp->query_drift >= -1.0 && sp->query_drift <= 1.0, FX_ERR_INVALID,
+                   "infeasible-spec: query drift outside [-1, 1]");
+        const int64_t l_cpu = (int64_t)sp->context_len - sp->sink_tokens - sp->local_tokens;
+        FX_REQUIRE(!(sp->sink_frac > 0.0 && l_cpu < (int64_t)sp->decoy_tokens + sp->decoy_payload_tokens + 256),
+                   FX_ERR_INVALID, "infeasible-spec: cpu segment too small for decoy runs");
+        FX_REQUIRE(!(sp->retrieval_frac > 0.0 && l_cpu < (int64_t)sp->needles * sp->needle_tokens),
+                   FX_ERR_INVALID, "infeasible-spec: cpu segment too small for needles");
+        FX_REQUIRE(L.kv_heads == sp->heads / sp->group_size && L.group_size == sp->group_size &&
+                       L.head_dim == sp->head_dim && L.l_sink == sp->sink_tokens &&
+                       L.l_local == sp->local_tokens && L.l_cpu == l_cpu && L.l_cap >= sp->context_len,
+                   FX_ERR_INVALID, "bad-shape: layout does not match the workload spec");
+        FX_REQUIRE(steps >= 0, FX_ERR_INVALID, "bad-shape: negative step count");
+        fx::generate_workload(L, *sp, seeds, layers, k, v, anchor_q, steps, step_q, step_new_k,
+                              step_new_v, archetypes, api_scratch, ctx, ctx->stream);
+        ctx->launches += 2;
     });
 }
 

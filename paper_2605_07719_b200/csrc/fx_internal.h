@@ -158,6 +158,12 @@ void launch_decode_features(const fx_layout& L, const void* k, const void* v, in
                             const float* q, const double* rec, double* feats, void* scratch,
                             cudaStream_t s);
 
+// fx_workload.cu: generate(spec) into the device cache
+void generate_workload(const fx_layout& L, const fx_workload_spec& sp, const uint64_t* seeds,
+                       const int32_t* layers, void* k, void* v, float* anchor_q, int32_t steps,
+                       float* step_q, float* step_new_k, float* step_new_v, int32_t* archetypes,
+                       void* scratch_alloc(size_t, void*), void* alloc_ctx, cudaStream_t s);
+
 // fx_attend.cu
 // 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},
 // box {64, box_rows, D/64}, 128-byte swizzle (D multiple of 64).

@@ -545,6 +545,31 @@ class SparseDecoder:
             return o.cpu().numpy().copy(), ls.cpu().numpy().copy()
         return o, ls
 
+    # -- synthetic workload (workload.cpp) --------------------------------------
+    def generate(self, spec: dict, seeds=None, layers=None, steps: int = 0) -> dict:
+        """generate(spec) (workload.cpp:154-308) into this cache: batch entry b is
+        layer layers[b] of the workload seeded seeds[b] (default seed + b, layer 0).
+        Returns device tensors anchor [B][H][D], step_q [steps][B][H][D],
+        new_k / new_v [steps][B][Hkv][D] and host archetypes [B][H]."""
+        lay = self.lay
+        B, H, D, Hkv = lay.batch, self.heads, lay.head_dim, lay.kv_heads
+        sp = N.WorkloadSpec.make(**spec)
+        seeds = np.ascontiguousarray(seeds if seeds is not None else [sp.seed + b for b in range(B)],
+                                     np.uint64)
+        layers = np.ascontiguousarray(layers if layers is not None else [0] * B, np.int32)
+        dev = self.eng.device
+        out = dict(anchor=torch.empty((B, H, D), dtype=torch.float32, device=dev),
+                   step_q=torch.empty((max(steps, 1), B, H, D), dtype=torch.float32, device=dev),
+                   new_k=torch.empty((max(steps, 1), B, Hkv, D), dtype=torch.float32, device=dev),
+                   new_v=torch.empty((max(steps, 1), B, Hkv, D), dtype=torch.float32, device=dev))
+        arch = np.zeros((B, H), np.int32)
+        check(LIB.fx_generate(self.eng.ctx, C.byref(sp), C.byref(lay), seeds.ctypes.data,
+                              layers.ctypes.data, _ptr(self.k), _ptr(self.v), _ptr(out["anchor"]),
+                              int(steps), _ptr(out["step_q"]), _ptr(out["new_k"]),
+                              _ptr(out["new_v"]), arch.ctypes.data))
+        out["archetypes"] = arch
+        return out
+
     # -- output-aware labels (budget_oracle.cpp) --------------------------------
     def label_heads(self, q: torch.Tensor, tau: float = 0.10, output_only: bool = False) -> dict:
         """Oracle head properties of every query head (pipeline.cpp:256-276):
