@@ -51,6 +51,9 @@ def args_parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling run: timed loop only")
+    ap.add_argument("--data", default="reference", choices=["reference", "normal"],
+                    help="reference: the reference generator's workload (generate(spec), on "
+                         "device); normal: plain N(0,1) K/V")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
                     help="c2: one layer, batch 16 (the metric's config); c4: 32 layers x batch 8 "
                          "per GPU (configs[3], one 8-GPU shard), the layers' independent tasks "
@@ -181,18 +184,24 @@ def run_reference_arm(a):
     l_cpu = a.context - L_SINK - L_LOCAL
     rng = np.random.default_rng(7)
     groups = []
-    for g in range(HKV):
-        k = rng.standard_normal((a.context, D), dtype=np.float32)
-        v = rng.standard_normal((a.context, D), dtype=np.float32)
-        groups.append((k, v))
+    if a.data == "reference":  # the reference's own generator, sequence 0 (seed 1), layer 0
+        w = ref.generate(seed=1, layers=1, heads=H, group_size=G, head_dim=D,
+                         context_len=a.context, decode_steps=1)
+        groups = [w.group_kv(0, g) for g in range(HKV)]
+        q = w.queries(0, 0)
+    else:
+        for g in range(HKV):
+            k = rng.standard_normal((a.context, D), dtype=np.float32)
+            v = rng.standard_normal((a.context, D), dtype=np.float32)
+            groups.append((k, v))
+        q = rng.standard_normal((H, D)).astype(np.float32)
+        q *= np.sqrt(D) / np.linalg.norm(q, axis=-1, keepdims=True)
     bgt0, ks, st = head_props(a.batch)
     plans = []
     for g in range(HKV):
         sl = slice(g * G, (g + 1) * G)
         p = ref.plan_group(bgt0[0, sl], ks[0, sl], st[0, sl], l_cpu)
         plans.append(None if p["streaming_group"] else (p["block_size"], p["budgets"]))
-    q = rng.standard_normal((H, D)).astype(np.float32)
-    q *= np.sqrt(D) / np.linalg.norm(q, axis=-1, keepdims=True)
     times, n_tasks = reference_sample(ref, groups, plans, q, workers, a.warmup + a.steps)
     t = float(np.mean(times[a.warmup:])) if len(times) > a.warmup else float(np.mean(times))
     per_step = t * a.batch  # one sequence sampled; the batch has `batch` of them
@@ -201,7 +210,8 @@ def run_reference_arm(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": per_step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "data": ("synthetic: the reference's generate(spec), seed 1" if a.data == "reference"
+                 else "synthetic N(0,1)"),
         "config": {"workload": "C2: Llama-3-8B layer (32q/8kv, d128), 128K ctx, batch 16, "
                                "per-head budgets + per-group granularity via plan_group",
                    "context": a.context, "global_batch": a.batch * a.gpus,
@@ -275,11 +285,30 @@ def run_ours(a):
     shape = (B, HKV, SparseDecoder.cap_rows(a.context, total_steps), D)
     k = torch.empty(shape, dtype=torch.bfloat16, device=dev)
     v = torch.empty(shape, dtype=torch.bfloat16, device=dev)
-    for b in range(B):  # synthetic N(0,1) KV, generated on device
-        k[b].normal_(generator=gen)
-        v[b].normal_(generator=gen)
+    if a.data == "normal":  # plain N(0,1) KV, generated on device
+        for b in range(B):
+            k[b].normal_(generator=gen)
+            v[b].normal_(generator=gen)
     dec = SparseDecoder(eng, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, max_new=total_steps,
                         dtype="bf16", k=k, v=v)
+    gen_ms = None
+    if a.data == "reference":
+        # the reference's generate(spec) (WorkloadSpec defaults: 0.5 streaming / 0.5
+        # retrieval heads, one 16-token needle per retrieval head, local boost,
+        # drifting decode queries) on the device; entry b = (layer, sequence), the
+        # sequence's seed = 1 + its global index
+        spec = dict(seed=1, layers=a.layers, heads=H, group_size=G, head_dim=D,
+                    context_len=a.context, decode_steps=total_steps)
+        seqs = [b % a.seqs for b in range(B)]
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t_gen = time.time()
+        out = dec.generate(spec, seeds=[1 + rank * a.seqs + sq for sq in seqs],
+                           layers=[b // a.seqs for b in range(B)], steps=total_steps)
+        gen_ms = (time.time() - t_gen) * 1e3
+        qs = out["step_q"]
+        kv_new = torch.stack([out["new_k"], out["new_v"]], dim=1)
+        del out
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -291,16 +320,17 @@ def run_ours(a):
     bgt0, ks, st = head_props(B, seed=1 + rank)
     props = (torch.as_tensor(bgt0, device=dev), torch.as_tensor(ks, device=dev),
              torch.as_tensor(st, device=dev))
-    # drifting decode queries (workload.cpp:280-296 recipe), pre-generated on device
-    rho = 0.98
-    qs = torch.empty((total_steps, B, H, D), dtype=torch.float32, device=dev)
-    qs[0].normal_(generator=gen)
-    for t in range(1, total_steps):
-        noise = torch.randn((B, H, D), generator=gen, device=dev)
-        noise = noise / noise.norm(dim=-1, keepdim=True)
-        qs[t] = rho * qs[t - 1] / qs[t - 1].norm(dim=-1, keepdim=True) + (1 - rho * rho) ** 0.5 * noise
-    qs = qs / qs.norm(dim=-1, keepdim=True) * (D ** 0.5)
-    kv_new = torch.randn((total_steps, 2, B, HKV, D), generator=gen, device=dev)
+    if a.data == "normal":
+        # drifting decode queries (workload.cpp:280-296 recipe), pre-generated on device
+        rho = 0.98
+        qs = torch.empty((total_steps, B, H, D), dtype=torch.float32, device=dev)
+        qs[0].normal_(generator=gen)
+        for t in range(1, total_steps):
+            noise = torch.randn((B, H, D), generator=gen, device=dev)
+            noise = noise / noise.norm(dim=-1, keepdim=True)
+            qs[t] = rho * qs[t - 1] / qs[t - 1].norm(dim=-1, keepdim=True) + (1 - rho * rho) ** 0.5 * noise
+        qs = qs / qs.norm(dim=-1, keepdim=True) * (D ** 0.5)
+        kv_new = torch.randn((total_steps, 2, B, HKV, D), generator=gen, device=dev)
 
     step_i = [0]
 
@@ -341,7 +371,10 @@ def run_ours(a):
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
               "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-              "data": "synthetic (N(0,1) K/V generated on device; head properties drawn, seed 1)",
+              "data": ("synthetic: the reference's generate(spec) on device (WorkloadSpec defaults, "
+                       "seed 1 + sequence; N(0,1) K/V with planted needles, local boost, drifting "
+                       "queries); head properties drawn (seed 1)") if a.data == "reference" else
+                      "synthetic (N(0,1) K/V generated on device; head properties drawn, seed 1)",
               "gpu_launches": int(launches), "clocks": clk}
 
     if not a.quick:
@@ -529,7 +562,7 @@ def run_ours(a):
         "context": a.context, "global_batch": a.seqs * world, "seq_len": a.context,
         "parallelism": f"batch-sharded x{world} (no collective)", "kv_dtype": "bf16",
         "l2": "per-step working set > 1 GB (inputs larger than the 126 MB L2); no flush",
-        "meta_build_ms": meta_build_ms,
+        "meta_build_ms": meta_build_ms, "generate_ms": gen_ms,
         "budget_source": "drawn head properties (bgt0~U(.01,.05), k~U(0,.01), streaming~B(.5))"}
 
     # ---- CPU baseline: the compiled reference on a bounded sample (rank 0, N=1) ----
