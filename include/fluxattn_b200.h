@@ -296,6 +296,31 @@ FX_API int fx_generate(fx_ctx* ctx, const fx_workload_spec* spec, const fx_layou
                        float* anchor_q, int32_t steps, float* step_q, float* step_new_k,
                        float* step_new_v, int32_t* archetypes);
 
+/* ---- FXT1 workload traces (workload.cpp:311-433) ------------------------- */
+typedef struct fx_trace_info {
+    uint64_t input_hash, seed;
+    int32_t layers, heads, group_size, head_dim, context_len, sink_tokens, local_tokens,
+        decode_steps;
+} fx_trace_info;
+/* Read an FXT1 header (import_trace's checks: corrupt-trace / io-error). */
+FX_API int fx_trace_info_read(const char* path, fx_trace_info* info);
+/* import_trace for one layer into batch entry b of the device cache (f32 ->
+ * layout dtype); optional outputs [dev]: anchor_q [H][D], step_q [steps][H][D],
+ * new_k / new_v [steps][Hkv][D]; archetypes [host] [H]. */
+FX_API int fx_trace_load(fx_ctx* ctx, const char* path, int32_t layer, const fx_layout* lay,
+                         int32_t b, void* k, void* v, float* anchor_q, float* step_q,
+                         float* new_k, float* new_v, int32_t* archetypes);
+/* export_trace: layer ly of the trace = batch entry entries[ly] [host] of the
+ * device cache; per-layer arrays [dev] anchor_q [layers][H][D], step_q
+ * [layers][steps][H][D], new_k / new_v [layers][steps][Hkv][D] (NULL = zeros);
+ * archetypes [host] [layers][H] (NULL = diffuse), needle_count [host]
+ * [layers][H] with needles [host] (start, end) pairs in that order (NULL = none). */
+FX_API int fx_trace_save(fx_ctx* ctx, const char* path, const fx_trace_info* info,
+                         const fx_layout* lay, const int32_t* entries, const void* k,
+                         const void* v, const float* anchor_q, const float* step_q,
+                         const float* new_k, const float* new_v, const int32_t* archetypes,
+                         const int32_t* needle_count, const uint32_t* needles);
+
 /* ---- context-parallel decode (C5) ------------------------------------------
  * The cpu segment is split into contiguous 128-row-aligned shards, one per
  * rank (sink rows on rank 0, local + decoded rows on the last rank), so block

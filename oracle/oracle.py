@@ -388,6 +388,9 @@ class RefOracle:
                                    C.c_int, C.c_int, _f32p, C.c_double, _f64p, _f64p]
         L.ref_gpu_output_norm.argtypes = seg
         L.ref_gpu_output_norm.restype = C.c_double
+        L.ref_export_trace.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
+        L.ref_import_trace.argtypes = [C.c_char_p]
+        L.ref_import_trace.restype = C.c_void_p
         self.lib = L
 
     def _check(self, rc):
@@ -547,6 +550,16 @@ class RefOracle:
     def gpu_output_norm(self, k, v, seg, q):
         k, v = _f32(k), _f32(v)
         return self.lib.ref_gpu_output_norm(k, v, k.shape[1], *seg, _f32(q))
+
+    def export_trace(self, workload, path, input_hash=0):
+        self._check(self.lib.ref_export_trace(workload.h, path.encode(), input_hash))
+
+    def import_trace(self, path, **spec):
+        """import_trace -> a workload handle (spec gives the accessor shapes)."""
+        h = self.lib.ref_import_trace(path.encode())
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return _RefWorkload(self, h, spec)
 
     # -- executed scheduler (CPU baseline) -------------------------------
     def batch(self):

@@ -536,4 +536,17 @@ double ref_gpu_output_norm(const float* k, const float* v, std::size_t dim, std:
     return gpu_output_norm(std::span<const float>(q, dim), cache);
 }
 
+// FXT1 traces (workload.cpp:311-433)
+int ref_export_trace(void* h, const char* path, std::uint64_t input_hash) {
+    return guarded([&] { export_trace(*static_cast<Workload*>(h), path, input_hash); });
+}
+void* ref_import_trace(const char* path) {
+    try {
+        return new Workload(import_trace(path, nullptr));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 } // extern "C"

@@ -76,6 +76,15 @@ class WorkloadSpec(C.Structure):
         return cls(**d)
 
 
+class TraceInfo(C.Structure):
+    """fx_trace_info: the FXT1 header (workload.cpp:311-340)."""
+
+    _fields_ = [("input_hash", C.c_uint64), ("seed", C.c_uint64), ("layers", _i32),
+                ("heads", _i32), ("group_size", _i32), ("head_dim", _i32),
+                ("context_len", _i32), ("sink_tokens", _i32), ("local_tokens", _i32),
+                ("decode_steps", _i32)]
+
+
 class NativeError(RuntimeError):
     """A non-zero fx_* status; the message carries the reference error code."""
 
@@ -131,6 +140,11 @@ _SIGS = {
     "fx_decode_features": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p]),
     "fx_generate": (C.c_int, [_p, C.POINTER(WorkloadSpec), C.POINTER(Layout), _p, _p, _p, _p, _p,
                               _i32, _p, _p, _p, _p]),
+    "fx_trace_info_read": (C.c_int, [C.c_char_p, C.POINTER(TraceInfo)]),
+    "fx_trace_load": (C.c_int, [_p, C.c_char_p, _i32, C.POINTER(Layout), _i32, _p, _p, _p, _p,
+                                _p, _p, _p]),
+    "fx_trace_save": (C.c_int, [_p, C.c_char_p, C.POINTER(TraceInfo), C.POINTER(Layout), _p, _p,
+                                _p, _p, _p, _p, _p, _p, _p, _p]),
     "fx_label_heads": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, C.POINTER(_p * 4), _p,
                                  C.c_double, _i32, _p, _p, _p, _p, _p, _p, _p]),
 }

@@ -931,6 +931,45 @@ int fx_generate(fx_ctx* ctx, const fx_workload_spec* sp, const fx_layout* lay, c
     });
 }
 
+// ---- FXT1 traces (workload.cpp:311-433) -------------------------------------
+
+int fx_trace_info_read(const char* path, fx_trace_info* info) {
+    return guarded([&] {
+        FX_REQUIRE(info != nullptr, FX_ERR_INVALID, "bad-shape: null info");
+        fx::trace_info(path, info);
+    });
+}
+
+int fx_trace_load(fx_ctx* ctx, const char* path, int32_t layer, const fx_layout* lay, int32_t b,
+                  void* k, void* v, float* anchor_q, float* step_q, float* new_k, float* new_v,
+                  int32_t* archetypes) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(k && v, FX_ERR_STATE, "no-context: trace load has no cache");
+        fx::trace_load(path, layer, *lay, b, k, v, anchor_q, step_q, new_k, new_v, archetypes,
+                       api_scratch, ctx, ctx->stream);
+        ctx->launches += lay->dtype == FX_BF16 ? 2 * lay->kv_heads : 0;
+    });
+}
+
+int fx_trace_save(fx_ctx* ctx, const char* path, const fx_trace_info* info, const fx_layout* lay,
+                  const int32_t* entries, const void* k, const void* v, const float* anchor_q,
+                  const float* step_q, const float* new_k, const float* new_v,
+                  const int32_t* archetypes, const int32_t* needle_count, const uint32_t* needles) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(info && entries && k && v, FX_ERR_STATE, "no-context: trace save has no payload");
+        FX_REQUIRE(info->layers > 0 && info->heads > 0 && info->group_size > 0 &&
+                       info->heads % info->group_size == 0 && info->decode_steps >= 0,
+                   FX_ERR_INVALID, "bad-shape: implausible trace header");
+        FX_REQUIRE(!needle_count || needles, FX_ERR_INVALID, "bad-shape: needle counts without ranges");
+        fx::trace_save(path, *info, *lay, entries, k, v, anchor_q, step_q, new_k, new_v, archetypes,
+                       needle_count, needles, ctx->stream);
+    });
+}
+
 // ---- context-parallel decode (C5) ----------------------------------------
 
 int fx_cp_candidates(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, int64_t cap,

@@ -164,6 +164,17 @@ void generate_workload(const fx_layout& L, const fx_workload_spec& sp, const uin
                        float* step_q, float* step_new_k, float* step_new_v, int32_t* archetypes,
                        void* scratch_alloc(size_t, void*), void* alloc_ctx, cudaStream_t s);
 
+// fx_trace.cu: FXT1 traces
+void trace_info(const char* path, fx_trace_info* info);
+void trace_load(const char* path, int32_t layer, const fx_layout& L, int32_t b, void* k, void* v,
+                float* anchor_q, float* step_q, float* new_k, float* new_v, int32_t* archetypes,
+                void* scratch_alloc(size_t, void*), void* alloc_ctx, cudaStream_t s);
+void trace_save(const char* path, const fx_trace_info& h, const fx_layout& L, const int32_t* entries,
+                const void* k, const void* v, const float* anchor_q, const float* step_q,
+                const float* new_k, const float* new_v, const int32_t* archetypes,
+                const int32_t* needle_count, const uint32_t* needles, cudaStream_t s);
+void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream_t s);
+
 // fx_attend.cu
 // 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},
 // box {64, box_rows, D/64}, 128-byte swizzle (D multiple of 64).

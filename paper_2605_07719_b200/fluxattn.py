@@ -570,6 +570,42 @@ class SparseDecoder:
         out["archetypes"] = arch
         return out
 
+    # -- FXT1 traces (workload.cpp:311-433) -------------------------------------
+    @staticmethod
+    def trace_info(path: str) -> "N.TraceInfo":
+        info = N.TraceInfo()
+        check(LIB.fx_trace_info_read(path.encode(), C.byref(info)))
+        return info
+
+    def load_trace(self, path: str, layer: int = 0, b: int = 0) -> dict:
+        """import_trace of one layer into batch entry b; returns the device
+        query / decoded-row arrays and the host archetypes of that layer."""
+        info = self.trace_info(path)
+        H, D, Hkv, S = info.heads, info.head_dim, info.heads // info.group_size, info.decode_steps
+        dev = self.eng.device
+        out = dict(anchor=torch.empty((H, D), dtype=torch.float32, device=dev),
+                   step_q=torch.empty((max(S, 1), H, D), dtype=torch.float32, device=dev),
+                   new_k=torch.empty((max(S, 1), Hkv, D), dtype=torch.float32, device=dev),
+                   new_v=torch.empty((max(S, 1), Hkv, D), dtype=torch.float32, device=dev))
+        arch = np.zeros(H, np.int32)
+        check(LIB.fx_trace_load(self.eng.ctx, path.encode(), int(layer), C.byref(self.lay), int(b),
+                                _ptr(self.k), _ptr(self.v), _ptr(out["anchor"]), _ptr(out["step_q"]),
+                                _ptr(out["new_k"]), _ptr(out["new_v"]), arch.ctypes.data))
+        out["archetypes"] = arch
+        return out
+
+    def save_trace(self, path: str, info: "N.TraceInfo", entries, anchor=None, step_q=None,
+                   new_k=None, new_v=None, archetypes=None) -> None:
+        """export_trace: trace layer ly = batch entry entries[ly]; per-layer
+        device arrays anchor [layers][H][D], step_q [layers][steps][H][D],
+        new_k / new_v [layers][steps][Hkv][D]; host archetypes [layers][H]."""
+        ent = np.ascontiguousarray(entries, np.int32)
+        arch = None if archetypes is None else np.ascontiguousarray(archetypes, np.int32)
+        check(LIB.fx_trace_save(self.eng.ctx, path.encode(), C.byref(info), C.byref(self.lay),
+                                ent.ctypes.data, _ptr(self.k), _ptr(self.v), _ptr(anchor),
+                                _ptr(step_q), _ptr(new_k), _ptr(new_v),
+                                None if arch is None else arch.ctypes.data, None, None))
+
     # -- output-aware labels (budget_oracle.cpp) --------------------------------
     def label_heads(self, q: torch.Tensor, tau: float = 0.10, output_only: bool = False) -> dict:
         """Oracle head properties of every query head (pipeline.cpp:256-276):

@@ -50,3 +50,53 @@ def test_generate_matches_reference(engine, refo, spec):
     w2 = refo.generate(**dict(spec, seed=spec["seed"] + 1))
     k2, _ = w2.group_kv(0, 0)
     assert np.mean(dec.k[1, 0, :L].cpu().numpy() == k2) > 0.999
+
+
+def test_fxt1_trace_roundtrip(engine, refo, tmp_path):
+    """export_trace (reference) -> fx_trace_load: the layer's K/V, queries and
+    decode trace bit-exact; fx_trace_save -> import_trace (reference): the same."""
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    spec = dict(heads=8, group_size=4, head_dim=64, context_len=2048, layers=2, decode_steps=2,
+                seed=3)
+    w = refo.generate(**spec)
+    path = str(tmp_path / "ref.fxt1")
+    refo.export_trace(w, path, 77)
+    info = SparseDecoder.trace_info(path)
+    assert (info.input_hash, info.seed, info.layers, info.heads) == (77, 3, 2, 8)
+    L, D, Hkv = 2048, 64, 2
+    dec = SparseDecoder(engine, 2, Hkv, 4, D, 64, L - 320, 256, max_new=4, dtype="f32")
+    for layer in range(2):
+        out = dec.load_trace(path, layer=layer, b=layer)
+        assert np.array_equal(out["archetypes"], [w.archetype(layer, h) for h in range(8)])
+        assert np.array_equal(out["anchor"].cpu().numpy(), w.queries(layer, -1))
+        for st in range(2):
+            assert np.array_equal(out["step_q"][st].cpu().numpy(), w.queries(layer, st))
+            nk, nv = w.new_kv(layer, st)
+            assert np.array_equal(out["new_k"][st].cpu().numpy(), nk)
+        for g in range(Hkv):
+            k, v = w.group_kv(layer, g)
+            assert np.array_equal(dec.k[layer, g, :L].cpu().numpy(), k)
+            assert np.array_equal(dec.v[layer, g, :L].cpu().numpy(), v)
+    # save from the device cache, read back with the reference's import_trace
+    anchors = torch.stack([torch.as_tensor(w.queries(ly, -1)) for ly in range(2)]).cuda()
+    steps_q = torch.stack([torch.stack([torch.as_tensor(w.queries(ly, st)) for st in range(2)])
+                           for ly in range(2)]).cuda()
+    nks = torch.stack([torch.stack([torch.as_tensor(w.new_kv(ly, st)[0]) for st in range(2)])
+                       for ly in range(2)]).cuda()
+    nvs = torch.stack([torch.stack([torch.as_tensor(w.new_kv(ly, st)[1]) for st in range(2)])
+                       for ly in range(2)]).cuda()
+    arch = np.array([[w.archetype(ly, h) for h in range(8)] for ly in range(2)], np.int32)
+    out_path = str(tmp_path / "ours.fxt1")
+    dec.save_trace(out_path, info, [0, 1], anchor=anchors, step_q=steps_q, new_k=nks, new_v=nvs,
+                   archetypes=arch)
+    w2 = refo.import_trace(out_path, **spec)
+    for ly in range(2):
+        for g in range(Hkv):
+            a, b = w.group_kv(ly, g), w2.group_kv(ly, g)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert np.array_equal(w.queries(ly, 1), w2.queries(ly, 1))
+        assert [w2.archetype(ly, h) for h in range(8)] == arch[ly].tolist()
+    with open(out_path, "r+b") as f:  # corrupt magic -> the reference's error code
+        f.write(b"XXXX")
+    with pytest.raises(RuntimeError, match="^corrupt-trace"):
+        SparseDecoder.trace_info(out_path)
