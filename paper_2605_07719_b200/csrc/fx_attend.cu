@@ -548,7 +548,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
     int st = 0;
     uint32_t ph = 0;
 #ifdef FX_TRACE
-    if (tid == 0) g_trace[blockIdx.x * 12 + 0] = globaltimer();
+    if (tid == 0) {
+        g_trace[blockIdx.x * 12 + 0] = globaltimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace[blockIdx.x * 12 + 11] = smid;
+    }
     int runs = 0, tiles = 0;
     long long t_wait = 0, t_first = 0, t_flush = 0, tw0 = 0;
 #endif

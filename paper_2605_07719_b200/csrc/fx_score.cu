@@ -30,6 +30,18 @@ namespace {
 
 constexpr int kTileBlocks = 512;  // blocks per CTA (8 MMA m-tiles per warp)
 
+#ifdef FX_TRACE  // profiling build only: per-CTA phase times of the TMA scorer
+__device__ long long g_score_trace[8 * 512];
+__device__ __forceinline__ long long stimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SC_MARK(i) g_score_trace[blockIdx.x * 8 + (i)] = stimer();
+#else
+#define SC_MARK(i)
+#endif
+
 struct MetaPtrs {
     const void* p[4];
 };
@@ -126,6 +138,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     int64_t l_cpu, float* __restrict__ approx, int64_t stride) {
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 0) { SC_MARK(0) }
     using C = ScoreCfg<D>;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -176,6 +189,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     if (warp == kSCWarps) {
         // ------------------------------ producer ------------------------------
         if (lane == 0) {
+            SC_MARK(1)
             for (int l = 0; l < 4; ++l) tma_prefetch_desc(&maps.lvl[l]);
             int st = 0;
             uint32_t ph = 0;
@@ -275,6 +289,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
         if (first_bg >= 0) {  // prefetched; now wait for the first box
             first_bg = -1;
             mbar_wait(full + st, ph);
+            if (tid == 0) { SC_MARK(2) }
             H = hdr[st];
             if (H.end) break;
             if (H.bg != cur) continue;  // (cannot happen: same range arithmetic)
@@ -310,6 +325,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
             ph ^= 1u;
         }
     }
+    if (tid == 0) { SC_MARK(3) }
 }
 
 // ---------------------------------------------------------------------------
@@ -468,5 +484,11 @@ void launch_approx_scores(const fx_layout& L, const void* const meta[4], const f
     else fail(FX_ERR_INVALID, "bad-shape: batched scoring supports head_dim 64 or 128");
     FX_CUDA(cudaGetLastError());
 }
+
+#ifdef FX_TRACE
+extern "C" FX_API int fx_debug_score_trace(long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_score_trace, sizeof(long long) * n) == cudaSuccess ? 0 : -2;
+}
+#endif
 
 }  // namespace fx
