@@ -54,10 +54,12 @@ def args_parse():
     ap.add_argument("--data", default="reference", choices=["reference", "normal"],
                     help="reference: the reference generator's workload (generate(spec), on "
                          "device); normal: plain N(0,1) K/V")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
                     help="c2: one layer, batch 16 (the metric's config); c4: 32 layers x batch 8 "
                          "per GPU (configs[3], one 8-GPU shard), the layers' independent tasks "
-                         "batched into one step like run_decode's single queue (pipeline.cpp:354)")
+                         "batched into one step like run_decode's single queue (pipeline.cpp:354); "
+                         "c5: 1M context, batch 4, context-parallel over the torchrun ranks "
+                         "(configs[4]; one rank = the single-device step)")
     a = ap.parse_args()
     if a.workload == "c4":
         a.layers, a.seqs = 32, 8
@@ -260,6 +262,97 @@ def algorithmic_bytes(dec, q_bytes_per_head=D * 4):
     return meta_bytes, attend
 
 
+def run_c5(a):
+    """configs[4]: 1M-token context, batch 4, the cpu segment split over the
+    ranks (context_parallel.py; NCCL all-gathers of the k-th keys, the
+    candidates and the (o, lse) partials).  Strong scaling: the job is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local)
+    from paper_2605_07719_b200.context_parallel import CPShard, TorchComm, cp_decode_step, shard_kv
+    from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
+
+    B, ctx = 4, 1 << 20
+    l_cpu = ctx - L_SINK - L_LOCAL
+    total = a.warmup + a.steps + 2
+    eng = Engine(local)
+    full = SparseDecoder(eng, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, max_new=total, dtype="bf16")
+    out = full.generate(dict(seed=1, layers=1, heads=H, group_size=G, head_dim=D, context_len=ctx,
+                             decode_steps=total), seeds=[1 + b for b in range(B)], layers=[0] * B,
+                        steps=total)
+    qs, nk, nv = out["step_q"], out["new_k"], out["new_v"]
+    bgt0, ks, st = head_props(B, seed=1)
+    props = tuple(torch.as_tensor(x, device=dev) for x in (bgt0, ks, st))
+    if world == 1:
+        full.build_metadata()
+        dec, shards, comm = full, None, None
+    else:
+        kr = shard_kv(full.k, L_SINK, l_cpu, L_LOCAL, rank, world, total)
+        vr = shard_kv(full.v, L_SINK, l_cpu, L_LOCAL, rank, world, total)
+        del full
+        torch.cuda.empty_cache()
+        sh = CPShard(eng, rank, world, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, total, "bf16", k=kr, v=vr)
+        sh.dec.build_metadata()
+        dec, shards, comm = sh.dec, [sh], TorchComm()
+    step_i = [0]
+
+    def one_step():
+        i = step_i[0]
+        if shards is None:
+            dec.step(qs[i], props=props)
+            dec.append(nk[i], nv[i])
+        else:
+            cp_decode_step(shards, comm, qs[i], props=props)
+            if shards[0].is_last:
+                dec.append(nk[i], nv[i])
+        step_i[0] += 1
+
+    for _ in range(a.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = eng.launches()
+    t0.record()
+    for _ in range(a.steps):
+        one_step()
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": a.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: the reference's generate(spec) on device, seed 1 + sequence",
+            "gpu_launches": int(eng.launches() - n0), "clocks": clk,
+            "config": {"workload": "C5: Llama-3-8B layer, 1M ctx, batch 4, per-head budgets from "
+                                   "plan_group over the whole sequence",
+                       "context": ctx, "global_batch": B, "seq_len": ctx,
+                       "parallelism": "single device" if world == 1 else
+                       f"context-parallel x{world} (NCCL all-gathers: k-th keys, candidates, "
+                       f"(o, lse))"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -377,6 +470,16 @@ def run_ours(a):
                       "synthetic (N(0,1) K/V generated on device; head properties drawn, seed 1)",
               "gpu_launches": int(launches), "clocks": clk}
 
+    if a.quick:
+        # profiling runs (ncu): the algorithmic bytes of the attention launch of a
+        # few more steps, so a captured launch's DRAM bytes can be set against
+        # the bytes it had to move (untimed)
+        qb = []
+        for _ in range(3):
+            one_step()
+            torch.cuda.synchronize()
+            qb.append(algorithmic_bytes(dec)[1])
+        result["quick_attend_bytes_next_steps"] = qb
     if not a.quick:
         # ---- per-kernel CUDA-event timing pass (same steps, same stream) ----
         import ctypes as C
@@ -601,6 +704,9 @@ def main():
     a = args_parse()
     if a.impl == "reference":
         run_reference_arm(a)
+        return
+    if a.workload == "c5":
+        run_c5(a)
         return
     run_ours(a)
 

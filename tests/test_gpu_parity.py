@@ -489,3 +489,17 @@ def test_decode_step_every_head_written_repeated(engine, G):
             first = o.clone()
         else:
             assert torch.equal(o, first)
+
+
+def test_decode_step_without_cpu_segment(engine, coracle):
+    """l_cpu = 0 (context fits the defaults): no metadata, no selection; the
+    output is default_kv_attention (sink, local, decoded; attention.cpp:143-151)."""
+    dec, host, q = make_decoder(engine, 2, 2, 4, 128, 64, 0, 256, "bf16", seed=3, n_new=3)
+    o, lse = dec.step(torch.as_tensor(q).cuda(), fixed=(16, 0.05))
+    torch.cuda.synchronize()
+    o, lse = o.cpu().numpy(), lse.cpu().numpy()
+    for (b, g), (k, v) in host.items():
+        wo, wl, _ = coracle.execute_group(k, v, (64, 0, 256, 3), q[b, g * 4:(g + 1) * 4], 16,
+                                          np.full(4, 0.05))
+        assert rel_err(o[b, g * 4:(g + 1) * 4], wo) < TOL["bf16"]
+        assert np.abs(lse[b, g * 4:(g + 1) * 4] - wl).max() < 1e-2
