@@ -97,7 +97,7 @@ def ncu_traffic(kernel, workload="c2"):
             t = json.load(f)
         for name, rec in t["kernels"].items():
             if kernel in name:
-                return rec["dram_bytes_per_launch"]
+                return rec
     except Exception:
         pass
     return None
@@ -505,7 +505,9 @@ def run_ours(a):
         result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3+K4)",
                               "achieved": achieved, "peak": peak, "unit": "GB/s",
                               "frac": achieved / peak, "peak_kind": peak_kind, "timing": "per-kernel CUDA events in a separate pass with PDL off (events bracket each kernel alone)",
-                              "traffic": ncu_traffic("k_attend", a.workload),
+                              "traffic": (ncu_traffic("k_attend", a.workload) or {}).get("dram_bytes_per_launch"),
+                              "traffic_launch_algorithmic_bytes": (ncu_traffic("k_attend", a.workload) or {}).get(
+                                  "algorithmic_bytes_of_captured_launch"),
                               "algorithmic_bytes_per_launch": attend_b / a.steps}
         score_ms = kt.get("score", float("nan"))
         step_bytes = (meta_b + attend_b) / a.steps
