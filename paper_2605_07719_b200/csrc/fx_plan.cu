@@ -118,12 +118,8 @@ __device__ __forceinline__ double linear_row(const double* __restrict__ wt, doub
 }
 
 constexpr int kF = 41, kH1 = 256, kH2 = 384;
-constexpr int kRows = 4;  // feature rows per CTA: each weight is read once per 4 rows
 
-// kRows feature rows per CTA (384 threads): normalize -> 41->256->384->3.
-// Thread o computes output o of every row: the weight w[i][o] is loaded once
-// and applied to the kRows activations; each row's sum stays bias-first,
-// sequential over i, unfused (predictor.cpp:40-53).
+// One CTA (384 threads) per feature row: normalize -> 41->256->384->3.
 __global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
                                                  const double* __restrict__ b1,
                                                  const double* __restrict__ w2t,
@@ -132,65 +128,35 @@ __global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
                                                  const double* __restrict__ b3,
                                                  const double* __restrict__ mu,
                                                  const double* __restrict__ sigma,
-                                                 const double* __restrict__ feats, int n,
+                                                 const double* __restrict__ feats,
                                                  double* __restrict__ bgt0, double* __restrict__ kslope,
                                                  int32_t* __restrict__ streaming,
                                                  double* __restrict__ zout) {
-    __shared__ double x[kRows][kF], a1[kRows][kH1], a2[kRows][kH2];
-    const int r0 = blockIdx.x * kRows, t = threadIdx.x;
-    const int nr = min(kRows, n - r0);
-    for (int e = t; e < kRows * kF; e += blockDim.x) {  // features.cpp:226-233
-        const int r = e / kF, f = e % kF;
-        double v = 0.0;
-        if (r < nr) {
-            const double sg = sigma[f];
-            v = sg > 0.0 ? __ddiv_rn(__dsub_rn(feats[(int64_t)(r0 + r) * kF + f], mu[f]), sg) : 0.0;
-        }
-        x[r][f] = v;
+    __shared__ double x[kF], a1[kH1], a2[kH2];
+    const int r = blockIdx.x, t = threadIdx.x;
+    if (t < kF) {  // features.cpp:226-233
+        const double sg = sigma[t];
+        x[t] = sg > 0.0 ? __ddiv_rn(__dsub_rn(feats[(int64_t)r * kF + t], mu[t]), sg) : 0.0;
     }
     __syncthreads();
     if (t < kH1) {
-        double s[kRows];
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) s[r] = b1[t];
-#pragma unroll 8
-        for (int i = 0; i < kF; ++i) {
-            const double w = w1t[(int64_t)i * kH1 + t];
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) s[r] = __dadd_rn(s[r], __dmul_rn(x[r][i], w));
-        }
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) a1[r][t] = s[r] > 0.0 ? s[r] : 0.0;
+        const double s = linear_row(w1t, b1[t], x, kF, kH1, t);
+        a1[t] = s > 0.0 ? s : 0.0;
     }
     __syncthreads();
     {
-        double s[kRows];
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) s[r] = b2[t];
-#pragma unroll 8
-        for (int i = 0; i < kH1; ++i) {
-            const double w = w2t[(int64_t)i * kH2 + t];
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) s[r] = __dadd_rn(s[r], __dmul_rn(a1[r][i], w));
-        }
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) a2[r][t] = s[r] > 0.0 ? s[r] : 0.0;
+        const double s = linear_row(w2t, b2[t], a1, kH1, kH2, t);
+        a2[t] = s > 0.0 ? s : 0.0;
     }
     __syncthreads();
-    if (t < 3 * kRows) {
-        const int r = t / 3, o = t % 3;
-        if (r < nr) {
-            double z = b3[o];
-#pragma unroll 8
-            for (int i = 0; i < kH2; ++i) z = __dadd_rn(z, __dmul_rn(a2[r][i], w3t[(int64_t)i * 3 + o]));
-            const int64_t row = r0 + r;
-            if (zout) zout[row * 3 + o] = z;
-            if (o == 0) bgt0[row] = clamp01(z);
-            if (o == 1) kslope[row] = z;
-            if (o == 2) {
-                const double sp = 1.0 / (1.0 + exp(-z));  // sigmoid, predictor.cpp:20
-                streaming[row] = sp >= 0.5 ? 1 : 0;          // pipeline.cpp:288
-            }
+    if (t < 3) {
+        const double z = linear_row(w3t, b3[t], a2, kH2, 3, t);
+        if (zout) zout[(int64_t)r * 3 + t] = z;
+        if (t == 0) bgt0[r] = clamp01(z);
+        if (t == 1) kslope[r] = z;
+        if (t == 2) {
+            const double sp = 1.0 / (1.0 + exp(-z));  // sigmoid, predictor.cpp:20
+            streaming[r] = sp >= 0.5 ? 1 : 0;          // pipeline.cpp:288
         }
     }
 }
@@ -227,8 +193,8 @@ void launch_predict(int n, const double* w1t, const double* b1, const double* w2
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
                     int32_t* streaming, double* z, cudaStream_t s) {
     if (n <= 0) return;
-    k_predict<<<(n + kRows - 1) / kRows, kH2, 0, s>>>(w1t, b1, w2t, b2, w3t, b3, mu, sigma, feats, n,
-                                                     bgt0, kslope, streaming, z);
+    k_predict<<<n, kH2, 0, s>>>(w1t, b1, w2t, b2, w3t, b3, mu, sigma, feats, bgt0, kslope,
+                                streaming, z);
     FX_CUDA(cudaGetLastError());
 }
 
