@@ -15,13 +15,12 @@ constexpr int kMaxWords = 4096;      // nblk <= 131072 per (b, g) at the chosen 
 // Standalone only when no k_select ran this step (given selection / empty cpu
 // segment); otherwise the selection kernel's fused tail builds the boxes.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_worklist(WorklistArgs w, int stage_words) {
+__global__ void __launch_bounds__(256) k_worklist(WorklistArgs w) {
     pdl_wait();
     pdl_trigger();
     __shared__ int32_t wcnt[kMaxWords];
     __shared__ int64_t wsum[257];
-    extern __shared__ uint32_t s_bits[];
-    worklist_group(w, blockIdx.x, wcnt, wsum, s_bits, stage_words);
+    worklist_group(w, blockIdx.x, wcnt, wsum);
     worklist_publish(w, gridDim.x);
 }
 
@@ -84,14 +83,9 @@ void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
                      int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s) {
     FX_REQUIRE(L.group_size <= 16, FX_ERR_INVALID, "bad-shape: group_size must be <= 16");
     const int n_bg = L.batch * L.kv_heads;
-    // stage up to 96 KB of selection words per group in smem
-    const int64_t want = (int64_t)L.group_size * cdiv(std::max<int64_t>(1, level_blocks(L.l_cpu, 16)), 32);
-    const int stage_words = (int)std::min<int64_t>(want, 24576);
-    const size_t smem = (size_t)stage_words * 4;
-    FX_CUDA(cudaFuncSetAttribute(k_worklist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const WorklistArgs w{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + l_new, blk, sel_bits,
                          sel_words, boxes, box_stride, bg_count, bg_start, done + n_bg};
-    launch_pdl(k_worklist, n_bg, 256, smem, s, w, stage_words);
+    launch_pdl(k_worklist, n_bg, 256, 0, s, w);
     FX_CUDA(cudaGetLastError());
 }
 

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kT) k_select(
     int D, int64_t l_cpu, const float* __restrict__ approx, int64_t astride, double eps_scale,
     uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap, WorklistArgs wl,
-    int32_t* __restrict__ sel_done, int stage_words) {
+    int32_t* __restrict__ sel_done) {
     pdl_wait();
     pdl_trigger();
     SEL_MARK(10);
@@ -414,11 +414,11 @@ __global__ void __launch_bounds__(kT) k_select(
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // dynamic smem (keys | histogram | ...) is free now: word counts, then staged masks
+    // dynamic smem (keys | histogram | ...) is free now: the per-word box counts
     extern __shared__ __align__(16) unsigned char dsm[];
     int32_t* wcnt = reinterpret_cast<int32_t*>(dsm);
     SEL_MARK(8);
-    worklist_group(wl, bg, wcnt, s_wsum, reinterpret_cast<uint32_t*>(dsm) + kMaxWords, stage_words);
+    worklist_group(wl, bg, wcnt, s_wsum);
     worklist_publish(wl, (int)(gridDim.x / G));
     SEL_MARK(9);
 }
@@ -442,14 +442,10 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
     size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)L.head_dim * 8 +
                   (size_t)kSmallCand * 12;
     WorklistArgs w{};
-    int stage_words = 0;
     if (wl) {
         FX_REQUIRE(L.group_size <= 16, FX_ERR_INVALID, "bad-shape: group_size must be <= 16");
         w = *wl;
-        // fused worklist: kMaxWords counts + the G staged masks (up to 96 KB) in the same smem
-        const int64_t want = (int64_t)L.group_size * cdiv(std::max<int64_t>(1, nmax), 32);
-        stage_words = (int)std::min<int64_t>(want, 24576);
-        smem = std::max(smem, (size_t)(kMaxWords + stage_words) * 4);
+        smem = std::max(smem, (size_t)kMaxWords * 4);  // fused worklist: the word counts
     }
     const double eps = approx_eps_scale(L);
     if (L.dtype == FX_BF16) {
@@ -457,13 +453,13 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
         launch_pdl(k_select<FX_BF16>, (unsigned)heads, kT, smem, s,
             mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
             approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
-            w, sel_done, stage_words);
+            w, sel_done);
     } else {
         FX_CUDA(cudaFuncSetAttribute(k_select<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         launch_pdl(k_select<FX_F32>, (unsigned)heads, kT, smem, s,
             mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
             approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
-            w, sel_done, stage_words);
+            w, sel_done);
     }
     FX_CUDA(cudaGetLastError());
 }

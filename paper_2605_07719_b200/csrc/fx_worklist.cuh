@@ -67,12 +67,11 @@ __device__ inline int64_t block_exclusive_scan(int32_t* cnt, int n, int64_t* wsu
     return wsum[nt];
 }
 
-// Boxes of group bg.  Smem: wcnt >= ceil(nblk/32) words, wsum >= blockDim + 1,
-// s_bits (stage_words words) stages the G masks when they fit.  All threads.
-__device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wcnt, int64_t* wsum,
-                                      uint32_t* s_bits, int stage_words) {
+// Boxes of group bg.  Smem: wcnt >= ceil(nblk/32) words, wsum >= blockDim + 1.
+// All threads of the CTA.
+__device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wcnt, int64_t* wsum) {
     const int b = bg / w.Hkv, g = bg % w.Hkv, G = w.G;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nt = blockDim.x;
+    const int t = threadIdx.x, nt = blockDim.x;
     const int blk = __ldcg(w.blk + bg);
     const uint16_t all = (uint16_t)((1u << G) - 1u);
     Box* out = w.boxes + (int64_t)bg * w.box_stride;
@@ -103,10 +102,6 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
         const int64_t last = nblk - 1;
         const int nb_last = (int)cdiv_dev(w.l_cpu - last * blk, kBoxRows);
         const uint32_t* hg = w.sel_bits + ((int64_t)b * w.Hkv * G + (int64_t)g * G) * w.sel_words;
-        (void)s_bits;
-        (void)stage_words;
-        (void)lane;
-        (void)warp;
         for (int j = t; j < W; j += nt) {
             uint32_t u = 0;
             for (int h = 0; h < G; ++h) u |= __ldcg(hg + (int64_t)h * w.sel_words + j);
