@@ -271,10 +271,10 @@ def run_c5(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(os.environ.get("FX_BENCH_BACKEND", "nccl"), init_method="env://")
     dev = torch.device("cuda", local)
     from paper_2605_07719_b200.context_parallel import CPShard, TorchComm, cp_decode_step, shard_kv
     from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
@@ -359,10 +359,12 @@ def run_ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; the modulo only matters for a multi-rank smoke test of this
+    # code path on a single-GPU box (FX_BENCH_BACKEND=gloo), never for a measurement
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(os.environ.get("FX_BENCH_BACKEND", "nccl"), init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 

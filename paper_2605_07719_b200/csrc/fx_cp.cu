@@ -222,7 +222,7 @@ void launch_cp_candidates(const fx_layout& L, const void* const meta[4], const f
     const int sort_n = cp_sort_n(std::max<int64_t>(1, level_blocks(L.l_cpu, 16)));
     const size_t smem = (size_t)sort_n * 12;
     FX_REQUIRE(smem <= 200 * 1024, FX_ERR_INVALID,
-               "bad-shape: context-parallel shard too long (more than 16384 blocks of 16)");
+               "bad-shape: context-parallel shard too long (more than 16384 blocks of 16, i.e. 262144 cpu rows per rank; use more ranks)");
     const MetaLevels ml{{meta[0], meta[1], meta[2], meta[3]}};
     if (L.dtype == FX_BF16) {
         auto kern = k_cp_candidates<FX_BF16>;
