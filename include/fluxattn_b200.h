@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FX_ABI_VERSION 2
+#define FX_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define FX_API __attribute__((visibility("default")))
@@ -115,6 +115,11 @@ typedef struct fx_step_args {
     int64_t cpu_offset;          /* global row of this shard's first cpu row (multiple of 128) */
     const uint32_t* sel_in;      /* given selection [B][H][sel_words] over this shard's blocks at
                                     plan_blk: skips score/select (requires FX_PLAN_GIVEN) */
+    /* optional fused append (append_new, kv_cache.hpp:68-73): [B][Hkv][D] f32 rows written
+       as decoded row l_new of every (b, g) before this step attends l_new + 1 rows -- the
+       previous step's token, saving the separate fx_append_kv launch */
+    const float* append_k;
+    const float* append_v;
 } fx_step_args;
 
 /* ---- context, errors, memory ------------------------------------------ */

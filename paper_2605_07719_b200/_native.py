@@ -19,7 +19,7 @@ FX_PLAN_PROPS = 0
 FX_PLAN_FIXED = 1
 FX_PLAN_FULL = 2
 FX_PLAN_GIVEN = 3
-ABI_VERSION = 2
+ABI_VERSION = 3
 KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append")
 
 _p = C.c_void_p
@@ -44,7 +44,9 @@ class StepArgs(C.Structure):
                 ("plan_cand_volumes", _p), ("plan_kblocks", _p), ("sel_bits", _p),
                 ("sel_words", _i32), ("o", _p), ("lse", _p),
                 # context-parallel shard (C5); zero on a single device
-                ("l_cpu_total", _i64), ("cpu_offset", _i64), ("sel_in", _p)]
+                ("l_cpu_total", _i64), ("cpu_offset", _i64), ("sel_in", _p),
+                # optional fused append of the previous step's token
+                ("append_k", _p), ("append_v", _p)]
 
 
 class WorkloadSpec(C.Structure):

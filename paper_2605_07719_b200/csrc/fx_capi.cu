@@ -267,9 +267,11 @@ struct Planned {
     bool fused;  // the worklist ran inside k_select
 };
 // wl != nullptr: fuse the worklist into the selection kernel (Planned.fused).
+// ap != nullptr: the plan kernel first appends one decoded row per (b, g).
 Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, StepScratch& s,
-                        bool need_meta_for_select, const fx::WorklistArgs* wl = nullptr) {
-    FX_REQUIRE(a->l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + a->l_new <= L.l_cap,
+                        bool need_meta_for_select, const fx::WorklistArgs* wl = nullptr,
+                        const fx::AppendArgs* ap = nullptr) {
+    FX_REQUIRE(a->l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + a->l_new + (ap ? 1 : 0) <= L.l_cap,
                FX_ERR_INVALID, "bad-shape: decoded rows exceed l_cap");
     FX_REQUIRE(a->plan_mode >= FX_PLAN_PROPS && a->plan_mode <= FX_PLAN_GIVEN, FX_ERR_INVALID,
                "bad-shape: unknown plan mode");
@@ -310,7 +312,8 @@ Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, 
         Timed tm(ctx, FX_KERNEL_PLAN);
         fx::launch_prepare(L, l_plan, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
                            a->kslope, a->streaming, p.blk, p.budgets, a->plan_volume,
-                           a->plan_cand_volumes, p.kblocks, s.bg_done, st);
+                           a->plan_cand_volumes, p.kblocks, s.bg_done, st,
+                           ap ? *ap : fx::AppendArgs());
     }
     p.launches = 1;
     p.fused = false;
@@ -673,17 +676,32 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         const int grid = fx::attend_grid(L, false, ctx->num_sms);
         StepScratch s = carve_step(ctx, L, grid, true);
         const int n_bg = L.batch * L.kv_heads;
-        const fx::WorklistArgs wl{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + a->l_new,
+        FX_REQUIRE((a->append_k == nullptr) == (a->append_v == nullptr), FX_ERR_INVALID,
+                   "bad-shape: append_k and append_v go together");
+        fx::AppendArgs ap;
+        if (a->append_k) {
+            ap.k = const_cast<void*>(a->k);
+            ap.v = const_cast<void*>(a->v);
+            ap.kn = a->append_k;
+            ap.vn = a->append_v;
+            ap.l_cap = L.l_cap;
+            ap.row = L.l_sink + L.l_cpu + L.l_local + a->l_new;
+            ap.D = L.head_dim;
+            ap.bf16 = L.dtype == FX_BF16;
+        }
+        const int64_t l_new = a->l_new + (a->append_k ? 1 : 0);  // rows attended this step
+        const fx::WorklistArgs wl{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + l_new,
                                   nullptr, nullptr, 0, s.boxes, s.box_stride, s.bg_count,
                                   s.bg_start, s.bg_done + n_bg};
         static const bool no_fuse = std::getenv("FX_DEBUG_NO_FUSED_WORKLIST") != nullptr;
-        const Planned pl = plan_and_select(ctx, L, a, s, false, no_fuse ? nullptr : &wl);
+        const Planned pl = plan_and_select(ctx, L, a, s, false, no_fuse ? nullptr : &wl,
+                                           a->append_k ? &ap : nullptr);
         int32_t* blk = pl.blk;
         int n = pl.launches;
         cudaStream_t st = ctx->stream;
         if (!pl.fused) {
             Timed tm(ctx, FX_KERNEL_WORKLIST);
-            fx::launch_worklist(L, a->l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
+            fx::launch_worklist(L, l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
                                 s.bg_count, s.bg_start, s.bg_done, st);
             n += 1;
         }
@@ -982,6 +1000,7 @@ int fx_cp_candidates(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, i
                    "no-context: candidate selection has no payload");
         FX_REQUIRE(L.l_cpu > 0, FX_ERR_INVALID, "empty-context: shard has no cpu rows");
         FX_REQUIRE(a->sel_in == nullptr, FX_ERR_INVALID, "bad-shape: candidates select, sel_in must be null");
+        FX_REQUIRE(a->append_k == nullptr, FX_ERR_INVALID, "bad-shape: append with the attend phase, not candidates");
         FX_REQUIRE(cap >= fx::level_blocks(L.l_cpu, 16), FX_ERR_INVALID,
                    "bad-shape: cap must hold every block of the shard at granularity 16");
         const int grid = fx::attend_grid(L, false, ctx->num_sms);

@@ -93,10 +93,19 @@ void launch_meta_generic(const void* k, int dtype, int64_t rows, int dim, int bl
                          cudaStream_t s);
 
 // fx_plan.cu
+// optional fused append of one decoded row per (b, g) (kv_cache.hpp:68-73)
+struct AppendArgs {
+    void* k = nullptr;
+    void* v = nullptr;
+    const float* kn = nullptr;
+    const float* vn = nullptr;
+    int64_t l_cap = 0, row = 0;
+    int D = 0, bf16 = 0;
+};
 void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed_blk, double fixed_budget,
                     const double* bgt0, const double* kslope, const int32_t* streaming,
                     int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
-                    int32_t* bg_done, cudaStream_t s);
+                    int32_t* bg_done, cudaStream_t s, const AppendArgs& ap = AppendArgs());
 void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, int64_t l_cpu,
                               int32_t* kblocks, cudaStream_t s);
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,

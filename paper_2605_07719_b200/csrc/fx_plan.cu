@@ -38,11 +38,25 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
                           const double* __restrict__ kslope, const int32_t* __restrict__ streaming,
                           int32_t* __restrict__ blk_out, double* __restrict__ budgets,
                           double* __restrict__ volume, double* __restrict__ cand,
-                          int32_t* __restrict__ kblocks, int32_t* __restrict__ bg_done) {
+                          int32_t* __restrict__ kblocks, int32_t* __restrict__ bg_done,
+                          AppendArgs ap) {
     pdl_wait();
     pdl_trigger();
     const int bg = blockIdx.x;
     const int h = threadIdx.x;
+    if (ap.kn) {  // fused append_new of the previous step's token (row ap.row of (b, g))
+        const int64_t o = ((int64_t)bg * ap.l_cap + ap.row) * ap.D;
+        for (int d = h; d < ap.D; d += 32) {
+            const float kx = ap.kn[(int64_t)bg * ap.D + d], vx = ap.vn[(int64_t)bg * ap.D + d];
+            if (ap.bf16) {
+                static_cast<__nv_bfloat16*>(ap.k)[o + d] = __float2bfloat16_rn(kx);
+                static_cast<__nv_bfloat16*>(ap.v)[o + d] = __float2bfloat16_rn(vx);
+            } else {
+                static_cast<float*>(ap.k)[o + d] = kx;
+                static_cast<float*>(ap.v)[o + d] = vx;
+            }
+        }
+    }
     const bool act = h < G;
     const int64_t head = (int64_t)bg * G + h;
     if (h == 0 && bg_done) {
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
 void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed_blk, double fixed_budget,
                     const double* bgt0, const double* kslope, const int32_t* streaming,
                     int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
-                    int32_t* bg_done, cudaStream_t s) {
+                    int32_t* bg_done, cudaStream_t s, const AppendArgs& ap) {
     const int n_bg = L.batch * L.kv_heads;
     FX_REQUIRE(L.group_size >= 1 && L.group_size <= 32, FX_ERR_INVALID,
                "bad-shape: group_size must be in [1, 32]");
@@ -177,7 +191,7 @@ void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed
     }
     launch_pdl(k_prepare, n_bg, 32, 0, s, n_bg, L.group_size, l_plan, plan_mode, fixed_blk, fixed_budget,
                                   bgt0, kslope, streaming, blk, budgets, volume, cand, kblocks,
-                                  bg_done);
+                                  bg_done, ap);
     FX_CUDA(cudaGetLastError());
 }
 

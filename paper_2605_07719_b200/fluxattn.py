@@ -471,7 +471,8 @@ class SparseDecoder:
 
     # -- one decode step ------------------------------------------------------
     def step(self, q, props=None, fixed=None, full=False, blk=None, budgets=None,
-             out: torch.Tensor = None, lse: torch.Tensor = None, sel_in: torch.Tensor = None):
+             out: torch.Tensor = None, lse: torch.Tensor = None, sel_in: torch.Tensor = None,
+             append=None):
         """Plan -> select -> attend+merge for every head of the batch.
 
         q: [B][H][D] f32 (device tensor or host array).  Budget source, one of:
@@ -482,6 +483,9 @@ class SparseDecoder:
           blk = "keep"                        (given plan = the last step's plan)
         sel_in: a given selection [B][H][sel_words] (skips score/select;
         needs a given plan) -- the context-parallel attend phase.
+        append: (k_new, v_new) [B][Hkv][D] f32 device rows appended as decoded row
+        l_new inside the step's first kernel (the previous step's token; saves the
+        separate append launch); the step then attends them.
         Returns (o [B][H][D] f32, lse [B][H]) as device tensors when q is a
         device tensor, else numpy arrays.
         """
@@ -489,7 +493,13 @@ class SparseDecoder:
         qd = torch.as_tensor(np.ascontiguousarray(q, np.float32)).to(self.eng.device) if host else q
         a = self._args(qd, props, fixed, full, blk, budgets)
         a.sel_in = None if sel_in is None else sel_in.data_ptr()
-        return self._finish(a, host, out, lse)
+        if append is not None:
+            self._append = [t.float().contiguous() for t in append]
+            a.append_k, a.append_v = (t.data_ptr() for t in self._append)
+        res = self._finish(a, host, out, lse)
+        if append is not None:
+            self.l_new += 1
+        return res
 
     def _args(self, qd, props, fixed, full, blk, budgets) -> N.StepArgs:
         a = self.args
@@ -502,6 +512,7 @@ class SparseDecoder:
         a.l_cpu_total = self.l_cpu_total
         a.cpu_offset = self.cpu_offset
         a.sel_in = None
+        a.append_k = a.append_v = None
         a.bgt0 = a.kslope = a.streaming = None
         if props is not None:
             a.plan_mode = N.FX_PLAN_PROPS

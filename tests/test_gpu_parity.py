@@ -503,3 +503,27 @@ def test_decode_step_without_cpu_segment(engine, coracle):
                                           np.full(4, 0.05))
         assert rel_err(o[b, g * 4:(g + 1) * 4], wo) < TOL["bf16"]
         assert np.abs(lse[b, g * 4:(g + 1) * 4] - wl).max() < 1e-2
+
+
+def test_decode_step_fused_append_matches_separate(engine, coracle):
+    """step(append=(k, v)) writes the row inside the plan kernel and attends it:
+    identical to fx_append_kv followed by a step (and to the oracle)."""
+    dec1, host, q = make_decoder(engine, 2, 2, 4, 128, 64, 2000, 256, "bf16", seed=12, n_new=2,
+                                 structured=True)
+    dec2, _, _ = make_decoder(engine, 2, 2, 4, 128, 64, 2000, 256, "bf16", seed=12, n_new=2,
+                              structured=True)
+    dec1.l_new = dec2.l_new = 1  # the second decoded row arrives through an append
+    kn = torch.stack([torch.as_tensor(host[(b, g)][0][64 + 2000 + 256 + 1])
+                      for b in range(2) for g in range(2)]).reshape(2, 2, 128).cuda()
+    vn = torch.stack([torch.as_tensor(host[(b, g)][1][64 + 2000 + 256 + 1])
+                      for b in range(2) for g in range(2)]).reshape(2, 2, 128).cuda()
+    qd = torch.as_tensor(q).cuda()
+    dec1.append(kn, vn)
+    o1, l1 = dec1.step(qd, fixed=(32, 0.1))
+    o1, l1 = o1.clone(), l1.clone()
+    o2, l2 = dec2.step(qd, fixed=(32, 0.1), append=(kn, vn))
+    torch.cuda.synchronize()
+    assert dec2.l_new == 2
+    assert torch.equal(dec1.k, dec2.k) and torch.equal(dec1.v, dec2.v)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    _check_step(dec2, host, q, coracle, lambda b, g: 32, lambda b, g: [0.1] * 4, "bf16", n_new=2)
