@@ -215,48 +215,73 @@ __device__ __forceinline__ void chunk_seg(const FeatChunks& c, int ci, int* sg, 
 }
 
 template <typename T>
+__device__ __forceinline__ void unpack8(const T* p, float* f);
+template <>
+__device__ __forceinline__ void unpack8<__nv_bfloat16>(const __nv_bfloat16* p, float* f) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = bf16lo_to_f(w[i]);
+        f[2 * i + 1] = bf16hi_to_f(w[i]);
+    }
+}
+template <>
+__device__ __forceinline__ void unpack8<float>(const float* p, float* f) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+// K and V of the chunk are staged raw (16-byte copies, rows padded by 16 bytes
+// so the score loop's row-parallel 16-byte reads hit distinct banks); q is
+// stored [D][G] in f64 so the G heads of one dimension are adjacent words.
+template <typename T>
 __global__ void __launch_bounds__(kFT) k_feat_chunk(fx_layout L, const void* kp, const void* vp,
                                                     int64_t l_new, const float* q, FeatChunks fc) {
     extern __shared__ __align__(16) unsigned char fsm[];
     const int D = L.head_dim, G = L.group_size, t = threadIdx.x;
-    float* Ks = reinterpret_cast<float*>(fsm);            // [kFC][D + 1]
-    float* Vs = Ks + kFC * (D + 1);                        // [kFC][D]
-    double* qs = reinterpret_cast<double*>(Vs + kFC * D);  // [G][D]
-    double* sc = qs + G * D;                               // [kFC][G] scores, then weights
+    const int pitch = D + 16 / (int)sizeof(T);             // elements per staged row
+    T* Ks = reinterpret_cast<T*>(fsm);                      // [kFC][pitch]
+    T* Vs = Ks + kFC * pitch;                               // [kFC][pitch]
+    double* qs = reinterpret_cast<double*>(Vs + kFC * pitch);  // [D][G]
+    double* sc = qs + G * D;                                // [kFC][G] scores, then weights
     __shared__ double cm[kFMaxG];
     const int ci = blockIdx.x;
     const int64_t bg = blockIdx.y;
     int sg, k;
     chunk_seg(fc, ci, &sg, &k);
-    const int64_t seg_r0[3] = {0, L.l_sink + L.l_cpu, L.l_sink + L.l_cpu + L.l_local};
-    const int64_t seg_n[3] = {L.l_sink, L.l_local, l_new};
+    const int64_t r0 = sg == 0 ? 0 : sg == 1 ? L.l_sink + L.l_cpu : L.l_sink + L.l_cpu + L.l_local;
+    const int64_t sn = sg == 0 ? L.l_sink : sg == 1 ? L.l_local : l_new;
     const int64_t c0 = (int64_t)k * kFC;
-    const int nr = (int)min((int64_t)kFC, seg_n[sg] - c0);
+    const int nr = (int)min((int64_t)kFC, sn - c0);
     const double isd = 1.0 / sqrt((double)D);
-    const T* K = static_cast<const T*>(kp) + bg * L.l_cap * D;
-    const T* V = static_cast<const T*>(vp) + bg * L.l_cap * D;
-    for (int i = t; i < G * D; i += kFT) qs[i] = (double)q[bg * G * D + i];
-    const int v8 = D / 8;  // stage the chunk: 16-byte (bf16) / 32-byte (f32) vectors
-    for (int i = t; i < nr * v8; i += kFT) {
-        const int r = i / v8, d0 = (i % v8) * 8;
-        const int64_t o = (seg_r0[sg] + c0 + r) * D + d0;
-        float kf[8], vf[8];
-        ld8(K + o, kf);
-        ld8(V + o, vf);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            Ks[r * (D + 1) + d0 + u] = kf[u];
-            Vs[r * D + d0 + u] = vf[u];
-        }
+    const T* K = static_cast<const T*>(kp) + (bg * L.l_cap + r0 + c0) * D;
+    const T* V = static_cast<const T*>(vp) + (bg * L.l_cap + r0 + c0) * D;
+    for (int i = t; i < G * D; i += kFT) {
+        const int h = i / D, d = i % D;
+        qs[d * G + h] = (double)q[bg * G * D + i];
+    }
+    const int vpr = D * (int)sizeof(T) / 16;  // 16-byte vectors per row
+    for (int i = t; i < nr * vpr; i += kFT) {
+        const int r = i / vpr, c = i % vpr;
+        const uint4 kx = __ldg(reinterpret_cast<const uint4*>(K + (int64_t)r * D) + c);
+        const uint4 vx = __ldg(reinterpret_cast<const uint4*>(V + (int64_t)r * D) + c);
+        *reinterpret_cast<uint4*>(Ks + r * pitch + c * (16 / (int)sizeof(T))) = kx;
+        *reinterpret_cast<uint4*>(Vs + r * pitch + c * (16 / (int)sizeof(T))) = vx;
     }
     __syncthreads();
     for (int pr = t; pr < nr * G; pr += kFT) {  // one (row, head) score per thread
         const int r = pr / G, h = pr % G;
-        const double* qh = qs + h * D;
-        const float* kr = Ks + r * (D + 1);
+        const T* kr = Ks + r * pitch;
         double a = 0.0;
-#pragma unroll 8
-        for (int d = 0; d < D; ++d) a += qh[d] * (double)kr[d];
+        for (int d0 = 0; d0 < D; d0 += 8) {
+            float f[8];
+            unpack8<T>(kr + d0, f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a += qs[(d0 + u) * G + h] * (double)f[u];
+        }
         sc[r * G + h] = a * isd;
     }
     __syncthreads();
@@ -278,7 +303,7 @@ __global__ void __launch_bounds__(kFT) k_feat_chunk(fx_layout L, const void* kp,
     for (int i = t; i < G * D; i += kFT) {
         const int h = i / D, d = i % D;
         double a = 0.0;
-        for (int r = 0; r < nr; ++r) a += sc[r * G + h] * (double)Vs[r * D + d];
+        for (int r = 0; r < nr; ++r) a += sc[r * G + h] * (double)tofl(Vs[r * pitch + d]);
         fc.o[(slot + h) * D + d] = a;
     }
 }
@@ -291,8 +316,8 @@ __global__ void __launch_bounds__(kFT) k_feat(fx_layout L, int64_t l_new, const 
     const int D = L.head_dim, G = L.group_size, t = threadIdx.x;
     double* qs = reinterpret_cast<double*>(fsm);  // [G][D]
     double* part_o = qs + G * D;                  // [3][G][D] segment outputs (sum e v)
+    double* cw = part_o + 3 * G * D;              // [n chunks][G] exp(m_chunk - m_segment)
     __shared__ double seg_m[3][kFMaxG], seg_z[3][kFMaxG];
-    __shared__ double red[kFT / 32];
     const int64_t bg = blockIdx.x;
     const int RS = kStatsN + 3 * D;
     for (int i = t; i < G * D; i += kFT) qs[i] = (double)q[bg * G * D + i];
@@ -312,18 +337,24 @@ __global__ void __launch_bounds__(kFT) k_feat(fx_layout L, int64_t l_new, const 
         seg_z[sg][h] = z;
     }
     __syncthreads();
+    for (int i = t; i < fc.n * G; i += kFT) {  // chunk weights, once per (chunk, head)
+        const int c = i / G, h = i % G;
+        const int sg = c < fc.n_sink ? 0 : c < fc.n_sink + fc.n_local ? 1 : 2;
+        cw[i] = exp(fc.m[(bg * fc.n + c) * G + h] - seg_m[sg][h]);
+    }
+    __syncthreads();
     for (int i = t; i < 3 * G * D; i += kFT) {
         const int sg = i / (G * D), h = (i / D) % G, d = i % D;
         double a = 0.0;
-        for (int c = 0; c < cnt[sg]; ++c) {
-            const int64_t sl = (bg * fc.n + first[sg] + c) * G + h;
-            a += fc.o[sl * D + d] * exp(fc.m[sl] - seg_m[sg][h]);
-        }
+        for (int c = first[sg]; c < first[sg] + cnt[sg]; ++c)
+            a += fc.o[((bg * fc.n + c) * G + h) * D + d] * cw[c * G + h];
         part_o[i] = a;
     }
     __syncthreads();
-    // per head: segment summaries, merged default norm, record-derived features
-    for (int h = 0; h < G; ++h) {
+    // per head (one warp each, no block barriers): segment summaries, merged
+    // default norm, record-derived features
+    const int lane = t & 31;
+    for (int h = t >> 5; h < G; h += kFT / 32) {
         const int64_t head = bg * G + h;
         const double* r = rec + head * RS;
         const double* mk = r + kStatsN;
@@ -338,7 +369,7 @@ __global__ void __launch_bounds__(kFT) k_feat(fx_layout L, int64_t l_new, const 
             zt += wsg[sg] * seg_z[sg][h];
         }
         double x0 = 0.0, x1 = 0.0, xg = 0.0, qn2 = 0.0, qk = 0.0, qa = 0.0, nmk = 0.0, nmv = 0.0;
-        for (int d = t; d < D; d += kFT) {
+        for (int d = lane; d < D; d += 32) {
             const double o0 = seg_n[0] > 0 ? part_o[h * D + d] / seg_z[0][h] : 0.0;
             const double o1 = seg_n[1] > 0 ? part_o[G * D + h * D + d] / seg_z[1][h] : 0.0;
             double og = 0.0;
@@ -353,15 +384,21 @@ __global__ void __launch_bounds__(kFT) k_feat(fx_layout L, int64_t l_new, const 
             nmk += mk[d] * mk[d];
             nmv += mv[d] * mv[d];
         }
-        on[0] = sqrt(block_sum128(x0, red));
-        on[1] = sqrt(block_sum128(x1, red));
-        const double gn = sqrt(block_sum128(xg, red));
-        qn2 = block_sum128(qn2, red);
-        qk = block_sum128(qk, red);
-        qa = block_sum128(qa, red);
-        nmk = block_sum128(nmk, red);
-        nmv = block_sum128(nmv, red);
-        if (t == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            x0 += __shfl_xor_sync(0xffffffffu, x0, o);
+            x1 += __shfl_xor_sync(0xffffffffu, x1, o);
+            xg += __shfl_xor_sync(0xffffffffu, xg, o);
+            qn2 += __shfl_xor_sync(0xffffffffu, qn2, o);
+            qk += __shfl_xor_sync(0xffffffffu, qk, o);
+            qa += __shfl_xor_sync(0xffffffffu, qa, o);
+            nmk += __shfl_xor_sync(0xffffffffu, nmk, o);
+            nmv += __shfl_xor_sync(0xffffffffu, nmv, o);
+        }
+        on[0] = sqrt(x0);
+        on[1] = sqrt(x1);
+        const double gn = sqrt(xg);
+        if (lane == 0) {
             double* f = feats + head * kFeat;
             const double qn = sqrt(qn2);
             const bool cpu_empty = r[5] != 0.0;
@@ -470,7 +507,8 @@ void launch_decode_features(const fx_layout& L, const void* k, const void* v, in
     fc.o = fc.z + n_bg * fc.n * G;
     const bool bf = L.dtype == FX_BF16;
     if (fc.n > 0) {
-        const size_t smem = (size_t)kFC * (D + 1) * 4 + (size_t)kFC * D * 4 + (size_t)G * D * 8 +
+        const size_t es = L.dtype == FX_BF16 ? 2 : 4;
+        const size_t smem = 2 * (size_t)kFC * ((size_t)D * es + 16) + (size_t)G * D * 8 +
                             (size_t)kFC * G * 8 + 16;
         const dim3 grid((unsigned)fc.n, (unsigned)n_bg);
         if (bf) {
@@ -482,7 +520,7 @@ void launch_decode_features(const fx_layout& L, const void* k, const void* v, in
         }
         FX_CUDA(cudaGetLastError());
     }
-    const size_t smem2 = (size_t)G * D * 8 + (size_t)3 * G * D * 8 + 16;
+    const size_t smem2 = (size_t)G * D * 8 + (size_t)3 * G * D * 8 + (size_t)fc.n * G * 8 + 16;
     FX_CUDA(cudaFuncSetAttribute(k_feat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     k_feat<<<(unsigned)n_bg, kFT, smem2, s>>>(L, l_new, q, rec, fc, feats, gpu_norm);
     FX_CUDA(cudaGetLastError());
