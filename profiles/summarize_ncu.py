@@ -52,8 +52,8 @@ def full_report(path):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     print(f"## ncu --set full: {path}\n")
-    print("| kernel | " + " | ".join(n for _, n in METRICS) + " | top stalls |")
-    print("|---" * (len(METRICS) + 2) + "|")
+    print("| kernel | " + " | ".join(n for _, n in METRICS) + " | LSU sectors/request | top stalls |")
+    print("|---" * (len(METRICS) + 3) + "|")
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
         cells = []
@@ -67,7 +67,14 @@ def full_report(path):
                float(r[i] or 0)) for i, h in enumerate(hdr)
               if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")]
         st = ", ".join(f"{n} {v:.2f}" for n, v in sorted(st, key=lambda x: -x[1])[:3])
-        print(f"| {name} | " + " | ".join(cells) + f" | {st} |")
+        spr = "-"
+        try:
+            sec = float(r[hdr.index("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")].replace(",", ""))
+            req = float(r[hdr.index("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")].replace(",", ""))
+            spr = f"{sec / req:.2f}" if req else "-"
+        except (ValueError, IndexError):
+            pass
+        print(f"| {name} | " + " | ".join(cells) + f" | {spr} | {st} |")
     print()
 
 
