@@ -149,11 +149,11 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
 
 // For n_bg > kMaxRunPrefix: the CTA that completes the last group publishes
 // the exclusive prefix of (box count + kRunPad) over (b, g) into bg_start.
-// All threads of a CTA that has just finished worklist_group(); blockDim <= 256.
+// All threads of a CTA that has just finished worklist_group(); blockDim <= 1024.
 __device__ inline void worklist_publish(const WorklistArgs& w, int n_bg) {
     if (n_bg <= kMaxRunPrefix) return;  // the attention kernels rebuild the run starts from the counts
     __shared__ int s_last;
-    __shared__ int wtot[8];
+    __shared__ int wtot[32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nt = blockDim.x;
     __threadfence();
     __syncthreads();
