@@ -216,6 +216,15 @@ FX_API int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* f
 /* One whole decode step of the batch: plan -> score/select -> sparse GQA
  * attention over defaults + selected blocks with the fused LSE merge. */
 FX_API int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* args);
+/* The step's two halves (SURVEY §8b batched extension):
+ * fx_plan_select -- plan (any plan mode) + approximate scores + bit-exact top-k:
+ *   fills plan_blk / plan_budgets / plan_kblocks and sel_bits (all required),
+ *   no attention (topk_blocks for every head, block_index.cpp:55-83);
+ * fx_sparse_decode -- attention over the defaults and a given selection
+ *   (args->sel_in, plan mode FX_PLAN_GIVEN) with the fused LSE merge
+ *   (sparse_attention + merge_into, block_index.cpp:85-94, attention.cpp:89-104). */
+FX_API int fx_plan_select(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* args);
+FX_API int fx_sparse_decode(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* args);
 /* gathered_attention_unchecked for one query over rows idx[0..n) (ascending)
  * of k/v [dev] [rows][dim]; o [dev] [dim] f32, lse [dev] f32 (-inf if n == 0). */
 FX_API int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void* v,

@@ -128,6 +128,8 @@ _SIGS = {
     "fx_model_destroy": (C.c_int, [_p]),
     "fx_predict": (C.c_int, [_p, _p, _i32, _p, _p, _p, _p, _p]),
     "fx_decode_step": (C.c_int, [_p, C.POINTER(Layout), C.POINTER(StepArgs)]),
+    "fx_plan_select": (C.c_int, [_p, C.POINTER(Layout), C.POINTER(StepArgs)]),
+    "fx_sparse_decode": (C.c_int, [_p, C.POINTER(Layout), C.POINTER(StepArgs)]),
     "fx_gathered_attention": (C.c_int, [_p, _p, _p, _p, _i32, _i64, _i32, _p, _i64, _p, _p]),
     "fx_merge_partials": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p]),
     "fx_append_kv": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p]),

@@ -165,6 +165,27 @@ TaskResult execute_task(const SparseTask& task) {
     return r;
 }
 
+std::vector<TaskResult> execute_batch(std::span<const SparseTask> tasks) {
+    std::vector<TaskResult> res(tasks.size());
+    std::vector<bool> done(tasks.size(), false);
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        if (done[i]) continue;
+        if (!tasks[i].cache || !tasks[i].metadata)
+            throw std::runtime_error("no-context: task has no executable payload");
+        const Shape s = shape_of(tasks[i]);
+        std::vector<const SparseTask*> batch;
+        std::vector<TaskResult*> out;
+        for (std::size_t j = i; j < tasks.size(); ++j) {
+            if (done[j] || !tasks[j].cache || !tasks[j].metadata || !(shape_of(tasks[j]) == s)) continue;
+            batch.push_back(&tasks[j]);
+            out.push_back(&res[j]);
+            done[j] = true;
+        }
+        execute_batch(batch, out);
+    }
+    return res;
+}
+
 ScheduleReport run(TaskQueue& queue, const WorkerProfile& workers, RunMode mode,
                    std::vector<TaskResult>* results) {
     if (mode == RunMode::Simulated)

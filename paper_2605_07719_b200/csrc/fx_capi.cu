@@ -729,6 +729,30 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
     });
 }
 
+int fx_plan_select(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(a != nullptr && a->q && a->sel_bits && a->plan_blk && a->plan_budgets &&
+                       a->plan_kblocks, FX_ERR_STATE,
+                   "no-context: plan_select needs q, sel_bits and the plan outputs");
+        FX_REQUIRE(a->sel_in == nullptr && a->append_k == nullptr, FX_ERR_INVALID,
+                   "bad-shape: plan_select takes no given selection or append");
+        const fx_layout& L = *lay;
+        StepScratch s = carve_step(ctx, L, fx::attend_grid(L, false, ctx->num_sms), true);
+        const Planned pl = plan_and_select(ctx, L, a, s, false, nullptr);
+        ctx->launches += pl.launches;
+    });
+}
+
+int fx_sparse_decode(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
+    const int rc = guarded([&] {
+        FX_REQUIRE(a != nullptr && a->sel_in != nullptr && a->plan_mode == FX_PLAN_GIVEN,
+                   FX_ERR_STATE, "no-context: sparse_decode needs a given plan and selection");
+    });
+    return rc != FX_OK ? rc : fx_decode_step(ctx, lay, a);
+}
+
 int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void* v,
                           int32_t dtype, int64_t rows, int32_t dim, const uint32_t* idx,
                           int64_t n, float* o, float* lse) {

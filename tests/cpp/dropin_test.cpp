@@ -158,6 +158,12 @@ int main(int argc, char** argv) {
     std::vector<TaskResult> results;
     ScheduleReport rep = run(queue, WorkerProfile::standard(D), RunMode::Executed, &results);
     EXPECT(!rep.aborted && results.size() == 4);
+    // the batched extension returns the same outputs, in task order
+    const std::vector<TaskResult> batched = execute_batch(std::span<const SparseTask>(queue.tasks()));
+    EXPECT(batched.size() == results.size());
+    for (std::size_t i = 0; i < batched.size(); ++i)
+        for (std::size_t h = 0; h < batched[i].head_outputs.size(); ++h)
+            EXPECT(batched[i].head_outputs[h] == results[i].head_outputs[h]);
     for (std::size_t i = 0; i < results.size(); ++i) {
         const SparseTask& t = queue.tasks()[i];
         EXPECT(results[i].group_id == t.group_id);

@@ -527,3 +527,35 @@ def test_decode_step_fused_append_matches_separate(engine, coracle):
     assert torch.equal(dec1.k, dec2.k) and torch.equal(dec1.v, dec2.v)
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
     _check_step(dec2, host, q, coracle, lambda b, g: 32, lambda b, g: [0.1] * 4, "bf16", n_new=2)
+
+
+def test_plan_select_then_sparse_decode_equals_step(engine, coracle):
+    """fx_plan_select + fx_sparse_decode (the step's two halves)
+    reproduce fx_decode_step bit-for-bit."""
+    import ctypes as C
+    from paper_2605_07719_b200 import _native as N
+    dec, host, q = make_decoder(engine, 2, 2, 4, 128, 64, 3000, 256, "bf16", seed=21,
+                                structured=True)
+    qd = torch.as_tensor(q).cuda()
+    rng = np.random.default_rng(4)
+    props = tuple(torch.as_tensor(x, device="cuda") for x in
+                  (rng.uniform(0.02, 0.1, (2, 8)), rng.uniform(0.0, 0.01, (2, 8)),
+                   np.zeros((2, 8), np.int32)))
+    o_ref, l_ref = dec.step(qd, props=props)
+    o_ref, l_ref, sel_ref = o_ref.clone(), l_ref.clone(), dec.sel_bits.clone()
+    a = dec._args(qd, props, None, False, None, None)
+    dec.sel_bits.zero_()
+    N.check(N.LIB.fx_plan_select(engine.ctx, C.byref(dec.lay), C.byref(a)))
+    assert torch.equal(dec.sel_bits, sel_ref)
+    sel = dec.sel_bits.clone()
+    a = dec._args(qd, None, None, False, "keep", None)
+    a.sel_in = sel.data_ptr()
+    o = torch.empty_like(o_ref)
+    lse = torch.empty_like(l_ref)
+    a.o, a.lse = o.data_ptr(), lse.data_ptr()
+    N.check(N.LIB.fx_sparse_decode(engine.ctx, C.byref(dec.lay), C.byref(a)))
+    torch.cuda.synchronize()
+    assert torch.equal(o, o_ref) and torch.equal(lse, l_ref)
+    a.sel_in = None
+    with pytest.raises(RuntimeError, match="^no-context"):
+        N.check(N.LIB.fx_sparse_decode(engine.ctx, C.byref(dec.lay), C.byref(a)))
