@@ -458,24 +458,51 @@ __global__ void __launch_bounds__(128) k_lab_scan(const LabelView p) {
         if (t < nb) cid[t] = order[c0 + t];
         if (t == 0) s_first = kChunk;
         __syncthreads();
-        for (int j = 0; j < nb; ++j) {
-            const int64_t b0 = (int64_t)cid[j] * blk;
-            const int64_t r0 = p.l_sink + b0;
-            const int64_t r1 = p.l_sink + min(p.l_cpu, b0 + blk);
-            double zj = 0.0, uj = 0.0;
-#pragma unroll 4
-            for (int64_t r = r0; r < r1; ++r) {
-                const double e = E[r];
-                zj += e;
-                uj += e * (double)tofl(V[r * D]);
+        if (blk == 1) {
+            // one row per block: all 32 rows' weights and values are loaded
+            // first (one round trip for the chunk), then the prefix chain runs
+            // on registers
+            double ev[kChunk];
+            float vv[kChunk];
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                const int64_t r = p.l_sink + (int64_t)cid[j < nb ? j : 0];
+                ev[j] = E[r];
+                vv[j] = tofl(V[r * D]);
             }
-            R += uj - zj * of;
-            Z += zj;
-            tokens += r1 - r0;
-            sq[j][t] = t < D ? R * R : 0.0;
-            if (t == 0) {
-                zz[j] = Z;
-                tk[j] = tokens;
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                if (j < nb) {
+                    R += ev[j] * (double)vv[j] - ev[j] * of;
+                    Z += ev[j];
+                    tokens += 1;
+                    sq[j][t] = t < D ? R * R : 0.0;
+                    if (t == 0) {
+                        zz[j] = Z;
+                        tk[j] = tokens;
+                    }
+                }
+            }
+        } else {
+            for (int j = 0; j < nb; ++j) {
+                const int64_t b0 = (int64_t)cid[j] * blk;
+                const int64_t r0 = p.l_sink + b0;
+                const int64_t r1 = p.l_sink + min(p.l_cpu, b0 + blk);
+                double zj = 0.0, uj = 0.0;
+#pragma unroll 8
+                for (int64_t r = r0; r < r1; ++r) {
+                    const double e = E[r];
+                    zj += e;
+                    uj += e * (double)tofl(V[r * D]);
+                }
+                R += uj - zj * of;
+                Z += zj;
+                tokens += r1 - r0;
+                sq[j][t] = t < D ? R * R : 0.0;
+                if (t == 0) {
+                    zz[j] = Z;
+                    tk[j] = tokens;
+                }
             }
         }
         __syncthreads();
