@@ -54,6 +54,9 @@ def args_parse():
     ap.add_argument("--data", default="reference", choices=["reference", "normal"],
                     help="reference: the reference generator's workload (generate(spec), on "
                          "device); normal: plain N(0,1) K/V")
+    ap.add_argument("--cp-exchange", default="peer", choices=["peer", "collective"],
+                    help="c5 exchanges: peer-memory one-shot kernels, or torch.distributed "
+                         "all-gathers (NCCL)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
                     help="c2: one layer, batch 16 (the metric's config); c4: 32 layers x batch 8 "
                          "per GPU (configs[3], one 8-GPU shard), the layers' independent tasks "
@@ -294,13 +297,16 @@ def run_c5(a):
         full.build_metadata()
         dec, shards, comm = full, None, None
     else:
+        from paper_2605_07719_b200.context_parallel import PeerShard, PeerTables, cp_decode_step_peer
         kr = shard_kv(full.k, L_SINK, l_cpu, L_LOCAL, rank, world, total)
         vr = shard_kv(full.v, L_SINK, l_cpu, L_LOCAL, rank, world, total)
         del full
         torch.cuda.empty_cache()
-        sh = CPShard(eng, rank, world, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, total, "bf16", k=kr, v=vr)
+        cls = PeerShard if a.cp_exchange == "peer" else CPShard
+        sh = cls(eng, rank, world, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, total, "bf16", k=kr, v=vr)
         sh.dec.build_metadata()
-        dec, shards, comm = sh.dec, [sh], TorchComm()
+        dec, shards = sh.dec, [sh]
+        comm = PeerTables.over_dist(eng, sh) if a.cp_exchange == "peer" else TorchComm()
     step_i = [0]
 
     def one_step():
@@ -309,7 +315,10 @@ def run_c5(a):
             dec.step(qs[i], props=props)
             dec.append(nk[i], nv[i])
         else:
-            cp_decode_step(shards, comm, qs[i], props=props)
+            if a.cp_exchange == "peer":
+                cp_decode_step_peer(shards, comm, qs[i], i + 1, props=props)
+            else:
+                cp_decode_step(shards, comm, qs[i], props=props)
             if shards[0].is_last:
                 dec.append(nk[i], nv[i])
         step_i[0] += 1
@@ -347,8 +356,11 @@ def run_c5(a):
                                    "plan_group over the whole sequence",
                        "context": ctx, "global_batch": B, "seq_len": ctx,
                        "parallelism": "single device" if world == 1 else
-                       f"context-parallel x{world} (NCCL all-gathers: k-th keys, candidates, "
-                       f"(o, lse))"}}), flush=True)
+                       (f"context-parallel x{world}, one-shot exchanges over peer memory (CUDA IPC "
+                        f"tables, flag waits in the select / combine kernels)"
+                        if a.cp_exchange == "peer" else
+                        f"context-parallel x{world} (all-gathers of k-th keys, candidates, "
+                        f"(o, lse))")}}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -376,6 +376,40 @@ FX_API int fx_cp_select(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_
 FX_API int fx_cp_combine(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim, const float* o_parts,
                          const float* lse_parts, float* o, float* lse);
 
+/* ---- context-parallel exchanges over peer memory (no NCCL) ---------------
+ * One-shot alternative to steps 2, 3 and 5 above: every rank's buffers are
+ * mapped into every rank (CUDA IPC over NVLink; plain device pointers when the
+ * shards share a process) and the kernels read the peers' candidate lists and
+ * (o, lse) partials directly, after waiting on each peer's ready flag -- no
+ * all-gather, no host round trip for the exchange size.  Pointers [dev]. */
+#define FX_CP_MAX_RANKS 16
+typedef struct fx_cp_peer {
+    const uint64_t* keys;   /* [n][cap] sorted candidate keys (fx_cp_candidates) */
+    const uint32_t* ids;    /* [n][cap] global block ids */
+    const uint64_t* kth;    /* [n] local k-th key */
+    const float* o;         /* [n][dim] attention partial of the shard */
+    const float* lse;       /* [n] */
+    const uint64_t* flags;  /* [2]: candidates ready, partials ready (step stamps) */
+    int64_t cap;
+} fx_cp_peer;
+/* flags[slot] = stamp after every prior op of the stream is visible system-wide. */
+FX_API int fx_cp_signal(fx_ctx* ctx, uint64_t* flags, int32_t slot, uint64_t stamp);
+/* Waits for peers[r].flags[0] >= stamp, then threshold + global rank in one
+ * kernel (fx_cp_threshold + fx_cp_select over the peers' lists in place). */
+FX_API int fx_cp_select_peer(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t self,
+                             const fx_cp_peer* peers, uint64_t stamp, const int32_t* kblocks,
+                             const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out,
+                             int32_t sel_words);
+/* Waits for peers[r].flags[1] >= stamp, then merge_into over the peers' (o, lse). */
+FX_API int fx_cp_combine_peer(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim,
+                              const fx_cp_peer* peers, uint64_t stamp, float* o, float* lse);
+/* CUDA IPC for the peer tables: export the allocation holding dptr (64-byte
+ * handle + dptr's offset in it), map a peer's handle into this context's
+ * device (add the offset), unmap. */
+FX_API int fx_ipc_handle(const void* dptr, unsigned char handle[64], int64_t* offset);
+FX_API int fx_ipc_open(fx_ctx* ctx, const unsigned char handle[64], void** dptr);
+FX_API int fx_ipc_close(fx_ctx* ctx, void* dptr);
+
 #ifdef __cplusplus
 }
 #endif

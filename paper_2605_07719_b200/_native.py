@@ -87,6 +87,13 @@ class TraceInfo(C.Structure):
                 ("decode_steps", _i32)]
 
 
+class CpPeer(C.Structure):
+    """fx_cp_peer: one rank's exchange tables as seen from this device."""
+
+    _fields_ = [("keys", _p), ("ids", _p), ("kth", _p), ("o", _p), ("lse", _p), ("flags", _p),
+                ("cap", _i64)]
+
+
 class NativeError(RuntimeError):
     """A non-zero fx_* status; the message carries the reference error code."""
 
@@ -149,6 +156,13 @@ _SIGS = {
                                 _p, _p, _p]),
     "fx_trace_save": (C.c_int, [_p, C.c_char_p, C.POINTER(TraceInfo), C.POINTER(Layout), _p, _p,
                                 _p, _p, _p, _p, _p, _p, _p, _p]),
+    "fx_cp_signal": (C.c_int, [_p, _p, _i32, C.c_uint64]),
+    "fx_cp_select_peer": (C.c_int, [_p, C.POINTER(Layout), _i32, _i32, _p, C.c_uint64, _p, _p, _i64,
+                                    _p, _i32]),
+    "fx_cp_combine_peer": (C.c_int, [_p, _i32, _i64, _i32, _p, C.c_uint64, _p, _p]),
+    "fx_ipc_handle": (C.c_int, [_p, C.c_char_p, C.POINTER(_i64)]),
+    "fx_ipc_open": (C.c_int, [_p, C.c_char_p, C.POINTER(_p)]),
+    "fx_ipc_close": (C.c_int, [_p, _p]),
     "fx_label_heads": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, C.POINTER(_p * 4), _p,
                                  C.c_double, _i32, _p, _p, _p, _p, _p, _p, _p]),
 }

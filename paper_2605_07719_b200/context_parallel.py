@@ -227,3 +227,142 @@ def cp_decode_step(shards: Sequence, comm, q: torch.Tensor, out: Sequence[Tuple[
         s.combine(o_all, lse_all, o, lse)
         res.append((o, lse))
     return res
+
+
+# ---------------------------------------------------------------------------
+# one-shot exchanges over peer memory (no NCCL): fx_cp_select_peer /
+# fx_cp_combine_peer read the other ranks' candidate lists and (o, lse)
+# partials where they live, after each rank's ready flag
+# ---------------------------------------------------------------------------
+class PeerShard(CPShard):
+    """A CPShard whose exchange tables (candidates, k-th keys, partials, ready
+    flags) are double-buffered by step parity and exported to the peers.  Two
+    sets suffice: a rank's step s+1 select waits for every peer's step s+1
+    candidates, which each peer publishes only after its step s combine has
+    read this rank's set s."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        dev = self.eng.device
+        nh, D = self.n_heads, self.dec.lay.head_dim
+        B, H = self.dec.lay.batch, self.dec.heads
+        self.sets = []
+        for _ in range(2):
+            self.sets.append(dict(
+                keys=torch.zeros((nh, self.cap), dtype=torch.int64, device=dev),
+                ids=torch.zeros((nh, self.cap), dtype=torch.int32, device=dev),
+                count=torch.zeros(nh, dtype=torch.int32, device=dev),
+                kth=torch.zeros(nh, dtype=torch.int64, device=dev),
+                o=torch.zeros((B, H, D), dtype=torch.float32, device=dev),
+                lse=torch.zeros((B, H), dtype=torch.float32, device=dev)))
+        self.flags = torch.zeros((2, 2), dtype=torch.int64, device=dev)  # [parity][slot]
+
+    def table(self, parity: int) -> "N.CpPeer":
+        st = self.sets[parity]
+        return N.CpPeer(st["keys"].data_ptr(), st["ids"].data_ptr(), st["kth"].data_ptr(),
+                        st["o"].data_ptr(), st["lse"].data_ptr(), self.flags[parity].data_ptr(),
+                        self.cap)
+
+    def exported(self):
+        """(name, handle bytes, offset) of every exchange buffer, for the peers."""
+        out = []
+        bufs = [(f"{n}{p}", self.sets[p][n]) for p in range(2)
+                for n in ("keys", "ids", "kth", "o", "lse")] + [("flags", self.flags)]
+        for name, t in bufs:
+            h = C.create_string_buffer(64)
+            off = C.c_int64(0)
+            check(LIB.fx_ipc_handle(C.c_void_p(t.data_ptr()), h, C.byref(off)))
+            out.append((name, h.raw, off.value))
+        return out
+
+    def candidates_into(self, q, parity, **plan):
+        st = self.sets[parity]
+        d = self.dec
+        a = d._args(q, plan.get("props"), plan.get("fixed"), plan.get("full", False),
+                    plan.get("blk"), plan.get("budgets"))
+        check(LIB.fx_cp_candidates(self.eng.ctx, C.byref(d.lay), C.byref(a), self.cap,
+                                   st["keys"].data_ptr(), st["ids"].data_ptr(),
+                                   st["count"].data_ptr(), st["kth"].data_ptr()))
+
+
+class PeerTables:
+    """The R ranks' exchange tables as device pointers of this process: local
+    shards directly, remote ranks through CUDA IPC (opened once)."""
+
+    def __init__(self, engine: Engine, ranks: int):
+        self.eng = engine
+        self.ranks = ranks
+        self.tabs = [[None] * ranks for _ in range(2)]  # [parity][rank] -> CpPeer
+        self._opened = []
+
+    def add_local(self, shard: PeerShard) -> None:
+        for p in range(2):
+            self.tabs[p][shard.rank] = shard.table(p)
+
+    def add_remote(self, rank: int, cap: int, exported) -> None:
+        ptr = {}
+        for name, handle, off in exported:
+            d = C.c_void_p()
+            check(LIB.fx_ipc_open(self.eng.ctx, handle, C.byref(d)))
+            self._opened.append(d)
+            ptr[name] = d.value + off
+        for p in range(2):
+            self.tabs[p][rank] = N.CpPeer(ptr[f"keys{p}"], ptr[f"ids{p}"], ptr[f"kth{p}"],
+                                          ptr[f"o{p}"], ptr[f"lse{p}"], ptr["flags"] + p * 16, cap)
+
+    def array(self, parity: int):
+        arr = (N.CpPeer * self.ranks)(*self.tabs[parity])
+        return arr
+
+    def close(self) -> None:
+        for d in self._opened:
+            LIB.fx_ipc_close(self.eng.ctx, d)
+        self._opened = []
+
+    @classmethod
+    def over_dist(cls, engine: Engine, shard: PeerShard, group=None) -> "PeerTables":
+        """Exchange IPC handles of every rank's tables over torch.distributed."""
+        import torch.distributed as dist
+        R = dist.get_world_size(group)
+        mine = (shard.rank, shard.cap, shard.exported())
+        allx = [None] * R
+        dist.all_gather_object(allx, mine, group=group)
+        t = cls(engine, R)
+        t.add_local(shard)
+        for rank, cap, exported in allx:
+            if rank != shard.rank:
+                t.add_remote(rank, cap, exported)
+        return t
+
+
+def cp_decode_step_peer(shards: Sequence[PeerShard], tables: PeerTables, q: torch.Tensor,
+                        stamp: int, out: Sequence[Tuple[torch.Tensor, torch.Tensor]] = None, **plan):
+    """One context-parallel decode step with the one-shot peer exchanges.
+    `stamp` increases by one per step (>= 1); this process's shards run in
+    order on one stream (all shards in one process, or one per rank)."""
+    par = stamp % 2
+    peers = tables.array(par)
+    for s in shards:
+        s.candidates_into(q, par, **plan)
+        check(LIB.fx_cp_signal(s.eng.ctx, C.c_void_p(s.flags[par].data_ptr()), 0, stamp))
+    for s in shards:
+        d = s.dec
+        check(LIB.fx_cp_select_peer(s.eng.ctx, C.byref(d.lay), tables.ranks, s.rank, peers, stamp,
+                                    d.plan_kblocks.data_ptr(), d.plan_blk.data_ptr(), s.offset,
+                                    s.sel.data_ptr(), d.sel_words))
+    for s in shards:
+        st = s.sets[par]
+        s.dec.step(q, blk="keep", out=st["o"], lse=st["lse"], sel_in=s.sel)
+        check(LIB.fx_cp_signal(s.eng.ctx, C.c_void_p(s.flags[par].data_ptr()), 1, stamp))
+    res = []
+    for i, s in enumerate(shards):
+        if out is not None:
+            o, lse = out[i]
+        else:
+            o, lse = torch.empty_like(s.o), torch.empty_like(s.lse)
+        D = o.shape[-1]
+        check(LIB.fx_cp_combine_peer(s.eng.ctx, tables.ranks, s.n_heads, D, peers, stamp,
+                                     o.data_ptr(), lse.data_ptr()))
+        res.append((o, lse))
+    return res
+

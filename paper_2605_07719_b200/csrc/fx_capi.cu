@@ -8,6 +8,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cuda.h>
+
 #include "fx_internal.h"
 #include "fx_worklist.cuh"
 
@@ -1062,6 +1064,84 @@ int fx_cp_select(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t self,
         fx::launch_cp_select(*lay, ranks, self, m, gkeys, gids, thresh, kblocks, blk, cpu_offset,
                              sel_out, sel_words, ctx->stream);
         ctx->launches += 1;
+    });
+}
+
+int fx_cp_signal(fx_ctx* ctx, uint64_t* flags, int32_t slot, uint64_t stamp) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(flags && (slot == 0 || slot == 1), FX_ERR_INVALID, "bad-shape: flag slot");
+        fx::launch_cp_signal(flags, slot, stamp, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_cp_select_peer(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t self,
+                      const fx_cp_peer* peers, uint64_t stamp, const int32_t* kblocks,
+                      const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out, int32_t sel_words) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(peers && kblocks && blk && sel_out, FX_ERR_STATE, "no-context: peer select has no payload");
+        FX_REQUIRE(cpu_offset >= 0 && cpu_offset % 128 == 0, FX_ERR_INVALID,
+                   "bad-shape: cpu_offset must be a multiple of 128");
+        FX_REQUIRE(sel_words >= fx::cdiv(std::max<int64_t>(1, fx::level_blocks(lay->l_cpu, 16)), 32),
+                   FX_ERR_INVALID, "bad-shape: sel_words too small");
+        fx::launch_cp_select_peer(*lay, ranks, self, peers, stamp, kblocks, blk, cpu_offset, sel_out,
+                                  sel_words, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_cp_combine_peer(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim, const fx_cp_peer* peers,
+                       uint64_t stamp, float* o, float* lse) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_REQUIRE(peers && o && n >= 0 && dim > 0, FX_ERR_INVALID, "bad-shape: peer combine input");
+        fx::launch_cp_combine_peer(ranks, n, dim, peers, stamp, o, lse, ctx->stream);
+        ctx->launches += n > 0 ? 1 : 0;
+    });
+}
+
+int fx_ipc_handle(const void* dptr, unsigned char handle[64], int64_t* offset) {
+    return guarded([&] {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        // the handle names the whole allocation: export its base and the offset
+        // of dptr inside it (caching allocators hand out sub-ranges)
+        typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static RangeFn range = nullptr;
+        if (!range) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            FX_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+            FX_REQUIRE(fn && q == cudaDriverEntryPointSuccess, FX_ERR_CUDA,
+                       "cuda-error: cuMemGetAddressRange unavailable");
+            range = reinterpret_cast<RangeFn>(fn);
+        }
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        FX_REQUIRE(range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) == CUDA_SUCCESS, FX_ERR_CUDA,
+                   "cuda-error: not a device allocation");
+        cudaIpcMemHandle_t h;
+        FX_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+        std::memcpy(handle, &h, 64);
+        if (offset) *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dptr) - base);
+    });
+}
+
+int fx_ipc_open(fx_ctx* ctx, const unsigned char handle[64], void** dptr) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, 64);
+        FX_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int fx_ipc_close(fx_ctx* ctx, void* dptr) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_CUDA(cudaIpcCloseMemHandle(dptr));
     });
 }
 

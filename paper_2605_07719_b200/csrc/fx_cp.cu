@@ -206,7 +206,141 @@ __global__ void k_cp_combine(int R, int64_t n, int D, const float* __restrict__ 
     if (threadIdx.x == 0 && lse) lse[i] = den > 0.f ? M + logf(den) : -INFINITY;
 }
 
+// ---------------------------------------------------------------------------
+// exchanges over peer memory
+// ---------------------------------------------------------------------------
+struct PeerSet {
+    fx_cp_peer p[FX_CP_MAX_RANKS];
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* a) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+// thread 0 waits until every rank's flag[slot] reached `stamp`; the acquire
+// loads make the peers' preceding writes visible to the whole CTA after the
+// barrier
+__device__ void wait_peers(const PeerSet& ps, int R, int slot, uint64_t stamp) {
+    if (threadIdx.x == 0)
+        for (int r = 0; r < R; ++r)
+            while (ld_acquire_sys(ps.p[r].flags + slot) < stamp) __nanosleep(64);
+    __syncthreads();
+}
+
+__global__ void k_cp_signal(uint64_t* flags, int slot, uint64_t stamp) {
+    __threadfence_system();  // everything this stream wrote before is visible first
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags + slot), "l"(stamp) : "memory");
+}
+
+// threshold (max over ranks of the local k-th key) + global rank of each own
+// entry by binary search in every peer's sorted list -- the fx_cp_threshold /
+// fx_cp_select pair reading the peers' lists where they are
+__global__ void __launch_bounds__(kT) k_cp_select_peer(
+    const __grid_constant__ PeerSet ps, int R, int self, int64_t n, uint64_t stamp,
+    const int32_t* __restrict__ kblocks, const int32_t* __restrict__ blk_arr, int G,
+    int64_t cpu_offset, uint32_t* __restrict__ sel_out, int sel_words) {
+    pdl_wait();
+    pdl_trigger();
+    wait_peers(ps, R, 0, stamp);
+    const int64_t head = blockIdx.x;
+    const int t = threadIdx.x;
+    uint32_t* bits = sel_out + head * sel_words;
+    for (int w = t; w < sel_words; w += kT) bits[w] = 0u;
+    __syncthreads();
+    const int blk = blk_arr[head / G];
+    const int64_t k = kblocks[head];
+    if (blk <= 0 || k <= 0) return;
+    uint64_t T = 0;
+    for (int r = 0; r < R; ++r) {
+        const uint64_t v = ps.p[r].kth[head];
+        T = v > T ? v : T;
+    }
+    const uint64_t lim = T > 0 ? T : 1ull;
+    const int64_t off_blk = cpu_offset / blk;
+    const fx_cp_peer& me = ps.p[self];
+    const uint64_t* own_k = me.keys + head * me.cap;
+    const uint32_t* own_i = me.ids + head * me.cap;
+    for (int64_t j = t; j < me.cap; j += kT) {
+        const uint64_t ke = own_k[j];
+        if (ke < lim) break;  // sorted descending: the rest is below the bound
+        const uint32_t ie = own_i[j];
+        int64_t rank = j;
+        for (int r = 0; r < R && rank < k; ++r) {
+            if (r == self) continue;
+            const uint64_t* kr = ps.p[r].keys + head * ps.p[r].cap;
+            const uint32_t* ir = ps.p[r].ids + head * ps.p[r].cap;
+            int64_t lo = 0, hi = ps.p[r].cap;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (kr[mid] >= lim && first_of(kr[mid], ir[mid], ke, ie)) lo = mid + 1;
+                else hi = mid;
+            }
+            rank += lo;
+        }
+        if (rank < k) {
+            const int64_t local = (int64_t)ie - off_blk;
+            atomicOr(&bits[local >> 5], 1u << (local & 31));
+        }
+    }
+}
+
+// merge_into over the ranks' (o, lse) partials, read from their memory
+__global__ void k_cp_combine_peer(const __grid_constant__ PeerSet ps, int R, int64_t n, int D,
+                                  uint64_t stamp, float* __restrict__ o, float* __restrict__ lse) {
+    pdl_wait();
+    pdl_trigger();
+    wait_peers(ps, R, 1, stamp);
+    const int64_t i = blockIdx.x;
+    float M = -INFINITY;
+    for (int r = 0; r < R; ++r) M = fmaxf(M, ps.p[r].lse[i]);
+    float den = 0.f;
+    for (int r = 0; r < R; ++r) {
+        const float l = ps.p[r].lse[i];
+        den += (l == -INFINITY) ? 0.f : expf(l - M);
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        float num = 0.f;
+        for (int r = 0; r < R; ++r) {
+            const float l = ps.p[r].lse[i];
+            if (l != -INFINITY) num += expf(l - M) * ps.p[r].o[i * D + d];
+        }
+        o[i * D + d] = den > 0.f ? num / den : 0.f;
+    }
+    if (threadIdx.x == 0 && lse) lse[i] = den > 0.f ? M + logf(den) : -INFINITY;
+}
+
 }  // namespace
+
+void launch_cp_signal(uint64_t* flags, int slot, uint64_t stamp, cudaStream_t s) {
+    k_cp_signal<<<1, 1, 0, s>>>(flags, slot, stamp);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_cp_select_peer(const fx_layout& L, int R, int self, const fx_cp_peer* peers, uint64_t stamp,
+                           const int32_t* kblocks, const int32_t* blk, int64_t cpu_offset,
+                           uint32_t* sel_out, int sel_words, cudaStream_t s) {
+    FX_REQUIRE(R >= 1 && R <= FX_CP_MAX_RANKS && self >= 0 && self < R, FX_ERR_INVALID,
+               "bad-shape: rank / rank count");
+    PeerSet ps{};
+    for (int r = 0; r < R; ++r) ps.p[r] = peers[r];
+    const int64_t n = (int64_t)L.batch * L.kv_heads * L.group_size;
+    if (n <= 0) return;
+    launch_pdl(k_cp_select_peer, (unsigned)n, kT, 0, s, ps, R, self, n, stamp, kblocks, blk,
+               L.group_size, cpu_offset, sel_out, sel_words);
+    FX_CUDA(cudaGetLastError());
+}
+
+void launch_cp_combine_peer(int R, int64_t n, int dim, const fx_cp_peer* peers, uint64_t stamp, float* o,
+                            float* lse, cudaStream_t s) {
+    FX_REQUIRE(R >= 1 && R <= FX_CP_MAX_RANKS, FX_ERR_INVALID, "bad-shape: rank count");
+    PeerSet ps{};
+    for (int r = 0; r < R; ++r) ps.p[r] = peers[r];
+    if (n <= 0) return;
+    launch_pdl(k_cp_combine_peer, (unsigned)n, 128, 0, s, ps, R, n, dim, stamp, o, lse);
+    FX_CUDA(cudaGetLastError());
+}
 
 int cp_sort_n(int64_t nblk16) {
     int64_t s = 1;

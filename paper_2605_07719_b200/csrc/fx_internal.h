@@ -184,6 +184,14 @@ void trace_save(const char* path, const fx_trace_info& h, const fx_layout& L, co
                 const int32_t* needle_count, const uint32_t* needles, cudaStream_t s);
 void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream_t s);
 
+// fx_cp.cu: peer-memory exchanges
+void launch_cp_signal(uint64_t* flags, int slot, uint64_t stamp, cudaStream_t s);
+void launch_cp_select_peer(const fx_layout& L, int R, int self, const fx_cp_peer* peers, uint64_t stamp,
+                           const int32_t* kblocks, const int32_t* blk, int64_t cpu_offset,
+                           uint32_t* sel_out, int sel_words, cudaStream_t s);
+void launch_cp_combine_peer(int R, int64_t n, int dim, const fx_cp_peer* peers, uint64_t stamp, float* o,
+                            float* lse, cudaStream_t s);
+
 // fx_attend.cu
 // 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},
 // box {64, box_rows, D/64}, 128-byte swizzle (D multiple of 64).

@@ -129,3 +129,64 @@ def test_cp_ties_bitexact(engine):
         want = full.selected_blocks(0, h)
         got = np.sort(np.concatenate([sh.global_selection(0, h) for sh in shards]))
         assert np.array_equal(got, want)
+
+
+def _peer_shards(engine, R, B, Hkv, G, D, l_sink, l_cpu, l_local, seed, n_new=0):
+    from paper_2605_07719_b200.context_parallel import PeerShard, PeerTables, shard_kv
+    full, shards, q = _full_and_shards(engine, R, B, Hkv, G, D, l_sink, l_cpu, l_local, "bf16", seed,
+                                       n_new=n_new)
+    max_new = max(4, n_new)
+    peers = []
+    for r in range(R):
+        kr = shards[r].dec.k
+        vr = shards[r].dec.v
+        ps = PeerShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new, "bf16", k=kr, v=vr)
+        ps.dec.l_new = shards[r].dec.l_new
+        ps.dec.build_metadata()
+        peers.append(ps)
+    tables = PeerTables(engine, R)
+    for s in peers:
+        tables.add_local(s)
+    return full, peers, tables, q
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3])
+@pytest.mark.parametrize("name,plan", PLANS)
+def test_cp_peer_exchange_matches_single_device(engine, R, name, plan):
+    """The one-shot peer-memory exchanges (no NCCL) give the single-device
+    selection bit-exactly and its output within the bf16 merge bound, over
+    two steps (both table parities)."""
+    from paper_2605_07719_b200.context_parallel import cp_decode_step_peer
+    B, Hkv, G, D = 2, 2, 4, 128
+    full, peers, tables, q = _peer_shards(engine, R, B, Hkv, G, D, 64, 5000 + 37, 256,
+                                          seed=R * 11 + len(name))
+    if plan == "props":
+        bgt0, ks, st = head_props(B, Hkv * G, seed=R)
+        plan = dict(props=tuple(torch.as_tensor(x, device=engine.device) for x in (bgt0, ks, st)))
+    for stamp in (1, 2):
+        qq = q if stamp == 1 else torch.roll(q, 1, dims=-1)
+        o_ref, lse_ref = full.step(qq, **plan)
+        o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
+        (o, lse), *_ = cp_decode_step_peer(peers, tables, qq, stamp, **plan)
+        torch.cuda.synchronize()
+        for b in range(B):
+            for h in range(Hkv * G):
+                want = full.selected_blocks(b, h)
+                got = np.sort(np.concatenate([sh.global_selection(b, h) for sh in peers]))
+                assert np.array_equal(got, want), (stamp, b, h)
+        torch.testing.assert_close(o, o_ref, rtol=BF16_TOL, atol=BF16_TOL)
+        torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_cp_peer_exchange_two_processes(tmp_path):
+    """Two processes, one rank each, on one GPU: the tables cross the process
+    boundary through CUDA IPC and the kernels synchronise on each other's
+    ready flags -- the multi-GPU protocol minus the NVLink hop."""
+    import random
+    import torch.multiprocessing as mp
+    import cp_peer_worker
+    port = random.randint(20000, 40000)
+    mp.spawn(cp_peer_worker.run, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    assert (tmp_path / "ok0").exists() and (tmp_path / "ok1").exists()
