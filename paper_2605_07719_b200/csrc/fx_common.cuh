@@ -70,6 +70,37 @@ __device__ double exact_score(const float* __restrict__ q, const T* __restrict__
     return s;
 }
 
+// The same score with q (f64) in shared memory and a bf16 [min | max] row read
+// as 16-byte vectors, fully unrolled so every load of the row is in flight
+// before the sequential sum consumes it (one memory round trip per row, not
+// one per dimension).  The sum order and rounding are exact_score's.
+__device__ __forceinline__ double exact_step(double s, double qd, float lo, float hi) {
+    const double a = __dmul_rn(qd, (double)lo), c = __dmul_rn(qd, (double)hi);
+    return __dadd_rn(s, (a < c) ? c : a);
+}
+template <int D>
+__device__ double exact_score_row(const double* qs, const __nv_bfloat16* __restrict__ row) {
+    constexpr int NV = D / 8;
+    uint4 a[NV], c[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        a[i] = __ldg(reinterpret_cast<const uint4*>(row) + i);
+        c[i] = __ldg(reinterpret_cast<const uint4*>(row + D) + i);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const uint32_t av[4] = {a[i].x, a[i].y, a[i].z, a[i].w}, cv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            s = exact_step(s, qs[8 * i + 2 * u], __uint_as_float(av[u] << 16), __uint_as_float(cv[u] << 16));
+            s = exact_step(s, qs[8 * i + 2 * u + 1], __uint_as_float(av[u] & 0xffff0000u),
+                           __uint_as_float(cv[u] & 0xffff0000u));
+        }
+    }
+    return s;
+}
+
 // (key desc, id asc) "less" = comes first
 __device__ __forceinline__ bool first_of(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
     return ka != kb ? ka > kb : ia < ib;

@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(kT) k_cp_candidates(
     uint64_t* sk = reinterpret_cast<uint64_t*>(dsm);
     uint32_t* si = reinterpret_cast<uint32_t*>(sk + sort_n);
     __shared__ int s_wpos[kT + 1];
+    __shared__ double s_q[256];
     const int64_t head = blockIdx.x;
     const int64_t H = (int64_t)Hkv * G;
     const int b = (int)(head / H), h = (int)(head % H);
@@ -77,11 +78,22 @@ __global__ void __launch_bounds__(kT) k_cp_candidates(
                                    (int64_t)bg * nblk * 2 * D
                              : nullptr;
     const float* qh = q + head * D;
+    for (int d = t; d < D; d += kT) s_q[d] = (double)qh[d];
+    __syncthreads();
     const int64_t off_blk = blk > 0 ? cpu_offset / blk : 0;
     for (int i = t; i < sort_n; i += kT) {
         if (i < n) {
             const uint32_t id = si[i];
-            sk[i] = f64_key(exact_score(qh, mbase + (int64_t)id * 2 * D, mbase + (int64_t)id * 2 * D + D, D));
+            const T* row = mbase + (int64_t)id * 2 * D;
+            double sc;
+            if constexpr (DT == FX_BF16) {
+                sc = D == 128 ? exact_score_row<128>(s_q, row)
+                   : D == 64  ? exact_score_row<64>(s_q, row)
+                              : exact_score(qh, row, row + D, D);
+            } else {
+                sc = exact_score(qh, row, row + D, D);
+            }
+            sk[i] = f64_key(sc);
             si[i] = (uint32_t)(id + off_blk);  // global block id
         } else {
             sk[i] = 0;
@@ -89,10 +101,14 @@ __global__ void __launch_bounds__(kT) k_cp_candidates(
         }
     }
     __syncthreads();
-    // 3. bitonic sort, (key desc, id asc) first
-    for (int kk = 2; kk <= sort_n; kk <<= 1)
+    // 3. bitonic sort, (key desc, id asc) first, over the smallest power of two
+    //    holding the n real entries (the padding sorts last and stays in place)
+    int len = 32;
+    while (len < n) len <<= 1;
+    len = len < sort_n ? len : sort_n;
+    for (int kk = 2; kk <= len; kk <<= 1)
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            for (int i = t; i < sort_n; i += kT) {
+            for (int i = t; i < len; i += kT) {
                 const int p = i ^ j;
                 if (p > i) {
                     const bool up = (i & kk) == 0;
@@ -353,6 +369,7 @@ void launch_cp_candidates(const fx_layout& L, const void* const meta[4], const f
                           int sel_words, int64_t cpu_offset, int64_t cap, uint64_t* keys,
                           uint32_t* ids, int32_t* count, uint64_t* kth, cudaStream_t s) {
     const int64_t heads = (int64_t)L.batch * L.kv_heads * L.group_size;
+    FX_REQUIRE(L.head_dim <= 256, FX_ERR_INVALID, "bad-shape: head_dim must be <= 256");
     const int sort_n = cp_sort_n(std::max<int64_t>(1, level_blocks(L.l_cpu, 16)));
     const size_t smem = (size_t)sort_n * 12;
     FX_REQUIRE(smem <= 200 * 1024, FX_ERR_INVALID,

@@ -30,6 +30,7 @@
 // reference's pairwise LSE merges, so a prefix whose deviation lies within
 // ~1e-12 of tau can land one block off; tests report those separately.
 #include <algorithm>
+#include <type_traits>
 
 #include "fx_common.cuh"
 
@@ -311,9 +312,12 @@ __global__ void __launch_bounds__(128) k_lab_norm(const LabelView p) {
 // K_keys: exact Quest bounds of the blocks at 16..128 (levels 1..4).
 template <typename T>
 __global__ void __launch_bounds__(256) k_lab_keys(const LabelView p) {
+    __shared__ double qs[128];
     const int64_t head = blockIdx.y;
     const int lvl = blockIdx.z + 1;
     if (p.streaming[head]) return;
+    for (int d = threadIdx.x; d < p.D; d += blockDim.x) qs[d] = (double)p.q[head * p.D + d];
+    __syncthreads();
     const int blk = c_label_blk[lvl];
     const int64_t nblk = cdiv_dev(p.l_cpu, blk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -323,7 +327,14 @@ __global__ void __launch_bounds__(256) k_lab_keys(const LabelView p) {
     const T* m = static_cast<const T*>(p.meta[lvl - 1]) + ((bg * nblk + i) * 2) * D;
     const int64_t n_tot = p.seg_off[kNL];
     const int64_t o = head * n_tot + p.seg_off[lvl] + i;
-    p.keys[0][o] = ~f64_key(exact_score(p.q + head * D, m, m + D, D));
+    double sc;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        sc = D == 128 ? exact_score_row<128>(qs, m) : D == 64 ? exact_score_row<64>(qs, m)
+                                                              : exact_score(p.q + head * D, m, m + D, D);
+    } else {
+        sc = exact_score(p.q + head * D, m, m + D, D);
+    }
+    p.keys[0][o] = ~f64_key(sc);
     p.ids[0][o] = (uint32_t)i;
 }
 
