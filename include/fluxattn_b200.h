@@ -384,13 +384,17 @@ FX_API int fx_cp_combine(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim, con
  * all-gather, no host round trip for the exchange size.  Pointers [dev]. */
 #define FX_CP_MAX_RANKS 16
 typedef struct fx_cp_peer {
-    const uint64_t* keys;   /* [n][cap] sorted candidate keys (fx_cp_candidates) */
+    const uint64_t* keys;   /* [n][cap] sorted candidate (or band) keys */
     const uint32_t* ids;    /* [n][cap] global block ids */
-    const uint64_t* kth;    /* [n] local k-th key */
+    const uint64_t* kth;    /* [n] local k-th key (candidate protocol) */
     const float* o;         /* [n][dim] attention partial of the shard */
     const float* lse;       /* [n] */
-    const uint64_t* flags;  /* [2]: candidates ready, partials ready (step stamps) */
+    const uint64_t* flags;  /* [4] step stamps: 0 candidates / stats, 1 histograms,
+                               2 bands, 3 partials */
     int64_t cap;
+    const double* stats;    /* [n][4] approx-score min, max, error bound, non-finite (bracket protocol) */
+    const int32_t* hist;    /* [n][2048] approx-score histogram over the global range */
+    const int32_t* defc;    /* [n] blocks certainly in the top-k */
 } fx_cp_peer;
 /* flags[slot] = stamp after every prior op of the stream is visible system-wide. */
 FX_API int fx_cp_signal(fx_ctx* ctx, uint64_t* flags, int32_t slot, uint64_t stamp);
@@ -400,7 +404,24 @@ FX_API int fx_cp_select_peer(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, i
                              const fx_cp_peer* peers, uint64_t stamp, const int32_t* kblocks,
                              const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out,
                              int32_t sel_words);
-/* Waits for peers[r].flags[1] >= stamp, then merge_into over the peers' (o, lse). */
+/* The single-device selection (K2b's bracket) distributed over the ranks --
+ * nothing but the band around the global k-th score is ever exact-scored or
+ * sorted.  Phases, each launched for every local shard before the next:
+ *   0  plan + approximate scores into `approx`; per-head min / max / error
+ *      bound -> own stats; (then fx_cp_signal slot 0)
+ *   1  wait stats of all ranks; histogram of the local scores over the global
+ *      range -> own hist; (signal 1)
+ *   2  wait hists; the summed histogram brackets the global k-th score: blocks
+ *      above it -> sel_out bits, count -> own defc; the band is exact-scored and
+ *      sorted (score desc, id asc) -> own keys / ids; (signal 2)
+ *   3  wait bands; global rank of each own band entry among all ranks' bands,
+ *      bits for rank < k - sum(defc).
+ * args: the shard's step arguments (q, meta, absmax, plan, l_cpu_total,
+ * cpu_offset; sel_bits = sel_out).  approx [dev] [n][approx_stride] f32. */
+FX_API int fx_cp_dist_phase(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* args,
+                            int32_t phase, int32_t ranks, int32_t self, const fx_cp_peer* peers,
+                            uint64_t stamp, float* approx, int64_t approx_stride);
+/* Waits for peers[r].flags[3] >= stamp, then merge_into over the peers' (o, lse). */
 FX_API int fx_cp_combine_peer(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim,
                               const fx_cp_peer* peers, uint64_t stamp, float* o, float* lse);
 /* CUDA IPC for the peer tables: export the allocation holding dptr (64-byte

@@ -91,7 +91,7 @@ class CpPeer(C.Structure):
     """fx_cp_peer: one rank's exchange tables as seen from this device."""
 
     _fields_ = [("keys", _p), ("ids", _p), ("kth", _p), ("o", _p), ("lse", _p), ("flags", _p),
-                ("cap", _i64)]
+                ("cap", _i64), ("stats", _p), ("hist", _p), ("defc", _p)]
 
 
 class NativeError(RuntimeError):
@@ -159,6 +159,8 @@ _SIGS = {
     "fx_cp_signal": (C.c_int, [_p, _p, _i32, C.c_uint64]),
     "fx_cp_select_peer": (C.c_int, [_p, C.POINTER(Layout), _i32, _i32, _p, C.c_uint64, _p, _p, _i64,
                                     _p, _i32]),
+    "fx_cp_dist_phase": (C.c_int, [_p, C.POINTER(Layout), C.POINTER(StepArgs), _i32, _i32, _i32, _p,
+                                   C.c_uint64, _p, _i64]),
     "fx_cp_combine_peer": (C.c_int, [_p, _i32, _i64, _i32, _p, C.c_uint64, _p, _p]),
     "fx_ipc_handle": (C.c_int, [_p, C.c_char_p, C.POINTER(_i64)]),
     "fx_ipc_open": (C.c_int, [_p, C.c_char_p, C.POINTER(_p)]),

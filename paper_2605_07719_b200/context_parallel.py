@@ -234,6 +234,9 @@ def cp_decode_step(shards: Sequence, comm, q: torch.Tensor, out: Sequence[Tuple[
 # fx_cp_combine_peer read the other ranks' candidate lists and (o, lse)
 # partials where they live, after each rank's ready flag
 # ---------------------------------------------------------------------------
+DIST_BINS = 2048  # fx_cp.cu kDBins
+
+
 class PeerShard(CPShard):
     """A CPShard whose exchange tables (candidates, k-th keys, partials, ready
     flags) are double-buffered by step parity and exported to the peers.  Two
@@ -254,26 +257,49 @@ class PeerShard(CPShard):
                 count=torch.zeros(nh, dtype=torch.int32, device=dev),
                 kth=torch.zeros(nh, dtype=torch.int64, device=dev),
                 o=torch.zeros((B, H, D), dtype=torch.float32, device=dev),
-                lse=torch.zeros((B, H), dtype=torch.float32, device=dev)))
-        self.flags = torch.zeros((2, 2), dtype=torch.int64, device=dev)  # [parity][slot]
+                lse=torch.zeros((B, H), dtype=torch.float32, device=dev),
+                stats=torch.zeros((nh, 4), dtype=torch.float64, device=dev),
+                hist=torch.zeros((nh, DIST_BINS), dtype=torch.int32, device=dev),
+                defc=torch.zeros(nh, dtype=torch.int32, device=dev)))
+        # [parity][slot]: 0 candidates / stats, 1 histograms, 2 bands, 3 partials
+        self.flags = torch.zeros((2, 4), dtype=torch.int64, device=dev)
+        self.approx = None  # [nh][cap] f32, the bracket protocol's local scores
 
     def table(self, parity: int) -> "N.CpPeer":
         st = self.sets[parity]
         return N.CpPeer(st["keys"].data_ptr(), st["ids"].data_ptr(), st["kth"].data_ptr(),
                         st["o"].data_ptr(), st["lse"].data_ptr(), self.flags[parity].data_ptr(),
-                        self.cap)
+                        self.cap, st["stats"].data_ptr(), st["hist"].data_ptr(), st["defc"].data_ptr())
 
     def exported(self):
         """(name, handle bytes, offset) of every exchange buffer, for the peers."""
         out = []
         bufs = [(f"{n}{p}", self.sets[p][n]) for p in range(2)
-                for n in ("keys", "ids", "kth", "o", "lse")] + [("flags", self.flags)]
+                for n in ("keys", "ids", "kth", "o", "lse", "stats", "hist", "defc")] + [("flags", self.flags)]
         for name, t in bufs:
             h = C.create_string_buffer(64)
             off = C.c_int64(0)
             check(LIB.fx_ipc_handle(C.c_void_p(t.data_ptr()), h, C.byref(off)))
             out.append((name, h.raw, off.value))
         return out
+
+    def dist_phase(self, q, parity, phase, tables: "PeerTables", peers, stamp, **plan):
+        """One phase of the distributed bracket selection (fx_cp_dist_phase)."""
+        d = self.dec
+        if phase == 0:
+            a = d._args(q, plan.get("props"), plan.get("fixed"), plan.get("full", False),
+                        plan.get("blk"), plan.get("budgets"))
+            if self.approx is None:
+                self.approx = torch.empty((self.n_heads, self.cap), dtype=torch.float32,
+                                          device=self.eng.device)
+        else:
+            a = d.args
+        a.sel_bits = self.sel.data_ptr()
+        a.sel_words = d.sel_words
+        check(LIB.fx_cp_dist_phase(self.eng.ctx, C.byref(d.lay), C.byref(a), phase, tables.ranks,
+                                   self.rank, peers, stamp, self.approx.data_ptr(), self.cap))
+        if phase < 3:
+            check(LIB.fx_cp_signal(self.eng.ctx, C.c_void_p(self.flags[parity].data_ptr()), phase, stamp))
 
     def candidates_into(self, q, parity, **plan):
         st = self.sets[parity]
@@ -308,7 +334,8 @@ class PeerTables:
             ptr[name] = d.value + off
         for p in range(2):
             self.tabs[p][rank] = N.CpPeer(ptr[f"keys{p}"], ptr[f"ids{p}"], ptr[f"kth{p}"],
-                                          ptr[f"o{p}"], ptr[f"lse{p}"], ptr["flags"] + p * 16, cap)
+                                          ptr[f"o{p}"], ptr[f"lse{p}"], ptr["flags"] + p * 32, cap,
+                                          ptr[f"stats{p}"], ptr[f"hist{p}"], ptr[f"defc{p}"])
 
     def array(self, parity: int):
         arr = (N.CpPeer * self.ranks)(*self.tabs[parity])
@@ -353,7 +380,7 @@ def cp_decode_step_peer(shards: Sequence[PeerShard], tables: PeerTables, q: torc
     for s in shards:
         st = s.sets[par]
         s.dec.step(q, blk="keep", out=st["o"], lse=st["lse"], sel_in=s.sel)
-        check(LIB.fx_cp_signal(s.eng.ctx, C.c_void_p(s.flags[par].data_ptr()), 1, stamp))
+        check(LIB.fx_cp_signal(s.eng.ctx, C.c_void_p(s.flags[par].data_ptr()), 3, stamp))
     res = []
     for i, s in enumerate(shards):
         if out is not None:
@@ -366,3 +393,30 @@ def cp_decode_step_peer(shards: Sequence[PeerShard], tables: PeerTables, q: torc
         res.append((o, lse))
     return res
 
+
+def cp_decode_step_dist(shards: Sequence[PeerShard], tables: PeerTables, q: torch.Tensor,
+                        stamp: int, out: Sequence[Tuple[torch.Tensor, torch.Tensor]] = None, **plan):
+    """cp_decode_step_peer with the selection distributed as the single-device
+    bracket (fx_cp_dist_phase): the ranks exchange per-head score ranges,
+    2048-bin histograms and the exact-scored band around the global k-th
+    score, so only the band is ever exact-scored or sorted.  Same selection
+    as the one-device step, bit for bit."""
+    par = stamp % 2
+    peers = tables.array(par)
+    for phase in range(4):
+        for s in shards:
+            s.dist_phase(q, par, phase, tables, peers, stamp, **plan)
+    res = []
+    for s in shards:
+        st = s.sets[par]
+        s.dec.step(q, blk="keep", out=st["o"], lse=st["lse"], sel_in=s.sel)
+        check(LIB.fx_cp_signal(s.eng.ctx, C.c_void_p(s.flags[par].data_ptr()), 3, stamp))
+    for i, s in enumerate(shards):
+        if out is not None:
+            o, lse = out[i]
+        else:
+            o, lse = torch.empty_like(s.o), torch.empty_like(s.lse)
+        check(LIB.fx_cp_combine_peer(s.eng.ctx, tables.ranks, s.n_heads, o.shape[-1], peers, stamp,
+                                     o.data_ptr(), lse.data_ptr()))
+        res.append((o, lse))
+    return res

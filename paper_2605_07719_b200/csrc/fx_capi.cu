@@ -1070,7 +1070,7 @@ int fx_cp_select(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t self,
 int fx_cp_signal(fx_ctx* ctx, uint64_t* flags, int32_t slot, uint64_t stamp) {
     return guarded([&] {
         DeviceGuard g(ctx);
-        FX_REQUIRE(flags && (slot == 0 || slot == 1), FX_ERR_INVALID, "bad-shape: flag slot");
+        FX_REQUIRE(flags && slot >= 0 && slot < 4, FX_ERR_INVALID, "bad-shape: flag slot");
         fx::launch_cp_signal(flags, slot, stamp, ctx->stream);
         ctx->launches += 1;
     });
@@ -1089,6 +1089,43 @@ int fx_cp_select_peer(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t 
                    FX_ERR_INVALID, "bad-shape: sel_words too small");
         fx::launch_cp_select_peer(*lay, ranks, self, peers, stamp, kblocks, blk, cpu_offset, sel_out,
                                   sel_words, ctx->stream);
+        ctx->launches += 1;
+    });
+}
+
+int fx_cp_dist_phase(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, int32_t phase,
+                     int32_t ranks, int32_t self, const fx_cp_peer* peers, uint64_t stamp,
+                     float* approx, int64_t approx_stride) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const fx_layout& L = *lay;
+        FX_REQUIRE(a && a->q && a->plan_blk && a->plan_budgets && a->plan_kblocks && a->sel_bits && peers &&
+                       approx,
+                   FX_ERR_STATE, "no-context: distributed selection has no payload");
+        FX_REQUIRE(phase >= 0 && phase <= 3, FX_ERR_INVALID, "bad-shape: unknown phase");
+        FX_REQUIRE(L.l_cpu > 0, FX_ERR_INVALID, "empty-context: shard has no cpu rows");
+        FX_REQUIRE(approx_stride >= fx::level_blocks(L.l_cpu, 16), FX_ERR_INVALID,
+                   "bad-shape: approx_stride below the shard's block count");
+        const int64_t l_plan = a->l_cpu_total > 0 ? a->l_cpu_total : L.l_cpu;
+        FX_REQUIRE(a->cpu_offset >= 0 && a->cpu_offset % 128 == 0 && a->cpu_offset + L.l_cpu <= l_plan,
+                   FX_ERR_INVALID, "bad-shape: shard [cpu_offset, +l_cpu) outside l_cpu_total or unaligned");
+        if (phase == 0) {
+            for (int i = 0; i < 4; ++i)
+                FX_REQUIRE(a->meta[i] != nullptr, FX_ERR_STATE, "no-context: missing block metadata");
+            FX_REQUIRE(a->absmax != nullptr, FX_ERR_STATE, "no-context: missing absmax");
+            const int grid = fx::attend_grid(L, false, ctx->num_sms);
+            StepScratch s = carve_step(ctx, L, grid, true);
+            fx::launch_prepare(L, l_plan, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
+                               a->kslope, a->streaming, a->plan_blk, a->plan_budgets, a->plan_volume,
+                               a->plan_cand_volumes, a->plan_kblocks, s.bg_done, ctx->stream);
+            fx::launch_approx_scores(L, a->meta, a->q, a->plan_blk, a->plan_kblocks, approx, approx_stride,
+                                     ctx->num_sms, ctx->stream, /*rank_all=*/true);
+            ctx->launches += 2;
+        }
+        fx::launch_cp_dist_phase(L, phase, ranks, self, peers, stamp, approx, approx_stride, a->q, a->absmax,
+                                 a->meta, a->plan_blk, a->plan_kblocks, l_plan, a->cpu_offset, a->sel_bits,
+                                 a->sel_words, ctx->stream);
         ctx->launches += 1;
     });
 }

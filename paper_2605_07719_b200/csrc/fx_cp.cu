@@ -17,6 +17,8 @@
 #include "fx_common.cuh"
 
 namespace fx {
+int cp_sort_n(int64_t nblk16);
+double approx_eps_scale(const fx_layout& L);
 namespace {
 
 constexpr int kT = 256;
@@ -307,7 +309,7 @@ __global__ void k_cp_combine_peer(const __grid_constant__ PeerSet ps, int R, int
                                   uint64_t stamp, float* __restrict__ o, float* __restrict__ lse) {
     pdl_wait();
     pdl_trigger();
-    wait_peers(ps, R, 1, stamp);
+    wait_peers(ps, R, 3, stamp);
     const int64_t i = blockIdx.x;
     float M = -INFINITY;
     for (int r = 0; r < R; ++r) M = fmaxf(M, ps.p[r].lse[i]);
@@ -327,7 +329,403 @@ __global__ void k_cp_combine_peer(const __grid_constant__ PeerSet ps, int R, int
     if (threadIdx.x == 0 && lse) lse[i] = den > 0.f ? M + logf(den) : -INFINITY;
 }
 
+// ---------------------------------------------------------------------------
+// the bracket selection distributed over the ranks
+// ---------------------------------------------------------------------------
+constexpr int kDBins = 2048;
+
+struct DistArgs {
+    int R, self, Hkv, G, D;
+    int64_t l_cpu, l_total, cpu_offset, astride;
+    double eps_scale;
+    const float* approx;
+    const float* q;
+    const float* absmax;
+    MetaLevels meta;
+    const int32_t* blk;
+    const int32_t* kblocks;
+    uint32_t* sel;
+    int sel_words, sort_n;
+    double* stats;     // own tables
+    int32_t* hist;
+    uint64_t* keys;
+    uint32_t* ids;
+    int32_t* defc;
+    int64_t cap;
+    uint64_t stamp;
+};
+
+struct HeadInfo {
+    int blk;
+    int64_t nblk_local, nblk_total, k;
+};
+__device__ __forceinline__ HeadInfo head_info(const DistArgs& a, int64_t head) {
+    HeadInfo h;
+    h.blk = a.blk[head / a.G];
+    h.k = a.kblocks[head];
+    h.nblk_local = h.blk > 0 ? cdiv_dev(a.l_cpu, h.blk) : 0;
+    h.nblk_total = h.blk > 0 ? cdiv_dev(a.l_total, h.blk) : 0;
+    return h;
+}
+
+// phase 0: min, max, finiteness of the local approximate scores; error bound
+__global__ void __launch_bounds__(kT) k_cpd_stats(const DistArgs a) {
+    __shared__ float rmx[kT / 32], rmn[kT / 32];
+    __shared__ double s_eps;
+    const int64_t head = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const HeadInfo hi = head_info(a, head);
+    const float* sc = a.approx + head * a.astride;
+    float mx = -INFINITY, mn = INFINITY;
+    bool fin = true;
+    for (int64_t i = t; i < hi.nblk_local; i += kT) {
+        const float x = sc[i];
+        if (isfinite(x)) {
+            mx = fmaxf(mx, x);
+            mn = fminf(mn, x);
+        } else {
+            fin = false;
+        }
+    }
+    if (warp == 0) {  // eps = c * sum_d |q_d| absmax_d (fx_topk.cu)
+        const int64_t bg = head / a.G;
+        double e = 0.0;
+        for (int d = lane; d < a.D; d += 32)
+            e += fabs((double)a.q[head * a.D + d]) * (double)a.absmax[bg * a.D + d];
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (lane == 0) s_eps = e * a.eps_scale * 1.01 + 1e-30;
+    }
+    mx = warp_max(mx);
+    mn = -warp_max(-mn);
+    if (lane == 0) {
+        rmx[warp] = mx;
+        rmn[warp] = mn;
+    }
+    const bool allfin = __syncthreads_and(fin);
+    if (t == 0) {
+        for (int w = 0; w < kT / 32; ++w) {
+            mx = fmaxf(mx, rmx[w]);
+            mn = fminf(mn, rmn[w]);
+        }
+        double* st = a.stats + head * 4;
+        st[0] = mn;
+        st[1] = mx;
+        st[2] = s_eps;
+        st[3] = (allfin && isfinite(s_eps)) ? 0.0 : 1.0;
+    }
+}
+
+// global range / bound / sanity of a head over all ranks
+struct Global {
+    float gmn, gmx;
+    double eps;
+    bool sane;
+};
+__device__ Global global_of(const PeerSet& ps, int R, int64_t head) {
+    Global g{INFINITY, -INFINITY, 0.0, true};
+    for (int r = 0; r < R; ++r) {
+        const double* st = ps.p[r].stats + head * 4;
+        g.gmn = fminf(g.gmn, (float)st[0]);
+        g.gmx = fmaxf(g.gmx, (float)st[1]);
+        g.eps = fmax(g.eps, st[2]);
+        g.sane = g.sane && st[3] == 0.0;
+    }
+    return g;
+}
+
+// phase 1: local histogram over the global range (the single-device bin map)
+__global__ void __launch_bounds__(kT) k_cpd_hist(const __grid_constant__ PeerSet ps, const DistArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    wait_peers(ps, a.R, 0, a.stamp);
+    __shared__ int hist[kDBins];
+    const int64_t head = blockIdx.x;
+    const int t = threadIdx.x;
+    const HeadInfo hi = head_info(a, head);
+    const Global g = global_of(ps, a.R, head);
+    for (int i = t; i < kDBins; i += kT) hist[i] = 0;
+    __syncthreads();
+    if (hi.blk > 0 && g.sane && g.gmx > g.gmn) {
+        const float scale = (float)kDBins / (g.gmx - g.gmn);
+        const float* sc = a.approx + head * a.astride;
+        for (int64_t i = t; i < hi.nblk_local; i += kT) {
+            const float f = (sc[i] - g.gmn) * scale;
+            atomicAdd(&hist[f >= (float)(kDBins - 1) ? kDBins - 1 : (f <= 0.f ? 0 : (int)f)], 1);
+        }
+    }
+    __syncthreads();
+    for (int i = t; i < kDBins; i += kT) a.hist[head * kDBins + i] = hist[i];
+}
+
+// phase 2: bracket from the summed histogram; definite bits; exact, sorted band
+template <int DT>
+__global__ void __launch_bounds__(kT) k_cpd_band(const __grid_constant__ PeerSet ps, const DistArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    wait_peers(ps, a.R, 1, a.stamp);
+    using T = typename Elem<DT>::T;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(dsm);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + a.sort_n);
+    __shared__ int hist[kDBins];
+    __shared__ int s_cnt[2][kT / 32];
+    __shared__ int s_bin;
+    __shared__ double s_q[256];
+    const int64_t head = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const HeadInfo hi = head_info(a, head);
+    uint32_t* bits = a.sel + head * a.sel_words;
+    const int W = (int)cdiv_dev(hi.nblk_local, 32);
+    for (int j = t; j < a.sel_words; j += kT) bits[j] = 0u;
+    int64_t ndef = 0, nband = 0;
+    const bool all = hi.blk > 0 && hi.k >= hi.nblk_total;  // clamped: every block
+    const bool none = hi.blk <= 0 || hi.k <= 0;
+    __syncthreads();
+    if (all) {
+        for (int j = t; j < W; j += kT) {
+            const int64_t rem = hi.nblk_local - (int64_t)j * 32;
+            bits[j] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+        }
+        ndef = hi.nblk_local;
+    } else if (!none) {
+        const Global g = global_of(ps, a.R, head);
+        double e_lo = -INFINITY, e_hi = INFINITY;  // insane: everything is band
+        if (g.sane && !(g.gmx > g.gmn)) {
+            e_lo = e_hi = (double)g.gmx;
+        } else if (g.sane) {
+            for (int i = t; i < kDBins; i += kT) {
+                int c = 0;
+                for (int r = 0; r < a.R; ++r) c += ps.p[r].hist[head * kDBins + i];
+                hist[i] = c;
+            }
+            __syncthreads();
+            constexpr int PB = kDBins / kT;
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < PB; ++i) c += hist[t * PB + i];
+            int x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_down_sync(0xffffffffu, x, o);
+                if (lane + o < 32) x += y;
+            }
+            if (lane == 0) s_cnt[0][warp] = x;
+            __syncthreads();
+            int S = x;
+            for (int w = warp + 1; w < kT / 32; ++w) S += s_cnt[0][w];
+            if (S >= hi.k && S - c < hi.k) {
+                int above = S - c;
+                for (int i = PB - 1; i >= 0; --i) {
+                    above += hist[t * PB + i];
+                    if (above >= hi.k) {
+                        s_bin = t * PB + i;
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            const double wdt = ((double)g.gmx - (double)g.gmn) / kDBins;
+            e_lo = (double)g.gmn + (s_bin - 1) * wdt;
+            e_hi = (double)g.gmn + (s_bin + 2) * wdt;
+        }
+        const double up = e_hi + 2.0 * g.eps, lo = e_lo - 2.0 * g.eps;
+        const float* sc = a.approx + head * a.astride;
+        // definite-in bits and the band ids (compacted in block order)
+        int wdef = 0, wband = 0;
+        for (int j = warp; j < W; j += kT / 32) {
+            const int64_t i = (int64_t)j * 32 + lane;
+            const bool in = i < hi.nblk_local;
+            const double x = in ? (double)sc[i] : 0.0;
+            const uint32_t bd = __ballot_sync(0xffffffffu, in && x > up);
+            const uint32_t bc = __ballot_sync(0xffffffffu, in && !(x > up) && x >= lo);
+            if (lane == 0) bits[j] = bd;
+            wdef += __popc(bd);
+            wband += __popc(bc);
+        }
+        if (lane == 0) {
+            s_cnt[0][warp] = wdef;
+            s_cnt[1][warp] = wband;
+        }
+        __syncthreads();
+        int64_t base = 0;
+        for (int w = 0; w < kT / 32; ++w) {
+            ndef += s_cnt[0][w];
+            nband += s_cnt[1][w];
+            if (w < warp) base += s_cnt[1][w];
+        }
+        for (int j = warp; j < W; j += kT / 32) {
+            const int64_t i = (int64_t)j * 32 + lane;
+            const bool in = i < hi.nblk_local;
+            const double x = in ? (double)sc[i] : 0.0;
+            const bool cand = in && !(x > up) && x >= lo;
+            const uint32_t bc = __ballot_sync(0xffffffffu, cand);
+            if (cand) {
+                const int64_t pos = base + __popc(bc & ((1u << lane) - 1u));
+                if (pos < a.sort_n) si[pos] = (uint32_t)i;
+            }
+            base += __popc(bc);
+        }
+        for (int d = t; d < a.D; d += kT) s_q[d] = (double)a.q[head * a.D + d];
+        __syncthreads();
+        const int64_t bgi = head / a.G;
+        const T* mbase = static_cast<const T*>(a.meta.p[hi.blk == 16 ? 0 : hi.blk == 32 ? 1 : hi.blk == 64 ? 2 : 3]) +
+                         bgi * hi.nblk_local * 2 * a.D;
+        const int64_t off_blk = a.cpu_offset / hi.blk;
+        int len = 32;
+        while (len < nband) len <<= 1;
+        for (int i = t; i < len; i += kT) {
+            if (i < nband) {
+                const uint32_t id = si[i];
+                const T* row = mbase + (int64_t)id * 2 * a.D;
+                double v;
+                if constexpr (DT == FX_BF16) {
+                    v = a.D == 128 ? exact_score_row<128>(s_q, row)
+                      : a.D == 64  ? exact_score_row<64>(s_q, row)
+                                   : exact_score(a.q + head * a.D, row, row + a.D, a.D);
+                } else {
+                    v = exact_score(a.q + head * a.D, row, row + a.D, a.D);
+                }
+                sk[i] = f64_key(v);
+                si[i] = (uint32_t)(id + off_blk);
+            } else {
+                sk[i] = 0;
+                si[i] = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        for (int kk = 2; kk <= len; kk <<= 1)
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int i = t; i < len; i += kT) {
+                    const int p2 = i ^ j;
+                    if (p2 > i) {
+                        const bool upd = (i & kk) == 0;
+                        const uint64_t x1 = sk[i], x2 = sk[p2];
+                        const uint32_t i1 = si[i], i2 = si[p2];
+                        if (upd ? first_of(x2, i2, x1, i1) : first_of(x1, i1, x2, i2)) {
+                            sk[i] = x2;
+                            sk[p2] = x1;
+                            si[i] = i2;
+                            si[p2] = i1;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+    }
+    __syncthreads();
+    for (int64_t i = t; i < a.cap; i += kT) {
+        a.keys[head * a.cap + i] = i < nband ? sk[i] : 0ull;
+        a.ids[head * a.cap + i] = i < nband ? si[i] : 0xffffffffu;
+    }
+    if (t == 0) a.defc[head] = (int32_t)ndef;
+}
+
+// phase 3: global ranks of the own band entries among all ranks' bands
+__global__ void __launch_bounds__(kT) k_cpd_rank(const __grid_constant__ PeerSet ps, const DistArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    wait_peers(ps, a.R, 2, a.stamp);
+    const int64_t head = blockIdx.x;
+    const int t = threadIdx.x;
+    const HeadInfo hi = head_info(a, head);
+    if (hi.blk <= 0 || hi.k <= 0 || hi.k >= hi.nblk_total) return;
+    int64_t need = hi.k;
+    for (int r = 0; r < a.R; ++r) need -= ps.p[r].defc[head];
+    uint32_t* bits = a.sel + head * a.sel_words;
+    const int64_t off_blk = a.cpu_offset / hi.blk;
+    const fx_cp_peer& me = ps.p[a.self];
+    const uint64_t* own_k = me.keys + head * me.cap;
+    const uint32_t* own_i = me.ids + head * me.cap;
+    for (int64_t j = t; j < me.cap; j += kT) {
+        const uint64_t ke = own_k[j];
+        if (ke == 0) break;  // end of the band (sorted, zero-padded)
+        const uint32_t ie = own_i[j];
+        int64_t rank = j;
+        for (int r = 0; r < a.R && rank < need; ++r) {
+            if (r == a.self) continue;
+            const uint64_t* kr = ps.p[r].keys + head * ps.p[r].cap;
+            const uint32_t* ir = ps.p[r].ids + head * ps.p[r].cap;
+            int64_t lo = 0, hi2 = ps.p[r].cap;
+            while (lo < hi2) {
+                const int64_t mid = (lo + hi2) >> 1;
+                if (kr[mid] != 0 && first_of(kr[mid], ir[mid], ke, ie)) lo = mid + 1;
+                else hi2 = mid;
+            }
+            rank += lo;
+        }
+        if (rank < need) {
+            const int64_t local = (int64_t)ie - off_blk;
+            atomicOr(&bits[local >> 5], 1u << (local & 31));
+        }
+    }
+}
+
 }  // namespace
+
+void launch_cp_dist_phase(const fx_layout& L, int phase, int R, int self, const fx_cp_peer* peers,
+                          uint64_t stamp, const float* approx, int64_t astride, const float* q,
+                          const float* absmax, const void* const meta[4], const int32_t* blk,
+                          const int32_t* kblocks, int64_t l_total, int64_t cpu_offset, uint32_t* sel,
+                          int sel_words, cudaStream_t s) {
+    FX_REQUIRE(R >= 1 && R <= FX_CP_MAX_RANKS && self >= 0 && self < R, FX_ERR_INVALID,
+               "bad-shape: rank / rank count");
+    FX_REQUIRE(L.head_dim <= 256 && L.group_size <= 8, FX_ERR_INVALID,
+               "bad-shape: head_dim must be <= 256 and group_size <= 8");
+    PeerSet ps{};
+    for (int r = 0; r < R; ++r) ps.p[r] = peers[r];
+    const fx_cp_peer& me = peers[self];
+    // a band never outgrows the tables: cap covers every local block at size 16
+    FX_REQUIRE(me.cap >= cdiv(L.l_cpu, 16) && me.stats && me.hist && me.defc && me.keys && me.ids,
+               FX_ERR_INVALID, "bad-shape: own exchange tables missing or cap below the shard's 16-blocks");
+    DistArgs a{};
+    a.R = R;
+    a.self = self;
+    a.Hkv = L.kv_heads;
+    a.G = L.group_size;
+    a.D = L.head_dim;
+    a.l_cpu = L.l_cpu;
+    a.l_total = l_total;
+    a.cpu_offset = cpu_offset;
+    a.astride = astride;
+    a.eps_scale = approx_eps_scale(L);
+    a.approx = approx;
+    a.q = q;
+    a.absmax = absmax;
+    for (int i = 0; i < 4; ++i) a.meta.p[i] = meta[i];
+    a.blk = blk;
+    a.kblocks = kblocks;
+    a.sel = sel;
+    a.sel_words = sel_words;
+    a.cap = me.cap;
+    a.sort_n = cp_sort_n(std::max<int64_t>(1, me.cap));
+    a.stats = const_cast<double*>(me.stats);
+    a.hist = const_cast<int32_t*>(me.hist);
+    a.keys = const_cast<uint64_t*>(me.keys);
+    a.ids = const_cast<uint32_t*>(me.ids);
+    a.defc = const_cast<int32_t*>(me.defc);
+    a.stamp = stamp;
+    const int64_t n = (int64_t)L.batch * L.kv_heads * L.group_size;
+    if (n <= 0) return;
+    if (phase == 0) {
+        k_cpd_stats<<<(unsigned)n, kT, 0, s>>>(a);
+    } else if (phase == 1) {
+        launch_pdl(k_cpd_hist, (unsigned)n, kT, 0, s, ps, a);
+    } else if (phase == 2) {
+        const size_t smem = (size_t)a.sort_n * 12;
+        FX_REQUIRE(smem <= 200 * 1024, FX_ERR_INVALID,
+                   "bad-shape: context-parallel shard too long (more than 16384 blocks of 16)");
+        if (L.dtype == FX_BF16) {
+            FX_CUDA(cudaFuncSetAttribute(k_cpd_band<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            launch_pdl(k_cpd_band<FX_BF16>, (unsigned)n, kT, smem, s, ps, a);
+        } else {
+            FX_CUDA(cudaFuncSetAttribute(k_cpd_band<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            launch_pdl(k_cpd_band<FX_F32>, (unsigned)n, kT, smem, s, ps, a);
+        }
+    } else {
+        launch_pdl(k_cpd_rank, (unsigned)n, kT, 0, s, ps, a);
+    }
+    FX_CUDA(cudaGetLastError());
+}
 
 void launch_cp_signal(uint64_t* flags, int slot, uint64_t stamp, cudaStream_t s) {
     k_cp_signal<<<1, 1, 0, s>>>(flags, slot, stamp);

@@ -117,7 +117,7 @@ void launch_predict(int n, const double* w1t, const double* b1, const double* w2
 double approx_eps_scale(const fx_layout& L);
 void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
                           const int32_t* blk, const int32_t* kblocks, float* approx,
-                          int64_t approx_stride, int num_sms, cudaStream_t s);
+                          int64_t approx_stride, int num_sms, cudaStream_t s, bool rank_all = false);
 struct WorklistArgs;
 // wl != nullptr: the selection kernel also builds the attention boxes (fused
 // worklist); sel_done = [n_bg] per-group head counters, zeroed by k_prepare.
@@ -191,6 +191,11 @@ void launch_cp_select_peer(const fx_layout& L, int R, int self, const fx_cp_peer
                            uint32_t* sel_out, int sel_words, cudaStream_t s);
 void launch_cp_combine_peer(int R, int64_t n, int dim, const fx_cp_peer* peers, uint64_t stamp, float* o,
                             float* lse, cudaStream_t s);
+void launch_cp_dist_phase(const fx_layout& L, int phase, int R, int self, const fx_cp_peer* peers,
+                          uint64_t stamp, const float* approx, int64_t astride, const float* q,
+                          const float* absmax, const void* const meta[4], const int32_t* blk,
+                          const int32_t* kblocks, int64_t l_total, int64_t cpu_offset, uint32_t* sel,
+                          int sel_words, cudaStream_t s);
 
 // fx_attend.cu
 // 3-D TMA map of a bf16 [rows][D] matrix: {64 columns, rows, D/64 chunks},

@@ -56,7 +56,7 @@ struct TileCtx {
     int64_t nblk, t0, head0;
 };
 __device__ __forceinline__ bool tile_ctx(const int32_t* blk_arr, const int32_t* kblocks, int Hkv,
-                                         int G, int64_t l_cpu, TileCtx& c) {
+                                         int G, int64_t l_cpu, TileCtx& c, int rank_all) {
     c.bg = blockIdx.y;
     c.b = c.bg / Hkv;
     c.g = c.bg % Hkv;
@@ -69,7 +69,7 @@ __device__ __forceinline__ bool tile_ctx(const int32_t* blk_arr, const int32_t* 
     bool any = false;
     for (int h = 0; h < G; ++h) {
         const int32_t kk = kblocks[c.head0 + h];
-        any |= (kk > 0 && kk < c.nblk);  // k = 0 or k >= nblk needs no ranking
+        any |= (kk > 0 && (rank_all || kk < c.nblk));  // k = 0 or k >= nblk needs no ranking
     }
     return any;
 }
@@ -117,7 +117,7 @@ __device__ __forceinline__ int level_of(int blk) { return blk == 16 ? 0 : blk ==
 // items of group bg (0: streaming, or no head needs ranking); blk and the
 // G per-head k load together (one round trip)
 __device__ __forceinline__ int group_items(const int32_t* blk_arr, const int32_t* kblocks, int bg,
-                                           int G, int64_t l_cpu, int* blk_out) {
+                                           int G, int64_t l_cpu, int* blk_out, int rank_all) {
     int32_t kk[8];
 #pragma unroll
     for (int h = 0; h < 8; ++h) kk[h] = h < G ? __ldg(kblocks + (int64_t)bg * G + h) : 0;
@@ -127,7 +127,7 @@ __device__ __forceinline__ int group_items(const int32_t* blk_arr, const int32_t
     const int64_t nblk = cdiv_dev(l_cpu, blk);
     bool any = false;
 #pragma unroll
-    for (int h = 0; h < 8; ++h) any |= (kk[h] > 0 && kk[h] < nblk);  // k = 0 or >= nblk: no ranking
+    for (int h = 0; h < 8; ++h) any |= (kk[h] > 0 && (rank_all || kk[h] < nblk));  // k = 0 or >= nblk: no ranking
     return any ? (int)cdiv_dev(nblk, kSRows) : 0;
 }
 
@@ -135,7 +135,7 @@ template <int D>
 __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     const __grid_constant__ MetaMaps maps, const float* __restrict__ q,
     const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int n_bg, int G,
-    int64_t l_cpu, float* __restrict__ approx, int64_t stride) {
+    int64_t l_cpu, float* __restrict__ approx, int64_t stride, int rank_all) {
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) { SC_MARK(0) }
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     for (int c0 = 0; c0 < n_bg; c0 += kSThreads) {
         const int i = c0 + tid;
         int bv = 0;
-        const int v = i < n_bg ? group_items(blk_arr, kblocks, i, G, l_cpu, &bv) : 0;
+        const int v = i < n_bg ? group_items(blk_arr, kblocks, i, G, l_cpu, &bv, rank_all) : 0;
         if (i < n_bg) s_blk[i] = bv;
         int x = v;
 #pragma unroll
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const 
                                                            const int32_t* __restrict__ kblocks,
                                                            int Hkv, int64_t l_cpu,
                                                            float* __restrict__ approx,
-                                                           int64_t stride) {
+                                                           int64_t stride, int rank_all) {
     pdl_wait();
     pdl_trigger();
     constexpr int LPR = D / 4;  // lanes per block row pair (4 dims per lane)
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const 
     constexpr int GP = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8;
     static_assert(GP <= LPR, "group too wide for the lane split");
     TileCtx c;
-    if (!tile_ctx(blk_arr, kblocks, Hkv, G, l_cpu, c)) return;
+    if (!tile_ctx(blk_arr, kblocks, Hkv, G, l_cpu, c, rank_all)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int col = (lane % LPR) * 4;
     const float* base = static_cast<const float*>(level_ptr(meta.p, c.blk)) + (int64_t)c.bg * c.nblk * 2 * D;
@@ -430,11 +430,11 @@ __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const 
 template <int D>
 void launch_f32(const fx_layout& L, MetaPtrs mp, const float* q, const int32_t* blk,
                 const int32_t* kblocks, float* approx, int64_t stride, dim3 grid,
-                cudaStream_t s) {
+                cudaStream_t s, int rank_all) {
 #define FX_G(GG)                                                                                \
     case GG:                                                                                    \
         launch_pdl(k_approx_scores_f32<D, GG>, grid, 256, 0, s, mp, q, blk, kblocks, L.kv_heads,       \
-                                                        L.l_cpu, approx, stride);               \
+                                                        L.l_cpu, approx, stride, rank_all);     \
         break;
     switch (L.group_size) {
         FX_G(1) FX_G(2) FX_G(3) FX_G(4) FX_G(5) FX_G(6) FX_G(7) FX_G(8)
@@ -446,7 +446,7 @@ void launch_f32(const fx_layout& L, MetaPtrs mp, const float* q, const int32_t* 
 template <int D>
 void launch_score_tma(const fx_layout& L, const void* const meta[4], const float* q,
                       const int32_t* blk, const int32_t* kblocks, float* approx, int64_t stride,
-                      int num_sms, cudaStream_t s) {
+                      int num_sms, cudaStream_t s, int rank_all) {
     const int n_bg = L.batch * L.kv_heads;
     FX_REQUIRE(n_bg <= kMaxScoreGroups, FX_ERR_INVALID, "bad-shape: more than 4096 (b, g) groups");
     MetaMaps maps;
@@ -457,7 +457,7 @@ void launch_score_tma(const fx_layout& L, const void* const meta[4], const float
     const size_t smem = ScoreCfg<D>::TOTAL;
     FX_CUDA(cudaFuncSetAttribute(k_score_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(k_score_tma<D>, (unsigned)std::max(1, num_sms), kSThreads, smem, s, maps, q, blk,
-               kblocks, n_bg, L.group_size, L.l_cpu, approx, stride);
+               kblocks, n_bg, L.group_size, L.l_cpu, approx, stride, rank_all);
 }
 
 }  // namespace
@@ -468,7 +468,7 @@ double approx_eps_scale(const fx_layout& L) {
 
 void launch_approx_scores(const fx_layout& L, const void* const meta[4], const float* q,
                           const int32_t* blk, const int32_t* kblocks, float* approx,
-                          int64_t approx_stride, int num_sms, cudaStream_t s) {
+                          int64_t approx_stride, int num_sms, cudaStream_t s, bool rank_all) {
     MetaPtrs mp{{meta[0], meta[1], meta[2], meta[3]}};
     const int D = L.head_dim;
     FX_REQUIRE(L.group_size <= 8, FX_ERR_INVALID, "bad-shape: group_size must be <= 8");
@@ -476,11 +476,11 @@ void launch_approx_scores(const fx_layout& L, const void* const meta[4], const f
                     (unsigned)(L.batch * L.kv_heads));
     const int n_bg = L.batch * L.kv_heads;
     if (L.dtype == FX_BF16 && D == 128)
-        launch_score_tma<128>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s);
+        launch_score_tma<128>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s, rank_all);
     else if (L.dtype == FX_BF16 && D == 64)
-        launch_score_tma<64>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s);
-    else if (L.dtype == FX_F32 && D == 128) launch_f32<128>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s);
-    else if (L.dtype == FX_F32 && D == 64) launch_f32<64>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s);
+        launch_score_tma<64>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s, rank_all);
+    else if (L.dtype == FX_F32 && D == 128) launch_f32<128>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s, rank_all);
+    else if (L.dtype == FX_F32 && D == 64) launch_f32<64>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s, rank_all);
     else fail(FX_ERR_INVALID, "bad-shape: batched scoring supports head_dim 64 or 128");
     FX_CUDA(cudaGetLastError());
 }

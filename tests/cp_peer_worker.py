@@ -9,11 +9,11 @@ import numpy as np
 import torch
 
 
-def run(rank, world, port, out_dir):
+def run(rank, world, port, out_dir, protocol="candidates"):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch.distributed as dist
-    from paper_2605_07719_b200.context_parallel import (PeerShard, PeerTables, cp_decode_step_peer,
-                                                        shard_kv)
+    from paper_2605_07719_b200.context_parallel import (PeerShard, PeerTables, cp_decode_step_dist,
+                                                        cp_decode_step_peer, shard_kv)
     from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     eng = Engine(0)
@@ -35,7 +35,8 @@ def run(rank, world, port, out_dir):
         qq = torch.roll(q, stamp, dims=-1)
         o_ref, lse_ref = full.step(qq, fixed=(16, 0.1))
         o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
-        (o, lse), = cp_decode_step_peer([sh], tables, qq, stamp, fixed=(16, 0.1))
+        step = cp_decode_step_dist if protocol == "dist" else cp_decode_step_peer
+        (o, lse), = step([sh], tables, qq, stamp, fixed=(16, 0.1))
         torch.cuda.synchronize()
         torch.testing.assert_close(o, o_ref, rtol=4e-3, atol=4e-3)
         torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)

@@ -180,6 +180,76 @@ def test_cp_peer_exchange_matches_single_device(engine, R, name, plan):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("name,plan", PLANS)
+def test_cp_dist_bracket_matches_single_device(engine, R, name, plan):
+    """The bracket selection distributed over the ranks (stats -> summed
+    histograms -> exact-scored bands -> global ranks) selects the
+    single-device blocks bit for bit, over three steps (both parities)."""
+    from paper_2605_07719_b200.context_parallel import cp_decode_step_dist
+    B, Hkv, G, D = 2, 2, 4, 128
+    full, peers, tables, q = _peer_shards(engine, R, B, Hkv, G, D, 64, 5000 + 37, 256,
+                                          seed=R * 13 + len(name))
+    if plan == "props":
+        bgt0, ks, st = head_props(B, Hkv * G, seed=R + 1)
+        plan = dict(props=tuple(torch.as_tensor(x, device=engine.device) for x in (bgt0, ks, st)))
+    for stamp in (1, 2, 3):
+        qq = torch.roll(q, stamp - 1, dims=-1)
+        o_ref, lse_ref = full.step(qq, **plan)
+        o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
+        (o, lse), *_ = cp_decode_step_dist(peers, tables, qq, stamp, **plan)
+        torch.cuda.synchronize()
+        for b in range(B):
+            for h in range(Hkv * G):
+                want = full.selected_blocks(b, h)
+                got = np.sort(np.concatenate([sh.global_selection(b, h) for sh in peers]))
+                assert np.array_equal(got, want), (stamp, b, h, len(got), len(want))
+        torch.testing.assert_close(o, o_ref, rtol=BF16_TOL, atol=BF16_TOL)
+        torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_cp_dist_bracket_ties_and_mixed_protocols(engine):
+    """Every block duplicated across the shards (the whole shard is the band):
+    ties resolve to the lower global id; then the candidate protocol and the
+    bracket protocol alternate on the same tables without a stale flag."""
+    from paper_2605_07719_b200.context_parallel import (PeerShard, PeerTables, cp_decode_step_dist,
+                                                        cp_decode_step_peer, shard_kv)
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    B, Hkv, G, D, R = 1, 1, 4, 64, 4
+    l_sink, l_cpu, l_local = 64, 4096, 256
+    dev = engine.device
+    cap = SparseDecoder.cap_rows(l_sink + l_cpu + l_local, 4)
+    base = torch.randn((1, 1, 128, D), device=dev).to(torch.bfloat16)
+    k = base.repeat(1, 1, cap // 128 + 1, 1)[:, :, :cap].contiguous()
+    v = torch.randn((B, Hkv, cap, D), device=dev).to(torch.bfloat16)
+    full = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16", k=k, v=v)
+    full.build_metadata()
+    peers = []
+    for r in range(R):
+        sh = PeerShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16",
+                       k=shard_kv(k, l_sink, l_cpu, l_local, r, R, 4),
+                       v=shard_kv(v, l_sink, l_cpu, l_local, r, R, 4))
+        sh.dec.build_metadata()
+        peers.append(sh)
+    tables = PeerTables(engine, R)
+    for s in peers:
+        tables.add_local(s)
+    q = torch.randn((B, Hkv * G, D), device=dev)
+    for stamp, fn in ((1, cp_decode_step_dist), (2, cp_decode_step_peer), (3, cp_decode_step_dist)):
+        qq = torch.roll(q, stamp, dims=-1)
+        o_ref, lse_ref = full.step(qq, fixed=(64, 0.2))
+        o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
+        (o, lse), *_ = fn(peers, tables, qq, stamp, fixed=(64, 0.2))
+        torch.cuda.synchronize()
+        for h in range(G):
+            want = full.selected_blocks(0, h)
+            got = np.sort(np.concatenate([sh.global_selection(0, h) for sh in peers]))
+            assert np.array_equal(got, want), (stamp, h)
+        torch.testing.assert_close(o, o_ref, rtol=BF16_TOL, atol=BF16_TOL)
+
+
+@pytest.mark.gpu
 def test_cp_peer_exchange_two_processes(tmp_path):
     """Two processes, one rank each, on one GPU: the tables cross the process
     boundary through CUDA IPC and the kernels synchronise on each other's
@@ -189,4 +259,16 @@ def test_cp_peer_exchange_two_processes(tmp_path):
     import cp_peer_worker
     port = random.randint(20000, 40000)
     mp.spawn(cp_peer_worker.run, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    assert (tmp_path / "ok0").exists() and (tmp_path / "ok1").exists()
+
+
+@pytest.mark.gpu
+def test_cp_dist_bracket_two_processes(tmp_path):
+    """The distributed bracket selection across a process boundary: stats,
+    histograms and bands read through CUDA IPC after the peers' flags."""
+    import random
+    import torch.multiprocessing as mp
+    import cp_peer_worker
+    port = random.randint(20000, 40000)
+    mp.spawn(cp_peer_worker.run, args=(2, port, str(tmp_path), "dist"), nprocs=2, join=True)
     assert (tmp_path / "ok0").exists() and (tmp_path / "ok1").exists()
