@@ -54,7 +54,7 @@ def args_parse():
     ap.add_argument("--data", default="reference", choices=["reference", "normal"],
                     help="reference: the reference generator's workload (generate(spec), on "
                          "device); normal: plain N(0,1) K/V")
-    ap.add_argument("--cp-exchange", default="peer", choices=["peer", "collective"],
+    ap.add_argument("--cp-exchange", default="dist", choices=["dist", "peer", "collective"],
                     help="c5 exchanges: peer-memory one-shot kernels, or torch.distributed "
                          "all-gathers (NCCL)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
@@ -297,16 +297,18 @@ def run_c5(a):
         full.build_metadata()
         dec, shards, comm = full, None, None
     else:
-        from paper_2605_07719_b200.context_parallel import PeerShard, PeerTables, cp_decode_step_peer
+        from paper_2605_07719_b200.context_parallel import (PeerShard, PeerTables, cp_decode_step_dist,
+                                                            cp_decode_step_peer)
+        peer = a.cp_exchange in ("peer", "dist")
         kr = shard_kv(full.k, L_SINK, l_cpu, L_LOCAL, rank, world, total)
         vr = shard_kv(full.v, L_SINK, l_cpu, L_LOCAL, rank, world, total)
         del full
         torch.cuda.empty_cache()
-        cls = PeerShard if a.cp_exchange == "peer" else CPShard
+        cls = PeerShard if peer else CPShard
         sh = cls(eng, rank, world, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, total, "bf16", k=kr, v=vr)
         sh.dec.build_metadata()
         dec, shards = sh.dec, [sh]
-        comm = PeerTables.over_dist(eng, sh) if a.cp_exchange == "peer" else TorchComm()
+        comm = PeerTables.over_dist(eng, sh) if peer else TorchComm()
     step_i = [0]
 
     def one_step():
@@ -315,7 +317,9 @@ def run_c5(a):
             dec.step(qs[i], props=props)
             dec.append(nk[i], nv[i])
         else:
-            if a.cp_exchange == "peer":
+            if a.cp_exchange == "dist":
+                cp_decode_step_dist(shards, comm, qs[i], i + 1, props=props)
+            elif a.cp_exchange == "peer":
                 cp_decode_step_peer(shards, comm, qs[i], i + 1, props=props)
             else:
                 cp_decode_step(shards, comm, qs[i], props=props)
@@ -356,7 +360,11 @@ def run_c5(a):
                                    "plan_group over the whole sequence",
                        "context": ctx, "global_batch": B, "seq_len": ctx,
                        "parallelism": "single device" if world == 1 else
-                       (f"context-parallel x{world}, one-shot exchanges over peer memory (CUDA IPC "
+                       (f"context-parallel x{world}, the selection bracket distributed over peer "
+                        f"memory (score ranges, summed histograms, exact-scored bands; CUDA IPC "
+                        f"tables, flag waits in the kernels)"
+                        if a.cp_exchange == "dist" else
+                        f"context-parallel x{world}, one-shot exchanges over peer memory (CUDA IPC "
                         f"tables, flag waits in the select / combine kernels)"
                         if a.cp_exchange == "peer" else
                         f"context-parallel x{world} (all-gathers of k-th keys, candidates, "

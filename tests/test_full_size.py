@@ -202,7 +202,8 @@ def test_c5_full_size_context_parallel(engine, coracle):
     """C5: 1M context, batch 4, 8 context-parallel shards -> the single-device
     selection bit-exactly, outputs within the bf16 bound; one group checked
     against the oracle at 1M."""
-    from paper_2605_07719_b200.context_parallel import CPShard, LoopbackComm, cp_decode_step, shard_kv
+    from paper_2605_07719_b200.context_parallel import (LoopbackComm, PeerShard, PeerTables, cp_decode_step,
+                                                        cp_decode_step_dist, shard_kv)
     B, Hkv, G, D, R = 4, 8, 4, 128, 8
     l_sink, l_cpu, l_local = 64, 1048576 - 320, 256
     full = _decoder(engine, B, Hkv, G, D, l_cpu, seed=41, max_new=4)
@@ -210,27 +211,36 @@ def test_c5_full_size_context_parallel(engine, coracle):
     for r in range(R):
         kr = shard_kv(full.k, l_sink, l_cpu, l_local, r, R, 4)
         vr = shard_kv(full.v, l_sink, l_cpu, l_local, r, R, 4)
-        sh = CPShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16", k=kr, v=vr)
+        sh = PeerShard(engine, r, R, B, Hkv, G, D, l_sink, l_cpu, l_local, 4, "bf16", k=kr, v=vr)
         sh.dec.build_metadata()
         shards.append(sh)
+    tables = PeerTables(engine, R)
+    for sh in shards:
+        tables.add_local(sh)
     props = _draw_props(B, Hkv * G, seed=5)
     dprops = tuple(torch.as_tensor(x, device=engine.device) for x in props)
     q = _queries(B, Hkv * G, D, seed=9, dev=engine.device)
     o_ref, lse_ref = full.step(q, props=dprops)
     torch.cuda.synchronize()
     o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
-    for sh in shards:
-        sh.o.fill_(float("nan"))
-    (o, lse), *_ = cp_decode_step(shards, LoopbackComm(R), q, props=dprops)
-    torch.cuda.synchronize()
-    assert torch.isfinite(o_ref).all() and torch.isfinite(o).all() and not torch.isnan(lse).any()
-    for b in range(B):
-        for h in range(Hkv * G):
-            want = full.selected_blocks(b, h)
-            got = np.sort(np.concatenate([sh.global_selection(b, h) for sh in shards]))
-            assert np.array_equal(got, want), (b, h)
-    torch.testing.assert_close(o, o_ref, rtol=4e-3, atol=4e-3)
-    torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
+    # the collective exchanges, then the distributed bracket over peer memory
+    for protocol in ("collective", "dist"):
+        for sh in shards:
+            sh.o.fill_(float("nan"))
+            sh.sel.fill_(-1)
+        if protocol == "collective":
+            (o, lse), *_ = cp_decode_step(shards, LoopbackComm(R), q, props=dprops)
+        else:
+            (o, lse), *_ = cp_decode_step_dist(shards, tables, q, 1, props=dprops)
+        torch.cuda.synchronize()
+        assert torch.isfinite(o_ref).all() and torch.isfinite(o).all() and not torch.isnan(lse).any()
+        for b in range(B):
+            for h in range(Hkv * G):
+                want = full.selected_blocks(b, h)
+                got = np.sort(np.concatenate([sh.global_selection(b, h) for sh in shards]))
+                assert np.array_equal(got, want), (protocol, b, h)
+        torch.testing.assert_close(o, o_ref, rtol=4e-3, atol=4e-3)
+        torch.testing.assert_close(lse, lse_ref, rtol=1e-4, atol=1e-3)
     _check_plans(full, coracle, props)
     _check_groups(full, coracle, q, _retrieval_groups(full, 1))
 
