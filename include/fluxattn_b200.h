@@ -394,7 +394,7 @@ typedef struct fx_cp_peer {
     int64_t cap;
     const double* stats;    /* [n][4] approx-score min, max, error bound, non-finite (bracket protocol) */
     const int32_t* hist;    /* [n][2048] approx-score histogram over the global range */
-    const int32_t* defc;    /* [n] blocks certainly in the top-k */
+    const int32_t* defc;    /* [n][2] blocks certainly in the top-k, band length */
 } fx_cp_peer;
 /* flags[slot] = stamp after every prior op of the stream is visible system-wide. */
 FX_API int fx_cp_signal(fx_ctx* ctx, uint64_t* flags, int32_t slot, uint64_t stamp);
@@ -412,8 +412,9 @@ FX_API int fx_cp_select_peer(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, i
  *   1  wait stats of all ranks; histogram of the local scores over the global
  *      range -> own hist; (signal 1)
  *   2  wait hists; the summed histogram brackets the global k-th score: blocks
- *      above it -> sel_out bits, count -> own defc; the band is exact-scored and
- *      sorted (score desc, id asc) -> own keys / ids; (signal 2)
+ *      above it -> sel_out bits, their count and the band length -> own defc;
+ *      the band is exact-scored and sorted (score desc, id asc) -> own keys /
+ *      ids; (signal 2)
  *   3  wait bands; global rank of each own band entry among all ranks' bands,
  *      bits for rank < k - sum(defc).
  * args: the shard's step arguments (q, meta, absmax, plan, l_cpu_total,

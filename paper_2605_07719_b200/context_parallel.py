@@ -260,7 +260,7 @@ class PeerShard(CPShard):
                 lse=torch.zeros((B, H), dtype=torch.float32, device=dev),
                 stats=torch.zeros((nh, 4), dtype=torch.float64, device=dev),
                 hist=torch.zeros((nh, DIST_BINS), dtype=torch.int32, device=dev),
-                defc=torch.zeros(nh, dtype=torch.int32, device=dev)))
+                defc=torch.zeros((nh, 2), dtype=torch.int32, device=dev)))
         # [parity][slot]: 0 candidates / stats, 1 histograms, 2 bands, 3 partials
         self.flags = torch.zeros((2, 4), dtype=torch.int64, device=dev)
         self.approx = None  # [nh][cap] f32, the bracket protocol's local scores

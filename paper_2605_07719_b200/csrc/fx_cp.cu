@@ -613,42 +613,76 @@ __global__ void __launch_bounds__(kT) k_cpd_band(const __grid_constant__ PeerSet
             }
     }
     __syncthreads();
-    for (int64_t i = t; i < a.cap; i += kT) {
-        a.keys[head * a.cap + i] = i < nband ? sk[i] : 0ull;
-        a.ids[head * a.cap + i] = i < nband ? si[i] : 0xffffffffu;
+    for (int64_t i = t; i < nband; i += kT) {
+        a.keys[head * a.cap + i] = sk[i];
+        a.ids[head * a.cap + i] = si[i];
     }
-    if (t == 0) a.defc[head] = (int32_t)ndef;
+    if (t == 0) {
+        a.defc[head * 2] = (int32_t)ndef;
+        a.defc[head * 2 + 1] = (int32_t)nband;
+    }
 }
 
-// phase 3: global ranks of the own band entries among all ranks' bands
+// phase 3: global ranks of the own band entries among all ranks' bands.  The
+// peers' bands (sorted, usually tens of entries) are staged in shared memory
+// with one coalesced pass each; a band too large for the stage is searched in
+// place.
+constexpr int kRankStage = 3840;  // entries (12 B each; static smem under 48 KB)
 __global__ void __launch_bounds__(kT) k_cpd_rank(const __grid_constant__ PeerSet ps, const DistArgs a) {
     pdl_wait();
     pdl_trigger();
     wait_peers(ps, a.R, 2, a.stamp);
+    __shared__ uint64_t s_k[kRankStage];
+    __shared__ uint32_t s_i[kRankStage];
+    __shared__ int s_off[FX_CP_MAX_RANKS + 1];
+    __shared__ int s_len[FX_CP_MAX_RANKS];
     const int64_t head = blockIdx.x;
     const int t = threadIdx.x;
     const HeadInfo hi = head_info(a, head);
     if (hi.blk <= 0 || hi.k <= 0 || hi.k >= hi.nblk_total) return;
+    if (t == 0) {
+        int off = 0;
+        for (int r = 0; r < a.R; ++r) {
+            const int n = ps.p[r].defc[head * 2 + 1];
+            s_len[r] = n;
+            s_off[r] = off;
+            off += (r != a.self && off + n <= kRankStage) ? n : 0;  // staged, or searched in place
+        }
+        s_off[a.R] = off;
+    }
+    __syncthreads();
     int64_t need = hi.k;
-    for (int r = 0; r < a.R; ++r) need -= ps.p[r].defc[head];
+    for (int r = 0; r < a.R; ++r) need -= ps.p[r].defc[head * 2];
+    for (int r = 0; r < a.R; ++r) {
+        const int n = s_off[r + 1] - s_off[r];
+        const uint64_t* kr = ps.p[r].keys + head * ps.p[r].cap;
+        const uint32_t* ir = ps.p[r].ids + head * ps.p[r].cap;
+        for (int j = t; j < n; j += kT) {
+            s_k[s_off[r] + j] = kr[j];
+            s_i[s_off[r] + j] = ir[j];
+        }
+    }
+    __syncthreads();
     uint32_t* bits = a.sel + head * a.sel_words;
     const int64_t off_blk = a.cpu_offset / hi.blk;
     const fx_cp_peer& me = ps.p[a.self];
     const uint64_t* own_k = me.keys + head * me.cap;
     const uint32_t* own_i = me.ids + head * me.cap;
-    for (int64_t j = t; j < me.cap; j += kT) {
+    const int own_n = s_len[a.self];
+    for (int64_t j = t; j < own_n; j += kT) {
         const uint64_t ke = own_k[j];
-        if (ke == 0) break;  // end of the band (sorted, zero-padded)
         const uint32_t ie = own_i[j];
         int64_t rank = j;
         for (int r = 0; r < a.R && rank < need; ++r) {
             if (r == a.self) continue;
-            const uint64_t* kr = ps.p[r].keys + head * ps.p[r].cap;
-            const uint32_t* ir = ps.p[r].ids + head * ps.p[r].cap;
-            int64_t lo = 0, hi2 = ps.p[r].cap;
+            const int n = s_len[r];
+            const bool staged = s_off[r + 1] - s_off[r] == n;
+            const uint64_t* kr = staged ? s_k + s_off[r] : ps.p[r].keys + head * ps.p[r].cap;
+            const uint32_t* ir = staged ? s_i + s_off[r] : ps.p[r].ids + head * ps.p[r].cap;
+            int lo = 0, hi2 = n;
             while (lo < hi2) {
-                const int64_t mid = (lo + hi2) >> 1;
-                if (kr[mid] != 0 && first_of(kr[mid], ir[mid], ke, ie)) lo = mid + 1;
+                const int mid = (lo + hi2) >> 1;
+                if (first_of(kr[mid], ir[mid], ke, ie)) lo = mid + 1;
                 else hi2 = mid;
             }
             rank += lo;

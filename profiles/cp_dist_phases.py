@@ -2,7 +2,8 @@
 import json, sys
 import ctypes as C
 import torch
-sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
 from paper_2605_07719_b200.context_parallel import PeerShard, PeerTables, shard_kv

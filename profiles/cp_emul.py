@@ -5,7 +5,8 @@ shards run one after another, so this is the protocol's serial cost, not an
 8-GPU number."""
 import json, sys, time
 import torch
-sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
 from paper_2605_07719_b200.context_parallel import (CPShard, PeerShard, PeerTables, LoopbackComm,
                                                     cp_decode_step, cp_decode_step_peer, cp_decode_step_dist, shard_kv)
