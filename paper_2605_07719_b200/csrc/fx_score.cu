@@ -227,6 +227,10 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
                     ph ^= 1u;
                 }
             }
+            SC_MARK(4)
+#ifdef FX_TRACE
+            g_score_trace[blockIdx.x * 8 + 5] = i1 - i0;
+#endif
             mbar_wait(empty + st, ph ^ 1u);
             hdr[st].end = 1;
             mbar_arrive(full + st);
