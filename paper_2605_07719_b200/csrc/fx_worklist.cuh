@@ -102,6 +102,62 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
         const int64_t last = nblk - 1;
         const int nb_last = (int)cdiv_dev(w.l_cpu - last * blk, kBoxRows);
         const uint32_t* hg = w.sel_bits + ((int64_t)b * w.Hkv * G + (int64_t)g * G) * w.sel_words;
+        if (W <= nt) {
+            // one word per thread: the head words stay in registers from the
+            // count to the emit (one L2 round trip), two-level shuffle scan
+            const int j = t;
+            uint32_t x[16];
+            uint32_t u = 0;
+#pragma unroll
+            for (int h = 0; h < 16; ++h) {
+                x[h] = (h < G && j < W) ? __ldcg(hg + (int64_t)h * w.sel_words + j) : 0u;
+                u |= x[h];
+            }
+            int c = __popc(u) * bpb;
+            if ((last >> 5) == j && ((u >> (last & 31)) & 1u)) c -= bpb - nb_last;
+            WL_MARK(12);
+            const int lane = t & 31, warp = t >> 5;
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) wcnt[warp] = inc;
+            __syncthreads();
+            int base = 0, tot = 0;
+            for (int q = 0; q < nt / 32; ++q) {
+                const int v = wcnt[q];
+                base += q < warp ? v : 0;
+                tot += v;
+            }
+            __syncthreads();  // wcnt is reused by the caller
+            total += tot;
+            WL_MARK(13);
+            int64_t o = nd + base + inc - c;
+            while (u) {
+                const int l = __ffs(u) - 1;
+                u &= u - 1;
+                uint32_t m = 0;
+#pragma unroll
+                for (int h = 0; h < 16; ++h) m |= ((x[h] >> l) & 1u) << h;
+                const int r0 = (j * 32 + l) * blk;
+                const int len = min(blk, (int)(w.l_cpu - r0));
+                const int nb = (len + kBoxRows - 1) >> 4;
+                const int row0 = (int)w.l_sink + r0;
+                for (int y = 0; y < nb; ++y) {
+                    Box bx;
+                    bx.row = row0 + y * kBoxRows;
+                    bx.n = (uint16_t)min(kBoxRows, len - y * kBoxRows);
+                    bx.mask = (uint16_t)m;
+                    out[o + y] = bx;
+                }
+                o += nb;
+            }
+            WL_MARK(14);
+            if (t == 0) w.bg_count[bg] = (int32_t)total;
+            return;
+        }
         for (int j = t; j < W; j += nt) {
             uint32_t u = 0;
             for (int h = 0; h < G; ++h) u |= __ldcg(hg + (int64_t)h * w.sel_words + j);
