@@ -386,6 +386,7 @@ int fx_ctx_destroy(fx_ctx* ctx) {
         for (auto e : ctx->pool) cudaEventDestroy(e);
         ctx->step.release();
         ctx->api.release();
+        ctx->label.release();
         if (ctx->own) cudaStreamDestroy(ctx->own);
         delete ctx;
     });

@@ -458,6 +458,34 @@ __global__ void __launch_bounds__(kT) k_cpd_hist(const __grid_constant__ PeerSet
 }
 
 // phase 2: bracket from the summed histogram; definite bits; exact, sorted band
+// Bitonic sort of n entries (score desc, id asc) in the "flip" form: every
+// stage sorts ascending and its first step pairs i with the mirror i ^ (kk - 1),
+// so a pair always has its larger index on the later side and the virtual
+// entries past n (+inf) never move -- no padding to a power of two.  Shared or
+// global memory, one CTA.
+__device__ void sort_band(uint64_t* k, uint32_t* id, int64_t n) {
+    int64_t len = 1;
+    while (len < n) len <<= 1;
+    for (int64_t kk = 2; kk <= len; kk <<= 1)
+        for (int64_t j = kk >> 1; j > 0; j >>= 1) {
+            const int64_t m = j == (kk >> 1) ? kk - 1 : j;
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                if (i & j) continue;
+                const int64_t p2 = i ^ m;
+                if (p2 >= n) continue;
+                const uint64_t x1 = k[i], x2 = k[p2];
+                const uint32_t i1 = id[i], i2 = id[p2];
+                if (first_of(x2, i2, x1, i1)) {
+                    k[i] = x2;
+                    k[p2] = x1;
+                    id[i] = i2;
+                    id[p2] = i1;
+                }
+            }
+            __syncthreads();
+        }
+}
+
 template <int DT>
 __global__ void __launch_bounds__(kT) k_cpd_band(const __grid_constant__ PeerSet ps, const DistArgs a) {
     pdl_wait();
@@ -465,8 +493,10 @@ __global__ void __launch_bounds__(kT) k_cpd_band(const __grid_constant__ PeerSet
     wait_peers(ps, a.R, 1, a.stamp);
     using T = typename Elem<DT>::T;
     extern __shared__ __align__(16) unsigned char dsm[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(dsm);
-    uint32_t* si = reinterpret_cast<uint32_t*>(sk + a.sort_n);
+    uint64_t* s_k = reinterpret_cast<uint64_t*>(dsm);  // the band when it fits (a.sort_n entries)
+    uint32_t* s_i = reinterpret_cast<uint32_t*>(s_k + a.sort_n);
+    uint64_t* sk = s_k;
+    uint32_t* si = s_i;
     __shared__ int hist[kDBins];
     __shared__ int s_cnt[2][kT / 32];
     __shared__ int s_bin;
@@ -553,16 +583,20 @@ __global__ void __launch_bounds__(kT) k_cpd_band(const __grid_constant__ PeerSet
             nband += s_cnt[1][w];
             if (w < warp) base += s_cnt[1][w];
         }
+        // a band larger than the shared stage (degenerate data: ties, NaN)
+        // is built and sorted in place in the own table row (cap >= nblk)
+        const bool big = nband > a.sort_n;
+        if (big) {
+            sk = a.keys + head * a.cap;
+            si = a.ids + head * a.cap;
+        }
         for (int j = warp; j < W; j += kT / 32) {
             const int64_t i = (int64_t)j * 32 + lane;
             const bool in = i < hi.nblk_local;
             const double x = in ? (double)sc[i] : 0.0;
             const bool cand = in && !(x > up) && x >= lo;
             const uint32_t bc = __ballot_sync(0xffffffffu, cand);
-            if (cand) {
-                const int64_t pos = base + __popc(bc & ((1u << lane) - 1u));
-                if (pos < a.sort_n) si[pos] = (uint32_t)i;
-            }
+            if (cand) si[base + __popc(bc & ((1u << lane) - 1u))] = (uint32_t)i;
             base += __popc(bc);
         }
         for (int d = t; d < a.D; d += kT) s_q[d] = (double)a.q[head * a.D + d];
@@ -571,52 +605,29 @@ __global__ void __launch_bounds__(kT) k_cpd_band(const __grid_constant__ PeerSet
         const T* mbase = static_cast<const T*>(a.meta.p[hi.blk == 16 ? 0 : hi.blk == 32 ? 1 : hi.blk == 64 ? 2 : 3]) +
                          bgi * hi.nblk_local * 2 * a.D;
         const int64_t off_blk = a.cpu_offset / hi.blk;
-        int len = 32;
-        while (len < nband) len <<= 1;
-        for (int i = t; i < len; i += kT) {
-            if (i < nband) {
-                const uint32_t id = si[i];
-                const T* row = mbase + (int64_t)id * 2 * a.D;
-                double v;
-                if constexpr (DT == FX_BF16) {
-                    v = a.D == 128 ? exact_score_row<128>(s_q, row)
-                      : a.D == 64  ? exact_score_row<64>(s_q, row)
-                                   : exact_score(a.q + head * a.D, row, row + a.D, a.D);
-                } else {
-                    v = exact_score(a.q + head * a.D, row, row + a.D, a.D);
-                }
-                sk[i] = f64_key(v);
-                si[i] = (uint32_t)(id + off_blk);
+        for (int64_t i = t; i < nband; i += kT) {
+            const uint32_t id = si[i];
+            const T* row = mbase + (int64_t)id * 2 * a.D;
+            double v;
+            if constexpr (DT == FX_BF16) {
+                v = a.D == 128 ? exact_score_row<128>(s_q, row)
+                  : a.D == 64  ? exact_score_row<64>(s_q, row)
+                               : exact_score(a.q + head * a.D, row, row + a.D, a.D);
             } else {
-                sk[i] = 0;
-                si[i] = 0xffffffffu;
+                v = exact_score(a.q + head * a.D, row, row + a.D, a.D);
             }
+            sk[i] = f64_key(v);
+            si[i] = (uint32_t)(id + off_blk);
         }
         __syncthreads();
-        for (int kk = 2; kk <= len; kk <<= 1)
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int i = t; i < len; i += kT) {
-                    const int p2 = i ^ j;
-                    if (p2 > i) {
-                        const bool upd = (i & kk) == 0;
-                        const uint64_t x1 = sk[i], x2 = sk[p2];
-                        const uint32_t i1 = si[i], i2 = si[p2];
-                        if (upd ? first_of(x2, i2, x1, i1) : first_of(x1, i1, x2, i2)) {
-                            sk[i] = x2;
-                            sk[p2] = x1;
-                            si[i] = i2;
-                            si[p2] = i1;
-                        }
-                    }
-                }
-                __syncthreads();
-            }
+        sort_band(sk, si, nband);
     }
     __syncthreads();
-    for (int64_t i = t; i < nband; i += kT) {
-        a.keys[head * a.cap + i] = sk[i];
-        a.ids[head * a.cap + i] = si[i];
-    }
+    if (sk == s_k)
+        for (int64_t i = t; i < nband; i += kT) {
+            a.keys[head * a.cap + i] = sk[i];
+            a.ids[head * a.cap + i] = si[i];
+        }
     if (t == 0) {
         a.defc[head * 2] = (int32_t)ndef;
         a.defc[head * 2 + 1] = (int32_t)nband;
@@ -731,7 +742,7 @@ void launch_cp_dist_phase(const fx_layout& L, int phase, int R, int self, const 
     a.sel = sel;
     a.sel_words = sel_words;
     a.cap = me.cap;
-    a.sort_n = cp_sort_n(std::max<int64_t>(1, me.cap));
+    a.sort_n = (int)std::min<int64_t>(cp_sort_n(std::max<int64_t>(1, me.cap)), 4096);
     a.stats = const_cast<double*>(me.stats);
     a.hist = const_cast<int32_t*>(me.hist);
     a.keys = const_cast<uint64_t*>(me.keys);
@@ -745,9 +756,7 @@ void launch_cp_dist_phase(const fx_layout& L, int phase, int R, int self, const 
     } else if (phase == 1) {
         launch_pdl(k_cpd_hist, (unsigned)n, kT, 0, s, ps, a);
     } else if (phase == 2) {
-        const size_t smem = (size_t)a.sort_n * 12;
-        FX_REQUIRE(smem <= 200 * 1024, FX_ERR_INVALID,
-                   "bad-shape: context-parallel shard too long (more than 16384 blocks of 16)");
+        const size_t smem = (size_t)a.sort_n * 12;  // larger bands sort in the own table row
         if (L.dtype == FX_BF16) {
             FX_CUDA(cudaFuncSetAttribute(k_cpd_band<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             launch_pdl(k_cpd_band<FX_BF16>, (unsigned)n, kT, smem, s, ps, a);

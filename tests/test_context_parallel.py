@@ -209,15 +209,18 @@ def test_cp_dist_bracket_matches_single_device(engine, R, name, plan):
 
 
 @pytest.mark.gpu
-def test_cp_dist_bracket_ties_and_mixed_protocols(engine):
-    """Every block duplicated across the shards (the whole shard is the band):
-    ties resolve to the lower global id; then the candidate protocol and the
-    bracket protocol alternate on the same tables without a stale flag."""
+@pytest.mark.parametrize("R,l_cpu,fixed", [(4, 4096, (64, 0.2)), (2, 140000, (16, 0.2))])
+def test_cp_dist_bracket_ties_and_mixed_protocols(engine, R, l_cpu, fixed):
+    """Every block duplicated across the shards (the whole shard is the band;
+    at 70,000 rows per shard it outgrows the shared-memory stage and sorts in
+    the table row): ties resolve to the lower global id; then the candidate
+    protocol and the bracket protocol alternate on the same tables without a
+    stale flag."""
     from paper_2605_07719_b200.context_parallel import (PeerShard, PeerTables, cp_decode_step_dist,
                                                         cp_decode_step_peer, shard_kv)
     from paper_2605_07719_b200.fluxattn import SparseDecoder
-    B, Hkv, G, D, R = 1, 1, 4, 64, 4
-    l_sink, l_cpu, l_local = 64, 4096, 256
+    B, Hkv, G, D = 1, 1, 4, 64
+    l_sink, l_local = 64, 256
     dev = engine.device
     cap = SparseDecoder.cap_rows(l_sink + l_cpu + l_local, 4)
     base = torch.randn((1, 1, 128, D), device=dev).to(torch.bfloat16)
@@ -238,9 +241,9 @@ def test_cp_dist_bracket_ties_and_mixed_protocols(engine):
     q = torch.randn((B, Hkv * G, D), device=dev)
     for stamp, fn in ((1, cp_decode_step_dist), (2, cp_decode_step_peer), (3, cp_decode_step_dist)):
         qq = torch.roll(q, stamp, dims=-1)
-        o_ref, lse_ref = full.step(qq, fixed=(64, 0.2))
+        o_ref, lse_ref = full.step(qq, fixed=fixed)
         o_ref, lse_ref = o_ref.clone(), lse_ref.clone()
-        (o, lse), *_ = fn(peers, tables, qq, stamp, fixed=(64, 0.2))
+        (o, lse), *_ = fn(peers, tables, qq, stamp, fixed=fixed)
         torch.cuda.synchronize()
         for h in range(G):
             want = full.selected_blocks(0, h)
