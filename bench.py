@@ -107,50 +107,79 @@ def ncu_traffic(kernel, workload="c2"):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML every 5 ms on a
+    side thread during the timed region (plus one sample at each end); the
+    samples also go to gpurun_out/clocks_rank<i>.csv."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+        self.rows = []
+        self.h = None
+        self.thread = None
+
+    def _sample(self):
+        import pynvml as nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except AttributeError:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((time.time(), sm, mx, r))
 
     def start(self):
-        os.makedirs(os.path.dirname(self.path), exist_ok=True)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
         try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            try:  # the NVML device whose PCI bus id matches this CUDA device
+                want = str(torch.cuda.get_device_properties(self.index).pci_bus_id).lower()[-7:]
+                for i in range(nv.nvmlDeviceGetCount()):
+                    h = nv.nvmlDeviceGetHandleByIndex(i)
+                    bid = nv.nvmlDeviceGetPciInfo(h).busId
+                    bid = (bid.decode() if isinstance(bid, bytes) else str(bid)).lower()
+                    if bid.endswith(want):
+                        self.h = h
+                        break
+            except Exception:
+                pass
+            self._sample()
         except Exception:
-            self.proc = None
+            self.h = None
+            return
+        self.stop_ev = threading.Event()
+
+        def loop():
+            while not self.stop_ev.wait(0.005):
+                try:
+                    self._sample()
+                except Exception:
+                    return
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        self.proc.wait()
-        self.f.close()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(max(mx)) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["unsampled"]}
+        self._sample()
+        self.stop_ev.set()
+        self.thread.join()
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        with open(self.path, "w") as f:
+            f.write("time,clocks.sm,clocks.max.sm,clocks_event_reasons\n")
+            for t, sm, mx, r in self.rows:
+                f.write(f"{t:.4f},{sm},{mx},{r:#x}\n")
+        sm = [r[1] for r in self.rows]
+        mx = [r[2] for r in self.rows]
+        reasons = sorted({n for *_, r in self.rows for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "samples": len(sm), "reasons": reasons}
 
 
 # ---------------------------------------------------------------------------
