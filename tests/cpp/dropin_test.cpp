@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fluxattn/attention.hpp"
@@ -164,6 +165,26 @@ int main(int argc, char** argv) {
     for (std::size_t i = 0; i < batched.size(); ++i)
         for (std::size_t h = 0; h < batched[i].head_outputs.size(); ++h)
             EXPECT(batched[i].head_outputs[h] == results[i].head_outputs[h]);
+    // the ops are pure and concurrently callable: four host
+    // threads (each gets its own device context) run every task at once and
+    // must reproduce the single-threaded execute_task bit for bit
+    {
+        std::vector<TaskResult> single;
+        for (const SparseTask& t : queue.tasks()) single.push_back(execute_task(t));
+        std::vector<std::vector<TaskResult>> per(4);
+        std::vector<std::thread> th;
+        for (int w = 0; w < 4; ++w)
+            th.emplace_back([&, w] {
+                for (int rep = 0; rep < 3; ++rep)
+                    for (const SparseTask& t : queue.tasks()) per[w].push_back(execute_task(t));
+            });
+        for (auto& x : th) x.join();
+        for (int w = 0; w < 4; ++w) {
+            EXPECT(per[w].size() == 3 * single.size());
+            for (std::size_t i = 0; i < per[w].size() && i < 3 * single.size(); ++i)
+                EXPECT(per[w][i].head_outputs == single[i % single.size()].head_outputs);
+        }
+    }
     for (std::size_t i = 0; i < results.size(); ++i) {
         const SparseTask& t = queue.tasks()[i];
         EXPECT(results[i].group_id == t.group_id);

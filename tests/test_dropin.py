@@ -16,7 +16,7 @@ def build_dropin(tmp):
     exe = os.path.join(tmp, "dropin_test")
     subprocess.run(["g++", "-std=gnu++20", "-O2", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp"), "-L", LIB_DIR,
-                    "-lfluxattn_b200", f"-Wl,-rpath,{LIB_DIR}", "-o", exe], check=True)
+                    "-lfluxattn_b200", f"-Wl,-rpath,{LIB_DIR}", "-pthread", "-o", exe], check=True)
     return exe
 
 
