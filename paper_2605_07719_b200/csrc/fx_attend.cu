@@ -386,6 +386,12 @@ struct TmaCfg {
 template <int D>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_constant__ KvMaps maps,
                                                        const View p) {
+    // the tensor-map descriptors do not depend on the preceding kernels:
+    // fetch them while those finish
+    if (threadIdx.x == kProducer * 32) {
+        tma_prefetch_desc(&maps.box[0]);
+        tma_prefetch_desc(&maps.box[1]);
+    }
     pdl_wait();
     pdl_trigger();
     using C = TmaCfg<D>;
@@ -417,10 +423,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
 
     if (warp == kProducer) {
         // ------------------------------ producer ------------------------------
-        if (lane == 0) {
-            tma_prefetch_desc(&maps.box[0]);
-            tma_prefetch_desc(&maps.box[1]);
-        }
         int st = 0;
 #ifdef FX_TRACE
         long long p_wait = 0;

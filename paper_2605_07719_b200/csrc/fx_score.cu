@@ -136,6 +136,8 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
     const __grid_constant__ MetaMaps maps, const float* __restrict__ q,
     const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int n_bg, int G,
     int64_t l_cpu, float* __restrict__ approx, int64_t stride, int rank_all) {
+    if (threadIdx.x == kSCWarps * 32)  // descriptors: independent of the preceding kernels
+        for (int l = 0; l < 4; ++l) tma_prefetch_desc(&maps.lvl[l]);
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) { SC_MARK(0) }
@@ -190,7 +192,6 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
         // ------------------------------ producer ------------------------------
         if (lane == 0) {
             SC_MARK(1)
-            for (int l = 0; l < 4; ++l) tma_prefetch_desc(&maps.lvl[l]);
             int st = 0;
             uint32_t ph = 0;
             int bg = 0, cur = -1, lvl = 0;
