@@ -194,8 +194,9 @@ StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
     const size_t o_kb = c.take<int32_t>(heads);
     const size_t o_apx = c.take<float>(heads * ((nblk16 + 3) & ~int64_t(3)));
     const size_t o_bits = c.take<uint32_t>(heads * words);
-    const size_t o_ck = c.take<uint64_t>(heads * nblk16);
-    const size_t o_ci = c.take<uint32_t>(heads * nblk16);
+    // the band lists use the approx row stride (nblk16 rounded up to 4)
+    const size_t o_ck = c.take<uint64_t>(heads * ((nblk16 + 3) & ~int64_t(3)));
+    const size_t o_ci = c.take<uint32_t>(heads * ((nblk16 + 3) & ~int64_t(3)));
     const size_t o_box = c.take<fx::Box>(n_bg * box_stride);
     const size_t o_cnt = c.take<int32_t>(n_bg);
     const size_t o_st = c.take<int32_t>(n_bg + 1);

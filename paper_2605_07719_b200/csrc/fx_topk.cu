@@ -127,6 +127,7 @@ __device__ __forceinline__ void select_head(
     __shared__ float red[2][kNW];
     __shared__ int s_wsum[2][kNW];
     __shared__ int s_bin;
+    __shared__ int s_ncand;
     __shared__ double s_eps;
 
     const int64_t head = blockIdx.x;
@@ -187,6 +188,7 @@ __device__ __forceinline__ void select_head(
         }
     }
     for (int i = t; i < kBins; i += kT) hist[i] = 0;
+    if (t == 0) s_ncand = 0;
     for (int d = t; d < D; d += kT) s_q[d] = (double)qh[d];
     if (warp == 0) {
         double a = 0.0;
@@ -259,46 +261,39 @@ __device__ __forceinline__ void select_head(
     const double hi = e_hi + 2.0 * eps, lo = e_lo - 2.0 * eps;
     SEL_MARK(2);
 
-    // ---- 2. classify: definite-in bits, band ids (two conflict-free warp passes) ----
+    // ---- 2. classify in one warp pass: definite-in bits, band ids appended
+    // through a shared counter (one atomic per warp word that has any).  The
+    // band's order is irrelevant: it is ranked by (exact score, id) below. ----
     uint32_t* cids = cand_ids + head * cand_stride;
     uint64_t* ckeys = cand_keys + head * cand_stride;
-    int wdef = 0, wcand = 0;  // this warp's totals (all lanes)
+    int wdef = 0;  // this warp's definite count (all lanes)
     for (int j = warp; j < W; j += kNW) {
         const int64_t i = (int64_t)j * 32 + lane;
         const bool in = i < nblk;
         const double a = in ? (double)src[i] : 0.0;
         const uint32_t bd = __ballot_sync(0xffffffffu, in && a > hi);
-        const uint32_t bc = __ballot_sync(0xffffffffu, in && !(a > hi) && a >= lo);
-        if (lane == 0) bits[j] = bd;
-        wdef += __popc(bd);
-        wcand += __popc(bc);
-    }
-    if (lane == 0) {
-        s_wsum[0][warp] = wdef;
-        s_wsum[1][warp] = wcand;
-    }
-    __syncthreads();
-    int64_t n_def = 0, n_cand = 0, base = 0;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-        n_def += s_wsum[0][w];
-        if (w < warp) base += s_wsum[1][w];
-        n_cand += s_wsum[1][w];
-    }
-    const bool small = n_cand <= kSmallCand;
-    for (int j = warp; j < W; j += kNW) {
-        const int64_t i = (int64_t)j * 32 + lane;
-        const bool in = i < nblk;
-        const double a = in ? (double)src[i] : 0.0;
         const bool cand = in && !(a > hi) && a >= lo;
         const uint32_t bc = __ballot_sync(0xffffffffu, cand);
-        if (cand) {
-            const int64_t pos = base + __popc(bc & ((1u << lane) - 1u));
-            if (small) ci[pos] = (uint32_t)i;
-            else cids[pos] = (uint32_t)i;
+        if (lane == 0) bits[j] = bd;
+        wdef += __popc(bd);
+        if (bc) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&s_ncand, __popc(bc));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (cand) {
+                const int pos = base + __popc(bc & ((1u << lane) - 1u));
+                if (pos < kSmallCand) ci[pos] = (uint32_t)i;
+                cids[pos] = (uint32_t)i;  // (read only when the band outgrows ci)
+            }
         }
-        base += __popc(bc);
     }
+    if (lane == 0) s_wsum[0][warp] = wdef;
+    __syncthreads();
+    int64_t n_def = 0;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) n_def += s_wsum[0][w];
+    const int64_t n_cand = s_ncand;
+    const bool small = n_cand <= kSmallCand;
     const int64_t need = k - n_def;
     __syncthreads();
     SEL_MARK(3);
