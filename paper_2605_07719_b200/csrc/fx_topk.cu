@@ -303,10 +303,51 @@ __device__ __forceinline__ void select_head(
 #endif
 
     // ---- 3. exact reference scores of the band ----
-    // The candidates' metadata rows are staged in smem (over the no longer
-    // needed keys + histogram) by coalesced 16-byte loads -- one round trip
-    // for a whole round -- then one thread per candidate sums its row.
-    {
+    // bf16: the terms max(q_d mn_d, q_d mx_d) (exact f64 products) are formed
+    // in parallel -- 8 dims per thread straight from the metadata row, one
+    // round trip -- into smem (over the no longer needed keys + histogram),
+    // then one thread per candidate adds its D terms in dimension order: the
+    // reference sum, with only the dependent adds left serial.
+    constexpr bool kTerms = DT == FX_BF16;
+    const int tpitch = D + 1;  // doubles; the odd pitch spreads the row-parallel reads over banks
+    const int per_round_t = ((int)((size_t)keys_cap * 4 + kBins * 4)) / (tpitch * 8);
+    if (kTerms && (D & 7) == 0 && per_round_t >= 1) {
+        double* term = reinterpret_cast<double*>(dsm);
+        const int v8 = D / 8;
+        for (int64_t c0 = 0; c0 < n_cand; c0 += per_round_t) {
+            const int nc = (int)(n_cand - c0 < per_round_t ? n_cand - c0 : per_round_t);
+            for (int e = t; e < nc * v8; e += kT) {
+                const int cc = e / v8, u = e % v8;
+                const uint32_t id = small ? ci[c0 + cc] : cids[c0 + cc];
+                const T* row = mbase + (int64_t)id * 2 * D;
+                const uint4 a = __ldg(reinterpret_cast<const uint4*>(row) + u);
+                const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + D) + u);
+                const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+                double* tr = term + (size_t)cc * tpitch + 8 * u;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double q0 = s_q[8 * u + 2 * j], q1 = s_q[8 * u + 2 * j + 1];
+                    const double x0 = __dmul_rn(q0, (double)bf16lo_to_f(av[j]));
+                    const double y0 = __dmul_rn(q0, (double)bf16lo_to_f(cv[j]));
+                    const double x1 = __dmul_rn(q1, (double)bf16hi_to_f(av[j]));
+                    const double y1 = __dmul_rn(q1, (double)bf16hi_to_f(cv[j]));
+                    tr[2 * j] = (x0 < y0) ? y0 : x0;
+                    tr[2 * j + 1] = (x1 < y1) ? y1 : x1;
+                }
+            }
+            __syncthreads();
+            for (int cc = t; cc < nc; cc += kT) {
+                const double* tr = term + (size_t)cc * tpitch;
+                double sum = 0.0;
+#pragma unroll 16
+                for (int d = 0; d < D; ++d) sum = __dadd_rn(sum, tr[d]);
+                const int64_t c = c0 + cc;
+                if (small) ck[c] = f64_key(sum);
+                else ckeys[c] = f64_key(sum);
+            }
+            __syncthreads();
+        }
+    } else {
         const int row_b = 2 * D * (int)sizeof(T);
         const int pitch = row_b + 16;  // 16-byte skew: conflict-free row-parallel reads
         const int per_round = ((int)((size_t)keys_cap * 4 + kBins * 4)) / pitch;
