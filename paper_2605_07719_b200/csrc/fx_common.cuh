@@ -205,6 +205,10 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, uint64_
         "l"(tmap), "r"(smem_u32(bar)), "r"(0), "r"(c3)
         : "memory");
 }
+// one bulk L2 prefetch of [p, p + bytes) (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }

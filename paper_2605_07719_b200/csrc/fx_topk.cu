@@ -284,6 +284,9 @@ __device__ __forceinline__ void select_head(
                 const int pos = base + __popc(bc & ((1u << lane) - 1u));
                 if (pos < kSmallCand) ci[pos] = (uint32_t)i;
                 cids[pos] = (uint32_t)i;  // (read only when the band outgrows ci)
+                // the row is exact-scored next: start it towards L2 now
+                if (pos < kSmallCand && ((2 * D * sizeof(T)) & 15) == 0)
+                    prefetch_l2_bulk(mbase + (int64_t)i * 2 * D, (uint32_t)(2 * D * sizeof(T)));
             }
         }
     }
