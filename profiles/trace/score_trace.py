@@ -1,0 +1,29 @@
+import os, sys, ctypes as C, numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+os.environ["FLUXATTN_B200_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfluxattn_b200.so")
+from paper_2605_07719_b200 import _native as N
+from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
+eng = Engine(0); dev = eng.device
+B, HKV, G, D = 16, 8, 4, 128
+ctx = 131072; l_cpu = ctx - 320
+dec = SparseDecoder(eng, B, HKV, G, D, 64, l_cpu, 256, max_new=64, dtype="bf16")
+dec.k.normal_(); dec.v.normal_(); dec.build_metadata()
+rng = np.random.default_rng(1)
+H = 32
+props = tuple(torch.as_tensor(x, device=dev) for x in (rng.uniform(0.01, 0.05, (B, H)), rng.uniform(0, 0.01, (B, H)), (rng.random((B, H)) < 0.5).astype(np.int32)))
+q = torch.randn((B, H, D), device=dev)
+for i in range(6):
+    dec.step(q, props=props)
+torch.cuda.synchronize()
+tr = np.zeros(8 * 512, np.int64)
+N.LIB.fx_debug_score_trace.argtypes = [C.c_void_p, C.c_int]
+N.LIB.fx_debug_score_trace(tr.ctypes.data, 8 * 148)
+t = tr[:8 * 148].reshape(148, 8)
+t0 = t[:, 0].min()
+for i, name in enumerate(["start (after pdl_wait)", "producer first TMA", "consumer first box", "consumer end", "producer last TMA"]):
+    x = (t[:, i] - t0) / 1e3
+    print("%-24s min %.2f median %.2f max %.2f" % (name, x.min(), np.median(x), x.max()))
+items = t[:, 5]
+per = (t[:, 3] - t[:, 2]) / np.maximum(items, 1)
+print("items per CTA min %d median %d max %d; ns per item (first box -> end) median %.0f" % (items.min(), np.median(items), items.max(), np.median(per)))
+print("end - last TMA issue median %.2f us" % (np.median(t[:, 3] - t[:, 4]) / 1e3))
