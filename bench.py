@@ -612,9 +612,9 @@ def run_ours(a):
             lh = torch.empty((a.steps, B, H), dtype=torch.float32).pin_memory()
             # a side stream moves step i+1's inputs in and step i's output out
             # while step i computes; every copy is inside the timed region and
-            # every step waits for its inputs.  The step appends the PREVIOUS
-            # step's token inside its plan kernel (the reference appends after a
-            # step, pipeline.cpp:410-412), so the new-KV rows are triple-buffered.
+            # every step waits for its inputs.  Each step is followed by the
+            # append of its token (append_new after a step, pipeline.cpp:410-412);
+            # the new-KV rows are triple-buffered.
             qd = [torch.empty((B, H, D), dtype=torch.float32, device=dev) for _ in range(2)]
             kvd = [torch.empty((2, B, HKV, D), dtype=torch.float32, device=dev) for _ in range(3)]
             od = [torch.empty((B, H, D), dtype=torch.float32, device=dev) for _ in range(2)]
@@ -632,7 +632,7 @@ def run_ours(a):
                     if i >= 2:
                         cs.wait_event(ev_q[i % 2])    # step i-2 read q buffer i%2
                     if i >= 3:
-                        cs.wait_event(ev_kv[i % 3])   # step i-2 appended kv buffer i%3
+                        cs.wait_event(ev_kv[i % 3])   # step i-3 appended from kv buffer i%3
                     qd[i % 2].copy_(qh[i], non_blocking=True)
                     kvd[i % 3].copy_(kvh[i], non_blocking=True)
                     ev_in[i % 2].record(cs)
@@ -647,13 +647,11 @@ def run_ours(a):
                 comp.wait_event(ev_in[j])
                 if i >= 2:
                     comp.wait_event(ev_read[j])  # output buffer j copied out
-                prev = kvd[(i - 1) % 3] if i > 0 else None
-                dec.step(qd[j], props=props, out=od[j], lse=ld[j],
-                         append=(prev[0], prev[1]) if prev is not None else None)
-                ev_q[j].record(comp)
-                if i > 0:
-                    ev_kv[(i - 1) % 3].record(comp)
+                dec.step(qd[j], props=props, out=od[j], lse=ld[j])
                 ev_out[j].record(comp)
+                dec.append(kvd[i % 3][0], kvd[i % 3][1])  # append_new after the step
+                ev_q[j].record(comp)
+                ev_kv[i % 3].record(comp)
                 if i + 1 < a.steps:
                     h2d(i + 1)
                 with torch.cuda.stream(cs):
@@ -672,9 +670,8 @@ def run_ours(a):
             result["e2e"] = {"value": world * a.steps / (ems / 1e3), "unit": UNIT,
                              "h2d_bytes_per_step": int(qd[0].numel() * 4 + kvd[0].numel() * 4),
                              "d2h_bytes_per_step": int(B * H * D * 4 + B * H * 4),
-                             "path": "C-ABI fx_decode_step (plan kernel appends the previous "
-                                     "step's token), pinned host buffers, copies overlapped on "
-                                     "a side stream"}
+                             "path": "C-ABI fx_decode_step + fx_append_kv per step, pinned "
+                                     "host buffers, copies overlapped on a side stream"}
 
         # ---- predictor-driven plan (C2 as configured: budgets from the predictor) ----
         # prefill_stats once (anchor = the first query), then every step:
