@@ -262,8 +262,10 @@ def run_reference_arm(a):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def algorithmic_bytes(dec, q_bytes_per_head=D * 4):
-    """SURVEY §8d bytes of one step: (metadata, attend) from the device plan."""
+def algorithmic_bytes(dec, q_bytes_per_head=D * 4, eq3=False):
+    """SURVEY §8d bytes of one step: (metadata, attend) from the device plan.
+    eq3: the Eq. 3 upper bound instead -- per-head selected rows summed over
+    the group's heads (Σ_h) rather than their union (∪_h), selector.cpp:12."""
     lay = dec.lay
     blk = dec.plan_blk.cpu().numpy()
     kb = dec.plan_kblocks.cpu().numpy()
@@ -282,13 +284,17 @@ def algorithmic_bytes(dec, q_bytes_per_head=D * 4):
             kk = kb[b, g * G:(g + 1) * G]
             if ((kk > 0) & (kk < nblk)).any():
                 meta_bytes += nblk * 2 * D * s
-            u = np.zeros(bits.shape[-1], np.uint32)
-            for h in range(G):
-                u |= bits[b, g * G + h]
-            sel = np.unpackbits(u.view(np.uint8), bitorder="little")[:nblk].astype(bool)
-            ids = np.nonzero(sel)[0]
-            lens = np.minimum(bk, lay.l_cpu - ids * bk)
-            kv_rows += int(lens.sum())
+            masks = [bits[b, g * G + h] for h in range(G)]
+            if not eq3:
+                u = np.zeros(bits.shape[-1], np.uint32)
+                for m in masks:
+                    u |= m
+                masks = [u]
+            for m in masks:
+                sel = np.unpackbits(m.view(np.uint8), bitorder="little")[:nblk].astype(bool)
+                ids = np.nonzero(sel)[0]
+                lens = np.minimum(bk, lay.l_cpu - ids * bk)
+                kv_rows += int(lens.sum())
     heads = lay.batch * H
     attend = kv_rows * 2 * D * s + heads * q_bytes_per_head + heads * (D + 1) * 4
     return meta_bytes, attend
@@ -603,6 +609,12 @@ def run_ours(a):
                                   "GB/s": meta_b / a.steps / (score_ms * 1e-3) / 1e9}
         result["step_bytes"] = step_bytes
         result["step_GBps"] = step_bytes / (ms_per_step * 1e-3) / 1e9
+        # Eq. 3 upper bound of the last step (Σ_h instead of ∪_h): what the
+        # per-head reference path would move; the batched K3 reads a block
+        # once for all heads of its group
+        mb3, ab3 = algorithmic_bytes(dec, eq3=True)
+        mb1, ab1 = algorithmic_bytes(dec)
+        result["eq3_bytes_last_step"] = {"sum_over_heads": mb3 + ab3, "union_over_heads": mb1 + ab1}
 
         # ---- end to end: pinned host q / new KV in, o out, every step ----
         if not a.no_e2e:
