@@ -1,30 +1,42 @@
 #!/usr/bin/env python
 """Fluxion sparse-attention decode step on B200 -- the BASELINE.json metric.
 
-Workload (BASELINE.json configs[1], "C2"): one Llama-3-8B-shaped decode layer
-(32 query / 8 KV heads, head_dim 128), 131072-token context per sequence
-(sink 64 | cpu 130752 | local 256 | decoded rows), batch 16 per GPU, bf16 KV,
-synthetic N(0,1) K/V generated on device.  Budgets: per-head properties
-(bgt0 ~ U(0.01, 0.05), k ~ U(0, 0.01), streaming ~ Bernoulli(0.5), seed 1;
-SURVEY §8d perf run) -> on-device plan_group picks each group's granularity
-(16/32/64/128) and per-head budgets every step.
+Default workload (BASELINE.json configs[1], "C2"): one Llama-3-8B-shaped decode
+layer (32 query / 8 KV heads, head_dim 128), 131072-token context per sequence
+(sink 64 | cpu 130752 | local 256 | decoded rows), batch 16 per GPU, bf16 KV
+from the reference's generate(spec) run on the device.  Budgets: per-head
+properties (bgt0 ~ U(0.01, 0.05), k ~ U(0, 0.01), streaming ~ Bernoulli(0.5),
+seed 1; SURVEY §8d perf run) -> on-device plan_group picks each group's
+granularity (16/32/64/128) and per-head budgets every step.
 
 One timed step = K5 plan -> K2 score/select (+ fused worklist) -> K3/K4 sparse
-GQA attention + fused LSE merge for all 512 heads of the batch, plus the append
+GQA attention + fused LSE merge for every head of the batch, plus the append
 of the step's new K/V row of every group.  Per-step working set is > 1 GB, far
 above the 126 MB L2, so no flush is needed between steps.
 
-Multi-GPU (torchrun): weak scaling, every rank decodes its own batch of 16
-(batch x KV-head sharding needs no collective); value = aggregate steps/s.
+Other configs (--workload): c1 (configs[0]: 32K, batch 1, f32, fixed (64,
+0.05)), c3 (configs[2]: Qwen 28q/4kv, 256K, batch 8, output-aware budgets
+labelled once on the device), c4 (configs[3]: 32 layers x batch 8 per GPU, the
+layers' tasks in one batched step), c5 (configs[4]: 1M context, batch 4,
+context-parallel over the torchrun ranks).  --plan fixed16: every head
+retrieving at (16, 0.05) -- BASELINE.md's 2,015 steps/s target row.
+
+Multi-GPU: `--gpus N` re-launches itself under torch.distributed.run when not
+already inside one (one rank per GPU).  C1-C4 shard by batch (weak scaling, no
+collective); C5 splits the context (strong scaling).
 
 --impl reference: the reference's own executed CPU path (oracle/_ref, the
-unmodified sources compiled here) on a bounded sample of the same workload.
+unmodified sources compiled here) on the same workload: every sequence of the
+batch (for C4 the 8 sequences of one layer, extrapolated x32), data from the
+reference's own generate(spec), one run(queue, profile, RunMode::Executed)
+per step.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -36,20 +48,46 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sparse-attn decode steps/s at 128K ctx, bs=16; achieved HBM GB/s vs peak"
 UNIT = "steps/s"
-H, HKV, G, D = 32, 8, 4, 128
+D = 128
 L_SINK, L_LOCAL = 64, 256
 
+# BASELINE.json configs; `seqs` sequences x `layers` layers per GPU
+WORKLOADS = {
+    "c1": dict(heads=32, G=4, context=32768, seqs=1, layers=1, dtype="f32", plan="fixed64",
+               desc="C1: Llama-3-8B layer (32q/8kv heads, d128), 32K ctx, batch 1, f32 KV"),
+    "c2": dict(heads=32, G=4, context=131072, seqs=16, layers=1, dtype="bf16", plan="props",
+               desc="C2: Llama-3-8B layer (32q/8kv heads, d128), 128K ctx, batch 16/GPU, bf16 KV"),
+    "c3": dict(heads=28, G=7, context=262144, seqs=8, layers=1, dtype="bf16", plan="labels",
+               desc="C3: Qwen2.5-7B layer (28q/4kv heads, d128), 256K ctx, batch 8/GPU, bf16 KV"),
+    "c4": dict(heads=32, G=4, context=131072, seqs=8, layers=32, dtype="bf16", plan="props",
+               desc="C4: Llama-3-8B 32-layer decode step, 128K ctx, batch 8/GPU (64 over 8 GPUs), "
+                    "the 32 layers' (b, g) tasks in one batched step, bf16 KV"),
+}
+PLANS = {
+    "props": "drawn head properties (bgt0~U(.01,.05), k~U(0,.01), streaming~B(.5), seed 1) -> "
+             "plan_group",
+    "fixed16": "fixed (blk 16, budget 0.05) for every head, every head retrieving "
+               "(pipeline.cpp:304-311)",
+    "fixed64": "fixed (blk 64, budget 0.05) for every head (pipeline.cpp:304-311)",
+    "labels": "output-aware oracle head properties (label_streaming / min_budget / fit_curve, "
+              "tau 0.10, pipeline.cpp:256-276) of the first decode query -> plan_group",
+}
 
-def args_parse():
+
+def args_parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--context", type=int, default=131072)
-    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--plan", default=None, choices=sorted(PLANS),
+                    help="budget source (default: the workload's own)")
+    ap.add_argument("--context", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling run: timed loop only")
     ap.add_argument("--data", default="reference", choices=["reference", "normal"],
                     help="reference: the reference generator's workload (generate(spec), on "
@@ -57,53 +95,88 @@ def args_parse():
     ap.add_argument("--cp-exchange", default="dist", choices=["dist", "peer", "collective"],
                     help="c5 exchanges: peer-memory one-shot kernels, or torch.distributed "
                          "all-gathers (NCCL)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
-                    help="c2: one layer, batch 16 (the metric's config); c4: 32 layers x batch 8 "
-                         "per GPU (configs[3], one 8-GPU shard), the layers' independent tasks "
-                         "batched into one step like run_decode's single queue (pipeline.cpp:354); "
-                         "c5: 1M context, batch 4, context-parallel over the torchrun ranks "
-                         "(configs[4]; one rank = the single-device step)")
-    a = ap.parse_args()
-    if a.workload == "c4":
-        a.layers, a.seqs = 32, 8
-        a.batch = a.layers * a.seqs  # (layer, sequence) pairs: independent (b, g) tasks
-    else:
-        a.layers, a.seqs = 1, a.batch
+    ap.add_argument("--dry-run-launch", action="store_true",
+                    help="launcher self-test without a GPU: ranks, barriers and the max-over-"
+                         "ranks reduction over gloo with an empty step (never a measurement)")
+    a = ap.parse_args(argv)
+    if a.workload != "c5":
+        w = WORKLOADS[a.workload]
+        a.heads, a.G = w["heads"], w["G"]
+        a.hkv = a.heads // a.G
+        a.context = a.context or w["context"]
+        a.seqs = a.batch or w["seqs"]
+        a.layers = w["layers"]
+        a.kv_dtype = w["dtype"]
+        a.plan = a.plan or w["plan"]
+        a.batch = a.layers * a.seqs  # (layer, sequence) entries: independent (b, g) tasks
     return a
 
 
-def head_props(batch, seed=1):
+def workload_config(a, world):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    return {"workload": f"{WORKLOADS[a.workload]['desc']}; budgets: {PLANS[a.plan]}",
+            "heads": a.heads, "kv_heads": a.hkv, "head_dim": D, "layers": a.layers,
+            "context": a.context, "seq_len": a.context, "global_batch": a.seqs * world,
+            "kv_dtype": a.kv_dtype, "plan": a.plan,
+            "data": "the reference's generate(spec), WorkloadSpec defaults, seed 1 + sequence"
+            if a.data == "reference" else "N(0,1) K/V",
+            "parallelism": f"batch-sharded x{world} (no collective)",
+            "l2": "per-step working set > 1 GB (inputs larger than the 126 MB L2); no flush"
+            if a.workload != "c1" else "32K f32 working set ~60 MB fits the 126 MB L2 across "
+                                       "steps; no flush (launch-bound config)"}
+
+
+def head_props(batch, heads, seed=1):
     rng = np.random.default_rng(seed)
-    bgt0 = rng.uniform(0.01, 0.05, (batch, H))
-    kslope = rng.uniform(0.0, 0.01, (batch, H))
-    streaming = (rng.random((batch, H)) < 0.5).astype(np.int32)
+    bgt0 = rng.uniform(0.01, 0.05, (batch, heads))
+    kslope = rng.uniform(0.0, 0.01, (batch, heads))
+    streaming = (rng.random((batch, heads)) < 0.5).astype(np.int32)
     return bgt0, kslope, streaming
+
+
+def fixed_plan(plan):
+    return {"fixed16": (16, 0.05), "fixed64": (64, 0.05)}.get(plan)
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel, workload="c2"):
+def ncu_traffic(kernel, tag):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the
-    committed `ncu --set full` extract of the same bench command and workload
-    (profiles/ncu_traffic.json for c2, profiles/ncu_traffic_<workload>.json
+    committed `ncu --set full` extract of the same bench command (profiles/
+    ncu_traffic.json for the default c2 line, profiles/ncu_traffic_<tag>.json
     otherwise; written by profiles/summarize_ncu.py); None if absent."""
-    name = "ncu_traffic.json" if workload == "c2" else f"ncu_traffic_{workload}.json"
+    name = "ncu_traffic.json" if tag == "c2" else f"ncu_traffic_{tag}.json"
     try:
         with open(os.path.join(ROOT, "profiles", name)) as f:
             t = json.load(f)
-        for name, rec in t["kernels"].items():
-            if kernel in name:
+        for kname, rec in t["kernels"].items():
+            if kernel in kname:
+                rec = dict(rec)
+                rec["source"] = f"profiles/{name}"
                 return rec
     except Exception:
         pass
     return None
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
 
 
 class ClockSampler:
@@ -183,80 +256,241 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference CPU path (oracle/_ref) on a bounded sample
+# the reference CPU path (oracle/_ref): run(queue, profile, RunMode::Executed)
 # ---------------------------------------------------------------------------
-def reference_sample(ref, kv_groups, plans, queries, host_workers, repeats):
-    """Run the reference's executed scheduler over one sequence's groups.
+def reference_plans(ref, a, props, fixed, l_cpu, entries):
+    """plan_group (selector.cpp:21-46) / the fixed plan (pipeline.cpp:304-311) of
+    every (entry, g): None for a streaming group (no task, pipeline.cpp:334-337)."""
+    G = a.G
+    plans = {}
+    for b in entries:
+        for g in range(a.hkv):
+            if fixed is not None:
+                plans[(b, g)] = (fixed[0], np.full(G, fixed[1]))
+                continue
+            sl = slice(g * G, (g + 1) * G)
+            p = ref.plan_group(props[0][b, sl], props[1][b, sl], props[2][b, sl], l_cpu)
+            plans[(b, g)] = None if p["streaming_group"] else (p["block_size"], np.asarray(p["budgets"]))
+    return plans
 
-    kv_groups[g] = (K, V) position-ordered f32; plans[g] = (blk, budgets) or
-    None for a streaming group (no task, like pipeline.cpp:334-337)."""
-    batch = ref.batch()
-    l_cpu = kv_groups[0][0].shape[0] - L_SINK - L_LOCAL
-    n_tasks = 0
-    for g, (k, v) in enumerate(kv_groups):
-        if plans[g] is None:
-            continue
-        blk, budgets = plans[g]
-        batch.add(k, v, (L_SINK, l_cpu, L_LOCAL, 0), queries[g * G:(g + 1) * G], blk, budgets)
-        n_tasks += 1
-    times = []
-    for _ in range(repeats):
-        sec, _ = batch.run(host_workers)
+
+def reference_labels(ref, a, data, entries, l_cpu, cores, tau=0.10):
+    """Oracle head properties (pipeline.cpp:256-276) with the reference's own
+    cache_attention / max_output_norm / label_streaming / min_budget /
+    fit_curve, heads in parallel host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+    seg = (L_SINK, l_cpu, L_LOCAL, 0)
+    props = tuple(np.zeros((a.batch, a.heads)) for _ in range(3))
+    for b in entries:
+        kvs, q = data[b]
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            outs = list(ex.map(lambda h: ref.cache_attention(*kvs[h // a.G], seg, q[h]),
+                               range(a.heads)))
+        nrm = ref.max_output_norm(np.stack(outs))
+
+        def label(h):
+            k, v = kvs[h // a.G]
+            if ref.label_streaming(k, v, seg, q[h], outs[h], nrm, tau):
+                return 0.0, 0.0, 1
+            buds = [ref.min_budget(k, v, seg, q[h], blk, outs[h], nrm, tau)[0]
+                    for blk in (1, 16, 32, 64, 128)]
+            kk, _, _ = ref.fit_curve([16, 32, 64, 128], buds[1:], buds[0], False)
+            return buds[0], kk, 0
+
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            for h, (b0, kk, st) in enumerate(ex.map(label, range(a.heads))):
+                props[0][b, h], props[1][b, h], props[2][b, h] = b0, kk, st
+    return props[0], props[1], props[2].astype(np.int32)
+
+
+def reference_run(ref, batch, workers, repeats, want_outputs=False):
+    """`repeats` executed runs of the whole queue; per-run wall seconds."""
+    times, out = [], None
+    for i in range(repeats):
+        sec, o = batch.run(workers, want_outputs=want_outputs and i == repeats - 1)
         times.append(sec)
-    return times, n_tasks
+        if o is not None:
+            out = o
+    return times, out
 
 
 def run_reference_arm(a):
-    """--impl reference: the reference CPU path, rank 0 only."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference CPU path on rank 0; other ranks exit."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle.oracle import RefOracle
     ref = RefOracle()
-    cores = os.cpu_count() or 1
+    ci = cpu_info()
+    cores = ci["nproc"] or 1
     workers = max(1, cores - 1)
+    if a.workload == "c5":
+        print(json.dumps({"impl": "reference", "unavailable": "C5 (1M context) reference run "
+                          "would need ~70 GB of f32 host KV per step sample; use --workload c2"}))
+        return
     l_cpu = a.context - L_SINK - L_LOCAL
-    rng = np.random.default_rng(7)
-    groups = []
-    if a.data == "reference":  # the reference's own generator, sequence 0 (seed 1), layer 0
-        w = ref.generate(seed=1, layers=1, heads=H, group_size=G, head_dim=D,
-                         context_len=a.context, decode_steps=1)
-        groups = [w.group_kv(0, g) for g in range(HKV)]
-        q = w.queries(0, 0)
-    else:
-        for g in range(HKV):
-            k = rng.standard_normal((a.context, D), dtype=np.float32)
-            v = rng.standard_normal((a.context, D), dtype=np.float32)
-            groups.append((k, v))
-        q = rng.standard_normal((H, D)).astype(np.float32)
-        q *= np.sqrt(D) / np.linalg.norm(q, axis=-1, keepdims=True)
-    bgt0, ks, st = head_props(a.batch)
-    plans = []
-    for g in range(HKV):
-        sl = slice(g * G, (g + 1) * G)
-        p = ref.plan_group(bgt0[0, sl], ks[0, sl], st[0, sl], l_cpu)
-        plans.append(None if p["streaming_group"] else (p["block_size"], p["budgets"]))
-    times, n_tasks = reference_sample(ref, groups, plans, q, workers, a.warmup + a.steps)
-    t = float(np.mean(times[a.warmup:])) if len(times) > a.warmup else float(np.mean(times))
-    per_step = t * a.batch  # one sequence sampled; the batch has `batch` of them
-    value = 1.0 / per_step
+    # C4: the 8 sequences of layer 0 (64 tasks; every layer is the same shape) x32
+    entries = list(range(a.seqs)) if a.workload == "c4" else list(range(a.batch))
+    scale = a.batch / len(entries)
+    t_gen = time.time()
+
+    def gen(b):
+        seq = b % a.seqs
+        layer = b // a.seqs
+        if a.data == "reference":
+            w = ref.generate(seed=1 + seq, layers=layer + 1, heads=a.heads, group_size=a.G,
+                             head_dim=D, context_len=a.context, decode_steps=1)
+            return [w.group_kv(layer, g) for g in range(a.hkv)], w.queries(layer, 0)
+        rng = np.random.default_rng(1 + b)
+        kv = [(rng.standard_normal((a.context, D), dtype=np.float32),
+               rng.standard_normal((a.context, D), dtype=np.float32)) for _ in range(a.hkv)]
+        q = rng.standard_normal((a.heads, D)).astype(np.float32)
+        return kv, q * (np.sqrt(D) / np.linalg.norm(q, axis=-1, keepdims=True))
+
+    with ThreadPoolExecutor(max_workers=min(len(entries), cores)) as ex:
+        data = dict(zip(entries, ex.map(gen, entries)))
+    gen_s = time.time() - t_gen
+    fixed = fixed_plan(a.plan)
+    props = head_props(a.batch, a.heads, seed=1)
+    if a.plan == "labels":  # the reference's own oracle labels of the first decode query
+        props = reference_labels(ref, a, data, entries, l_cpu, cores)
+    plans = reference_plans(ref, a, props, fixed, l_cpu, entries)
+    batch = ref.batch()
+    meta_s = 0.0
+    n_tasks = 0
+    for b in entries:
+        kvs, q = data[b]
+        for g in range(a.hkv):
+            if plans[(b, g)] is None:
+                continue
+            blk, bud = plans[(b, g)]
+            meta_s += batch.add(kvs[g][0], kvs[g][1], (L_SINK, l_cpu, L_LOCAL, 0),
+                                q[g * a.G:(g + 1) * a.G], blk, bud)
+            n_tasks += 1
+        data[b] = None  # the batch holds its own copy
+    times, _ = reference_run(ref, batch, workers, a.warmup + a.steps)
+    timed = times[a.warmup:] if len(times) > a.warmup else times
+    best = min(timed) * scale
+    mean = float(np.mean(timed)) * scale
+    value = 1.0 / best
+    sample = (f"every sequence of the batch: {n_tasks} retrieval-group tasks of {len(entries)} "
+              f"entries per step" + (f", x{scale:g} for the {a.layers} layers" if scale != 1 else "")
+              + f"; run(queue, profile, RunMode::Executed) with {workers} host workers + 1 "
+                f"accelerator-model thread; value = best of {len(timed)} timed runs "
+                f"(BASELINE.md §2), mean {1.0 / mean:.3g} steps/s")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": per_step * 1e3,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": best * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": ("synthetic: the reference's generate(spec), seed 1" if a.data == "reference"
-                 else "synthetic N(0,1)"),
-        "config": {"workload": "C2: Llama-3-8B layer (32q/8kv, d128), 128K ctx, batch 16, "
-                               "per-head budgets + per-group granularity via plan_group",
-                   "context": a.context, "global_batch": a.batch * a.gpus,
-                   "sample": "1 of 16 sequences (8 KV groups) per step, extrapolated x16"},
+        "data": "synthetic: " + workload_config(a, 1)["data"],
+        "config": workload_config(a, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers + 1, "kind": "reference",
-                         "sample": f"{n_tasks} retrieval-group tasks of 1 sequence per step, "
-                                   f"run(queue, profile, RunMode::Executed), "
-                                   f"{workers} host workers + 1 accelerator-model thread"},
+                         "sample": sample, "cpu_model": ci["model"], "nproc": ci["nproc"],
+                         "mean_value": 1.0 / mean, "generate_s": gen_s,
+                         "metadata_build_s": meta_s},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_and_parity(a, dec, q, o, lse, plan_step, ref_runs=5, parity=True):
+    """The compiled reference on the GPU step's exact data (bf16 bits upcast to
+    f32, the same plan and queries, the same decoded rows): whole batch (C4: one
+    layer's 8 sequences, x32), best of `ref_runs` executed runs.  Then parity of
+    that step: the reference's outputs vs ours for every task, every head's
+    selection vs the C restatement's topk_blocks, every plan vs plan_group."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    from oracle.oracle import COracle, RefOracle
+    ref = RefOracle()
+    ci = cpu_info()
+    cores = ci["nproc"] or 1
+    workers = max(1, cores - 1)
+    lay = dec.lay
+    G, hkv = lay.group_size, lay.kv_heads
+    l_cpu, l_new = lay.l_cpu, dec.l_new
+    n_rows = lay.l_sink + l_cpu + lay.l_local + l_new
+    seg = (lay.l_sink, l_cpu, lay.l_local, l_new)
+    entries = list(range(a.seqs)) if a.workload == "c4" else list(range(lay.batch))
+    scale = lay.batch / len(entries)
+    blk = dec.plan_blk.cpu().numpy()
+    bud = dec.plan_budgets.cpu().numpy()
+    kbl = dec.plan_kblocks.cpu().numpy()
+    bits = dec.sel_bits.cpu().numpy().view(np.uint32)
+    qn = q.cpu().numpy()
+    on, ln = o.cpu().numpy(), lse.cpu().numpy()
+    batch = ref.batch()
+    tasks = []
+    for b in entries:
+        for g in range(hkv):
+            if int(blk[b, g]) == 0:
+                continue
+            k = dec.k[b, g, :n_rows].float().cpu().numpy()
+            v = dec.v[b, g, :n_rows].float().cpu().numpy()
+            batch.add(k, v, seg, qn[b, g * G:(g + 1) * G], int(blk[b, g]), bud[b, g * G:(g + 1) * G])
+            tasks.append((b, g))
+    times, ro = reference_run(ref, batch, workers, ref_runs, want_outputs=parity)
+    t = min(times) * scale
+    res = {"value": 1.0 / t, "unit": UNIT, "cores": workers + 1, "kind": "reference",
+           "cpu_model": ci["model"], "nproc": ci["nproc"],
+           "sample": f"{len(tasks)} retrieval-group tasks = every (b, g) of "
+                     + (f"layer 0's {len(entries)} sequences, x{scale:g} for the layers"
+                        if scale != 1 else f"all {len(entries)} sequences")
+                     + f" (the GPU step's data, plan and queries), run(queue, profile, "
+                       f"RunMode::Executed) with {workers} host workers + 1 accelerator-model "
+                       f"thread, best of {ref_runs}",
+           "mean_value": 1.0 / (float(np.mean(times)) * scale)}
+    if not parity:
+        return res, None
+    # ---- parity of the step against the reference / the C restatement ----
+    errs = []
+    for i, (b, g) in enumerate(tasks):
+        want = ro[i]
+        got = on[b, g * G:(g + 1) * G]
+        errs.append(float(np.abs(got - want).max() / max(1.0, np.abs(want).max())))
+    corc = COracle()
+
+    def sel_check(bg):
+        b, g = bg
+        bk = int(blk[b, g])
+        k_cpu = dec_kcpu[bg]
+        mins, maxs = corc.build_metadata(k_cpu, bk)
+        nblk = mins.shape[0]
+        mism = 0
+        for hg in range(G):
+            h = g * G + hg
+            want, _ = corc.topk_blocks(qn[b, h], mins, maxs, int(kbl[b, h]))
+            got = np.nonzero(np.unpackbits(bits[b, h].view(np.uint8), bitorder="little")[:nblk])[0]
+            if not np.array_equal(np.sort(want.astype(np.int64)), got):
+                mism += 1
+        return mism
+
+    dec_kcpu = {}
+    for bg in tasks:
+        b, g = bg
+        dec_kcpu[bg] = dec.k[b, g, lay.l_sink:lay.l_sink + l_cpu].float().cpu().numpy()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        mism = sum(ex.map(sel_check, tasks))
+    plan_mism = 0
+    if plan_step is not None:
+        for b in entries:
+            for g in range(hkv):
+                sl = slice(g * G, (g + 1) * G)
+                p = ref.plan_group(plan_step[0][b, sl], plan_step[1][b, sl], plan_step[2][b, sl], l_cpu)
+                want_blk = 0 if p["streaming_group"] else p["block_size"]
+                if int(blk[b, g]) != want_blk or (want_blk and not np.array_equal(bud[b, sl], p["budgets"])):
+                    plan_mism += 1
+    par = {"tasks": len(tasks), "heads": len(tasks) * G, "max_rel_err": max(errs) if errs else 0.0,
+           "tolerance": 2e-2 if lay.dtype == 1 else 1e-3,
+           "selection_mismatches": int(mism), "plan_mismatches": int(plan_mism),
+           "against": "outputs: the compiled reference's run(Executed) results of the same step; "
+                      "selections: the C restatement's topk_blocks of every head (oracle/"
+                      "fx_oracle.c, pinned to the reference); plans: the reference's plan_group",
+           "lse_finite": bool(np.isfinite(ln).all())}
+    return res, par
 
 
 # ---------------------------------------------------------------------------
@@ -267,10 +501,11 @@ def algorithmic_bytes(dec, q_bytes_per_head=D * 4, eq3=False):
     eq3: the Eq. 3 upper bound instead -- per-head selected rows summed over
     the group's heads (Σ_h) rather than their union (∪_h), selector.cpp:12."""
     lay = dec.lay
+    G = lay.group_size
     blk = dec.plan_blk.cpu().numpy()
     kb = dec.plan_kblocks.cpu().numpy()
     bits = dec.sel_bits.cpu().numpy().view(np.uint32)
-    s = 2  # bf16
+    s = 2 if lay.dtype == 1 else 4
     meta_bytes = 0
     kv_rows = 0
     for b in range(lay.batch):
@@ -283,7 +518,7 @@ def algorithmic_bytes(dec, q_bytes_per_head=D * 4, eq3=False):
             nblk = (lay.l_cpu + bk - 1) // bk
             kk = kb[b, g * G:(g + 1) * G]
             if ((kk > 0) & (kk < nblk)).any():
-                meta_bytes += nblk * 2 * D * s
+                meta_bytes += nblk * 2 * lay.head_dim * s
             masks = [bits[b, g * G + h] for h in range(G)]
             if not eq3:
                 u = np.zeros(bits.shape[-1], np.uint32)
@@ -295,15 +530,14 @@ def algorithmic_bytes(dec, q_bytes_per_head=D * 4, eq3=False):
                 ids = np.nonzero(sel)[0]
                 lens = np.minimum(bk, lay.l_cpu - ids * bk)
                 kv_rows += int(lens.sum())
-    heads = lay.batch * H
-    attend = kv_rows * 2 * D * s + heads * q_bytes_per_head + heads * (D + 1) * 4
+    heads = lay.batch * dec.heads
+    attend = kv_rows * 2 * lay.head_dim * s + heads * q_bytes_per_head + heads * (lay.head_dim + 1) * 4
     return meta_bytes, attend
 
 
 def run_c5(a):
     """configs[4]: 1M-token context, batch 4, the cpu segment split over the
-    ranks (context_parallel.py; NCCL all-gathers of the k-th keys, the
-    candidates and the (o, lse) partials).  Strong scaling: the job is fixed."""
+    ranks (context_parallel.py).  Strong scaling: the job is fixed."""
     import torch
     import torch.distributed as dist
 
@@ -317,16 +551,17 @@ def run_c5(a):
     from paper_2605_07719_b200.context_parallel import CPShard, TorchComm, cp_decode_step, shard_kv
     from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
 
+    H, HKV, G = 32, 8, 4
     B, ctx = 4, 1 << 20
     l_cpu = ctx - L_SINK - L_LOCAL
-    total = a.warmup + a.steps + 2
+    total = a.warmup + 2 * a.steps + 4
     eng = Engine(local)
     full = SparseDecoder(eng, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, max_new=total, dtype="bf16")
     out = full.generate(dict(seed=1, layers=1, heads=H, group_size=G, head_dim=D, context_len=ctx,
                              decode_steps=total), seeds=[1 + b for b in range(B)], layers=[0] * B,
                         steps=total)
     qs, nk, nv = out["step_q"], out["new_k"], out["new_v"]
-    bgt0, ks, st = head_props(B, seed=1)
+    bgt0, ks, st = head_props(B, H, seed=1)
     props = tuple(torch.as_tensor(x, device=dev) for x in (bgt0, ks, st))
     if world == 1:
         full.build_metadata()
@@ -384,26 +619,77 @@ def run_c5(a):
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
+    result = {
+        "metric": METRIC, "value": a.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: the reference's generate(spec) on device, seed 1 + sequence",
+        "gpu_launches": int(eng.launches() - n0), "clocks": clk,
+        "config": {"workload": "C5: Llama-3-8B layer, 1M ctx, batch 4, per-head budgets from "
+                               "plan_group over the whole sequence",
+                   "context": ctx, "global_batch": B, "seq_len": ctx,
+                   "parallelism": "single device" if world == 1 else
+                   (f"context-parallel x{world}, the selection bracket distributed over peer "
+                    f"memory (score ranges, summed histograms, exact-scored bands; CUDA IPC "
+                    f"tables, flag waits in the kernels)"
+                    if a.cp_exchange == "dist" else
+                    f"context-parallel x{world}, one-shot exchanges over peer memory (CUDA IPC "
+                    f"tables, flag waits in the select / combine kernels)"
+                    if a.cp_exchange == "peer" else
+                    f"context-parallel x{world} (all-gathers of k-th keys, candidates, "
+                    f"(o, lse))")}}
+    if world == 1 and not a.quick:
+        import ctypes as C
+
+        from paper_2605_07719_b200 import _native as N
+        N.check(N.LIB.fx_ctx_reset_timing(eng.ctx))
+        N.check(N.LIB.fx_ctx_set_timing(eng.ctx, 1))
+        attend_b = meta_b = 0
+        for _ in range(a.steps):
+            one_step()
+            mb, ab = algorithmic_bytes(dec)
+            meta_b += mb
+            attend_b += ab
+        N.check(N.LIB.fx_ctx_set_timing(eng.ctx, 0))
+        kt = {}
+        for i, name in enumerate(N.KERNELS):
+            tot, cnt = C.c_double(0), C.c_int64(0)
+            N.check(N.LIB.fx_ctx_kernel_time(eng.ctx, i, C.byref(tot), C.byref(cnt)))
+            if cnt.value:
+                kt[name] = tot.value / cnt.value
+        peak, peak_kind = peaks()
+        achieved = attend_b / a.steps / (kt["attend"] * 1e-3) / 1e9
+        tr = ncu_traffic("k_attend", "c5")
+        result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3+K4)", "achieved": achieved,
+                              "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                              "peak_kind": peak_kind, "traffic": (tr or {}).get("dram_bytes_per_launch"),
+                              "traffic_source": (tr or {}).get("source"),
+                              "algorithmic_bytes_per_launch": attend_b / a.steps}
+        result["kernels_ms"] = kt
+        step_bytes = (meta_b + attend_b) / a.steps
+        result["step_bytes"] = step_bytes
+        result["step_GBps"] = step_bytes / (result["ms_per_step"] * 1e-3) / 1e9
+        # e2e: pinned host q in, o + lse out, per step, through the C-ABI
+        qh = qs[: a.steps].cpu().pin_memory()
+        oh = torch.empty((a.steps, B, H, D), dtype=torch.float32).pin_memory()
+        lh = torch.empty((a.steps, B, H), dtype=torch.float32).pin_memory()
+        qd = torch.empty((B, H, D), dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        t0.record()
+        for i in range(a.steps):
+            qd.copy_(qh[i], non_blocking=True)
+            o, lse = dec.step(qd, props=props)
+            oh[i].copy_(o, non_blocking=True)
+            lh[i].copy_(lse, non_blocking=True)
+        t1.record()
+        torch.cuda.synchronize()
+        ems = t0.elapsed_time(t1)
+        result["e2e"] = {"value": a.steps / (ems / 1e3), "unit": UNIT,
+                         "h2d_bytes_per_step": B * H * D * 4, "d2h_bytes_per_step": B * H * (D + 1) * 4,
+                         "path": "C-ABI fx_decode_step per step, pinned host q in, o + lse out, "
+                                 "copies on the compute stream"}
     if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": a.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic: the reference's generate(spec) on device, seed 1 + sequence",
-            "gpu_launches": int(eng.launches() - n0), "clocks": clk,
-            "config": {"workload": "C5: Llama-3-8B layer, 1M ctx, batch 4, per-head budgets from "
-                                   "plan_group over the whole sequence",
-                       "context": ctx, "global_batch": B, "seq_len": ctx,
-                       "parallelism": "single device" if world == 1 else
-                       (f"context-parallel x{world}, the selection bracket distributed over peer "
-                        f"memory (score ranges, summed histograms, exact-scored bands; CUDA IPC "
-                        f"tables, flag waits in the kernels)"
-                        if a.cp_exchange == "dist" else
-                        f"context-parallel x{world}, one-shot exchanges over peer memory (CUDA IPC "
-                        f"tables, flag waits in the select / combine kernels)"
-                        if a.cp_exchange == "peer" else
-                        f"context-parallel x{world} (all-gathers of k-th keys, candidates, "
-                        f"(o, lse))")}}), flush=True)
+        print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -414,34 +700,38 @@ def run_ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"bench: --gpus {a.gpus} but WORLD_SIZE={world}; run `bench.py --gpus N` "
+                         f"(it launches N ranks itself) or torchrun with --nproc-per-node N")
     # one rank per GPU; the modulo only matters for a multi-rank smoke test of this
     # code path on a single-GPU box (FX_BENCH_BACKEND=gloo), never for a measurement
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group(os.environ.get("FX_BENCH_BACKEND", "nccl"), init_method="env://")
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group(os.environ.get("FX_BENCH_BACKEND", "nccl"), init_method="env://")
     dev = torch.device("cuda", local)
 
     from paper_2605_07719_b200 import _native as N
     from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
 
-    B = a.batch
+    B, H, HKV, G = a.batch, a.heads, a.hkv, a.G
     l_cpu = a.context - L_SINK - L_LOCAL
-    total_steps = 2 * a.warmup + 5 * a.steps + 8  # timed, graph replay, timing pass, e2e, predictor
+    total_steps = 2 * a.warmup + 5 * a.steps + 10  # timed, graph replay, timing pass, e2e, predictor
     eng = Engine(local)
+    tdt = torch.bfloat16 if a.kv_dtype == "bf16" else torch.float32
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     shape = (B, HKV, SparseDecoder.cap_rows(a.context, total_steps), D)
-    k = torch.empty(shape, dtype=torch.bfloat16, device=dev)
-    v = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+    k = torch.empty(shape, dtype=tdt, device=dev)
+    v = torch.empty(shape, dtype=tdt, device=dev)
     if a.data == "normal":  # plain N(0,1) KV, generated on device
         for b in range(B):
             k[b].normal_(generator=gen)
             v[b].normal_(generator=gen)
     dec = SparseDecoder(eng, B, HKV, G, D, L_SINK, l_cpu, L_LOCAL, max_new=total_steps,
-                        dtype="bf16", k=k, v=v)
+                        dtype=a.kv_dtype, k=k, v=v)
     gen_ms = None
+    anchor = None
     if a.data == "reference":
         # the reference's generate(spec) (WorkloadSpec defaults: 0.5 streaming / 0.5
         # retrieval heads, one 16-token needle per retrieval head, local boost,
@@ -449,14 +739,12 @@ def run_ours(a):
         # sequence's seed = 1 + its global index
         spec = dict(seed=1, layers=a.layers, heads=H, group_size=G, head_dim=D,
                     context_len=a.context, decode_steps=total_steps)
-        seqs = [b % a.seqs for b in range(B)]
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
         t_gen = time.time()
-        out = dec.generate(spec, seeds=[1 + rank * a.seqs + sq for sq in seqs],
+        out = dec.generate(spec, seeds=[1 + rank * a.seqs + b % a.seqs for b in range(B)],
                            layers=[b // a.seqs for b in range(B)], steps=total_steps)
         gen_ms = (time.time() - t_gen) * 1e3
         qs = out["step_q"]
+        anchor = out["anchor"]
         kv_new = torch.stack([out["new_k"], out["new_v"]], dim=1)
         del out
     torch.cuda.synchronize()
@@ -467,9 +755,6 @@ def run_ours(a):
     torch.cuda.synchronize()
     meta_build_ms = e0.elapsed_time(e1)
 
-    bgt0, ks, st = head_props(B, seed=1 + rank)
-    props = (torch.as_tensor(bgt0, device=dev), torch.as_tensor(ks, device=dev),
-             torch.as_tensor(st, device=dev))
     if a.data == "normal":
         # drifting decode queries (workload.cpp:280-296 recipe), pre-generated on device
         rho = 0.98
@@ -481,15 +766,35 @@ def run_ours(a):
             qs[t] = rho * qs[t - 1] / qs[t - 1].norm(dim=-1, keepdim=True) + (1 - rho * rho) ** 0.5 * noise
         qs = qs / qs.norm(dim=-1, keepdim=True) * (D ** 0.5)
         kv_new = torch.randn((total_steps, 2, B, HKV, D), generator=gen, device=dev)
+        anchor = qs[0]
+
+    fixed = fixed_plan(a.plan)
+    label_ms = None
+    props_host = None
+    if a.plan == "labels":
+        # output-aware budgets (pipeline.cpp:256-276) of the first decode query,
+        # labelled once on the device and fed to plan_group every step
+        e0.record()
+        lab = dec.label_heads(qs[0], tau=0.10)
+        e1.record()
+        torch.cuda.synchronize()
+        label_ms = e0.elapsed_time(e1)
+        props = (lab["bgt0"], lab["kslope"], lab["streaming"])
+        props_host = tuple(t.cpu().numpy() for t in props)
+    elif fixed is None:
+        props_host = head_props(B, H, seed=1 + rank)
+        props = tuple(torch.as_tensor(x, device=dev) for x in props_host)
+    else:
+        props = None
+    plan_kw = dict(fixed=fixed) if fixed is not None else dict(props=props)
 
     step_i = [0]
 
     def one_step():
         # one decode step, then the append of its token (append_new after a step,
-        # pipeline.cpp:410-412).  (step(append=...) fuses the append into the next
-        # step's plan kernel instead; measured ~1 % slower here, so not used.)
+        # pipeline.cpp:410-412)
         i = step_i[0]
-        dec.step(qs[i], props=props)
+        dec.step(qs[i], **plan_kw)
         dec.append(kv_new[i, 0], kv_new[i, 1])
         step_i[0] += 1
 
@@ -521,6 +826,13 @@ def run_ours(a):
     ms_per_step = ms / a.steps
     value = world * a.steps / (ms / 1e3)
 
+    def max_over_ranks(x):
+        if world > 1:
+            tt = torch.tensor([x], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt.item())
+        return x
+
     # the same K steps captured once as a CUDA graph (untimed) and replayed:
     # every kernel still runs; only the host launch path leaves the loop
     graph = None
@@ -541,11 +853,7 @@ def run_ours(a):
             g.replay()
             t1.record()
             torch.cuda.synchronize()
-            gms = t0.elapsed_time(t1)
-            if world > 1:
-                tt = torch.tensor([gms], device=dev)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                gms = float(tt.item())
+            gms = max_over_ranks(t0.elapsed_time(t1))
             graph = {"value": world * a.steps / (gms / 1e3), "ms_per_step": gms / a.steps,
                      "how": f"{a.steps} steps captured once as one CUDA graph (PDL edges kept), "
                             f"replayed once inside the timed region"}
@@ -556,11 +864,12 @@ def run_ours(a):
 
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
               "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-              "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+              "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+              "dtype": a.kv_dtype,
               "data": ("synthetic: the reference's generate(spec) on device (WorkloadSpec defaults, "
                        "seed 1 + sequence; N(0,1) K/V with planted needles, local boost, drifting "
-                       "queries); head properties drawn (seed 1)") if a.data == "reference" else
-                      "synthetic (N(0,1) K/V generated on device; head properties drawn, seed 1)",
+                       "queries)") if a.data == "reference" else
+                      "synthetic (N(0,1) K/V generated on device)",
               "gpu_launches": int(launches), "clocks": clk, "graph_replay": graph}
 
     if a.quick:
@@ -595,20 +904,28 @@ def run_ours(a):
         peak, peak_kind = peaks()
         attend_ms = kt.get("attend", float("nan"))
         achieved = attend_b / a.steps / (attend_ms * 1e-3) / 1e9
-        result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3+K4)",
+        tag = a.workload if a.plan == WORKLOADS[a.workload]["plan"] else f"{a.workload}_{a.plan}"
+        tr = ncu_traffic("k_attend", tag)
+        kname = "k_attend_tma (K3+K4)" if a.kv_dtype == "bf16" else "k_attend_generic (K3+K4, f32)"
+        result["roofline"] = {"bound": "hbm", "kernel": kname,
                               "achieved": achieved, "peak": peak, "unit": "GB/s",
-                              "frac": achieved / peak, "peak_kind": peak_kind, "timing": "per-kernel CUDA events in a separate pass with PDL off (events bracket each kernel alone)",
-                              "traffic": (ncu_traffic("k_attend", a.workload) or {}).get("dram_bytes_per_launch"),
-                              "traffic_launch_algorithmic_bytes": (ncu_traffic("k_attend", a.workload) or {}).get(
+                              "frac": achieved / peak, "peak_kind": peak_kind,
+                              "timing": "per-kernel CUDA events on the ctx stream in a separate pass "
+                                        "over the same workload, PDL off (events bracket each kernel "
+                                        "alone)",
+                              "traffic": (tr or {}).get("dram_bytes_per_launch"),
+                              "traffic_source": (tr or {}).get("source"),
+                              "traffic_launch_algorithmic_bytes": (tr or {}).get(
                                   "algorithmic_bytes_of_captured_launch"),
                               "algorithmic_bytes_per_launch": attend_b / a.steps}
         score_ms = kt.get("score", float("nan"))
         step_bytes = (meta_b + attend_b) / a.steps
         result["kernels_ms"] = kt
         result["score_kernel"] = {"ms": score_ms, "metadata_bytes": meta_b / a.steps,
-                                  "GB/s": meta_b / a.steps / (score_ms * 1e-3) / 1e9}
+                                  "GB/s": meta_b / a.steps / (score_ms * 1e-3) / 1e9 if meta_b else None}
         result["step_bytes"] = step_bytes
         result["step_GBps"] = step_bytes / (ms_per_step * 1e-3) / 1e9
+        result["step_frac_of_peak"] = result["step_GBps"] / peak
         # Eq. 3 upper bound of the last step (Σ_h instead of ∪_h): what the
         # per-head reference path would move; the batched K3 reads a block
         # once for all heads of its group
@@ -659,7 +976,7 @@ def run_ours(a):
                 comp.wait_event(ev_in[j])
                 if i >= 2:
                     comp.wait_event(ev_read[j])  # output buffer j copied out
-                dec.step(qd[j], props=props, out=od[j], lse=ld[j])
+                dec.step(qd[j], out=od[j], lse=ld[j], **plan_kw)
                 ev_out[j].record(comp)
                 dec.append(kvd[i % 3][0], kvd[i % 3][1])  # append_new after the step
                 ev_q[j].record(comp)
@@ -674,24 +991,20 @@ def run_ours(a):
             comp.wait_stream(cs)
             t1.record()
             torch.cuda.synchronize()
-            ems = t0.elapsed_time(t1)
-            if world > 1:
-                tt = torch.tensor([ems], device=dev)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                ems = float(tt.item())
+            ems = max_over_ranks(t0.elapsed_time(t1))
             result["e2e"] = {"value": world * a.steps / (ems / 1e3), "unit": UNIT,
                              "h2d_bytes_per_step": int(qd[0].numel() * 4 + kvd[0].numel() * 4),
                              "d2h_bytes_per_step": int(B * H * D * 4 + B * H * 4),
                              "path": "C-ABI fx_decode_step + fx_append_kv per step, pinned "
                                      "host buffers, copies overlapped on a side stream"}
 
-        # ---- predictor-driven plan (C2 as configured: budgets from the predictor) ----
-        # prefill_stats once (anchor = the first query), then every step:
-        # decode_features -> predict -> plan_group -> select -> attend, all on
-        # the device.  Random-init 41->256->384->3 weights (the reference ships
-        # no trained model); the output-layer bias is set to the drawn-props
-        # operating point (bgt0 ~ 0.03, k ~ 0.005, streaming ~ half).
-    if not a.quick and a.workload == "c2":
+    # ---- predictor-driven plan (C2 as configured: budgets from the predictor) ----
+    # prefill_stats once (anchor = the generator's prefill query), then every step:
+    # decode_features -> predict -> plan_group -> select -> attend, all on the
+    # device.  Random-init 41->256->384->3 weights (the reference ships no
+    # trained model); the output-layer bias is set to the drawn-props operating
+    # point (bgt0 ~ 0.03, k ~ 0.005, streaming ~ half).
+    if not a.quick and a.workload == "c2" and a.plan == "props":
         from paper_2605_07719_b200.fluxattn import Predictor
         rs = np.random.default_rng(5)
         params = {"w1": rs.standard_normal((256, 41)) * (2.0 / 41) ** 0.5, "b1": np.zeros(256),
@@ -735,7 +1048,7 @@ def run_ours(a):
             pred_step()
         t1.record()
         torch.cuda.synchronize()
-        pms = t0.elapsed_time(t1)
+        pms = max_over_ranks(t0.elapsed_time(t1))
         # phase split of one more step (events serialize the phases)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         i = step_i[0]
@@ -755,44 +1068,28 @@ def run_ours(a):
             "features_ms": ev[0].elapsed_time(ev[1]), "predict_ms": ev[1].elapsed_time(ev[2]),
             "decode_step_ms": ev[2].elapsed_time(ev[3]), "retrieval_groups": retr_groups,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
-            "per_step": "fx_decode_features + fx_predict + fx_decode_step + fx_append_kv",
+            "per_step": "fx_decode_features + fx_predict + fx_decode_step (append fused)",
             "model": "random-init 41-256-384-3, output bias at the drawn-props operating point"}
         pred.close()
 
-    result["config"] = {
-        "workload": ("C2: Llama-3-8B layer (32q/8kv heads, d128), 128K ctx, batch 16/GPU, "
-                     "per-head budgets + per-group granularity (16/32/64/128) from plan_group")
-        if a.workload == "c2" else
-        ("C4: Llama-3-8B 32-layer decode step, 128K ctx, batch 8/GPU (64 over 8 GPUs), the 32 "
-         "layers' (b, g) tasks in one batched step; per-head budgets from plan_group"),
-        "layers": a.layers,
-        "context": a.context, "global_batch": a.seqs * world, "seq_len": a.context,
-        "parallelism": f"batch-sharded x{world} (no collective)", "kv_dtype": "bf16",
-        "l2": "per-step working set > 1 GB (inputs larger than the 126 MB L2); no flush",
-        "meta_build_ms": meta_build_ms, "generate_ms": gen_ms,
-        "budget_source": "drawn head properties (bgt0~U(.01,.05), k~U(0,.01), streaming~B(.5))"}
+    result["config"] = workload_config(a, world)
+    result["setup"] = {"meta_build_ms": meta_build_ms, "generate_ms": gen_ms,
+                       "label_ms": label_ms}
 
-    # ---- CPU baseline: the compiled reference on a bounded sample (rank 0, N=1) ----
+    # ---- CPU baseline + in-run parity: the compiled reference on this step's data ----
     if rank == 0 and world == 1 and not a.quick and not a.no_cpu_baseline:
         try:
-            from oracle.oracle import RefOracle
-            ref = RefOracle()
-            cores = os.cpu_count() or 1
-            workers = max(1, cores - 1)
-            kk = dec.k[0, :, : a.context].float().cpu().numpy()
-            vv = dec.v[0, :, : a.context].float().cpu().numpy()
-            blk = dec.plan_blk[0].cpu().numpy()
-            bud = dec.plan_budgets[0].cpu().numpy()
-            plans = [None if int(blk[g]) == 0 else (int(blk[g]), bud[g * G:(g + 1) * G])
-                     for g in range(HKV)]
-            qn = qs[step_i[0] - 1, 0].cpu().numpy()
-            times, n_tasks = reference_sample(ref, [(kk[g], vv[g]) for g in range(HKV)], plans,
-                                              qn, workers, 5)
-            t = min(times) * B
-            result["cpu_baseline"] = {
-                "value": 1.0 / t, "unit": UNIT, "cores": workers + 1, "kind": "reference",
-                "sample": f"1 of {B} sequences ({n_tasks} retrieval-group tasks, same plan and "
-                          f"data as the GPU step), best of 5, x{B} extrapolated"}
+            # one more step without its append: the step the reference re-runs
+            i = step_i[0]
+            q_par = qs[i].contiguous()
+            o_par, lse_par = dec.step(q_par, **plan_kw)
+            torch.cuda.synchronize()
+            o_par, lse_par = o_par.clone(), lse_par.clone()
+            cb, par = cpu_baseline_and_parity(a, dec, q_par, o_par, lse_par, props_host,
+                                              parity=not a.no_parity)
+            result["cpu_baseline"] = cb
+            if par is not None:
+                result["parity"] = par
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
                                       "kind": "reference", "sample": f"failed: {e}"}
@@ -804,8 +1101,60 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def run_dry_launch(a):
+    """Launcher self-test (CPU, gloo): every rank times an empty step; the
+    max-over-ranks reduction and the aggregate follow the real arm.  The line
+    says dry_run -- it is never a measurement."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"bench: --gpus {a.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    for _ in range(a.warmup):
+        time.sleep(0.001)
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(a.steps):
+        time.sleep(0.001)
+    ms = (time.perf_counter() - t) * 1e3
+    if world > 1:
+        tt = torch.tensor([ms])
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "ranks": world,
+                          "value": world * a.steps / (ms / 1e3), "unit": UNIT,
+                          "ms_per_step": ms / a.steps, "steps": a.steps, "warmup": a.warmup}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     a = args_parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+               "--nproc-per-node", str(a.gpus), "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        env = dict(os.environ)
+        if a.impl == "ours" and not a.dry_run_launch:
+            env.setdefault("NCCL_DEBUG", "INFO")
+            env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        sys.exit(subprocess.call(cmd, env=env))
+    if a.dry_run_launch:
+        run_dry_launch(a)
+        return
     if a.impl == "reference":
         run_reference_arm(a)
         return

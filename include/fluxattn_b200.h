@@ -131,6 +131,10 @@ FX_API int fx_ctx_destroy(fx_ctx* ctx);
  * stream.  Until this is called the ctx uses its own non-blocking stream. */
 FX_API int fx_ctx_set_stream(fx_ctx* ctx, void* stream);
 FX_API void* fx_ctx_stream(fx_ctx* ctx);
+/* Waits for the ctx stream, then reports device-detected argument errors of
+ * the work since the last call (FX_ERR_INVALID "invalid-granularity: ..." when
+ * a FX_PLAN_GIVEN plan held a block size outside {0, 16, 32, 64, 128}; such
+ * groups are attended over their resident defaults only, like blk 0). */
 FX_API int fx_ctx_synchronize(fx_ctx* ctx);
 /* Kernels launched through this context so far. */
 FX_API uint64_t fx_ctx_launches(fx_ctx* ctx);
@@ -158,8 +162,9 @@ FX_API int fx_memset(fx_ctx* ctx, void* dptr, int value, size_t bytes);
 FX_API int64_t fx_block_count(int64_t rows, int32_t block_size);
 /* bytes of one metadata level for the whole batch */
 FX_API size_t fx_meta_level_bytes(const fx_layout* lay, int32_t block_size);
-/* device scratch fx_decode_step needs (allocated lazily inside the ctx) */
-FX_API size_t fx_step_scratch_bytes(const fx_layout* lay);
+/* device scratch fx_decode_step needs (allocated lazily inside the ctx), for the
+ * ctx's device (its SM count sets the attention grid); ctx NULL = the current device */
+FX_API size_t fx_step_scratch_bytes(fx_ctx* ctx, const fx_layout* lay);
 
 /* ---- K1: metadata -------------------------------------------------------- */
 /* All four candidate levels of every (b, g) in one streaming pass over the cpu

@@ -121,7 +121,7 @@ _SIGS = {
     "fx_memset": (C.c_int, [_p, _p, C.c_int, _sz]),
     "fx_block_count": (_i64, [_i64, _i32]),
     "fx_meta_level_bytes": (_sz, [C.POINTER(Layout), _i32]),
-    "fx_step_scratch_bytes": (_sz, [C.POINTER(Layout)]),
+    "fx_step_scratch_bytes": (_sz, [C.c_void_p, C.POINTER(Layout)]),
     "fx_build_metadata_levels": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _p, _p, _p, _p]),
     "fx_build_metadata": (C.c_int, [_p, _p, _i32, _i64, _i32, _i32, _p]),
     "fx_block_scores": (C.c_int, [_p, _p, _p, _i32, _i64, _i32, _p]),

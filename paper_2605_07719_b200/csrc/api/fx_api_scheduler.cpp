@@ -201,36 +201,48 @@ ScheduleReport run(TaskQueue& queue, const WorkerProfile& workers, RunMode mode,
     rep.workers.resize(1);
     rep.workers[0].accelerator = true;
     const auto t0 = std::chrono::steady_clock::now();
-    // one device step per distinct task shape (one in practice: a decode step)
-    std::vector<bool> done(tasks.size(), false);
-    try {
-        for (std::size_t i = 0; i < tasks.size(); ++i) {
-            if (done[i]) continue;
+    // one device step per distinct task shape (one in practice: a decode step);
+    // a task counts as done only once its batch has executed
+    std::vector<bool> done(tasks.size(), false), claimed(tasks.size(), false);
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        if (claimed[i]) continue;
+        std::vector<std::size_t> idx;
+        std::vector<const SparseTask*> batch;
+        std::vector<TaskResult*> out;
+        try {
             if (!tasks[i].cache || !tasks[i].metadata)
                 throw std::runtime_error("no-context: task has no executable payload");
             const Shape s = shape_of(tasks[i]);
-            std::vector<const SparseTask*> batch;
-            std::vector<TaskResult*> out;
             for (std::size_t j = i; j < tasks.size(); ++j) {
-                if (done[j] || !tasks[j].cache || !tasks[j].metadata || !(shape_of(tasks[j]) == s)) continue;
+                if (claimed[j] || !tasks[j].cache || !tasks[j].metadata || !(shape_of(tasks[j]) == s)) continue;
+                idx.push_back(j);
                 batch.push_back(&tasks[j]);
                 out.push_back(&res[j]);
-                done[j] = true;
+                claimed[j] = true;
             }
             execute_batch(batch, out);
+            for (std::size_t j : idx) done[j] = true;
+        } catch (const std::exception&) {
+            // the reference records the group whose task threw (scheduler.cpp:247-252)
+            if (idx.empty()) idx.push_back(i);
+            for (std::size_t j : idx) {
+                claimed[j] = true;
+                rep.failed_groups.push_back(tasks[j].group_id);
+            }
+            rep.aborted = true;
+            break;
         }
-    } catch (const std::exception&) {
-        for (std::size_t i = 0; i < tasks.size(); ++i)
-            if (!done[i]) rep.failed_groups.push_back(tasks[i].group_id);
-        if (rep.failed_groups.empty() && !tasks.empty()) rep.failed_groups.push_back(tasks.front().group_id);
-        rep.aborted = true;
     }
     const double end = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     rep.makespan = end;
     rep.workers[0].busy = end;
-    rep.workers[0].tasks = static_cast<int>(tasks.size());
-    for (std::size_t i = 0; i < tasks.size(); ++i)
+    int ndone = 0;
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        if (!done[i]) continue;
+        ++ndone;
         rep.events.push_back({static_cast<int>(i), tasks[i].group_id, 0, 0.0, end});
+    }
+    rep.workers[0].tasks = ndone;
     return rep;
 }
 

@@ -89,6 +89,7 @@ struct fx_ctx {
     DevBuf step;  // fx_decode_step scratch
     DevBuf api;   // per-query API scratch
     DevBuf label; // fx_label_heads scratch
+    DevBuf errw;  // sticky device error word (invalid given block sizes), read by fx_ctx_synchronize
     // optional per-kernel CUDA-event timing (fx_ctx_set_timing)
     bool timing = false;
     std::vector<cudaEvent_t> pool;
@@ -180,74 +181,64 @@ struct StepScratch {
     float* part_lse;
 };
 
-StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
+// Offsets of the decode-step scratch regions (one layout for the allocation
+// and for the public size query fx_step_scratch_bytes).
+struct StepOffsets {
+    size_t blk, bud, kb, apx, bits, ck, ci, box, cnt, st, dn, po, pl, total;
+    int64_t approx_stride, box_stride;
+    int words;
+};
+
+StepOffsets step_offsets(const fx_layout& L, int grid) {
     const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
     const int64_t heads = n_bg * L.group_size;
     const int64_t nblk16 = std::max<int64_t>(1, fx::level_blocks(L.l_cpu, 16));
-    const int words = (int)fx::cdiv(nblk16, 32);
     const int64_t tail_max = L.l_cap - L.l_sink - L.l_cpu;
-    const int64_t box_stride =
-        fx::cdiv(L.l_sink, fx::kBoxRows) + fx::cdiv(tail_max, fx::kBoxRows) + nblk16 + 2;
+    StepOffsets o;
+    o.words = (int)fx::cdiv(nblk16, 32);
+    o.approx_stride = (nblk16 + 3) & ~int64_t(3);
+    o.box_stride = fx::cdiv(L.l_sink, fx::kBoxRows) + fx::cdiv(tail_max, fx::kBoxRows) + nblk16 + 2;
     Carve c;
-    const size_t o_blk = c.take<int32_t>(n_bg);
-    const size_t o_bud = c.take<double>(heads);
-    const size_t o_kb = c.take<int32_t>(heads);
-    const size_t o_apx = c.take<float>(heads * ((nblk16 + 3) & ~int64_t(3)));
-    const size_t o_bits = c.take<uint32_t>(heads * words);
+    o.blk = c.take<int32_t>(n_bg);
+    o.bud = c.take<double>(heads);
+    o.kb = c.take<int32_t>(heads);
+    o.apx = c.take<float>(heads * o.approx_stride);
+    o.bits = c.take<uint32_t>(heads * o.words);
     // the band lists use the approx row stride (nblk16 rounded up to 4)
-    const size_t o_ck = c.take<uint64_t>(heads * ((nblk16 + 3) & ~int64_t(3)));
-    const size_t o_ci = c.take<uint32_t>(heads * ((nblk16 + 3) & ~int64_t(3)));
-    const size_t o_box = c.take<fx::Box>(n_bg * box_stride);
-    const size_t o_cnt = c.take<int32_t>(n_bg);
-    const size_t o_st = c.take<int32_t>(n_bg + 1);
-    const size_t o_dn = c.take<int32_t>(2 * n_bg + 1);
-    const size_t o_po = c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
-    const size_t o_pl = c.take<float>((grid + n_bg) * L.group_size);
-    if (alloc) ctx->step.ensure(c.off);
-    char* b = static_cast<char*>(ctx->step.p);
-    StepScratch s;
-    s.blk = reinterpret_cast<int32_t*>(b + o_blk);
-    s.budgets = reinterpret_cast<double*>(b + o_bud);
-    s.kblocks = reinterpret_cast<int32_t*>(b + o_kb);
-    s.approx = reinterpret_cast<float*>(b + o_apx);
-    s.approx_stride = (nblk16 + 3) & ~int64_t(3);
-    s.sel_bits = reinterpret_cast<uint32_t*>(b + o_bits);
-    s.sel_words = words;
-    s.cand_keys = reinterpret_cast<uint64_t*>(b + o_ck);
-    s.cand_ids = reinterpret_cast<uint32_t*>(b + o_ci);
-    s.boxes = reinterpret_cast<fx::Box*>(b + o_box);
-    s.box_stride = box_stride;
-    s.bg_count = reinterpret_cast<int32_t*>(b + o_cnt);
-    s.bg_start = reinterpret_cast<int32_t*>(b + o_st);
-    s.bg_done = reinterpret_cast<int32_t*>(b + o_dn);
-    s.part_o = reinterpret_cast<float*>(b + o_po);
-    s.part_lse = reinterpret_cast<float*>(b + o_pl);
-    return s;
+    o.ck = c.take<uint64_t>(heads * o.approx_stride);
+    o.ci = c.take<uint32_t>(heads * o.approx_stride);
+    o.box = c.take<fx::Box>(n_bg * o.box_stride);
+    o.cnt = c.take<int32_t>(n_bg);
+    o.st = c.take<int32_t>(n_bg + 1);
+    o.dn = c.take<int32_t>(2 * n_bg + 1);
+    o.po = c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
+    o.pl = c.take<float>((grid + n_bg) * L.group_size);
+    o.total = c.off;
+    return o;
 }
 
-size_t step_bytes(const fx_layout& L, int grid) {
-    const int64_t n_bg = (int64_t)L.batch * L.kv_heads;
-    const int64_t heads = n_bg * L.group_size;
-    const int64_t nblk16 = std::max<int64_t>(1, fx::level_blocks(L.l_cpu, 16));
-    const int words = (int)fx::cdiv(nblk16, 32);
-    const int64_t tail_max = L.l_cap - L.l_sink - L.l_cpu;
-    const int64_t box_stride =
-        fx::cdiv(L.l_sink, fx::kBoxRows) + fx::cdiv(tail_max, fx::kBoxRows) + nblk16 + 2;
-    Carve c;
-    c.take<int32_t>(n_bg);
-    c.take<double>(heads);
-    c.take<int32_t>(heads);
-    c.take<float>(heads * ((nblk16 + 3) & ~int64_t(3)));
-    c.take<uint32_t>(heads * words);
-    c.take<uint64_t>(heads * nblk16);
-    c.take<uint32_t>(heads * nblk16);
-    c.take<fx::Box>(n_bg * box_stride);
-    c.take<int32_t>(n_bg);
-    c.take<int32_t>(n_bg + 1);
-    c.take<int32_t>(2 * n_bg + 1);
-    c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
-    c.take<float>((grid + n_bg) * L.group_size);
-    return c.off;
+StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
+    const StepOffsets o = step_offsets(L, grid);
+    if (alloc) ctx->step.ensure(o.total);
+    char* b = static_cast<char*>(ctx->step.p);
+    StepScratch s;
+    s.blk = reinterpret_cast<int32_t*>(b + o.blk);
+    s.budgets = reinterpret_cast<double*>(b + o.bud);
+    s.kblocks = reinterpret_cast<int32_t*>(b + o.kb);
+    s.approx = reinterpret_cast<float*>(b + o.apx);
+    s.approx_stride = o.approx_stride;
+    s.sel_bits = reinterpret_cast<uint32_t*>(b + o.bits);
+    s.sel_words = o.words;
+    s.cand_keys = reinterpret_cast<uint64_t*>(b + o.ck);
+    s.cand_ids = reinterpret_cast<uint32_t*>(b + o.ci);
+    s.boxes = reinterpret_cast<fx::Box*>(b + o.box);
+    s.box_stride = o.box_stride;
+    s.bg_count = reinterpret_cast<int32_t*>(b + o.cnt);
+    s.bg_start = reinterpret_cast<int32_t*>(b + o.st);
+    s.bg_done = reinterpret_cast<int32_t*>(b + o.dn);
+    s.part_o = reinterpret_cast<float*>(b + o.po);
+    s.part_lse = reinterpret_cast<float*>(b + o.pl);
+    return s;
 }
 
 int64_t next_pow2(int64_t x) {
@@ -316,7 +307,7 @@ Planned plan_and_select(fx_ctx* ctx, const fx_layout& L, const fx_step_args* a, 
         fx::launch_prepare(L, l_plan, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
                            a->kslope, a->streaming, p.blk, p.budgets, a->plan_volume,
                            a->plan_cand_volumes, p.kblocks, s.bg_done, st,
-                           ap ? *ap : fx::AppendArgs());
+                           ap ? *ap : fx::AppendArgs(), static_cast<int32_t*>(ctx->errw.p));
     }
     p.launches = 1;
     p.fused = false;
@@ -374,6 +365,8 @@ int fx_ctx_create(int device, fx_ctx** out) {
         c->num_sms = prop.multiProcessorCount;
         FX_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         c->stream = c->own;
+        c->errw.ensure(sizeof(int32_t));
+        FX_CUDA(cudaMemset(c->errw.p, 0, sizeof(int32_t)));
         *out = c;
     });
 }
@@ -388,6 +381,7 @@ int fx_ctx_destroy(fx_ctx* ctx) {
         ctx->step.release();
         ctx->api.release();
         ctx->label.release();
+        ctx->errw.release();
         if (ctx->own) cudaStreamDestroy(ctx->own);
         delete ctx;
     });
@@ -407,6 +401,14 @@ int fx_ctx_synchronize(fx_ctx* ctx) {
     return guarded([&] {
         DeviceGuard g(ctx);
         FX_CUDA(cudaStreamSynchronize(ctx->stream));
+        int32_t e = 0;
+        FX_CUDA(cudaMemcpy(&e, ctx->errw.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (e) {
+            FX_CUDA(cudaMemset(ctx->errw.p, 0, sizeof(int32_t)));
+            fx::fail(FX_ERR_INVALID,
+                     "invalid-granularity: a given plan held a block size outside {0, 16, 32, 64, 128}; "
+                     "those groups attended their resident defaults only");
+        }
     });
 }
 
@@ -492,9 +494,18 @@ size_t fx_meta_level_bytes(const fx_layout* lay, int32_t block_size) {
            lay->head_dim * elem_bytes(lay->dtype);
 }
 
-size_t fx_step_scratch_bytes(const fx_layout* lay) {
+size_t fx_step_scratch_bytes(fx_ctx* ctx, const fx_layout* lay) {
     if (!lay) return 0;
-    return step_bytes(*lay, 148 * 4);
+    int sms = ctx ? ctx->num_sms : 148;
+    if (!ctx) {
+        int dev = 0;
+        cudaDeviceProp prop;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
+            sms = prop.multiProcessorCount;
+        else
+            cudaGetLastError();
+    }
+    return step_offsets(*lay, fx::attend_grid(*lay, false, sms)).total;
 }
 
 int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, void* m16,
@@ -1120,7 +1131,8 @@ int fx_cp_dist_phase(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, i
             StepScratch s = carve_step(ctx, L, grid, true);
             fx::launch_prepare(L, l_plan, a->plan_mode, a->fixed_block_size, a->fixed_budget, a->bgt0,
                                a->kslope, a->streaming, a->plan_blk, a->plan_budgets, a->plan_volume,
-                               a->plan_cand_volumes, a->plan_kblocks, s.bg_done, ctx->stream);
+                               a->plan_cand_volumes, a->plan_kblocks, s.bg_done, ctx->stream,
+                               fx::AppendArgs(), static_cast<int32_t*>(ctx->errw.p));
             fx::launch_approx_scores(L, a->meta, a->q, a->plan_blk, a->plan_kblocks, approx, approx_stride,
                                      ctx->num_sms, ctx->stream, /*rank_all=*/true);
             ctx->launches += 2;

@@ -105,7 +105,8 @@ struct AppendArgs {
 void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed_blk, double fixed_budget,
                     const double* bgt0, const double* kslope, const int32_t* streaming,
                     int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
-                    int32_t* bg_done, cudaStream_t s, const AppendArgs& ap = AppendArgs());
+                    int32_t* bg_done, cudaStream_t s, const AppendArgs& ap = AppendArgs(),
+                    int32_t* err = nullptr);
 void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, int64_t l_cpu,
                               int32_t* kblocks, cudaStream_t s);
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,

@@ -39,7 +39,7 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
                           int32_t* __restrict__ blk_out, double* __restrict__ budgets,
                           double* __restrict__ volume, double* __restrict__ cand,
                           int32_t* __restrict__ kblocks, int32_t* __restrict__ bg_done,
-                          AppendArgs ap) {
+                          AppendArgs ap, int32_t* __restrict__ err) {
     pdl_wait();
     pdl_trigger();
     const int bg = blockIdx.x;
@@ -100,11 +100,19 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
         }
     } else {  // FX_PLAN_GIVEN
         blk = blk_out[bg];
+        // a caller's block size outside {0} u kCandidateBlocks (selector.hpp:12) has no
+        // metadata level: the group falls back to its resident defaults (blk 0) and the
+        // ctx error word reports invalid-granularity at the next fx_ctx_synchronize
+        if (blk != 0 && blk != 16 && blk != 32 && blk != 64 && blk != 128) {
+            if (h == 0 && err) atomicExch(err, 1);
+            blk = 0;
+        }
         bud = act ? budgets[head] : 0.0;
         if (blk > 0) vol = volume_of(blk, l_cpu, seq_sum(bud, G));
     }
+    __syncwarp();  // every lane has read blk_out[bg] before lane 0 rewrites it
     if (h == 0) {
-        if (mode != FX_PLAN_GIVEN) blk_out[bg] = blk;
+        if (mode != FX_PLAN_GIVEN || blk == 0) blk_out[bg] = blk;
         if (volume) volume[bg] = vol;
         if (cand)
             for (int c = 0; c < 4; ++c) cand[bg * 4 + c] = cv[c];
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
 void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed_blk, double fixed_budget,
                     const double* bgt0, const double* kslope, const int32_t* streaming,
                     int32_t* blk, double* budgets, double* volume, double* cand, int32_t* kblocks,
-                    int32_t* bg_done, cudaStream_t s, const AppendArgs& ap) {
+                    int32_t* bg_done, cudaStream_t s, const AppendArgs& ap, int32_t* err) {
     const int n_bg = L.batch * L.kv_heads;
     FX_REQUIRE(L.group_size >= 1 && L.group_size <= 32, FX_ERR_INVALID,
                "bad-shape: group_size must be in [1, 32]");
@@ -191,7 +199,7 @@ void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed
     }
     launch_pdl(k_prepare, n_bg, 32, 0, s, n_bg, L.group_size, l_plan, plan_mode, fixed_blk, fixed_budget,
                                   bgt0, kslope, streaming, blk, budgets, volume, cand, kblocks,
-                                  bg_done, ap);
+                                  bg_done, ap, err);
     FX_CUDA(cudaGetLastError());
 }
 

@@ -178,6 +178,11 @@ class Engine:
     def launches(self) -> int:
         return int(LIB.fx_ctx_launches(self.ctx))
 
+    def synchronize(self) -> None:
+        """Wait for the ctx stream; raises device-detected argument errors
+        (e.g. invalid-granularity from a device-resident given plan)."""
+        check(LIB.fx_ctx_synchronize(self.ctx))
+
     def close(self):
         if getattr(self, "ctx", None):
             LIB.fx_ctx_destroy(self.ctx)
@@ -527,7 +532,11 @@ class SparseDecoder:
             a.plan_mode = N.FX_PLAN_GIVEN
         else:
             a.plan_mode = N.FX_PLAN_GIVEN
-            self.plan_blk.copy_(torch.as_tensor(np.asarray(blk, np.int32)))
+            bk = np.asarray(blk, np.int32)
+            if not np.isin(bk, (0,) + CANDIDATE_BLOCKS).all():
+                raise RuntimeError("invalid-granularity: a given block size must be 0 or one of "
+                                   "16/32/64/128 (selector.hpp:12)")
+            self.plan_blk.copy_(torch.as_tensor(bk))
             bb = np.zeros((self.lay.batch, self.heads))
             bud = np.asarray(budgets, dtype=object)
             for b in range(self.lay.batch):
