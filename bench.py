@@ -791,11 +791,11 @@ def run_ours(a):
     step_i = [0]
 
     def one_step():
-        # one decode step, then the append of its token (append_new after a step,
-        # pipeline.cpp:410-412)
+        # one decode step; the previous step's token (append_new after a step,
+        # pipeline.cpp:410-412) is appended inside this step's first kernel
         i = step_i[0]
-        dec.step(qs[i], **plan_kw)
-        dec.append(kv_new[i, 0], kv_new[i, 1])
+        ap = (kv_new[i - 1, 0], kv_new[i - 1, 1]) if i > 0 else None
+        dec.step(qs[i], append=ap, **plan_kw)
         step_i[0] += 1
 
     for _ in range(a.warmup):
@@ -961,7 +961,7 @@ def run_ours(a):
                     if i >= 2:
                         cs.wait_event(ev_q[i % 2])    # step i-2 read q buffer i%2
                     if i >= 3:
-                        cs.wait_event(ev_kv[i % 3])   # step i-3 appended from kv buffer i%3
+                        cs.wait_event(ev_kv[i % 3])   # step i-2 appended kv_{i-3} from buffer i%3
                     qd[i % 2].copy_(qh[i], non_blocking=True)
                     kvd[i % 3].copy_(kvh[i], non_blocking=True)
                     ev_in[i % 2].record(cs)
@@ -976,11 +976,13 @@ def run_ours(a):
                 comp.wait_event(ev_in[j])
                 if i >= 2:
                     comp.wait_event(ev_read[j])  # output buffer j copied out
-                dec.step(qd[j], out=od[j], lse=ld[j], **plan_kw)
+                # the previous step's token is appended inside this step (append_new)
+                ap = (kvd[(i - 1) % 3][0], kvd[(i - 1) % 3][1]) if i > 0 else None
+                dec.step(qd[j], out=od[j], lse=ld[j], append=ap, **plan_kw)
                 ev_out[j].record(comp)
-                dec.append(kvd[i % 3][0], kvd[i % 3][1])  # append_new after the step
                 ev_q[j].record(comp)
-                ev_kv[i % 3].record(comp)
+                if i > 0:
+                    ev_kv[(i - 1) % 3].record(comp)
                 if i + 1 < a.steps:
                     h2d(i + 1)
                 with torch.cuda.stream(cs):
@@ -995,8 +997,8 @@ def run_ours(a):
             result["e2e"] = {"value": world * a.steps / (ems / 1e3), "unit": UNIT,
                              "h2d_bytes_per_step": int(qd[0].numel() * 4 + kvd[0].numel() * 4),
                              "d2h_bytes_per_step": int(B * H * D * 4 + B * H * 4),
-                             "path": "C-ABI fx_decode_step + fx_append_kv per step, pinned "
-                                     "host buffers, copies overlapped on a side stream"}
+                             "path": "C-ABI fx_decode_step per step (the previous token's append "
+                                     "fused), pinned host buffers, copies overlapped on a side stream"}
 
     # ---- predictor-driven plan (C2 as configured: budgets from the predictor) ----
     # prefill_stats once (anchor = the generator's prefill query), then every step:

@@ -44,17 +44,16 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
     pdl_trigger();
     const int bg = blockIdx.x;
     const int h = threadIdx.x;
-    if (ap.kn) {  // fused append_new of the previous step's token (row ap.row of (b, g))
-        const int64_t o = ((int64_t)bg * ap.l_cap + ap.row) * ap.D;
-        for (int d = h; d < ap.D; d += 32) {
-            const float kx = ap.kn[(int64_t)bg * ap.D + d], vx = ap.vn[(int64_t)bg * ap.D + d];
-            if (ap.bf16) {
-                static_cast<__nv_bfloat16*>(ap.k)[o + d] = __float2bfloat16_rn(kx);
-                static_cast<__nv_bfloat16*>(ap.v)[o + d] = __float2bfloat16_rn(vx);
-            } else {
-                static_cast<float*>(ap.k)[o + d] = kx;
-                static_cast<float*>(ap.v)[o + d] = vx;
-            }
+    // fused append_new of the previous step's token (row ap.row of (b, g)): its
+    // loads are issued with the head-property loads, its stores go out last
+    constexpr int kAppendPerLane = 8;  // D <= 256
+    float ak[kAppendPerLane], av[kAppendPerLane];
+    if (ap.kn) {
+#pragma unroll
+        for (int j = 0; j < kAppendPerLane; ++j) {
+            const int d = h + 32 * j;
+            ak[j] = d < ap.D ? ap.kn[(int64_t)bg * ap.D + d] : 0.f;
+            av[j] = d < ap.D ? ap.vn[(int64_t)bg * ap.D + d] : 0.f;
         }
     }
     const bool act = h < G;
@@ -120,6 +119,21 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
     if (act) {
         if (mode != FX_PLAN_GIVEN) budgets[head] = bud;
         if (kblocks) kblocks[head] = blk > 0 ? blocks_for_budget(bud, l_cpu, blk) : 0;
+    }
+    if (ap.kn) {
+        const int64_t o = ((int64_t)bg * ap.l_cap + ap.row) * ap.D;
+#pragma unroll
+        for (int j = 0; j < kAppendPerLane; ++j) {
+            const int d = h + 32 * j;
+            if (d >= ap.D) break;
+            if (ap.bf16) {
+                static_cast<__nv_bfloat16*>(ap.k)[o + d] = __float2bfloat16_rn(ak[j]);
+                static_cast<__nv_bfloat16*>(ap.v)[o + d] = __float2bfloat16_rn(av[j]);
+            } else {
+                static_cast<float*>(ap.k)[o + d] = ak[j];
+                static_cast<float*>(ap.v)[o + d] = av[j];
+            }
+        }
     }
 }
 
@@ -192,6 +206,7 @@ void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed
     const int n_bg = L.batch * L.kv_heads;
     FX_REQUIRE(L.group_size >= 1 && L.group_size <= 32, FX_ERR_INVALID,
                "bad-shape: group_size must be in [1, 32]");
+    FX_REQUIRE(ap.kn == nullptr || ap.D <= 256, FX_ERR_INVALID, "bad-shape: fused append needs head_dim <= 256");
     if (plan_mode == FX_PLAN_FIXED) {
         bool ok = false;
         for (int c = 0; c < 4; ++c) ok |= kLevels[c] == fixed_blk;

@@ -12,8 +12,12 @@ rng = np.random.default_rng(1)
 H = 32
 props = tuple(torch.as_tensor(x, device=dev) for x in (rng.uniform(0.01, 0.05, (B, H)), rng.uniform(0, 0.01, (B, H)), (rng.random((B, H)) < 0.5).astype(np.int32)))
 q = torch.randn((B, H, D), device=dev)
-for i in range(6):
-    dec.step(q, props=props)
+import time
+t = time.time()
+while time.time() - t < 2.0:  # warm: SM clocks up before the traced step
+    for i in range(50):
+        dec.step(q, props=props)
+    torch.cuda.synchronize()
 torch.cuda.synchronize()
 tr = np.zeros(8 * 512, np.int64)
 N.LIB.fx_debug_score_trace.argtypes = [C.c_void_p, C.c_int]
@@ -26,4 +30,8 @@ for i, name in enumerate(["start (after pdl_wait)", "producer first TMA", "consu
 items = t[:, 5]
 per = (t[:, 3] - t[:, 2]) / np.maximum(items, 1)
 print("items per CTA min %d median %d max %d; ns per item (first box -> end) median %.0f" % (items.min(), np.median(items), items.max(), np.median(per)))
+for i, name in ((6, "plan: props staged"), (7, "plan: volumes")):
+    x = (t[:, i] - t0) / 1e3
+    if (t[:, i] > 0).all():
+        print("%-24s min %.2f median %.2f max %.2f" % (name, x.min(), np.median(x), x.max()))
 print("end - last TMA issue median %.2f us" % (np.median(t[:, 3] - t[:, 4]) / 1e3))
