@@ -317,19 +317,18 @@ __device__ void finish_cta(const View& p, int64_t NB, int grid, int t, int nt, i
                            MergeSmem<MG>* ms, bool fast) {
     const int nruns = ms->nruns;  // written before the caller's last barrier
     if (nruns == 0) return;
-    __threadfence();
-    named_bar_sync(bar, nt);
+    named_bar_sync(bar, nt);  // the partials are written; the release below publishes them
     if (t < nruns) {  // both counter round trips in flight together
         const int bg = ms->runs[t];
         const int cf = cta_of(ms->rs[t], NB, grid), cl = cta_of(ms->re[t] - 1, NB, grid);
         int n = 0;
         for (int c = cf; c <= cl; ++c) n += cta_nonempty(c, NB, grid);
-        ms->flag[t] = atomicAdd(p.bg_done + bg, 1) == n - 1;
+        ms->flag[t] = atomic_add_acq_rel_gpu(p.bg_done + bg, 1) == n - 1;
     }
     named_bar_sync(bar, nt);
     for (int k = 0; k < nruns; ++k) {
         if (!ms->flag[k]) continue;
-        __threadfence();
+        fence_acq_rel_gpu();
         const int bg = ms->runs[k];
         if (fast) {
             const int cf = cta_of(ms->rs[k], NB, grid), cl = cta_of(ms->re[k] - 1, NB, grid);

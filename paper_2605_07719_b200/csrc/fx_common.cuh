@@ -166,6 +166,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+// "Last CTA to finish" hand-offs.  Writer side: every thread's global writes,
+// then a CTA barrier, then ONE thread's acq_rel counter atomic (release is
+// cumulative over the writes the barrier ordered before it; the CUTLASS
+// semaphore pattern) -- no per-thread fence.  Reader side (the CTA that saw
+// the final count): fence_acq_rel_gpu() before reading the others' data.
+// Both replace __threadfence(), which is a sequentially-consistent MEMBAR.SC.
+__device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // Non-blocking probe (never suspends the warp in the barrier unit).
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
     uint32_t ok;

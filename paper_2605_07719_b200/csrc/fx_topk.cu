@@ -447,12 +447,11 @@ __global__ void __launch_bounds__(kT) k_select(
     __shared__ int s_last;
     __shared__ int64_t s_wsum[kT + 1];
     const int bg = (int)(blockIdx.x / G);
-    __threadfence();  // this head's bits visible before the group counter moves
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(sel_done + bg, 1) == G - 1;
+    __syncthreads();  // this head's bits written; the release below publishes them
+    if (threadIdx.x == 0) s_last = atomic_add_acq_rel_gpu(sel_done + bg, 1) == G - 1;
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
+    fence_acq_rel_gpu();
     // dynamic smem (keys | histogram | ...) is free now: the per-word box counts
     extern __shared__ __align__(16) unsigned char dsm[];
     int32_t* wcnt = reinterpret_cast<int32_t*>(dsm);

@@ -211,12 +211,11 @@ __device__ inline void worklist_publish(const WorklistArgs& w, int n_bg) {
     __shared__ int s_last;
     __shared__ int wtot[32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nt = blockDim.x;
-    __threadfence();
     __syncthreads();
-    if (t == 0) s_last = atomicAdd(w.publish_done, 1) == n_bg - 1;
+    if (t == 0) s_last = atomic_add_acq_rel_gpu(w.publish_done, 1) == n_bg - 1;
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
+    fence_acq_rel_gpu();
     const int nw = nt / 32;
     for (int i0 = 0, run = 0; i0 < n_bg; i0 += nt) {
         const int i = i0 + t;
