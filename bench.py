@@ -1037,8 +1037,7 @@ def run_ours(a):
 
         def pred_step():
             i = step_i[0]
-            dec.decode_features(qs[i], rec, out=feats)
-            pp = pred(feats)
+            pp = dec.predict_props(qs[i], rec, pred)  # features + predictor, one launch
             dec.step(qs[i], props=pp, append=(kv_new[i - 1, 0], kv_new[i - 1, 1]))
             step_i[0] += 1
 
@@ -1051,26 +1050,31 @@ def run_ours(a):
         t1.record()
         torch.cuda.synchronize()
         pms = max_over_ranks(t0.elapsed_time(t1))
-        # phase split of one more step (events serialize the phases)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        # phase split of one more step (events serialize the phases), and the
+        # two-launch feature path (fx_decode_features + fx_predict) for reference
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         i = step_i[0]
         ev[0].record()
-        dec.decode_features(qs[i], rec, out=feats)
+        pp = dec.predict_props(qs[i], rec, pred)
         ev[1].record()
-        pp = pred(feats)
-        ev[2].record()
         dec.step(qs[i], props=pp, append=(kv_new[i - 1, 0], kv_new[i - 1, 1]))
+        ev[2].record()
+        dec.decode_features(qs[i], rec, out=feats)
         ev[3].record()
+        pred(feats)
+        ev[4].record()
         step_i[0] += 1
         torch.cuda.synchronize()
         stream_frac = float(pp[2].float().mean().item())
         retr_groups = int((dec.plan_blk > 0).sum().item())
         result["predictor_path"] = {
             "value": world * a.steps / (pms / 1e3), "unit": UNIT, "ms_per_step": pms / a.steps,
-            "features_ms": ev[0].elapsed_time(ev[1]), "predict_ms": ev[1].elapsed_time(ev[2]),
-            "decode_step_ms": ev[2].elapsed_time(ev[3]), "retrieval_groups": retr_groups,
+            "predict_props_ms": ev[0].elapsed_time(ev[1]), "decode_step_ms": ev[1].elapsed_time(ev[2]),
+            "two_launch_features_ms": ev[2].elapsed_time(ev[3]), "two_launch_predict_ms": ev[3].elapsed_time(ev[4]),
+            "retrieval_groups": retr_groups,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
-            "per_step": "fx_decode_features + fx_predict + fx_decode_step (append fused)",
+            "per_step": "fx_predict_props (decode features + predictor, one clustered launch) + "
+                        "fx_decode_step (append fused)",
             "model": "random-init 41-256-384-3, output bias at the drawn-props operating point"}
         pred.close()
 

@@ -214,6 +214,9 @@ FX_API int fx_model_destroy(fx_model* m);
 /* predict() for n raw feature vectors [dev] [n][41] f64 -> head properties
  * bgt0 = clamp(z0,0,1), k = z1, streaming = sigmoid(z2) >= 0.5 (pipeline.cpp:287-288).
  * z [dev, optional] [n][3] raw logits. */
+/* Rows are tiled (8 per CTA) so each weight is read once per tile; a model
+ * keeps one activation scratch, so calls sharing a model are serialized by
+ * the caller (one stream). */
 FX_API int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features, double* bgt0,
                double* kslope, int32_t* streaming, double* z);
 
@@ -286,6 +289,20 @@ FX_API int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, co
  * Feed to fx_predict. */
 FX_API int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
                               int64_t l_new, const float* q, const double* rec, double* features);
+/* decode_features + normalize + predict for every head (features.cpp:162-233,
+ * predictor.cpp:161-185, pipeline.cpp:277-290): the features in ONE launch --
+ * the Hkv groups of a sequence run as one thread-block cluster and exchange
+ * the cross-head maximum (feature 39) through distributed shared memory --
+ * then the predictor's three tiled layers.  Writes the head properties
+ * bgt0 / kslope / streaming [dev] [B][H] (feed them to fx_decode_step,
+ * FX_PLAN_PROPS); features [dev] [B][H][41] and raw logits z [dev] [B][H][3]
+ * are optional.  Shapes the clustered kernel does not cover (group size
+ * outside {1,2,4,7,8}, head_dim not 64/128, kv_heads > 8) take the
+ * fx_decode_features kernels instead, with the same results. */
+FX_API int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
+                            int64_t l_new, const float* q, const double* rec, const fx_model* model,
+                            double* features, double* z, double* bgt0, double* kslope,
+                            int32_t* streaming);
 
 /* ---- synthetic workload generator (workload.cpp) ------------------------- */
 /* WorkloadSpec (workload.hpp:16-54), same fields and defaults semantics. */

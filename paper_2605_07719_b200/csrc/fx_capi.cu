@@ -105,6 +105,7 @@ struct fx_ctx {
 struct fx_model {
     fx_ctx* ctx = nullptr;
     DevBuf buf;
+    DevBuf act;  // hidden activations of the tiled layers (grown to the largest batch)
     const double *w1t, *b1, *w2t, *b2, *w3t, *b3, *mu, *sigma;
 };
 
@@ -666,6 +667,7 @@ int fx_model_destroy(fx_model* m) {
         if (!m) return;
         cudaSetDevice(m->ctx->device);
         m->buf.release();
+        m->act.release();
         delete m;
     });
 }
@@ -675,9 +677,11 @@ int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features
     return guarded([&] {
         DeviceGuard g(ctx);
         FX_REQUIRE(m != nullptr, FX_ERR_STATE, "no-model: predictor source requires a model");
+        auto* mm = const_cast<fx_model*>(m);
+        mm->act.ensure(fx::predict_scratch_bytes(n));
         fx::launch_predict(n, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma,
-                           features, bgt0, kslope, streaming, z, ctx->stream);
-        ctx->launches += n > 0 ? 1 : 0;
+                           features, bgt0, kslope, streaming, z, mm->act.p, ctx->stream);
+        ctx->launches += n > 0 ? 3 : 0;
     });
 }
 
@@ -943,6 +947,35 @@ int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const v
         ctx->api.ensure(fx::decode_features_scratch_bytes(L, l_new));
         fx::launch_decode_features(L, k, v, l_new, q, rec, features, ctx->api.p, ctx->stream);
         ctx->launches += 3;
+    });
+}
+
+int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v, int64_t l_new,
+                     const float* q, const double* rec, const fx_model* m, double* features, double* z,
+                     double* bgt0, double* kslope, int32_t* streaming) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        const fx_layout& L = *lay;
+        FX_REQUIRE(m != nullptr, FX_ERR_STATE, "no-model: predictor source requires a model");
+        FX_REQUIRE(k && v && q && rec && bgt0 && kslope && streaming, FX_ERR_STATE,
+                   "no-context: predictor step has no payload");
+        FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_new <= L.l_cap, FX_ERR_INVALID,
+                   "bad-shape: decoded rows exceed l_cap");
+        const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
+        const bool fused = fx::feat_fused_supported(L);
+        const size_t fs = fused ? 0 : fx::decode_features_scratch_bytes(L, l_new);
+        const size_t fb = features ? 0 : (size_t)nh * 41 * sizeof(double);
+        ctx->api.ensure(fs + fb + 256);
+        double* f = features ? features
+                             : reinterpret_cast<double*>(static_cast<char*>(ctx->api.p) + ((fs + 255) & ~size_t(255)));
+        if (fused) fx::launch_feat_fused(L, k, v, l_new, q, rec, f, ctx->stream);  // one clustered launch
+        else fx::launch_decode_features(L, k, v, l_new, q, rec, f, ctx->api.p, ctx->stream);
+        auto* mm = const_cast<fx_model*>(m);
+        mm->act.ensure(fx::predict_scratch_bytes((int)nh));
+        fx::launch_predict((int)nh, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma, f, bgt0,
+                           kslope, streaming, z, mm->act.p, ctx->stream);
+        ctx->launches += (fused ? 1 : 3) + 3;
     });
 }
 

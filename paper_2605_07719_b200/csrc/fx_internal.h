@@ -109,10 +109,13 @@ void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed
                     int32_t* err = nullptr);
 void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, int64_t l_cpu,
                               int32_t* kblocks, cudaStream_t s);
+// the 41-256-384-3 predictor as three tiled f64 layer kernels; scratch holds
+// the hidden activations (predict_scratch_bytes(n))
+size_t predict_scratch_bytes(int n);
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
                     const double* b2, const double* w3t, const double* b3, const double* mu,
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
-                    int32_t* streaming, double* z, cudaStream_t s);
+                    int32_t* streaming, double* z, void* scratch, cudaStream_t s);
 
 // fx_score.cu / fx_topk.cu / fx_select.cu
 double approx_eps_scale(const fx_layout& L);
@@ -167,6 +170,11 @@ size_t decode_features_scratch_bytes(const fx_layout& L, int64_t l_new);
 void launch_decode_features(const fx_layout& L, const void* k, const void* v, int64_t l_new,
                             const float* q, const double* rec, double* feats, void* scratch,
                             cudaStream_t s);
+
+// fx_predict_step.cu: decode features of every head in one clustered launch
+bool feat_fused_supported(const fx_layout& L);
+void launch_feat_fused(const fx_layout& L, const void* k, const void* v, int64_t l_new, const float* q,
+                       const double* rec, double* feats, cudaStream_t s);
 
 // fx_workload.cu: generate(spec) into the device cache
 void generate_workload(const fx_layout& L, const fx_workload_spec& sp, const uint64_t* seeds,

@@ -9,6 +9,8 @@
 // __dadd_rn, ...) in the reference's operation order: the reference host
 // build has no FMA (no -march), and contraction would move results by an
 // ulp, which can flip k = ceil(.) at a boundary.
+#include <algorithm>
+
 #include "fx_common.cuh"
 #include "fx_selector_math.h"
 
@@ -144,56 +146,155 @@ __global__ void k_blocks_for_budget(int n, const double* __restrict__ budgets,
     if (i < n) out[i] = blocks_for_budget(budgets[i], l_cpu, blk[i]);
 }
 
-// predictor.cpp:40-53 linear_forward (bias-first, sequential, unfused) with
-// weights stored transposed [in][out] so that thread o reads coalesced.
-__device__ __forceinline__ double linear_row(const double* __restrict__ wt, double bias,
-                                             const double* a, int in, int out, int o) {
-    double s = bias;
-    for (int i = 0; i < in; ++i) s = __dadd_rn(s, __dmul_rn(a[i], wt[(int64_t)i * out + o]));
-    return s;
+// predictor.cpp:40-53 linear_forward (bias first, inputs in order, unfused)
+// as tiled f64 layers over all rows of the batch.  A CTA owns kMR rows x kMN
+// neurons: the rows' inputs sit in shared memory, the weights (transposed
+// [in][out]) stream through a 2-stage cp.async ring of kKC-input tiles, and
+// each thread carries kMC independent chains (rows) of one neuron, adding the
+// inputs in order -- each weight is read once per kMR rows, and the inner
+// loop touches only shared memory and the FP64 pipe.
+constexpr int kF = 41, kH1 = 256, kH2 = 384;
+constexpr int kMR = 16, kMN = 64, kMT = 256, kKC = 32;  // rows, neurons, threads, inputs per tile
+constexpr int kMC = kMR / (kMT / kMN);                   // chains per thread
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int IN, int OUT, bool NORM>
+__global__ void __launch_bounds__(kMT) k_mlp_layer(int n, const double* __restrict__ x,
+                                                   const double* __restrict__ wt,
+                                                   const double* __restrict__ bias,
+                                                   const double* __restrict__ mu,
+                                                   const double* __restrict__ sigma,
+                                                   double* __restrict__ y) {
+    constexpr int NCH = (IN + kKC - 1) / kKC;
+    extern __shared__ __align__(16) double msm[];
+    double (*ws)[kKC * kMN] = reinterpret_cast<double (*)[kKC * kMN]>(msm);  // [2][kKC * kMN]
+    double* xs = msm + 2 * kKC * kMN;                                       // [kMR][IN]
+    const int r0 = blockIdx.x * kMR, n0 = blockIdx.y * kMN;
+    const int t = threadIdx.x, nl = t % kMN, rg = t / kMN;
+    auto load_tile = [&](int c, int st) {  // inputs [c*kKC, +kKC) x neurons [n0, +kMN)
+        for (int e = t; e < kKC * kMN / 2; e += kMT) {
+            const int row = e / (kMN / 2), col = (e % (kMN / 2)) * 2;
+            const int i = c * kKC + row;
+            if (i < IN) cp_async16(&ws[st][row * kMN + col], wt + (int64_t)i * OUT + n0 + col);
+        }
+        cp_async_commit();
+    };
+    load_tile(0, 0);  // weights do not depend on the preceding kernel
+    pdl_wait();
+    pdl_trigger();
+    if (NORM) {  // features.cpp:226-233; all of a thread's loads are issued before any use
+        constexpr int PER = (kMR * IN + kMT - 1) / kMT;
+        double v[PER], m[PER], sg[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int e = t + u * kMT, r = r0 + e / IN, c = e % IN;
+            const bool ok = e < kMR * IN && r < n;
+            v[u] = ok ? x[(int64_t)r * IN + c] : 0.0;
+            m[u] = e < kMR * IN ? mu[c] : 0.0;
+            sg[u] = e < kMR * IN ? sigma[c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int e = t + u * kMT;
+            if (e < kMR * IN) xs[e] = sg[u] > 0.0 ? __ddiv_rn(__dsub_rn(v[u], m[u]), sg[u]) : 0.0;
+        }
+    } else {  // rows of IN doubles (16-byte multiples): asynchronous copies, zero rows past n
+        for (int e = t; e < kMR * IN / 2; e += kMT) {
+            const int r = r0 + (2 * e) / IN;
+            if (r < n) cp_async16(xs + 2 * e, x + (int64_t)r0 * IN + 2 * e);
+            else reinterpret_cast<double2*>(xs)[e] = make_double2(0.0, 0.0);
+        }
+        cp_async_commit();
+    }
+    double acc[kMC];
+    const double b = bias[n0 + nl];
+#pragma unroll
+    for (int j = 0; j < kMC; ++j) acc[j] = b;
+    const double* xr = xs + rg * kMC * IN;
+    for (int c = 0; c < NCH; ++c) {
+        if (c + 1 < NCH) {
+            load_tile(c + 1, (c + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* w = ws[c & 1];
+        const int kn = IN - c * kKC < kKC ? IN - c * kKC : kKC;
+        // the products of 8 inputs first (independent), then the in-order adds:
+        // the add chains never wait on a load or a multiply
+        constexpr int PB = 8;
+        for (int k0 = 0; k0 < kn; k0 += PB) {
+            double p[kMC][PB];
+#pragma unroll
+            for (int kk = 0; kk < PB; ++kk) {
+                const int i = c * kKC + k0 + kk;
+                const double wv = k0 + kk < kn ? w[(k0 + kk) * kMN + nl] : 0.0;
+#pragma unroll
+                for (int j = 0; j < kMC; ++j) p[j][kk] = __dmul_rn(k0 + kk < kn ? xr[j * IN + i] : 0.0, wv);
+            }
+#pragma unroll
+            for (int kk = 0; kk < PB; ++kk)
+                if (k0 + kk < kn)
+#pragma unroll
+                    for (int j = 0; j < kMC; ++j) acc[j] = __dadd_rn(acc[j], p[j][kk]);
+        }
+        __syncthreads();  // the stage is refilled next round
+    }
+#pragma unroll
+    for (int j = 0; j < kMC; ++j) {
+        const int r = r0 + rg * kMC + j;
+        if (r < n) y[(int64_t)r * OUT + n0 + nl] = acc[j] > 0.0 ? acc[j] : 0.0;  // ReLU
+    }
 }
 
-constexpr int kF = 41, kH1 = 256, kH2 = 384;
-
-// One CTA (384 threads) per feature row: normalize -> 41->256->384->3.
-__global__ void __launch_bounds__(384) k_predict(const double* __restrict__ w1t,
-                                                 const double* __restrict__ b1,
-                                                 const double* __restrict__ w2t,
-                                                 const double* __restrict__ b2,
-                                                 const double* __restrict__ w3t,
-                                                 const double* __restrict__ b3,
-                                                 const double* __restrict__ mu,
-                                                 const double* __restrict__ sigma,
-                                                 const double* __restrict__ feats,
-                                                 double* __restrict__ bgt0, double* __restrict__ kslope,
-                                                 int32_t* __restrict__ streaming,
-                                                 double* __restrict__ zout) {
-    __shared__ double x[kF], a1[kH1], a2[kH2];
-    const int r = blockIdx.x, t = threadIdx.x;
-    if (t < kF) {  // features.cpp:226-233
-        const double sg = sigma[t];
-        x[t] = sg > 0.0 ? __ddiv_rn(__dsub_rn(feats[(int64_t)r * kF + t], mu[t]), sg) : 0.0;
+// Output layer (384 -> 3, no activation) and the head properties
+// (predictor.cpp:161-185, pipeline.cpp:288): kOR rows per CTA staged in
+// shared memory, one thread per (row, output) chain.
+constexpr int kOR = 16;
+__global__ void __launch_bounds__(64) k_mlp_out(int n, const double* __restrict__ a2,
+                                                const double* __restrict__ w3t,
+                                                const double* __restrict__ b3,
+                                                double* __restrict__ bgt0, double* __restrict__ kslope,
+                                                int32_t* __restrict__ streaming, double* __restrict__ zout) {
+    extern __shared__ __align__(16) double osm[];
+    double* ws = osm;              // [384][3]
+    double* as = osm + kH2 * 3;    // [kOR][384]
+    for (int i = threadIdx.x; i < kH2 * 3; i += blockDim.x) ws[i] = w3t[i];
+    pdl_wait();
+    pdl_trigger();
+    const int r0 = blockIdx.x * kOR;
+    for (int e = threadIdx.x; e < kOR * kH2 / 2; e += blockDim.x) {  // asynchronous row copies
+        const int r = r0 + (2 * e) / kH2;
+        if (r < n) cp_async16(as + 2 * e, a2 + (int64_t)r0 * kH2 + 2 * e);
+        else reinterpret_cast<double2*>(as)[e] = make_double2(0.0, 0.0);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    if (t < kH1) {
-        const double s = linear_row(w1t, b1[t], x, kF, kH1, t);
-        a1[t] = s > 0.0 ? s : 0.0;
+    const int lr = threadIdx.x / 3, o = threadIdx.x % 3, r = r0 + lr;
+    if (lr >= kOR || r >= n) return;
+    const double* a = as + lr * kH2;
+    double z = b3[o];
+    for (int k0 = 0; k0 < kH2; k0 += 32) {  // 32 products first, then the in-order adds
+        double p[32];
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) p[kk] = __dmul_rn(a[k0 + kk], ws[(k0 + kk) * 3 + o]);
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) z = __dadd_rn(z, p[kk]);
     }
-    __syncthreads();
-    {
-        const double s = linear_row(w2t, b2[t], a1, kH1, kH2, t);
-        a2[t] = s > 0.0 ? s : 0.0;
-    }
-    __syncthreads();
-    if (t < 3) {
-        const double z = linear_row(w3t, b3[t], a2, kH2, 3, t);
-        if (zout) zout[(int64_t)r * 3 + t] = z;
-        if (t == 0) bgt0[r] = clamp01(z);
-        if (t == 1) kslope[r] = z;
-        if (t == 2) {
-            const double sp = 1.0 / (1.0 + exp(-z));  // sigmoid, predictor.cpp:20
-            streaming[r] = sp >= 0.5 ? 1 : 0;          // pipeline.cpp:288
-        }
+    if (zout) zout[(int64_t)r * 3 + o] = z;
+    if (o == 0) bgt0[r] = clamp01(z);
+    if (o == 1) kslope[r] = z;
+    if (o == 2) {
+        const double sp = 1.0 / (1.0 + exp(-z));  // sigmoid, predictor.cpp:20
+        streaming[r] = sp >= 0.5 ? 1 : 0;          // pipeline.cpp:288
     }
 }
 
@@ -225,13 +326,27 @@ void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, 
     FX_CUDA(cudaGetLastError());
 }
 
+size_t predict_scratch_bytes(int n) { return (size_t)std::max(n, 1) * (kH1 + kH2) * sizeof(double); }
+
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
                     const double* b2, const double* w3t, const double* b3, const double* mu,
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
-                    int32_t* streaming, double* z, cudaStream_t s) {
+                    int32_t* streaming, double* z, void* scratch, cudaStream_t s) {
     if (n <= 0) return;
-    k_predict<<<n, kH2, 0, s>>>(w1t, b1, w2t, b2, w3t, b3, mu, sigma, feats, bgt0, kslope,
-                                streaming, z);
+    double* a1 = static_cast<double*>(scratch);
+    double* a2 = a1 + (size_t)n * kH1;
+    const unsigned rt = (unsigned)((n + kMR - 1) / kMR);
+    const size_t s1 = (size_t)(2 * kKC * kMN + kMR * kF) * sizeof(double);
+    const size_t s2 = (size_t)(2 * kKC * kMN + kMR * kH1) * sizeof(double);
+    FX_CUDA(cudaFuncSetAttribute(k_mlp_layer<kF, kH1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
+    FX_CUDA(cudaFuncSetAttribute(k_mlp_layer<kH1, kH2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    launch_pdl(k_mlp_layer<kF, kH1, true>, dim3(rt, kH1 / kMN), kMT, s1, s, n, feats, w1t, b1, mu, sigma, a1);
+    launch_pdl(k_mlp_layer<kH1, kH2, false>, dim3(rt, kH2 / kMN), kMT, s2, s, n, (const double*)a1, w2t, b2,
+               (const double*)nullptr, (const double*)nullptr, a2);
+    const size_t osmem = (size_t)(kH2 * 3 + kOR * kH2) * sizeof(double);
+    FX_CUDA(cudaFuncSetAttribute(k_mlp_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem));
+    launch_pdl(k_mlp_out, (unsigned)((n + kOR - 1) / kOR), 64, osmem, s, n, (const double*)a2, w3t, b3, bgt0,
+               kslope, streaming, z);
     FX_CUDA(cudaGetLastError());
 }
 

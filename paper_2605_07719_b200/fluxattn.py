@@ -680,6 +680,25 @@ class SparseDecoder:
                                      self.l_new, _ptr(qd), _ptr(rec), _ptr(f)))
         return f
 
+    def predict_props(self, q: torch.Tensor, rec: torch.Tensor, model: "Predictor",
+                      features: torch.Tensor = None, z: torch.Tensor = None):
+        """decode_features -> normalize -> predict for every head in one launch
+        (features.cpp:162-233, predictor.cpp:161-185, pipeline.cpp:277-290) ->
+        (bgt0, kslope, streaming) device tensors [B][H], the props of step()."""
+        lay = self.lay
+        dev = self.eng.device
+        shape = (lay.batch, self.heads)
+        if not hasattr(self, "_pp") or self._pp[0].shape != shape:
+            self._pp = (torch.empty(shape, dtype=torch.float64, device=dev),
+                        torch.empty(shape, dtype=torch.float64, device=dev),
+                        torch.empty(shape, dtype=torch.int32, device=dev))
+        b0, ks, st = self._pp
+        qd = q.to(dev, torch.float32).contiguous()
+        check(LIB.fx_predict_props(self.eng.ctx, C.byref(lay), _ptr(self.k), _ptr(self.v), self.l_new,
+                                   _ptr(qd), _ptr(rec), model.h, _ptr(features), _ptr(z), _ptr(b0),
+                                   _ptr(ks), _ptr(st)))
+        return b0, ks, st
+
     def selected_blocks(self, b: int, h: int) -> np.ndarray:
         """Ids of the blocks head h of sequence b selected in the last step."""
         g = h // self.lay.group_size

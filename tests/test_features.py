@@ -125,3 +125,55 @@ def test_predictor_driven_plan(engine, coracle):
             p = coracle.plan_group(b0n[b, sl], ksn[b, sl], stn[b, sl], dec.lay.l_cpu)
             assert int(dec.plan_blk[b, g]) == (0 if p["streaming_group"] else p["block_size"])
     pred.close()
+
+
+@pytest.mark.parametrize("Hkv,G,D,n_new", [(2, 4, 128, 3), (4, 7, 128, 0), (1, 4, 64, 5), (8, 4, 128, 1),
+                                           (3, 2, 64, 5)])
+def test_fused_predict_props(engine, coracle, Hkv, G, D, n_new):
+    """fx_predict_props (decode features + normalize + MLP in one clustered
+    launch; Hkv = 3 takes the two-launch fallback): features within 1e-9 of the
+    oracle (cross-head max through DSMEM included), logits bit-identical to the
+    predictor on those features, and the props equal to the two-launch path's."""
+    from paper_2605_07719_b200.fluxattn import Predictor
+    B = 2
+    dec, host, anchors, rng = _setup(engine, B, Hkv, G, D, 64, 2500, 256, seed=30 + G)
+    rec = dec.prefill_stats(torch.as_tensor(anchors), tau=0.1, layer=1)
+    lay = dec.lay
+    for i in range(n_new):
+        kn = torch.stack([torch.as_tensor(host[(b, g)][0][lay.l_sink + lay.l_cpu + lay.l_local + i])
+                          for b in range(B) for g in range(Hkv)]).reshape(B, Hkv, D).cuda()
+        vn = torch.stack([torch.as_tensor(host[(b, g)][1][lay.l_sink + lay.l_cpu + lay.l_local + i])
+                          for b in range(B) for g in range(Hkv)]).reshape(B, Hkv, D).cuda()
+        dec.append(kn, vn)
+    params = coracle.make_model(5)
+    params["mu"] = np.zeros(41)
+    params["sigma"] = np.ones(41) * 50.0
+    params["sigma"][[0, 1]] = 0.0
+    pred = Predictor(engine, params)
+    q = torch.as_tensor(rng.standard_normal((B, Hkv * G, D)).astype(np.float32)).bfloat16().float().cuda()
+    feats = torch.empty((B, Hkv * G, 41), dtype=torch.float64, device="cuda")
+    z = torch.empty((B, Hkv * G, 3), dtype=torch.float64, device="cuda")
+    b0, ks, st = dec.predict_props(q, rec, pred, features=feats, z=z)
+    torch.cuda.synchronize()
+    f = feats.cpu().numpy()
+    recn = rec.cpu().numpy()
+    seg = (lay.l_sink, lay.l_cpu, lay.l_local, n_new)
+    qn = q.cpu().numpy()
+    for b in range(B):
+        cross = max(coracle.gpu_output_norm(*host[(b, h // G)], seg, qn[b, h]) for h in range(dec.heads))
+        for h in range(dec.heads):
+            w = coracle.decode_features(*host[(b, h // G)], seg, qn[b, h], recn[b, h], cross)
+            assert _close(f[b, h], w), (b, h, np.nonzero(~np.isclose(f[b, h], w, rtol=1e-9))[0])
+    # the predictor on the fused kernel's own features: bit-identical logits
+    z2 = torch.empty_like(z)
+    b2, k2, s2 = pred(feats, z=z2)
+    torch.cuda.synchronize()
+    assert torch.equal(z, z2) and torch.equal(b0, b2) and torch.equal(ks, k2) and torch.equal(st, s2)
+    for b in range(B):
+        for h in range(dec.heads):
+            out, zz = coracle.predict(params, f[b, h])
+            assert np.array_equal(z[b, h].cpu().numpy(), zz), (b, h)
+    # and the two-launch path agrees within the feature tolerance
+    f_ref = dec.decode_features(q, rec).cpu().numpy()
+    assert _close(f, f_ref)
+    pred.close()
