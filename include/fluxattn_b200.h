@@ -172,6 +172,13 @@ FX_API size_t fx_step_scratch_bytes(fx_ctx* ctx, const fx_layout* lay);
  * error bound.  meta*: [B][Hkv][nblk(blk)][2][D] in lay->dtype. */
 FX_API int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, void* meta16,
                              void* meta32, void* meta64, void* meta128, float* absmax);
+/* The same pass with per-block MEAN keys as well (north-star item 1: min /
+ * max / mean representative keys per block at every candidate granularity;
+ * the reference's Quest score uses min / max only, block_index.hpp:16-22):
+ * levels[i] as meta16..meta128 above, means[i] [dev] [B][Hkv][nblk(16 << i)][D]
+ * f32 = the block's row sum / row count. */
+FX_API int fx_build_metadata_means(fx_ctx* ctx, const fx_layout* lay, const void* k, void* const levels[4],
+                                   float* absmax, float* const means[4]);
 /* One matrix at any granularity >= 1 (the per-head reference API). k: [dev]
  * [rows][dim] in dtype; meta: [dev] [nblk][2][dim] in dtype. */
 FX_API int fx_build_metadata(fx_ctx* ctx, const void* k, int32_t dtype, int64_t rows, int32_t dim,

@@ -520,6 +520,20 @@ int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, v
     });
 }
 
+int fx_build_metadata_means(fx_ctx* ctx, const fx_layout* lay, const void* k, void* const levels[4],
+                            float* absmax, float* const means[4]) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        check_layout(lay);
+        FX_REQUIRE(levels && means, FX_ERR_INVALID, "bad-shape: null level / mean arrays");
+        for (int i = 0; i < 4; ++i)
+            FX_REQUIRE(levels[i] && means[i], FX_ERR_INVALID, "bad-shape: every level needs its min/max and mean output");
+        Timed tm(ctx, FX_KERNEL_METADATA);
+        fx::launch_meta_levels(*lay, k, levels[0], levels[1], levels[2], levels[3], absmax, ctx->stream, means);
+        ctx->launches += 1;
+    });
+}
+
 int fx_build_metadata(fx_ctx* ctx, const void* k, int32_t dtype, int64_t rows, int32_t dim,
                       int32_t block_size, void* meta) {
     return guarded([&] {

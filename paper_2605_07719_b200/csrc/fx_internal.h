@@ -87,8 +87,9 @@ inline int64_t level_blocks(int64_t l_cpu, int blk) { return cdiv(l_cpu, blk); }
 
 // ---- kernel launchers (one per .cu) --------------------------------------
 // fx_metadata.cu
+// mean (optional): per-block mean keys of the four levels, f32 [B*Hkv][nblk][D]
 void launch_meta_levels(const fx_layout& L, const void* k, void* m16, void* m32, void* m64,
-                        void* m128, float* absmax, cudaStream_t s);
+                        void* m128, float* absmax, cudaStream_t s, float* const mean[4] = nullptr);
 void launch_meta_generic(const void* k, int dtype, int64_t rows, int dim, int blk, void* meta,
                          cudaStream_t s);
 

@@ -57,128 +57,189 @@ __device__ __forceinline__ uint4 pack16<FX_F32>(const float* v) {
 __device__ __forceinline__ float fold_min(float L, float R) { return (R < L) ? R : L; }
 __device__ __forceinline__ float fold_max(float L, float R) { return (L < R) ? R : L; }
 
-constexpr int kSlab = 128;  // rows per CTA
-constexpr int kWarps = 8;   // 16 rows per warp
+// Streaming builder: every warp owns whole level-128 blocks (128 rows) and
+// walks them in 16-row sub-blocks -- with 16 lanes per row, slot 0 folds rows
+// 0..7, slot 1 rows 8..15 (contiguous, so the slot combine keeps the earlier
+// rows first) -- keeping the running level-32 / -64 / -128 folds and the
+// absmax in registers.  Each warp streams its rows through a private ring of
+// 1-D bulk copies (TMA engine, one mbarrier per stage, ~16 KB in flight per
+// warp, 128 KB per SM) -- no CTA barrier between loads -- and each level's
+// rows leave as one 16-byte store per lane (min from slot 0, max from slot 1).  A CTA covers a
+// contiguous range of one (b, g)'s blocks and reduces absmax once per
+// dimension (one atomic per dim per CTA).  Optional per-block mean keys
+// (f32, sum / rows; north-star item 1, not used by the reference's Quest
+// score) come from the same pass.
+constexpr int kMW = 8;    // warps per CTA
+constexpr int kMB = 16;   // level-128 blocks per warp (the ring's ramp is paid once per warp)
+constexpr int kSub = 16;  // rows per sub-block (= level 16)
 
 template <int DT, int D>
-__global__ void __launch_bounds__(256) k_meta_levels(const typename Elem<DT>::T* __restrict__ k,
-                                                     int64_t l_cap, int64_t l_sink, int64_t l_cpu,
-                                                     typename Elem<DT>::T* __restrict__ m16,
-                                                     typename Elem<DT>::T* __restrict__ m32,
-                                                     typename Elem<DT>::T* __restrict__ m64,
-                                                     typename Elem<DT>::T* __restrict__ m128,
-                                                     float* __restrict__ absmax) {
+struct MetaOut {
+    typename Elem<DT>::T* lv[4];  // levels 16 / 32 / 64 / 128: [B*Hkv][nblk][2][D]
+    float* mean[4];               // optional per-block means [B*Hkv][nblk][D] (f32)
+};
+
+template <int DT, int D, bool MEAN>
+__global__ void __launch_bounds__(kMW * 32, 2) k_meta_stream(const typename Elem<DT>::T* __restrict__ k,
+                                                          int64_t l_cap, int64_t l_sink, int64_t l_cpu,
+                                                          MetaOut<DT, D> out, float* __restrict__ absmax) {
     using T = typename Elem<DT>::T;
     constexpr int V = 16 / Elem<DT>::kBytes;  // elements per 128-bit vector
     constexpr int LPR = D / V;                // lanes per row
     static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "row must fit one warp");
-    constexpr int RPW = 32 / LPR;             // rows per warp load
-    constexpr int RPS = kBoxRows / RPW;       // rows per lane slot (contiguous)
-
-    __shared__ float s16[kWarps][2][D];
-    __shared__ float s32[4][2][D];
-    __shared__ float s64[2][2][D];
-
+    constexpr int NSLOT = 32 / LPR;           // row slots of the warp
+    constexpr int RPS = kSub / NSLOT;         // contiguous rows per slot
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t bg = blockIdx.y;
-    const int64_t slab = blockIdx.x;
     const int slot = lane / LPR, col = (lane % LPR) * V;
+    const int64_t bg = blockIdx.y;
     const T* kb = k + (bg * l_cap + l_sink) * D;
-
-    float mn[V], mx[V];
+    const int64_t n16 = cdiv_dev(l_cpu, 16), n32 = cdiv_dev(l_cpu, 32), n64 = cdiv_dev(l_cpu, 64),
+                  n128 = cdiv_dev(l_cpu, 128);
+    const int64_t nlev[4] = {n16, n32, n64, n128};
+    constexpr bool want_mean = MEAN;
+    float amax[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-        mn[i] = __int_as_float(0x7f800000);
-        mx[i] = -__int_as_float(0x7f800000);
+    for (int j = 0; j < V; ++j) amax[j] = 0.f;
+    // this warp's level-128 blocks: kMB consecutive ones of the CTA's range
+    const int64_t jb0 = ((int64_t)blockIdx.x * kMW + warp) * kMB;
+    const int nsub = (int)max((int64_t)0, min((int64_t)kMB * 8, cdiv_dev(l_cpu - jb0 * 128, kSub)));
+    // this warp's bulk-copy ring: NST sub-blocks of kSub rows in flight
+    constexpr int SB = kSub * D * (int)sizeof(T);
+    constexpr int NST = SB >= 4096 ? 2 : 8192 / SB;
+    extern __shared__ __align__(128) unsigned char msm[];
+    T* ring = reinterpret_cast<T*>(msm) + (size_t)warp * NST * kSub * D;
+    __shared__ __align__(8) uint64_t s_full[kMW][16];
+    uint64_t* full = s_full[warp];
+    auto issue = [&](int sidx) {  // lane 0: rows of sub-block sidx -> stage sidx % NST
+        const int64_t r0 = jb0 * 128 + (int64_t)sidx * kSub;
+        const int rows = (int)min((int64_t)kSub, l_cpu - r0);
+        const int st = sidx % NST;
+        fence_proxy_async();  // the stage's previous rows were read through the generic proxy
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(rows * D * sizeof(T)));
+        bulk_g2s(ring + (size_t)st * kSub * D, kb + r0 * D, (uint32_t)(rows * D * sizeof(T)), &full[st]);
+    };
+    if (lane == 0) {
+        for (int i = 0; i < NST; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+        for (int i = 0; i < NST && i < nsub; ++i) issue(i);
     }
-    const int64_t r0 = slab * kSlab + warp * kBoxRows + slot * RPS;
-    uint4 raw[RPS];
+    __syncwarp();
+    float m32[2][V], m64[2][V], m128[2][V];  // running folds (min, max)
+    float s32[V], s64[V], s128[V];           // running sums (means)
+    auto emit = [&](int lvl, int64_t jl, const float* lo, const float* hi, const float* sum, int rows_per) {
+        if (jl >= nlev[lvl]) return;
+        T* dst = out.lv[lvl] + (bg * nlev[lvl] + jl) * 2 * D + col;
+        if (NSLOT == 1) {  // one lane per vector: both rows
+            *reinterpret_cast<uint4*>(dst) = pack16<DT>(lo);
+            *reinterpret_cast<uint4*>(dst + D) = pack16<DT>(hi);
+        } else if (slot < 2) {  // slot 0 the min row, slot 1 the max row
+            *reinterpret_cast<uint4*>(dst + slot * D) = pack16<DT>(slot == 0 ? lo : hi);
+        }
+        if (MEAN && slot == 0) {
+            const float n = (float)min((int64_t)rows_per, l_cpu - jl * rows_per);
+            float4* md = reinterpret_cast<float4*>(out.mean[lvl] + (bg * nlev[lvl] + jl) * D + col);
 #pragma unroll
-    for (int i = 0; i < RPS; ++i) {
-        const int64_t r = r0 + i;
-        raw[i] = r < l_cpu ? __ldg(reinterpret_cast<const uint4*>(kb + r * D + col))
-                           : make_uint4(0, 0, 0, 0);
-    }
+            for (int j = 0; j < V; j += 4) md[j / 4] = make_float4(sum[j] / n, sum[j + 1] / n, sum[j + 2] / n, sum[j + 3] / n);
+        }
+    };
+    // one sub-block: fold this slot's RPS rows in order, combine the slots in
+    // row order, emit level 16 and carry the level 32 / 64 / 128 folds
+    auto process = [&](int si) {
+        const int st = si % NST;
+        mbar_wait(&full[st], (uint32_t)((si / NST) & 1));
+        const T* rw = ring + (size_t)st * kSub * D + (size_t)(slot * RPS) * D + col;
+        float mn[V], mx[V], sm[V];
 #pragma unroll
-    for (int i = 0; i < RPS; ++i) {
-        if (r0 + i < l_cpu) {
-            float x[V];
-            unpack16<DT>(raw[i], x);
+        for (int j = 0; j < V; ++j) {
+            mn[j] = __int_as_float(0x7f800000);
+            mx[j] = -__int_as_float(0x7f800000);
+            sm[j] = 0.f;
+        }
+        const int64_t rbase = jb0 * 128 + (int64_t)si * kSub + slot * RPS;
+#pragma unroll
+        for (int i = 0; i < RPS; ++i) {
+            if (rbase + i < l_cpu) {
+                float x[V];
+                unpack16<DT>(*reinterpret_cast<const uint4*>(rw + (size_t)i * D), x);
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    mn[j] = fold_min(mn[j], x[j]);
+                    mx[j] = fold_max(mx[j], x[j]);
+                    if (MEAN) sm[j] += x[j];
+                }
+            }
+        }
+#pragma unroll
+        for (int step = LPR; step < 32; step <<= 1) {  // slots in row order: the lower slot is earlier
+            const bool lower = ((lane / step) & 1) == 0;
 #pragma unroll
             for (int j = 0; j < V; ++j) {
-                mn[j] = fold_min(mn[j], x[j]);
-                mx[j] = fold_max(mx[j], x[j]);
+                const float pmn = __shfl_xor_sync(0xffffffffu, mn[j], step);
+                const float pmx = __shfl_xor_sync(0xffffffffu, mx[j], step);
+                mn[j] = lower ? fold_min(mn[j], pmn) : fold_min(pmn, mn[j]);
+                mx[j] = lower ? fold_max(mx[j], pmx) : fold_max(pmx, mx[j]);
+                if (MEAN) {
+                    const float psm = __shfl_xor_sync(0xffffffffu, sm[j], step);
+                    sm[j] = lower ? sm[j] + psm : psm + sm[j];
+                }
             }
         }
-    }
-    // fold the RPW row slots of the warp in row order
-#pragma unroll
-    for (int step = LPR; step < 32; step <<= 1) {
-        const bool lower = ((lane / step) & 1) == 0;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const float pmn = __shfl_xor_sync(0xffffffffu, mn[j], step);
-            const float pmx = __shfl_xor_sync(0xffffffffu, mx[j], step);
-            mn[j] = lower ? fold_min(mn[j], pmn) : fold_min(pmn, mn[j]);
-            mx[j] = lower ? fold_max(mx[j], pmx) : fold_max(pmx, mx[j]);
-        }
-    }
-    const int64_t j16 = slab * kWarps + warp;
-    const int64_t n16 = cdiv_dev(l_cpu, 16);
-    if (slot == 0) {
+        const int64_t j16 = jb0 * 8 + si;
+        emit(0, j16, mn, mx, sm, 16);
+        const int q32 = si & 1, q64 = si & 3, q128 = si & 7;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            s16[warp][0][col + j] = mn[j];
-            s16[warp][1][col + j] = mx[j];
+            m32[0][j] = q32 ? fold_min(m32[0][j], mn[j]) : mn[j];
+            m32[1][j] = q32 ? fold_max(m32[1][j], mx[j]) : mx[j];
+            if (MEAN) s32[j] = q32 ? s32[j] + sm[j] : sm[j];
         }
-        if (j16 < n16) {
-            T* dst = m16 + (bg * n16 + j16) * 2 * D;
-            *reinterpret_cast<uint4*>(dst + col) = pack16<DT>(mn);
-            *reinterpret_cast<uint4*>(dst + D + col) = pack16<DT>(mx);
-        }
-    }
-    __syncthreads();
-    // level 32
-    {
-        const int64_t n32 = cdiv_dev(l_cpu, 32);
-        for (int e = threadIdx.x; e < 4 * 2 * D; e += blockDim.x) {
-            const int i = e / (2 * D), which = (e / D) & 1, d = e % D;
-            const float L = s16[2 * i][which][d], R = s16[2 * i + 1][which][d];
-            const float val = which ? fold_max(L, R) : fold_min(L, R);
-            s32[i][which][d] = val;
-            const int64_t j = slab * 4 + i;
-            if (j < n32) m32[((bg * n32 + j) * 2 + which) * D + d] = Elem<DT>::from_f(val);
-        }
-    }
-    __syncthreads();
-    {
-        const int64_t n64 = cdiv_dev(l_cpu, 64);
-        for (int e = threadIdx.x; e < 2 * 2 * D; e += blockDim.x) {
-            const int i = e / (2 * D), which = (e / D) & 1, d = e % D;
-            const float L = s32[2 * i][which][d], R = s32[2 * i + 1][which][d];
-            const float val = which ? fold_max(L, R) : fold_min(L, R);
-            s64[i][which][d] = val;
-            const int64_t j = slab * 2 + i;
-            if (j < n64) m64[((bg * n64 + j) * 2 + which) * D + d] = Elem<DT>::from_f(val);
-        }
-    }
-    __syncthreads();
-    {
-        const int64_t n128 = cdiv_dev(l_cpu, 128);
-        for (int e = threadIdx.x; e < D; e += blockDim.x) {
-            const float lo = fold_min(s64[0][0][e], s64[1][0][e]);
-            const float hi = fold_max(s64[0][1][e], s64[1][1][e]);
-            if (slab < n128) {
-                T* dst = m128 + (bg * n128 + slab) * 2 * D;
-                dst[e] = Elem<DT>::from_f(lo);
-                dst[D + e] = Elem<DT>::from_f(hi);
+        if (q32 == 1 || si + 1 == nsub) {
+            emit(1, j16 >> 1, m32[0], m32[1], s32, 32);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                m64[0][j] = (q64 >> 1) ? fold_min(m64[0][j], m32[0][j]) : m32[0][j];
+                m64[1][j] = (q64 >> 1) ? fold_max(m64[1][j], m32[1][j]) : m32[1][j];
+                if (MEAN) s64[j] = (q64 >> 1) ? s64[j] + s32[j] : s32[j];
             }
-            if (absmax) {
-                const float a = fmaxf(fabsf(lo), fabsf(hi));
-                atomicMax(reinterpret_cast<int*>(absmax + bg * D + e), __float_as_int(a));
+            if (q64 == 3 || si + 1 == nsub) {
+                emit(2, j16 >> 2, m64[0], m64[1], s64, 64);
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    m128[0][j] = (q128 >> 2) ? fold_min(m128[0][j], m64[0][j]) : m64[0][j];
+                    m128[1][j] = (q128 >> 2) ? fold_max(m128[1][j], m64[1][j]) : m64[1][j];
+                    if (MEAN) s128[j] = (q128 >> 2) ? s128[j] + s64[j] : s64[j];
+                }
+                if (q128 == 7 || si + 1 == nsub) {
+                    emit(3, j16 >> 3, m128[0], m128[1], s128, 128);
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        amax[j] = fmaxf(amax[j], fmaxf(fabsf(m128[0][j]), fabsf(m128[1][j])));
+                }
             }
         }
+    };
+    for (int si = 0; si < nsub; ++si) {
+        process(si);
+        __syncwarp();  // every lane has read the stage
+        if (lane == 0 && si + NST < nsub) issue(si + NST);
     }
+    // absmax: fold the two slots, then the CTA's warps, one atomic per dim
+    __shared__ float s_amax[kMW][D];
+#pragma unroll
+    for (int step = LPR; step < 32; step <<= 1)
+#pragma unroll
+        for (int j = 0; j < V; ++j) amax[j] = fmaxf(amax[j], __shfl_xor_sync(0xffffffffu, amax[j], step));
+    if (slot == 0)
+#pragma unroll
+        for (int j = 0; j < V; ++j) s_amax[warp][col + j] = amax[j];
+    __syncthreads();
+    if (absmax)
+        for (int d = threadIdx.x; d < D; d += blockDim.x) {
+            float a = 0.f;
+#pragma unroll
+            for (int w = 0; w < kMW; ++w) a = fmaxf(a, s_amax[w][d]);
+            if (a > 0.f) atomicMax(reinterpret_cast<int*>(absmax + bg * D + d), __float_as_int(a));
+        }
 }
 
 // Any granularity >= 1: one CTA per block, threads over dims, rows in order.
@@ -201,27 +262,46 @@ __global__ void k_meta_generic(const typename Elem<DT>::T* __restrict__ k, int64
 }
 
 template <int DT, int D>
-void meta_levels_t(const fx_layout& L, const void* k, void* m16, void* m32, void* m64, void* m128,
-                   float* absmax, cudaStream_t s) {
+void meta_levels_t(const fx_layout& L, const void* k, void* const lv[4], float* const mean[4], float* absmax,
+                   cudaStream_t s) {
     using T = typename Elem<DT>::T;
-    const dim3 grid((unsigned)cdiv(L.l_cpu, kSlab), (unsigned)(L.batch * L.kv_heads));
-    k_meta_levels<DT, D><<<grid, 256, 0, s>>>(
-        static_cast<const T*>(k), L.l_cap, L.l_sink, L.l_cpu, static_cast<T*>(m16),
-        static_cast<T*>(m32), static_cast<T*>(m64), static_cast<T*>(m128), absmax);
+    MetaOut<DT, D> out;
+    for (int i = 0; i < 4; ++i) {
+        out.lv[i] = static_cast<T*>(lv[i]);
+        out.mean[i] = mean ? mean[i] : nullptr;
+    }
+    const int64_t n128 = cdiv(L.l_cpu, 128);
+    const dim3 grid((unsigned)cdiv(n128, kMW * kMB), (unsigned)(L.batch * L.kv_heads));
+    constexpr int SB = kSub * D * (int)sizeof(T);
+    constexpr int NST = SB >= 4096 ? 2 : 8192 / SB;
+    const size_t smem = (size_t)kMW * NST * SB;
+    auto kern = mean ? k_meta_stream<DT, D, true> : k_meta_stream<DT, D, false>;
+    FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, kMW * 32, smem, s>>>(static_cast<const T*>(k), L.l_cap, L.l_sink, L.l_cpu, out, absmax);
 }
 
 }  // namespace
 
 void launch_meta_levels(const fx_layout& L, const void* k, void* m16, void* m32, void* m64,
-                        void* m128, float* absmax, cudaStream_t s) {
+                        void* m128, float* absmax, cudaStream_t s, float* const mean[4]) {
     FX_REQUIRE(L.l_cpu > 0, FX_ERR_INVALID, "empty-context: cpu segment is empty");
+    if (mean) {
+        bool all = true, none = true;
+        for (int i = 0; i < 4; ++i) {
+            all = all && mean[i] != nullptr;
+            none = none && mean[i] == nullptr;
+        }
+        FX_REQUIRE(all || none, FX_ERR_INVALID, "bad-shape: per-block means need all four levels or none");
+        if (none) mean = nullptr;
+    }
     if (absmax)
         FX_CUDA(cudaMemsetAsync(absmax, 0, sizeof(float) * L.batch * L.kv_heads * L.head_dim, s));
+    void* const lv[4] = {m16, m32, m64, m128};
     const int D = L.head_dim;
-    if (L.dtype == FX_BF16 && D == 128) meta_levels_t<FX_BF16, 128>(L, k, m16, m32, m64, m128, absmax, s);
-    else if (L.dtype == FX_BF16 && D == 64) meta_levels_t<FX_BF16, 64>(L, k, m16, m32, m64, m128, absmax, s);
-    else if (L.dtype == FX_F32 && D == 128) meta_levels_t<FX_F32, 128>(L, k, m16, m32, m64, m128, absmax, s);
-    else if (L.dtype == FX_F32 && D == 64) meta_levels_t<FX_F32, 64>(L, k, m16, m32, m64, m128, absmax, s);
+    if (L.dtype == FX_BF16 && D == 128) meta_levels_t<FX_BF16, 128>(L, k, lv, mean, absmax, s);
+    else if (L.dtype == FX_BF16 && D == 64) meta_levels_t<FX_BF16, 64>(L, k, lv, mean, absmax, s);
+    else if (L.dtype == FX_F32 && D == 128) meta_levels_t<FX_F32, 128>(L, k, lv, mean, absmax, s);
+    else if (L.dtype == FX_F32 && D == 64) meta_levels_t<FX_F32, 64>(L, k, lv, mean, absmax, s);
     else fail(FX_ERR_INVALID, "bad-shape: batched metadata supports head_dim 64 or 128");
     FX_CUDA(cudaGetLastError());
 }

@@ -460,12 +460,22 @@ class SparseDecoder:
         self.k[b, g, :n] = torch.as_tensor(np.ascontiguousarray(k)).to(self.k.device, self.tdtype)
         self.v[b, g, :n] = torch.as_tensor(np.ascontiguousarray(v)).to(self.v.device, self.tdtype)
 
-    def build_metadata(self) -> None:
-        """K1 over every (b, g): levels 16/32/64/128 + absmax (one launch)."""
+    def build_metadata(self, means: bool = False) -> None:
+        """K1 over every (b, g): levels 16/32/64/128 + absmax (one launch);
+        means=True also writes the per-block mean keys self.means[i]
+        [B][Hkv][nblk][D] f32 (north-star item 1)."""
         if self.lay.l_cpu == 0:
             return
-        check(LIB.fx_build_metadata_levels(self.eng.ctx, C.byref(self.lay), _ptr(self.k),
-                                           *[_ptr(m) for m in self.meta], _ptr(self.absmax)))
+        if not means:
+            check(LIB.fx_build_metadata_levels(self.eng.ctx, C.byref(self.lay), _ptr(self.k),
+                                               *[_ptr(m) for m in self.meta], _ptr(self.absmax)))
+            return
+        lay = self.lay
+        self.means = [torch.empty((lay.batch, lay.kv_heads, m.shape[2], lay.head_dim), dtype=torch.float32,
+                                  device=self.eng.device) for m in self.meta]
+        lv = (C.c_void_p * 4)(*[m.data_ptr() for m in self.meta])
+        mv = (C.c_void_p * 4)(*[m.data_ptr() for m in self.means])
+        check(LIB.fx_build_metadata_means(self.eng.ctx, C.byref(lay), _ptr(self.k), lv, _ptr(self.absmax), mv))
 
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
         """append_new (kv_cache.hpp:68-73) for every group: [B][Hkv][D] f32 device."""

@@ -60,7 +60,8 @@ def make_decoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, dtype, seed, n_ne
 # K1 metadata
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("dtype,D,l_cpu", [("bf16", 128, 1000), ("f32", 128, 777),
-                                           ("bf16", 64, 300), ("f32", 64, 128)])
+                                           ("bf16", 64, 300), ("f32", 64, 128), ("bf16", 128, 4096 * 3 + 40),
+                                           ("bf16", 128, 5)])
 def test_metadata_levels_bitexact(engine, coracle, dtype, D, l_cpu):
     dec, host, _ = make_decoder(engine, 2, 2, 4, D, 64, l_cpu, 256, dtype, seed=1)
     torch.cuda.synchronize()
@@ -73,6 +74,48 @@ def test_metadata_levels_bitexact(engine, coracle, dtype, D, l_cpu):
     am = dec.absmax.cpu().numpy()
     for (b, g), (k, _) in host.items():
         assert np.array_equal(am[b, g], np.abs(k[64:64 + l_cpu]).max(0))
+
+
+@pytest.mark.parametrize("dtype,D", [("bf16", 128), ("f32", 64), ("bf16", 64), ("f32", 128)])
+def test_metadata_signed_zeros_keep_first(engine, coracle, dtype, D):
+    """Blocks full of +0 / -0 ties: the streaming fold keeps the earlier row
+    like the reference's sequential min/max (block_index.cpp:24-31), to the bit."""
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    rng = np.random.default_rng(3)
+    l_cpu = 1000
+    dec = SparseDecoder(engine, 1, 1, 4, D, 64, l_cpu, 256, max_new=4, dtype=dtype)
+    k = rng.standard_normal((64 + l_cpu + 256, D)).astype(np.float32)
+    z = rng.random(k.shape) < 0.6
+    k[z] = np.where(rng.random(z.sum()) < 0.5, 0.0, -0.0).astype(np.float32)
+    if dtype == "bf16":
+        k = bf16_round(k)
+    dec.load_group(0, 0, k, k)
+    dec.build_metadata()
+    torch.cuda.synchronize()
+    for lvl, blk in enumerate((16, 32, 64, 128)):
+        m = dec.meta[lvl].float().cpu().numpy()
+        mins, maxs = coracle.build_metadata(k[64:64 + l_cpu], blk)
+        assert np.array_equal(m[0, 0, :, 0].view(np.uint32), mins.view(np.uint32)), blk
+        assert np.array_equal(m[0, 0, :, 1].view(np.uint32), maxs.view(np.uint32)), blk
+
+
+@pytest.mark.parametrize("dtype,D,l_cpu", [("bf16", 128, 1000), ("f32", 64, 4097), ("bf16", 64, 129)])
+def test_metadata_mean_keys(engine, coracle, dtype, D, l_cpu):
+    """Per-block mean keys (north-star item 1; no reference counterpart): the
+    f64 mean of the block's rows within 1e-5, from the same pass that writes
+    min / max bit-identical to the default build."""
+    dec, host, _ = make_decoder(engine, 2, 2, 4, D, 64, l_cpu, 256, dtype, seed=9)
+    ref = [m.clone() for m in dec.meta]
+    dec.build_metadata(means=True)
+    torch.cuda.synchronize()
+    for lvl, blk in enumerate((16, 32, 64, 128)):
+        assert torch.equal(dec.meta[lvl], ref[lvl])
+        got = dec.means[lvl].cpu().numpy()
+        for (b, g), (k, _) in host.items():
+            kc = k[64:64 + l_cpu].astype(np.float64)
+            nb = (l_cpu + blk - 1) // blk
+            want = np.stack([kc[i * blk:(i + 1) * blk].mean(0) for i in range(nb)])
+            assert np.allclose(got[b, g], want, rtol=1e-5, atol=1e-6), (blk, b, g)
 
 
 @pytest.mark.parametrize("blk", [1, 3, 16, 100])
