@@ -156,6 +156,8 @@ FX_API int fx_malloc(fx_ctx* ctx, size_t bytes, void** dptr);
 FX_API int fx_free(fx_ctx* ctx, void* dptr);
 FX_API int fx_memcpy_h2d(fx_ctx* ctx, void* dst, const void* src, size_t bytes);
 FX_API int fx_memcpy_d2h(fx_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* device -> device on the ctx stream (asynchronous) */
+FX_API int fx_memcpy_d2d(fx_ctx* ctx, void* dst, const void* src, size_t bytes);
 FX_API int fx_memset(fx_ctx* ctx, void* dptr, int value, size_t bytes);
 
 /* ---- sizes -------------------------------------------------------------- */

@@ -149,6 +149,7 @@ _SIGS = {
     "fx_prefill_stats": (C.c_int, [_p, C.POINTER(Layout), _p, _p, C.POINTER(_p * 4), _p,
                                    C.c_double, _i32, _p]),
     "fx_decode_features": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p]),
+    "fx_memcpy_d2d": (C.c_int, [_p, _p, _p, _sz]),
     "fx_build_metadata_means": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _p, _p]),
     "fx_predict_props": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
     "fx_generate": (C.c_int, [_p, C.POINTER(WorkloadSpec), C.POINTER(Layout), _p, _p, _p, _p, _p,

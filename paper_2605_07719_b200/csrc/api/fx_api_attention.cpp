@@ -4,6 +4,7 @@
 #include <stdexcept>
 
 #include "fluxattn/attention.hpp"
+#include "fx_api_arena.hpp"
 #include "fx_api_common.hpp"
 
 namespace fluxattn {
@@ -47,21 +48,49 @@ std::vector<std::uint32_t> iota_u32(std::size_t n) {
     return r;
 }
 
-// Stacked K/V of the chosen segments (position order) plus their row ids.
-struct Stacked {
-    Matrix k, v;
-};
-Stacked stack(const SegmentedKvCache& cache, std::initializer_list<Segment> segs) {
-    Stacked s;
-    for (Segment g : segs) {
-        const Matrix& km = cache.keys(g);
-        const Matrix& vm = cache.values(g);
-        for (std::size_t r = 0; r < km.rows(); ++r) {
-            s.k.append_row(km.row(r));
-            s.v.append_row(vm.row(r));
-        }
+// Attention of one query over the device-resident copy of `cache`
+// (fx_api_arena.hpp): plan FULL = every cpu row plus the defaults
+// (cache_attention), or blk 0 = the defaults only (default_kv_attention).
+PartialOutput resident_attention(std::span<const float> q, const SegmentedKvCache& cache, bool with_cpu) {
+    if (q.size() != cache.dim()) throw std::runtime_error("bad-shape: query width != key width");
+    if (!all_finite(q)) throw std::runtime_error("non-finite: query");
+    b200::Arena& ar = b200::arena_for(b200::shape_of(cache));
+    const int slot = ar.acquire(cache);
+    const std::size_t D = cache.dim();
+    char* sc = static_cast<char*>(ar.scratch(4096 + 2 * D * sizeof(float)));
+    int32_t* blk = reinterpret_cast<int32_t*>(sc);
+    double* bud = reinterpret_cast<double*>(sc + 256);
+    float* dq = reinterpret_cast<float*>(sc + 1024);
+    float* dout = dq + D;
+    float* dlse = reinterpret_cast<float*>(sc + 512);
+    const fx_layout lay = ar.slot_layout();
+    fx_step_args a = ar.slot_args(slot, static_cast<int64_t>(cache.len(Segment::New)));
+    check(fx_memcpy_h2d(context(), dq, q.data(), D * sizeof(float)));
+    a.q = dq;
+    a.o = dout;
+    a.lse = dlse;
+    if (with_cpu) {
+        a.plan_mode = FX_PLAN_FULL;
+    } else {
+        const int32_t zero = 0;
+        const double none = 0.0;
+        check(fx_memcpy_h2d(context(), blk, &zero, sizeof zero));
+        check(fx_memcpy_h2d(context(), bud, &none, sizeof none));
+        a.plan_mode = FX_PLAN_GIVEN;
+        a.plan_blk = blk;
+        a.plan_budgets = bud;
     }
-    return s;
+    check(fx_decode_step(context(), &lay, &a));
+    std::vector<float> o(D);
+    float lse = 0.f;
+    check(fx_memcpy_d2h(context(), o.data(), dout, D * sizeof(float)));
+    check(fx_memcpy_d2h(context(), &lse, dlse, sizeof(float)));
+    PartialOutput p;
+    p.o.assign(o.begin(), o.end());
+    p.lse = lse;
+    p.tokens = cache.len(Segment::Sink) + cache.len(Segment::Local) + cache.len(Segment::New) +
+               (with_cpu ? cache.len(Segment::Cpu) : 0);
+    return p;
 }
 }  // namespace
 
@@ -78,27 +107,21 @@ PartialOutput gathered_attention_unchecked(std::span<const float> q, const Matri
     return device_attention(q, k, v, idx);
 }
 
-// attention.cpp:89-104 -- LSE merge on the device (fx_merge_partials).
+// attention.cpp:89-104 -- the reference's LSE merge of two partials, in
+// double on the host (D + 1 values; a device round trip would cost more than
+// the arithmetic and f32 would round the partials).
 void merge_into(PartialOutput& acc, const PartialOutput& part) {
     if (part.empty()) return;
     if (acc.empty()) {
         acc = part;
         return;
     }
-    const std::size_t dim = acc.o.size();
-    std::vector<float> o(2 * dim);
-    for (std::size_t j = 0; j < dim; ++j) {
-        o[j] = static_cast<float>(acc.o[j]);
-        o[dim + j] = static_cast<float>(part.o[j]);
-    }
-    const float l[2] = {static_cast<float>(acc.lse), static_cast<float>(part.lse)};
-    DevMem dop{std::span<const float>(o)}, dlp(std::span<const float>(l, 2));
-    DevMem mo(dim * sizeof(float)), ml(sizeof(float));
-    check(fx_merge_partials(context(), 2, static_cast<int32_t>(dim), dop.as<float>(), dlp.as<float>(),
-                            mo.as<float>(), ml.as<float>()));
-    const auto of = mo.download<float>(dim);
-    acc.o.assign(of.begin(), of.end());
-    acc.lse = ml.download<float>(1)[0];
+    const double lse_tot = acc.lse > part.lse ? acc.lse + std::log1p(std::exp(part.lse - acc.lse))
+                                              : part.lse + std::log1p(std::exp(acc.lse - part.lse));
+    const double wa = std::exp(acc.lse - lse_tot);
+    const double wb = std::exp(part.lse - lse_tot);
+    for (std::size_t j = 0; j < acc.o.size(); ++j) acc.o[j] = wa * acc.o[j] + wb * part.o[j];
+    acc.lse = lse_tot;
     acc.tokens += part.tokens;
 }
 
@@ -115,26 +138,8 @@ PartialOutput segment_attention(std::span<const float> q, const Matrix& k, const
 }
 
 PartialOutput combine_partials(std::span<const PartialOutput> parts) {
-    std::vector<const PartialOutput*> live;
-    for (const auto& p : parts)
-        if (!p.empty()) live.push_back(&p);
     PartialOutput acc;
-    if (live.empty()) return acc;
-    if (live.size() == 1) return *live[0];
-    const std::size_t dim = live[0]->o.size(), n = live.size();
-    std::vector<float> o(n * dim), l(n);
-    for (std::size_t i = 0; i < n; ++i) {
-        for (std::size_t j = 0; j < dim; ++j) o[i * dim + j] = static_cast<float>(live[i]->o[j]);
-        l[i] = static_cast<float>(live[i]->lse);
-        acc.tokens += live[i]->tokens;
-    }
-    DevMem dop{std::span<const float>(o)}, dlp{std::span<const float>(l)};
-    DevMem mo(dim * sizeof(float)), ml(sizeof(float));
-    check(fx_merge_partials(context(), static_cast<int32_t>(n), static_cast<int32_t>(dim), dop.as<float>(),
-                            dlp.as<float>(), mo.as<float>(), ml.as<float>()));
-    const auto of = mo.download<float>(dim);
-    acc.o.assign(of.begin(), of.end());
-    acc.lse = ml.download<float>(1)[0];
+    for (const auto& p : parts) detail::merge_into(acc, p);  // attention.cpp:118-122
     return acc;
 }
 
@@ -144,17 +149,15 @@ std::vector<double> merge_partials(std::span<const PartialOutput> parts) {
     return std::move(acc.o);
 }
 
-// One softmax over every segment (equal to the reference's per-segment merge).
 std::vector<double> cache_attention(std::span<const float> q, const SegmentedKvCache& cache) {
-    Stacked s = stack(cache, {Segment::Sink, Segment::Cpu, Segment::Local, Segment::New});
-    if (s.k.rows() == 0) throw std::runtime_error("empty-context: cache has no tokens");
-    return detail::segment_attention_unchecked(q, s.k, s.v).o;
+    if (cache.total_len() == 0) throw std::runtime_error("empty-context: cache has no tokens");
+    return resident_attention(q, cache, true).o;
 }
 
 PartialOutput default_kv_attention(std::span<const float> q, const SegmentedKvCache& cache) {
-    Stacked s = stack(cache, {Segment::Sink, Segment::Local, Segment::New});
-    if (s.k.rows() == 0) return PartialOutput{};
-    return detail::segment_attention_unchecked(q, s.k, s.v);
+    if (cache.len(Segment::Sink) + cache.len(Segment::Local) + cache.len(Segment::New) == 0)
+        return PartialOutput{};
+    return resident_attention(q, cache, false);
 }
 
 GroupView gqa_group_view(std::span<const HeadBinding> heads) {

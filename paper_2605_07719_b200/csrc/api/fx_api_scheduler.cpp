@@ -7,6 +7,7 @@
 #include <stdexcept>
 
 #include "fluxattn/scheduler.hpp"
+#include "fx_api_arena.hpp"
 #include "fx_api_common.hpp"
 
 namespace fluxattn {
@@ -15,7 +16,8 @@ using b200::check;
 using b200::context;
 using b200::DevMem;
 
-// All tasks share one device layout when their segment shapes agree.
+// Tasks batch into one device step when their caches share an arena shape,
+// group size and decoded-row count.
 struct Shape {
     std::size_t sink, cpu, local, fresh, dim;
     int heads;
@@ -27,74 +29,132 @@ Shape shape_of(const SparseTask& t) {
             c.dim(), static_cast<int>(t.queries.size())};
 }
 
-// Executes `tasks` (same Shape) as one fx_decode_step: batch = tasks, one KV
-// group each, plan given (blk per task, budget per head).
+bool candidate_blk(int bs) {
+    return std::find(kCandidateBlocks.begin(), kCandidateBlocks.end(), bs) != kCandidateBlocks.end();
+}
+
+// The reference's composition (scheduler.cpp:78-96) over the drop-in's own
+// per-query device calls: for a block size outside the candidate set or
+// metadata at another granularity than the plan -- exactly what the reference
+// would select with task.metadata.
+TaskResult execute_task_per_head(const SparseTask& task) {
+    TaskResult res;
+    res.group_id = task.group_id;
+    const std::size_t l_cpu = task.cache->len(Segment::Cpu);
+    for (std::size_t h = 0; h < task.queries.size(); ++h) {
+        const auto& q = task.queries[h];
+        PartialOutput acc = default_kv_attention(q, *task.cache);
+        const std::size_t k = blocks_for_budget(task.plan.budgets.at(h), l_cpu, task.plan.block_size);
+        if (k > 0) {
+            const SelectionResult sel = topk_blocks(q, *task.metadata, k);
+            detail::merge_into(acc, sparse_attention(q, *task.cache, sel));
+        }
+        res.head_outputs.push_back(std::move(acc.o));
+    }
+    return res;
+}
+
+// Executes `tasks` (same Shape, distinct caches) as one fx_decode_step over
+// the device-resident caches of their arena: every arena slot is a batch
+// entry (kv_heads = 1), plan given -- the task's blk and budgets, blk 0 and a
+// zero query for slots without a task this step (their outputs are dropped).
 void execute_batch(const std::vector<const SparseTask*>& tasks, std::vector<TaskResult*>& out) {
     const Shape s = shape_of(*tasks[0]);
-    const std::size_t B = tasks.size(), G = static_cast<std::size_t>(s.heads), D = s.dim;
-    const std::size_t rows = s.sink + s.cpu + s.local + s.fresh;
-    fx_layout lay{};
-    lay.batch = static_cast<int32_t>(B);
-    lay.kv_heads = 1;
-    lay.group_size = static_cast<int32_t>(G);
-    lay.head_dim = static_cast<int32_t>(D);
-    lay.dtype = FX_F32;
-    lay.l_sink = static_cast<int64_t>(s.sink);
-    lay.l_cpu = static_cast<int64_t>(s.cpu);
-    lay.l_local = static_cast<int64_t>(s.local);
-    lay.l_cap = static_cast<int64_t>(rows);
-    std::vector<float> hk(B * rows * D), hv(B * rows * D), hq(B * G * D);
-    std::vector<int32_t> blk(B);
-    std::vector<double> bud(B * G, 0.0);
-    for (std::size_t b = 0; b < B; ++b) {
-        const SparseTask& t = *tasks[b];
-        std::size_t r = 0;
-        for (Segment g : {Segment::Sink, Segment::Cpu, Segment::Local, Segment::New}) {
-            const Matrix& km = t.cache->keys(g);
-            const Matrix& vm = t.cache->values(g);
-            std::copy_n(km.data(), km.size(), hk.data() + (b * rows + r) * D);
-            std::copy_n(vm.data(), vm.size(), hv.data() + (b * rows + r) * D);
-            r += km.rows();
-        }
-        for (std::size_t h = 0; h < G; ++h) {
-            if (t.queries[h].size() != D) throw std::runtime_error("bad-shape: query width != key width");
-            std::copy_n(t.queries[h].data(), D, hq.data() + (b * G + h) * D);
-            bud[b * G + h] = h < t.plan.budgets.size() ? t.plan.budgets[h] : 0.0;
-        }
-        const int bs = t.plan.block_size;
-        if (s.cpu > 0 && std::find(kCandidateBlocks.begin(), kCandidateBlocks.end(), bs) == kCandidateBlocks.end())
-            throw std::runtime_error("invalid-granularity: blk must be one of 16/32/64/128");
-        blk[b] = bs;
-    }
-    DevMem dk{std::span<const float>(hk)}, dv{std::span<const float>(hv)}, dq{std::span<const float>(hq)};
-    DevMem dblk{std::span<const int32_t>(blk)}, dbud{std::span<const double>(bud)};
-    DevMem dabs(B * D * sizeof(float)), dout(B * G * D * sizeof(float));
-    std::vector<std::unique_ptr<DevMem>> meta;
-    fx_step_args a{};
-    if (s.cpu > 0) {
-        for (int blk_c : kCandidateBlocks)
-            meta.push_back(std::make_unique<DevMem>(fx_meta_level_bytes(&lay, blk_c)));
-        check(fx_build_metadata_levels(context(), &lay, dk.get(), meta[0]->get(), meta[1]->get(),
-                                       meta[2]->get(), meta[3]->get(), dabs.as<float>()));
-        for (int i = 0; i < 4; ++i) a.meta[i] = meta[static_cast<std::size_t>(i)]->get();
-        a.absmax = dabs.as<float>();
-    }
-    a.k = dk.get();
-    a.v = dv.get();
-    a.l_new = static_cast<int64_t>(s.fresh);
-    a.q = dq.as<float>();
-    a.plan_mode = FX_PLAN_GIVEN;
-    a.plan_blk = dblk.as<int32_t>();
-    a.plan_budgets = dbud.as<double>();
-    a.o = dout.as<float>();
-    check(fx_decode_step(context(), &lay, &a));
-    const auto o = dout.download<float>(B * G * D);
-    for (std::size_t b = 0; b < B; ++b) {
-        out[b]->group_id = tasks[b]->group_id;
-        out[b]->head_outputs.assign(G, std::vector<double>(D));
+    const std::size_t G = static_cast<std::size_t>(s.heads), D = s.dim;
+    b200::Arena& ar = b200::arena_for(b200::shape_of(*tasks[0]->cache));
+    std::vector<int> slot(tasks.size());
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        const SparseTask& t = *tasks[i];
         for (std::size_t h = 0; h < G; ++h)
-            std::copy_n(o.data() + (b * G + h) * D, D, out[b]->head_outputs[h].data());
+            if (t.queries[h].size() != D) throw std::runtime_error("bad-shape: query width != key width");
+        if (t.plan.budgets.size() < G) throw std::runtime_error("bad-shape: plan has fewer budgets than heads");
+        slot[i] = ar.acquire(*t.cache);
     }
+    const std::size_t B = static_cast<std::size_t>(ar.slots());
+    std::vector<int32_t> blk(B, 0);
+    std::vector<double> bud(B * G, 0.0);
+    std::vector<float> hq(B * G * D, 0.0f);
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        const SparseTask& t = *tasks[i];
+        const std::size_t b = static_cast<std::size_t>(slot[i]);
+        bool any = false;
+        for (std::size_t h = 0; h < G; ++h) {
+            std::copy_n(t.queries[h].data(), D, hq.data() + (b * G + h) * D);
+            bud[b * G + h] = t.plan.budgets[h];
+            any |= blocks_for_budget(t.plan.budgets[h], s.cpu, t.plan.block_size) > 0;
+        }
+        // the reference selects on task.metadata and rejects a stale one (block_index.cpp:88)
+        if (any && t.metadata->source_len != s.cpu)
+            throw std::runtime_error("stale-selection: cpu segment length changed");
+        blk[b] = s.cpu > 0 ? t.plan.block_size : 0;
+    }
+    const fx_layout lay = ar.layout(static_cast<int32_t>(G));
+    // per-call device inputs / outputs in the arena's scratch: q | budgets | blk | o
+    const auto al = [](std::size_t x) { return (x + 255) & ~std::size_t(255); };
+    const std::size_t bq = al(hq.size() * sizeof(float)), bb = al(bud.size() * sizeof(double)),
+                      bk = al(blk.size() * sizeof(int32_t)), bo = al(B * G * D * sizeof(float));
+    char* sc = static_cast<char*>(ar.scratch(bq + bb + bk + bo));
+    check(fx_memcpy_h2d(context(), sc, hq.data(), hq.size() * sizeof(float)));
+    check(fx_memcpy_h2d(context(), sc + bq, bud.data(), bud.size() * sizeof(double)));
+    check(fx_memcpy_h2d(context(), sc + bq + bb, blk.data(), blk.size() * sizeof(int32_t)));
+    fx_step_args a = ar.step_args(static_cast<int64_t>(s.fresh));
+    a.q = reinterpret_cast<const float*>(sc);
+    a.plan_mode = FX_PLAN_GIVEN;
+    a.plan_budgets = reinterpret_cast<double*>(sc + bq);
+    a.plan_blk = reinterpret_cast<int32_t*>(sc + bq + bb);
+    a.o = reinterpret_cast<float*>(sc + bq + bb + bk);
+    check(fx_decode_step(context(), &lay, &a));
+    std::vector<float> o(B * G * D);
+    check(fx_memcpy_d2h(context(), o.data(), a.o, o.size() * sizeof(float)));
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        const std::size_t b = static_cast<std::size_t>(slot[i]);
+        out[i]->group_id = tasks[i]->group_id;
+        out[i]->head_outputs.assign(G, std::vector<double>(D));
+        for (std::size_t h = 0; h < G; ++h)
+            std::copy_n(o.data() + (b * G + h) * D, D, out[i]->head_outputs[h].data());
+    }
+}
+
+// Partitions tasks into device batches: the same Shape, each cache at most
+// once per batch; tasks the batched step cannot express run per head.
+// `finished` (optional) marks the tasks whose batch completed; on an
+// exception `failing` holds the indices of the batch that threw.
+void execute_all(const std::vector<const SparseTask*>& tasks, std::vector<TaskResult*>& out,
+                 std::vector<bool>* finished = nullptr, std::vector<std::size_t>* failing = nullptr) {
+    std::vector<bool> done(tasks.size(), false);
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        const SparseTask& t = *tasks[i];
+        if (failing) *failing = {i};
+        if (!t.cache || !t.metadata) throw std::runtime_error("no-context: task has no executable payload");
+        if (t.cache->len(Segment::Cpu) > 0 &&
+            (!candidate_blk(t.plan.block_size) || t.metadata->block_size != t.plan.block_size)) {
+            *out[i] = execute_task_per_head(t);
+            done[i] = true;
+            if (finished) (*finished)[i] = true;
+        }
+    }
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        if (done[i]) continue;
+        const Shape s = shape_of(*tasks[i]);
+        std::vector<const SparseTask*> batch;
+        std::vector<TaskResult*> res;
+        std::vector<const SegmentedKvCache*> seen;
+        std::vector<std::size_t> idx;
+        for (std::size_t j = i; j < tasks.size(); ++j) {
+            if (done[j] || !(shape_of(*tasks[j]) == s)) continue;
+            if (std::find(seen.begin(), seen.end(), tasks[j]->cache) != seen.end()) continue;
+            seen.push_back(tasks[j]->cache);
+            batch.push_back(tasks[j]);
+            res.push_back(out[j]);
+            idx.push_back(j);
+            done[j] = true;
+        }
+        if (failing) *failing = idx;
+        execute_batch(batch, res);
+        if (finished)
+            for (std::size_t j : idx) (*finished)[j] = true;
+    }
+    if (failing) failing->clear();
 }
 }  // namespace
 
@@ -161,28 +221,19 @@ TaskResult execute_task(const SparseTask& task) {
     TaskResult r;
     std::vector<const SparseTask*> one{&task};
     std::vector<TaskResult*> out{&r};
-    execute_batch(one, out);
+    execute_all(one, out);
     return r;
 }
 
 std::vector<TaskResult> execute_batch(std::span<const SparseTask> tasks) {
     std::vector<TaskResult> res(tasks.size());
-    std::vector<bool> done(tasks.size(), false);
+    std::vector<const SparseTask*> ptrs;
+    std::vector<TaskResult*> out;
     for (std::size_t i = 0; i < tasks.size(); ++i) {
-        if (done[i]) continue;
-        if (!tasks[i].cache || !tasks[i].metadata)
-            throw std::runtime_error("no-context: task has no executable payload");
-        const Shape s = shape_of(tasks[i]);
-        std::vector<const SparseTask*> batch;
-        std::vector<TaskResult*> out;
-        for (std::size_t j = i; j < tasks.size(); ++j) {
-            if (done[j] || !tasks[j].cache || !tasks[j].metadata || !(shape_of(tasks[j]) == s)) continue;
-            batch.push_back(&tasks[j]);
-            out.push_back(&res[j]);
-            done[j] = true;
-        }
-        execute_batch(batch, out);
+        ptrs.push_back(&tasks[i]);
+        out.push_back(&res[i]);
     }
+    execute_all(ptrs, out);
     return res;
 }
 
@@ -201,37 +252,23 @@ ScheduleReport run(TaskQueue& queue, const WorkerProfile& workers, RunMode mode,
     rep.workers.resize(1);
     rep.workers[0].accelerator = true;
     const auto t0 = std::chrono::steady_clock::now();
-    // one device step per distinct task shape (one in practice: a decode step);
-    // a task counts as done only once its batch has executed
-    std::vector<bool> done(tasks.size(), false), claimed(tasks.size(), false);
+    // the whole queue as device steps (one per distinct task shape: one for a
+    // decode step); a task counts as done only once its step has executed
+    std::vector<bool> done(tasks.size(), false);
+    std::vector<const SparseTask*> ptrs;
+    std::vector<TaskResult*> out;
     for (std::size_t i = 0; i < tasks.size(); ++i) {
-        if (claimed[i]) continue;
-        std::vector<std::size_t> idx;
-        std::vector<const SparseTask*> batch;
-        std::vector<TaskResult*> out;
-        try {
-            if (!tasks[i].cache || !tasks[i].metadata)
-                throw std::runtime_error("no-context: task has no executable payload");
-            const Shape s = shape_of(tasks[i]);
-            for (std::size_t j = i; j < tasks.size(); ++j) {
-                if (claimed[j] || !tasks[j].cache || !tasks[j].metadata || !(shape_of(tasks[j]) == s)) continue;
-                idx.push_back(j);
-                batch.push_back(&tasks[j]);
-                out.push_back(&res[j]);
-                claimed[j] = true;
-            }
-            execute_batch(batch, out);
-            for (std::size_t j : idx) done[j] = true;
-        } catch (const std::exception&) {
-            // the reference records the group whose task threw (scheduler.cpp:247-252)
-            if (idx.empty()) idx.push_back(i);
-            for (std::size_t j : idx) {
-                claimed[j] = true;
-                rep.failed_groups.push_back(tasks[j].group_id);
-            }
-            rep.aborted = true;
-            break;
-        }
+        ptrs.push_back(&tasks[i]);
+        out.push_back(&res[i]);
+    }
+    std::vector<std::size_t> failing;
+    try {
+        execute_all(ptrs, out, &done, &failing);
+    } catch (const std::exception&) {
+        // the reference records the group whose task threw (scheduler.cpp:247-252);
+        // a device step fails as a whole: every group of that step is reported
+        for (std::size_t j : failing) rep.failed_groups.push_back(tasks[j].group_id);
+        rep.aborted = true;
     }
     const double end = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     rep.makespan = end;

@@ -478,6 +478,13 @@ int fx_memcpy_d2h(fx_ctx* ctx, void* dst, const void* src, size_t bytes) {
     });
 }
 
+int fx_memcpy_d2d(fx_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        DeviceGuard g(ctx);
+        FX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    });
+}
+
 int fx_memset(fx_ctx* ctx, void* dptr, int value, size_t bytes) {
     return guarded([&] {
         DeviceGuard g(ctx);
