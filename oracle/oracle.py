@@ -33,7 +33,7 @@ def build(ref: bool = True) -> None:
     /root/reference exists (this container); the GPU box uses prebuilt files."""
     targets = ["oracle"]
     if ref and os.path.isdir("/root/reference/proj/src"):
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 

@@ -165,7 +165,47 @@ void Arena::build_metadata(int slot) {
                                    const_cast<float*>(a.absmax)));
 }
 
-int Arena::acquire(const SegmentedKvCache& cache) {
+void Arena::flush_pending() {
+    std::size_t n = 0, row = 0;
+    bool uniform = true;
+    for (const Owner& o : owners_)
+        if (o.pending) {
+            if (n == 0) row = o.uploaded_new;
+            uniform = uniform && o.uploaded_new == row;
+            ++n;
+        }
+    if (n == 0) return;
+    const std::size_t base = shape_.sink + shape_.cpu + shape_.local, D = shape_.dim;
+    if (n == owners_.size() && uniform) {  // a decode step: one row per slot, one kernel
+        std::vector<float> kn(n * D), vn(n * D);
+        for (std::size_t s = 0; s < n; ++s) {
+            const Owner& o = owners_[s];
+            std::copy_n(o.cache->keys(Segment::New).row(o.uploaded_new).data(), D, kn.data() + s * D);
+            std::copy_n(o.cache->values(Segment::New).row(o.uploaded_new).data(), D, vn.data() + s * D);
+        }
+        float* st = thread_staging(2 * n * D * sizeof(float));
+        check(fx_memcpy_h2d(context(), st, kn.data(), n * D * sizeof(float)));
+        check(fx_memcpy_h2d(context(), st + n * D, vn.data(), n * D * sizeof(float)));
+        fx_layout L = layout(1);
+        check(fx_append_kv(context(), &L, k_, v_, static_cast<std::int64_t>(base + row), st, st + n * D));
+        for (Owner& o : owners_) {
+            o.uploaded_new += 1;
+            o.pending = false;
+        }
+        return;
+    }
+    for (std::size_t s = 0; s < owners_.size(); ++s) {
+        Owner& o = owners_[s];
+        if (!o.pending) continue;
+        upload_rows(static_cast<int>(s), static_cast<std::int64_t>(base + o.uploaded_new),
+                    o.cache->keys(Segment::New).row(o.uploaded_new).data(),
+                    o.cache->values(Segment::New).row(o.uploaded_new).data(), 1);
+        o.uploaded_new += 1;
+        o.pending = false;
+    }
+}
+
+int Arena::acquire(const SegmentedKvCache& cache, bool defer) {
     const std::size_t fresh = cache.len(Segment::New);
     const std::size_t base = shape_.sink + shape_.cpu + shape_.local;
     // rows to hold now, plus decode headroom (regrowth copies the slots)
@@ -176,9 +216,15 @@ int Arena::acquire(const SegmentedKvCache& cache) {
     if (it != index_.end()) {
         slot = it->second;
         Owner& o = owners_[static_cast<std::size_t>(slot)];
-        if (o.generation == cache.generation() && fresh >= o.uploaded_new) {
+        if (o.generation == cache.generation() && fresh >= o.uploaded_new + (o.pending ? 1 : 0)) {
+            if (o.pending && defer && fresh == o.uploaded_new + 1) return slot;
+            o.pending = false;  // upload whatever is outstanding below
+            if (need > l_cap_) reserve(cap_slots_, room);
+            if (defer && fresh == o.uploaded_new + 1) {
+                o.pending = true;
+                return slot;
+            }
             if (fresh > o.uploaded_new) {  // append_new since the last use: those rows only
-                if (need > l_cap_) reserve(cap_slots_, room);
                 const Matrix& kn = cache.keys(Segment::New);
                 const Matrix& vn = cache.values(Segment::New);
                 const std::size_t D = shape_.dim;

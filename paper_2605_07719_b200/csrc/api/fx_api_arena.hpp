@@ -40,8 +40,12 @@ public:
     Arena(const Arena&) = delete;
     Arena& operator=(const Arena&) = delete;
 
-    // The cache's slot, with its rows up to date on the device.
-    int acquire(const SegmentedKvCache& cache);
+    // The cache's slot, with its rows up to date on the device.  defer: a
+    // single newly appended row is left pending for flush_pending().
+    int acquire(const SegmentedKvCache& cache, bool defer = false);
+    // Uploads the deferred rows: one batched fx_append_kv when every slot has
+    // exactly one pending row at the same position (a decode step), else row by row.
+    void flush_pending();
     int slots() const { return static_cast<int>(owners_.size()); }
     // Layout over every slot for `l_new` decoded rows attended (rows per slot = l_cap).
     fx_layout layout(int group_size) const;
@@ -60,6 +64,7 @@ private:
         const SegmentedKvCache* cache;
         std::uint64_t generation;
         std::size_t uploaded_new;
+        bool pending = false;  // one deferred New row (uploaded_new + 1)
     };
     void reserve(int slots, std::int64_t l_cap);
     void upload_rows(int slot, std::int64_t row0, const float* k, const float* v, std::size_t rows);

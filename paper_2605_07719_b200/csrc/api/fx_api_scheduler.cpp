@@ -3,6 +3,7 @@
 // Cites: /root/reference/proj/src/scheduler.cpp:11-287, 290-330.
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <sstream>
 #include <stdexcept>
 
@@ -68,8 +69,9 @@ void execute_batch(const std::vector<const SparseTask*>& tasks, std::vector<Task
         for (std::size_t h = 0; h < G; ++h)
             if (t.queries[h].size() != D) throw std::runtime_error("bad-shape: query width != key width");
         if (t.plan.budgets.size() < G) throw std::runtime_error("bad-shape: plan has fewer budgets than heads");
-        slot[i] = ar.acquire(*t.cache);
+        slot[i] = ar.acquire(*t.cache, /*defer=*/true);
     }
+    ar.flush_pending();  // this step's appended rows: one batched append when they line up
     const std::size_t B = static_cast<std::size_t>(ar.slots());
     std::vector<int32_t> blk(B, 0);
     std::vector<double> bud(B * G, 0.0);
@@ -89,14 +91,17 @@ void execute_batch(const std::vector<const SparseTask*>& tasks, std::vector<Task
         blk[b] = s.cpu > 0 ? t.plan.block_size : 0;
     }
     const fx_layout lay = ar.layout(static_cast<int32_t>(G));
-    // per-call device inputs / outputs in the arena's scratch: q | budgets | blk | o
+    // per-call device inputs / outputs in the arena's scratch: q | budgets | blk | o,
+    // the inputs packed on the host and sent in one copy
     const auto al = [](std::size_t x) { return (x + 255) & ~std::size_t(255); };
     const std::size_t bq = al(hq.size() * sizeof(float)), bb = al(bud.size() * sizeof(double)),
                       bk = al(blk.size() * sizeof(int32_t)), bo = al(B * G * D * sizeof(float));
     char* sc = static_cast<char*>(ar.scratch(bq + bb + bk + bo));
-    check(fx_memcpy_h2d(context(), sc, hq.data(), hq.size() * sizeof(float)));
-    check(fx_memcpy_h2d(context(), sc + bq, bud.data(), bud.size() * sizeof(double)));
-    check(fx_memcpy_h2d(context(), sc + bq + bb, blk.data(), blk.size() * sizeof(int32_t)));
+    std::vector<char> packed(bq + bb + bk, 0);
+    std::memcpy(packed.data(), hq.data(), hq.size() * sizeof(float));
+    std::memcpy(packed.data() + bq, bud.data(), bud.size() * sizeof(double));
+    std::memcpy(packed.data() + bq + bb, blk.data(), blk.size() * sizeof(int32_t));
+    check(fx_memcpy_h2d(context(), sc, packed.data(), packed.size()));
     fx_step_args a = ar.step_args(static_cast<int64_t>(s.fresh));
     a.q = reinterpret_cast<const float*>(sc);
     a.plan_mode = FX_PLAN_GIVEN;

@@ -118,14 +118,34 @@ def test_reference_pipeline_through_dropin(tmp_path, cfg):
 
 
 @pytest.mark.gpu
-def test_reference_pipeline_c2_shape_through_dropin(tmp_path):
+def test_reference_pipeline_c2_shape_through_dropin(tmp_path, engine):
     """run_decode at the C2 layer shape (32 q / 8 kv heads, d128, 128K context,
     fixed (16, 0.05)) through the drop-in: the caches stay resident on the
-    device between steps (only the appended row is uploaded), so a step costs
-    the batched device decode plus the host marshalling of the queries."""
+    device between steps (only the appended rows go up, in one batched append),
+    so a run(queue, Executed) step costs one fx_decode_step over the f32 caches
+    plus the host marshalling -- within 2x of fx_decode_step timed alone (with
+    its output read back) on the same shape."""
+    import time
+
+    import torch
+
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
     got = _pipeline("pipeline_dropin", str(tmp_path / "c2.json"), 131072, 32, 4, 128, 1, 6, 16, 0.05, 0, 1)
     ms = [s["makespan"] * 1e3 for s in got["steps"]]
-    print("run(queue, Executed) per step (ms):", ["%.3f" % m for m in ms])
     assert all(s["scheduled_tasks"] == 8 for s in got["steps"])
-    # the first step uploads the caches; later steps are device-resident
-    assert max(ms[2:]) < 0.25 * ms[0]
+    dec = SparseDecoder(engine, 8, 1, 4, 128, 64, 131072 - 320, 256, max_new=8, dtype="f32")
+    dec.k.normal_()
+    dec.v.normal_()
+    dec.build_metadata()
+    q = torch.randn((8, 4, 128), device=engine.device)
+    for _ in range(10):
+        dec.step(q, fixed=(16, 0.05))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(20):
+        o, _ = dec.step(q, fixed=(16, 0.05))
+        o.cpu()
+    step_ms = (time.perf_counter() - t) / 20 * 1e3
+    print("run(queue, Executed) per step (ms):", ["%.3f" % m for m in ms], "fx_decode_step %.3f ms" % step_ms)
+    assert max(ms[2:]) < 2.0 * step_ms
+    del dec
