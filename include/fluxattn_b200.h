@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FX_ABI_VERSION 3
+#define FX_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define FX_API __attribute__((visibility("default")))

@@ -19,7 +19,7 @@ FX_PLAN_PROPS = 0
 FX_PLAN_FIXED = 1
 FX_PLAN_FULL = 2
 FX_PLAN_GIVEN = 3
-ABI_VERSION = 3
+ABI_VERSION = 4
 KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append")
 
 _p = C.c_void_p
