@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kPT, 2) k_feat_fused(fx_layout L, const void* 
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+            __syncwarp();  // every lane has read s_m[h] before lane 0 rewrites it
             if (lane == 0) {
                 const double scale = m_old == -INFINITY ? 0.0 : exp(m_old - m_new);
                 s_scale[h] = scale;
