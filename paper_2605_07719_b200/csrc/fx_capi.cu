@@ -9,12 +9,20 @@
 #include <vector>
 
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "fx_internal.h"
 #include "fx_worklist.cuh"
 
 namespace {
 thread_local std::string g_last_error;
+
+// NVTX range over one C-ABI call (header-only NVTX3: a no-op unless a
+// profiler injects itself), so nsys / ncu timelines show the API phases.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class F>
 int guarded(F&& f) {
@@ -519,6 +527,7 @@ size_t fx_step_scratch_bytes(fx_ctx* ctx, const fx_layout* lay) {
 int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, void* m16,
                              void* m32, void* m64, void* m128, float* absmax) {
     return guarded([&] {
+        NvtxRange nv("fx_build_metadata_levels");
         DeviceGuard g(ctx);
         check_layout(lay);
         Timed tm(ctx, FX_KERNEL_METADATA);
@@ -530,6 +539,7 @@ int fx_build_metadata_levels(fx_ctx* ctx, const fx_layout* lay, const void* k, v
 int fx_build_metadata_means(fx_ctx* ctx, const fx_layout* lay, const void* k, void* const levels[4],
                             float* absmax, float* const means[4]) {
     return guarded([&] {
+        NvtxRange nv("fx_build_metadata_means");
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(levels && means, FX_ERR_INVALID, "bad-shape: null level / mean arrays");
@@ -696,6 +706,7 @@ int fx_model_destroy(fx_model* m) {
 int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features, double* bgt0,
                double* kslope, int32_t* streaming, double* z) {
     return guarded([&] {
+        NvtxRange nv("fx_predict");
         DeviceGuard g(ctx);
         FX_REQUIRE(m != nullptr, FX_ERR_STATE, "no-model: predictor source requires a model");
         auto* mm = const_cast<fx_model*>(m);
@@ -708,6 +719,7 @@ int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features
 
 int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
     return guarded([&] {
+        NvtxRange nv("fx_decode_step");
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(a != nullptr && a->k && a->v && a->q && a->o, FX_ERR_STATE,
@@ -771,6 +783,7 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
 
 int fx_plan_select(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
     return guarded([&] {
+        NvtxRange nv("fx_plan_select");
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(a != nullptr && a->q && a->sel_bits && a->plan_blk && a->plan_budgets &&
@@ -853,6 +866,7 @@ int fx_merge_partials(fx_ctx* ctx, int32_t n, int32_t dim, const float* o_parts,
 int fx_append_kv(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_t row,
                  const float* k_new, const float* v_new) {
     return guarded([&] {
+        NvtxRange nv("fx_append_kv");
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(row >= 0 && row < lay->l_cap, FX_ERR_INVALID, "bad-shape: append row out of range");
@@ -877,6 +891,7 @@ int fx_label_heads(fx_ctx* ctx, const fx_layout* lay, const void* k, const void*
                    double* o_full, double* normalizer, double* budgets, int64_t* blocks,
                    double* bgt0, double* kslope, int32_t* streaming) {
     return guarded([&] {
+        NvtxRange nv("fx_label_heads");
         DeviceGuard g(ctx);
         check_layout(lay);
         const fx_layout& L = *lay;
@@ -912,6 +927,7 @@ int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, const voi
                      const void* const meta[4], const float* anchor, double tau, int32_t layer,
                      double* rec) {
     return guarded([&] {
+        NvtxRange nv("fx_prefill_stats");
         DeviceGuard g(ctx);
         check_layout(lay);
         const fx_layout& L = *lay;
@@ -959,6 +975,7 @@ int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, const voi
 int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
                        int64_t l_new, const float* q, const double* rec, double* features) {
     return guarded([&] {
+        NvtxRange nv("fx_decode_features");
         DeviceGuard g(ctx);
         check_layout(lay);
         const fx_layout& L = *lay;
@@ -975,6 +992,7 @@ int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, const void* k, const voi
                      const float* q, const double* rec, const fx_model* m, double* features, double* z,
                      double* bgt0, double* kslope, int32_t* streaming) {
     return guarded([&] {
+        NvtxRange nv("fx_predict_props");
         DeviceGuard g(ctx);
         check_layout(lay);
         const fx_layout& L = *lay;
@@ -1012,6 +1030,7 @@ int fx_generate(fx_ctx* ctx, const fx_workload_spec* sp, const fx_layout* lay, c
                 const int32_t* layers, void* k, void* v, float* anchor_q, int32_t steps,
                 float* step_q, float* step_new_k, float* step_new_v, int32_t* archetypes) {
     return guarded([&] {
+        NvtxRange nv("fx_generate");
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(sp && seeds && layers && k && v, FX_ERR_STATE, "no-context: generate has no payload");
@@ -1086,6 +1105,7 @@ int fx_trace_save(fx_ctx* ctx, const char* path, const fx_trace_info* info, cons
 int fx_cp_candidates(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, int64_t cap,
                      uint64_t* keys, uint32_t* ids, int32_t* count, uint64_t* kth) {
     return guarded([&] {
+        NvtxRange nv("fx_cp_candidates");
         DeviceGuard g(ctx);
         check_layout(lay);
         const fx_layout& L = *lay;
@@ -1147,6 +1167,7 @@ int fx_cp_select_peer(fx_ctx* ctx, const fx_layout* lay, int32_t ranks, int32_t 
                       const fx_cp_peer* peers, uint64_t stamp, const int32_t* kblocks,
                       const int32_t* blk, int64_t cpu_offset, uint32_t* sel_out, int32_t sel_words) {
     return guarded([&] {
+        NvtxRange nv("fx_cp_select_peer");
         DeviceGuard g(ctx);
         check_layout(lay);
         FX_REQUIRE(peers && kblocks && blk && sel_out, FX_ERR_STATE, "no-context: peer select has no payload");
@@ -1164,6 +1185,7 @@ int fx_cp_dist_phase(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, i
                      int32_t ranks, int32_t self, const fx_cp_peer* peers, uint64_t stamp,
                      float* approx, int64_t approx_stride) {
     return guarded([&] {
+        NvtxRange nv("fx_cp_dist_phase");
         DeviceGuard g(ctx);
         check_layout(lay);
         const fx_layout& L = *lay;
@@ -1201,6 +1223,7 @@ int fx_cp_dist_phase(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a, i
 int fx_cp_combine_peer(fx_ctx* ctx, int32_t ranks, int64_t n, int32_t dim, const fx_cp_peer* peers,
                        uint64_t stamp, float* o, float* lse) {
     return guarded([&] {
+        NvtxRange nv("fx_cp_combine_peer");
         DeviceGuard g(ctx);
         FX_REQUIRE(peers && o && n >= 0 && dim > 0, FX_ERR_INVALID, "bad-shape: peer combine input");
         fx::launch_cp_combine_peer(ranks, n, dim, peers, stamp, o, lse, ctx->stream);
