@@ -394,33 +394,70 @@ __device__ __forceinline__ void select_head(
             }
             if (rank < need) atomicOr(&bits[idc >> 5], 1u << (idc & 31));
         }
-    } else if (t == 0) {
-        // Large band (degenerate data): bisect the threshold key, then take the
-        // tied keys lowest id first.
-        uint64_t lo_k = 0, hi_k = ~0ull;  // invariant: count(>= lo_k) >= need
-        while (lo_k < hi_k) {
-            const uint64_t mid = lo_k + ((hi_k - lo_k) >> 1) + 1;
-            int64_t ge = 0;
-            for (int64_t c = 0; c < n_cand; ++c) ge += ckeys[c] >= mid;
-            if (ge >= need) lo_k = mid;
-            else hi_k = mid - 1;
-        }
-        int64_t take = need;
-        for (int64_t c = 0; c < n_cand; ++c)
-            if (ckeys[c] > lo_k) {
-                atomicOr(&bits[cids[c] >> 5], 1u << (cids[c] & 31));
-                --take;
+    } else {
+        // Large band (degenerate data, e.g. equal keys): block-wide radix select
+        // of the need-th largest key K* (8 passes of 8 bits over the band in
+        // global scratch), every key > K* in, then the tied keys == K* lowest
+        // id first -- the take-th smallest id by a second radix select.
+        int32_t* h = reinterpret_cast<int32_t*>(dsm);  // 256 bins (the keys area is free)
+        __shared__ uint64_t s_pref;
+        __shared__ int64_t s_cnt;
+        uint64_t pref = 0, msk = 0;
+        int64_t above = 0;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int i = t; i < 256; i += kT) h[i] = 0;
+            __syncthreads();
+            for (int64_t c = t; c < n_cand; c += kT) {
+                const uint64_t kc = ckeys[c];
+                if ((kc & msk) == pref) atomicAdd(&h[(kc >> shift) & 255], 1);
             }
-        uint32_t last = 0;  // ids taken so far are < ... strictly increasing sweep
-        bool first = true;
-        while (take-- > 0) {
-            uint32_t best = 0xffffffffu;
-            for (int64_t c = 0; c < n_cand; ++c)
-                if (ckeys[c] == lo_k && (first || cids[c] > last) && cids[c] < best) best = cids[c];
-            atomicOr(&bits[best >> 5], 1u << (best & 31));
-            last = best;
-            first = false;
+            __syncthreads();
+            if (t == 0) {  // highest digit whose cumulative count from the top reaches need
+                int64_t cum = above;
+                int d = 255;
+                for (; d > 0; --d) {
+                    if (cum + h[d] >= need) break;
+                    cum += h[d];
+                }
+                s_pref = pref | ((uint64_t)d << shift);
+                s_cnt = cum;  // keys above digit d's bucket
+            }
+            __syncthreads();
+            pref = s_pref;
+            above = s_cnt;
+            msk |= 0xffull << shift;
         }
+        const uint64_t kstar = pref;
+        const int64_t take = need - above;  // >= 1 keys equal to K*
+        for (int64_t c = t; c < n_cand; c += kT)
+            if (ckeys[c] > kstar) atomicOr(&bits[cids[c] >> 5], 1u << (cids[c] & 31));
+        uint32_t ipref = 0, imsk = 0;
+        int64_t below = 0;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int i = t; i < 256; i += kT) h[i] = 0;
+            __syncthreads();
+            for (int64_t c = t; c < n_cand; c += kT) {
+                const uint32_t ic = cids[c];
+                if (ckeys[c] == kstar && (ic & imsk) == ipref) atomicAdd(&h[(ic >> shift) & 255], 1);
+            }
+            __syncthreads();
+            if (t == 0) {  // lowest digit whose cumulative count from the bottom reaches take
+                int64_t cum = below;
+                int d = 0;
+                for (; d < 255; ++d) {
+                    if (cum + h[d] >= take) break;
+                    cum += h[d];
+                }
+                s_pref = ipref | ((uint32_t)d << shift);
+                s_cnt = cum;
+            }
+            __syncthreads();
+            ipref = (uint32_t)s_pref;
+            below = s_cnt;
+            imsk |= 0xffu << shift;
+        }
+        for (int64_t c = t; c < n_cand; c += kT)  // ids are distinct: exactly `take` of them
+            if (ckeys[c] == kstar && cids[c] <= ipref) atomicOr(&bits[cids[c] >> 5], 1u << (cids[c] & 31));
     }
     __syncthreads();
     SEL_MARK(5);

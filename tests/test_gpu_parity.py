@@ -392,6 +392,35 @@ def test_decode_step_ties_constant_keys(engine, coracle):
     _check_step(dec, {(0, 0): (k, v)}, q, coracle, lambda b, g: 16, lambda b, g: [0.1] * 4, "bf16")
 
 
+def test_decode_step_large_tie_band(engine, coracle):
+    """Hundreds of blocks tied at the cut-off score (> the 512-entry smem band):
+    the block-wide radix select takes the tied blocks lowest id first, exactly
+    as the reference's (score desc, id asc) order, and the step stays fast."""
+    import time
+    from paper_2605_07719_b200.fluxattn import SparseDecoder
+    D, l_cpu = 128, 32768
+    rng = np.random.default_rng(5)
+    dec = SparseDecoder(engine, 1, 1, 4, D, 64, l_cpu, 256, dtype="bf16")
+    nb = l_cpu // 16
+    level = rng.choice([0.25, 0.5, 0.75], nb)
+    k = rng.standard_normal((64 + l_cpu + 256, D)).astype(np.float32) * 0.01
+    k[64:64 + l_cpu] = np.repeat(level, 16)[:, None] * np.ones((1, D), np.float32)
+    k, v = bf16_round(k), bf16_round(rng.standard_normal(k.shape).astype(np.float32))
+    dec.load_group(0, 0, k, v)
+    dec.build_metadata()
+    q = np.abs(rng.standard_normal((1, 4, D))).astype(np.float32)
+    q[0, 1] *= -1.0  # head 1 ranks the low level first
+    q = bf16_round(q)
+    qd = torch.as_tensor(q).cuda()
+    dec.step(qd, fixed=(16, 0.3))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    dec.step(qd, fixed=(16, 0.3))
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t < 0.05
+    _check_step(dec, {(0, 0): (k, v)}, q, coracle, lambda b, g: 16, lambda b, g: [0.3] * 4, "bf16")
+
+
 def test_decode_step_reference_workload(engine, refo, coracle):
     """Reference generator (planted needles / streaming heads) end to end."""
     from paper_2605_07719_b200.fluxattn import SparseDecoder
