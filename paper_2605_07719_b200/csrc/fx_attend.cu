@@ -206,9 +206,17 @@ __device__ void merge_run(const View& p, int bg, int64_t s, int64_t e, int64_t N
         for (int i = t; i < G * D; i += nt) {
             const int h = i / D, d = i % D;
             float num = 0.f;
-            for (int j = 0; j < n; ++j) {
-                const float wj = ms->w[j * G + h];
-                if (wj != 0.f) num += wj * __ldcg(p.part_o + ((int64_t)(ms->list[j] + bg) * G + h) * D + d);
+            // eight contributors' partials in flight per round (L2 round trips overlap)
+            for (int j0 = 0; j0 < n; j0 += 8) {
+                float pv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    pv[u] = j0 + u < n ? __ldcg(p.part_o + ((int64_t)(ms->list[j0 + u] + bg) * G + h) * D + d) : 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float wj = j0 + u < n ? ms->w[(j0 + u) * G + h] : 0.f;
+                    if (wj != 0.f) num += wj * pv[u];
+                }
             }
             const float den = ms->den[h];
             p.o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
