@@ -134,8 +134,10 @@ __device__ __forceinline__ void select_head(
     const int64_t H = (int64_t)Hkv * G;
     const int b = (int)(head / H), h = (int)(head % H), g = h / G;
     const int bg = b * Hkv + g;
-    const int blk = blk_arr[bg];
-    const int64_t k = kblocks[head];
+    // the plan comes from k_prepare (two launches back, complete before the
+    // scorer began, hence before this grid launched); read through L2
+    const int blk = __ldcg(blk_arr + bg);
+    const int64_t k = __ldcg(kblocks + head);
     uint32_t* bits = sel_bits + head * sel_words;
     const int64_t nblk = blk > 0 ? cdiv_dev(l_cpu, blk) : 0;
     const int W = (int)cdiv_dev(nblk, 32);
@@ -158,6 +160,19 @@ __device__ __forceinline__ void select_head(
     const float* sc = approx + head * astride;
     const bool staged = nblk <= keys_cap;
 
+    // everything that does not depend on the scorer first: q, the error bound,
+    // the histogram; then the programmatic wait for the scorer's output
+    for (int i = t; i < kBins; i += kT) hist[i] = 0;
+    if (t == 0) s_ncand = 0;
+    for (int d = t; d < D; d += kT) s_q[d] = (double)qh[d];
+    if (warp == 0) {
+        double a = 0.0;
+        for (int d = lane; d < D; d += 32)
+            a += fabs((double)qh[d]) * (double)absmax[(int64_t)bg * D + d];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) s_eps = a * eps_scale * 1.01 + 1e-30;
+    }
+    pdl_wait();
     // ---- 0. stage (128-bit loads, several in flight), min/max, error bound ----
     float mx = -INFINITY, mn = INFINITY;
     bool fin_all = true;
@@ -186,16 +201,6 @@ __device__ __forceinline__ void select_head(
             if (staged) s_keys[i] = a;
             see(a);
         }
-    }
-    for (int i = t; i < kBins; i += kT) hist[i] = 0;
-    if (t == 0) s_ncand = 0;
-    for (int d = t; d < D; d += kT) s_q[d] = (double)qh[d];
-    if (warp == 0) {
-        double a = 0.0;
-        for (int d = lane; d < D; d += 32)
-            a += fabs((double)qh[d]) * (double)absmax[(int64_t)bg * D + d];
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) s_eps = a * eps_scale * 1.01 + 1e-30;
     }
     // one barrier round for max, min and finiteness
     mx = warp_max(mx);
@@ -230,9 +235,13 @@ __device__ __forceinline__ void select_head(
         // bin holding the k-th largest: each thread owns kBins/kT bins; suffix
         // sums over threads (from the top) locate the owner, which scans them
         constexpr int PB = kBins / kT;
+        static_assert(PB == 8, "two 16-byte reads per thread");
+        const int4 h0 = reinterpret_cast<const int4*>(hist)[2 * t];  // 16-byte reads: no bank conflicts
+        const int4 h1 = reinterpret_cast<const int4*>(hist)[2 * t + 1];
+        const int hb[PB] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
         int c = 0;
 #pragma unroll
-        for (int i = 0; i < PB; ++i) c += hist[t * PB + i];
+        for (int i = 0; i < PB; ++i) c += hb[i];
         int x = c;  // suffix sum within the warp (lanes >= lane)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -245,8 +254,9 @@ __device__ __forceinline__ void select_head(
         for (int w = warp + 1; w < kNW; ++w) S += s_wsum[0][w];
         if (S >= k && S - c < k) {
             int above = S - c;
+#pragma unroll
             for (int i = PB - 1; i >= 0; --i) {
-                above += hist[t * PB + i];
+                above += hb[i];
                 if (above >= k) {
                     s_bin = t * PB + i;
                     break;
@@ -474,8 +484,7 @@ __global__ void __launch_bounds__(kT) k_select(
     uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap, WorklistArgs wl,
     int32_t* __restrict__ sel_done) {
-    pdl_wait();
-    pdl_trigger();
+    pdl_trigger();  // select_head waits for the scorer once its independent setup is done
     SEL_MARK(10);
     select_head<DT>(meta, absmax, q, blk_arr, kblocks, Hkv, G, D, l_cpu, approx, astride,
                     eps_scale, sel_bits, sel_words, cand_keys, cand_ids, cand_stride, keys_cap);
