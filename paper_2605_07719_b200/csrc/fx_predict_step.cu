@@ -50,6 +50,32 @@ __device__ __forceinline__ double elem_f64(__nv_bfloat16 x) {
 }
 __device__ __forceinline__ double elem_f64(float x) { return f32bits_to_f64(__float_as_uint(x)); }
 
+// N contiguous elements of a row (16-byte aligned slice) as f64, vector loads
+template <typename T, int N>
+__device__ __forceinline__ void load_row_slice(const T* p, double* out) {
+    constexpr int EPV = 16 / (int)sizeof(T);
+    if constexpr (N % EPV == 0) {
+#pragma unroll
+        for (int v = 0; v < N / EPV; ++v) {
+            const uint4 w = reinterpret_cast<const uint4*>(p)[v];
+            const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+            if constexpr (sizeof(T) == 2) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    out[v * 8 + 2 * i] = f32bits_to_f64(u[i] << 16);
+                    out[v * 8 + 2 * i + 1] = f32bits_to_f64(u[i] & 0xffff0000u);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) out[v * 4 + i] = f32bits_to_f64(u[i]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) out[i] = elem_f64(p[i]);
+    }
+}
+
 #ifdef FX_TRACE  // profiling build only: per-CTA phase times
 __device__ long long g_fp_trace[16 * 1024];
 #define FP_MARK(i)                                                                        \
@@ -70,7 +96,7 @@ constexpr size_t feat_smem_bytes() {
 }
 
 template <typename T, int G, int D>
-__global__ void __launch_bounds__(kPT, 2) k_feat_fused(fx_layout L, const void* __restrict__ kp,
+__global__ void __launch_bounds__(kPT, G <= 4 ? 2 : 1) k_feat_fused(fx_layout L, const void* __restrict__ kp,
                                                        const void* __restrict__ vp, int64_t l_new,
                                                        const float* __restrict__ q,
                                                        const double* __restrict__ rec,
@@ -136,6 +162,13 @@ __global__ void __launch_bounds__(kPT, 2) k_feat_fused(fx_layout L, const void* 
     FP_MARK(1);
     const double isd = 1.0 / sqrt((double)D);
     constexpr int DV = D / 32;
+    constexpr int LPR = G <= 4 ? 16 : 32, DPL = D / LPR, RPI = 32 / LPR;  // score-loop lane mapping
+    const int sub = lane / LPR, sl = lane % LPR;
+    double qreg[DPL][G];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j)
+#pragma unroll
+        for (int h = 0; h < G; ++h) qreg[j][h] = qs[(sl * DPL + j) * G + h];
     double acc[G][DV];  // sum_r w_r v_r, lanes own DV dims (warps < kOW)
 #pragma unroll
     for (int h = 0; h < G; ++h)
@@ -151,37 +184,32 @@ __global__ void __launch_bounds__(kPT, 2) k_feat_fused(fx_layout L, const void* 
         if (c == nch0) { FP_MARK(8); }
         const T* Ks = ring + (size_t)(2 * st) * CR * D;
         const T* Vs = ring + (size_t)(2 * st + 1) * CR * D;
-        // scores: 8 lanes per row (4 rows per warp at a time), lane sl takes
-        // dims sl, sl + 8, ... (interleaved: the 8 lanes' q rows are adjacent
-        // in smem, conflict-free); a 3-level butterfly per head
-        {
-            constexpr int LPR = 8, DL = D / LPR;
-            const int sub = lane / LPR, sl = lane % LPR;
-            for (int r0 = warp * 4; r0 < nr; r0 += kPW * 4) {
-                const int r = r0 + sub;
-                const bool live = r < nr;
-                double p[G];
+        // scores: LPR lanes per row (32 / LPR rows per warp at a time), lane sl
+        // owns DPL contiguous dims whose q values sit in registers (qreg);
+        // one vector load of the row slice, then a butterfly per head
+        for (int r0 = warp * RPI; r0 < nr; r0 += kPW * RPI) {
+            const int r = r0 + sub;
+            const bool live = r < nr;
+            double p[G];
 #pragma unroll
-                for (int h = 0; h < G; ++h) p[h] = 0.0;
-                const T* kr = Ks + (live ? r : r0) * D + sl;
+            for (int h = 0; h < G; ++h) p[h] = 0.0;
+            const T* kr = Ks + (live ? r : r0) * D + sl * DPL;
+            double kv[DPL];
+            load_row_slice<T, DPL>(kr, kv);
 #pragma unroll
-                for (int j = 0; j < DL; ++j) {
-                    const double kv = elem_f64(kr[j * LPR]);
-                    const double* qd = qs + (j * LPR + sl) * G;
+            for (int j = 0; j < DPL; ++j)
 #pragma unroll
-                    for (int h = 0; h < G; ++h) p[h] += qd[h] * kv;
-                }
+                for (int h = 0; h < G; ++h) p[h] += qreg[j][h] * kv[j];
 #pragma unroll
-                for (int h = 0; h < G; ++h) {
+            for (int h = 0; h < G; ++h) {
 #pragma unroll
-                    for (int o = LPR / 2; o > 0; o >>= 1) p[h] += __shfl_xor_sync(0xffffffffu, p[h], o);
-                }
-                if (live && sl < G) {
-                    double v = p[0];
+                for (int o = LPR / 2; o > 0; o >>= 1) p[h] += __shfl_xor_sync(0xffffffffu, p[h], o);
+            }
+            if (live && sl < G) {
+                double v = p[0];
 #pragma unroll
-                    for (int h = 1; h < G; ++h) v = sl == h ? p[h] : v;
-                    sc[r * G + sl] = v * isd;
-                }
+                for (int h = 1; h < G; ++h) v = sl == h ? p[h] : v;
+                sc[r * G + sl] = v * isd;
             }
         }
         __syncthreads();
