@@ -228,16 +228,33 @@ __global__ void __launch_bounds__(kMT) k_mlp_layer(int n, const double* __restri
         const double* w = ws[c & 1];
         const int kn = IN - c * kKC < kKC ? IN - c * kKC : kKC;
         // the products of 8 inputs first (independent), then the in-order adds:
-        // the add chains never wait on a load or a multiply
+        // the add chains never wait on a load or a multiply.  Full rounds read
+        // each chain's 8 inputs as four 16-byte vectors (IN even: 16-byte rows)
         constexpr int PB = 8;
         for (int k0 = 0; k0 < kn; k0 += PB) {
+            const int i0 = c * kKC + k0;
             double p[kMC][PB];
+            if (k0 + PB <= kn && (IN % 2) == 0) {
+                double wv[PB];
 #pragma unroll
-            for (int kk = 0; kk < PB; ++kk) {
-                const int i = c * kKC + k0 + kk;
-                const double wv = k0 + kk < kn ? w[(k0 + kk) * kMN + nl] : 0.0;
+                for (int kk = 0; kk < PB; ++kk) wv[kk] = w[(k0 + kk) * kMN + nl];
 #pragma unroll
-                for (int j = 0; j < kMC; ++j) p[j][kk] = __dmul_rn(k0 + kk < kn ? xr[j * IN + i] : 0.0, wv);
+                for (int j = 0; j < kMC; ++j) {
+                    const double2* xv = reinterpret_cast<const double2*>(xr + j * IN + i0);
+#pragma unroll
+                    for (int v = 0; v < PB / 2; ++v) {
+                        const double2 x2 = xv[v];
+                        p[j][2 * v] = __dmul_rn(x2.x, wv[2 * v]);
+                        p[j][2 * v + 1] = __dmul_rn(x2.y, wv[2 * v + 1]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < PB; ++kk) {
+                    const double wv = k0 + kk < kn ? w[(k0 + kk) * kMN + nl] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < kMC; ++j) p[j][kk] = __dmul_rn(k0 + kk < kn ? xr[j * IN + i0 + kk] : 0.0, wv);
+                }
             }
 #pragma unroll
             for (int kk = 0; kk < PB; ++kk)
