@@ -394,7 +394,7 @@ def run_reference_arm(a):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_and_parity(a, dec, q, o, lse, plan_step, ref_runs=5, parity=True):
+def cpu_baseline_and_parity(a, dec, q, o, lse, plan_step, ref_runs=5, parity=True, entries=None):
     """The compiled reference on the GPU step's exact data (bf16 bits upcast to
     f32, the same plan and queries, the same decoded rows): whole batch (C4: one
     layer's 8 sequences, x32), best of `ref_runs` executed runs.  Then parity of
@@ -414,7 +414,8 @@ def cpu_baseline_and_parity(a, dec, q, o, lse, plan_step, ref_runs=5, parity=Tru
     l_cpu, l_new = lay.l_cpu, dec.l_new
     n_rows = lay.l_sink + l_cpu + lay.l_local + l_new
     seg = (lay.l_sink, l_cpu, lay.l_local, l_new)
-    entries = list(range(a.seqs)) if a.workload == "c4" else list(range(lay.batch))
+    if entries is None:
+        entries = list(range(a.seqs)) if a.workload == "c4" else list(range(lay.batch))
     scale = lay.batch / len(entries)
     blk = dec.plan_blk.cpu().numpy()
     bud = dec.plan_budgets.cpu().numpy()
@@ -437,7 +438,7 @@ def cpu_baseline_and_parity(a, dec, q, o, lse, plan_step, ref_runs=5, parity=Tru
     res = {"value": 1.0 / t, "unit": UNIT, "cores": workers + 1, "kind": "reference",
            "cpu_model": ci["model"], "nproc": ci["nproc"],
            "sample": f"{len(tasks)} retrieval-group tasks = every (b, g) of "
-                     + (f"layer 0's {len(entries)} sequences, x{scale:g} for the layers"
+                     + (f"{len(entries)} of the {lay.batch} batch entries, x{scale:g}"
                         if scale != 1 else f"all {len(entries)} sequences")
                      + f" (the GPU step's data, plan and queries), run(queue, profile, "
                        f"RunMode::Executed) with {workers} host workers + 1 accelerator-model "
@@ -688,6 +689,20 @@ def run_c5(a):
                          "h2d_bytes_per_step": B * H * D * 4, "d2h_bytes_per_step": B * H * (D + 1) * 4,
                          "path": "C-ABI fx_decode_step per step, pinned host q in, o + lse out, "
                                  "copies on the compute stream"}
+        if not a.no_cpu_baseline:  # the reference on 1 of the 4 sequences (8 GB of f32 KV), x4
+            try:
+                q_par = qs[step_i[0]].contiguous()
+                o_par, lse_par = dec.step(q_par, props=props)
+                torch.cuda.synchronize()
+                a.workload, a.seqs = "c5", B
+                cb, par = cpu_baseline_and_parity(a, dec, q_par, o_par.clone(), lse_par.clone(),
+                                                  (bgt0, ks, st), ref_runs=3, entries=[0])
+                result["cpu_baseline"] = cb
+                if par is not None:
+                    result["parity"] = par
+            except Exception as e:  # noqa: BLE001
+                result["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                          "kind": "reference", "sample": f"failed: {e}"}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
