@@ -7,24 +7,27 @@
 // i.e. exact softmax attention of q over  sink + local + new  and the
 // selected cpu-segment blocks, merged by LSE (attention.cpp:89-104).
 //
-// Work decomposition.  k_worklist (fx_select.cu) lays every (b, g) out as a
-// list of 16-row "boxes" (defaults first, then the union of the group's
-// selected blocks) with a G-bit head mask per box; all lists concatenate
-// into one global box sequence.  A persistent grid splits that sequence into
-// equal contiguous ranges (split-K over the whole batch): a CTA walks its
-// range, keeps running (m, l, O) per head, and at the end of each (b, g) run
-// writes the final output when the run lay wholly inside its range, else one
-// partial (o, lse).  Only the two runs cut by a range end can be partial; at
-// the end of its range a CTA counts itself in for those, and the last
-// contributor merges the partials -- the fused epilogue, with no global
-// fence or atomic issued mid-stream.
+// Work decomposition.  The worklist (fx_worklist.cuh; fused into k_select)
+// lays every (b, g) out as a list of 16-row "boxes" (defaults first, then the
+// union of the group's selected blocks) with a G-bit head mask per box.
 //
-// k_attend_tma (bf16, D in {64, 128}, G <= 8):
-//   warp 4        producer: one 3-D TMA per 16-row box and tensor
-//                 (SWIZZLE_128B) into a kStages-deep ring of 8-box tiles,
-//                 mbarrier completion;
-//   warps 0..3    consumers: two boxes each per 8-box tile (q of the next
-//                 run prefetched into registers);
+// k_attend_tma (bf16, D in {64, 128}, G <= 8) is fed by a unit queue: as soon
+// as a group's boxes exist, the worklist publishes them as units of
+// kUnitBoxes boxes (epoch-tagged flag words, release/acquire), and the
+// persistent CTAs -- resident while the selection of later groups is still
+// running -- claim units in publication order with one atomic each.  A
+// single-unit group is written final; otherwise every unit leaves an (o, lse)
+// partial and the CTA that finishes a group's last unit merges them (in unit
+// order, so the result does not depend on which CTA ran what).  Dynamic
+// claiming also balances the per-SM bandwidth differences at the end.
+//   warp 4        producer: claims units, one 3-D TMA per 16-row box and
+//                 tensor (SWIZZLE_128B) into a kStages-deep ring of 8-box
+//                 tiles plus a 1-D bulk copy of the unit's q rows, mbarrier
+//                 completion;
+//   warp 5        epilogue: combines the consumer warps' states of a unit,
+//                 writes the partial / final output, counts the unit in and
+//                 merges a finished group -- off the consumers' path;
+//   warps 0..3    consumers: two boxes each per 8-box tile;
 //                 S^T[16 tok x 8 heads] = K . Q^T  (mma.sync m16n8k16 bf16,
 //                 q split hi+lo so q keeps ~16 mantissa bits),
 //                 online softmax in f32 (exp2 domain),
@@ -36,7 +39,9 @@
 //   the widest dense side is G <= 8, so the legacy m16n8k16 shape is the
 //   right tool here (the kernel is HBM-bound: ~4 flop/byte).
 // k_attend_generic: any dtype (f32 path of config 1), any G <= 16, D <= 256,
-//   and index lists (the per-query reference API); CUDA-core f32 math.
+//   and index lists (the per-query reference API); CUDA-core f32 math; the
+//   global box sequence split into equal contiguous ranges over a persistent
+//   grid, runs cut by a range end merged by their last contributor.
 #include <cuda.h>
 
 #include "fx_common.cuh"
@@ -60,8 +65,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_SOLE = 8;
 
 struct TileHdr {
-    int32_t bg, flags, nb, pad;
-    int32_t s, e;  // the run's real box range [s, e) in the global sequence
+    int32_t bg, flags, nb;
+    int32_t u, c, nun;  // unit id, its index in the group, the group's unit count
     int32_t unused[2];
     Box box[kTileBoxes];
 };
@@ -266,63 +271,11 @@ __device__ void write_empty_runs(const View& p, const int32_t* starts, int64_t r
 // partials.  Count this CTA in for each; the last contributor merges.  Done
 // once, after the CTA's streaming: a global fence or atomic issued while the
 // SM saturates HBM with its own TMA reads waits microseconds behind that
-// traffic, so none is issued mid-stream.
-// Fast merge for the TMA kernel (G * D / 8 <= nt, at most kFastN
-// contributors): every thread owns 8 consecutive columns of one head and
-// issues all its loads (LSE + two float4 per contributor) before using any,
-// so the merge costs one L2 round trip.
-constexpr int kFastN = 4;
-__device__ bool merge_run_fast(const View& p, int bg, const int* list, int n, int t) {
-    const int G = p.G, D = p.D, per = D / 8;
-    if (n > kFastN || G * per > kCWarps * 32 || (D & 7) || (reinterpret_cast<uintptr_t>(p.o) & 15) ||
-        (reinterpret_cast<uintptr_t>(p.part_o) & 15))
-        return false;
-    if (t < G * per) {
-        const int h = t / per, d0 = (t % per) * 8;
-        float l[kFastN];
-        float4 a[kFastN], b[kFastN];
-#pragma unroll
-        for (int j = 0; j < kFastN; ++j)
-            if (j < n) {
-                const int64_t slot = (int64_t)(list[j] + bg) * G + h;
-                l[j] = __ldcg(p.part_lse + slot);
-                a[j] = __ldcg(reinterpret_cast<const float4*>(p.part_o + slot * D + d0));
-                b[j] = __ldcg(reinterpret_cast<const float4*>(p.part_o + slot * D + d0 + 4));
-            }
-        float M = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < kFastN; ++j)
-            if (j < n) M = fmaxf(M, l[j]);
-        float den = 0.f, o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < kFastN; ++j)
-            if (j < n && l[j] != -INFINITY) {
-                const float w = __expf(l[j] - M);
-                den += w;
-                o[0] += w * a[j].x; o[1] += w * a[j].y; o[2] += w * a[j].z; o[3] += w * a[j].w;
-                o[4] += w * b[j].x; o[5] += w * b[j].y; o[6] += w * b[j].z; o[7] += w * b[j].w;
-            }
-        const int b_ = bg / p.Hkv, g = bg % p.Hkv;
-        const int64_t oh = (int64_t)b_ * p.Hkv * G + (int64_t)g * G + h;
-        const float inv = den > 0.f ? 1.f / den : 0.f;
-        float4* dst = reinterpret_cast<float4*>(p.o + oh * D + d0);
-        dst[0] = make_float4(o[0] * inv, o[1] * inv, o[2] * inv, o[3] * inv);
-        dst[1] = make_float4(o[4] * inv, o[5] * inv, o[6] * inv, o[7] * inv);
-        if (d0 == 0 && p.lse) p.lse[oh] = den > 0.f ? M + __logf(den) : -INFINITY;
-    }
-    return true;
-}
-
-// End of a CTA's range.  Runs wholly inside the CTA were written final at
-// their flush; only the (at most two) runs cut by the range ends left
-// partials.  Count this CTA in for each; the last contributor merges.  Done
-// once, after the CTA's streaming: a global fence or atomic issued while the
-// SM saturates HBM with its own TMA reads waits microseconds behind that
-// traffic, so none is issued mid-stream.  Cost: fence + counter atomic +
-// one round trip per merged run (fast path).
+// traffic, so none is issued mid-stream.  (The generic kernel's static
+// split; the TMA kernel claims units from the queue instead.)
 template <int MG>
 __device__ void finish_cta(const View& p, int64_t NB, int grid, int t, int nt, int bar,
-                           MergeSmem<MG>* ms, bool fast) {
+                           MergeSmem<MG>* ms) {
     const int nruns = ms->nruns;  // written before the caller's last barrier
     if (nruns == 0) return;
     named_bar_sync(bar, nt);  // the partials are written; the release below publishes them
@@ -338,37 +291,39 @@ __device__ void finish_cta(const View& p, int64_t NB, int grid, int t, int nt, i
         if (!ms->flag[k]) continue;
         fence_acq_rel_gpu();
         const int bg = ms->runs[k];
-        if (fast) {
-            const int cf = cta_of(ms->rs[k], NB, grid), cl = cta_of(ms->re[k] - 1, NB, grid);
-            int list[kFastN], n = 0;
-            for (int c = cf; c <= cl && n <= kFastN; ++c)
-                if (cta_nonempty(c, NB, grid)) {
-                    if (n < kFastN) list[n] = c;
-                    ++n;
-                }
-            if (merge_run_fast(p, bg, list, n, t)) continue;
-        }
         merge_run(p, bg, ms->rs[k], ms->re[k], NB, grid, t, nt, bar, ms);
     }
 }
 
-#ifdef FX_TRACE  // profiling build only: per-CTA start/end time, runs, tiles
-__device__ long long g_trace[12 * 2048];
-__device__ __forceinline__ long long globaltimer() {
-    long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#endif
-
 // ---------------------------------------------------------------------------
-// TMA + mma.sync kernel
+// TMA + mma.sync kernel, fed by the unit queue
 // ---------------------------------------------------------------------------
 // Tensor maps of K (0) and V (1) viewed 3-D {64 cols, rows, D/64 chunks}
 // (strides: row D*2 B, chunk 128 B); box = 16 rows x all chunks, 128-B swizzle.
 struct KvMaps {
     CUtensorMap box[2];
 };
+
+// One attention unit = up to kUnitBoxes consecutive boxes of one (b, g)
+// (fx_worklist.cuh publish_units).  A unit of a single-unit group writes the
+// final (o, lse); otherwise one (o, lse) partial per unit, and the epilogue
+// warp of whichever CTA finishes a group's last unit merges the group.
+struct QView {
+    int n_bg, Hkv, G;
+    int64_t l_cap;
+    const float* q;
+    const Box* boxes;
+    int64_t box_stride;
+    const int32_t* bg_count;
+    UnitQueue uq;      // ctl zeroed by k_prepare
+    float* part_o;     // [unit][G][D]
+    float* part_lse;   // [unit][G] (natural log)
+    float* o;
+    float* lse;
+};
+
+constexpr int kEpi = kCWarps + 1;  // epilogue warp: combines a unit's consumer states
+constexpr int kQThreads = (kCWarps + 2) * 32;
 
 template <int D>
 struct TmaCfg {
@@ -379,27 +334,126 @@ struct TmaCfg {
     static constexpr int STAGE_BYTES = 2 * KV_BYTES;
     static constexpr int NT = D / 16;                  // k-steps (QK) and m-tiles (PV)
     static constexpr int WO_LD = D + 4;
+    static constexpr int QB_BYTES = 8 * D * 4;         // the unit's q rows (f32, G <= 8)
     static constexpr size_t TILES = (size_t)kStages * STAGE_BYTES;
-    static constexpr size_t HDR = TILES;
+    static constexpr size_t QB = TILES;
+    static constexpr size_t HDR = QB + (size_t)kStages * QB_BYTES;
     static constexpr size_t BAR = HDR + kStages * sizeof(TileHdr);
-    static constexpr size_t WO = BAR + 2 * kStages * sizeof(uint64_t);
+    static constexpr size_t SINFO = BAR + (2 * kStages + 2) * sizeof(uint64_t);
+    static constexpr size_t WO = SINFO + 32;
     static constexpr size_t WM = WO + (size_t)kCWarps * 8 * WO_LD * sizeof(float);
     static constexpr size_t WL = WM + kCWarps * 8 * sizeof(float);
-    static constexpr size_t MRG = WL + kCWarps * 8 * sizeof(float);
-    static constexpr size_t STARTS = MRG + sizeof(MergeSmem<8>);
-    static constexpr size_t TOTAL = STARTS + (kMaxPrefix + 1) * sizeof(int32_t) + 1024;  // + align slack
+    static constexpr size_t TOTAL = WL + kCWarps * 8 * sizeof(float) + 1024;  // + align slack
 };
 
+// Merge of the unit partials of every multi-unit group (attention.cpp:89-104
+// across the units, in unit order): one CTA per (b, g), launched behind the
+// attention kernel (PDL), every partial's loads in flight at once -- each
+// thread owns one float4 column of a fixed subset of the units, the subsets
+// are combined in a fixed order, so the result is deterministic.
+constexpr int kMergeThreads = 1024;
+__global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, int D,
+                                                              const int32_t* __restrict__ bg_count,
+                                                              const int32_t* __restrict__ ubase,
+                                                              const float* __restrict__ part_o,
+                                                              const float* __restrict__ part_lse,
+                                                              float* __restrict__ o, float* __restrict__ lse) {
+    pdl_wait();
+    pdl_trigger();
+    const int bg = blockIdx.x, t = threadIdx.x;
+    const int total = __ldg(bg_count + bg);
+    const int nun = total > 0 ? (total + kUnitBoxes - 1) / kUnitBoxes : 1;
+    if (nun <= 1) return;  // written final by the attention kernel
+    const int base = __ldg(ubase + bg);
+    const int VP = G * D / 4;               // float4 columns per partial
+    const int S = kMergeThreads / VP;       // unit subsets (>= 1: G * D <= 4096)
+    __shared__ float s_m[8];
+    __shared__ float4 s_acc[kMergeThreads];
+    __shared__ float s_den[kMergeThreads];
+    // per-head max of the unit LSEs
+    if (t < 32 * G) {
+        const int h = t >> 5, ln = t & 31;
+        float m = -INFINITY;
+        for (int i = ln; i < nun; i += 32) m = fmaxf(m, __ldg(part_lse + (int64_t)(base + i) * G + h));
+        m = warp_max(m);
+        if (ln == 0) s_m[h] = m;
+    }
+    __syncthreads();
+    const int v = t % VP, sub = t / VP;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float den = 0.f;
+    if (sub < S) {
+        const int h = v * 4 / D;
+        const float M = s_m[h];
+        constexpr int kIn = 8;
+        for (int i0 = sub; i0 < nun; i0 += S * kIn) {
+            float4 x[kIn];
+            float l[kIn];
+#pragma unroll
+            for (int j = 0; j < kIn; ++j) {
+                const int i = i0 + j * S;
+                const int64_t slot = (int64_t)(base + i) * G;
+                l[j] = i < nun ? __ldg(part_lse + slot + h) : -INFINITY;
+                x[j] = i < nun ? __ldg(reinterpret_cast<const float4*>(part_o + slot * D) + v)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < kIn; ++j) {
+                if (l[j] == -INFINITY) continue;
+                const float w = __expf(l[j] - M);
+                den += w;
+                acc.x += w * x[j].x;
+                acc.y += w * x[j].y;
+                acc.z += w * x[j].z;
+                acc.w += w * x[j].w;
+            }
+        }
+    }
+    s_acc[t] = acc;
+    s_den[t] = den;
+    __syncthreads();
+    if (sub != 0) return;
+    for (int k = 1; k < S; ++k) {
+        const float4 a = s_acc[k * VP + v];
+        acc.x += a.x;
+        acc.y += a.y;
+        acc.z += a.z;
+        acc.w += a.w;
+        den += s_den[k * VP + v];
+    }
+    const int b = bg / Hkv, g = bg % Hkv, h = v * 4 / D;
+    const int64_t head0 = (int64_t)b * Hkv * G + (int64_t)g * G;
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    float* dst = o + head0 * D + v * 4;
+    dst[0] = acc.x * inv;
+    dst[1] = acc.y * inv;
+    dst[2] = acc.z * inv;
+    dst[3] = acc.w * inv;
+    if ((v * 4) % D == 0 && lse) lse[head0 + h] = den > 0.f ? s_m[h] + __logf(den) : -INFINITY;
+}
+
+#ifdef FX_TRACE  // profiling build only: per-CTA start/end time, units, tiles
+__device__ long long g_trace[12 * 2048];
+__device__ __forceinline__ long long globaltimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+// Warp roles: 0..3 consumers (MMA), 4 producer (claims units, TMA), 5
+// epilogue.  No griddepcontrol.wait: the kernel reads only the worklist's
+// boxes (ordered by the acquire of the unit words), q and K/V; it becomes
+// resident once every selection CTA has started, and those were launched
+// after the scorer passed its wait on k_prepare (appended rows, zeroed
+// counters), so every earlier write of the step is visible.
 template <int D>
-__global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_constant__ KvMaps maps,
-                                                       const View p) {
-    // the tensor-map descriptors do not depend on the preceding kernels:
-    // fetch them while those finish
+__global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_constant__ KvMaps maps,
+                                                      const QView p) {
     if (threadIdx.x == kProducer * 32) {
         tma_prefetch_desc(&maps.box[0]);
         tma_prefetch_desc(&maps.box[1]);
     }
-    pdl_wait();
     pdl_trigger();
     using C = TmaCfg<D>;
     extern __shared__ unsigned char smem_raw[];
@@ -407,101 +461,134 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
     TileHdr* hdr = reinterpret_cast<TileHdr*>(smem + C::HDR);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR);
     uint64_t* empty = full + kStages;
+    uint64_t* sfull = empty + kStages;  // staging (wO / wm / wl) holds a finished unit
+    uint64_t* sempty = sfull + 1;       // ... and is free again
+    int* sinfo = reinterpret_cast<int*>(smem + C::SINFO);  // bg, u, c, nun, flags
     float* wO = reinterpret_cast<float*>(smem + C::WO);
     float* wm = reinterpret_cast<float*>(smem + C::WM);
     float* wl = reinterpret_cast<float*>(smem + C::WL);
-    MergeSmem<8>* ms = reinterpret_cast<MergeSmem<8>*>(smem + C::MRG);
-    int32_t* s_start = reinterpret_cast<int32_t*>(smem + C::STARTS);
-    __shared__ int s_wtmp[kTmaThreads / 32];
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(full + i, 1);
             mbar_init(empty + i, kCWarps);
         }
-        ms->nruns = 0;
+        mbar_init(sfull, kCWarps);
+        mbar_init(sempty, 1);
         fence_mbar_init();
     }
-    const int32_t* starts = run_starts(p, s_start, s_wtmp, tid, kTmaThreads);  // (syncs the CTA)
-    const int grid = gridDim.x, cta = blockIdx.x;
-    const int64_t NB = starts[p.n_bg];
-    const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
+    __syncthreads();
+#ifdef FX_TRACE
+    if (tid == 0) {
+        g_trace[blockIdx.x * 12 + 0] = globaltimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace[blockIdx.x * 12 + 11] = smid;
+    }
+#endif
 
     if (warp == kProducer) {
         // ------------------------------ producer ------------------------------
+        // Units are claimed one ahead: while unit `cur` streams, the next
+        // claim's flag word, box count and box descriptors are fetched.
+        struct Unit {
+            int u, bg, c, total;
+            Box wb;  // this lane's box descriptor
+        };
         int st = 0;
+        uint32_t ph = 0;
 #ifdef FX_TRACE
         long long p_wait = 0;
 #endif
-        uint32_t ph = 0;
-        int64_t x = r0;
-        int bg = r0 < r1 ? find_bg_warp(starts, p.n_bg, r0, lane) : 0;
-        while (x < r1) {
-            const int64_t s_bg = starts[bg];
-            const int64_t next_bg = starts[bg + 1];
-            const int64_t bg_end = min(r1, next_bg - p.pad);  // real boxes only
-            if (x >= bg_end) {  // only virtual boxes of this run in our range
-                x = next_bg;
-                ++bg;
-                continue;
-            }
-            const Box* bl = p.boxes + (int64_t)bg * p.box_stride - s_bg;
-            const int sole = (s_bg >= r0 && next_bg - p.pad <= r1) ? F_SOLE : 0;
-            bool first = true;
-            // box descriptors in two 32-box register windows, the next one
-            // loaded 8 tiles ahead so its latency never stalls the TMA issue
-            int64_t win = x;
-            Box wbox{0, 0, 0}, wnext{0, 0, 0};
-            if (x + lane < bg_end) wbox = bl[x + lane];
-            if (x + 32 + lane < bg_end) wnext = bl[x + 32 + lane];
-            while (x < bg_end) {
-                if (x >= win + 32) {  // tiles never straddle windows (both 4-aligned from s_bg)
-                    win += 32;
-                    wbox = wnext;
-                    const int64_t gx = win + 32 + lane;
-                    if (gx < bg_end) wnext = bl[gx];
+        // 1 = fetched, 0 = not published yet (block == false), -1 = queue drained
+        auto fetch = [&](int u, bool block, Unit& f) -> int {
+            uint64_t wd = 0;
+            int state = 0;
+            if (lane == 0) {
+                while (true) {
+                    wd = ld_acquire_gpu_u64(p.uq.words + u);
+                    if ((uint32_t)(wd >> 32) == p.uq.epoch) {
+                        state = 1;
+                        break;
+                    }
+                    if (ld_acquire_gpu_s32(p.uq.ctl + 1) == p.n_bg && u >= ld_relaxed_gpu_s32(p.uq.ctl + 0)) {
+                        state = -1;
+                        break;
+                    }
+                    if (!block) break;
+                    __nanosleep(64);
                 }
-                const int nb = (int)min((int64_t)kTileBoxes, bg_end - x);
+            }
+            __syncwarp();  // lane 0's acquire orders the other lanes' box loads
+            state = __shfl_sync(0xffffffffu, state, 0);
+            if (state != 1) return state;
+            const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)wd, 0);
+            f.u = u;
+            f.bg = (int)(lo >> kUnitIdxBits);
+            f.c = (int)(lo & ((1u << kUnitIdxBits) - 1u));
+            f.total = __ldcg(p.bg_count + f.bg);
+            const int x0 = f.c * kUnitBoxes, x1 = min(x0 + kUnitBoxes, f.total);
+            f.wb = Box{0, 0, 0};
+            if (x0 + lane < x1) {
+                const int2 r = __ldcg(reinterpret_cast<const int2*>(p.boxes + (int64_t)f.bg * p.box_stride + x0 + lane));
+                f.wb.row = r.x;
+                f.wb.n = (uint16_t)(r.y & 0xffff);
+                f.wb.mask = (uint16_t)((uint32_t)r.y >> 16);
+            }
+            return 1;
+        };
+        auto claim = [&]() {
+            int u = 0;
+            if (lane == 0) u = atomicAdd(p.uq.ctl + 2, 1);
+            return __shfl_sync(0xffffffffu, u, 0);
+        };
+        static_assert(kUnitBoxes == 32, "one box descriptor per lane");
+        Unit cur, nxt;
+#ifdef FX_TRACE
+        long long pw0 = globaltimer();
+#endif
+        int have = fetch(claim(), true, cur);
+#ifdef FX_TRACE
+        p_wait += globaltimer() - pw0;
+#endif
+        while (have == 1) {
+            const int un = claim();
+            int nstate = 0;
+            const int nun = cur.total > 0 ? (cur.total + kUnitBoxes - 1) / kUnitBoxes : 1;
+            const int x0 = cur.c * kUnitBoxes, x1 = min(x0 + kUnitBoxes, cur.total);
+            const int b = cur.bg / p.Hkv, g = cur.bg % p.Hkv;
+            const float* qsrc = p.q + ((int64_t)b * p.Hkv * p.G + (int64_t)g * p.G) * D;
+            const int64_t base = (int64_t)cur.bg * p.l_cap;
+            int x = x0;
+            bool first = true;
+            do {
+                const int nb = max(0, min(kTileBoxes, x1 - x));
                 Box bx[kTileBoxes];
 #pragma unroll
                 for (int i = 0; i < kTileBoxes; ++i) {
-                    const int src = (int)(x - win) + i;
-                    bx[i].row = __shfl_sync(0xffffffffu, wbox.row, src & 31);
-                    const uint32_t nm = __shfl_sync(0xffffffffu, (uint32_t)wbox.n | ((uint32_t)wbox.mask << 16), src & 31);
+                    const int src = (x - x0 + i) & 31;
+                    bx[i].row = __shfl_sync(0xffffffffu, cur.wb.row, src);
+                    const uint32_t nm = __shfl_sync(0xffffffffu, (uint32_t)cur.wb.n | ((uint32_t)cur.wb.mask << 16), src);
                     bx[i].n = (uint16_t)(nm & 0xffffu);
                     bx[i].mask = (uint16_t)(nm >> 16);
                 }
                 if (lane == 0) {
-#ifdef FX_TRACE
-                    const long long pw0 = globaltimer();
                     mbar_wait(empty + st, ph ^ 1u);
-                    p_wait += globaltimer() - pw0;
-#else
-                    mbar_wait(empty + st, ph ^ 1u);
-#endif
                     TileHdr& H = hdr[st];
-                    H.bg = bg;
+                    const bool last = x + nb >= x1;
+                    H.bg = cur.bg;
                     H.nb = nb;
-                    H.s = (int32_t)s_bg;
-                    H.e = (int32_t)(next_bg - p.pad);
-                    H.flags = (first ? F_FIRST : 0) | (x + nb == bg_end ? F_LAST | sole : 0);
+                    H.u = cur.u;
+                    H.c = cur.c;
+                    H.nun = nun;
+                    H.flags = (first ? F_FIRST : 0) | (last ? F_LAST | (nun == 1 ? F_SOLE : 0) : 0);
 #pragma unroll
                     for (int i = 0; i < kTileBoxes; ++i) H.box[i] = bx[i];
                     unsigned char* kt = smem + (size_t)st * C::STAGE_BYTES;
                     unsigned char* vt = kt + C::KV_BYTES;
-                    // Maximal runs of row-contiguous boxes move as power-of-two
-                    // pieces (8/4/2/1 boxes), ONE TMA per piece and tensor: a
-                    // piece of n boxes starting at tile slot s lands chunk-major
-                    // [chunk][16 n rows][128 B] in slots s..s+n-1 (each slot is
-                    // one box across all chunks), so a scattered box is one op
-                    // and a contiguous 8-box tile is one op.  The header records
-                    // each box's piece start / length for the consumers.
-                    // one 3-D TMA per box and tensor (measured faster than merging
-                    // contiguous runs: scratch/tma_bench.cu); box-major smem
-                    // [box][chunk][16 rows][128 B], 128-byte swizzle.
-                    mbar_arrive_expect_tx(full + st, (uint32_t)(nb * 2 * C::NCH * C::BOX_BYTES));
-                    const int64_t base = (int64_t)bg * p.l_cap;
+                    const uint32_t qbytes = first ? (uint32_t)(p.G * D * 4) : 0u;
+                    mbar_arrive_expect_tx(full + st, (uint32_t)(nb * 2 * C::NCH * C::BOX_BYTES) + qbytes);
+                    if (first) bulk_g2s(smem + C::QB + (size_t)st * C::QB_BYTES, qsrc, qbytes, full + st);
                     for (int i = 0; i < nb; ++i) {
                         const int row0 = (int)(base + bx[i].row);
                         tma_load_3d(kt + i * C::UNIT_BYTES, &maps.box[0], full + st, 0, row0, 0);
@@ -515,9 +602,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
                     st = 0;
                     ph ^= 1u;
                 }
-            }
-            x = max(x, next_bg);  // skip the run's virtual boxes
-            ++bg;
+                // the next unit's descriptors, while this unit's tiles are in flight
+                if (nstate == 0) nstate = fetch(un, false, nxt);
+            } while (x < x1);
+#ifdef FX_TRACE
+            pw0 = globaltimer();
+#endif
+            if (nstate == 0) nstate = fetch(un, true, nxt);
+#ifdef FX_TRACE
+            p_wait += globaltimer() - pw0;
+#endif
+            have = nstate;
+            cur = nxt;
         }
         if (lane == 0) {
             mbar_wait(empty + st, ph ^ 1u);
@@ -530,7 +626,69 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
         return;
     }
 
+    if (warp == kEpi) {
+        // ------------------------------ epilogue ------------------------------
+        uint32_t sph = 0;
+        const int G = p.G;
+        while (true) {
+            mbar_wait(sfull, sph);
+            const int bg = sinfo[0], u = sinfo[1], flags = sinfo[4];
+            if (flags & F_END) break;
+            const bool sole = flags & F_SOLE;
+            const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * G + (int64_t)(bg % p.Hkv) * G
+                                       : (int64_t)u * G;
+            float* dst_o = sole ? p.o : p.part_o;
+            float* dst_l = sole ? p.lse : p.part_lse;
+            // the four consumer warps' states of the unit -> one (o, lse): lane
+            // h < G forms head h's warp weights f_w / den once (into wl), then
+            // every lane combines float4 columns
+            if (lane < G) {
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) M = fmaxf(M, wm[w * 8 + lane]);
+                float hf[kCWarps], den = 0.f;
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) {
+                    const float mw = wm[w * 8 + lane];
+                    hf[w] = (M == -INFINITY || mw == -INFINITY) ? 0.f : exp2f(mw - M);
+                    den += hf[w] * wl[w * 8 + lane];
+                }
+                const float inv = den > 0.f ? 1.f / den : 0.f;
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) wl[w * 8 + lane] = hf[w] * inv;
+                if (dst_l) dst_l[head0 + lane] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
+            }
+            __syncwarp();
+            for (int e = lane; e < G * D / 4; e += 32) {
+                const int h = e * 4 / D, d = e * 4 % D;
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) {
+                    const float f = wl[w * 8 + h];
+                    const float4 x = *reinterpret_cast<const float4*>(wO + ((size_t)w * 8 + h) * C::WO_LD + d);
+                    acc.x += f * x.x;
+                    acc.y += f * x.y;
+                    acc.z += f * x.z;
+                    acc.w += f * x.w;
+                }
+                float* dst = dst_o + (head0 + h) * D + d;
+                dst[0] = acc.x;
+                dst[1] = acc.y;
+                dst[2] = acc.z;
+                dst[3] = acc.w;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sempty);
+            sph ^= 1u;
+        }
+#ifdef FX_TRACE
+        if (lane == 0) g_trace[blockIdx.x * 12 + 8] = globaltimer();
+#endif
+        return;
+    }
+
     // ------------------------------- consumers -------------------------------
+    const int G = p.G;
     const float sl2 = rsqrtf((float)D) * kLog2e;
     const int tok0 = lane >> 2, h0 = 2 * (lane & 3);
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
@@ -538,33 +696,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
     uint32_t qh[C::NT][2], ql[C::NT][2];
 #pragma unroll
     for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
-    float2 qn[C::NT][2];  // raw fp32 q of run qn_bg (prefetched)
-    int qn_bg = -1;
-    auto load_q = [&](int qb) {
-        const int b = qb / p.Hkv, g = qb % p.Hkv, hq = lane >> 2;
-        const float* qp = p.q + ((int64_t)b * p.Hkv * p.G + (int64_t)g * p.G + hq) * D;
-#pragma unroll
-        for (int j = 0; j < C::NT; ++j) {
-            const int d0 = 16 * j + 2 * (lane & 3);
-            qn[j][0] = qn[j][1] = make_float2(0.f, 0.f);
-            if (hq < p.G) {
-                qn[j][0] = __ldg(reinterpret_cast<const float2*>(qp + d0));
-                qn[j][1] = __ldg(reinterpret_cast<const float2*>(qp + d0 + 8));
-            }
-        }
-        qn_bg = qb;
-    };
     int st = 0;
-    uint32_t ph = 0;
+    uint32_t ph = 0, sph = 0;
 #ifdef FX_TRACE
-    if (tid == 0) {
-        g_trace[blockIdx.x * 12 + 0] = globaltimer();
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_trace[blockIdx.x * 12 + 11] = smid;
-    }
-    int runs = 0, tiles = 0;
-    long long t_wait = 0, t_first = 0, t_flush = 0, tw0 = 0;
+    int units = 0, tiles = 0;
+    long long t_wait = 0, tw0 = 0;
 #endif
     while (true) {
 #ifdef FX_TRACE
@@ -579,35 +715,36 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
 #ifdef FX_TRACE
             if (tid == 0) {
                 g_trace[blockIdx.x * 12 + 1] = globaltimer();
-                g_trace[blockIdx.x * 12 + 2] = runs;
+                g_trace[blockIdx.x * 12 + 2] = units;
                 g_trace[blockIdx.x * 12 + 3] = tiles;
                 g_trace[blockIdx.x * 12 + 4] = t_wait;
-                g_trace[blockIdx.x * 12 + 5] = t_first;
-                g_trace[blockIdx.x * 12 + 6] = t_flush;
             }
 #endif
             break;
         }
 #ifdef FX_TRACE
         ++tiles;
-        runs += (hdr[st].flags & F_FIRST) ? 1 : 0;
+        units += (flags & F_FIRST) ? 1 : 0;
 #endif
-        // everything the flush needs from the header is read before this warp
-        // releases the stage: once all warps arrive on empty[st] the producer
-        // refills hdr[st] with a later tile
+        // everything the unit's end needs from the header is read before this
+        // warp releases the stage (the producer then refills hdr[st])
         const int bg = hdr[st].bg, nb = hdr[st].nb;
-        const int run_s = hdr[st].s, run_e = hdr[st].e;
-        const int i0 = warp * kBPW;          // this warp's boxes: i0, i0 + 1
+        const int u = hdr[st].u, c = hdr[st].c, nun = hdr[st].nun;
+        const int i0 = warp * kBPW;  // this warp's boxes: i0, i0 + 1
         const Box bxa = hdr[st].box[i0];
         const Box bxb = hdr[st].box[i0 + 1];
-#ifdef FX_TRACE
-        tw0 = globaltimer();
-#endif
         if (flags & F_FIRST) {
-            if (bg != qn_bg) load_q(bg);  // prefetch missed (a skipped run)
+            // the unit's q rows arrived with this stage: split into bf16 hi + lo
+            const float* qs = reinterpret_cast<const float*>(smem + C::QB + (size_t)st * C::QB_BYTES);
+            const int hq = lane >> 2;
 #pragma unroll
             for (int j = 0; j < C::NT; ++j) {
-                const float2 x0 = qn[j][0], x1 = qn[j][1];
+                const int d0 = 16 * j + 2 * (lane & 3);
+                float2 x0 = make_float2(0.f, 0.f), x1 = make_float2(0.f, 0.f);
+                if (hq < G) {
+                    x0 = *reinterpret_cast<const float2*>(qs + hq * D + d0);
+                    x1 = *reinterpret_cast<const float2*>(qs + hq * D + d0 + 8);
+                }
                 const float a0 = __bfloat162float(__float2bfloat16_rn(x0.x));
                 const float a1 = __bfloat162float(__float2bfloat16_rn(x0.y));
                 const float a2 = __bfloat162float(__float2bfloat16_rn(x1.x));
@@ -617,17 +754,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
                 ql[j][0] = pack_bf16(x0.x - a0, x0.y - a1);
                 ql[j][1] = pack_bf16(x1.x - a2, x1.y - a3);
             }
-            // the next run of this CTA is almost always bg + 1: its q loads
-            // stay in flight for the whole run
-            if (bg + 1 < p.n_bg) load_q(bg + 1);
             m0 = m1 = -INFINITY;
             l0 = l1 = 0.f;
 #pragma unroll
             for (int i = 0; i < C::NT; ++i) O[i][0] = O[i][1] = O[i][2] = O[i][3] = 0.f;
         }
-#ifdef FX_TRACE
-        if (flags & F_FIRST) { __syncwarp(); t_first += globaltimer() - tw0; }
-#endif
 #ifdef FX_ATTEND_NO_MATH  // profiling variant: data delivery only
         if (false) {
 #else
@@ -721,84 +852,51 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_attend_tma(const __grid_cons
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + st);
-#ifdef FX_TRACE
-        tw0 = globaltimer();
-#endif
         if (flags & F_LAST) {
-            // ---- flush: hand this warp's run state to the epilogue warp ----
+            // ---- unit end: hand this warp's state to the epilogue warp ----
             float t0 = l0, t1 = l1;
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 t0 += __shfl_xor_sync(0xffffffffu, t0, o);
                 t1 += __shfl_xor_sync(0xffffffffu, t1, o);
             }
+            mbar_wait(sempty, sph ^ 1u);
             if (lane < 4) {
                 wm[warp * 8 + h0] = m0;
                 wm[warp * 8 + h0 + 1] = m1;
                 wl[warp * 8 + h0] = t0;
                 wl[warp * 8 + h0 + 1] = t1;
             }
-            {
-                float* wo = wO + (size_t)warp * 8 * C::WO_LD;
+            float* wo = wO + (size_t)warp * 8 * C::WO_LD;
 #pragma unroll
-                for (int i = 0; i < C::NT; ++i) {
-                    const int d0 = 16 * i + tok0;
-                    wo[h0 * C::WO_LD + d0] = O[i][0];
-                    wo[(h0 + 1) * C::WO_LD + d0] = O[i][1];
-                    wo[h0 * C::WO_LD + d0 + 8] = O[i][2];
-                    wo[(h0 + 1) * C::WO_LD + d0 + 8] = O[i][3];
-                }
+            for (int i = 0; i < C::NT; ++i) {
+                const int d0 = 16 * i + tok0;
+                wo[h0 * C::WO_LD + d0] = O[i][0];
+                wo[(h0 + 1) * C::WO_LD + d0] = O[i][1];
+                wo[h0 * C::WO_LD + d0 + 8] = O[i][2];
+                wo[(h0 + 1) * C::WO_LD + d0 + 8] = O[i][3];
             }
-            named_bar_sync(1, kCWarps * 32);
-            // a run wholly inside this CTA is final; else a partial for finish_cta
-            const bool sole = flags & F_SOLE;
-            if (!sole && tid == 0) {
-                ms->runs[ms->nruns] = bg;
-                ms->rs[ms->nruns] = run_s;
-                ms->re[ms->nruns] = run_e;
-                ++ms->nruns;
+            if (warp == 0 && lane == 0) {
+                sinfo[0] = bg;
+                sinfo[1] = u;
+                sinfo[2] = c;
+                sinfo[3] = nun;
+                sinfo[4] = flags;
             }
-            const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * p.G + (int64_t)(bg % p.Hkv) * p.G
-                                       : (int64_t)(blockIdx.x + bg) * p.G;
-            float* dst_o = sole ? p.o : p.part_o;
-            float* dst_l = sole ? p.lse : p.part_lse;
-            for (int e = tid; e < p.G * D; e += kCWarps * 32) {
-                const int h = e / D, d = e % D;
-                float M = -INFINITY;
-#pragma unroll
-                for (int w = 0; w < kCWarps; ++w) M = fmaxf(M, wm[w * 8 + h]);
-                float num = 0.f, den = 0.f;
-                if (M != -INFINITY) {
-#pragma unroll
-                    for (int w = 0; w < kCWarps; ++w) {
-                        const float mw = wm[w * 8 + h];
-                        const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
-                        num += f * wO[((size_t)w * 8 + h) * C::WO_LD + d];
-                        den += f * wl[w * 8 + h];
-                    }
-                }
-                dst_o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
-                if (d == 0 && dst_l) dst_l[head0 + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
-            }
-            named_bar_sync(1, kCWarps * 32);  // wO / wm / wl reused by the next run
-#ifdef FX_TRACE
-            t_flush += globaltimer() - tw0;
-#endif
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sfull);
+            sph ^= 1u;
         }
         if (++st == kStages) {
             st = 0;
             ph ^= 1u;
         }
     }
-    write_empty_runs(p, starts, r0, r1, tid, kCWarps * 32);
-    finish_cta(p, NB, grid, tid, kCWarps * 32, 1, ms, true);
-#ifdef FX_TRACE
-    if (tid == 0) {
-        g_trace[blockIdx.x * 12 + 8] = globaltimer();
-        g_trace[blockIdx.x * 12 + 9] = ms->nruns;
-        g_trace[blockIdx.x * 12 + 10] = ms->nruns > 0 ? ms->flag[0] + (ms->nruns > 1 ? ms->flag[1] : 0) : 0;
-    }
-#endif
+    // no more units: release the epilogue warp
+    mbar_wait(sempty, sph ^ 1u);
+    if (warp == 0 && lane == 0) sinfo[4] = F_END;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sfull);
 }
 
 // ---------------------------------------------------------------------------
@@ -951,7 +1049,7 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
 done:
     __syncthreads();
     write_empty_runs(p, starts, r0, r1, t, kGen);
-    finish_cta(p, NB, grid, t, kGen, 1, &ms, false);
+    finish_cta(p, NB, grid, t, kGen, 1, &ms);
 }
 
 #undef Ks
@@ -1052,14 +1150,33 @@ View make_view(const AttendArgs& a) {
 
 template <int D>
 void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
-    const View v = make_view(a);
+    FX_REQUIRE(a.uq.words != nullptr && a.uq.ctl != nullptr && a.uq.ubase != nullptr && a.uq.epoch != 0,
+               FX_ERR_STATE,
+               "no-context: the TMA attention kernel needs the worklist's unit queue");
+    QView v;
+    v.n_bg = a.L.batch * a.L.kv_heads;
+    v.Hkv = a.L.kv_heads;
+    v.G = a.L.group_size;
+    v.l_cap = a.L.l_cap;
+    v.q = a.q;
+    v.boxes = a.boxes;
+    v.box_stride = a.box_stride;
+    v.bg_count = a.bg_count;
+    v.uq = a.uq;
+    v.part_o = a.part_o;
+    v.part_lse = a.part_lse;
+    v.o = a.o;
+    v.lse = a.lse;
     const int64_t rows = (int64_t)v.n_bg * a.L.l_cap;
     KvMaps maps;
     maps.box[0] = make_row_map(a.k, D, rows, kBoxRows);
     maps.box[1] = make_row_map(a.v, D, rows, kBoxRows);
     const size_t smem = TmaCfg<D>::TOTAL;
     FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_pdl(k_attend_tma<D>, grid, kTmaThreads, smem, s, maps, v);
+    launch_pdl(k_attend_tma<D>, grid, kQThreads, smem, s, maps, v);
+    FX_CUDA(cudaGetLastError());
+    launch_pdl(k_merge_units, v.n_bg, kMergeThreads, 0, s, v.Hkv, v.G, D, a.bg_count,
+               (const int32_t*)a.uq.ubase, (const float*)a.part_o, (const float*)a.part_lse, a.o, a.lse);
 }
 
 }  // namespace
@@ -1099,6 +1216,12 @@ CUtensorMap make_row_map(const void* base, int D, int64_t rows, int box_rows) {
     return m;
 }
 
+int64_t unit_capacity(int64_t n_bg, int64_t box_stride) {
+    // every group's units at the worst case, plus the claims that run past the
+    // tail (at most two per CTA)
+    return n_bg * cdiv(std::max<int64_t>(box_stride, 1), kUnitBoxes) + 4096;
+}
+
 bool attend_uses_tma(const fx_layout& L, bool has_idx) {
     return !has_idx && L.dtype == FX_BF16 && (L.head_dim == 64 || L.head_dim == 128) &&
            L.group_size <= 8;
@@ -1113,9 +1236,11 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
                "bad-shape: group_size must be in [1, 16]");
     FX_REQUIRE(a.L.head_dim >= 1 && a.L.head_dim <= kGenMaxD, FX_ERR_INVALID,
                "bad-shape: head_dim must be in [1, 256]");
+    int n = 1;
     if (allow_tma && attend_uses_tma(a.L, a.idx != nullptr)) {
         if (a.L.head_dim == 128) launch_tma<128>(a, grid, s);
         else launch_tma<64>(a, grid, s);
+        n = 2;  // + the unit merge
     } else {
         const View v = make_view(a);
         const int D = a.L.head_dim, G = a.L.group_size;
@@ -1130,7 +1255,7 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
         }
     }
     FX_CUDA(cudaGetLastError());
-    return 1;
+    return n;
 }
 
 void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_count,

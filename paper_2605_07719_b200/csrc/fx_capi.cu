@@ -98,6 +98,10 @@ struct fx_ctx {
     DevBuf api;   // per-query API scratch
     DevBuf label; // fx_label_heads scratch
     DevBuf errw;  // sticky device error word (invalid given block sizes), read by fx_ctx_synchronize
+    // attention unit queue flag words (epoch-tagged; zeroed when grown, so a
+    // fresh buffer never holds the current epoch)
+    DevBuf uq;
+    uint32_t uq_epoch = 0;
     // optional per-kernel CUDA-event timing (fx_ctx_set_timing)
     bool timing = false;
     std::vector<cudaEvent_t> pool;
@@ -185,7 +189,8 @@ struct StepScratch {
     int64_t box_stride;
     int32_t* bg_count;
     int32_t* bg_start;
-    int32_t* bg_done;  // [2 n_bg + 1]: attend counters | publish counter | select counters
+    int32_t* bg_done;  // [2 n_bg + 5]: attend counters | publish counter | select counters | unit queue
+    int32_t* ubase;    // [n_bg] first unit of each group
     float* part_o;
     float* part_lse;
 };
@@ -193,7 +198,7 @@ struct StepScratch {
 // Offsets of the decode-step scratch regions (one layout for the allocation
 // and for the public size query fx_step_scratch_bytes).
 struct StepOffsets {
-    size_t blk, bud, kb, apx, bits, ck, ci, box, cnt, st, dn, po, pl, total;
+    size_t blk, bud, kb, apx, bits, ck, ci, box, cnt, st, dn, ub, po, pl, total;
     int64_t approx_stride, box_stride;
     int words;
 };
@@ -219,9 +224,12 @@ StepOffsets step_offsets(const fx_layout& L, int grid) {
     o.box = c.take<fx::Box>(n_bg * o.box_stride);
     o.cnt = c.take<int32_t>(n_bg);
     o.st = c.take<int32_t>(n_bg + 1);
-    o.dn = c.take<int32_t>(2 * n_bg + 1);
-    o.po = c.take<float>((grid + n_bg) * L.group_size * L.head_dim);
-    o.pl = c.take<float>((grid + n_bg) * L.group_size);
+    o.dn = c.take<int32_t>(2 * n_bg + 5);
+    o.ub = c.take<int32_t>(n_bg);
+    // partial slots: the generic kernel's (grid + n_bg), the TMA kernel's units
+    const int64_t slots = std::max<int64_t>(grid + n_bg, fx::unit_capacity(n_bg, o.box_stride));
+    o.po = c.take<float>(slots * L.group_size * L.head_dim);
+    o.pl = c.take<float>(slots * L.group_size);
     o.total = c.off;
     return o;
 }
@@ -245,6 +253,7 @@ StepScratch carve_step(fx_ctx* ctx, const fx_layout& L, int grid, bool alloc) {
     s.bg_count = reinterpret_cast<int32_t*>(b + o.cnt);
     s.bg_start = reinterpret_cast<int32_t*>(b + o.st);
     s.bg_done = reinterpret_cast<int32_t*>(b + o.dn);
+    s.ubase = reinterpret_cast<int32_t*>(b + o.ub);
     s.part_o = reinterpret_cast<float*>(b + o.po);
     s.part_lse = reinterpret_cast<float*>(b + o.pl);
     return s;
@@ -391,6 +400,7 @@ int fx_ctx_destroy(fx_ctx* ctx) {
         ctx->api.release();
         ctx->label.release();
         ctx->errw.release();
+        ctx->uq.release();
         if (ctx->own) cudaStreamDestroy(ctx->own);
         delete ctx;
     });
@@ -742,9 +752,23 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
             ap.bf16 = L.dtype == FX_BF16;
         }
         const int64_t l_new = a->l_new + (a->append_k ? 1 : 0);  // rows attended this step
+        // the TMA attention kernel is fed by the worklist's unit queue
+        fx::UnitQueue uq;
+        if (fx::attend_uses_tma(L, false)) {
+            const size_t wbytes = sizeof(uint64_t) * (size_t)fx::unit_capacity(n_bg, s.box_stride);
+            if (wbytes > ctx->uq.bytes) {
+                ctx->uq.ensure(wbytes);
+                FX_CUDA(cudaMemsetAsync(ctx->uq.p, 0, ctx->uq.bytes, ctx->stream));
+            }
+            if (++ctx->uq_epoch == 0) ctx->uq_epoch = 1;
+            uq.words = static_cast<uint64_t*>(ctx->uq.p);
+            uq.ctl = s.bg_done + 2 * n_bg + 1;
+            uq.ubase = s.ubase;
+            uq.epoch = ctx->uq_epoch;
+        }
         const fx::WorklistArgs wl{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + l_new,
                                   nullptr, nullptr, 0, s.boxes, s.box_stride, s.bg_count,
-                                  s.bg_start, s.bg_done + n_bg};
+                                  s.bg_start, s.bg_done + n_bg, uq};
         static const bool no_fuse = std::getenv("FX_DEBUG_NO_FUSED_WORKLIST") != nullptr;
         const Planned pl = plan_and_select(ctx, L, a, s, false, no_fuse ? nullptr : &wl,
                                            a->append_k ? &ap : nullptr);
@@ -754,7 +778,7 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         if (!pl.fused) {
             Timed tm(ctx, FX_KERNEL_WORKLIST);
             fx::launch_worklist(L, l_new, blk, s.sel_bits, s.sel_words, s.boxes, s.box_stride,
-                                s.bg_count, s.bg_start, s.bg_done, st);
+                                s.bg_count, s.bg_start, s.bg_done, st, uq);
             n += 1;
         }
         fx::AttendArgs aa{};
@@ -773,6 +797,7 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         aa.bg_done = s.bg_done;
         aa.o = a->o;
         aa.lse = a->lse;
+        aa.uq = uq;
         {
             Timed tm(ctx, FX_KERNEL_ATTEND);
             n += fx::launch_attend(aa, grid, true, st);

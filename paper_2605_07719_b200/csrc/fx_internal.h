@@ -22,6 +22,13 @@ constexpr int kRunPad = 16;
 // Batches up to this many (b, g) runs get their run starts rebuilt in smem
 // by the attention kernels from the worklist's per-run counts.
 constexpr int kMaxRunPrefix = 1024;
+// Attention work unit of the TMA kernel: up to this many consecutive boxes of
+// one (b, g) (4 pipeline tiles).  The worklist publishes a group's units to a
+// queue as soon as the group's boxes exist; persistent attention CTAs claim
+// units in publication order.
+constexpr int kUnitBoxes = 32;
+// Unit queue flag word: epoch (32) | bg (19) | unit index in the group (13).
+constexpr int kUnitBgBits = 19, kUnitIdxBits = 13;
 // Candidate granularities, selector.hpp:12.
 constexpr int kLevels[4] = {16, 32, 64, 128};
 
@@ -124,6 +131,13 @@ void launch_approx_scores(const fx_layout& L, const void* const meta[4], const f
                           const int32_t* blk, const int32_t* kblocks, float* approx,
                           int64_t approx_stride, int num_sms, cudaStream_t s, bool rank_all = false);
 struct WorklistArgs;
+// The attention unit queue a worklist publishes into (words == nullptr: none).
+struct UnitQueue {
+    uint64_t* words = nullptr;  // [unit_capacity] epoch-tagged flag words
+    int32_t* ctl = nullptr;     // [4]: tail, groups, claim, (spare); zeroed by k_prepare
+    int32_t* ubase = nullptr;   // [n_bg] first unit id of each group (for the unit merge)
+    uint32_t epoch = 0;
+};
 // wl != nullptr: the selection kernel also builds the attention boxes (fused
 // worklist); sel_done = [n_bg] per-group head counters, zeroed by k_prepare.
 void launch_select(const fx_layout& L, const void* const meta[4], const float* absmax,
@@ -133,7 +147,8 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
                    const WorklistArgs* wl = nullptr, int32_t* sel_done = nullptr);
 void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
                      const uint32_t* sel_bits, int sel_words, Box* boxes, int64_t box_stride,
-                     int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s);
+                     int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s,
+                     const UnitQueue& uq = UnitQueue());
 void launch_exact_scores(const float* q, const void* meta, int dtype, int64_t nblk, int dim,
                          double* scores, cudaStream_t s);
 // exact scores of all blocks, sorted (score desc, id asc); first k ids out.
@@ -222,12 +237,16 @@ struct AttendArgs {
     const int32_t* bg_start;  // [n_bg + 1] exclusive prefix of (box count + pad), for n_bg > 1024
     const int32_t* bg_count;  // [n_bg] box counts (run starts rebuilt in smem for n_bg <= 1024)
     int pad;                  // virtual boxes at the end of each run (kRunPad or 0)
-    float* part_o;            // [(grid + n_bg)][G][D]
-    float* part_lse;          // [(grid + n_bg)][G]
+    float* part_o;            // generic: [(grid + n_bg)][G][D]; TMA: [unit][G][D]
+    float* part_lse;          // generic: [(grid + n_bg)][G];    TMA: [unit][G]
     int32_t* bg_done;         // [n_bg], zeroed before the launch
     float* o;                 // [B][H][D]
     float* lse;               // [B][H] or nullptr
+    // unit queue of the TMA kernel (published by the worklist; see kUnitBoxes)
+    UnitQueue uq;             // TMA kernel only; epoch != 0
 };
+// Units a step can publish at most (partial slots of the TMA kernel).
+int64_t unit_capacity(int64_t n_bg, int64_t box_stride);
 bool attend_uses_tma(const fx_layout& L, bool has_idx);
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms);
 // returns the number of kernels launched

@@ -63,7 +63,10 @@ __global__ void k_prepare(int n_bg, int G, int64_t l_cpu, int mode, int fixed_bl
     if (h == 0 && bg_done) {
         bg_done[bg] = 0;                 // attention contributors of (b, g)
         bg_done[n_bg + 1 + bg] = 0;      // selected heads of (b, g) (fused worklist)
-        if (bg == 0) bg_done[n_bg] = 0;  // worklist publish counter
+        if (bg == 0) {
+            bg_done[n_bg] = 0;  // worklist publish counter
+            for (int i = 0; i < 4; ++i) bg_done[2 * n_bg + 1 + i] = 0;  // attention unit queue
+        }
     }
     int blk = 0;
     double bud = 0.0, vol = 0.0, cv[4] = {0, 0, 0, 0};

@@ -80,11 +80,12 @@ __global__ void k_bitonic(uint64_t* keys, uint32_t* ids, int64_t n, int64_t j, i
 
 void launch_worklist(const fx_layout& L, int64_t l_new, const int32_t* blk,
                      const uint32_t* sel_bits, int sel_words, Box* boxes, int64_t box_stride,
-                     int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s) {
+                     int32_t* bg_count, int32_t* bg_start, int32_t* done, cudaStream_t s,
+                     const UnitQueue& uq) {
     FX_REQUIRE(L.group_size <= 16, FX_ERR_INVALID, "bad-shape: group_size must be <= 16");
     const int n_bg = L.batch * L.kv_heads;
     const WorklistArgs w{L.kv_heads, L.group_size, L.l_sink, L.l_cpu, L.l_local + l_new, blk, sel_bits,
-                         sel_words, boxes, box_stride, bg_count, bg_start, done + n_bg};
+                         sel_words, boxes, box_stride, bg_count, bg_start, done + n_bg, uq};
     launch_pdl(k_worklist, n_bg, 256, 0, s, w);
     FX_CUDA(cudaGetLastError());
 }

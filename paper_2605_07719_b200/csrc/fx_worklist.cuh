@@ -30,7 +30,34 @@ struct WorklistArgs {
     int32_t* bg_count;              // [n_bg]
     int32_t* bg_start;              // [n_bg + 1] (published only when n_bg > kMaxRunPrefix)
     int32_t* publish_done;          // completion counter for the publish
+    UnitQueue uq;                   // the attention unit queue (uq.words == nullptr: none)
 };
+
+// A group's boxes are final: publish its attention units (kUnitBoxes boxes
+// each; one empty unit for a group without boxes, whose output is then the
+// merge identity) to the unit queue.  All threads of the CTA, after the boxes
+// and bg_count are written.  Release: each publishing lane fences after the
+// CTA barrier, then stores its epoch-tagged flag words; the group counter is a
+// release add after the words (a claimer that sees every group published reads
+// the final tail).
+__device__ inline void publish_units(const WorklistArgs& w, int bg, int64_t total) {
+    if (w.uq.words == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const int n = total > 0 ? (int)((total + kUnitBoxes - 1) / kUnitBoxes) : 1;
+    int base = 0;
+    if (lane == 0) {
+        base = atomicAdd(w.uq.ctl + 0, n);
+        w.uq.ubase[bg] = base;
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    fence_acq_rel_gpu();
+    const uint64_t tag = ((uint64_t)w.uq.epoch << 32) | ((uint64_t)(uint32_t)bg << kUnitIdxBits);
+    for (int i = lane; i < n; i += 32) st_relaxed_gpu_u64(w.uq.words + base + i, tag | (uint64_t)i);
+    __syncwarp();
+    if (lane == 0) red_release_gpu_add(w.uq.ctl + 1, 1);
+}
 
 // Exclusive block scan of cnt[0..n) in place; returns the total.  wsum: nt + 1.
 __device__ inline int64_t block_exclusive_scan(int32_t* cnt, int n, int64_t* wsum) {
@@ -156,6 +183,7 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
             }
             WL_MARK(14);
             if (t == 0) w.bg_count[bg] = (int32_t)total;
+            publish_units(w, bg, total);
             return;
         }
         for (int j = t; j < W; j += nt) {
@@ -201,6 +229,7 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
     }
     WL_MARK(14);
     if (t == 0) w.bg_count[bg] = (int32_t)total;
+    publish_units(w, bg, total);
 }
 
 // For n_bg > kMaxRunPrefix: the CTA that completes the last group publishes
@@ -208,6 +237,7 @@ __device__ inline void worklist_group(const WorklistArgs& w, int bg, int32_t* wc
 // All threads of a CTA that has just finished worklist_group(); blockDim <= 1024.
 __device__ inline void worklist_publish(const WorklistArgs& w, int n_bg) {
     if (n_bg <= kMaxRunPrefix) return;  // the attention kernels rebuild the run starts from the counts
+    if (w.uq.words) return;             // the unit queue needs no global prefix
     __shared__ int s_last;
     __shared__ int wtot[32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nt = blockDim.x;
