@@ -1051,45 +1051,48 @@ def run_ours(a):
         pred = Predictor(eng, params)
 
         def pred_step():
+            # the previous token is appended inside the feature kernel (the
+            # features see it, as decode_features after append_new does)
             i = step_i[0]
-            pp = dec.predict_props(qs[i], rec, pred)  # features + predictor, one launch
-            dec.step(qs[i], props=pp, append=(kv_new[i - 1, 0], kv_new[i - 1, 1]))
+            pp = dec.predict_props(qs[i], rec, pred, append=(kv_new[i - 1, 0], kv_new[i - 1, 1]))
+            dec.step(qs[i], props=pp)
             step_i[0] += 1
+            return pp
 
         for _ in range(a.warmup):
             pred_step()
         torch.cuda.synchronize()
         t0.record()
         for _ in range(a.steps):
-            pred_step()
+            pp = pred_step()
         t1.record()
         torch.cuda.synchronize()
         pms = max_over_ranks(t0.elapsed_time(t1))
-        # phase split of one more step (events serialize the phases), and the
-        # two-launch feature path (fx_decode_features + fx_predict) for reference
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        # phase split: the props launch alone and the step alone, each repeated
+        # back to back on the same inputs (no append), CUDA events around the loop
+        nrep = 20
         i = step_i[0]
-        ev[0].record()
-        pp = dec.predict_props(qs[i], rec, pred)
-        ev[1].record()
-        dec.step(qs[i], props=pp, append=(kv_new[i - 1, 0], kv_new[i - 1, 1]))
-        ev[2].record()
-        dec.decode_features(qs[i], rec, out=feats)
-        ev[3].record()
-        pred(feats)
-        ev[4].record()
-        step_i[0] += 1
+        t0.record()
+        for _ in range(nrep):
+            pp = dec.predict_props(qs[i], rec, pred)
+        t1.record()
         torch.cuda.synchronize()
+        props_ms = t0.elapsed_time(t1) / nrep
+        t0.record()
+        for _ in range(nrep):
+            dec.step(qs[i], props=pp)
+        t1.record()
+        torch.cuda.synchronize()
+        pstep_ms = t0.elapsed_time(t1) / nrep
         stream_frac = float(pp[2].float().mean().item())
         retr_groups = int((dec.plan_blk > 0).sum().item())
         result["predictor_path"] = {
             "value": world * a.steps / (pms / 1e3), "unit": UNIT, "ms_per_step": pms / a.steps,
-            "predict_props_ms": ev[0].elapsed_time(ev[1]), "decode_step_ms": ev[1].elapsed_time(ev[2]),
-            "two_launch_features_ms": ev[2].elapsed_time(ev[3]), "two_launch_predict_ms": ev[3].elapsed_time(ev[4]),
+            "predict_props_ms": props_ms, "decode_step_ms": pstep_ms, "decoded_rows": dec.l_new,
             "retrieval_groups": retr_groups,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
-            "per_step": "fx_predict_props (decode features + predictor, one clustered launch) + "
-                        "fx_decode_step (append fused)",
+            "per_step": "fx_predict_props (previous token appended; decode features as chunk "
+                        "partials + one clustered merge; the predictor's three layers) + fx_decode_step",
             "model": "random-init 41-256-384-3, output bias at the drawn-props operating point"}
         pred.close()
 

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FX_ABI_VERSION 4
+#define FX_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define FX_API __attribute__((visibility("default")))
@@ -299,19 +299,24 @@ FX_API int fx_prefill_stats(fx_ctx* ctx, const fx_layout* lay, const void* k, co
 FX_API int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
                               int64_t l_new, const float* q, const double* rec, double* features);
 /* decode_features + normalize + predict for every head (features.cpp:162-233,
- * predictor.cpp:161-185, pipeline.cpp:277-290): the features in ONE launch --
- * the Hkv groups of a sequence run as one thread-block cluster and exchange
- * the cross-head maximum (feature 39) through distributed shared memory --
- * then the predictor's three tiled layers.  Writes the head properties
- * bgt0 / kslope / streaming [dev] [B][H] (feed them to fx_decode_step,
- * FX_PLAN_PROPS); features [dev] [B][H][41] and raw logits z [dev] [B][H][3]
- * are optional.  Shapes the clustered kernel does not cover (group size
- * outside {1,2,4,7,8}, head_dim not 64/128, kv_heads > 8) take the
+ * predictor.cpp:161-185, pipeline.cpp:277-290).  The features take two
+ * launches: the f64 default-segment attention as 64-row chunk partials over
+ * the whole machine, then one merge launch in which the Hkv groups of a
+ * sequence run as one thread-block cluster and exchange the cross-head
+ * maximum (feature 39) through distributed shared memory; then the
+ * predictor's three tiled layers.  append_k / append_v [dev] [B][Hkv][D] f32
+ * (nullable, together): the previous token (append_new, pipeline.cpp:406-412)
+ * is written at decoded row l_new first and counted in (l_new + 1 decoded rows
+ * attended) -- pass l_new + 1 to the step that follows.  Writes the head
+ * properties bgt0 / kslope / streaming [dev] [B][H] (feed them to
+ * fx_decode_step, FX_PLAN_PROPS); features [dev] [B][H][41] and raw logits z
+ * [dev] [B][H][3] are optional.  Shapes the split kernels do not cover (group
+ * size outside {1,2,4,7,8}, head_dim not 64/128, kv_heads > 8) take the
  * fx_decode_features kernels instead, with the same results. */
-FX_API int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v,
-                            int64_t l_new, const float* q, const double* rec, const fx_model* model,
-                            double* features, double* z, double* bgt0, double* kslope,
-                            int32_t* streaming);
+FX_API int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_t l_new,
+                            const float* append_k, const float* append_v, const float* q,
+                            const double* rec, const fx_model* model, double* features, double* z,
+                            double* bgt0, double* kslope, int32_t* streaming);
 
 /* ---- synthetic workload generator (workload.cpp) ------------------------- */
 /* WorkloadSpec (workload.hpp:16-54), same fields and defaults semantics. */

@@ -19,7 +19,7 @@ FX_PLAN_PROPS = 0
 FX_PLAN_FIXED = 1
 FX_PLAN_FULL = 2
 FX_PLAN_GIVEN = 3
-ABI_VERSION = 4
+ABI_VERSION = 5
 KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append")
 
 _p = C.c_void_p
@@ -151,7 +151,7 @@ _SIGS = {
     "fx_decode_features": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p]),
     "fx_memcpy_d2d": (C.c_int, [_p, _p, _p, _sz]),
     "fx_build_metadata_means": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _p, _p]),
-    "fx_predict_props": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "fx_predict_props": (C.c_int, [_p, C.POINTER(Layout), _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "fx_generate": (C.c_int, [_p, C.POINTER(WorkloadSpec), C.POINTER(Layout), _p, _p, _p, _p, _p,
                               _i32, _p, _p, _p, _p]),
     "fx_trace_info_read": (C.c_int, [C.c_char_p, C.POINTER(TraceInfo)]),

@@ -1007,15 +1007,23 @@ int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, const v
         FX_REQUIRE(k && v && q && rec && features, FX_ERR_STATE, "no-context: features have no payload");
         FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_new <= L.l_cap, FX_ERR_INVALID,
                    "bad-shape: decoded rows exceed l_cap");
-        ctx->api.ensure(fx::decode_features_scratch_bytes(L, l_new));
-        fx::launch_decode_features(L, k, v, l_new, q, rec, features, ctx->api.p, ctx->stream);
-        ctx->launches += 3;
+        if (fx::feat_fused_supported(L)) {
+            ctx->api.ensure(fx::feat_fused_scratch_bytes(L, l_new));
+            fx::launch_feat_fused(L, const_cast<void*>(k), const_cast<void*>(v), l_new, q, rec, features,
+                                  ctx->api.p, ctx->stream, nullptr, nullptr, nullptr, nullptr, ctx->num_sms);
+            ctx->launches += 2;
+        } else {
+            ctx->api.ensure(fx::decode_features_scratch_bytes(L, l_new));
+            fx::launch_decode_features(L, k, v, l_new, q, rec, features, ctx->api.p, ctx->stream);
+            ctx->launches += 3;
+        }
     });
 }
 
-int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, const void* k, const void* v, int64_t l_new,
-                     const float* q, const double* rec, const fx_model* m, double* features, double* z,
-                     double* bgt0, double* kslope, int32_t* streaming) {
+int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_t l_new,
+                     const float* append_k, const float* append_v, const float* q, const double* rec,
+                     const fx_model* m, double* features, double* z, double* bgt0, double* kslope,
+                     int32_t* streaming) {
     return guarded([&] {
         NvtxRange nv("fx_predict_props");
         DeviceGuard g(ctx);
@@ -1024,22 +1032,40 @@ int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, const void* k, const voi
         FX_REQUIRE(m != nullptr, FX_ERR_STATE, "no-model: predictor source requires a model");
         FX_REQUIRE(k && v && q && rec && bgt0 && kslope && streaming, FX_ERR_STATE,
                    "no-context: predictor step has no payload");
-        FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_new <= L.l_cap, FX_ERR_INVALID,
+        FX_REQUIRE((append_k == nullptr) == (append_v == nullptr), FX_ERR_INVALID,
+                   "bad-shape: append_k and append_v go together");
+        const int64_t l_eff = l_new + (append_k ? 1 : 0);  // rows attended (the appended one included)
+        FX_REQUIRE(l_new >= 0 && L.l_sink + L.l_cpu + L.l_local + l_eff <= L.l_cap, FX_ERR_INVALID,
                    "bad-shape: decoded rows exceed l_cap");
         const int64_t nh = (int64_t)L.batch * L.kv_heads * L.group_size;
         const bool fused = fx::feat_fused_supported(L);
-        const size_t fs = fused ? 0 : fx::decode_features_scratch_bytes(L, l_new);
-        const size_t fb = features ? 0 : (size_t)nh * 41 * sizeof(double);
-        ctx->api.ensure(fs + fb + 256);
-        double* f = features ? features
-                             : reinterpret_cast<double*>(static_cast<char*>(ctx->api.p) + ((fs + 255) & ~size_t(255)));
-        if (fused) fx::launch_feat_fused(L, k, v, l_new, q, rec, f, ctx->stream);  // one clustered launch
-        else fx::launch_decode_features(L, k, v, l_new, q, rec, f, ctx->api.p, ctx->stream);
+        if (!fused && append_k) {  // the general-shape feature kernels read the cache only
+            fx::launch_append(L, k, v, L.l_sink + L.l_cpu + L.l_local + l_new, append_k, append_v, ctx->stream);
+            ctx->launches += 1;
+        }
         auto* mm = const_cast<fx_model*>(m);
         mm->act.ensure(fx::predict_scratch_bytes((int)nh));
-        fx::launch_predict((int)nh, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma, f, bgt0,
-                           kslope, streaming, z, mm->act.p, ctx->stream);
-        ctx->launches += (fused ? 1 : 3) + 3;
+        double* a1 = static_cast<double*>(mm->act.p);
+        double* a2 = a1 + (size_t)nh * 256;
+        if (fused) {  // features -> normalize -> layer 1 inside the merge kernel, then layers 2 and 3
+            ctx->api.ensure(fx::feat_fused_scratch_bytes(L, l_eff));
+            const double* l1[4] = {m->w1t, m->b1, m->mu, m->sigma};
+            fx::launch_feat_fused(L, k, v, l_eff, q, rec, features, ctx->api.p, ctx->stream, append_k, append_v,
+                                  l1, a1, ctx->num_sms);
+            fx::launch_predict_tail((int)nh, a1, m->w2t, m->b2, m->w3t, m->b3, bgt0, kslope, streaming, z, a2,
+                                    ctx->stream);
+            ctx->launches += 4;
+        } else {
+            const size_t fs = fx::decode_features_scratch_bytes(L, l_eff);
+            const size_t fb = features ? 0 : (size_t)nh * 41 * sizeof(double);
+            ctx->api.ensure(fs + fb + 256);
+            double* f = features ? features
+                                 : reinterpret_cast<double*>(static_cast<char*>(ctx->api.p) + ((fs + 255) & ~size_t(255)));
+            fx::launch_decode_features(L, k, v, l_eff, q, rec, f, ctx->api.p, ctx->stream);
+            fx::launch_predict((int)nh, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma, f, bgt0,
+                               kslope, streaming, z, mm->act.p, ctx->stream);
+            ctx->launches += 6;
+        }
     });
 }
 

@@ -120,6 +120,11 @@ void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, 
 // the 41-256-384-3 predictor as three tiled f64 layer kernels; scratch holds
 // the hidden activations (predict_scratch_bytes(n))
 size_t predict_scratch_bytes(int n);
+// layers 2 and 3 + the head properties from the first hidden layer's output
+// a1 [n][256]; a2 [n][384] scratch (the fused feature path computes layer 1)
+void launch_predict_tail(int n, const double* a1, const double* w2t, const double* b2, const double* w3t,
+                         const double* b3, double* bgt0, double* kslope, int32_t* streaming, double* z,
+                         double* a2, cudaStream_t s);
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
                     const double* b2, const double* w3t, const double* b3, const double* mu,
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
@@ -187,10 +192,16 @@ void launch_decode_features(const fx_layout& L, const void* k, const void* v, in
                             const float* q, const double* rec, double* feats, void* scratch,
                             cudaStream_t s);
 
-// fx_predict_step.cu: decode features of every head in one clustered launch
+// fx_predict_step.cu: decode features of every head -- chunk partials over the
+// machine, then one clustered merge; l_new counts the appended row (if any)
 bool feat_fused_supported(const fx_layout& L);
-void launch_feat_fused(const fx_layout& L, const void* k, const void* v, int64_t l_new, const float* q,
-                       const double* rec, double* feats, cudaStream_t s);
+size_t feat_fused_scratch_bytes(const fx_layout& L, int64_t l_new);
+// layer1 = {w1t, b1, mu, sigma} (nullable): the merge kernel also normalizes
+// the features and runs the predictor's first layer into a1 [heads][256]
+void launch_feat_fused(const fx_layout& L, void* k, void* v, int64_t l_new, const float* q, const double* rec,
+                       double* feats, void* scratch, cudaStream_t s, const float* append_k = nullptr,
+                       const float* append_v = nullptr, const double* const layer1[4] = nullptr,
+                       double* a1 = nullptr, int num_sms = 148);
 
 // fx_workload.cu: generate(spec) into the device cache
 void generate_workload(const fx_layout& L, const fx_workload_spec& sp, const uint64_t* seeds,

@@ -274,11 +274,89 @@ __global__ void __launch_bounds__(kMT) k_mlp_layer(int n, const double* __restri
     }
 }
 
+// Hidden layer 2 (256 -> 384, ReLU), the predictor's FP64-bound layer: the
+// same in-order unfused chains, tiled so every SM sub-partition carries
+// chains: a CTA owns 16 rows x 32 neurons (4 warps, 8 rows x 16 neurons
+// each), a thread 2 rows x 2 neurons = 4 interleaved chains (one weight
+// load serves two rows, one input load two neurons).  The rows' inputs sit
+// in shared memory (row stride padded by 16 bytes: the four row pairs a warp
+// reads are in different banks); the weights are read from L2 / L1 directly,
+// a window of 8 inputs ahead in registers, so the warps never synchronize
+// inside the 256-input loop.  384 CTAs of 128 threads.
+constexpr int kH2R = 16, kH2N = 32, kH2T = 128, kH2XS = kH1 + 2, kH2W = 8;
+__global__ void __launch_bounds__(kH2T) k_mlp_h2(int n, const double* __restrict__ x,
+                                                 const double* __restrict__ wt,
+                                                 const double* __restrict__ bias, double* __restrict__ y) {
+    extern __shared__ __align__(16) double h2sm[];
+    double* xs = h2sm;  // [kH2R][kH2XS]
+    const int r0 = blockIdx.x * kH2R, n0 = blockIdx.y * kH2N;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int rl = (warp >> 1) * 8 + (lane >> 3) * 2;  // this thread's rows rl, rl + 1 (in the tile)
+    const int nl = (warp & 1) * 16 + (lane & 7) * 2;   // and neurons nl, nl + 1
+    const double* wp = wt + n0 + nl;                   // + i * kH2: input i's weights of the two neurons
+    double2 wc[kH2W], wn[kH2W];
+#pragma unroll
+    for (int k = 0; k < kH2W; ++k) wc[k] = __ldg(reinterpret_cast<const double2*>(wp + (int64_t)k * kH2));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(bias + n0 + nl));
+    pdl_wait();
+    pdl_trigger();
+    for (int e = t; e < kH2R * kH1 / 2; e += kH2T) {
+        const int r = (2 * e) / kH1, c = (2 * e) % kH1;
+        if (r0 + r < n) cp_async16(xs + r * kH2XS + c, x + (int64_t)(r0 + r) * kH1 + c);
+        else *reinterpret_cast<double2*>(xs + r * kH2XS + c) = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    double a00 = b.x, a01 = b.y, a10 = b.x, a11 = b.y;  // [row][neuron]
+    const double* x0 = xs + rl * kH2XS;
+    const double* x1 = x0 + kH2XS;
+#pragma unroll 1
+    for (int i0 = 0; i0 < kH1; i0 += kH2W) {
+        if (i0 + kH2W < kH1) {
+#pragma unroll
+            for (int k = 0; k < kH2W; ++k)
+                wn[k] = __ldg(reinterpret_cast<const double2*>(wp + (int64_t)(i0 + kH2W + k) * kH2));
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < kH2W; k0 += 2) {
+            // products of 2 inputs first (independent), then the in-order adds,
+            // the four chains interleaved
+            const double2 xa = *reinterpret_cast<const double2*>(x0 + i0 + k0);
+            const double2 xb = *reinterpret_cast<const double2*>(x1 + i0 + k0);
+            const double2 wa = wc[k0], wb = wc[k0 + 1];
+            const double p00 = __dmul_rn(xa.x, wa.x), p01 = __dmul_rn(xa.x, wa.y);
+            const double p02 = __dmul_rn(xb.x, wa.x), p03 = __dmul_rn(xb.x, wa.y);
+            const double p10 = __dmul_rn(xa.y, wb.x), p11 = __dmul_rn(xa.y, wb.y);
+            const double p12 = __dmul_rn(xb.y, wb.x), p13 = __dmul_rn(xb.y, wb.y);
+            a00 = __dadd_rn(a00, p00);
+            a01 = __dadd_rn(a01, p01);
+            a10 = __dadd_rn(a10, p02);
+            a11 = __dadd_rn(a11, p03);
+            a00 = __dadd_rn(a00, p10);
+            a01 = __dadd_rn(a01, p11);
+            a10 = __dadd_rn(a10, p12);
+            a11 = __dadd_rn(a11, p13);
+        }
+#pragma unroll
+        for (int k = 0; k < kH2W; ++k) wc[k] = wn[k];
+    }
+    const int ra = r0 + rl;
+    if (ra < n)
+        *reinterpret_cast<double2*>(y + (int64_t)ra * kH2 + n0 + nl) =
+            make_double2(a00 > 0.0 ? a00 : 0.0, a01 > 0.0 ? a01 : 0.0);  // ReLU
+    if (ra + 1 < n)
+        *reinterpret_cast<double2*>(y + (int64_t)(ra + 1) * kH2 + n0 + nl) =
+            make_double2(a10 > 0.0 ? a10 : 0.0, a11 > 0.0 ? a11 : 0.0);
+}
+
 // Output layer (384 -> 3, no activation) and the head properties
-// (predictor.cpp:161-185, pipeline.cpp:288): kOR rows per CTA staged in
-// shared memory, one thread per (row, output) chain.
-constexpr int kOR = 16;
-__global__ void __launch_bounds__(64) k_mlp_out(int n, const double* __restrict__ a2,
+// (predictor.cpp:161-185, pipeline.cpp:288): its chains are 384 dependent adds
+// long, so the kernel is latency-bound -- kOR = 4 rows per CTA (128 CTAs for
+// 512 heads), the rows and w3 staged by cp.async (both from L2), one lane per
+// (row, output) chain.
+constexpr int kOR = 4;
+__global__ void __launch_bounds__(32) k_mlp_out(int n, const double* __restrict__ a2,
                                                 const double* __restrict__ w3t,
                                                 const double* __restrict__ b3,
                                                 double* __restrict__ bgt0, double* __restrict__ kslope,
@@ -286,11 +364,13 @@ __global__ void __launch_bounds__(64) k_mlp_out(int n, const double* __restrict_
     extern __shared__ __align__(16) double osm[];
     double* ws = osm;              // [384][3]
     double* as = osm + kH2 * 3;    // [kOR][384]
-    for (int i = threadIdx.x; i < kH2 * 3; i += blockDim.x) ws[i] = w3t[i];
+    const int t = threadIdx.x;
+    for (int e = t; e < kH2 * 3 / 2; e += 32) cp_async16(ws + 2 * e, w3t + 2 * e);
+    cp_async_commit();
     pdl_wait();
     pdl_trigger();
     const int r0 = blockIdx.x * kOR;
-    for (int e = threadIdx.x; e < kOR * kH2 / 2; e += blockDim.x) {  // asynchronous row copies
+    for (int e = t; e < kOR * kH2 / 2; e += 32) {  // asynchronous row copies
         const int r = r0 + (2 * e) / kH2;
         if (r < n) cp_async16(as + 2 * e, a2 + (int64_t)r0 * kH2 + 2 * e);
         else reinterpret_cast<double2*>(as)[e] = make_double2(0.0, 0.0);
@@ -298,7 +378,7 @@ __global__ void __launch_bounds__(64) k_mlp_out(int n, const double* __restrict_
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    const int lr = threadIdx.x / 3, o = threadIdx.x % 3, r = r0 + lr;
+    const int lr = t / 3, o = t % 3, r = r0 + lr;
     if (lr >= kOR || r >= n) return;
     const double* a = as + lr * kH2;
     double z = b3[o];
@@ -348,6 +428,20 @@ void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, 
 
 size_t predict_scratch_bytes(int n) { return (size_t)std::max(n, 1) * (kH1 + kH2) * sizeof(double); }
 
+void launch_predict_tail(int n, const double* a1, const double* w2t, const double* b2, const double* w3t,
+                         const double* b3, double* bgt0, double* kslope, int32_t* streaming, double* z,
+                         double* a2, cudaStream_t s) {
+    if (n <= 0) return;
+    const size_t s2 = (size_t)kH2R * kH2XS * sizeof(double);
+    FX_CUDA(cudaFuncSetAttribute(k_mlp_h2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    launch_pdl(k_mlp_h2, dim3((unsigned)((n + kH2R - 1) / kH2R), kH2 / kH2N), kH2T, s2, s, n, a1, w2t, b2, a2);
+    const size_t osmem = (size_t)(kH2 * 3 + kOR * kH2) * sizeof(double);
+    FX_CUDA(cudaFuncSetAttribute(k_mlp_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem));
+    launch_pdl(k_mlp_out, (unsigned)((n + kOR - 1) / kOR), 32, osmem, s, n, (const double*)a2, w3t, b3, bgt0,
+               kslope, streaming, z);
+    FX_CUDA(cudaGetLastError());
+}
+
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
                     const double* b2, const double* w3t, const double* b3, const double* mu,
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
@@ -357,17 +451,9 @@ void launch_predict(int n, const double* w1t, const double* b1, const double* w2
     double* a2 = a1 + (size_t)n * kH1;
     const unsigned rt = (unsigned)((n + kMR - 1) / kMR);
     const size_t s1 = (size_t)(2 * kKC * kMN + kMR * kF) * sizeof(double);
-    const size_t s2 = (size_t)(2 * kKC * kMN + kMR * kH1) * sizeof(double);
     FX_CUDA(cudaFuncSetAttribute(k_mlp_layer<kF, kH1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
-    FX_CUDA(cudaFuncSetAttribute(k_mlp_layer<kH1, kH2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
     launch_pdl(k_mlp_layer<kF, kH1, true>, dim3(rt, kH1 / kMN), kMT, s1, s, n, feats, w1t, b1, mu, sigma, a1);
-    launch_pdl(k_mlp_layer<kH1, kH2, false>, dim3(rt, kH2 / kMN), kMT, s2, s, n, (const double*)a1, w2t, b2,
-               (const double*)nullptr, (const double*)nullptr, a2);
-    const size_t osmem = (size_t)(kH2 * 3 + kOR * kH2) * sizeof(double);
-    FX_CUDA(cudaFuncSetAttribute(k_mlp_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem));
-    launch_pdl(k_mlp_out, (unsigned)((n + kOR - 1) / kOR), 64, osmem, s, n, (const double*)a2, w3t, b3, bgt0,
-               kslope, streaming, z);
-    FX_CUDA(cudaGetLastError());
+    launch_predict_tail(n, a1, w2t, b2, w3t, b3, bgt0, kslope, streaming, z, a2, s);
 }
 
 }  // namespace fx

@@ -691,10 +691,13 @@ class SparseDecoder:
         return f
 
     def predict_props(self, q: torch.Tensor, rec: torch.Tensor, model: "Predictor",
-                      features: torch.Tensor = None, z: torch.Tensor = None):
-        """decode_features -> normalize -> predict for every head in one launch
+                      features: torch.Tensor = None, z: torch.Tensor = None, append=None):
+        """decode_features -> normalize -> predict for every head
         (features.cpp:162-233, predictor.cpp:161-185, pipeline.cpp:277-290) ->
-        (bgt0, kslope, streaming) device tensors [B][H], the props of step()."""
+        (bgt0, kslope, streaming) device tensors [B][H], the props of step().
+        append=(k_new, v_new) [B][Hkv][D]: the previous token is appended first
+        (append_new, pipeline.cpp:406-412) and seen by the features; the step
+        that follows then takes no append."""
         lay = self.lay
         dev = self.eng.device
         shape = (lay.batch, self.heads)
@@ -704,9 +707,17 @@ class SparseDecoder:
                         torch.empty(shape, dtype=torch.int32, device=dev))
         b0, ks, st = self._pp
         qd = q.to(dev, torch.float32).contiguous()
+        ak = av = None
+        if append is not None:
+            if self.lay.l_sink + self.lay.l_cpu + self.lay.l_local + self.l_new + 1 > self.lay.l_cap:
+                raise ValueError("bad-shape: decoded rows exceed l_cap")
+            ak = append[0].to(dev, torch.float32).contiguous()
+            av = append[1].to(dev, torch.float32).contiguous()
         check(LIB.fx_predict_props(self.eng.ctx, C.byref(lay), _ptr(self.k), _ptr(self.v), self.l_new,
-                                   _ptr(qd), _ptr(rec), model.h, _ptr(features), _ptr(z), _ptr(b0),
-                                   _ptr(ks), _ptr(st)))
+                                   _ptr(ak), _ptr(av), _ptr(qd), _ptr(rec), model.h, _ptr(features),
+                                   _ptr(z), _ptr(b0), _ptr(ks), _ptr(st)))
+        if append is not None:
+            self.l_new += 1
         return b0, ks, st
 
     def selected_blocks(self, b: int, h: int) -> np.ndarray:

@@ -1,5 +1,7 @@
-"""Phase times of the clustered decode-features kernel (k_feat_fused) at C2,
-and the fx_predict_props total (features + the tiled predictor layers)."""
+"""Phase times (%globaltimer) of the decode-feature kernels at C2 (16 x 8
+groups, 128K, bf16): k_feat_part per CTA (start, item ends, end) and
+k_feat_final per CTA (start, before / after the grid-dependency wait, heads
+merged, cluster exchange done, layer 1 done), one fx_predict_props call."""
 import os, sys, time, ctypes as C, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 os.environ["FLUXATTN_B200_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfluxattn_b200.so")
@@ -8,7 +10,7 @@ from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder, Predictor
 eng = Engine(0); dev = eng.device
 B, HKV, G, D = 16, 8, 4, 128
 ctx = 131072; l_cpu = ctx - 320
-dec = SparseDecoder(eng, B, HKV, G, D, 64, l_cpu, 256, max_new=300, dtype="bf16")
+dec = SparseDecoder(eng, B, HKV, G, D, 64, l_cpu, 256, max_new=640, dtype="bf16")
 dec.k.normal_(); dec.v.normal_(); dec.build_metadata()
 q = torch.randn((B, 32, D), device=dev)
 rs = np.random.default_rng(5)
@@ -19,31 +21,33 @@ params = {"w1": rs.standard_normal((256, 41)) * (2.0 / 41) ** 0.5, "b1": np.zero
 pred = Predictor(eng, params)
 rec = dec.prefill_stats(q, tau=0.10, layer=0)
 dec.l_new = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 t = time.time()
-while time.time() - t < 2.0:
+while time.time() - t < 1.0:
     for i in range(50):
         dec.predict_props(q, rec, pred)
     torch.cuda.synchronize()
-e0.record()
-for i in range(100):
-    dec.predict_props(q, rec, pred)
-e1.record(); torch.cuda.synchronize()
-print("predict_props us %.2f (l_new %d)" % (e0.elapsed_time(e1) / 100 * 1e3, dec.l_new))
-tr = np.zeros(16 * 1024, np.int64)
 N.LIB.fx_debug_fp_trace.argtypes = [C.c_void_p, C.c_int]
-N.LIB.fx_debug_fp_trace(tr.ctypes.data, 16 * 128)
-t = tr[:16 * 128].reshape(128, 16)
-t0 = t[:, 0].min()
-names = ["start", "q staged", "sink", "local", "new", "features", "feats out", "L0 begin", "L0 data", "L0 scores", "L0 weights", "L0 o"]
-N.LIB.fx_ctx_set_timing(eng.ctx, 1)
-for i in range(20):
+for rep in range(3):
+    torch.cuda.synchronize()
     dec.predict_props(q, rec, pred)
-N.LIB.fx_ctx_set_timing(eng.ctx, 0)
-for i, nm in enumerate(names):
-    x = (t[:, i] - t0) / 1e3
-    print("%-12s min %7.2f median %7.2f max %7.2f" % (nm, x.min(), np.median(x), x.max()))
-
-cyc = (t[:, 15] - t[:, 14]).astype(np.float64)
-ns = (t[:, 6] - t[:, 0]).astype(np.float64)
-print("effective SM clock over the kernel: median %.0f MHz" % np.median(cyc / ns * 1e3))
+    torch.cuda.synchronize()
+    tr = np.zeros(16 * 2048, np.int64)
+    N.LIB.fx_debug_fp_trace(tr.ctypes.data, 16 * 2048)
+    t = tr.reshape(2048, 16)
+    part = t[:296]
+    part = part[part[:, 0] > 0]
+    fin = t[1024:1024 + 128]
+    t0 = part[:, 0].min()
+    us = lambda x: (x - t0) / 1e3
+    print("rep", rep, "l_new", dec.l_new)
+    print("  part: start min %.2f max %.2f | item0 end med %.2f | end med %.2f max %.2f" % (
+        us(part[:, 0].min()), us(part[:, 0].max()), np.median(us(part[:, 2])), np.median(us(part[:, 1])), us(part[:, 1].max())))
+    for i, nm in [(12, "it1 top"), (13, "it1 data"), (9, "it1 scores"), (10, "it1 exp"), (11, "it1 PV"), (3, "it1 end")]:
+        x = us(part[:, i])
+        print("  part %-9s min %7.2f med %7.2f max %7.2f" % (nm, x.min(), np.median(x), x.max()))
+    for i, nm in [(0, "start"), (1, "pre-wait"), (2, "post-wait"), (6, "m/z in"), (7, "weights"), (8, "outputs"), (9, "norms"), (3, "heads"), (4, "cluster"), (5, "layer1")]:
+        x = us(fin[:, i])
+        print("  final %-9s min %7.2f med %7.2f max %7.2f" % (nm, x.min(), np.median(x), x.max()))
+    cyc = (fin[:, 15] - fin[:, 14]).astype(np.float64)
+    ns = (fin[:, 5] - fin[:, 0]).astype(np.float64)
+    print("  effective SM clock over k_feat_final: median %.0f MHz" % np.median(cyc / ns * 1e3))

@@ -15,12 +15,12 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _setup(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, seed):
+def _setup(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, seed, max_new=8):
     from paper_2605_07719_b200.fluxattn import SparseDecoder
     rng = np.random.default_rng(seed)
-    dec = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new=8, dtype="bf16")
+    dec = SparseDecoder(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, max_new=max_new, dtype="bf16")
     host = {}
-    L = l_sink + l_cpu + l_local + 8
+    L = l_sink + l_cpu + l_local + max_new
     for b in range(B):
         for g in range(Hkv):
             k = rng.standard_normal((L, D)).astype(np.float32)
@@ -30,7 +30,7 @@ def _setup(engine, B, Hkv, G, D, l_sink, l_cpu, l_local, seed):
             k = torch.as_tensor(k).bfloat16().float().numpy()
             v = torch.as_tensor(v).bfloat16().float().numpy()
             host[(b, g)] = (k, v)
-            dec.load_group(b, g, k[:L - 8], v[:L - 8])
+            dec.load_group(b, g, k[:L - max_new], v[:L - max_new])
     dec.build_metadata()
     anchors = rng.standard_normal((B, Hkv * G, D)).astype(np.float32)
     anchors = torch.as_tensor(anchors * 1.3).bfloat16().float().numpy()
@@ -67,8 +67,9 @@ def _close(a, b, rtol=1e-9, atol=1e-12):
     return np.all(np.abs(a - b) <= atol + rtol * np.abs(b))
 
 
-def test_prefill_stats_and_decode_features(engine, coracle):
-    B, Hkv, G, D = 2, 2, 4, 128
+@pytest.mark.parametrize("G", [4, 3])  # G = 3: the general-shape decode-feature kernels
+def test_prefill_stats_and_decode_features(engine, coracle, G):
+    B, Hkv, D = 2, 2, 128
     dec, host, anchors, rng = _setup(engine, B, Hkv, G, D, 64, 3000, 256, seed=4)
     rec = dec.prefill_stats(torch.as_tensor(anchors), tau=0.1, layer=3).cpu().numpy()
     want = _oracle_records(coracle, dec, host, anchors, 0.1, 3)
@@ -127,24 +128,33 @@ def test_predictor_driven_plan(engine, coracle):
     pred.close()
 
 
-@pytest.mark.parametrize("Hkv,G,D,n_new", [(2, 4, 128, 3), (4, 7, 128, 0), (1, 4, 64, 5), (8, 4, 128, 1),
-                                           (3, 2, 64, 5)])
-def test_fused_predict_props(engine, coracle, Hkv, G, D, n_new):
-    """fx_predict_props (decode features + normalize + MLP in one clustered
-    launch; Hkv = 3 takes the two-launch fallback): features within 1e-9 of the
-    oracle (cross-head max through DSMEM included), logits bit-identical to the
-    predictor on those features, and the props equal to the two-launch path's."""
+@pytest.mark.parametrize("Hkv,G,D,n_new,via_append", [
+    (2, 4, 128, 3, False), (4, 7, 128, 0, False), (1, 4, 64, 5, False), (8, 4, 128, 1, False),
+    (3, 2, 64, 5, False), (2, 4, 128, 66, True), (2, 8, 128, 1, True), (2, 4, 64, 64, True)])
+def test_fused_predict_props(engine, coracle, Hkv, G, D, n_new, via_append):
+    """fx_predict_props (decode features as 64-row chunk partials + a clustered
+    merge, normalize, MLP): features within 1e-9 of the oracle (cross-head max
+    through DSMEM included), logits bit-identical to the predictor on those
+    features, and the props equal to the fx_decode_features path's.
+    via_append: the last decoded row is appended by fx_predict_props itself
+    (written to the cache by the CTA that holds its chunk, and seen by the
+    features), checked in the cache afterwards."""
     from paper_2605_07719_b200.fluxattn import Predictor
     B = 2
-    dec, host, anchors, rng = _setup(engine, B, Hkv, G, D, 64, 2500, 256, seed=30 + G)
+    dec, host, anchors, rng = _setup(engine, B, Hkv, G, D, 64, 2500, 256, seed=30 + G, max_new=max(8, n_new))
     rec = dec.prefill_stats(torch.as_tensor(anchors), tau=0.1, layer=1)
     lay = dec.lay
-    for i in range(n_new):
-        kn = torch.stack([torch.as_tensor(host[(b, g)][0][lay.l_sink + lay.l_cpu + lay.l_local + i])
+    base = lay.l_sink + lay.l_cpu + lay.l_local
+
+    def new_row(i):
+        kn = torch.stack([torch.as_tensor(host[(b, g)][0][base + i])
                           for b in range(B) for g in range(Hkv)]).reshape(B, Hkv, D).cuda()
-        vn = torch.stack([torch.as_tensor(host[(b, g)][1][lay.l_sink + lay.l_cpu + lay.l_local + i])
+        vn = torch.stack([torch.as_tensor(host[(b, g)][1][base + i])
                           for b in range(B) for g in range(Hkv)]).reshape(B, Hkv, D).cuda()
-        dec.append(kn, vn)
+        return kn, vn
+
+    for i in range(n_new - (1 if via_append else 0)):
+        dec.append(*new_row(i))
     params = coracle.make_model(5)
     params["mu"] = np.zeros(41)
     params["sigma"] = np.ones(41) * 50.0
@@ -153,8 +163,16 @@ def test_fused_predict_props(engine, coracle, Hkv, G, D, n_new):
     q = torch.as_tensor(rng.standard_normal((B, Hkv * G, D)).astype(np.float32)).bfloat16().float().cuda()
     feats = torch.empty((B, Hkv * G, 41), dtype=torch.float64, device="cuda")
     z = torch.empty((B, Hkv * G, 3), dtype=torch.float64, device="cuda")
-    b0, ks, st = dec.predict_props(q, rec, pred, features=feats, z=z)
+    b0, ks, st = dec.predict_props(q, rec, pred, features=feats, z=z,
+                                   append=new_row(n_new - 1) if via_append else None)
     torch.cuda.synchronize()
+    assert dec.l_new == n_new
+    if via_append:
+        for b in range(B):
+            for g in range(Hkv):
+                row = base + n_new - 1
+                assert np.array_equal(dec.k[b, g, row].float().cpu().numpy(), host[(b, g)][0][row])
+                assert np.array_equal(dec.v[b, g, row].float().cpu().numpy(), host[(b, g)][1][row])
     f = feats.cpu().numpy()
     recn = rec.cpu().numpy()
     seg = (lay.l_sink, lay.l_cpu, lay.l_local, n_new)

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_errors_without_gpu():
     from paper_2605_07719_b200 import _native
-    assert _native.LIB.fx_abi_version() == _native.ABI_VERSION == 4
+    assert _native.LIB.fx_abi_version() == _native.ABI_VERSION == 5
     assert _native.LIB.fx_block_count(33, 16) == 3
     assert _native.LIB.fx_block_count(10, 0) == 0
 
