@@ -661,7 +661,8 @@ def run_c5(a):
         peak, peak_kind = peaks()
         achieved = attend_b / a.steps / (kt["attend"] * 1e-3) / 1e9
         tr = ncu_traffic("k_attend", "c5")
-        result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3+K4)", "achieved": achieved,
+        result["roofline"] = {"bound": "hbm", "kernel": "k_attend_tma (K3 with its per-unit epilogue; "
+                              "the unit-partial merge kernel is kernels_ms.merge)", "achieved": achieved,
                               "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                               "peak_kind": peak_kind, "traffic": (tr or {}).get("dram_bytes_per_launch"),
                               "traffic_source": (tr or {}).get("source"),
@@ -921,7 +922,8 @@ def run_ours(a):
         achieved = attend_b / a.steps / (attend_ms * 1e-3) / 1e9
         tag = a.workload if a.plan == WORKLOADS[a.workload]["plan"] else f"{a.workload}_{a.plan}"
         tr = ncu_traffic("k_attend", tag)
-        kname = "k_attend_tma (K3+K4)" if a.kv_dtype == "bf16" else "k_attend_generic (K3+K4, f32)"
+        kname = ("k_attend_tma (K3 with its per-unit epilogue; the unit-partial merge kernel is "
+                 "kernels_ms.merge)") if a.kv_dtype == "bf16" else "k_attend_generic (K3+K4, f32)"
         result["roofline"] = {"bound": "hbm", "kernel": kname,
                               "achieved": achieved, "peak": peak, "unit": "GB/s",
                               "frac": achieved / peak, "peak_kind": peak_kind,

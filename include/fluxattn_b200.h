@@ -144,10 +144,11 @@ FX_API uint64_t fx_ctx_launches(fx_ctx* ctx);
 #define FX_KERNEL_SCORE 1    /* K2a approximate scores   */
 #define FX_KERNEL_SELECT 2   /* K2b exact top-k select   */
 #define FX_KERNEL_WORKLIST 3 /* union -> boxes           */
-#define FX_KERNEL_ATTEND 4   /* K3+K4 attention + merge  */
+#define FX_KERNEL_ATTEND 4   /* K3+K4 attention          */
 #define FX_KERNEL_METADATA 5 /* K1 metadata levels       */
 #define FX_KERNEL_APPEND 6   /* decode-row append        */
-#define FX_KERNEL_COUNT 7
+#define FX_KERNEL_MERGE 7    /* unit-partial merge (TMA) */
+#define FX_KERNEL_COUNT 8
 FX_API int fx_ctx_set_timing(fx_ctx* ctx, int enable);
 /* Accumulated milliseconds and launch count of one kernel id (synchronizes). */
 FX_API int fx_ctx_kernel_time(fx_ctx* ctx, int32_t kernel, double* total_ms, int64_t* launches);

@@ -20,7 +20,7 @@ FX_PLAN_FIXED = 1
 FX_PLAN_FULL = 2
 FX_PLAN_GIVEN = 3
 ABI_VERSION = 5
-KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append")
+KERNELS = ("plan", "score", "select", "worklist", "attend", "metadata", "append", "merge")
 
 _p = C.c_void_p
 _i32 = C.c_int32

@@ -1175,8 +1175,6 @@ void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
     FX_CUDA(cudaFuncSetAttribute(k_attend_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(k_attend_tma<D>, grid, kQThreads, smem, s, maps, v);
     FX_CUDA(cudaGetLastError());
-    launch_pdl(k_merge_units, v.n_bg, kMergeThreads, 0, s, v.Hkv, v.G, D, a.bg_count,
-               (const int32_t*)a.uq.ubase, (const float*)a.part_o, (const float*)a.part_lse, a.o, a.lse);
 }
 
 }  // namespace
@@ -1240,7 +1238,7 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
     if (allow_tma && attend_uses_tma(a.L, a.idx != nullptr)) {
         if (a.L.head_dim == 128) launch_tma<128>(a, grid, s);
         else launch_tma<64>(a, grid, s);
-        n = 2;  // + the unit merge
+        n = 1;  // launch_unit_merge follows
     } else {
         const View v = make_view(a);
         const int D = a.L.head_dim, G = a.L.group_size;
@@ -1256,6 +1254,16 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
     }
     FX_CUDA(cudaGetLastError());
     return n;
+}
+
+int launch_unit_merge(const AttendArgs& a, bool allow_tma, cudaStream_t s) {
+    if (!allow_tma || !attend_uses_tma(a.L, a.idx != nullptr)) return 0;
+    const int n_bg = a.L.batch * a.L.kv_heads;
+    launch_pdl(k_merge_units, n_bg, kMergeThreads, 0, s, a.L.kv_heads, a.L.group_size, a.L.head_dim,
+               (const int32_t*)a.bg_count, (const int32_t*)a.uq.ubase, (const float*)a.part_o,
+               (const float*)a.part_lse, a.o, a.lse);
+    FX_CUDA(cudaGetLastError());
+    return 1;
 }
 
 void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_count,

@@ -802,6 +802,10 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
             Timed tm(ctx, FX_KERNEL_ATTEND);
             n += fx::launch_attend(aa, grid, true, st);
         }
+        {
+            Timed tm(ctx, FX_KERNEL_MERGE);
+            n += fx::launch_unit_merge(aa, true, st);
+        }
         ctx->launches += n;
     });
 }

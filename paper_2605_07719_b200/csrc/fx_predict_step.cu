@@ -174,7 +174,8 @@ struct FeatAppend {
 template <typename T, int D>
 constexpr size_t part_stage_bytes() { return (size_t)2 * kCR * D * sizeof(T); }
 constexpr int kPartStages = 2;
-constexpr int kPartCtasPerSm = 2;
+constexpr int kPartCtasPerSm = 3;
+constexpr int kPT2 = 128, kPW2 = kPT2 / 32;  // threads / warps of k_feat_part
 
 // Chunk partials: a persistent grid, each CTA walking a contiguous range of
 // (b, g, chunk) items (mostly one group, so the q slice is reloaded only at a
@@ -185,15 +186,15 @@ constexpr int kPartCtasPerSm = 2;
 // dim pair x row slab)
 // -> one partial (m, z, sum e v) per (item, head).
 template <typename T, int G, int D>
-__global__ void __launch_bounds__(kPT, kPartCtasPerSm) k_feat_part(fx_layout L, void* kp, void* vp, int64_t l_new,
+__global__ void __launch_bounds__(kPT2, kPartCtasPerSm) k_feat_part(fx_layout L, void* kp, void* vp, int64_t l_new,
                                                                    const float* __restrict__ q, FeatAppend ap,
                                                                    double* __restrict__ part, int items) {
     extern __shared__ __align__(128) unsigned char fsm[];
     constexpr size_t STG = part_stage_bytes<T, D>();
-    constexpr int NP = D / 2, NS = kPT / NP;  // dim pairs, row slabs of the P.V pass
+    constexpr int NP = D / 2, NS = kPT2 / NP;  // dim pairs, row slabs of the P.V pass
     __shared__ double sc[kCR][G];
     __shared__ double red[NS][G][D];
-    __shared__ double s_wm[kPW][G], s_wz[kPW][G];  // per warp and head: score max, sum of weights
+    __shared__ double s_wm[kPW2][G], s_wz[kPW2][G];  // per warp and head: score max, sum of weights
     __shared__ __align__(8) uint64_t full[kPartStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const FeatChunks fc = feat_chunks(L, l_new);
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kPT, kPartCtasPerSm) k_feat_part(fx_layout L, 
             const int rr = (int)(ap.row - r0);
             T* K = static_cast<T*>(kp) + bg * L.l_cap * D;
             T* V = static_cast<T*>(vp) + bg * L.l_cap * D;
-            for (int d = tid; d < D; d += kPT) {
+            for (int d = tid; d < D; d += kPT2) {
                 const float a = ap.kn[bg * D + d], b = ap.vn[bg * D + d];
                 T ka, va;
                 if constexpr (sizeof(T) == 2) {
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kPT, kPartCtasPerSm) k_feat_part(fx_layout L, 
         // running maximum per head on the lanes that hold the sums
         const bool writer = sl % LPH == 0 && sl / LPH < G;
         double mloc = -INFINITY;
-        for (int rb = warp * RPI; rb < nr; rb += kPW * RPI) {
+        for (int rb = warp * RPI; rb < nr; rb += kPW2 * RPI) {
             const int r = rb + sub;
             const bool live = r < nr;
             double kv[DPL];
@@ -311,11 +312,11 @@ __global__ void __launch_bounds__(kPT, kPartCtasPerSm) k_feat_part(fx_layout L, 
             double zh[G];
 #pragma unroll
             for (int h = 0; h < G; ++h) zh[h] = 0.0;
-            for (int i = tid; i < nr * G; i += kPT) {
+            for (int i = tid; i < nr * G; i += kPT2) {
                 const int r = i / G, h = i - r * G;
                 double M = s_wm[0][h];
 #pragma unroll
-                for (int w = 1; w < kPW; ++w) M = fmax(M, s_wm[w][h]);
+                for (int w = 1; w < kPW2; ++w) M = fmax(M, s_wm[w][h]);
                 const double e = exp(sc[r][h] - M) * kUp;
                 sc[r][h] = e;
 #pragma unroll
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(kPT, kPartCtasPerSm) k_feat_part(fx_layout L, 
         __syncthreads();  // the stage is consumed: refill it with the item two ahead
         if (it == 1) FP_MARK(blockIdx.x, 11);
         if (tid == 0 && item + kPartStages < i1) issue(item + kPartStages, st);
-        for (int i = tid; i < G * D; i += kPT) {
+        for (int i = tid; i < G * D; i += kPT2) {
             const int h = i / D, d = i % D;
             double s2 = 0.0;
 #pragma unroll
@@ -365,9 +366,9 @@ __global__ void __launch_bounds__(kPT, kPartCtasPerSm) k_feat_part(fx_layout L, 
         if (tid < G) {  // the chunk max and sum of weights (the 2^896 taken back exactly)
             double M = s_wm[0][tid], z = 0.0;
 #pragma unroll
-            for (int w = 1; w < kPW; ++w) M = fmax(M, s_wm[w][tid]);
+            for (int w = 1; w < kPW2; ++w) M = fmax(M, s_wm[w][tid]);
 #pragma unroll
-            for (int w = 0; w < kPW; ++w) z += s_wz[w][tid];
+            for (int w = 0; w < kPW2; ++w) z += s_wz[w][tid];
             out[tid * part_stride<D>()] = M;
             out[tid * part_stride<D>() + 1] = z * 0x1p-896;
         }
@@ -696,7 +697,7 @@ void launch_ff(const fx_layout& L, void* k, void* v, int64_t l_new, const float*
         FX_CUDA(cudaFuncSetAttribute(k_feat_part<T, G, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int items = fc.total() * n_bg;
         const int grid = std::min(items, num_sms * kPartCtasPerSm);
-        launch_pdl(k_feat_part<T, G, D>, dim3((unsigned)grid), kPT, smem, s, L, k, v, l_new, q, ap, part, items);
+        launch_pdl(k_feat_part<T, G, D>, dim3((unsigned)grid), kPT2, smem, s, L, k, v, l_new, q, ap, part, items);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)L.kv_heads, (unsigned)L.batch);
