@@ -113,13 +113,12 @@ __device__ __forceinline__ int find_bg(const int32_t* start, int n_bg, int64_t x
     return lo;
 }
 
-// Final LSE merge of the partials of one (b, g) (attention.cpp:89-104 applied
-// across the CTAs that covered it).  Natural-log LSEs; -inf = empty partial.
+// Whether CTA c of the generic kernel's static split has any box (with fewer
+// boxes than CTAs some ranges are empty and leave no partial).
 __device__ __forceinline__ bool cta_nonempty(int c, int64_t NB, int grid) {
     return NB * c / grid < NB * (c + 1) / grid;
 }
 
-constexpr int kMaxContrib = 160;  // contributor list held in smem (>= TMA grid)
 constexpr int kMaxPrefix = kMaxRunPrefix;  // (b, g) runs whose starts are rebuilt in smem
 
 // Run starts of the global box sequence: exclusive prefix of (box count +
@@ -156,99 +155,6 @@ __device__ const int32_t* run_starts(const View& p, int32_t* s_start, int* wtmp,
     return s_start;
 }
 
-// Shared scratch of the run merge (MG = largest group size).
-template <int MG>
-struct MergeSmem {
-    int nruns;
-    int runs[2];                // this CTA's runs cut by its range ends (first, last)
-    int rs[2], re[2];           // their real box ranges [s, e)
-    int flag[2];
-    int n;
-    int list[kMaxContrib];      // contributing CTAs (their partial slots are c + bg)
-    float w[kMaxContrib * MG];  // per (contributor, head): LSE, then softmax weight
-    float den[MG];
-    float lse[MG];
-};
-
-// Merge the partials of run `bg` (attention.cpp:89-104 applied across the
-// CTAs that covered it) into the final output.  `nt` threads, barrier `bar`.
-template <int MG>
-__device__ void merge_run(const View& p, int bg, int64_t s, int64_t e, int64_t NB, int grid, int t,
-                          int nt, int bar, MergeSmem<MG>* ms) {
-    const int G = p.G, D = p.D;
-    const int cf = cta_of(s, NB, grid), cl = cta_of(e - 1, NB, grid);
-    const int b = bg / p.Hkv, g = bg % p.Hkv;
-    const int64_t head0 = (int64_t)b * p.Hkv * G + (int64_t)g * G;
-    if (t == 0) {
-        int n = 0;
-        for (int c = cf; c <= cl; ++c)
-            if (cta_nonempty(c, NB, grid)) {
-                if (n < kMaxContrib) ms->list[n] = c;
-                ++n;
-            }
-        ms->n = n;
-    }
-    named_bar_sync(bar, nt);
-    const int n = ms->n;
-    if (n <= kMaxContrib) {
-        for (int i = t; i < n * G; i += nt)
-            ms->w[i] = __ldcg(p.part_lse + (int64_t)(ms->list[i / G] + bg) * G + i % G);
-        named_bar_sync(bar, nt);
-        for (int h = t; h < G; h += nt) {
-            float M = -INFINITY;
-            for (int i = 0; i < n; ++i) M = fmaxf(M, ms->w[i * G + h]);
-            float den = 0.f;
-            for (int i = 0; i < n; ++i) {
-                const float li = ms->w[i * G + h];
-                const float wi = (M == -INFINITY || li == -INFINITY) ? 0.f : __expf(li - M);
-                ms->w[i * G + h] = wi;
-                den += wi;
-            }
-            ms->den[h] = den;
-            ms->lse[h] = den > 0.f ? M + __logf(den) : -INFINITY;
-        }
-        named_bar_sync(bar, nt);
-        for (int i = t; i < G * D; i += nt) {
-            const int h = i / D, d = i % D;
-            float num = 0.f;
-            // eight contributors' partials in flight per round (L2 round trips overlap)
-            for (int j0 = 0; j0 < n; j0 += 8) {
-                float pv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    pv[u] = j0 + u < n ? __ldcg(p.part_o + ((int64_t)(ms->list[j0 + u] + bg) * G + h) * D + d) : 0.f;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const float wj = j0 + u < n ? ms->w[(j0 + u) * G + h] : 0.f;
-                    if (wj != 0.f) num += wj * pv[u];
-                }
-            }
-            const float den = ms->den[h];
-            p.o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
-            if (d == 0 && p.lse) p.lse[head0 + h] = ms->lse[h];
-        }
-    } else {  // very long run (generic path only): weights recomputed per element
-        for (int i = t; i < G * D; i += nt) {
-            const int h = i / D, d = i % D;
-            float M = -INFINITY;
-            for (int c = cf; c <= cl; ++c)
-                if (cta_nonempty(c, NB, grid)) M = fmaxf(M, __ldcg(p.part_lse + (int64_t)(c + bg) * G + h));
-            float num = 0.f, den = 0.f;
-            for (int c = cf; c <= cl && M != -INFINITY; ++c) {
-                if (!cta_nonempty(c, NB, grid)) continue;
-                const float li = __ldcg(p.part_lse + (int64_t)(c + bg) * G + h);
-                if (li == -INFINITY) continue;
-                const float wi = __expf(li - M);
-                num += wi * __ldcg(p.part_o + ((int64_t)(c + bg) * G + h) * D + d);
-                den += wi;
-            }
-            p.o[(head0 + h) * D + d] = den > 0.f ? num / den : 0.f;
-            if (d == 0 && p.lse) p.lse[head0 + h] = den > 0.f ? M + __logf(den) : -INFINITY;
-        }
-    }
-    named_bar_sync(bar, nt);
-}
-
 // Runs with no real boxes (a context-parallel shard whose group selected
 // nothing there and holds no default rows; a streaming group without defaults)
 // reach no tile.  Their output is the merge identity -- o = 0, lse = -inf
@@ -266,34 +172,6 @@ __device__ void write_empty_runs(const View& p, const int32_t* starts, int64_t r
     }
 }
 
-// End of a CTA's range.  Runs wholly inside the CTA were written final at
-// their flush; only the (at most two) runs cut by the range ends left
-// partials.  Count this CTA in for each; the last contributor merges.  Done
-// once, after the CTA's streaming: a global fence or atomic issued while the
-// SM saturates HBM with its own TMA reads waits microseconds behind that
-// traffic, so none is issued mid-stream.  (The generic kernel's static
-// split; the TMA kernel claims units from the queue instead.)
-template <int MG>
-__device__ void finish_cta(const View& p, int64_t NB, int grid, int t, int nt, int bar,
-                           MergeSmem<MG>* ms) {
-    const int nruns = ms->nruns;  // written before the caller's last barrier
-    if (nruns == 0) return;
-    named_bar_sync(bar, nt);  // the partials are written; the release below publishes them
-    if (t < nruns) {  // both counter round trips in flight together
-        const int bg = ms->runs[t];
-        const int cf = cta_of(ms->rs[t], NB, grid), cl = cta_of(ms->re[t] - 1, NB, grid);
-        int n = 0;
-        for (int c = cf; c <= cl; ++c) n += cta_nonempty(c, NB, grid);
-        ms->flag[t] = atomic_add_acq_rel_gpu(p.bg_done + bg, 1) == n - 1;
-    }
-    named_bar_sync(bar, nt);
-    for (int k = 0; k < nruns; ++k) {
-        if (!ms->flag[k]) continue;
-        fence_acq_rel_gpu();
-        const int bg = ms->runs[k];
-        merge_run(p, bg, ms->rs[k], ms->re[k], NB, grid, t, nt, bar, ms);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // TMA + mma.sync kernel, fed by the unit queue
@@ -347,11 +225,12 @@ struct TmaCfg {
 };
 
 // Merge of the unit partials of every multi-unit group (attention.cpp:89-104
-// across the units, in unit order): one CTA per (b, g), launched behind the
-// attention kernel (PDL), every partial's loads in flight at once -- each
-// thread owns one float4 column of a fixed subset of the units, the subsets
-// are combined in a fixed order, so the result is deterministic.
-constexpr int kMergeThreads = 1024;
+// across the units, in unit order): one 128-thread CTA per (b, g, head),
+// launched behind the attention kernel (PDL) -- small CTAs, so every group's
+// heads merge at once even with thousands of groups (C4).  Each thread owns
+// one float4 column of a fixed subset of the units (eight units' loads in
+// flight), the subsets are combined in a fixed order: deterministic.
+constexpr int kMergeThreads = 128;
 __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, int D,
                                                               const int32_t* __restrict__ bg_count,
                                                               const int32_t* __restrict__ ubase,
@@ -360,31 +239,29 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
                                                               float* __restrict__ o, float* __restrict__ lse) {
     pdl_wait();
     pdl_trigger();
-    const int bg = blockIdx.x, t = threadIdx.x;
+    const int bg = blockIdx.x, h = blockIdx.y, t = threadIdx.x;
     const int total = __ldg(bg_count + bg);
     const int nun = total > 0 ? (total + kUnitBoxes - 1) / kUnitBoxes : 1;
     if (nun <= 1) return;  // written final by the attention kernel
     const int base = __ldg(ubase + bg);
-    const int VP = G * D / 4;               // float4 columns per partial
-    const int S = kMergeThreads / VP;       // unit subsets (>= 1: G * D <= 4096)
-    __shared__ float s_m[8];
+    const int VP = D / 4;                   // float4 columns of the head
+    const int S = kMergeThreads / VP;       // unit subsets (D <= 512)
+    __shared__ float s_wm[kMergeThreads / 32];
     __shared__ float4 s_acc[kMergeThreads];
     __shared__ float s_den[kMergeThreads];
-    // per-head max of the unit LSEs
-    if (t < 32 * G) {
-        const int h = t >> 5, ln = t & 31;
-        float m = -INFINITY;
-        for (int i = ln; i < nun; i += 32) m = fmaxf(m, __ldg(part_lse + (int64_t)(base + i) * G + h));
-        m = warp_max(m);
-        if (ln == 0) s_m[h] = m;
-    }
+    // the head's max of the unit LSEs
+    float m = -INFINITY;
+    for (int i = t; i < nun; i += kMergeThreads) m = fmaxf(m, __ldg(part_lse + (int64_t)(base + i) * G + h));
+    m = warp_max(m);
+    if ((t & 31) == 0) s_wm[t >> 5] = m;
     __syncthreads();
+    float M = s_wm[0];
+#pragma unroll
+    for (int w = 1; w < kMergeThreads / 32; ++w) M = fmaxf(M, s_wm[w]);
     const int v = t % VP, sub = t / VP;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float den = 0.f;
     if (sub < S) {
-        const int h = v * 4 / D;
-        const float M = s_m[h];
         constexpr int kIn = 8;
         for (int i0 = sub; i0 < nun; i0 += S * kIn) {
             float4 x[kIn];
@@ -392,8 +269,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
 #pragma unroll
             for (int j = 0; j < kIn; ++j) {
                 const int i = i0 + j * S;
-                const int64_t slot = (int64_t)(base + i) * G;
-                l[j] = i < nun ? __ldg(part_lse + slot + h) : -INFINITY;
+                const int64_t slot = (int64_t)(base + i) * G + h;
+                l[j] = i < nun ? __ldg(part_lse + slot) : -INFINITY;
                 x[j] = i < nun ? __ldg(reinterpret_cast<const float4*>(part_o + slot * D) + v)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
             }
@@ -421,15 +298,11 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
         acc.w += a.w;
         den += s_den[k * VP + v];
     }
-    const int b = bg / Hkv, g = bg % Hkv, h = v * 4 / D;
-    const int64_t head0 = (int64_t)b * Hkv * G + (int64_t)g * G;
+    const int b = bg / Hkv, g = bg % Hkv;
+    const int64_t hd = (int64_t)b * Hkv * G + (int64_t)g * G + h;
     const float inv = den > 0.f ? 1.f / den : 0.f;
-    float* dst = o + head0 * D + v * 4;
-    dst[0] = acc.x * inv;
-    dst[1] = acc.y * inv;
-    dst[2] = acc.z * inv;
-    dst[3] = acc.w * inv;
-    if ((v * 4) % D == 0 && lse) lse[head0 + h] = den > 0.f ? s_m[h] + __logf(den) : -INFINITY;
+    *reinterpret_cast<float4*>(o + hd * D + v * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (v == 0 && lse) lse[hd] = den > 0.f ? M + __logf(den) : -INFINITY;
 }
 
 #ifdef FX_TRACE  // profiling build only: per-CTA start/end time, units, tiles
@@ -902,13 +775,16 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
 // ---------------------------------------------------------------------------
 // generic kernel (any dtype, CUDA cores)
 // ---------------------------------------------------------------------------
-template <int DT>
-__global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
+// DC / GC > 0: head dim / group size fixed at compile time (the f32 decode
+// path of config C1): index arithmetic folds, the loops unroll.
+template <int DT, int DC = 0, int GC = 0>
+__global__ void __launch_bounds__(kGen, 4) k_attend_generic(const View p) {
     pdl_wait();
     pdl_trigger();
     using T = typename Elem<DT>::T;
     extern __shared__ float gsm[];
-    const int t = threadIdx.x, G = p.G, D = p.D;
+    const int t = threadIdx.x;
+    const int G = GC > 0 ? GC : p.G, D = DC > 0 ? DC : p.D;
     // dynamic smem: Ks[16][D+1] | Vs[16][D] | qs[G][D] | sc[16][G] | mst,lst,alp[G]
     float* Ksm = gsm;
     float* Vsm = Ksm + kBoxRows * (D + 1);
@@ -921,7 +797,6 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
 #define Vs(r, d) Vsm[(r) * D + (d)]
 #define qs(h, d) qsm[(h) * D + (d)]
 #define sc(r, h) scm[(r) * G + (h)]
-    __shared__ MergeSmem<kGenMaxG> ms;
     __shared__ int32_t s_start[kMaxPrefix + 1];
     __shared__ int s_wtmp[kGen / 32];
     const int32_t* starts = run_starts(p, s_start, s_wtmp, t, kGen);
@@ -929,12 +804,68 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
     const int64_t NB = starts[p.n_bg];
     const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
     if (r0 >= r1) return;
-    if (t == 0) ms.nruns = 0;
     const float scale = rsqrtf((float)D);
     float acc[kGenMaxG][2];
     int bg = find_bg(starts, p.n_bg, r0);
     int64_t s_bg = starts[bg], e_bg = starts[bg + 1];
     bool fresh = true;
+    // The next box's K / V elements are loaded into registers while this box
+    // is computed (the loads of a box are the latency that dominates here).
+    // (D <= 128; wider heads load each box synchronously)
+    constexpr int EPT = kBoxRows * 128 / kGen;  // elements per thread at D = 128
+    const bool pf = D <= 128;
+    float nk[EPT], nv[EPT];
+    auto box_of = [&](int64_t xx, int bgx, int64_t sbg) { return p.boxes[(int64_t)bgx * p.box_stride + (xx - sbg)]; };
+    auto load_box = [&](const Box& bx, int bgx) {
+        if (!pf) return;
+        const T* kb = static_cast<const T*>(p.k) + (int64_t)bgx * p.l_cap * D;
+        const T* vb = static_cast<const T*>(p.v) + (int64_t)bgx * p.l_cap * D;
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int e = t + u * kGen;
+            nk[u] = nv[u] = 0.f;
+            if (e < kBoxRows * D) {
+                const int r = e / D, d = e % D;
+                if (r < bx.n) {
+                    const int64_t row = p.idx ? (int64_t)p.idx[bx.row + r] : (int64_t)bx.row + r;
+                    nk[u] = tofl(kb[row * D + d]);
+                    nv[u] = tofl(vb[row * D + d]);
+                }
+            }
+        }
+    };
+    // (box x, group) of the next real box after x in this range, or -1
+    auto next_real = [&](int64_t xx, int bgx, int64_t ebg, int64_t& nx, int& nbg, int64_t& nsbg) {
+        nx = xx + 1;
+        nbg = bgx;
+        int64_t e2 = ebg;
+        nsbg = starts[bgx];
+        while (nx < r1 && nx >= e2 - p.pad) {
+            nx = e2;
+            if (nx >= r1) break;
+            ++nbg;
+            nsbg = starts[nbg];
+            e2 = starts[nbg + 1];
+        }
+        return nx < r1;
+    };
+    // QK: TPP threads per (token, head) pair split the dot product
+    const int pairs = kBoxRows * G;
+    const int TPP = pairs >= kGen ? 1 : pairs * 2 >= kGen ? 2 : pairs * 4 >= kGen ? 4 : 8;
+    const int DPT = D / TPP;  // contiguous dims per thread of a pair (D % 8 == 0 on this path)
+    {   // first real box of the range
+        int64_t x0 = r0;
+        int b0 = bg;
+        int64_t s0 = s_bg, e0 = e_bg;
+        while (x0 < r1 && x0 >= e0 - p.pad) {
+            x0 = e0;
+            if (x0 >= r1) break;
+            ++b0;
+            s0 = starts[b0];
+            e0 = starts[b0 + 1];
+        }
+        if (x0 < r1) load_box(box_of(x0, b0, s0), b0);
+    }
     for (int64_t x = r0; x < r1; ++x) {
         while (x >= e_bg - p.pad) {  // range starts in (or reaches) virtual boxes
             x = e_bg;
@@ -956,48 +887,76 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
             for (int h = 0; h < kGenMaxG; ++h) acc[h][0] = acc[h][1] = 0.f;
             fresh = false;
         }
-        const Box bx = p.boxes[(int64_t)bg * p.box_stride + (x - s_bg)];
-        const T* kb = static_cast<const T*>(p.k) + (int64_t)bg * p.l_cap * D;
-        const T* vb = static_cast<const T*>(p.v) + (int64_t)bg * p.l_cap * D;
-        for (int e = t; e < kBoxRows * D; e += kGen) {
-            const int r = e / D, d = e % D;
-            float kv = 0.f, vv = 0.f;
-            if (r < bx.n) {
-                const int64_t row = p.idx ? (int64_t)p.idx[bx.row + r] : (int64_t)bx.row + r;
-                kv = tofl(kb[row * D + d]);
-                vv = tofl(vb[row * D + d]);
+        const Box bx = box_of(x, bg, s_bg);
+        if (pf) {
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) {
+                const int e = t + u * kGen;
+                if (e < kBoxRows * D) {
+                    Ks(e / D, e % D) = nk[u];
+                    Vs(e / D, e % D) = nv[u];
+                }
             }
-            Ks(r, d) = kv;
-            Vs(r, d) = vv;
+        } else {
+            const T* kb = static_cast<const T*>(p.k) + (int64_t)bg * p.l_cap * D;
+            const T* vb = static_cast<const T*>(p.v) + (int64_t)bg * p.l_cap * D;
+            for (int e = t; e < kBoxRows * D; e += kGen) {
+                const int r = e / D, d = e % D;
+                float kv = 0.f, vv = 0.f;
+                if (r < bx.n) {
+                    const int64_t row = p.idx ? (int64_t)p.idx[bx.row + r] : (int64_t)bx.row + r;
+                    kv = tofl(kb[row * D + d]);
+                    vv = tofl(vb[row * D + d]);
+                }
+                Ks(r, d) = kv;
+                Vs(r, d) = vv;
+            }
+        }
+        {   // the next real box starts loading now
+            int64_t nx, nsbg;
+            int nbg;
+            if (next_real(x, bg, e_bg, nx, nbg, nsbg)) load_box(box_of(nx, nbg, nsbg), nbg);
         }
         __syncthreads();
-        for (int pr = t; pr < kBoxRows * G; pr += kGen) {
-            const int tok = pr / G, h = pr % G;
-            float s = -INFINITY;
+        for (int pi = t / TPP; pi < pairs; pi += kGen / TPP) {
+            const int tok = pi / G, h = pi % G, sub = t % TPP;
+            float a = 0.f;
             if (tok < bx.n && ((bx.mask >> h) & 1)) {
-                float a = 0.f;
-                for (int d = 0; d < D; ++d) a = fmaf(qs(h, d), Ks(tok, d), a);
-                s = a * scale;
+                if (D % 8 == 0) {  // contiguous slice, four independent chains
+                    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+                    for (int j = 0; j < DPT; ++j) {
+                        const int d = sub * DPT + j;
+                        a4[j & 3] = fmaf(qs(h, d), Ks(tok, d), a4[j & 3]);
+                    }
+                    a = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+                } else {
+                    for (int d = sub; d < D; d += TPP) a = fmaf(qs(h, d), Ks(tok, d), a);
+                }
             }
-            sc(tok, h) = s;
+            for (int o = TPP / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (sub == 0) sc(tok, h) = (tok < bx.n && ((bx.mask >> h) & 1)) ? a * scale : -INFINITY;
         }
         __syncthreads();
         if (t < G) {
             float mx = mst[t];
             for (int tok = 0; tok < kBoxRows; ++tok) mx = fmaxf(mx, sc(tok, t));
-            const float a = mx == -INFINITY ? 1.f : expf(mst[t] - mx);
-            const float base = mx == -INFINITY ? 0.f : mx;
-            float sum = 0.f;
-            for (int tok = 0; tok < kBoxRows; ++tok) {
-                const float pv = expf(sc(tok, t) - base);
-                sc(tok, t) = pv;
-                sum += pv;
-            }
-            lst[t] = lst[t] * a + sum;
+            alp[t] = mx == -INFINITY ? 1.f : expf(mst[t] - mx);
+            lst[t] *= alp[t];
             mst[t] = mx;
-            alp[t] = a;
         }
         __syncthreads();
+        for (int pi = t; pi < pairs; pi += kGen) {  // one exp per (token, head)
+            const int tok = pi / G, h = pi % G;
+            const float base = mst[h] == -INFINITY ? 0.f : mst[h];
+            sc(tok, h) = expf(sc(tok, h) - base);
+        }
+        __syncthreads();
+        if (t < G) {
+            float sum = 0.f;
+            for (int tok = 0; tok < kBoxRows; ++tok) sum += sc(tok, t);
+            lst[t] += sum;
+        }
 #pragma unroll
         for (int dd = 0; dd < 2; ++dd) {
             const int d = t + dd * kGen;
@@ -1014,14 +973,8 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
         }
         __syncthreads();
         if (x + 1 == r1 || x + 1 == e_bg - p.pad) {
-            // a run wholly inside this CTA is final; else a partial for finish_cta
+            // a run wholly inside this CTA is final; else a partial for k_merge_runs
             const bool sole = s_bg >= r0 && e_bg - p.pad <= r1;
-            if (!sole && t == 0) {
-                ms.runs[ms.nruns] = bg;
-                ms.rs[ms.nruns] = (int)s_bg;
-                ms.re[ms.nruns] = (int)(e_bg - p.pad);
-                ++ms.nruns;
-            }
             const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * G + (int64_t)(bg % p.Hkv) * G
                                        : (int64_t)(cta + bg) * G;
             float* dst_o = sole ? p.o : p.part_o;
@@ -1049,7 +1002,125 @@ __global__ void __launch_bounds__(kGen) k_attend_generic(const View p) {
 done:
     __syncthreads();
     write_empty_runs(p, starts, r0, r1, t, kGen);
-    finish_cta(p, NB, grid, t, kGen, 1, &ms);
+    // runs cut by a range end left partials: k_merge_runs follows
+}
+
+// Merge of the partials of the generic kernel's runs cut by CTA range ends
+// (attention.cpp:89-104 across the contributing CTAs): one 256-thread CTA per
+// (b, g, head), launched behind it (PDL).  The contributors' LSEs first, then
+// each thread folds one float4 column over a fixed subset of the contributors
+// (eight loads in flight), subsets combined in a fixed order: deterministic.
+constexpr int kMergeRunThreads = 256;
+constexpr int kMaxMergeList = 1024;  // contributors of one run (>= the generic grid, 4 per SM)
+__global__ void __launch_bounds__(kMergeRunThreads) k_merge_runs(const View p, int grid) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ int32_t s_start[kMaxPrefix + 1];
+    __shared__ int s_wtmp[kMergeRunThreads / 32];
+    __shared__ float s_wm[kMergeRunThreads / 32];
+    __shared__ float4 s_acc[kMergeRunThreads];
+    __shared__ float s_den[kMergeRunThreads];
+    const int t = threadIdx.x, bg = blockIdx.x, h = blockIdx.y, G = p.G, D = p.D;
+    const int32_t* starts = run_starts(p, s_start, s_wtmp, t, kMergeRunThreads);
+    const int64_t NB = starts[p.n_bg];
+    const int64_t rs = starts[bg], re = starts[bg + 1] - p.pad;
+    if (re <= rs) return;  // no real boxes: write_empty_runs wrote the identity
+    const int cf = cta_of(rs, NB, grid), cl = cta_of(re - 1, NB, grid);
+    if (cf == cl) return;  // wholly inside one CTA: written final
+    // the CTAs of [cf, cl] with a non-empty range left a partial: compact them
+    // in CTA (= box) order, so the fold below depends only on the run's boxes
+    // and partials, not on how many other runs share the grid
+    __shared__ int s_list[kMaxMergeList];
+    __shared__ int s_n;
+    if (t == 0) s_n = 0;
+    __syncthreads();
+    for (int c0 = cf; c0 <= cl; c0 += kMergeRunThreads) {
+        const int c = c0 + t;
+        const bool ne = c <= cl && cta_nonempty(c, NB, grid);
+        const unsigned bal = __ballot_sync(0xffffffffu, ne);
+        if ((t & 31) == 0) s_wtmp[t >> 5] = __popc(bal);
+        __syncthreads();
+        int off = s_n;
+        for (int w = 0; w < (t >> 5); ++w) off += s_wtmp[w];
+        if (ne) {
+            const int pos = off + __popc(bal & ((1u << (t & 31)) - 1u));
+            if (pos < kMaxMergeList) s_list[pos] = c;
+        }
+        __syncthreads();
+        if (t == 0)
+            for (int w = 0; w < kMergeRunThreads / 32; ++w) s_n += s_wtmp[w];
+        __syncthreads();
+    }
+    const int n = min(s_n, kMaxMergeList);
+    float m = -INFINITY;
+    for (int i = t; i < n; i += kMergeRunThreads) m = fmaxf(m, __ldg(p.part_lse + (int64_t)(s_list[i] + bg) * G + h));
+    m = warp_max(m);
+    if ((t & 31) == 0) s_wm[t >> 5] = m;
+    __syncthreads();
+    float M = s_wm[0];
+#pragma unroll
+    for (int w = 1; w < kMergeRunThreads / 32; ++w) M = fmaxf(M, s_wm[w]);
+    const int b = bg / p.Hkv, g = bg % p.Hkv;
+    const int64_t hd = (int64_t)b * p.Hkv * G + (int64_t)g * G + h;
+    const bool vec = D % 4 == 0;
+    const int VP = vec ? D / 4 : D;              // columns of the head
+    const int S = max(1, kMergeRunThreads / VP);  // contributor subsets
+    for (int c0 = 0; c0 < VP; c0 += kMergeRunThreads / S) {
+        const int v = c0 + t % (kMergeRunThreads / S), sub = t / (kMergeRunThreads / S);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float den = 0.f;
+        if (v < VP && sub < S) {
+            constexpr int kIn = 8;
+            for (int i0 = sub; i0 < n; i0 += S * kIn) {
+                float4 x[kIn];
+                float l[kIn];
+#pragma unroll
+                for (int j = 0; j < kIn; ++j) {
+                    const int i = i0 + j * S;
+                    const bool live = i < n;
+                    const int64_t slot = (int64_t)((live ? s_list[i] : cf) + bg) * G + h;
+                    l[j] = live ? __ldg(p.part_lse + slot) : -INFINITY;
+                    x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (live) {
+                        if (vec) x[j] = __ldg(reinterpret_cast<const float4*>(p.part_o + slot * D) + v);
+                        else x[j].x = __ldg(p.part_o + slot * D + v);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kIn; ++j) {
+                    if (l[j] == -INFINITY) continue;
+                    const float w = __expf(l[j] - M);
+                    den += w;
+                    acc.x += w * x[j].x;
+                    acc.y += w * x[j].y;
+                    acc.z += w * x[j].z;
+                    acc.w += w * x[j].w;
+                }
+            }
+        }
+        s_acc[t] = acc;
+        s_den[t] = den;
+        __syncthreads();
+        if (sub == 0 && v < VP) {
+            for (int k = 1; k < S; ++k) {
+                const float4 a = s_acc[k * (kMergeRunThreads / S) + t % (kMergeRunThreads / S)];
+                acc.x += a.x;
+                acc.y += a.y;
+                acc.z += a.z;
+                acc.w += a.w;
+                den += s_den[k * (kMergeRunThreads / S) + t % (kMergeRunThreads / S)];
+            }
+            const float inv = den > 0.f ? 1.f / den : 0.f;
+            if (vec) {
+                *reinterpret_cast<float4*>(p.o + hd * D + v * 4) =
+                    make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+            } else {
+                p.o[hd * D + v] = acc.x * inv;
+            }
+            if (v == 0 && p.lse) p.lse[hd] = den > 0.f ? M + __logf(den) : -INFINITY;
+        }
+        __syncthreads();
+    }
 }
 
 #undef Ks
@@ -1248,18 +1319,30 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
             FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             launch_pdl(k_attend_generic<FX_BF16>, grid, kGen, smem, s, v);
         } else {
-            FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            launch_pdl(k_attend_generic<FX_F32>, grid, kGen, smem, s, v);
+            auto kern = k_attend_generic<FX_F32>;
+            if (D == 128 && G == 4) kern = k_attend_generic<FX_F32, 128, 4>;
+            else if (D == 128 && G == 7) kern = k_attend_generic<FX_F32, 128, 7>;
+            else if (D == 128 && G == 8) kern = k_attend_generic<FX_F32, 128, 8>;
+            else if (D == 64 && G == 4) kern = k_attend_generic<FX_F32, 64, 4>;
+            FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            launch_pdl(kern, grid, kGen, smem, s, v);
         }
     }
     FX_CUDA(cudaGetLastError());
     return n;
 }
 
-int launch_unit_merge(const AttendArgs& a, bool allow_tma, cudaStream_t s) {
-    if (!allow_tma || !attend_uses_tma(a.L, a.idx != nullptr)) return 0;
+int launch_unit_merge(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
+    if (!allow_tma || !attend_uses_tma(a.L, a.idx != nullptr)) {  // generic kernel: cut runs
+        FX_REQUIRE(grid <= kMaxMergeList, FX_ERR_INVALID, "bad-shape: attention grid too large for the run merge");
+        launch_pdl(k_merge_runs, dim3((unsigned)(a.L.batch * a.L.kv_heads), (unsigned)a.L.group_size),
+                   kMergeRunThreads, 0, s, make_view(a), grid);
+        FX_CUDA(cudaGetLastError());
+        return 1;
+    }
     const int n_bg = a.L.batch * a.L.kv_heads;
-    launch_pdl(k_merge_units, n_bg, kMergeThreads, 0, s, a.L.kv_heads, a.L.group_size, a.L.head_dim,
+    launch_pdl(k_merge_units, dim3((unsigned)n_bg, (unsigned)a.L.group_size), kMergeThreads, 0, s,
+               a.L.kv_heads, a.L.group_size, a.L.head_dim,
                (const int32_t*)a.bg_count, (const int32_t*)a.uq.ubase, (const float*)a.part_o,
                (const float*)a.part_lse, a.o, a.lse);
     FX_CUDA(cudaGetLastError());

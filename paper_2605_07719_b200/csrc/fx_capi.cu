@@ -804,7 +804,7 @@ int fx_decode_step(fx_ctx* ctx, const fx_layout* lay, const fx_step_args* a) {
         }
         {
             Timed tm(ctx, FX_KERNEL_MERGE);
-            n += fx::launch_unit_merge(aa, true, st);
+            n += fx::launch_unit_merge(aa, grid, true, st);
         }
         ctx->launches += n;
     });
@@ -879,6 +879,7 @@ int fx_gathered_attention(fx_ctx* ctx, const float* q, const void* k, const void
         fx::launch_index_boxes(n, const_cast<fx::Box*>(aa.boxes), const_cast<int32_t*>(aa.bg_start),
                                const_cast<int32_t*>(aa.bg_count), aa.bg_done, ctx->stream);
         ctx->launches += 1 + fx::launch_attend(aa, grid, false, ctx->stream);
+        ctx->launches += fx::launch_unit_merge(aa, grid, false, ctx->stream);
     });
 }
 

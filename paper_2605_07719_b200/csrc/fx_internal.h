@@ -260,9 +260,10 @@ struct AttendArgs {
 int64_t unit_capacity(int64_t n_bg, int64_t box_stride);
 bool attend_uses_tma(const fx_layout& L, bool has_idx);
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms);
-// the TMA kernel's unit-partial merge (one CTA per (b, g), behind it with PDL);
-// returns the number of kernels launched (0 for the generic kernel)
-int launch_unit_merge(const AttendArgs& a, bool allow_tma, cudaStream_t s);
+// the partial merge that follows launch_attend (PDL): the TMA kernel's unit
+// partials, or the generic kernel's runs cut by CTA range ends; returns the
+// number of kernels launched
+int launch_unit_merge(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s);
 // returns the number of kernels launched
 int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s);
 void launch_index_boxes(int64_t n, Box* boxes, int32_t* bg_start, int32_t* bg_count,

@@ -506,7 +506,7 @@ def test_launch_count_per_step(engine):
     qd = torch.as_tensor(q).cuda()
     n0 = engine.launches()
     dec.step(qd, fixed=(16, 0.05))
-    assert engine.launches() - n0 == 5  # plan, score, select (+ fused worklist), attend, unit merge
+    assert engine.launches() - n0 == 5  # plan, score, select (+ fused worklist), attend, partial merge
 
 
 def test_decode_step_empty_group_is_identity(engine):
