@@ -732,7 +732,7 @@ def run_ours(a):
 
     B, H, HKV, G = a.batch, a.heads, a.hkv, a.G
     l_cpu = a.context - L_SINK - L_LOCAL
-    total_steps = 2 * a.warmup + 5 * a.steps + 10  # timed, graph replay, timing pass, e2e, predictor
+    total_steps = 2 * a.warmup + 5 * a.steps + 60  # timed, graph replay, timing pass, e2e, predictor (+ its split)
     eng = Engine(local)
     tdt = torch.bfloat16 if a.kv_dtype == "bf16" else torch.float32
     gen = torch.Generator(device=dev)
@@ -1070,6 +1070,22 @@ def run_ours(a):
         t1.record()
         torch.cuda.synchronize()
         pms = max_over_ranks(t0.elapsed_time(t1))
+        # per-step split of 40 more steps (events around each call, synchronized
+        # per step): the plan the predictor produces changes with the decoded rows
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        split = []
+        for _ in range(40):
+            i = step_i[0]
+            evs[0].record()
+            pp = dec.predict_props(qs[i], rec, pred, append=(kv_new[i - 1, 0], kv_new[i - 1, 1]))
+            evs[1].record()
+            dec.step(qs[i], props=pp)
+            evs[2].record()
+            step_i[0] += 1
+            torch.cuda.synchronize()
+            split.append((evs[0].elapsed_time(evs[1]), evs[1].elapsed_time(evs[2]),
+                          int((dec.plan_blk > 0).sum().item())))
+        split = np.array(split)
         # phase split: the props launch alone and the step alone, each repeated
         # back to back on the same inputs (no append), CUDA events around the loop
         nrep = 20
@@ -1091,6 +1107,12 @@ def run_ours(a):
         result["predictor_path"] = {
             "value": world * a.steps / (pms / 1e3), "unit": UNIT, "ms_per_step": pms / a.steps,
             "predict_props_ms": props_ms, "decode_step_ms": pstep_ms, "decoded_rows": dec.l_new,
+            "per_step_split": {"steps": len(split), "props_ms_median": float(np.median(split[:, 0])),
+                               "step_ms_median": float(np.median(split[:, 1])),
+                               "step_ms_p90": float(np.percentile(split[:, 1], 90)),
+                               "step_ms_max": float(split[:, 1].max()),
+                               "retrieval_groups_min": int(split[:, 2].min()),
+                               "retrieval_groups_max": int(split[:, 2].max())},
             "retrieval_groups": retr_groups,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
             "per_step": "fx_predict_props (previous token appended; decode features as chunk "

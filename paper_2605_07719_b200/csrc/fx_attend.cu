@@ -364,9 +364,10 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
         // ------------------------------ producer ------------------------------
         // Units are claimed one ahead: while unit `cur` streams, the next
         // claim's flag word, box count and box descriptors are fetched.
+        constexpr int UPL = kUnitBoxes / 32;  // box descriptors per lane
         struct Unit {
             int u, bg, c, total;
-            Box wb;  // this lane's box descriptor
+            Box wb[UPL];  // this lane's box descriptors (boxes lane, lane + 32, ...)
         };
         int st = 0;
         uint32_t ph = 0;
@@ -401,12 +402,16 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
             f.c = (int)(lo & ((1u << kUnitIdxBits) - 1u));
             f.total = __ldcg(p.bg_count + f.bg);
             const int x0 = f.c * kUnitBoxes, x1 = min(x0 + kUnitBoxes, f.total);
-            f.wb = Box{0, 0, 0};
-            if (x0 + lane < x1) {
-                const int2 r = __ldcg(reinterpret_cast<const int2*>(p.boxes + (int64_t)f.bg * p.box_stride + x0 + lane));
-                f.wb.row = r.x;
-                f.wb.n = (uint16_t)(r.y & 0xffff);
-                f.wb.mask = (uint16_t)((uint32_t)r.y >> 16);
+#pragma unroll
+            for (int k = 0; k < UPL; ++k) {
+                f.wb[k] = Box{0, 0, 0};
+                if (x0 + lane + 32 * k < x1) {
+                    const int2 r = __ldcg(reinterpret_cast<const int2*>(p.boxes + (int64_t)f.bg * p.box_stride + x0 +
+                                                                       lane + 32 * k));
+                    f.wb[k].row = r.x;
+                    f.wb[k].n = (uint16_t)(r.y & 0xffff);
+                    f.wb[k].mask = (uint16_t)((uint32_t)r.y >> 16);
+                }
             }
             return 1;
         };
@@ -415,7 +420,8 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
             if (lane == 0) u = atomicAdd(p.uq.ctl + 2, 1);
             return __shfl_sync(0xffffffffu, u, 0);
         };
-        static_assert(kUnitBoxes == 32, "one box descriptor per lane");
+        static_assert(kUnitBoxes % 32 == 0 && kTileBoxes <= 32 && 32 % kTileBoxes == 0,
+                      "whole descriptor sets per lane; a tile's boxes in one set");
         Unit cur, nxt;
 #ifdef FX_TRACE
         long long pw0 = globaltimer();
@@ -437,11 +443,16 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
             do {
                 const int nb = max(0, min(kTileBoxes, x1 - x));
                 Box bx[kTileBoxes];
+                // the tile's descriptor set (warp-uniform: tiles are 8-aligned in the unit)
+                Box ws = cur.wb[0];
+#pragma unroll
+                for (int k = 1; k < UPL; ++k)
+                    if (((x - x0) >> 5) == k) ws = cur.wb[k];
 #pragma unroll
                 for (int i = 0; i < kTileBoxes; ++i) {
                     const int src = (x - x0 + i) & 31;
-                    bx[i].row = __shfl_sync(0xffffffffu, cur.wb.row, src);
-                    const uint32_t nm = __shfl_sync(0xffffffffu, (uint32_t)cur.wb.n | ((uint32_t)cur.wb.mask << 16), src);
+                    bx[i].row = __shfl_sync(0xffffffffu, ws.row, src);
+                    const uint32_t nm = __shfl_sync(0xffffffffu, (uint32_t)ws.n | ((uint32_t)ws.mask << 16), src);
                     bx[i].n = (uint16_t)(nm & 0xffffu);
                     bx[i].mask = (uint16_t)(nm >> 16);
                 }

@@ -44,6 +44,9 @@ struct DevBuf {
     size_t bytes = 0;
     void ensure(size_t n) {
         if (n <= bytes) return;
+        // regrowth frees (a device-wide synchronization): grow by half again at
+        // least, so sizes that creep up step by step (the decoded rows) regrow rarely
+        if (p) n = std::max(n, bytes + bytes / 2);
         if (p) FX_CUDA(cudaFree(p));
         p = nullptr;
         bytes = 0;

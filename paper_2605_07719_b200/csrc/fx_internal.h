@@ -26,7 +26,7 @@ constexpr int kMaxRunPrefix = 1024;
 // one (b, g) (4 pipeline tiles).  The worklist publishes a group's units to a
 // queue as soon as the group's boxes exist; persistent attention CTAs claim
 // units in publication order.
-constexpr int kUnitBoxes = 32;
+constexpr int kUnitBoxes = 64;
 // Unit queue flag word: epoch (32) | bg (19) | unit index in the group (13).
 constexpr int kUnitBgBits = 19, kUnitIdxBits = 13;
 // Candidate granularities, selector.hpp:12.
