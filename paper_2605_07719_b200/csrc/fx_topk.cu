@@ -322,7 +322,11 @@ __device__ __forceinline__ void select_head(
     // then one thread per candidate adds its D terms in dimension order: the
     // reference sum, with only the dependent adds left serial.
     constexpr bool kTerms = DT == FX_BF16;
-    const int tpitch = D + 1;  // doubles; the odd pitch spreads the row-parallel reads over banks
+    // term layout of a candidate: dims in groups of 8 with a one-double skew
+    // per group (index (d / 8) * 9 + d % 8), so the 16 writers of a candidate
+    // (8 dims each) hit 16 distinct bank pairs; odd candidate pitch, so the
+    // serial readers (one candidate each) spread over the banks too
+    const int tpitch = (D / 8) * 9 + 1;  // doubles
     const int per_round_t = ((int)((size_t)keys_cap * 4 + kBins * 4)) / (tpitch * 8);
     if (kTerms && (D & 7) == 0 && per_round_t >= 1) {
         double* term = reinterpret_cast<double*>(dsm);
@@ -336,7 +340,7 @@ __device__ __forceinline__ void select_head(
                 const uint4 a = __ldg(reinterpret_cast<const uint4*>(row) + u);
                 const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + D) + u);
                 const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
-                double* tr = term + (size_t)cc * tpitch + 8 * u;
+                double* tr = term + (size_t)cc * tpitch + 9 * u;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const double q0 = s_q[8 * u + 2 * j], q1 = s_q[8 * u + 2 * j + 1];
@@ -352,8 +356,9 @@ __device__ __forceinline__ void select_head(
             for (int cc = t; cc < nc; cc += kT) {
                 const double* tr = term + (size_t)cc * tpitch;
                 double sum = 0.0;
-#pragma unroll 16
-                for (int d = 0; d < D; ++d) sum = __dadd_rn(sum, tr[d]);
+                for (int g8 = 0; g8 < D / 8; ++g8)  // dimension order
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) sum = __dadd_rn(sum, tr[9 * g8 + j]);
                 const int64_t c = c0 + cc;
                 if (small) ck[c] = f64_key(sum);
                 else ckeys[c] = f64_key(sum);
