@@ -331,6 +331,17 @@ __device__ __forceinline__ void select_head(
     if (kTerms && (D & 7) == 0 && per_round_t >= 1) {
         double* term = reinterpret_cast<double*>(dsm);
         const int v8 = D / 8;
+        // a thread's 8 dims are the same for every candidate (kT % v8 == 0):
+        // its q slice in registers, read from global (L1) -- the shared copy's
+        // 64-byte-strided reads were 8-way bank conflicts
+        double qv[8];
+        const bool qreg = kT % v8 == 0;
+        if (qreg) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(qh + 8 * (t % v8)));
+            const float4 c = __ldg(reinterpret_cast<const float4*>(qh + 8 * (t % v8)) + 1);
+            qv[0] = a.x, qv[1] = a.y, qv[2] = a.z, qv[3] = a.w;
+            qv[4] = c.x, qv[5] = c.y, qv[6] = c.z, qv[7] = c.w;
+        }
         for (int64_t c0 = 0; c0 < n_cand; c0 += per_round_t) {
             const int nc = (int)(n_cand - c0 < per_round_t ? n_cand - c0 : per_round_t);
             for (int e = t; e < nc * v8; e += kT) {
@@ -343,7 +354,8 @@ __device__ __forceinline__ void select_head(
                 double* tr = term + (size_t)cc * tpitch + 9 * u;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const double q0 = s_q[8 * u + 2 * j], q1 = s_q[8 * u + 2 * j + 1];
+                    const double q0 = qreg ? qv[2 * j] : s_q[8 * u + 2 * j];
+                    const double q1 = qreg ? qv[2 * j + 1] : s_q[8 * u + 2 * j + 1];
                     const double x0 = __dmul_rn(q0, (double)bf16lo_to_f(av[j]));
                     const double y0 = __dmul_rn(q0, (double)bf16lo_to_f(cv[j]));
                     const double x1 = __dmul_rn(q1, (double)bf16hi_to_f(av[j]));
