@@ -671,25 +671,55 @@ def run_c5(a):
         step_bytes = (meta_b + attend_b) / a.steps
         result["step_bytes"] = step_bytes
         result["step_GBps"] = step_bytes / (result["ms_per_step"] * 1e-3) / 1e9
-        # e2e: pinned host q in, o + lse out, per step, through the C-ABI
+        # e2e: pinned host q in, o + lse out, per step, through the C-ABI; a side
+        # stream moves step i+1's q in and step i's output out while step i
+        # computes (double-buffered), every copy inside the timed region
         qh = qs[: a.steps].cpu().pin_memory()
         oh = torch.empty((a.steps, B, H, D), dtype=torch.float32).pin_memory()
         lh = torch.empty((a.steps, B, H), dtype=torch.float32).pin_memory()
-        qd = torch.empty((B, H, D), dtype=torch.float32, device=dev)
+        qd = [torch.empty((B, H, D), dtype=torch.float32, device=dev) for _ in range(2)]
+        od = [torch.empty((B, H, D), dtype=torch.float32, device=dev) for _ in range(2)]
+        ld = [torch.empty((B, H), dtype=torch.float32, device=dev) for _ in range(2)]
+        comp = torch.cuda.current_stream(dev)
+        cs = torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_q = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_read = [torch.cuda.Event() for _ in range(2)]
+
+        def h2d(i):
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(ev_q[i % 2])  # step i-2 read q buffer i%2
+                qd[i % 2].copy_(qh[i], non_blocking=True)
+                ev_in[i % 2].record(cs)
+
         torch.cuda.synchronize()
         t0.record()
+        h2d(0)
         for i in range(a.steps):
-            qd.copy_(qh[i], non_blocking=True)
-            o, lse = dec.step(qd, props=props)
-            oh[i].copy_(o, non_blocking=True)
-            lh[i].copy_(lse, non_blocking=True)
+            j = i % 2
+            comp.wait_event(ev_in[j])
+            if i >= 2:
+                comp.wait_event(ev_read[j])  # output buffer j copied out
+            dec.step(qd[j], props=props, out=od[j], lse=ld[j])
+            ev_out[j].record(comp)
+            ev_q[j].record(comp)
+            if i + 1 < a.steps:
+                h2d(i + 1)
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_out[j])
+                oh[i].copy_(od[j], non_blocking=True)
+                lh[i].copy_(ld[j], non_blocking=True)
+                ev_read[j].record(cs)
+        comp.wait_stream(cs)
         t1.record()
         torch.cuda.synchronize()
         ems = t0.elapsed_time(t1)
         result["e2e"] = {"value": a.steps / (ems / 1e3), "unit": UNIT,
                          "h2d_bytes_per_step": B * H * D * 4, "d2h_bytes_per_step": B * H * (D + 1) * 4,
                          "path": "C-ABI fx_decode_step per step, pinned host q in, o + lse out, "
-                                 "copies on the compute stream"}
+                                 "copies overlapped on a side stream (double-buffered)"}
         if not a.no_cpu_baseline:  # the reference on 1 of the 4 sequences (8 GB of f32 KV), x4
             try:
                 q_par = qs[step_i[0]].contiguous()
