@@ -18,7 +18,7 @@ dev = eng.device
 rng = np.random.default_rng(0)
 B, HKV, G, D = 2, 2, 4, 128
 for dtype in ("bf16", "f32"):
-    dec = SparseDecoder(eng, B, HKV, G, D, 64, 3000, 256, max_new=8, dtype=dtype)
+    dec = SparseDecoder(eng, B, HKV, G, D, 64, 3000, 256, max_new=80, dtype=dtype)
     dec.k.normal_()
     dec.v.normal_()
     dec.build_metadata(means=True)
@@ -40,6 +40,13 @@ for dtype in ("bf16", "f32"):
         rec = dec.prefill_stats(q, tau=0.10, layer=0)
         pp = dec.predict_props(q, rec, pred)
         dec.step(q, props=pp)
+        # decoded rows across a 64-row chunk boundary, the last one appended by
+        # the feature kernel itself; the features alone (fx_decode_features)
+        for _ in range(66):
+            dec.append(kv[0], kv[1])
+        pp = dec.predict_props(q, rec, pred, append=(kv[0], kv[1]))
+        dec.step(q, props=pp)
+        dec.decode_features(q, rec)
         torch.cuda.synchronize()
         pred.close()
     print(dtype, "ok", float(o.abs().sum()))
