@@ -431,7 +431,7 @@ __device__ __forceinline__ double feature_value(int i, const double* r, double l
 // chunk maxima / weights are formed lane-parallel (lane = chunk), the chunk
 // outputs' loads are all independent; lane i forms feature i (and i + 32).
 template <int G, int D>
-__global__ void __launch_bounds__(kPT, 1) k_feat_final(fx_layout L, int64_t l_new, const float* __restrict__ q,
+__global__ void __launch_bounds__(kPT, 2) k_feat_final(fx_layout L, int64_t l_new, const float* __restrict__ q,
                                                     const double* __restrict__ rec,
                                                     const double* __restrict__ part,
                                                     double* __restrict__ feats, Layer1 l1) {
@@ -514,6 +514,21 @@ __global__ void __launch_bounds__(kPT, 1) k_feat_final(fx_layout L, int64_t l_ne
         s_m[i] = mz.x;
         s_wz[i] = mz.y;
     }
+    // the (head, dim) outputs of every chunk, loaded now (one round trip, in
+    // flight while the chunk weights are formed) when they fit in registers
+    constexpr int kMaxT = 16;
+    const bool vreg = PPT <= 2 && T <= kMaxT;
+    double pv[PPT <= 2 ? PPT : 1][kMaxT];
+    if (vreg) {
+#pragma unroll
+        for (int pp = 0; pp < (PPT <= 2 ? PPT : 1); ++pp) {
+            const int i = tid + pp * kPT;
+            const int hh = min(i / D, G - 1), d = i % D;
+            const double* pa = pb + (int64_t)hh * PS + 2 + d;
+#pragma unroll
+            for (int c = 0; c < kMaxT; ++c) pv[pp][c] = (c < T && i < G * D) ? pa[(int64_t)c * G * PS] : 0.0;
+        }
+    }
     __syncthreads();
     FP_MARK(tslot, 6);
     if (tid < G * 3) {  // per (head, segment): the maximum of the chunk maxima
@@ -548,14 +563,26 @@ __global__ void __launch_bounds__(kPT, 1) k_feat_final(fx_layout L, int64_t l_ne
         const int i = tid + pp * kPT;
         if (i < G * D) {
             const int hh = i / D, d = i - hh * D;
-            const double* pa = pb + (int64_t)hh * PS + 2 + d;
+            if (vreg) {
+#pragma unroll
+                for (int c = 0; c < kMaxT; ++c) {
+                    if (c >= T) break;
+                    const double v = pv[PPT <= 2 ? pp : 0][c] * s_m[hh * T + c];
+                    const int sg = seg_of(c);
+                    o[pp][0] += sg == 0 ? v : 0.0;
+                    o[pp][1] += sg == 1 ? v : 0.0;
+                    o[pp][2] += sg == 2 ? v : 0.0;
+                }
+            } else {
+                const double* pa = pb + (int64_t)hh * PS + 2 + d;
 #pragma unroll 8
-            for (int c = 0; c < T; ++c) {
-                const double v = pa[(int64_t)c * G * PS] * s_m[hh * T + c];
-                const int sg = seg_of(c);
-                o[pp][0] += sg == 0 ? v : 0.0;
-                o[pp][1] += sg == 1 ? v : 0.0;
-                o[pp][2] += sg == 2 ? v : 0.0;
+                for (int c = 0; c < T; ++c) {
+                    const double v = pa[(int64_t)c * G * PS] * s_m[hh * T + c];
+                    const int sg = seg_of(c);
+                    o[pp][0] += sg == 0 ? v : 0.0;
+                    o[pp][1] += sg == 1 ? v : 0.0;
+                    o[pp][2] += sg == 2 ? v : 0.0;
+                }
             }
         }
     }
