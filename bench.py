@@ -1146,7 +1146,7 @@ def run_ours(a):
             "retrieval_groups": retr_groups,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
             "per_step": "fx_predict_props (previous token appended; decode features as chunk "
-                        "partials + one clustered merge; the predictor's three layers) + fx_decode_step",
+                        "partials + one clustered merge with layer 1; layers 2 + 3) + fx_decode_step",
             "model": "random-init 41-256-384-3, output bias at the drawn-props operating point"}
         pred.close()
 

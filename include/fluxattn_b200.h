@@ -305,7 +305,8 @@ FX_API int fx_decode_features(fx_ctx* ctx, const fx_layout* lay, const void* k, 
  * the whole machine, then one merge launch in which the Hkv groups of a
  * sequence run as one thread-block cluster and exchange the cross-head
  * maximum (feature 39) through distributed shared memory; then the
- * predictor's three tiled layers.  append_k / append_v [dev] [B][Hkv][D] f32
+ * predictor's second layer with the output layer fused into its last CTA per
+ * row tile.  append_k / append_v [dev] [B][Hkv][D] f32
  * (nullable, together): the previous token (append_new, pipeline.cpp:406-412)
  * is written at decoded row l_new first and counted in (l_new + 1 decoded rows
  * attended) -- pass l_new + 1 to the step that follows.  Writes the head

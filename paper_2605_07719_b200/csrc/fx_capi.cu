@@ -121,7 +121,16 @@ struct fx_model {
     fx_ctx* ctx = nullptr;
     DevBuf buf;
     DevBuf act;  // hidden activations of the tiled layers (grown to the largest batch)
+    DevBuf tiles;  // monotonic row-tile counters of the layer-2 kernel (zeroed when allocated)
     const double *w1t, *b1, *w2t, *b2, *w3t, *b3, *mu, *sigma;
+    int32_t* row_tiles(int n, cudaStream_t s) {
+        const size_t need = (size_t)fx::predict_row_tiles(n) * sizeof(int32_t);
+        if (need > tiles.bytes) {
+            tiles.ensure(need);
+            FX_CUDA(cudaMemsetAsync(tiles.p, 0, tiles.bytes, s));
+        }
+        return static_cast<int32_t*>(tiles.p);
+    }
 };
 
 namespace {
@@ -712,6 +721,7 @@ int fx_model_destroy(fx_model* m) {
         cudaSetDevice(m->ctx->device);
         m->buf.release();
         m->act.release();
+        m->tiles.release();
         delete m;
     });
 }
@@ -724,9 +734,10 @@ int fx_predict(fx_ctx* ctx, const fx_model* m, int32_t n, const double* features
         FX_REQUIRE(m != nullptr, FX_ERR_STATE, "no-model: predictor source requires a model");
         auto* mm = const_cast<fx_model*>(m);
         mm->act.ensure(fx::predict_scratch_bytes(n));
+        int32_t* tiles = mm->row_tiles(n, ctx->stream);
         fx::launch_predict(n, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma,
-                           features, bgt0, kslope, streaming, z, mm->act.p, ctx->stream);
-        ctx->launches += n > 0 ? 3 : 0;
+                           features, bgt0, kslope, streaming, z, mm->act.p, tiles, ctx->stream);
+        ctx->launches += n > 0 ? 2 : 0;
     });
 }
 
@@ -1053,6 +1064,7 @@ int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_
         }
         auto* mm = const_cast<fx_model*>(m);
         mm->act.ensure(fx::predict_scratch_bytes((int)nh));
+        int32_t* tiles = mm->row_tiles((int)nh, ctx->stream);
         double* a1 = static_cast<double*>(mm->act.p);
         double* a2 = a1 + (size_t)nh * 256;
         if (fused) {  // features -> normalize -> layer 1 inside the merge kernel, then layers 2 and 3
@@ -1061,8 +1073,8 @@ int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_
             fx::launch_feat_fused(L, k, v, l_eff, q, rec, features, ctx->api.p, ctx->stream, append_k, append_v,
                                   l1, a1, ctx->num_sms);
             fx::launch_predict_tail((int)nh, a1, m->w2t, m->b2, m->w3t, m->b3, bgt0, kslope, streaming, z, a2,
-                                    ctx->stream);
-            ctx->launches += 4;
+                                    tiles, ctx->stream);
+            ctx->launches += 3;
         } else {
             const size_t fs = fx::decode_features_scratch_bytes(L, l_eff);
             const size_t fb = features ? 0 : (size_t)nh * 41 * sizeof(double);
@@ -1071,8 +1083,8 @@ int fx_predict_props(fx_ctx* ctx, const fx_layout* lay, void* k, void* v, int64_
                                  : reinterpret_cast<double*>(static_cast<char*>(ctx->api.p) + ((fs + 255) & ~size_t(255)));
             fx::launch_decode_features(L, k, v, l_eff, q, rec, f, ctx->api.p, ctx->stream);
             fx::launch_predict((int)nh, m->w1t, m->b1, m->w2t, m->b2, m->w3t, m->b3, m->mu, m->sigma, f, bgt0,
-                               kslope, streaming, z, mm->act.p, ctx->stream);
-            ctx->launches += 6;
+                               kslope, streaming, z, mm->act.p, tiles, ctx->stream);
+            ctx->launches += 5;
         }
     });
 }

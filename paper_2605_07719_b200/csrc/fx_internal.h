@@ -117,18 +117,21 @@ void launch_prepare(const fx_layout& L, int64_t l_plan, int plan_mode, int fixed
                     int32_t* err = nullptr);
 void launch_blocks_for_budget(int n, const double* budgets, const int32_t* blk, int64_t l_cpu,
                               int32_t* kblocks, cudaStream_t s);
-// the 41-256-384-3 predictor as three tiled f64 layer kernels; scratch holds
-// the hidden activations (predict_scratch_bytes(n))
+// the 41-256-384-3 predictor as tiled f64 layer kernels; scratch holds the
+// hidden activations (predict_scratch_bytes(n)); tiles = the model's
+// monotonic row-tile counters (predict_row_tiles(n) ints, zeroed once): the
+// last layer-2 CTA of a row tile runs the output layer
 size_t predict_scratch_bytes(int n);
+int predict_row_tiles(int n);
+void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
+                    const double* b2, const double* w3t, const double* b3, const double* mu,
+                    const double* sigma, const double* feats, double* bgt0, double* kslope,
+                    int32_t* streaming, double* z, void* scratch, int32_t* tiles, cudaStream_t s);
 // layers 2 and 3 + the head properties from the first hidden layer's output
 // a1 [n][256]; a2 [n][384] scratch (the fused feature path computes layer 1)
 void launch_predict_tail(int n, const double* a1, const double* w2t, const double* b2, const double* w3t,
                          const double* b3, double* bgt0, double* kslope, int32_t* streaming, double* z,
-                         double* a2, cudaStream_t s);
-void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
-                    const double* b2, const double* w3t, const double* b3, const double* mu,
-                    const double* sigma, const double* feats, double* bgt0, double* kslope,
-                    int32_t* streaming, double* z, void* scratch, cudaStream_t s);
+                         double* a2, int32_t* tiles, cudaStream_t s);
 
 // fx_score.cu / fx_topk.cu / fx_select.cu
 double approx_eps_scale(const fx_layout& L);

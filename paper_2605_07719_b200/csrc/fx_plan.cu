@@ -284,9 +284,19 @@ __global__ void __launch_bounds__(kMT) k_mlp_layer(int n, const double* __restri
 // a window of 8 inputs ahead in registers, so the warps never synchronize
 // inside the 256-input loop.  384 CTAs of 128 threads.
 constexpr int kH2R = 16, kH2N = 32, kH2T = 128, kH2XS = kH1 + 2, kH2W = 8;
+struct OutLayer {  // the output layer, run by the last neuron-tile CTA of each row tile
+    const double* w3t;  // [384][3]
+    const double* b3;
+    double* bgt0;
+    double* kslope;
+    int32_t* streaming;
+    double* z;        // raw logits [n][3] (nullable)
+    int32_t* tiles;   // [row tiles] monotonic counters: + gridDim.y per call
+};
 __global__ void __launch_bounds__(kH2T) k_mlp_h2(int n, const double* __restrict__ x,
                                                  const double* __restrict__ wt,
-                                                 const double* __restrict__ bias, double* __restrict__ y) {
+                                                 const double* __restrict__ bias, double* __restrict__ y,
+                                                 OutLayer ol) {
     extern __shared__ __align__(16) double h2sm[];
     double* xs = h2sm;  // [kH2R][kH2XS]
     const int r0 = blockIdx.x * kH2R, n0 = blockIdx.y * kH2N;
@@ -348,53 +358,46 @@ __global__ void __launch_bounds__(kH2T) k_mlp_h2(int n, const double* __restrict
     if (ra + 1 < n)
         *reinterpret_cast<double2*>(y + (int64_t)(ra + 1) * kH2 + n0 + nl) =
             make_double2(a10 > 0.0 ? a10 : 0.0, a11 > 0.0 ? a11 : 0.0);
-}
-
-// Output layer (384 -> 3, no activation) and the head properties
-// (predictor.cpp:161-185, pipeline.cpp:288): its chains are 384 dependent adds
-// long, so the kernel is latency-bound -- kOR = 4 rows per CTA (128 CTAs for
-// 512 heads), the rows and w3 staged by cp.async (both from L2), one lane per
-// (row, output) chain.
-constexpr int kOR = 4;
-__global__ void __launch_bounds__(32) k_mlp_out(int n, const double* __restrict__ a2,
-                                                const double* __restrict__ w3t,
-                                                const double* __restrict__ b3,
-                                                double* __restrict__ bgt0, double* __restrict__ kslope,
-                                                int32_t* __restrict__ streaming, double* __restrict__ zout) {
-    extern __shared__ __align__(16) double osm[];
-    double* ws = osm;              // [384][3]
-    double* as = osm + kH2 * 3;    // [kOR][384]
-    const int t = threadIdx.x;
-    for (int e = t; e < kH2 * 3 / 2; e += 32) cp_async16(ws + 2 * e, w3t + 2 * e);
-    cp_async_commit();
-    pdl_wait();
-    pdl_trigger();
-    const int r0 = blockIdx.x * kOR;
-    for (int e = t; e < kOR * kH2 / 2; e += 32) {  // asynchronous row copies
+    // The output layer (384 -> 3, no activation) and the head properties
+    // (predictor.cpp:161-185, pipeline.cpp:288) of this row tile, by the CTA
+    // that writes its last neurons: the barrier orders every thread's stores
+    // before thread 0's acq_rel count (the counters only grow: gridDim.y per
+    // call, so the last arrival sees a multiple of it).  Its 48 chains are 384
+    // dependent adds long, overlapping the other row tiles' layer-2 work.
+    __shared__ int s_last;
+    __syncthreads();
+    if (t == 0) s_last = (atomic_add_acq_rel_gpu(ol.tiles + blockIdx.x, 1) + 1) % (int)gridDim.y == 0;
+    __syncthreads();
+    if (!s_last) return;
+    fence_acq_rel_gpu();
+    double* w3s = h2sm;               // [384][3]
+    double* as = h2sm + kH2 * 3;      // [kH2R][384]
+    for (int e = t; e < kH2 * 3 / 2; e += kH2T) cp_async16(w3s + 2 * e, ol.w3t + 2 * e);
+    for (int e = t; e < kH2R * kH2 / 2; e += kH2T) {
         const int r = r0 + (2 * e) / kH2;
-        if (r < n) cp_async16(as + 2 * e, a2 + (int64_t)r0 * kH2 + 2 * e);
+        if (r < n) cp_async16(as + 2 * e, y + (int64_t)r0 * kH2 + 2 * e);
         else reinterpret_cast<double2*>(as)[e] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     const int lr = t / 3, o = t % 3, r = r0 + lr;
-    if (lr >= kOR || r >= n) return;
+    if (lr >= kH2R || r >= n) return;
     const double* a = as + lr * kH2;
-    double z = b3[o];
+    double z = ol.b3[o];
     for (int k0 = 0; k0 < kH2; k0 += 32) {  // 32 products first, then the in-order adds
         double p[32];
 #pragma unroll
-        for (int kk = 0; kk < 32; ++kk) p[kk] = __dmul_rn(a[k0 + kk], ws[(k0 + kk) * 3 + o]);
+        for (int kk = 0; kk < 32; ++kk) p[kk] = __dmul_rn(a[k0 + kk], w3s[(k0 + kk) * 3 + o]);
 #pragma unroll
         for (int kk = 0; kk < 32; ++kk) z = __dadd_rn(z, p[kk]);
     }
-    if (zout) zout[(int64_t)r * 3 + o] = z;
-    if (o == 0) bgt0[r] = clamp01(z);
-    if (o == 1) kslope[r] = z;
+    if (ol.z) ol.z[(int64_t)r * 3 + o] = z;
+    if (o == 0) ol.bgt0[r] = clamp01(z);
+    if (o == 1) ol.kslope[r] = z;
     if (o == 2) {
         const double sp = 1.0 / (1.0 + exp(-z));  // sigmoid, predictor.cpp:20
-        streaming[r] = sp >= 0.5 ? 1 : 0;          // pipeline.cpp:288
+        ol.streaming[r] = sp >= 0.5 ? 1 : 0;      // pipeline.cpp:288
     }
 }
 
@@ -430,22 +433,21 @@ size_t predict_scratch_bytes(int n) { return (size_t)std::max(n, 1) * (kH1 + kH2
 
 void launch_predict_tail(int n, const double* a1, const double* w2t, const double* b2, const double* w3t,
                          const double* b3, double* bgt0, double* kslope, int32_t* streaming, double* z,
-                         double* a2, cudaStream_t s) {
+                         double* a2, int32_t* tiles, cudaStream_t s) {
     if (n <= 0) return;
-    const size_t s2 = (size_t)kH2R * kH2XS * sizeof(double);
+    const size_t s2 = std::max((size_t)kH2R * kH2XS, (size_t)kH2 * 3 + (size_t)kH2R * kH2) * sizeof(double);
     FX_CUDA(cudaFuncSetAttribute(k_mlp_h2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-    launch_pdl(k_mlp_h2, dim3((unsigned)((n + kH2R - 1) / kH2R), kH2 / kH2N), kH2T, s2, s, n, a1, w2t, b2, a2);
-    const size_t osmem = (size_t)(kH2 * 3 + kOR * kH2) * sizeof(double);
-    FX_CUDA(cudaFuncSetAttribute(k_mlp_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem));
-    launch_pdl(k_mlp_out, (unsigned)((n + kOR - 1) / kOR), 32, osmem, s, n, (const double*)a2, w3t, b3, bgt0,
-               kslope, streaming, z);
+    const OutLayer ol{w3t, b3, bgt0, kslope, streaming, z, tiles};
+    launch_pdl(k_mlp_h2, dim3((unsigned)((n + kH2R - 1) / kH2R), kH2 / kH2N), kH2T, s2, s, n, a1, w2t, b2, a2, ol);
     FX_CUDA(cudaGetLastError());
 }
+
+int predict_row_tiles(int n) { return (std::max(n, 1) + kH2R - 1) / kH2R; }
 
 void launch_predict(int n, const double* w1t, const double* b1, const double* w2t,
                     const double* b2, const double* w3t, const double* b3, const double* mu,
                     const double* sigma, const double* feats, double* bgt0, double* kslope,
-                    int32_t* streaming, double* z, void* scratch, cudaStream_t s) {
+                    int32_t* streaming, double* z, void* scratch, int32_t* tiles, cudaStream_t s) {
     if (n <= 0) return;
     double* a1 = static_cast<double*>(scratch);
     double* a2 = a1 + (size_t)n * kH1;
@@ -453,7 +455,7 @@ void launch_predict(int n, const double* w1t, const double* b1, const double* w2
     const size_t s1 = (size_t)(2 * kKC * kMN + kMR * kF) * sizeof(double);
     FX_CUDA(cudaFuncSetAttribute(k_mlp_layer<kF, kH1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
     launch_pdl(k_mlp_layer<kF, kH1, true>, dim3(rt, kH1 / kMN), kMT, s1, s, n, feats, w1t, b1, mu, sigma, a1);
-    launch_predict_tail(n, a1, w2t, b2, w3t, b3, bgt0, kslope, streaming, z, a2, s);
+    launch_predict_tail(n, a1, w2t, b2, w3t, b3, bgt0, kslope, streaming, z, a2, tiles, s);
 }
 
 }  // namespace fx

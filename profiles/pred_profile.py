@@ -1,5 +1,5 @@
 """fx_predict_props at the C2 shape (16 x 8 groups, 128K, 100 decoded rows):
-the clustered features kernel + the three tiled predictor layers, for ncu."""
+the feature kernels (partials + clustered merge with layer 1) + layers 2 + 3, for ncu."""
 import os
 import sys
 
