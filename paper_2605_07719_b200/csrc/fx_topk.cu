@@ -25,6 +25,10 @@ namespace {
 constexpr int kT = 256;           // threads per selection CTA
 constexpr int kNW = kT / 32;
 constexpr int kBins = 2048;
+// the histogram is stored with one padding word per 32 bins (bin b at
+// b + b / 32): lanes whose bins differ by a multiple of 32 hit different banks
+constexpr int kHistWords = kBins + kBins / 32;
+__device__ __forceinline__ int hidx(int b) { return b + (b >> 5); }
 constexpr int kMaxWords = 4096;   // nblk <= 131072 at the chosen granularity
 constexpr int kSmemKeys = 16384;  // approximate scores staged in smem up to this many
 constexpr int kSmallCand = 512;   // band ranked in smem by counting up to this size
@@ -117,11 +121,11 @@ __device__ __forceinline__ void select_head(
     uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap) {
     using T = typename Elem<DT>::T;
-    // dynamic smem: keys[keys_cap] f32 | hist[kBins] | q[D] f64 | ck[kSmallCand] | ci[kSmallCand]
+    // dynamic smem: keys[keys_cap] f32 | hist[kHistWords] | q[D] f64 | ck[kSmallCand] | ci[kSmallCand]
     extern __shared__ __align__(16) unsigned char dsm[];
     float* s_keys = reinterpret_cast<float*>(dsm);
     int32_t* hist = reinterpret_cast<int32_t*>(dsm + (size_t)keys_cap * 4);
-    double* s_q = reinterpret_cast<double*>(hist + kBins);
+    double* s_q = reinterpret_cast<double*>(hist + kHistWords);
     uint64_t* ck = reinterpret_cast<uint64_t*>(s_q + D);
     uint32_t* ci = reinterpret_cast<uint32_t*>(ck + kSmallCand);
     __shared__ float red[2][kNW];
@@ -162,7 +166,7 @@ __device__ __forceinline__ void select_head(
 
     // everything that does not depend on the scorer first: q, the error bound,
     // the histogram; then the programmatic wait for the scorer's output
-    for (int i = t; i < kBins; i += kT) hist[i] = 0;
+    for (int i = t; i < kHistWords; i += kT) hist[i] = 0;
     if (t == 0) s_ncand = 0;
     for (int d = t; d < D; d += kT) s_q[d] = (double)qh[d];
     if (warp == 0) {
@@ -229,16 +233,16 @@ __device__ __forceinline__ void select_head(
         const float scale = (float)kBins / (gmx - gmn);
         for (int64_t i = t; i < nblk; i += kT) {
             const float f = (src[i] - gmn) * scale;
-            atomicAdd(&hist[f >= (float)(kBins - 1) ? kBins - 1 : (f <= 0.f ? 0 : (int)f)], 1);
+            atomicAdd(&hist[hidx(f >= (float)(kBins - 1) ? kBins - 1 : (f <= 0.f ? 0 : (int)f))], 1);
         }
         __syncthreads();
         // bin holding the k-th largest: each thread owns kBins/kT bins; suffix
         // sums over threads (from the top) locate the owner, which scans them
         constexpr int PB = kBins / kT;
         static_assert(PB == 8, "two 16-byte reads per thread");
-        const int4 h0 = reinterpret_cast<const int4*>(hist)[2 * t];  // 16-byte reads: no bank conflicts
-        const int4 h1 = reinterpret_cast<const int4*>(hist)[2 * t + 1];
-        const int hb[PB] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        int hb[PB];  // this thread's 8 consecutive bins (one padded row of 32 holds them)
+#pragma unroll
+        for (int i = 0; i < PB; ++i) hb[i] = hist[hidx(t * PB + i)];
         int c = 0;
 #pragma unroll
         for (int i = 0; i < PB; ++i) c += hb[i];
@@ -327,7 +331,7 @@ __device__ __forceinline__ void select_head(
     // (8 dims each) hit 16 distinct bank pairs; odd candidate pitch, so the
     // serial readers (one candidate each) spread over the banks too
     const int tpitch = (D / 8) * 9 + 1;  // doubles
-    const int per_round_t = ((int)((size_t)keys_cap * 4 + kBins * 4)) / (tpitch * 8);
+    const int per_round_t = ((int)((size_t)keys_cap * 4 + kHistWords * 4)) / (tpitch * 8);
     if (kTerms && (D & 7) == 0 && per_round_t >= 1) {
         double* term = reinterpret_cast<double*>(dsm);
         const int v8 = D / 8;
@@ -380,7 +384,7 @@ __device__ __forceinline__ void select_head(
     } else {
         const int row_b = 2 * D * (int)sizeof(T);
         const int pitch = row_b + 16;  // 16-byte skew: conflict-free row-parallel reads
-        const int per_round = ((int)((size_t)keys_cap * 4 + kBins * 4)) / pitch;
+        const int per_round = ((int)((size_t)keys_cap * 4 + kHistWords * 4)) / pitch;
         const bool vec = (row_b & 15) == 0 && per_round >= 1;
         unsigned char* stage = dsm;
         for (int64_t c0 = 0; c0 < n_cand; c0 += (vec ? per_round : n_cand)) {
@@ -540,7 +544,7 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
     const int64_t heads = (int64_t)L.batch * L.kv_heads * L.group_size;
     const int64_t nmax = level_blocks(L.l_cpu, 16);
     const int keys_cap = (int)((std::min<int64_t>(nmax, kSmemKeys) + 3) & ~int64_t(3));
-    size_t smem = (size_t)keys_cap * 4 + (size_t)kBins * 4 + (size_t)L.head_dim * 8 +
+    size_t smem = (size_t)keys_cap * 4 + (size_t)kHistWords * 4 + (size_t)L.head_dim * 8 +
                   (size_t)kSmallCand * 12;
     WorklistArgs w{};
     if (wl) {

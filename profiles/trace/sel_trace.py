@@ -4,12 +4,13 @@ os.environ["FLUXATTN_B200_LIB"] = os.path.join(os.path.dirname(os.path.abspath(_
 from paper_2605_07719_b200 import _native as N
 from paper_2605_07719_b200.fluxattn import Engine, SparseDecoder
 eng = Engine(0); dev = eng.device
-B, HKV, G, D = 16, 8, 4, 128
-ctx = 131072; l_cpu = ctx - 320
+# shape from the environment (default C2; C3: SEL_B=8 SEL_HKV=4 SEL_G=7 SEL_CTX=262144)
+B, HKV, G, D = int(os.environ.get("SEL_B", 16)), int(os.environ.get("SEL_HKV", 8)), int(os.environ.get("SEL_G", 4)), 128
+ctx = int(os.environ.get("SEL_CTX", 131072)); l_cpu = ctx - 320
 dec = SparseDecoder(eng, B, HKV, G, D, 64, l_cpu, 256, max_new=64, dtype="bf16")
 dec.k.normal_(); dec.v.normal_(); dec.build_metadata()
 rng = np.random.default_rng(1)
-H = 32
+H = HKV * G
 props = tuple(torch.as_tensor(x, device=dev) for x in (rng.uniform(0.01, 0.05, (B, H)), rng.uniform(0, 0.01, (B, H)), (rng.random((B, H)) < 0.5).astype(np.int32)))
 q = torch.randn((B, H, D), device=dev)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -23,8 +24,8 @@ torch.cuda.synchronize()
 print("step ms %.3f" % ev[0].elapsed_time(ev[1]))
 tr = np.zeros(16 * 8192, np.int64)
 N.LIB.fx_debug_sel_trace.argtypes = [C.c_void_p, C.c_int]
-N.LIB.fx_debug_sel_trace(tr.ctypes.data, 16 * 512)
-t = tr[:16 * 512].reshape(512, 16)
+N.LIB.fx_debug_sel_trace(tr.ctypes.data, 16 * B * H)
+t = tr[:16 * B * H].reshape(B * H, 16)
 t0 = t[:, 10].min()
 print("kernel CTA start spread (us): %.2f" % ((t[:, 10].max() - t0) / 1e3))
 print("select_head end (us): median %.2f max %.2f" % (np.median(t[:, 11] - t0) / 1e3, (t[:, 11].max() - t0) / 1e3))
