@@ -216,7 +216,9 @@ FX_API int fx_blocks_for_budget(fx_ctx* ctx, int32_t n, const double* budgets, c
 
 typedef struct fx_model fx_model;
 /* Upload a 41->256->384->3 predictor: weights row-major [out][in] f64 and the
- * 41 (mu, sigma) normalization pairs, all [host]. */
+ * 41 (mu, sigma) normalization pairs, all [host].  A model holds device scratch
+ * (hidden activations, per-row-tile counters of its layer-2 kernel): use it
+ * from one stream at a time. */
 FX_API int fx_model_create(fx_ctx* ctx, const double* w1, const double* b1, const double* w2,
                     const double* b2, const double* w3, const double* b3, const double* mu,
                     const double* sigma, fx_model** out);

@@ -20,6 +20,6 @@ ncu --set full --import-source on --clock-control none -k regex:'k_attend|k_scor
 ncu --set full --import-source on --clock-control none -k regex:'k_attend|k_score|k_select|k_prepare|k_merge_units' -s 55 -c 5 \
     -o $O/step_fixed16 python bench.py --quick --plan fixed16 --steps 8 --warmup 3 > $O/step_fixed16_quick.json 2> $O/step_fixed16.err
 ncu --set full --clock-control none -k regex:k_meta_stream -c 1 -o $O/meta python bench.py --quick --steps 2 --warmup 3 > /dev/null 2> $O/meta.err
-ncu --set full --import-source on --clock-control none -k regex:'k_feat|k_mlp' -s 8 -c 4 -o $O/pred python profiles/pred_profile.py 4 > /dev/null 2> $O/pred.err
+ncu --set full --import-source on --clock-control none -k regex:"k_feat|k_mlp" -s 6 -c 3 -o $O/pred python profiles/pred_profile.py 4 > /dev/null 2> $O/pred.err
 python profiles/pred_timing.py > $O/pred_timing.json 2> $O/pred_timing.err
 ls -la $O
