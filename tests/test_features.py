@@ -130,7 +130,8 @@ def test_predictor_driven_plan(engine, coracle):
 
 @pytest.mark.parametrize("Hkv,G,D,n_new,via_append", [
     (2, 4, 128, 3, False), (4, 7, 128, 0, False), (1, 4, 64, 5, False), (8, 4, 128, 1, False),
-    (3, 2, 64, 5, False), (2, 4, 128, 66, True), (2, 8, 128, 1, True), (2, 4, 64, 64, True)])
+    (3, 2, 64, 5, False), (2, 4, 128, 66, True), (2, 8, 128, 1, True), (2, 4, 64, 64, True),
+    (1, 4, 128, 1100, True)])  # 1100 decoded rows: more chunks than the merge keeps in registers
 def test_fused_predict_props(engine, coracle, Hkv, G, D, n_new, via_append):
     """fx_predict_props (decode features as 64-row chunk partials + a clustered
     merge, normalize, MLP): features within 1e-9 of the oracle (cross-head max
