@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
 // DC / GC > 0: head dim / group size fixed at compile time (the f32 decode
 // path of config C1): index arithmetic folds, the loops unroll.
 template <int DT, int DC = 0, int GC = 0>
-__global__ void __launch_bounds__(kGen, 4) k_attend_generic(const View p) {
+__global__ void __launch_bounds__(kGen, 8) k_attend_generic(const View p) {
     pdl_wait();
     pdl_trigger();
     using T = typename Elem<DT>::T;
@@ -1022,7 +1022,7 @@ done:
 // each thread folds one float4 column over a fixed subset of the contributors
 // (eight loads in flight), subsets combined in a fixed order: deterministic.
 constexpr int kMergeRunThreads = 256;
-constexpr int kMaxMergeList = 1024;  // contributors of one run (>= the generic grid, 4 per SM)
+constexpr int kMaxMergeList = 2048;  // contributors of one run (>= the generic grid, 8 per SM)
 __global__ void __launch_bounds__(kMergeRunThreads) k_merge_runs(const View p, int grid) {
     pdl_wait();
     pdl_trigger();
@@ -1308,7 +1308,7 @@ bool attend_uses_tma(const fx_layout& L, bool has_idx) {
 }
 
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms) {
-    return attend_uses_tma(L, has_idx) ? num_sms : num_sms * 4;
+    return attend_uses_tma(L, has_idx) ? num_sms : num_sms * 8;
 }
 
 int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
