@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
 
 #ifdef FX_TRACE  // profiling build only: per-CTA start/end time, units, tiles
 __device__ long long g_trace[12 * 2048];
+__device__ long long g_gtrace[8 * 2048];  // generic kernel: per-CTA phase times
 __device__ __forceinline__ long long globaltimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -790,8 +791,15 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
 // path of config C1): index arithmetic folds, the loops unroll.
 template <int DT, int DC = 0, int GC = 0>
 __global__ void __launch_bounds__(kGen, 8) k_attend_generic(const View p) {
+#ifdef FX_TRACE
+#define GT_MARK(i) if (threadIdx.x == 0 && blockIdx.x < 2048) g_gtrace[blockIdx.x * 8 + (i)] = globaltimer()
+#else
+#define GT_MARK(i)
+#endif
+    GT_MARK(0);
     pdl_wait();
     pdl_trigger();
+    GT_MARK(1);
     using T = typename Elem<DT>::T;
     extern __shared__ float gsm[];
     const int t = threadIdx.x;
@@ -811,6 +819,7 @@ __global__ void __launch_bounds__(kGen, 8) k_attend_generic(const View p) {
     __shared__ int32_t s_start[kMaxPrefix + 1];
     __shared__ int s_wtmp[kGen / 32];
     const int32_t* starts = run_starts(p, s_start, s_wtmp, t, kGen);
+    GT_MARK(2);
     const int grid = gridDim.x, cta = blockIdx.x;
     const int64_t NB = starts[p.n_bg];
     const int64_t r0 = NB * cta / grid, r1 = NB * (cta + 1) / grid;
@@ -929,6 +938,7 @@ __global__ void __launch_bounds__(kGen, 8) k_attend_generic(const View p) {
             if (next_real(x, bg, e_bg, nx, nbg, nsbg)) load_box(box_of(nx, nbg, nsbg), nbg);
         }
         __syncthreads();
+        if (x == r0) GT_MARK(3);
         for (int pi = t / TPP; pi < pairs; pi += kGen / TPP) {
             const int tok = pi / G, h = pi % G, sub = t % TPP;
             float a = 0.f;
@@ -1013,6 +1023,7 @@ __global__ void __launch_bounds__(kGen, 8) k_attend_generic(const View p) {
 done:
     __syncthreads();
     write_empty_runs(p, starts, r0, r1, t, kGen);
+    GT_MARK(5);
     // runs cut by a range end left partials: k_merge_runs follows
 }
 
@@ -1399,5 +1410,8 @@ void launch_convert(const float* src, void* dst, int dtype, size_t n, cudaStream
 #ifdef FX_TRACE
 extern "C" FX_API int fx_debug_trace(long long* out, int n) {
     return cudaMemcpyFromSymbol(out, fx::g_trace, sizeof(long long) * n) == cudaSuccess ? 0 : -2;
+}
+extern "C" FX_API int fx_debug_gtrace(long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, fx::g_gtrace, sizeof(long long) * n) == cudaSuccess ? 0 : -2;
 }
 #endif
