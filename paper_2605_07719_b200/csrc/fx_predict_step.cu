@@ -1,6 +1,6 @@
 // fx_predict_step.cu -- decode features of every head (features.cpp:162-224)
-// as two short kernels; fx_predict_props then runs the tiled predictor
-// (fx_plan.cu) on them: features -> normalize -> 41-256-384-3 -> head
+// as two short kernels; fx_predict_props then runs the predictor's remaining
+// layers (fx_plan.cu): features -> normalize -> 41-256-384-3 -> head
 // properties (pipeline.cpp:277-290), which the decode step plans from.
 //
 // The per-step work of decode_features is the f64 attention of every head
@@ -9,21 +9,24 @@
 // cross-head maximum output norm of feature 39 (gpu_output_norm,
 // features.cpp:80-83, pipeline.cpp:279-282).  It is FP64-bound (~2 G D f64
 // multiply-adds per row and head group), so it is spread over the machine:
-//   k_feat_part   one CTA per 64-row chunk of one segment of one (b, g):
-//                 the chunk's K and V arrive by two 1-D bulk copies; f64
+//   k_feat_part   a persistent grid (3 CTAs of 128 threads per SM) walking
+//                 contiguous ranges of (b, g, 64-row chunk) items; per item
+//                 the chunk's K and V arrive by two 1-D bulk copies (a
+//                 2-stage ring: the next item streams in meanwhile); f64
 //                 scores of the G heads (lanes split D, q slice in registers,
-//                 butterfly sum), the chunk max m, weights e = exp(s - m),
-//                 z = sum e and sum e v (f64) -> one partial per (chunk, head).
-//                 With an append, the CTA holding the appended row writes it
-//                 to the cache and patches its staged copy (the previous
-//                 token, append_new after a step, pipeline.cpp:406-412).
+//                 a head-splitting butterfly), the chunk max m, weights
+//                 e = exp(s - m), z = sum e and sum e v -> one partial per
+//                 (item, head).  With an append, the CTA holding the appended
+//                 row writes it to the cache and patches its staged copy (the
+//                 previous token, append_new after a step, pipeline.cpp:406-412).
 //   k_feat_final  one CTA per (b, g), the sequence's Hkv CTAs in a cluster:
-//                 a warp per head merges its chunk partials per segment
-//                 (lse, output, norm), merges the segments in order
-//                 (merge_into, attention.cpp:89-104), forms the 41 features,
-//                 and the cluster exchanges the per-sequence maximum of the
-//                 default output norms (feature 39) through distributed
-//                 shared memory.
+//                 the chunk partials merged per segment over all threads
+//                 (lse, output, norm), the segments merged in order
+//                 (merge_into, attention.cpp:89-104), the 41 features (lane i
+//                 forms feature i), the per-sequence maximum of the default
+//                 output norms (feature 39) exchanged through distributed
+//                 shared memory; with a model, the normalization and the
+//                 predictor's first layer for the CTA's G rows.
 // Results agree with the reference within 1e-9 relative (sums associate
 // differently), like fx_decode_features.
 #include <algorithm>
