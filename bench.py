@@ -34,6 +34,7 @@ per step.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import socket
@@ -762,7 +763,7 @@ def run_ours(a):
 
     B, H, HKV, G = a.batch, a.heads, a.hkv, a.G
     l_cpu = a.context - L_SINK - L_LOCAL
-    total_steps = 2 * a.warmup + 5 * a.steps + 60  # timed, graph replay, timing pass, e2e, predictor (+ its split)
+    total_steps = 2 * a.warmup + 5 * a.steps + 60 + (200 if os.environ.get("FX_BENCH_PRED_DIAG") else 0)
     eng = Engine(local)
     tdt = torch.bfloat16 if a.kv_dtype == "bf16" else torch.float32
     gen = torch.Generator(device=dev)
@@ -1100,6 +1101,39 @@ def run_ours(a):
         t1.record()
         torch.cuda.synchronize()
         pms = max_over_ranks(t0.elapsed_time(t1))
+        if os.environ.get("FX_BENCH_PRED_DIAG"):  # loop-structure diagnostics (stderr)
+            def loop_ms(fn, n=40):
+                torch.cuda.synchronize()
+                t0.record()
+                for _ in range(n):
+                    fn()
+                t1.record()
+                torch.cuda.synchronize()
+                return t0.elapsed_time(t1) / n
+
+            def step_noappend():
+                i = step_i[0]
+                dec.step(qs[i], props=dec.predict_props(qs[i], rec, pred))
+                step_i[0] += 1
+
+            def step_split_append():
+                i = step_i[0]
+                dec.append(kv_new[i - 1, 0], kv_new[i - 1, 1])
+                dec.step(qs[i], props=dec.predict_props(qs[i], rec, pred))
+                step_i[0] += 1
+
+            def props_only():
+                i = step_i[0]
+                dec.predict_props(qs[i], rec, pred)
+
+            def step_only():
+                i = step_i[0]
+                dec.step(qs[i], props=pp)
+
+            for nm, fn in [("pred_step", pred_step), ("no_append", step_noappend),
+                           ("separate_append", step_split_append), ("props_only", props_only),
+                           ("step_only", step_only), ("pred_step_again", pred_step)]:
+                print(f"pred diag {nm}: {loop_ms(fn):.4f} ms/iter (l_new {dec.l_new})", file=sys.stderr, flush=True)
         # per-step split of 40 more steps (events around each call, synchronized
         # per step): the plan the predictor produces changes with the decoded rows
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -1230,6 +1264,11 @@ def main():
             env.setdefault("NCCL_DEBUG", "INFO")
             env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         sys.exit(subprocess.call(cmd, env=env))
+    # Python's cyclic collector off for the run: a gen-2 pass inside an
+    # unsynchronized timed loop stalls the launching thread and drains the GPU
+    # (reference counting still frees everything the loops allocate)
+    gc.collect()
+    gc.disable()
     if a.dry_run_launch:
         run_dry_launch(a)
         return
