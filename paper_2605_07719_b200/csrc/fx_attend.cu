@@ -673,6 +673,24 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
                     }
                 }
             }
+            // V fragments into registers now, so the stage goes back to the
+            // producer before the softmax and the PV products (it refills
+            // the ring a few hundred cycles earlier every tile)
+            uint32_t vfa[C::NT][4], vfb[C::NT][4];
+            {
+                const uint32_t va = ka + C::KV_BYTES, vb2 = kb2 + C::KV_BYTES;
+                const int mi = lane >> 3;
+                const int r = (lane & 7) + (mi >> 1) * 8;
+#pragma unroll
+                for (int i = 0; i < C::NT; ++i) {
+                    const int u = ((i & 3) << 1) + (mi & 1);
+                    const uint32_t off = r * 128 + ((u ^ (r & 7)) << 4);
+                    ldsm_x4_t(va + (i >> 2) * csa + off, vfa[i][0], vfa[i][1], vfa[i][2], vfa[i][3]);
+                    if (two) ldsm_x4_t(vb2 + (i >> 2) * csb + off, vfb[i][0], vfb[i][1], vfb[i][2], vfb[i][3]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + st);
             // scores (log2 domain), masked by token validity and head selection
             float s[2][4];
             {
@@ -715,28 +733,19 @@ __global__ void __launch_bounds__(kQThreads, 1) k_attend_tma(const __grid_consta
             m1 = n1;
             const uint32_t pa0 = movmatrix_t(x[0][0]), pa1 = movmatrix_t(x[0][1]);
             const uint32_t pb0 = movmatrix_t(x[1][0]), pb1 = movmatrix_t(x[1][1]);
-            const uint32_t va = ka + C::KV_BYTES, vb2 = kb2 + C::KV_BYTES;
-            const int mi = lane >> 3;
-            const int r = (lane & 7) + (mi >> 1) * 8;
 #pragma unroll
             for (int i = 0; i < C::NT; ++i) {
                 O[i][0] *= al0;
                 O[i][1] *= al1;
                 O[i][2] *= al0;
                 O[i][3] *= al1;
-                const int u = ((i & 3) << 1) + (mi & 1);
-                const uint32_t off = r * 128 + ((u ^ (r & 7)) << 4);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(va + (i >> 2) * csa + off, a0, a1, a2, a3);
-                mma_bf16_16816(O[i], a0, a1, a2, a3, pa0, pa1);
-                if (two) {
-                    ldsm_x4_t(vb2 + (i >> 2) * csb + off, a0, a1, a2, a3);
-                    mma_bf16_16816(O[i], a0, a1, a2, a3, pb0, pb1);
-                }
+                mma_bf16_16816(O[i], vfa[i][0], vfa[i][1], vfa[i][2], vfa[i][3], pa0, pa1);
+                if (two) mma_bf16_16816(O[i], vfb[i][0], vfb[i][1], vfb[i][2], vfb[i][3], pb0, pb1);
             }
+        } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + st);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + st);
         if (flags & F_LAST) {
             // ---- unit end: hand this warp's state to the epilogue warp ----
             float t0 = l0, t1 = l1;
