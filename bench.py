@@ -1168,6 +1168,11 @@ def run_ours(a):
         pstep_ms = t0.elapsed_time(t1) / nrep
         stream_frac = float(pp[2].float().mean().item())
         retr_groups = int((dec.plan_blk > 0).sum().item())
+        # bytes of the step on the predictor's plan (same formula as
+        # step_bytes): the predictor's plan is a different, heavier plan than the
+        # drawn properties' (more retrieval heads), so compare HBM fractions
+        pmb, pab = algorithmic_bytes(dec)
+        ppeak, _ = peaks()
         result["predictor_path"] = {
             "value": world * a.steps / (pms / 1e3), "unit": UNIT, "ms_per_step": pms / a.steps,
             "predict_props_ms": props_ms, "decode_step_ms": pstep_ms, "decoded_rows": dec.l_new,
@@ -1178,6 +1183,8 @@ def run_ours(a):
                                "retrieval_groups_min": int(split[:, 2].min()),
                                "retrieval_groups_max": int(split[:, 2].max())},
             "retrieval_groups": retr_groups,
+            "decode_step_bytes": pmb + pab,
+            "decode_step_frac_of_peak": (pmb + pab) / (pstep_ms * 1e-3) / 1e9 / ppeak,
             "prefill_stats_ms": prefill_ms, "streaming_frac": stream_frac,
             "per_step": "fx_predict_props (previous token appended; decode features as chunk "
                         "partials + one clustered merge with layer 1; layers 2 + 3) + fx_decode_step",
