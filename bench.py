@@ -796,8 +796,10 @@ def run_ours(a):
         del out
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dec.build_metadata()  # first call: module load (lazy loading) and attribute setup
+    torch.cuda.synchronize()
     e0.record()
-    dec.build_metadata()
+    dec.build_metadata()  # timed: the same levels rebuilt from the same K
     e1.record()
     torch.cuda.synchronize()
     meta_build_ms = e0.elapsed_time(e1)

@@ -23,3 +23,8 @@ ncu --set full --clock-control none -k regex:k_meta_stream -c 1 -o $O/meta pytho
 ncu --set full --import-source on --clock-control none -k regex:"k_feat|k_mlp" -s 6 -c 3 -o $O/pred python profiles/pred_profile.py 4 > /dev/null 2> $O/pred.err
 python profiles/pred_timing.py > $O/pred_timing.json 2> $O/pred_timing.err
 ls -la $O
+# compute-sanitizer over the small end-to-end run (profiles/sanitizer/README.md)
+for t in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $t --print-limit 50 python profiles/sanitizer/small_step.py > $O/san_$t.log 2>&1
+  tail -2 $O/san_$t.log
+done
