@@ -956,7 +956,8 @@ def run_ours(a):
         tag = a.workload if a.plan == WORKLOADS[a.workload]["plan"] else f"{a.workload}_{a.plan}"
         tr = ncu_traffic("k_attend", tag)
         kname = ("k_attend_tma (K3 with its per-unit epilogue; the unit-partial merge kernel is "
-                 "kernels_ms.merge)") if a.kv_dtype == "bf16" else "k_attend_generic (K3+K4, f32)"
+                 "kernels_ms.merge)") if a.kv_dtype == "bf16" else ("k_attend_f32w (K3, f32 warp streams; the "
+                                                                    "chunk merge is kernels_ms.merge)")
         result["roofline"] = {"bound": "hbm", "kernel": kname,
                               "achieved": achieved, "peak": peak, "unit": "GB/s",
                               "frac": achieved / peak, "peak_kind": peak_kind,

@@ -224,32 +224,20 @@ struct TmaCfg {
     static constexpr size_t TOTAL = WL + kCWarps * 8 * sizeof(float) + 1024;  // + align slack
 };
 
-// Merge of the unit partials of every multi-unit group (attention.cpp:89-104
-// across the units, in unit order): one 128-thread CTA per (b, g, head),
-// launched behind the attention kernel (PDL) -- small CTAs, so every group's
-// heads merge at once even with thousands of groups (C4).  Each thread owns
-// one float4 column of a fixed subset of the units (eight units' loads in
-// flight), the subsets are combined in a fixed order: deterministic.
 constexpr int kMergeThreads = 128;
-__global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, int D,
-                                                              const int32_t* __restrict__ bg_count,
-                                                              const int32_t* __restrict__ ubase,
-                                                              const float* __restrict__ part_o,
-                                                              const float* __restrict__ part_lse,
-                                                              float* __restrict__ o, float* __restrict__ lse) {
-    pdl_wait();
-    pdl_trigger();
-    const int bg = blockIdx.x, h = blockIdx.y, t = threadIdx.x;
-    const int total = __ldg(bg_count + bg);
-    const int nun = total > 0 ? (total + kUnitBoxes - 1) / kUnitBoxes : 1;
-    if (nun <= 1) return;  // written final by the attention kernel
-    const int base = __ldg(ubase + bg);
+// Fold the partials at slots [base, base + nun) of head h into (o, lse): the
+// max of the slot LSEs, then each thread owns one float4 column of a fixed
+// subset of the slots (eight slots' loads in flight), the subsets combined in
+// a fixed order: deterministic.  All kMergeThreads threads.
+__device__ void merge_slots(int G, int D, int h, int base, int nun, const float* __restrict__ part_o,
+                            const float* __restrict__ part_lse, float* __restrict__ o_dst,
+                            float* __restrict__ lse_dst) {
+    const int t = threadIdx.x;
     const int VP = D / 4;                   // float4 columns of the head
-    const int S = kMergeThreads / VP;       // unit subsets (D <= 512)
+    const int S = kMergeThreads / VP;       // slot subsets (D <= 512)
     __shared__ float s_wm[kMergeThreads / 32];
     __shared__ float4 s_acc[kMergeThreads];
     __shared__ float s_den[kMergeThreads];
-    // the head's max of the unit LSEs
     float m = -INFINITY;
     for (int i = t; i < nun; i += kMergeThreads) m = fmaxf(m, __ldg(part_lse + (int64_t)(base + i) * G + h));
     m = warp_max(m);
@@ -298,11 +286,30 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
         acc.w += a.w;
         den += s_den[k * VP + v];
     }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    *reinterpret_cast<float4*>(o_dst + v * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (v == 0 && lse_dst) *lse_dst = den > 0.f ? M + __logf(den) : -INFINITY;
+}
+
+// Merge of the unit partials of every multi-unit group (attention.cpp:89-104
+// across the units, in unit order): one 128-thread CTA per (b, g, head),
+// launched behind the attention kernel (PDL) -- small CTAs, so every group's
+// heads merge at once even with thousands of groups (C4).
+__global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, int D,
+                                                              const int32_t* __restrict__ bg_count,
+                                                              const int32_t* __restrict__ ubase,
+                                                              const float* __restrict__ part_o,
+                                                              const float* __restrict__ part_lse,
+                                                              float* __restrict__ o, float* __restrict__ lse) {
+    pdl_wait();
+    pdl_trigger();
+    const int bg = blockIdx.x, h = blockIdx.y;
+    const int total = __ldg(bg_count + bg);
+    const int nun = total > 0 ? (total + kUnitBoxes - 1) / kUnitBoxes : 1;
+    if (nun <= 1) return;  // written final by the attention kernel
     const int b = bg / Hkv, g = bg % Hkv;
     const int64_t hd = (int64_t)b * Hkv * G + (int64_t)g * G + h;
-    const float inv = den > 0.f ? 1.f / den : 0.f;
-    *reinterpret_cast<float4*>(o + hd * D + v * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    if (v == 0 && lse) lse[hd] = den > 0.f ? M + __logf(den) : -INFINITY;
+    merge_slots(G, D, h, __ldg(ubase + bg), nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
 }
 
 #ifdef FX_TRACE  // profiling build only: per-CTA start/end time, units, tiles
@@ -1036,6 +1043,285 @@ done:
     // runs cut by a range end left partials: k_merge_runs follows
 }
 
+// ---------------------------------------------------------------------------
+// f32 kernel with per-warp box streams (contiguous boxes, the decode path of
+// config C1: f32 KV, D 64 / 128, G in {4, 7, 8})
+// ---------------------------------------------------------------------------
+// Every run (b, g) is cut into chunks of kFChunk consecutive boxes from its
+// start; chunk k of the batch (runs in order) goes to warp k % (grid * kFW)
+// of one CTA per SM, through a private ring of 1-D bulk copies (the K and V
+// rows of a box are contiguous), so a box costs no CTA barrier and the warp's
+// stream continues across its chunks.  Per box: QK with lane = (row, half of
+// the dims), the row softmax by shuffles (exp2 domain), PV with lane = D/32
+// dims.  A chunk's (o, lse) is a partial in chunk slot k (final when the run
+// has one chunk); k_merge_chunks folds a run's chunks in chunk order.  The
+// cut points depend only on the run, so a result does not depend on the other
+// runs of the batch (the drop-in arena's batch sizes).
+constexpr int kFW = 6;       // warps per CTA
+constexpr int kFStages = 2;  // boxes in flight per warp
+constexpr int kFChunk = 4;   // boxes per chunk
+
+bool f32w_supported(const fx_layout& L, bool has_idx) {
+    return !has_idx && L.dtype == FX_F32 && (L.head_dim == 128 || L.head_dim == 64) &&
+           (L.group_size == 4 || L.group_size == 7 || L.group_size == 8) &&
+           L.batch * L.kv_heads <= kMaxPrefix;
+}
+
+// Chunk prefix of the runs in smem (n_bg <= kMaxPrefix): cstart[bg] = first
+// chunk of run bg, cstart[n_bg] = the total.  All threads; ends in a barrier.
+__device__ const int32_t* chunk_starts(const int32_t* bg_count, int n_bg, int32_t* cs, int* wtmp, int t, int nt) {
+    const int lane = t & 31, warp = t >> 5, nw = nt >> 5;
+    int carry = 0;
+    for (int c0 = 0; c0 < n_bg; c0 += nt) {
+        const int i = c0 + t;
+        const int v = i < n_bg ? (__ldcg(bg_count + i) + kFChunk - 1) / kFChunk : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wtmp[warp] = x;
+        __syncthreads();
+        int off = carry, tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) off += wtmp[w];
+            tot += wtmp[w];
+        }
+        if (i < n_bg) cs[i] = off + x - v;
+        __syncthreads();
+        carry += tot;
+    }
+    if (t == 0) cs[n_bg] = carry;
+    __syncthreads();
+    return cs;
+}
+
+template <int D>
+struct F32wCfg {
+    static constexpr int BOXF = kBoxRows * D;  // floats of one box of K (or V)
+    static constexpr size_t BAR = 0;
+    static constexpr size_t RING = 128;
+    static constexpr size_t QS = RING + (size_t)kFW * kFStages * 2 * BOXF * 4;
+    static size_t total(int G) { return QS + (size_t)kFW * G * D * 4; }
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(kFW * 32, 1) k_attend_f32w(const View p) {
+    GT_MARK(0);
+    pdl_wait();
+    pdl_trigger();
+    GT_MARK(1);
+    using C = F32wCfg<D>;
+    constexpr int DL = D / 32;  // PV: dims per lane
+    constexpr int Q4 = D / 8;   // QK: float4s per half row
+    extern __shared__ __align__(128) unsigned char fsm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(fsm + C::BAR);
+    __shared__ int32_t s_cs[kMaxPrefix + 1];
+    __shared__ int s_wtmp[kFW];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (t < kFW * kFStages) mbar_init(bars + t, 1);
+    fence_mbar_init();
+    const int32_t* cs = chunk_starts(p.bg_count, p.n_bg, s_cs, s_wtmp, t, kFW * 32);  // + barrier
+    GT_MARK(2);
+    const int NC = cs[p.n_bg];
+    const int W = gridDim.x * kFW;            // warps of the grid
+    const int w0 = blockIdx.x * kFW + warp;   // this warp's chunks: w0, w0 + W, ...
+    const float sl2 = rsqrtf((float)D) * kLog2e;
+    uint64_t* wbar = bars + warp * kFStages;
+    float* wring = reinterpret_cast<float*>(fsm + C::RING) + (size_t)warp * kFStages * 2 * C::BOXF;
+    float* wq = reinterpret_cast<float*>(fsm + C::QS) + (size_t)warp * G * D;
+    // a cursor over this warp's boxes: chunk k, its run bg, box x of [x0, x1)
+    struct Cur {
+        int k, bg, x, x1;
+    };
+    auto chunk_at = [&](int k, Cur& c) -> bool {
+        c.k = k;
+        if (k >= NC) return false;
+        int lo = 0, hi = p.n_bg - 1;  // last run whose first chunk is <= k
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cs[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
+        c.bg = lo;
+        c.x = (k - cs[lo]) * kFChunk;
+        c.x1 = min(c.x + kFChunk, __ldcg(p.bg_count + lo));
+        return true;
+    };
+    auto advance = [&](Cur& c) -> bool {  // next box of this warp's stream
+        if (++c.x < c.x1) return true;
+        return chunk_at(c.k + W, c);
+    };
+    auto issue = [&](const Cur& c, uint32_t slot) {  // lane 0
+        const Box bx = p.boxes[(int64_t)c.bg * p.box_stride + c.x];
+        const int st = (int)(slot % kFStages);
+        float* kt = wring + (size_t)st * 2 * C::BOXF;
+        const uint32_t bytes = (uint32_t)bx.n * D * 4;
+        const int64_t row = (int64_t)c.bg * p.l_cap + bx.row;
+        fence_proxy_async();  // this warp's earlier reads of the slot before the async writes
+        mbar_arrive_expect_tx(wbar + st, 2 * bytes);
+        bulk_g2s(kt, static_cast<const float*>(p.k) + row * D, bytes, wbar + st);
+        bulk_g2s(kt + C::BOXF, static_cast<const float*>(p.v) + row * D, bytes, wbar + st);
+    };
+    Cur cur, pre;
+    bool have = chunk_at(w0, cur);
+    pre = cur;
+    bool pre_ok = have;
+    uint32_t issued = 0;  // (lane 0) boxes issued into the ring so far
+    if (lane == 0)
+        for (; pre_ok && issued < (uint32_t)kFStages; ++issued) {
+            issue(pre, issued);
+            pre_ok = advance(pre);
+        }
+    const int r = lane >> 1, hf = lane & 1;
+    uint32_t slot = 0;
+    bool marked = false;
+    while (have) {
+        // ---- one chunk: q of its group, then its boxes ----
+        const int bg = cur.bg, k = cur.k;
+        {
+            const int bb = bg / p.Hkv, g = bg % p.Hkv;
+            const float4* qp = reinterpret_cast<const float4*>(p.q + ((int64_t)bb * p.Hkv * G + (int64_t)g * G) * D);
+            __syncwarp();
+            for (int e = lane; e < G * D / 4; e += 32) reinterpret_cast<float4*>(wq)[e] = qp[e];
+            __syncwarp();
+        }
+        float m[G], l[G], acc[G][DL];
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            m[h] = -INFINITY;
+            l[h] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < DL; ++kk) acc[h][kk] = 0.f;
+        }
+        bool more = true;
+        while (more) {
+            const Box bx = p.boxes[(int64_t)bg * p.box_stride + cur.x];
+            const int st = (int)(slot % kFStages);
+            mbar_wait(wbar + st, (slot / kFStages) & 1u);
+            if (!marked) {
+                if (warp == 0) GT_MARK(3);
+                marked = true;
+            }
+            const float* kt = wring + (size_t)st * 2 * C::BOXF;
+            const float* vt = kt + C::BOXF;
+            // QK: lane (row r, half hf) over D/2 dims, float4 reads rotated by lane
+            float sc[G];
+#pragma unroll
+            for (int h = 0; h < G; ++h) sc[h] = 0.f;
+            const bool rv = r < bx.n;  // rows past the box's end hold stale bytes: never read
+            if (rv) {
+                const float4* krow = reinterpret_cast<const float4*>(kt + r * D + hf * (D / 2));
+                const float4* qrow = reinterpret_cast<const float4*>(wq + hf * (D / 2));
+#pragma unroll
+                for (int j = 0; j < Q4; ++j) {
+                    const int jj = (j + lane) & (Q4 - 1);
+                    const float4 k4 = krow[jj];
+#pragma unroll
+                    for (int h = 0; h < G; ++h) {
+                        const float4 q4 = qrow[h * (D / 4) + jj];
+                        sc[h] = fmaf(q4.x, k4.x, sc[h]);
+                        sc[h] = fmaf(q4.y, k4.y, sc[h]);
+                        sc[h] = fmaf(q4.z, k4.z, sc[h]);
+                        sc[h] = fmaf(q4.w, k4.w, sc[h]);
+                    }
+                }
+            }
+            float pr[G];
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                float x = sc[h] + __shfl_xor_sync(0xffffffffu, sc[h], 1);
+                x = (rv && ((bx.mask >> h) & 1)) ? x * sl2 : -INFINITY;
+                // row softmax (16 rows: lanes 2r and 2r + 1 hold the same value)
+                float mx = x;
+#pragma unroll
+                for (int o = 2; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const float nm = fmaxf(m[h], mx);
+                const float base = nm == -INFINITY ? 0.f : nm;
+                const float al = nm == -INFINITY ? 1.f : exp2f(m[h] - nm);
+                pr[h] = exp2f(x - base);
+                float sum = pr[h];
+#pragma unroll
+                for (int o = 2; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                l[h] = l[h] * al + sum;
+                m[h] = nm;
+#pragma unroll
+                for (int kk = 0; kk < DL; ++kk) acc[h][kk] *= al;
+            }
+            // PV: lane owns dims [lane * DL, lane * DL + DL)
+#pragma unroll 4
+            for (int rr = 0; rr < kBoxRows; ++rr) {
+                if (rr >= bx.n) break;  // (warp-uniform)
+                float v[DL];
+                if constexpr (DL == 4) {
+                    const float4 v4 = reinterpret_cast<const float4*>(vt + rr * D)[lane];
+                    v[0] = v4.x, v[1] = v4.y, v[2] = v4.z, v[3] = v4.w;
+                } else {
+                    const float2 v2 = reinterpret_cast<const float2*>(vt + rr * D)[lane];
+                    v[0] = v2.x, v[1] = v2.y;
+                }
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    const float ph = __shfl_sync(0xffffffffu, pr[h], 2 * rr);
+#pragma unroll
+                    for (int kk = 0; kk < DL; ++kk) acc[h][kk] = fmaf(ph, v[kk], acc[h][kk]);
+                }
+            }
+            __syncwarp();  // every lane is done with the slot
+            ++slot;
+            if (lane == 0 && pre_ok) {  // refill the slot with the stream's next box
+                issue(pre, issued++);
+                pre_ok = advance(pre);
+            }
+            more = ++cur.x < cur.x1;
+        }
+        // ---- the chunk's (o, lse): final when its run has one chunk ----
+        const bool sole = cs[bg + 1] - cs[bg] == 1;
+        const int64_t head0 = sole ? (int64_t)(bg / p.Hkv) * p.Hkv * G + (int64_t)(bg % p.Hkv) * G
+                                   : (int64_t)k * G;
+        float* dst_o = sole ? p.o : p.part_o;
+        float* dst_l = sole ? p.lse : p.part_lse;
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            const float inv = l[h] > 0.f ? 1.f / l[h] : 0.f;
+            if constexpr (DL == 4)
+                reinterpret_cast<float4*>(dst_o + (head0 + h) * D)[lane] =
+                    make_float4(acc[h][0] * inv, acc[h][1] * inv, acc[h][2] * inv, acc[h][3] * inv);
+            else
+                reinterpret_cast<float2*>(dst_o + (head0 + h) * D)[lane] = make_float2(acc[h][0] * inv, acc[h][1] * inv);
+            if (lane == 0 && dst_l) dst_l[head0 + h] = l[h] > 0.f ? (m[h] + log2f(l[h])) * kLn2 : -INFINITY;
+        }
+        have = chunk_at(k + W, cur);
+    }
+    GT_MARK(5);
+}
+
+// Merge of a run's chunk partials (k_attend_f32w), in chunk order: one
+// 128-thread CTA per (b, g, head) as k_merge_units; a run with no boxes gets
+// the merge identity, a one-chunk run was written final.
+__global__ void __launch_bounds__(kMergeThreads) k_merge_chunks(int n_bg, int G, int D,
+                                                               const int32_t* __restrict__ bg_count,
+                                                               const float* __restrict__ part_o,
+                                                               const float* __restrict__ part_lse,
+                                                               float* __restrict__ o, float* __restrict__ lse) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ int32_t s_cs[kMaxPrefix + 1];
+    __shared__ int s_wtmp[kMergeThreads / 32];
+    const int bg = blockIdx.x, h = blockIdx.y, t = threadIdx.x;
+    const int32_t* cs = chunk_starts(bg_count, n_bg, s_cs, s_wtmp, t, kMergeThreads);
+    const int base = cs[bg], nun = cs[bg + 1] - cs[bg];
+    if (nun == 1) return;  // written final by the attention kernel
+    const int64_t hd = (int64_t)bg * G + h;  // (b, g, h) = b * Hkv * G + g * G + h
+    if (nun == 0) {
+        for (int d = t; d < D; d += kMergeThreads) o[hd * D + d] = 0.f;
+        if (t == 0 && lse) lse[hd] = -INFINITY;
+        return;
+    }
+    merge_slots(G, D, h, base, nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
+}
+
 // Merge of the partials of the generic kernel's runs cut by CTA range ends
 // (attention.cpp:89-104 across the contributing CTAs): one 256-thread CTA per
 // (b, g, head), launched behind it (PDL).  The contributors' LSEs first, then
@@ -1316,6 +1602,10 @@ CUtensorMap make_row_map(const void* base, int D, int64_t rows, int box_rows) {
     return m;
 }
 
+int64_t chunk_capacity(int64_t n_bg, int64_t box_stride) {
+    return n_bg * cdiv(std::max<int64_t>(box_stride, 1), kFChunk);
+}
+
 int64_t unit_capacity(int64_t n_bg, int64_t box_stride) {
     // every group's units at the worst case, plus the claims that run past the
     // tail (at most two per CTA)
@@ -1328,7 +1618,7 @@ bool attend_uses_tma(const fx_layout& L, bool has_idx) {
 }
 
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms) {
-    return attend_uses_tma(L, has_idx) ? num_sms : num_sms * 8;
+    return attend_uses_tma(L, has_idx) || f32w_supported(L, has_idx) ? num_sms : num_sms * 8;
 }
 
 int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
@@ -1349,6 +1639,19 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
         if (a.L.dtype == FX_BF16) {
             FX_CUDA(cudaFuncSetAttribute(k_attend_generic<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             launch_pdl(k_attend_generic<FX_BF16>, grid, kGen, smem, s, v);
+        } else if (f32w_supported(a.L, a.idx != nullptr)) {
+            using KernFn = void (*)(View);
+            KernFn kern = nullptr;
+            size_t fs = 0;
+            if (D == 128) {
+                fs = F32wCfg<128>::total(G);
+                kern = G == 4 ? k_attend_f32w<128, 4> : G == 7 ? k_attend_f32w<128, 7> : k_attend_f32w<128, 8>;
+            } else {
+                fs = F32wCfg<64>::total(G);
+                kern = G == 4 ? k_attend_f32w<64, 4> : G == 7 ? k_attend_f32w<64, 7> : k_attend_f32w<64, 8>;
+            }
+            FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs));
+            launch_pdl(kern, grid, kFW * 32, fs, s, v);
         } else {
             auto kern = k_attend_generic<FX_F32>;
             if (D == 128 && G == 4) kern = k_attend_generic<FX_F32, 128, 4>;
@@ -1364,6 +1667,14 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
 }
 
 int launch_unit_merge(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
+    if (!(allow_tma && attend_uses_tma(a.L, a.idx != nullptr)) && f32w_supported(a.L, a.idx != nullptr)) {
+        const int n_bg = a.L.batch * a.L.kv_heads;  // f32 warp streams: chunk partials
+        launch_pdl(k_merge_chunks, dim3((unsigned)n_bg, (unsigned)a.L.group_size), kMergeThreads, 0, s, n_bg,
+                   a.L.group_size, a.L.head_dim, (const int32_t*)a.bg_count, (const float*)a.part_o,
+                   (const float*)a.part_lse, a.o, a.lse);
+        FX_CUDA(cudaGetLastError());
+        return 1;
+    }
     if (!allow_tma || !attend_uses_tma(a.L, a.idx != nullptr)) {  // generic kernel: cut runs
         FX_REQUIRE(grid <= kMaxMergeList, FX_ERR_INVALID, "bad-shape: attention grid too large for the run merge");
         launch_pdl(k_merge_runs, dim3((unsigned)(a.L.batch * a.L.kv_heads), (unsigned)a.L.group_size),

@@ -28,7 +28,6 @@
 namespace fx {
 namespace {
 
-constexpr int kTileBlocks = 512;  // blocks per CTA (8 MMA m-tiles per warp)
 
 #ifdef FX_TRACE  // profiling build only: per-CTA phase times of the TMA scorer
 __device__ long long g_score_trace[8 * 512];
@@ -56,14 +55,14 @@ struct TileCtx {
     int64_t nblk, t0, head0;
 };
 __device__ __forceinline__ bool tile_ctx(const int32_t* blk_arr, const int32_t* kblocks, int Hkv,
-                                         int G, int64_t l_cpu, TileCtx& c, int rank_all) {
+                                         int G, int64_t l_cpu, TileCtx& c, int rank_all, int tile) {
     c.bg = blockIdx.y;
     c.b = c.bg / Hkv;
     c.g = c.bg % Hkv;
     c.blk = blk_arr[c.bg];
     if (c.blk <= 0) return false;
     c.nblk = cdiv_dev(l_cpu, c.blk);
-    c.t0 = (int64_t)blockIdx.x * kTileBlocks;
+    c.t0 = (int64_t)blockIdx.x * tile;
     if (c.t0 >= c.nblk) return false;
     c.head0 = (int64_t)c.b * Hkv * G + (int64_t)c.g * G;
     bool any = false;
@@ -336,6 +335,11 @@ __global__ void __launch_bounds__(kSThreads, 1) k_score_tma(
 // ---------------------------------------------------------------------------
 // CUDA-core path (f32 metadata): lanes split the head dimension
 // ---------------------------------------------------------------------------
+// f32 scorer tile: one pass of the CTA's 8 warps (U = 4 rows per lane group),
+// so a batch-1 layer's few groups still spread over many SMs
+template <int D>
+constexpr int kTileF32 = 8 * (32 / (D / 4)) * 4;
+
 template <int D, int G>
 __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const float* __restrict__ q,
                                                            const int32_t* __restrict__ blk_arr,
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const 
     constexpr int GP = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8;
     static_assert(GP <= LPR, "group too wide for the lane split");
     TileCtx c;
-    if (!tile_ctx(blk_arr, kblocks, Hkv, G, l_cpu, c, rank_all)) return;
+    if (!tile_ctx(blk_arr, kblocks, Hkv, G, l_cpu, c, rank_all, kTileF32<D>)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int col = (lane % LPR) * 4;
     const float* base = static_cast<const float*>(level_ptr(meta.p, c.blk)) + (int64_t)c.bg * c.nblk * 2 * D;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(256) k_approx_scores_f32(MetaPtrs meta, const 
             }
     }
     const bool writer = (lane % (LPR / GP)) == 0 && my_h < G;
-    const int64_t t1 = min(c.nblk, c.t0 + kTileBlocks);
+    const int64_t t1 = min(c.nblk, c.t0 + kTileF32<D>);
     constexpr int U = 4;
     for (int64_t j0 = c.t0 + warp * RPW * U; j0 < t1; j0 += 8 * RPW * U) {
         float4 mn[U], mx[U];
@@ -477,15 +481,17 @@ void launch_approx_scores(const fx_layout& L, const void* const meta[4], const f
     MetaPtrs mp{{meta[0], meta[1], meta[2], meta[3]}};
     const int D = L.head_dim;
     FX_REQUIRE(L.group_size <= 8, FX_ERR_INVALID, "bad-shape: group_size must be <= 8");
-    const dim3 grid((unsigned)cdiv(level_blocks(L.l_cpu, 16), kTileBlocks),
-                    (unsigned)(L.batch * L.kv_heads));
     const int n_bg = L.batch * L.kv_heads;
     if (L.dtype == FX_BF16 && D == 128)
         launch_score_tma<128>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s, rank_all);
     else if (L.dtype == FX_BF16 && D == 64)
         launch_score_tma<64>(L, meta, q, blk, kblocks, approx, approx_stride, num_sms, s, rank_all);
-    else if (L.dtype == FX_F32 && D == 128) launch_f32<128>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s, rank_all);
-    else if (L.dtype == FX_F32 && D == 64) launch_f32<64>(L, mp, q, blk, kblocks, approx, approx_stride, grid, s, rank_all);
+    else if (L.dtype == FX_F32 && D == 128)
+        launch_f32<128>(L, mp, q, blk, kblocks, approx, approx_stride,
+                        dim3((unsigned)cdiv(level_blocks(L.l_cpu, 16), kTileF32<128>), (unsigned)n_bg), s, rank_all);
+    else if (L.dtype == FX_F32 && D == 64)
+        launch_f32<64>(L, mp, q, blk, kblocks, approx, approx_stride,
+                       dim3((unsigned)cdiv(level_blocks(L.l_cpu, 16), kTileF32<64>), (unsigned)n_bg), s, rank_all);
     else fail(FX_ERR_INVALID, "bad-shape: batched scoring supports head_dim 64 or 128");
     FX_CUDA(cudaGetLastError());
 }

@@ -78,7 +78,7 @@ def full_report(path):
     print()
 
 
-STEP_KERNELS = ("k_prepare", "k_score", "k_select", "k_worklist", "k_attend", "k_merge_units", "k_append", "k_approx")
+STEP_KERNELS = ("k_prepare", "k_score", "k_select", "k_worklist", "k_attend", "k_merge_units", "k_append", "k_approx", "k_merge_chunks", "k_merge_runs")
 
 
 def launch_list(path):
