@@ -1061,12 +1061,6 @@ constexpr int kFW = 6;       // warps per CTA
 constexpr int kFStages = 2;  // boxes in flight per warp
 constexpr int kFChunk = 4;   // boxes per chunk
 
-bool f32w_supported(const fx_layout& L, bool has_idx) {
-    return !has_idx && L.dtype == FX_F32 && (L.head_dim == 128 || L.head_dim == 64) &&
-           (L.group_size == 4 || L.group_size == 7 || L.group_size == 8) &&
-           L.batch * L.kv_heads <= kMaxPrefix;
-}
-
 // Chunk prefix of the runs in smem (n_bg <= kMaxPrefix): cstart[bg] = first
 // chunk of run bg, cstart[n_bg] = the total.  All threads; ends in a barrier.
 __device__ const int32_t* chunk_starts(const int32_t* bg_count, int n_bg, int32_t* cs, int* wtmp, int t, int nt) {
@@ -1566,6 +1560,13 @@ void launch_tma(const AttendArgs& a, int grid, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool f32w_supported(const fx_layout& L, bool has_idx) {
+    return !has_idx && L.dtype == FX_F32 && (L.head_dim == 128 || L.head_dim == 64) &&
+           (L.group_size == 4 || L.group_size == 7 || L.group_size == 8) &&
+           L.batch * L.kv_heads <= kMaxPrefix;
+}
+
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

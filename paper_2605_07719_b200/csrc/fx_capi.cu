@@ -239,8 +239,10 @@ StepOffsets step_offsets(const fx_layout& L, int grid) {
     o.dn = c.take<int32_t>(2 * n_bg + 5);
     o.ub = c.take<int32_t>(n_bg);
     // partial slots: the generic kernel's (grid + n_bg), the TMA kernel's units
+    // (the f32 warp-stream kernel's chunk slots only when that kernel runs)
     const int64_t slots = std::max<int64_t>({grid + n_bg, fx::unit_capacity(n_bg, o.box_stride),
-                                             fx::chunk_capacity(n_bg, o.box_stride)});
+                                             fx::f32w_supported(L, false) ? fx::chunk_capacity(n_bg, o.box_stride)
+                                                                          : int64_t(0)});
     o.po = c.take<float>(slots * L.group_size * L.head_dim);
     o.pl = c.take<float>(slots * L.group_size);
     o.total = c.off;

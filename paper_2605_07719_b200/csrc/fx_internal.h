@@ -261,7 +261,9 @@ struct AttendArgs {
 };
 // Units a step can publish at most (partial slots of the TMA kernel).
 int64_t unit_capacity(int64_t n_bg, int64_t box_stride);
-// Chunk partial slots of the f32 warp-stream kernel (k_attend_f32w).
+// The f32 warp-stream kernel (k_attend_f32w) runs this layout; its chunk
+// partial slots.
+bool f32w_supported(const fx_layout& L, bool has_idx);
 int64_t chunk_capacity(int64_t n_bg, int64_t box_stride);
 bool attend_uses_tma(const fx_layout& L, bool has_idx);
 int attend_grid(const fx_layout& L, bool has_idx, int num_sms);
