@@ -323,13 +323,17 @@ def test_decode_step_fixed_plan(engine, coracle, dtype, blk, bgt):
     _check_step(dec, host, q, coracle, lambda b, g: blk, lambda b, g: [bgt] * 4, dtype)
 
 
-@pytest.mark.parametrize("G,D", [(7, 128), (1, 128), (8, 64), (4, 64)])
-def test_decode_step_shapes(engine, coracle, G, D):
-    dec, host, q = make_decoder(engine, 2, 3, G, D, 64, 1500, 256, "bf16", seed=G * D,
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("G,D", [(7, 128), (1, 128), (8, 64), (4, 64), (8, 128)])
+def test_decode_step_shapes(engine, coracle, G, D, dtype):
+    """Group sizes and head dims of every attention kernel instantiation: the
+    TMA kernel (bf16), the f32 warp-stream kernel (G 4/7/8, D 64/128) and the
+    generic kernel (G = 1)."""
+    dec, host, q = make_decoder(engine, 2, 3, G, D, 64, 1500, 256, dtype, seed=G * D,
                                 structured=True, n_new=5)
     dec.step(torch.as_tensor(q).cuda(), fixed=(32, 0.06))
     torch.cuda.synchronize()
-    _check_step(dec, host, q, coracle, lambda b, g: 32, lambda b, g: [0.06] * G, "bf16",
+    _check_step(dec, host, q, coracle, lambda b, g: 32, lambda b, g: [0.06] * G, dtype,
                 n_new=5)
 
 
@@ -509,13 +513,14 @@ def test_launch_count_per_step(engine):
     assert engine.launches() - n0 == 5  # plan, score, select (+ fused worklist), attend, partial merge
 
 
-def test_decode_step_empty_group_is_identity(engine):
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_decode_step_empty_group_is_identity(engine, dtype):
     """A (b, g) with nothing to attend (no sink/local/decoded rows, streaming
     plan) gets the merge identity o = 0, lse = -inf (attention.cpp:89-104),
     not stale memory; its neighbours are unaffected."""
     from paper_2605_07719_b200.fluxattn import SparseDecoder
     B, Hkv, G, D, l_cpu = 4, 8, 4, 128, 4096
-    dec = SparseDecoder(engine, B, Hkv, G, D, 0, l_cpu, 0, max_new=4, dtype="bf16")
+    dec = SparseDecoder(engine, B, Hkv, G, D, 0, l_cpu, 0, max_new=4, dtype=dtype)
     dec.k.normal_()
     dec.v.normal_()
     dec.build_metadata()
