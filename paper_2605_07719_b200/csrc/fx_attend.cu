@@ -229,23 +229,24 @@ constexpr int kMergeThreads = 128;
 // max of the slot LSEs, then each thread owns one float4 column of a fixed
 // subset of the slots (eight slots' loads in flight), the subsets combined in
 // a fixed order: deterministic.  All kMergeThreads threads.
+template <int NT>
 __device__ void merge_slots(int G, int D, int h, int base, int nun, const float* __restrict__ part_o,
                             const float* __restrict__ part_lse, float* __restrict__ o_dst,
                             float* __restrict__ lse_dst) {
     const int t = threadIdx.x;
     const int VP = D / 4;                   // float4 columns of the head
-    const int S = kMergeThreads / VP;       // slot subsets (D <= 512)
-    __shared__ float s_wm[kMergeThreads / 32];
-    __shared__ float4 s_acc[kMergeThreads];
-    __shared__ float s_den[kMergeThreads];
+    const int S = NT / VP;       // slot subsets (D <= 512)
+    __shared__ float s_wm[NT / 32];
+    __shared__ float4 s_acc[NT];
+    __shared__ float s_den[NT];
     float m = -INFINITY;
-    for (int i = t; i < nun; i += kMergeThreads) m = fmaxf(m, __ldg(part_lse + (int64_t)(base + i) * G + h));
+    for (int i = t; i < nun; i += NT) m = fmaxf(m, __ldg(part_lse + (int64_t)(base + i) * G + h));
     m = warp_max(m);
     if ((t & 31) == 0) s_wm[t >> 5] = m;
     __syncthreads();
     float M = s_wm[0];
 #pragma unroll
-    for (int w = 1; w < kMergeThreads / 32; ++w) M = fmaxf(M, s_wm[w]);
+    for (int w = 1; w < NT / 32; ++w) M = fmaxf(M, s_wm[w]);
     const int v = t % VP, sub = t / VP;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float den = 0.f;
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
     if (nun <= 1) return;  // written final by the attention kernel
     const int b = bg / Hkv, g = bg % Hkv;
     const int64_t hd = (int64_t)b * Hkv * G + (int64_t)g * G + h;
-    merge_slots(G, D, h, __ldg(ubase + bg), nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
+    merge_slots<kMergeThreads>(G, D, h, __ldg(ubase + bg), nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
 }
 
 #ifdef FX_TRACE  // profiling build only: per-CTA start/end time, units, tiles
@@ -1292,9 +1293,11 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_attend_f32w(const View p) {
 }
 
 // Merge of a run's chunk partials (k_attend_f32w), in chunk order: one
-// 128-thread CTA per (b, g, head) as k_merge_units; a run with no boxes gets
-// the merge identity, a one-chunk run was written final.
-__global__ void __launch_bounds__(kMergeThreads) k_merge_chunks(int n_bg, int G, int D,
+// 512-thread CTA per (b, g, head) (a batch-1 layer has few runs of many
+// chunks: 16 slot subsets, one round of loads in flight); a run with no boxes
+// gets the merge identity, a one-chunk run was written final.
+constexpr int kMergeChunkThreads = 512;
+__global__ void __launch_bounds__(kMergeChunkThreads) k_merge_chunks(int n_bg, int G, int D,
                                                                const int32_t* __restrict__ bg_count,
                                                                const float* __restrict__ part_o,
                                                                const float* __restrict__ part_lse,
@@ -1302,18 +1305,18 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_chunks(int n_bg, int G,
     pdl_wait();
     pdl_trigger();
     __shared__ int32_t s_cs[kMaxPrefix + 1];
-    __shared__ int s_wtmp[kMergeThreads / 32];
+    __shared__ int s_wtmp[kMergeChunkThreads / 32];
     const int bg = blockIdx.x, h = blockIdx.y, t = threadIdx.x;
-    const int32_t* cs = chunk_starts(bg_count, n_bg, s_cs, s_wtmp, t, kMergeThreads);
+    const int32_t* cs = chunk_starts(bg_count, n_bg, s_cs, s_wtmp, t, kMergeChunkThreads);
     const int base = cs[bg], nun = cs[bg + 1] - cs[bg];
     if (nun == 1) return;  // written final by the attention kernel
     const int64_t hd = (int64_t)bg * G + h;  // (b, g, h) = b * Hkv * G + g * G + h
     if (nun == 0) {
-        for (int d = t; d < D; d += kMergeThreads) o[hd * D + d] = 0.f;
+        for (int d = t; d < D; d += kMergeChunkThreads) o[hd * D + d] = 0.f;
         if (t == 0 && lse) lse[hd] = -INFINITY;
         return;
     }
-    merge_slots(G, D, h, base, nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
+    merge_slots<kMergeChunkThreads>(G, D, h, base, nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
 }
 
 // Merge of the partials of the generic kernel's runs cut by CTA range ends
@@ -1670,7 +1673,7 @@ int launch_attend(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s)
 int launch_unit_merge(const AttendArgs& a, int grid, bool allow_tma, cudaStream_t s) {
     if (!(allow_tma && attend_uses_tma(a.L, a.idx != nullptr)) && f32w_supported(a.L, a.idx != nullptr)) {
         const int n_bg = a.L.batch * a.L.kv_heads;  // f32 warp streams: chunk partials
-        launch_pdl(k_merge_chunks, dim3((unsigned)n_bg, (unsigned)a.L.group_size), kMergeThreads, 0, s, n_bg,
+        launch_pdl(k_merge_chunks, dim3((unsigned)n_bg, (unsigned)a.L.group_size), kMergeChunkThreads, 0, s, n_bg,
                    a.L.group_size, a.L.head_dim, (const int32_t*)a.bg_count, (const float*)a.part_o,
                    (const float*)a.part_lse, a.o, a.lse);
         FX_CUDA(cudaGetLastError());
