@@ -17,16 +17,16 @@
 // persistent CTAs -- resident while the selection of later groups is still
 // running -- claim units in publication order with one atomic each.  A
 // single-unit group is written final; otherwise every unit leaves an (o, lse)
-// partial and the CTA that finishes a group's last unit merges them (in unit
-// order, so the result does not depend on which CTA ran what).  Dynamic
+// partial and k_merge_units (launched behind this kernel, PDL) folds them in
+// unit order, so the result does not depend on which CTA ran what.  Dynamic
 // claiming also balances the per-SM bandwidth differences at the end.
 //   warp 4        producer: claims units, one 3-D TMA per 16-row box and
 //                 tensor (SWIZZLE_128B) into a kStages-deep ring of 8-box
 //                 tiles plus a 1-D bulk copy of the unit's q rows, mbarrier
 //                 completion;
 //   warp 5        epilogue: combines the consumer warps' states of a unit,
-//                 writes the partial / final output, counts the unit in and
-//                 merges a finished group -- off the consumers' path;
+//                 writes the partial / final output -- off the consumers'
+//                 path;
 //   warps 0..3    consumers: two boxes each per 8-box tile;
 //                 S^T[16 tok x 8 heads] = K . Q^T  (mma.sync m16n8k16 bf16,
 //                 q split hi+lo so q keeps ~16 mantissa bits),
@@ -184,8 +184,8 @@ struct KvMaps {
 
 // One attention unit = up to kUnitBoxes consecutive boxes of one (b, g)
 // (fx_worklist.cuh publish_units).  A unit of a single-unit group writes the
-// final (o, lse); otherwise one (o, lse) partial per unit, and the epilogue
-// warp of whichever CTA finishes a group's last unit merges the group.
+// final (o, lse); otherwise one (o, lse) partial per unit, folded by
+// k_merge_units.
 struct QView {
     int n_bg, Hkv, G;
     int64_t l_cap;
