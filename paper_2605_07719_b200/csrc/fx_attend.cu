@@ -224,7 +224,7 @@ struct TmaCfg {
     static constexpr size_t TOTAL = WL + kCWarps * 8 * sizeof(float) + 1024;  // + align slack
 };
 
-constexpr int kMergeThreads = 128;
+constexpr int kMergeThreads = 128;  // the narrowest unit-merge CTA (launch_unit_merge picks 128 / 256 / 512)
 // Fold the partials at slots [base, base + nun) of head h into (o, lse): the
 // max of the slot LSEs, then each thread owns one float4 column of a fixed
 // subset of the slots (eight slots' loads in flight), the subsets combined in
@@ -296,7 +296,8 @@ __device__ void merge_slots(int G, int D, int h, int base, int nun, const float*
 // across the units, in unit order): one 128-thread CTA per (b, g, head),
 // launched behind the attention kernel (PDL) -- small CTAs, so every group's
 // heads merge at once even with thousands of groups (C4).
-__global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, int D,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_merge_units(int Hkv, int G, int D,
                                                               const int32_t* __restrict__ bg_count,
                                                               const int32_t* __restrict__ ubase,
                                                               const float* __restrict__ part_o,
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_units(int Hkv, int G, i
     if (nun <= 1) return;  // written final by the attention kernel
     const int b = bg / Hkv, g = bg % Hkv;
     const int64_t hd = (int64_t)b * Hkv * G + (int64_t)g * G + h;
-    merge_slots<kMergeThreads>(G, D, h, __ldg(ubase + bg), nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
+    merge_slots<NT>(G, D, h, __ldg(ubase + bg), nun, part_o, part_lse, o + hd * D, lse ? lse + hd : nullptr);
 }
 
 #ifdef FX_TRACE  // profiling build only: per-CTA start/end time, units, tiles
@@ -1687,10 +1688,27 @@ int launch_unit_merge(const AttendArgs& a, int grid, bool allow_tma, cudaStream_
         return 1;
     }
     const int n_bg = a.L.batch * a.L.kv_heads;
-    launch_pdl(k_merge_units, dim3((unsigned)n_bg, (unsigned)a.L.group_size), kMergeThreads, 0, s,
-               a.L.kv_heads, a.L.group_size, a.L.head_dim,
-               (const int32_t*)a.bg_count, (const int32_t*)a.uq.ubase, (const float*)a.part_o,
-               (const float*)a.part_lse, a.o, a.lse);
+    // the widest CTA that still holds every (b, g, head) in one wave: a small
+    // batch (C3, C5) folds more slots per round of loads (S = NT / (D / 4))
+    static int occ[3] = {0, 0, 0};
+    if (occ[0] == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_merge_units<512>, 512, 0) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_merge_units<256>, 256, 0) != cudaSuccess) {
+            cudaGetLastError();
+            occ[0] = occ[1] = 0;
+        }
+        occ[2] = 1;
+    }
+    const int64_t ctas = (int64_t)n_bg * a.L.group_size;
+    auto go = [&](auto kern, int nt) {
+        launch_pdl(kern, dim3((unsigned)n_bg, (unsigned)a.L.group_size), nt, 0, s,
+                   a.L.kv_heads, a.L.group_size, a.L.head_dim,
+                   (const int32_t*)a.bg_count, (const int32_t*)a.uq.ubase, (const float*)a.part_o,
+                   (const float*)a.part_lse, a.o, a.lse);
+    };
+    if (a.L.head_dim / 4 <= 512 && ctas <= (int64_t)grid * occ[0]) go(k_merge_units<512>, 512);
+    else if (a.L.head_dim / 4 <= 256 && ctas <= (int64_t)grid * occ[1]) go(k_merge_units<256>, 256);
+    else go(k_merge_units<kMergeThreads>, kMergeThreads);
     FX_CUDA(cudaGetLastError());
     return 1;
 }

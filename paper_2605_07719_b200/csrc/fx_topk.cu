@@ -22,8 +22,11 @@
 namespace fx {
 namespace {
 
-constexpr int kT = 256;           // threads per selection CTA
-constexpr int kNW = kT / 32;
+// threads per selection CTA: 256 (four CTAs per SM) when the heads outnumber
+// the SMs; 512 / 1024 when two / one CTA per SM hold every head and a head
+// has >= 16 blocks per thread at blk 16, so a small batch of long contexts
+// (C3, C5) splits each head's passes over more threads
+constexpr int kTMin = 256, kTMax = 1024;
 constexpr int kBins = 2048;
 // the histogram is stored with one padding word per 32 bins (bin b at
 // b + b / 32): lanes whose bins differ by a multiple of 32 hit different banks
@@ -113,7 +116,7 @@ __device__ __forceinline__ double exact_score_smem(const double* qs, const float
     return exact_score_vec(qs, mn, mx, D);
 }
 
-template <int DT>
+template <int DT, int kT>
 __device__ __forceinline__ void select_head(
     MetaPtrs meta, const float* __restrict__ absmax, const float* __restrict__ q,
     const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int Hkv, int G,
@@ -121,6 +124,7 @@ __device__ __forceinline__ void select_head(
     uint32_t* __restrict__ sel_bits, int sel_words, uint64_t* __restrict__ cand_keys,
     uint32_t* __restrict__ cand_ids, int64_t cand_stride, int keys_cap) {
     using T = typename Elem<DT>::T;
+    constexpr int kNW = kT / 32;
     // dynamic smem: keys[keys_cap] f32 | hist[kHistWords] | q[D] f64 | ck[kSmallCand] | ci[kSmallCand]
     extern __shared__ __align__(16) unsigned char dsm[];
     float* s_keys = reinterpret_cast<float*>(dsm);
@@ -239,8 +243,8 @@ __device__ __forceinline__ void select_head(
         // bin holding the k-th largest: each thread owns kBins/kT bins; suffix
         // sums over threads (from the top) locate the owner, which scans them
         constexpr int PB = kBins / kT;
-        static_assert(PB == 8, "two 16-byte reads per thread");
-        int hb[PB];  // this thread's 8 consecutive bins (one padded row of 32 holds them)
+        static_assert(PB >= 2 && PB <= 8, "kBins / kT consecutive bins per thread");
+        int hb[PB];  // this thread's PB consecutive bins (one padded row of 32 holds them)
 #pragma unroll
         for (int i = 0; i < PB; ++i) hb[i] = hist[hidx(t * PB + i)];
         int c = 0;
@@ -497,7 +501,7 @@ __device__ __forceinline__ void select_head(
 // One CTA per head.  With `wl.boxes` set, the CTA that completes the last head
 // of a group (sel_done[bg] reaches G) goes on to build that group's attention
 // boxes (fx_worklist.cuh) -- the union of the G selections is final then.
-template <int DT>
+template <int DT, int kT>
 __global__ void __launch_bounds__(kT) k_select(
     MetaPtrs meta, const float* __restrict__ absmax, const float* __restrict__ q,
     const int32_t* __restrict__ blk_arr, const int32_t* __restrict__ kblocks, int Hkv, int G,
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(kT) k_select(
     int32_t* __restrict__ sel_done) {
     pdl_trigger();  // select_head waits for the scorer once its independent setup is done
     SEL_MARK(10);
-    select_head<DT>(meta, absmax, q, blk_arr, kblocks, Hkv, G, D, l_cpu, approx, astride,
+    select_head<DT, kT>(meta, absmax, q, blk_arr, kblocks, Hkv, G, D, l_cpu, approx, astride,
                     eps_scale, sel_bits, sel_words, cand_keys, cand_ids, cand_stride, keys_cap);
     SEL_MARK(11);
     if (wl.boxes == nullptr) return;
@@ -553,18 +557,42 @@ void launch_select(const fx_layout& L, const void* const meta[4], const float* a
         smem = std::max(smem, (size_t)kMaxWords * 4);  // fused worklist: the word counts
     }
     const double eps = approx_eps_scale(L);
+    // widest CTA whose residency (64 registers per thread; the dynamic smem)
+    // still holds every head in one wave
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+            cudaGetLastError();
+            sms = 148;
+        }
+    }
+    int nt = kTMin;
+    for (int c = kTMax; c > kTMin; c >>= 1) {
+        if (nmax < (int64_t)c * 16) continue;  // short heads: the extra warps only add barrier cost
+        const int64_t by_regs = 65536 / (c * 64);
+        const int64_t by_smem = (int64_t)(227 * 1024) / (int64_t)(smem + 1024);
+        if (heads <= (int64_t)sms * std::min(by_regs, by_smem)) {
+            nt = c;
+            break;
+        }
+    }
+    auto go = [&](auto kern) {
+        FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        launch_pdl(kern, (unsigned)heads, nt, smem, s,
+            mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
+            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
+            w, sel_done);
+    };
     if (L.dtype == FX_BF16) {
-        FX_CUDA(cudaFuncSetAttribute(k_select<FX_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        launch_pdl(k_select<FX_BF16>, (unsigned)heads, kT, smem, s,
-            mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
-            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
-            w, sel_done);
+        if (nt == 1024) go(k_select<FX_BF16, 1024>);
+        else if (nt == 512) go(k_select<FX_BF16, 512>);
+        else go(k_select<FX_BF16, kTMin>);
     } else {
-        FX_CUDA(cudaFuncSetAttribute(k_select<FX_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        launch_pdl(k_select<FX_F32>, (unsigned)heads, kT, smem, s,
-            mp, absmax, q, blk, kblocks, L.kv_heads, L.group_size, L.head_dim, L.l_cpu, approx,
-            approx_stride, eps, sel_bits, sel_words, cand_keys, cand_ids, approx_stride, keys_cap,
-            w, sel_done);
+        if (nt == 1024) go(k_select<FX_F32, 1024>);
+        else if (nt == 512) go(k_select<FX_F32, 512>);
+        else go(k_select<FX_F32, kTMin>);
     }
     FX_CUDA(cudaGetLastError());
 }
