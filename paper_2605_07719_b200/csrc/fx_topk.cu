@@ -419,14 +419,23 @@ __device__ __forceinline__ void select_head(
     __syncthreads();
     SEL_MARK(4);
     if (small) {
-        for (int64_t c = t; c < n_cand; c += kT) {
+        // rank of each candidate by counting the ones ahead of it; four
+        // (key, id) pairs per 16-byte shared read (ck / ci are 16-byte
+        // aligned unless D is odd), stopping once `need` are ahead (it is out)
+        const int nc = (int)n_cand, nc4 = (D & 1) ? 0 : nc & ~3;
+        for (int c = t; c < nc; c += kT) {
             const uint64_t kc = ck[c];
             const uint32_t idc = ci[c];
-            int64_t rank = 0;
-            for (int64_t j = 0; j < n_cand; ++j) {
-                const uint64_t kj = ck[j];
-                rank += (kj > kc) || (kj == kc && ci[j] < idc);
+            int rank = 0;
+            auto ahead = [&](uint64_t kj, uint32_t ij) { return (int)((kj > kc) || (kj == kc && ij < idc)); };
+            int j = 0;
+            for (; j < nc4 && rank < need; j += 4) {
+                const ulonglong2 k01 = *reinterpret_cast<const ulonglong2*>(ck + j);
+                const ulonglong2 k23 = *reinterpret_cast<const ulonglong2*>(ck + j + 2);
+                const uint4 i4 = *reinterpret_cast<const uint4*>(ci + j);
+                rank += ahead(k01.x, i4.x) + ahead(k01.y, i4.y) + ahead(k23.x, i4.z) + ahead(k23.y, i4.w);
             }
+            for (; j < nc && rank < need; ++j) rank += ahead(ck[j], ci[j]);
             if (rank < need) atomicOr(&bits[idc >> 5], 1u << (idc & 31));
         }
     } else {
