@@ -73,6 +73,7 @@ __device__ double exact_score_vec(const double* __restrict__ qs, const __nv_bflo
                                   const __nv_bfloat16* __restrict__ mx, int D) {
     double s = 0.0;
     if ((D & 7) == 0) {
+#pragma unroll 4
         for (int d = 0; d < D; d += 8) {
             const uint4 a = *reinterpret_cast<const uint4*>(mn + d);
             const uint4 c = *reinterpret_cast<const uint4*>(mx + d);
@@ -336,7 +337,18 @@ __device__ __forceinline__ void select_head(
     // serial readers (one candidate each) spread over the banks too
     const int tpitch = (D / 8) * 9 + 1;  // doubles
     const int per_round_t = ((int)((size_t)keys_cap * 4 + kHistWords * 4)) / (tpitch * 8);
-    if (kTerms && (D & 7) == 0 && per_round_t >= 1) {
+    // a band of more than two term rounds: one candidate per thread instead,
+    // its row read straight from L2 in 16-byte vectors (all candidates at once)
+    const bool direct = kTerms && (D & 7) == 0 && n_cand > 2 * (int64_t)per_round_t;
+    if (direct) {
+        for (int64_t c = t; c < n_cand; c += kT) {
+            const uint32_t id = small ? ci[c] : cids[c];
+            const T* row = mbase + (int64_t)id * 2 * D;
+            const double sc_ = exact_score_vec(s_q, row, row + D, D);
+            if (small) ck[c] = f64_key(sc_);
+            else ckeys[c] = f64_key(sc_);
+        }
+    } else if (kTerms && (D & 7) == 0 && per_round_t >= 1) {
         double* term = reinterpret_cast<double*>(dsm);
         const int v8 = D / 8;
         // a thread's 8 dims are the same for every candidate (kT % v8 == 0):
