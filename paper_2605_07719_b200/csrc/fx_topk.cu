@@ -34,7 +34,8 @@ constexpr int kHistWords = kBins + kBins / 32;
 __device__ __forceinline__ int hidx(int b) { return b + (b >> 5); }
 constexpr int kMaxWords = 4096;   // nblk <= 131072 at the chosen granularity
 constexpr int kSmemKeys = 16384;  // approximate scores staged in smem up to this many
-constexpr int kSmallCand = 512;   // band ranked in smem by counting up to this size
+constexpr int kSmallCand = 512;   // band ranked in smem up to this size (a power of two)
+constexpr int kSortCand = 192;    // ... by counting up to this size, by a bitonic sort above
 
 #ifdef FX_TRACE  // profiling build only: per-head phase times and band sizes
 __device__ long long g_sel_trace[16 * 8192];
@@ -430,7 +431,40 @@ __device__ __forceinline__ void select_head(
     }
     __syncthreads();
     SEL_MARK(4);
-    if (small) {
+    if (small && n_cand > kSortCand) {
+        // a wide band: bitonic sort of the (key, id) pairs in place, best
+        // first (key desc, id asc; pad entries (0, ~0u) sort last), then the
+        // first `need` are in -- log2(p) (log2(p) + 1) / 2 barrier stages
+        // instead of the O(n^2) ranking below
+        const int nc = (int)n_cand;
+        int p = 1;
+        while (p < nc) p <<= 1;
+        for (int i = nc + t; i < p; i += kT) {
+            ck[i] = 0ull;
+            ci[i] = 0xffffffffu;
+        }
+        __syncthreads();
+        for (int size = 2; size <= p; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = t; i < (p >> 1); i += kT) {
+                    const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const uint64_t ka = ck[lo], kb = ck[hi];
+                    const uint32_t ia = ci[lo], ib = ci[hi];
+                    const bool b_first = (kb > ka) || (kb == ka && ib < ia);
+                    const bool a_first = (ka > kb) || (ka == kb && ia < ib);
+                    if ((lo & size) == 0 ? b_first : a_first) {
+                        ck[lo] = kb;
+                        ck[hi] = ka;
+                        ci[lo] = ib;
+                        ci[hi] = ia;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const int take = (int)(need < (int64_t)nc ? need : (int64_t)nc);
+        for (int i = t; i < take; i += kT) atomicOr(&bits[ci[i] >> 5], 1u << (ci[i] & 31));
+    } else if (small) {
         // rank of each candidate by counting the ones ahead of it; four
         // (key, id) pairs per 16-byte shared read (ck / ci are 16-byte
         // aligned unless D is odd), stopping once `need` are ahead (it is out)

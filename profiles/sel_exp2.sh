@@ -1,4 +1,4 @@
-O=gpurun_out/sel3
+O=gpurun_out/sel4
 mkdir -p $O
 python -m pytest tests -m gpu -q -x > $O/gputests.log 2>&1; tail -2 $O/gputests.log
 for w in c3 c5 c1; do python bench.py --workload $w --steps 20 --warmup 5 --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; done
